@@ -1,0 +1,155 @@
+/*
+ * fvdb_b200.h — C ABI of the B200-native sparse-convolution hot path.
+ *
+ * Drop-in boundary for the reference `idxgrid` Python API (reference paths are
+ * relative to pkg/src/idxgrid/).  The reference has no FFI layer of its own: its
+ * operator surface is the Python functions named beside each entry point, and
+ * this library is what those names call into (see INTEGRATION.md for the ctypes
+ * binding).  Conventions:
+ *   - every pointer argument is DEVICE memory unless marked (host);
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ *   - return 0 on success or a negative FVDB_ERR_* code; `detail` (host) receives
+ *     the offending row / count for the data errors so the caller can raise the
+ *     reference's exact message;
+ *   - the library never allocates device memory outside the caller-provided
+ *     workspace, never frees caller memory, and keeps no global mutable state
+ *     (the last CUDA error string is thread-local).
+ */
+#ifndef FVDB_B200_H
+#define FVDB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FVDB_OK 0
+#define FVDB_ERR_INVALID (-1)      /* bad argument (shape / unsupported channel count) */
+#define FVDB_ERR_COORD_RANGE (-2)  /* |coord| > 2^30; detail = first bad row   (build.py:96-101) */
+#define FVDB_ERR_ROOT_LIMIT (-3)   /* > 2^28 root tiles; detail = tile count  (build.py:121-122) */
+#define FVDB_ERR_NONFINITE (-4)    /* non-finite point; detail = first bad row (build.py:226-229) */
+#define FVDB_ERR_CUDA (-5)         /* CUDA runtime error; see fvdb_last_error() */
+#define FVDB_ERR_WORKSPACE (-6)    /* workspace smaller than the *_workspace_bytes() query */
+
+#define FVDB_DTYPE_F32 0
+#define FVDB_DTYPE_F64 1
+#define FVDB_DTYPE_BF16 2
+
+/* Read-only device view of one IndexGrid (topology.py:140-177). Only the arrays the
+ * device probes need; `uint64` arrays hold the reference's uint64 bit patterns. */
+typedef struct fvdb_grid_view {
+    const uint64_t* tile_keys;          /* [num_upper]   sorted unsigned root keys */
+    const uint64_t* leaf_keys;          /* [num_leaf]    rank<<27 | upper<<12 | lower */
+    const int64_t* leaf_origins;        /* [num_leaf,3] */
+    const uint64_t* leaf_masks;         /* [num_leaf,8] */
+    const uint64_t* leaf_prefix;        /* [num_leaf]    7 x 9-bit cumulative popcounts */
+    const uint64_t* leaf_value_offset;  /* [num_leaf]    1-based index of the leaf's first voxel */
+    int64_t num_upper;
+    int64_t num_leaf;
+    int64_t num_voxels;
+} fvdb_grid_view;
+
+/* Writable device arrays of one IndexGrid, sized from fvdb_build_plan's counts. */
+typedef struct fvdb_grid_arrays {
+    uint64_t* tile_keys;              /* [U]   */
+    int64_t* upper_origins;           /* [U,3] */
+    int64_t* upper_child_starts;      /* [U+1] */
+    uint16_t* lower_offset_in_upper;  /* [Lo]  */
+    int64_t* lower_origins;           /* [Lo,3] */
+    int64_t* lower_child_starts;      /* [Lo+1] */
+    uint16_t* leaf_offset_in_lower;   /* [L]   */
+    uint64_t* leaf_keys;              /* [L]   */
+    int64_t* leaf_origins;            /* [L,3] */
+    uint64_t* leaf_masks;             /* [L,8] */
+    uint64_t* leaf_prefix;            /* [L]   */
+    uint64_t* leaf_value_offset;      /* [L]   */
+} fvdb_grid_arrays;
+
+const char* fvdb_version(void);
+const char* fvdb_last_error(void);
+int fvdb_device_sm_count(int device);
+
+/* ---- a1: VoxelTransform.quantize + finite check (topology.py:135-137, build.py:219-230) ----
+ * coords_out[n,3] = floor((p - origin)/voxel_size + 0.5) computed in IEEE f64 (sub, div, add).
+ * voxel_size3 / origin3 are HOST arrays. Synchronizes `stream` to report FVDB_ERR_NONFINITE. */
+int fvdb_quantize_points(const double* points, int64_t n, const double* voxel_size3,
+                         const double* origin3, int64_t* coords_out, int64_t* detail,
+                         void* stream);
+
+/* ---- a2-a4: build_from_coords (build.py:82-198), two-phase count -> fill ----
+ * plan: validates ±2^30, sorts tile keys, ranks, sorts/dedupes voxel keys and counts
+ * nodes; writes counts (host) = {num_upper, num_lower, num_leaf, num_voxels}.
+ * Synchronizes `stream`. The workspace must stay untouched until fill returns. */
+size_t fvdb_build_workspace_bytes(int64_t n_coords);
+int fvdb_build_plan(const int64_t* coords, int64_t n, void* workspace, size_t workspace_bytes,
+                    int64_t* counts, int64_t* detail, void* stream);
+int fvdb_build_fill(void* workspace, size_t workspace_bytes, int64_t n, const int64_t* counts,
+                    const fvdb_grid_arrays* out, void* stream);
+/* a6: coarsen input — floor_divide(coords, factor) (build.py:325-339) */
+int fvdb_floor_div_coords(const int64_t* coords, int64_t n, int64_t factor, int64_t* out,
+                          void* stream);
+
+/* ---- a5: IndexGrid.coord_to_index_many / active_coords (topology.py:253-299) ---- */
+int fvdb_coord_to_index(const fvdb_grid_view* grid, const int64_t* coords, int64_t n,
+                        int64_t* out, void* stream);
+int fvdb_active_coords(const fvdb_grid_view* grid, int64_t* out, void* stream);
+
+/* ---- a7: build_kernel_map (conv.py:105-122) ----
+ * nbr[27, n_out] int32: 0-based input row of output o at stencil offset d, -1 if none.
+ * pair_counts[27] int64 (device). Works for stride 1 and 2 (conv.py:113, 118). */
+size_t fvdb_kmap_workspace_bytes(int64_t num_leaf_out);
+int fvdb_kernel_map(const fvdb_grid_view* grid_in, const fvdb_grid_view* grid_out, int stride,
+                    int32_t* nbr, int64_t* pair_counts, void* workspace, size_t workspace_bytes,
+                    void* stream);
+/* per-offset (in_rows, out_rows) lists, concatenated in offset order, out ascending */
+size_t fvdb_kmap_compact_workspace_bytes(int64_t n_out);
+int fvdb_kmap_compact(const int32_t* nbr, int64_t n_out, int64_t* in_rows, int64_t* out_rows,
+                      void* workspace, size_t workspace_bytes, void* stream);
+/* inverse table nbrT[27, n_in] (nbrT[d][i] = o  iff  nbr[d][o] = i), for dgrad / transposed conv */
+int fvdb_kmap_transpose(const int32_t* nbr, int64_t n_out, int64_t n_in, int32_t* nbrT,
+                        void* stream);
+
+/* ---- a9/a11: conv forward, dgrad, wgrad (conv.py:180-191, 339-368) ----
+ * Output-stationary gather conv:  out[o,:] = sum_d  in[nbr[d][o],:] @ Wk[d]   (Wk[d] is [K,N]).
+ *   forward:  nbr = kernel map,            Wk[d][ci][co] = W[co][ci][d]
+ *   dgrad  :  nbr = fvdb_kmap_transpose(), Wk[d][co][ci] = W[co][ci][d]
+ *   transposed conv = dgrad form with x_coarse as `in`.
+ * SIMT path (FVDB_DTYPE_F32 / F64): exact-precision parity path.
+ *   wk: [27, K, N] in the feature dtype (see fvdb_pack_weights_kn). */
+int fvdb_conv_gather_simt(int dtype, const void* in, int64_t n_in, int K, const void* wk, int N,
+                          const int32_t* nbr, int64_t n_out, void* out, void* stream);
+/* weight relayout [Cout,Cin,27] -> Wk[27][K][N]; transpose=0: K=Cin,N=Cout; 1: K=Cout,N=Cin */
+int fvdb_pack_weights_kn(int dtype, const void* w, int cout, int cin, int transpose, void* wk,
+                         void* stream);
+/* wgrad: gw[co][ci][d] = sum_{o: nbr[d][o]>=0} go[o][co] * in[nbr[d][o]][ci]   (conv.py:367)
+ * deterministic split-K (fixed-order reduction over splits). */
+size_t fvdb_wgrad_workspace_bytes(int dtype, int64_t n_out, int cin, int cout);
+int fvdb_conv_wgrad_simt(int dtype, const void* in, int64_t n_in, int cin, const void* go,
+                         int cout, const int32_t* nbr, int64_t n_out, void* gw, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
+/* Tensor-core path (bf16 in, fp32 accumulate in TMEM, tcgen05.mma):
+ *   fvdb_pack_weights_umma: fp32 W[Cout,Cin,27] -> per-offset UMMA B-operand images (bf16,
+ *   K-major, 128B/64B swizzle), transpose as in fvdb_pack_weights_kn. Image bytes: 27*K*N*2.
+ *   fvdb_conv_gather_tc: out (fp32 if out_dtype==F32, bf16 if BF16) [n_out, N].
+ *   Supported K, N: K in {32, 64, 128, 256}, N in {32, 64, 128, 256}. */
+int fvdb_pack_weights_umma(const float* w, int cout, int cin, int transpose, void* image,
+                           void* stream);
+int fvdb_conv_gather_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
+                        const int32_t* nbr, int64_t n_out, void* out, int out_dtype,
+                        void* stream);
+/* wgrad on tensor cores: gw fp32 [cout][cin][27]. */
+size_t fvdb_wgrad_tc_workspace_bytes(int64_t n_out, int cin, int cout);
+int fvdb_conv_wgrad_tc(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,
+                       const int32_t* nbr, int64_t n_out, float* gw, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* dtype conversion helpers (fp32 -> bf16 RNE), used at the module boundary */
+int fvdb_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FVDB_B200_H */

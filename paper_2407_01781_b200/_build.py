@@ -1,0 +1,79 @@
+"""In-tree build of the C-ABI CUDA library (``libfvdb_b200.so``) for sm_100a.
+
+``python -m paper_2407_01781_b200._build`` or ``__graft_entry__.build()``.
+nvcc cross-compiles without a GPU; the resulting .so lives in the package
+directory so it travels with the repo snapshot to the GPU box.
+"""
+
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import pathlib
+import shutil
+import subprocess
+import sys
+
+PKG = pathlib.Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+LIBDIR = PKG / "_lib"
+LIBNAME = "libfvdb_b200.so"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-warn-spills", "-I", str(PKG.parent / "include")]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def sources():
+    return sorted(CSRC.glob("*.cu"))
+
+
+def _stale(lib: pathlib.Path) -> bool:
+    if not lib.exists():
+        return True
+    t = lib.stat().st_mtime
+    deps = list(CSRC.glob("*")) + [PKG.parent / "include" / "fvdb_b200.h"]
+    return any(p.stat().st_mtime > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = True) -> pathlib.Path:
+    LIBDIR.mkdir(exist_ok=True)
+    lib = LIBDIR / LIBNAME
+    if not force and not _stale(lib):
+        return lib
+    objdir = LIBDIR / "obj"
+    objdir.mkdir(exist_ok=True)
+    cc = nvcc()
+
+    def compile_one(src: pathlib.Path):
+        obj = objdir / (src.stem + ".o")
+        cmd = [cc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")
+        return obj, r.stderr
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, sources()))
+    for obj, err in results:
+        if verbose and err.strip():
+            print(f"[nvcc {obj.stem}] {err.strip()}", file=sys.stderr)
+    tmp = lib.with_suffix(".so.tmp")
+    cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *[str(o) for o, _ in results]]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, lib)
+    if verbose:
+        print(f"built {lib}", file=sys.stderr)
+    return lib
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

@@ -1,0 +1,451 @@
+"""Sparse 3×3×3 convolution on the GPU (drop-in for reference ``idxgrid.conv`` hot path).
+
+Reference surface kept (conv.py:34-383): ``STENCIL``, ``ConvKernel``, ``KernelMap``,
+``build_kernel_map``, ``choose_variant``, ``conv``, ``conv_backward``, ``conv_batch``
+— same signatures, same ValueError / TypeError texts.  New:
+``conv_transpose``.  All four reference ``variant`` schedules compute one operator;
+here every variant runs the same output-stationary CUDA kernels:
+
+* float32 / float64 features → CUDA-core gather kernel (exact-precision parity path);
+* bfloat16 features          → tcgen05 tensor-core kernel (fp32 accumulation in TMEM).
+
+The kernel map is kept on the device as a dense offset-major table
+``nbr[27, N_out]`` (int32, -1 = no neighbour); the reference's per-offset
+``in_rows`` / ``out_rows`` lists are materialised lazily by one compaction.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .build import coarsen as _coarsen_grid
+
+VARIANTS = ("igemm", "leaf", "brick", "lggs")
+_R = np.array([-1, 0, 1], np.int64)
+STENCIL = np.stack(np.meshgrid(_R, _R, _R, indexing="ij"), axis=-1).reshape(-1, 3)  # conv.py:36-38
+LGGS_BLOCK = 64
+LGGS_PAD = 16
+TC_CHANNELS = (32, 64, 128)  # channel counts the tcgen05 kernels are instantiated for
+
+
+def _to_device_tensor(x, device, dtype=None):
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
+        t = t.to(device)
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.contiguous()
+
+
+class ConvKernel:
+    """Dense 3×3×3 stencil weights [C_out, C_in, 3, 3, 3] (conv.py:44-73)."""
+
+    __slots__ = ("weights",)
+
+    def __init__(self, weights):
+        w = weights if isinstance(weights, torch.Tensor) else torch.from_numpy(np.asarray(weights).copy())
+        if w.ndim != 5 or tuple(w.shape[2:]) != (3, 3, 3):
+            raise ValueError(f"kernel weights must be [C_out, C_in, 3, 3, 3], got {tuple(w.shape)}")
+        if w.is_floating_point() and not bool(torch.isfinite(w).all()):
+            raise ValueError("kernel weights must be finite")
+        self.weights = w
+
+    @property
+    def c_out(self):
+        return int(self.weights.shape[0])
+
+    @property
+    def c_in(self):
+        return int(self.weights.shape[1])
+
+    def spoke(self, di, dj, dk):
+        return self.weights[:, :, di + 1, dj + 1, dk + 1]
+
+    @staticmethod
+    def identity(channels, dtype=torch.float64):
+        w = torch.zeros((channels, channels, 3, 3, 3), dtype=dtype)
+        w[:, :, 1, 1, 1] = torch.eye(channels, dtype=dtype)
+        return ConvKernel(w)
+
+
+def _kernel_weights(kernel):
+    return kernel.weights if isinstance(kernel, ConvKernel) else kernel
+
+
+class KernelMap:
+    """Per-offset (input_row, output_row) pairs (conv.py:80-102), device-resident.
+
+    Constructed either from the reference's lists (``KernelMap(in_rows, out_rows,
+    num_in, num_out, stride)``) or from a neighbour table (``nbr=``).
+    """
+
+    __slots__ = ("nbr", "num_in", "num_out", "stride", "_counts", "_lists", "_nbrT")
+
+    def __init__(self, in_rows=None, out_rows=None, num_in=0, num_out=0, stride=1, *, nbr=None,
+                 pair_counts=None):
+        self.num_in, self.num_out, self.stride = int(num_in), int(num_out), int(stride)
+        self._lists = None
+        self._nbrT = None
+        if nbr is None:
+            from .topology import _device
+            dev = _device()
+            nbr = torch.full((27, self.num_out), -1, dtype=torch.int32, device=dev)
+            ins = [_to_device_tensor(r, dev, torch.int64) for r in in_rows]
+            outs = [_to_device_tensor(r, dev, torch.int64) for r in out_rows]
+            for d in range(27):
+                if outs[d].numel():
+                    nbr[d, outs[d]] = ins[d].to(torch.int32)
+            self._lists = (ins, outs)
+            pair_counts = torch.tensor([int(o.numel()) for o in outs], dtype=torch.int64)
+        self.nbr = nbr
+        self._counts = pair_counts
+
+    @property
+    def device(self):
+        return self.nbr.device
+
+    @property
+    def pair_counts(self):
+        return self._counts.cpu().numpy().astype(np.int64)
+
+    @property
+    def total_pairs(self):
+        return int(self._counts.sum().item())
+
+    @staticmethod
+    def offset_index(di, dj, dk):
+        return (di + 1) * 9 + (dj + 1) * 3 + (dk + 1)
+
+    def _compact(self):
+        if self._lists is None:
+            counts = self.pair_counts
+            total = int(counts.sum())
+            dev = self.device
+            ins = torch.empty(total, dtype=torch.int64, device=dev)
+            outs = torch.empty(total, dtype=torch.int64, device=dev)
+            if total:
+                L = _lib.lib()
+                wsb = L.fvdb_kmap_compact_workspace_bytes(self.num_out)
+                ws = _lib.workspace(wsb, dev)
+                _lib.check(L.fvdb_kmap_compact(self.nbr.data_ptr(), self.num_out, ins.data_ptr(),
+                                               outs.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()),
+                           "kmap_compact")
+            bounds = np.concatenate([[0], np.cumsum(counts)])
+            self._lists = ([ins[bounds[d]:bounds[d + 1]] for d in range(27)],
+                           [outs[bounds[d]:bounds[d + 1]] for d in range(27)])
+        return self._lists
+
+    @property
+    def in_rows(self):
+        return self._compact()[0]
+
+    @property
+    def out_rows(self):
+        return self._compact()[1]
+
+    def transposed_table(self):
+        """nbrT[27, num_in]: nbrT[d][i] = o iff nbr[d][o] = i (dgrad / transposed conv)."""
+        if self._nbrT is None:
+            t = torch.empty((27, self.num_in), dtype=torch.int32, device=self.device)
+            L = _lib.lib()
+            _lib.check(L.fvdb_kmap_transpose(self.nbr.data_ptr(), self.num_out, self.num_in, t.data_ptr(),
+                                             _lib.stream_ptr()), "kmap_transpose")
+            self._nbrT = t
+        return self._nbrT
+
+    def __repr__(self):
+        return f"KernelMap(num_in={self.num_in}, num_out={self.num_out}, stride={self.stride})"
+
+
+def build_kernel_map(grid_in, grid_out, stride=1):
+    """Exactly the active (input, output) links per stencil offset (conv.py:105-122)."""
+    stride = int(stride)
+    if stride not in (1, 2):
+        raise ValueError(f"stride must be 1 or 2, got {stride}")
+    dev = grid_out.device
+    nbr = torch.empty((27, grid_out.num_voxels), dtype=torch.int32, device=dev)
+    counts = torch.zeros(27, dtype=torch.int64, device=dev)
+    if grid_out.num_voxels:
+        L = _lib.lib()
+        wsb = L.fvdb_kmap_workspace_bytes(grid_out.num_leaf_nodes)
+        ws = _lib.workspace(wsb, dev)
+        _lib.check(L.fvdb_kernel_map(C.byref(grid_in.view()), C.byref(grid_out.view()), stride, nbr.data_ptr(),
+                                     counts.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()), "kernel_map")
+    return KernelMap(num_in=grid_in.num_voxels, num_out=grid_out.num_voxels, stride=stride, nbr=nbr,
+                     pair_counts=counts)
+
+
+def batch_kernel_map(kmaps, in_offsets, out_offsets):
+    """Concatenate per-grid kernel maps into one batch-global table (row offsets added)."""
+    parts = []
+    for km, io in zip(kmaps, in_offsets):
+        t = km.nbr
+        parts.append(torch.where(t >= 0, t + int(io), t))
+    nbr = torch.cat(parts, dim=1).contiguous() if parts else None
+    counts = torch.stack([km._counts.to(nbr.device) for km in kmaps]).sum(0)
+    num_in = sum(km.num_in for km in kmaps)
+    num_out = sum(km.num_out for km in kmaps)
+    return KernelMap(num_in=num_in, num_out=num_out, stride=kmaps[0].stride, nbr=nbr, pair_counts=counts)
+
+
+def choose_variant(grid, c_in, c_out):
+    """Advisory heuristic keyed on leaf occupancy and channel depth (conv.py:125-133)."""
+    occ = grid.leaf_occupancy()
+    depth = min(c_in, c_out)
+    if occ < 0.20:
+        return "lggs" if depth >= 64 else "igemm"
+    if occ > 0.40 and depth >= 16:
+        return "brick"
+    return "leaf" if depth <= 32 else "igemm"
+
+
+# ---------------------------------------------------------------------------
+# low-level device operators (shared by the functional API and SparseConv3d)
+# ---------------------------------------------------------------------------
+
+def _dtype_code(dt):
+    if dt == torch.float32:
+        return _lib.DTYPE_F32
+    if dt == torch.float64:
+        return _lib.DTYPE_F64
+    if dt == torch.bfloat16:
+        return _lib.DTYPE_BF16
+    raise TypeError(f"unsupported feature dtype {dt}; expected float32, float64 or bfloat16")
+
+
+def pack_weights_kn(w: torch.Tensor, transpose: bool, dtype) -> torch.Tensor:
+    """[Cout,Cin,3,3,3] -> Wk[27][K][N] in `dtype` (transpose: K=Cout, N=Cin)."""
+    from .topology import _device
+    w = w.to(device=_device(), dtype=dtype).contiguous()
+    cout, cin = int(w.shape[0]), int(w.shape[1])
+    K, N = (cout, cin) if transpose else (cin, cout)
+    out = torch.empty((27, K, N), dtype=dtype, device=w.device)
+    L = _lib.lib()
+    _lib.check(L.fvdb_pack_weights_kn(_dtype_code(dtype), w.data_ptr(), cout, cin, int(transpose), out.data_ptr(),
+                                      _lib.stream_ptr()), "pack_weights_kn")
+    return out
+
+
+def pack_weights_umma(w: torch.Tensor, transpose: bool) -> torch.Tensor:
+    """fp32 [Cout,Cin,3,3,3] -> bf16 UMMA B-operand images (27 x K x N, swizzled)."""
+    from .topology import _device
+    w = w.to(device=_device(), dtype=torch.float32).contiguous()
+    cout, cin = int(w.shape[0]), int(w.shape[1])
+    img = torch.empty(27 * cout * cin * 2, dtype=torch.uint8, device=w.device)
+    L = _lib.lib()
+    _lib.check(L.fvdb_pack_weights_umma(w.data_ptr(), cout, cin, int(transpose), img.data_ptr(), _lib.stream_ptr()),
+               "pack_weights_umma")
+    return img
+
+
+def _pad_cols(x: torch.Tensor, c: int) -> torch.Tensor:
+    if x.shape[1] == c:
+        return x.contiguous()
+    out = torch.zeros((x.shape[0], c), dtype=x.dtype, device=x.device)
+    out[:, :x.shape[1]] = x
+    return out
+
+
+def _tc_width(c: int) -> int:
+    for t in TC_CHANNELS:
+        if c <= t:
+            return t
+    raise ValueError(f"bf16 tensor-core path supports up to 128 channels per operand, got {c}")
+
+
+def gather_conv(x: torch.Tensor, nbr: torch.Tensor, w: torch.Tensor, transpose: bool = False,
+                out_dtype=None, w_image=None) -> torch.Tensor:
+    """out[o] = Σ_d x[nbr[d][o]] @ Wk[d]; Wk from w [Cout,Cin,3,3,3] (transpose → dgrad form).
+
+    x: [n_in, K] float32 / float64 / bfloat16 CUDA tensor.  Returns [n_out, N].
+    """
+    n_out = int(nbr.shape[1])
+    cout, cin = int(w.shape[0]), int(w.shape[1])
+    K, N = (cout, cin) if transpose else (cin, cout)
+    if x.shape[1] != K:
+        raise ValueError(f"feature channels {x.shape[1]} != kernel K {K}")
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    x = x.contiguous()
+    if x.dtype in (torch.float32, torch.float64):
+        wk = pack_weights_kn(w, transpose, x.dtype)
+        out = torch.empty((n_out, N), dtype=x.dtype, device=x.device)
+        if n_out:
+            _lib.check(L.fvdb_conv_gather_simt(_dtype_code(x.dtype), x.data_ptr(), x.shape[0], K, wk.data_ptr(), N,
+                                               nbr.data_ptr(), n_out, out.data_ptr(), st), "conv_gather_simt")
+        return out
+    if x.dtype != torch.bfloat16:
+        raise TypeError(f"unsupported feature dtype {x.dtype}")
+    out_dtype = out_dtype or torch.bfloat16
+    Kp, Np = _tc_width(K), _tc_width(N)
+    if (Kp, Np) != (K, N):
+        wp = torch.zeros(((Np, Kp) if not transpose else (Kp, Np)) + (3, 3, 3), dtype=torch.float32,
+                         device=x.device)
+        wp[:cout, :cin] = w.to(device=x.device, dtype=torch.float32)
+        y = gather_conv(_pad_cols(x, Kp), nbr, wp, transpose, out_dtype)
+        return y[:, :N].contiguous()
+    img = w_image if w_image is not None else pack_weights_umma(w, transpose)
+    out = torch.empty((n_out, N), dtype=out_dtype, device=x.device)
+    if n_out:
+        _lib.check(L.fvdb_conv_gather_tc(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, nbr.data_ptr(), n_out,
+                                         out.data_ptr(), _dtype_code(out_dtype), st), "conv_gather_tc")
+    return out
+
+
+def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: torch.Tensor) -> torch.Tensor:
+    """gw[co][ci][d] = Σ_o go[o,co]·x[nbr[d][o],ci]  → [Cout, Cin, 3, 3, 3] (fp32 for bf16 inputs)."""
+    n_out = int(nbr.shape[1])
+    cin, cout = int(x.shape[1]), int(go.shape[1])
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    x, go = x.contiguous(), go.contiguous()
+    if x.dtype in (torch.float32, torch.float64):
+        gw = torch.empty((cout, cin, 3, 3, 3), dtype=x.dtype, device=x.device)
+        code = _dtype_code(x.dtype)
+        wsb = L.fvdb_wgrad_workspace_bytes(code, n_out, cin, cout)
+        ws = _lib.workspace(wsb, x.device)
+        _lib.check(L.fvdb_conv_wgrad_simt(code, x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, nbr.data_ptr(),
+                                          n_out, gw.data_ptr(), ws.data_ptr(), wsb, st), "conv_wgrad_simt")
+        return gw
+    ci_p, co_p = _tc_width(cin), _tc_width(cout)
+    if (ci_p, co_p) != (cin, cout):
+        gw = wgrad(_pad_cols(x, ci_p), _pad_cols(go, co_p), nbr)
+        return gw[:cout, :cin].contiguous()
+    gw = torch.empty((cout, cin, 3, 3, 3), dtype=torch.float32, device=x.device)
+    wsb = L.fvdb_wgrad_tc_workspace_bytes(n_out, cin, cout)
+    ws = _lib.workspace(wsb, x.device)
+    _lib.check(L.fvdb_conv_wgrad_tc(x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, nbr.data_ptr(), n_out,
+                                    gw.data_ptr(), ws.data_ptr(), wsb, st), "conv_wgrad_tc")
+    return gw
+
+
+def lggs_stats(nbr: torch.Tensor, stats: dict):
+    """LGGS instrumentation counters (conv.py:264-301): 64-row blocks, per-offset pad to 16."""
+    n = int(nbr.shape[1])
+    nblocks = (n + LGGS_BLOCK - 1) // LGGS_BLOCK
+    valid = (nbr >= 0).to(torch.int32)
+    pad = nblocks * LGGS_BLOCK - n
+    if pad:
+        valid = torch.nn.functional.pad(valid, (0, pad))
+    cnt = valid.reshape(27, nblocks, LGGS_BLOCK).sum(-1)
+    pads = (-cnt) % LGGS_PAD
+    stats["lggs_blocks"] = nblocks
+    stats["lggs_pad_rows_total"] = int(pads.sum().item())
+    stats["lggs_pad_rows_max"] = int(pads.max().item()) if pads.numel() else 0
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible functional API
+# ---------------------------------------------------------------------------
+
+def conv(grid_in, features, kernel, grid_out=None, variant="igemm", stride=1, kmap=None, stats=None):
+    """Sparse convolution out[o] = Σ_d W[:, :, d] @ in[stride·o + d] (conv.py:136-177)."""
+    stride = int(stride)
+    weights = _kernel_weights(kernel)
+    dev = grid_in.device
+    features = _to_device_tensor(features, dev)
+    w_shape = tuple(weights.shape)
+    if features.ndim != 2 or features.shape[0] != grid_in.num_voxels:
+        raise ValueError(f"features must be [{grid_in.num_voxels}, C_in], got {tuple(features.shape)}")
+    if features.shape[1] != w_shape[1]:
+        raise ValueError(f"feature channels {features.shape[1]} != kernel C_in {w_shape[1]}")
+    if len(w_shape) != 5 or w_shape[2:] != (3, 3, 3):
+        raise ValueError(f"kernel weights must be [C_out, C_in, 3, 3, 3], got {w_shape}")
+    if grid_out is None:
+        grid_out = grid_in if stride == 1 else _coarsen_grid(grid_in, 2)
+    if variant == "auto":
+        variant = choose_variant(grid_in, w_shape[1], w_shape[0])
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+    if variant != "igemm" and stride != 1:
+        raise ValueError(f"variant {variant!r} supports stride 1 only (got stride {stride})")
+    _dtype_code(features.dtype)
+    w = _to_device_tensor(weights, dev)
+    if features.dtype != torch.bfloat16:
+        w = w.to(features.dtype)  # conv.py:164
+    if kmap is None:
+        kmap = build_kernel_map(grid_in, grid_out, stride)
+    out = gather_conv(features, kmap.nbr, w, transpose=False)
+    if variant == "lggs" and stats is not None:
+        lggs_stats(kmap.nbr, stats)
+    return out
+
+
+def conv_backward(kmap, grad_out, features_in, kernel):
+    """(grad_in, grad_kernel) of the forward (conv.py:339-368)."""
+    weights = _kernel_weights(kernel)
+    dev = kmap.device
+    grad_out = _to_device_tensor(grad_out, dev)
+    features_in = _to_device_tensor(features_in, dev)
+    c_out, c_in = int(weights.shape[0]), int(weights.shape[1])
+    if tuple(grad_out.shape) != (kmap.num_out, c_out):
+        raise ValueError(f"grad_out must be [{kmap.num_out}, {c_out}], got {tuple(grad_out.shape)}")
+    if tuple(features_in.shape) != (kmap.num_in, c_in):
+        raise ValueError(f"features_in must be [{kmap.num_in}, {c_in}], got {tuple(features_in.shape)}")
+    w = _to_device_tensor(weights, dev)
+    w_dtype = w.dtype
+    if grad_out.dtype != torch.bfloat16:
+        w = w.to(grad_out.dtype)
+    grad_in = gather_conv(grad_out, kmap.transposed_table(), w, transpose=True,
+                          out_dtype=features_in.dtype if features_in.dtype == torch.bfloat16 else None)
+    grad_in = grad_in.to(features_in.dtype)
+    gw = wgrad(features_in.to(grad_out.dtype) if grad_out.dtype != torch.bfloat16 else features_in.to(torch.bfloat16),
+               grad_out, kmap.nbr)
+    return grad_in, gw.to(w_dtype)
+
+
+def conv_transpose(kmap, x_coarse, kernel, out_dtype=None):
+    """Transposed (stride-2 adjoint) conv, SURVEY §8.0 C7.
+
+    y[i] = Σ_d Σ_{(i,o)∈K_d} x_coarse[o] @ W_d  with ``kernel`` [C_coarse, C_fine, 3, 3, 3]
+    (PyTorch ConvTranspose orientation) and ``kmap`` the stride-2 fine→coarse map.
+    Equals ``conv_backward(kmap, x_coarse, 0, kernel)[0]``.
+    """
+    weights = _kernel_weights(kernel)
+    dev = kmap.device
+    x = _to_device_tensor(x_coarse, dev)
+    if tuple(x.shape) != (kmap.num_out, int(weights.shape[0])):
+        raise ValueError(f"x_coarse must be [{kmap.num_out}, {int(weights.shape[0])}], got {tuple(x.shape)}")
+    w = _to_device_tensor(weights, dev)
+    if x.dtype != torch.bfloat16:
+        w = w.to(x.dtype)
+    return gather_conv(x, kmap.transposed_table(), w, transpose=True, out_dtype=out_dtype)
+
+
+def conv_batch(batch, features, kernel, variant="igemm"):
+    """Stride-1 convolution per batch element, one launch for the batch (conv.py:371-383)."""
+    from .jagged import GridBatch
+    if not isinstance(batch, GridBatch):
+        raise TypeError("conv_batch needs a GridBatch; use conv() for a single grid")
+    feats = _to_device_tensor(batch.check_features(features), batch.device)
+    weights = _kernel_weights(kernel)
+    if variant == "auto":
+        variant = choose_variant(batch.grids[0], int(weights.shape[1]), int(weights.shape[0]))
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+    if feats.shape[1] != int(weights.shape[1]):
+        raise ValueError(f"feature channels {feats.shape[1]} != kernel C_in {int(weights.shape[1])}")
+    km = batch_grid_kernel_map(batch, batch, 1)
+    w = _to_device_tensor(weights, feats.device)
+    if feats.dtype != torch.bfloat16:
+        w = w.to(feats.dtype)
+    return batch.jagged(gather_conv(feats, km.nbr, w))
+
+
+def batch_grid_kernel_map(batch_in, batch_out, stride):
+    """Batch-global kernel map of two aligned GridBatches (cached on ``batch_out``)."""
+    key = (id(batch_in), stride)
+    cached = batch_out._kmaps.get(key)
+    if cached is not None:
+        return cached
+    kms = [build_kernel_map(gi, go, stride) for gi, go in zip(batch_in.grids, batch_out.grids)]
+    km = kms[0] if len(kms) == 1 else batch_kernel_map(kms, batch_in.voxel_joffsets[:, 0].tolist(),
+                                                       batch_out.voxel_joffsets[:, 0].tolist())
+    batch_out._kmaps[key] = km
+    return km

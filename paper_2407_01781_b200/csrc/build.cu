@@ -1,0 +1,384 @@
+// build.cu — index-grid construction on the GPU.
+//
+// Reference algorithm (pkg/src/idxgrid/build.py:82-198): pack 63-bit tile keys,
+// stable radix sort, run-length encode into root tiles, pack per-run voxel keys
+// (rank<<36 | upper<<21 | lower<<9 | leaf), sort, dedupe, then register nodes from
+// the distinct key prefixes (>>9 leaf, >>21 lower, >>36 upper).
+//
+// B200 mapping:
+//   * one pass computes tile keys, the ±2^30 range check (first bad row by
+//     atomicMin) and the OR/AND of all keys; when every coordinate falls in one
+//     root tile (the common case) the tile sort is skipped entirely, otherwise
+//     only the varying bit range [lo,hi] is radix-sorted;
+//   * the voxel keys are radix-sorted over only 36 + ceil(log2 #tiles) bits;
+//   * dedupe = DeviceSelect::Unique; node heads are flags over the unique keys
+//     and node ids are inclusive scans — no per-node loops, no host round trips
+//     beyond the count reads the two-phase ABI needs;
+//   * node registration writes every topology array in one voxel-parallel pass;
+//     leaf masks are built with 64-bit atomicOr (bits within one word commute, so
+//     the result is deterministic).
+// Sort / unique / scan primitives come from CUB (header-only, compiled into this
+// library for sm_100a).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace fvdb {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct BuildScalars {
+    unsigned long long bad_row;   // min offending row, ~0 if none
+    unsigned long long key_or;
+    unsigned long long key_and;
+    long long n_tiles;
+    int n_unique;
+    int pad;
+};
+
+struct BuildWs {
+    uint64_t *tk, *tk_alt, *vk, *vk_alt, *tiles, *uvox;
+    int *leaf_id, *lower_id, *upper_id, *n_sel;
+    BuildScalars* sc;
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+
+size_t cub_temp_bytes(int n) {
+    size_t a = 0, b = 0, c = 0, d = 0;
+    cub::DoubleBuffer<uint64_t> db(nullptr, nullptr);
+    cub::DeviceRadixSort::SortKeys(nullptr, a, db, n, 0, 64);
+    cub::DeviceSelect::Unique(nullptr, b, (uint64_t*)nullptr, (uint64_t*)nullptr, (int*)nullptr, n);
+    cub::DeviceScan::InclusiveSum(nullptr, c, (int*)nullptr, (int*)nullptr, n);
+    cub::DeviceScan::ExclusiveSum(nullptr, d, (int*)nullptr, (int*)nullptr, n);
+    size_t m = a > b ? a : b;
+    m = m > c ? m : c;
+    return m > d ? m : d;
+}
+
+template <class C>
+void carve(C& c, int64_t n, size_t cub_bytes, BuildWs* w) {
+    size_t m = (size_t)(n > 0 ? n : 1);
+    if constexpr (std::is_same_v<C, Carver>) {
+        w->tk = c.template take<uint64_t>(m);
+        w->tk_alt = c.template take<uint64_t>(m);
+        w->vk = c.template take<uint64_t>(m);
+        w->vk_alt = c.template take<uint64_t>(m);
+        w->tiles = c.template take<uint64_t>(m);
+        w->uvox = c.template take<uint64_t>(m);
+        w->leaf_id = c.template take<int>(m);
+        w->lower_id = c.template take<int>(m);
+        w->upper_id = c.template take<int>(m);
+        w->n_sel = c.template take<int>(4);
+        w->sc = c.template take<BuildScalars>(1);
+        w->cub_tmp = c.template take<char>(cub_bytes);
+        w->cub_bytes = cub_bytes;
+    } else {
+        for (int i = 0; i < 6; ++i) c.template take<uint64_t>(m);
+        for (int i = 0; i < 3; ++i) c.template take<int>(m);
+        c.template take<int>(4);
+        c.template take<BuildScalars>(1);
+        c.template take<char>(cub_bytes);
+    }
+}
+
+__global__ void k_init_scalars(BuildScalars* s) {
+    s->bad_row = ~0ull;
+    s->key_or = 0ull;
+    s->key_and = ~0ull;
+    s->n_tiles = 0;
+    s->n_unique = 0;
+}
+
+// tile keys + range check + OR/AND reduction (build.py:96-101, topology.py:83-88)
+__global__ void k_tile_keys(const int64_t* __restrict__ coords, int64_t n, uint64_t* __restrict__ tk,
+                            BuildScalars* sc) {
+    uint64_t k_or = 0, k_and = ~0ull;
+    const int64_t lim = (int64_t)1 << 30;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
+        bool bad = (i > lim) | (i < -lim) | (j > lim) | (j < -lim) | (k > lim) | (k < -lim);
+        if (bad) atomicMin(&sc->bad_row, (unsigned long long)r);
+        uint64_t key = tile_key(i, j, k);
+        tk[r] = key;
+        k_or |= key;
+        k_and &= key;
+    }
+    typedef cub::BlockReduce<uint64_t, kThreads> BR;
+    __shared__ typename BR::TempStorage t1;
+    uint64_t bo = BR(t1).Reduce(k_or, [](uint64_t a, uint64_t b) { return a | b; });
+    __syncthreads();
+    uint64_t ba = BR(t1).Reduce(k_and, [](uint64_t a, uint64_t b) { return a & b; });
+    if (threadIdx.x == 0) {
+        atomicOr(&sc->key_or, (unsigned long long)bo);
+        atomicAnd(&sc->key_and, (unsigned long long)ba);
+    }
+}
+
+// voxel keys: rank<<36 | upper<<21 | lower<<9 | leaf (build.py:74-79, 126-131)
+__global__ void k_voxel_keys(const int64_t* __restrict__ coords, int64_t n,
+                             const uint64_t* __restrict__ tiles, int64_t n_tiles,
+                             uint64_t* __restrict__ vk) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
+        uint64_t rank = 0;
+        if (n_tiles > 1) rank = (uint64_t)lower_bound_u64(tiles, n_tiles, tile_key(i, j, k));
+        vk[r] = (rank << 36) | ((uint64_t)upper_off(i, j, k) << 21) |
+                ((uint64_t)lower_off(i, j, k) << 9) | leaf_off(i, j, k);
+    }
+}
+
+// node head flags over the sorted unique voxel keys (build.py:150-152)
+__global__ void k_node_heads(const uint64_t* __restrict__ uvox, int n, int* __restrict__ leaf_h,
+                             int* __restrict__ lower_h, int* __restrict__ upper_h) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint64_t v = uvox[i];
+        uint64_t p = i ? uvox[i - 1] : ~v;
+        leaf_h[i] = (v >> 9) != (p >> 9);
+        lower_h[i] = (v >> 21) != (p >> 21);
+        upper_h[i] = (v >> 36) != (p >> 36);
+    }
+}
+
+// one pass writing every topology array (build.py:145-198)
+__global__ void k_register(const uint64_t* __restrict__ uvox, int n, const uint64_t* __restrict__ tiles,
+                           const int* __restrict__ leaf_id, const int* __restrict__ lower_id,
+                           const int* __restrict__ upper_id, fvdb_grid_arrays o, int64_t n_leaf,
+                           int64_t n_lower, int64_t n_upper) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint64_t v = uvox[i];
+        int leaf = leaf_id[i] - 1;
+        atomicOr((unsigned long long*)&o.leaf_masks[(int64_t)leaf * 8 + ((v >> 6) & 7)],
+                 1ull << (v & 63));
+        uint64_t p = i ? uvox[i - 1] : ~v;
+        if ((v >> 9) == (p >> 9)) continue;  // not a leaf head
+        uint64_t rank = v >> 36;
+        uint64_t tkey = tiles[rank];
+        int64_t ox = tile_field_origin(tkey, 42), oy = tile_field_origin(tkey, 21),
+                oz = tile_field_origin(tkey, 0);
+        uint32_t up = (uint32_t)((v >> 21) & 0x7FFF), lo = (uint32_t)((v >> 9) & 0xFFF);
+        int64_t lx = ox + ((int64_t)((up >> 10) & 31) << 7), ly = oy + ((int64_t)((up >> 5) & 31) << 7),
+                lz = oz + ((int64_t)(up & 31) << 7);
+        o.leaf_keys[leaf] = v >> 9;
+        o.leaf_offset_in_lower[leaf] = (uint16_t)lo;
+        o.leaf_value_offset[leaf] = (uint64_t)i + 1;  // 1 + exclusive scan of leaf popcounts
+        o.leaf_origins[3 * (int64_t)leaf + 0] = lx + ((int64_t)((lo >> 8) & 15) << 3);
+        o.leaf_origins[3 * (int64_t)leaf + 1] = ly + ((int64_t)((lo >> 4) & 15) << 3);
+        o.leaf_origins[3 * (int64_t)leaf + 2] = lz + ((int64_t)(lo & 15) << 3);
+        if ((v >> 21) == (p >> 21)) continue;  // not a lower head
+        int lower = lower_id[i] - 1;
+        o.lower_child_starts[lower] = leaf;
+        o.lower_offset_in_upper[lower] = (uint16_t)up;
+        o.lower_origins[3 * (int64_t)lower + 0] = lx;
+        o.lower_origins[3 * (int64_t)lower + 1] = ly;
+        o.lower_origins[3 * (int64_t)lower + 2] = lz;
+        if ((v >> 36) == (p >> 36)) continue;  // not an upper head
+        int upper = upper_id[i] - 1;
+        o.upper_child_starts[upper] = lower;
+        o.tile_keys[upper] = tkey;
+        o.upper_origins[3 * (int64_t)upper + 0] = ox;
+        o.upper_origins[3 * (int64_t)upper + 1] = oy;
+        o.upper_origins[3 * (int64_t)upper + 2] = oz;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        o.lower_child_starts[n_lower] = n_leaf;
+        o.upper_child_starts[n_upper] = n_lower;
+    }
+}
+
+// packed 9-bit cumulative popcounts of words 0..6 (build.py:161-166)
+__global__ void k_leaf_prefix(const uint64_t* __restrict__ masks, int64_t n_leaf,
+                              uint64_t* __restrict__ prefix) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n_leaf;
+         l += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t acc = 0, cum = 0;
+        for (int t = 0; t < 7; ++t) {
+            cum += __popcll(masks[8 * l + t]);
+            acc |= cum << (9 * t);
+        }
+        prefix[l] = acc;
+    }
+}
+
+__global__ void k_floor_div(const int64_t* __restrict__ c, int64_t n, int64_t f, int64_t* __restrict__ o) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < 3 * n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v = c[r];
+        int64_t q = v / f;
+        if ((v % f != 0) && ((v < 0) != (f < 0))) --q;  // floor semantics (build.py:331)
+        o[r] = q;
+    }
+}
+
+// IEEE f64: sub -> div -> add(0.5) -> floor, no contraction (topology.py:128-137)
+__global__ void k_quantize(const double* __restrict__ p, int64_t n, double vx, double vy, double vz,
+                           double ox, double oy, double oz, int64_t* __restrict__ out,
+                           unsigned long long* bad) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double x = p[3 * r], y = p[3 * r + 1], z = p[3 * r + 2];
+        if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
+            atomicMin(bad, (unsigned long long)r);
+            x = y = z = 0.0;
+        }
+        out[3 * r + 0] = (int64_t)floor(__dadd_rn(__ddiv_rn(__dsub_rn(x, ox), vx), 0.5));
+        out[3 * r + 1] = (int64_t)floor(__dadd_rn(__ddiv_rn(__dsub_rn(y, oy), vy), 0.5));
+        out[3 * r + 2] = (int64_t)floor(__dadd_rn(__ddiv_rn(__dsub_rn(z, oz), vz), 0.5));
+    }
+}
+
+int grid_for(int64_t n) {
+    int64_t b = ceil_div(n > 0 ? n : 1, kThreads);
+    return (int)(b < 148 * 16 ? b : 148 * 16);
+}
+
+int bit_length(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+}  // namespace
+}  // namespace fvdb
+
+using namespace fvdb;
+
+extern "C" size_t fvdb_build_workspace_bytes(int64_t n) {
+    Sizer s;
+    BuildWs w;
+    carve(s, n, cub_temp_bytes((int)(n > 0 ? n : 1)), &w);
+    return s.used + 256;
+}
+
+extern "C" int fvdb_build_plan(const int64_t* coords, int64_t n, void* workspace, size_t ws_bytes,
+                               int64_t* counts, int64_t* detail, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n <= 0 || n >= (int64_t)INT32_MAX) return FVDB_ERR_INVALID;
+    Carver c(workspace, ws_bytes);
+    BuildWs w;
+    carve(c, n, cub_temp_bytes((int)n), &w);
+    if (!c.ok()) return FVDB_ERR_WORKSPACE;
+    const int g = grid_for(n);
+
+    k_init_scalars<<<1, 1, 0, st>>>(w.sc);
+    k_tile_keys<<<g, kThreads, 0, st>>>(coords, n, w.tk, w.sc);
+    FVDB_LAUNCH_CHECK();
+    BuildScalars hs;
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hs.bad_row != ~0ull) {
+        *detail = (int64_t)hs.bad_row;
+        return FVDB_ERR_COORD_RANGE;
+    }
+
+    // root tiles: sorted distinct tile keys (build.py:111-124)
+    int64_t n_tiles = 1;
+    uint64_t diff = hs.key_or ^ hs.key_and;
+    if (diff == 0) {
+        FVDB_CUDA_TRY(cudaMemcpyAsync(w.tiles, &hs.key_or, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    } else {
+        int lo_bit = __builtin_ctzll(diff), hi_bit = bit_length(diff);
+        cub::DoubleBuffer<uint64_t> db(w.tk, w.tk_alt);
+        size_t tb = w.cub_bytes;
+        FVDB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, db, (int)n, lo_bit, hi_bit, st));
+        tb = w.cub_bytes;
+        FVDB_CUDA_TRY(cub::DeviceSelect::Unique(w.cub_tmp, tb, db.Current(), w.tiles, w.n_sel, (int)n, st));
+        int nt = 0;
+        FVDB_CUDA_TRY(cudaMemcpyAsync(&nt, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
+        FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+        n_tiles = nt;
+    }
+    if (n_tiles > ((int64_t)1 << 28)) {
+        *detail = n_tiles;
+        return FVDB_ERR_ROOT_LIMIT;
+    }
+
+    // voxel keys sorted over the significant bits only, then dedupe (build.py:126-134)
+    k_voxel_keys<<<g, kThreads, 0, st>>>(coords, n, w.tiles, n_tiles, w.vk);
+    FVDB_LAUNCH_CHECK();
+    int end_bit = 36 + bit_length((uint64_t)(n_tiles - 1));
+    cub::DoubleBuffer<uint64_t> vb(w.vk, w.vk_alt);
+    size_t tb = w.cub_bytes;
+    FVDB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, vb, (int)n, 0, end_bit, st));
+    tb = w.cub_bytes;
+    FVDB_CUDA_TRY(cub::DeviceSelect::Unique(w.cub_tmp, tb, vb.Current(), w.uvox, w.n_sel, (int)n, st));
+    int nu = 0;
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&nu, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+
+    // node ids = inclusive scans of head flags (build.py:148-150)
+    const int gu = grid_for(nu);
+    k_node_heads<<<gu, kThreads, 0, st>>>(w.uvox, nu, w.leaf_id, w.lower_id, w.upper_id);
+    FVDB_LAUNCH_CHECK();
+    int* ids[3] = {w.leaf_id, w.lower_id, w.upper_id};
+    for (int t = 0; t < 3; ++t) {
+        tb = w.cub_bytes;
+        FVDB_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, ids[t], ids[t], nu, st));
+    }
+    int last[3];
+    for (int t = 0; t < 3; ++t)
+        FVDB_CUDA_TRY(cudaMemcpyAsync(&last[t], ids[t] + (nu - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+    // store counts for fill()
+    BuildScalars fin = hs;
+    fin.n_tiles = n_tiles;
+    fin.n_unique = nu;
+    FVDB_CUDA_TRY(cudaMemcpyAsync(w.sc, &fin, sizeof(fin), cudaMemcpyHostToDevice, st));
+    FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+    counts[0] = last[2];  // num_upper
+    counts[1] = last[1];  // num_lower
+    counts[2] = last[0];  // num_leaf
+    counts[3] = nu;       // num_voxels
+    if (counts[0] != n_tiles) {
+        set_error_msg("internal: tile count mismatch");
+        return FVDB_ERR_INVALID;
+    }
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_build_fill(void* workspace, size_t ws_bytes, int64_t n, const int64_t* counts,
+                               const fvdb_grid_arrays* out, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n <= 0 || n >= (int64_t)INT32_MAX) return FVDB_ERR_INVALID;
+    Carver c(workspace, ws_bytes);
+    BuildWs w;
+    carve(c, n, cub_temp_bytes((int)n), &w);
+    if (!c.ok()) return FVDB_ERR_WORKSPACE;
+    const int64_t n_upper = counts[0], n_lower = counts[1], n_leaf = counts[2];
+    const int nu = (int)counts[3];
+    // ids are inclusive scans of head flags; k_register subtracts one
+    FVDB_CUDA_TRY(cudaMemsetAsync(out->leaf_masks, 0, (size_t)n_leaf * 8 * sizeof(uint64_t), st));
+    const int gu = grid_for(nu);
+    k_register<<<gu, kThreads, 0, st>>>(w.uvox, nu, w.tiles, w.leaf_id, w.lower_id, w.upper_id, *out,
+                                        n_leaf, n_lower, n_upper);
+    k_leaf_prefix<<<grid_for(n_leaf), kThreads, 0, st>>>(out->leaf_masks, n_leaf, out->leaf_prefix);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_floor_div_coords(const int64_t* coords, int64_t n, int64_t factor, int64_t* out,
+                                     void* stream_) {
+    if (factor < 1) return FVDB_ERR_INVALID;
+    if (n == 0) return FVDB_OK;
+    k_floor_div<<<grid_for(3 * n), kThreads, 0, as_stream(stream_)>>>(coords, n, factor, out);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_quantize_points(const double* points, int64_t n, const double* vs, const double* og,
+                                    int64_t* coords_out, int64_t* detail, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n == 0) return FVDB_OK;
+    // the offending-row slot lives just past the output (caller allocates n*3+1 int64)
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(coords_out + 3 * n);
+    FVDB_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), st));
+    k_quantize<<<grid_for(n), kThreads, 0, st>>>(points, n, vs[0], vs[1], vs[2], og[0], og[1], og[2],
+                                                 coords_out, bad);
+    FVDB_LAUNCH_CHECK();
+    unsigned long long hb = 0;
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hb != ~0ull) {
+        *detail = (int64_t)hb;
+        return FVDB_ERR_NONFINITE;
+    }
+    return FVDB_OK;
+}

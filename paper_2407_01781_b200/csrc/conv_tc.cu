@@ -1,0 +1,514 @@
+// conv_tc.cu — tensor-core sparse convolution for sm_100a (tcgen05 + TMEM).
+//
+// Operator (reference conv.py:180-191 forward, conv.py:339-368 backward):
+//   gather conv:  out[o,:] = Σ_d in[nbr[d][o],:] · Wk[d]          (forward, dgrad)
+//   wgrad:        gw[:,:,d] = Σ_o go[o,:]ᵀ ⊗ in[nbr[d][o],:]
+//
+// Forward / dgrad kernel ("implicit GEMM, output-stationary", LGGS-style
+// sequential write-back: conv.py:264-301 is the blocked CPU analogue):
+//   * a persistent CTA owns tiles of 128 consecutive output rows; for each of the
+//     27 offsets a 128×K bf16 A tile is gathered row-by-row with 16-byte
+//     cp.async (L1-allocating: each input row is re-read by ~20 neighbours) into
+//     a 128B-swizzled K-major shared-memory stage, and the offset's pre-swizzled
+//     weight image (N×K, the UMMA B operand) lands by one TMA bulk copy;
+//   * one elected thread issues tcgen05.mma (M=128, N=Cout, K=16 steps) into a
+//     TMEM fp32 accumulator — all 27 offsets accumulate in TMEM, no scatter;
+//   * accumulators are double-buffered in TMEM so the 4 epilogue warps
+//     (tcgen05.ld → registers → global) drain tile t while tile t+1 computes;
+//   * warp roles: 4 producer warps, 4 epilogue warps, 1 MMA/TMEM warp, with
+//     mbarrier full/empty rings between producer and MMA and tmem full/empty
+//     barriers between MMA and epilogue.
+// Missing neighbours are zero-filled by cp.async (src-size 0): no branches in
+// the MMA stream, results independent of the schedule.
+//
+// wgrad kernel: D[(d,ci), co] = Σ_o in[nbr[d][o], ci] · go[o, co].  M=128 packs
+// 128/Cin offsets × Cin input channels (MN-major A = gathered input rows), N=Cout
+// (MN-major B = grad_out rows, shared by every offset of the CTA), K = output rows.
+// A CTA owns up to 8 M-blocks (TMEM ≤ 512 columns) for one output-row split;
+// partial [split][27][Cin][Cout] sums are reduced in a fixed order (deterministic).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace fvdb {
+namespace {
+
+using bf16 = __nv_bfloat16;
+using namespace tc;
+
+constexpr int kTile = 128;        // output rows per tile (UMMA M)
+constexpr int kThreadsTC = 288;   // 4 producer + 4 epilogue + 1 MMA warp
+
+__host__ __device__ constexpr int pow2_cols(int c) {
+    return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
+}
+
+// swizzled byte offset of 16-B chunk `c` in row `r` of a K-major tile with `rowb`-byte rows
+__host__ __device__ __forceinline__ uint32_t swz_off(int r, int c, int rowb) {
+    int x = rowb == 128 ? (r & 7) : ((r >> 1) & 3);
+    return (uint32_t)(r * rowb + ((c ^ x) << 4));
+}
+
+template <int K, int N>
+struct FwdCfg {
+    static constexpr int KB = K >= 64 ? 64 : K;  // K elements per swizzle row
+    static constexpr int ROWB = KB * 2;
+    static constexpr int NKB = K / KB;
+    static constexpr int A_BYTES = kTile * K * 2;
+    static constexpr int B_BYTES = N * K * 2;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (STAGE * 4 <= 100 * 1024) ? 4 : ((STAGE * 3 <= 200 * 1024) ? 3 : 2);
+    static constexpr int SMEM = STAGES * STAGE + 1024;
+    static constexpr uint32_t LAYOUT = ROWB == 128 ? kSwizzle128B : kSwizzle64B;
+    static constexpr int CPR = K / 8;           // 16-B chunks per gathered row
+    static constexpr int RSTEP = kTile / CPR;   // rows per producer pass
+    static constexpr int TMEM_COLS = pow2_cols(2 * N);
+    static constexpr uint32_t IDESC = idesc_bf16_f32(kTile, N, false, false);
+};
+
+template <int K, int N, bool OUT_BF16>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    k_conv_fwd_tc(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, const int32_t* __restrict__ nbr,
+                  int64_t n_out, void* __restrict__ out, int num_tiles) {
+    using C = FwdCfg<K, N>;
+    extern __shared__ uint8_t dsmem[];
+    __shared__ __align__(8) uint64_t bar_full[C::STAGES], bar_empty[C::STAGES], bar_tfull[2], bar_tempty[2];
+    __shared__ uint32_t tmem_slot;
+
+    const uint32_t base = (smem_u32(dsmem) + 1023u) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(smem_u32(&bar_full[s]), kTile + 1);  // 128 cp.async arrivals + 1 expect_tx
+            mbar_init(smem_u32(&bar_empty[s]), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(smem_u32(&bar_tfull[a]), 1);
+            mbar_init(smem_u32(&bar_tempty[a]), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 8) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp < 4) {
+        // ------------------------------ producers ------------------------------
+        const int pt = threadIdx.x;
+        const int cchunk = pt % C::CPR, rbase = pt / C::CPR;
+        const int kb = cchunk / (C::KB / 8), cc = cchunk % (C::KB / 8);
+        uint32_t it = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int64_t row0 = (int64_t)tile * kTile;
+            for (int d = 0; d < 27; ++d, ++it) {
+                const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
+                int32_t idx[C::CPR];
+#pragma unroll
+                for (int j = 0; j < C::CPR; ++j) {
+                    int64_t row = row0 + rbase + j * C::RSTEP;
+                    idx[j] = row < n_out ? __ldg(nbr + (int64_t)d * n_out + row) : -1;
+                }
+                mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+                const uint32_t sA = base + s * C::STAGE;
+#pragma unroll
+                for (int j = 0; j < C::CPR; ++j) {
+                    const int r = rbase + j * C::RSTEP;
+                    const uint32_t dst = sA + kb * (kTile * C::ROWB) + swz_off(r, cc, C::ROWB);
+                    const int32_t i = idx[j] < 0 ? 0 : idx[j];
+                    cp_async_16(dst, in + (int64_t)i * K + cchunk * 8, idx[j] < 0 ? 0u : 16u);
+                }
+                const uint32_t fb = smem_u32(&bar_full[s]);
+                if (pt == 0) {
+                    mbar_arrive_expect_tx(fb, C::B_BYTES);
+                    bulk_g2s(sA + C::A_BYTES, wimg + (size_t)d * C::B_BYTES, C::B_BYTES, fb);
+                }
+                cp_async_arrive_noinc(fb);
+            }
+        }
+    } else if (warp == 8) {
+        // ------------------------------ MMA issuer -----------------------------
+        uint32_t it = 0, lt = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
+            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+            mbar_wait(smem_u32(&bar_tempty[acc]), aph ^ 1);
+            tc_fence_after();
+            const uint32_t dt = tmem + acc * N;
+            for (int d = 0; d < 27; ++d, ++it) {
+                const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
+                mbar_wait(smem_u32(&bar_full[s]), ph);
+                fence_proxy_async_smem();
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sA = base + s * C::STAGE, sB = sA + C::A_BYTES;
+#pragma unroll
+                    for (int kb = 0; kb < C::NKB; ++kb)
+#pragma unroll
+                        for (int ks = 0; ks < C::KB / 16; ++ks) {
+                            uint64_t ad = smem_desc(sA + kb * kTile * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
+                            uint64_t bd = smem_desc(sB + kb * N * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
+                            mma_bf16(dt, ad, bd, C::IDESC, (d | kb | ks) != 0);
+                        }
+                    mma_commit(smem_u32(&bar_empty[s]));
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mma_commit(smem_u32(&bar_tfull[acc]));
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------ epilogue -------------------------------
+        const int q = warp & 3;
+        uint32_t lt = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
+            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+            mbar_wait(smem_u32(&bar_tfull[acc]), aph);
+            tc_fence_after();
+            const int64_t row = (int64_t)tile * kTile + q * 32 + lane;
+#pragma unroll
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * N + c0, v);
+                tmem_ld_wait();
+                if (row < n_out) {
+                    if constexpr (OUT_BF16) {
+                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(out) + row * N + c0);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint32_t p[4];
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * h]),
+                                                                          __uint_as_float(v[8 * j + 2 * h + 1]));
+                                p[h] = *reinterpret_cast<uint32_t*>(&b2);
+                            }
+                            dst[j] = make_uint4(p[0], p[1], p[2], p[3]);
+                        }
+                    } else {
+                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(out) + row * N + c0);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(smem_u32(&bar_tempty[acc]));
+        }
+    }
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+}
+
+// fp32 W[Cout][Cin][27] -> per-offset bf16 UMMA B images: [27][K/KB][N rows][KB] swizzled
+__global__ void k_pack_umma(const float* __restrict__ w, int cout, int cin, int transpose, uint8_t* __restrict__ img) {
+    const int K = transpose ? cout : cin, N = transpose ? cin : cout;
+    const int KB = K >= 64 ? 64 : K, rowb = KB * 2;
+    const int64_t total = (int64_t)27 * cout * cin;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t co = t / ((int64_t)cin * 27);
+        int64_t rem = t - co * cin * 27;
+        int ci = (int)(rem / 27), d = (int)(rem - (int64_t)ci * 27);
+        int n = transpose ? ci : (int)co, k = transpose ? (int)co : ci;
+        int kb = k / KB, e = k % KB;
+        size_t off = (size_t)d * N * K * 2 + (size_t)kb * N * rowb + swz_off(n, e >> 3, rowb) + (e & 7) * 2;
+        *reinterpret_cast<bf16*>(img + off) = __float2bfloat16_rn(w[t]);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// wgrad
+// ----------------------------------------------------------------------------
+template <int CIN, int COUT>
+struct WgCfg {
+    static constexpr int OPB = 128 / CIN;                      // offsets per M-block
+    static constexpr int NMB = (27 + OPB - 1) / OPB;           // M-blocks for all offsets
+    static constexpr int NACC0 = (512 / COUT) < NMB ? (512 / COUT) : NMB;
+    static constexpr int NACC = NACC0 < 8 ? NACC0 : 8;         // M-blocks (TMEM accumulators) per CTA
+    static constexpr int OFFS = NACC * OPB;                    // offsets per CTA
+    static constexpr int GROUPS = (27 + OFFS - 1) / OFFS;
+    static constexpr int TK = 32;                              // output rows (K) per stage
+    static constexpr int A_BLK = TK * 256;                     // one M-block: TK k-rows x 128 m bf16
+    static constexpr int B_BYTES = TK * COUT * 2;
+    static constexpr int STAGE = B_BYTES + NACC * A_BLK;
+    static constexpr int STAGES = (STAGE * 4 <= 200 * 1024) ? 4 : ((STAGE * 3 <= 216 * 1024) ? 3 : 2);
+    static constexpr int SMEM = STAGES * STAGE + 1024;
+    static constexpr int TMEM_COLS = pow2_cols(NACC * COUT);
+    static constexpr bool B_SW128 = (COUT % 64) == 0;
+    static constexpr uint32_t IDESC = idesc_bf16_f32(128, COUT, true, true);
+};
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    k_wgrad_tc(const bf16* __restrict__ in, const bf16* __restrict__ go, const int32_t* __restrict__ nbr,
+               int64_t n_out, int64_t rows_per_split, float* __restrict__ part) {
+    using C = WgCfg<CIN, COUT>;
+    extern __shared__ uint8_t dsmem[];
+    __shared__ __align__(8) uint64_t bar_full[C::STAGES], bar_empty[C::STAGES], bar_tfull;
+    __shared__ uint32_t tmem_slot;
+    const uint32_t base = (smem_u32(dsmem) + 1023u) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int group = blockIdx.x % C::GROUPS, split = blockIdx.x / C::GROUPS;
+    const int d0 = group * C::OFFS;
+    const int n_off = (27 - d0) < C::OFFS ? (27 - d0) : C::OFFS;     // offsets of this CTA
+    const int n_acc = (n_off + C::OPB - 1) / C::OPB;                  // live M-blocks
+    const int64_t o_begin = (int64_t)split * rows_per_split;
+    const int64_t o_end = (o_begin + rows_per_split) < n_out ? (o_begin + rows_per_split) : n_out;
+    const int n_steps = o_end > o_begin ? (int)ceil_div(o_end - o_begin, C::TK) : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(smem_u32(&bar_full[s]), 128);
+            mbar_init(smem_u32(&bar_empty[s]), 1);
+        }
+        mbar_init(smem_u32(&bar_tfull), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 8) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp < 4) {
+        const int pt = threadIdx.x;
+        const int a_rows = n_off * C::TK;
+        for (int step = 0; step < n_steps; ++step) {
+            const uint32_t s = step % C::STAGES, ph = (step / C::STAGES) & 1;
+            const int64_t o0 = o_begin + (int64_t)step * C::TK;
+            mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+            const uint32_t sB = base + s * C::STAGE, sA = sB + C::B_BYTES;
+            for (int t = pt; t < a_rows + C::TK; t += 128) {
+                if (t < a_rows) {
+                    const int u = t / C::TK, r = t % C::TK;
+                    const int64_t o = o0 + r;
+                    const int32_t i = o < o_end ? __ldg(nbr + (int64_t)(d0 + u) * n_out + o) : -1;
+                    const int a = u / C::OPB, m0 = (u % C::OPB) * CIN;
+                    const bf16* src = in + (int64_t)(i < 0 ? 0 : i) * CIN;
+#pragma unroll
+                    for (int c = 0; c < CIN / 8; ++c) {
+                        const int m = m0 + c * 8;
+                        const uint32_t dst = sA + a * C::A_BLK + (m >> 6) * (C::TK * 128) + swz_off(r, (m & 63) >> 3, 128);
+                        cp_async_16(dst, src + c * 8, i < 0 ? 0u : 16u);
+                    }
+                } else {
+                    const int r = t - a_rows;
+                    const int64_t o = o0 + r;
+                    const bool ok = o < o_end;
+                    const bf16* src = go + (ok ? o : 0) * COUT;
+#pragma unroll
+                    for (int c = 0; c < COUT / 8; ++c) {
+                        uint32_t dst;
+                        if constexpr (C::B_SW128)
+                            dst = sB + (c >> 3) * (C::TK * 128) + swz_off(r, c & 7, 128);
+                        else
+                            dst = sB + swz_off(r, c, 64);
+                        cp_async_16(dst, src + c * 8, ok ? 16u : 0u);
+                    }
+                }
+            }
+            cp_async_arrive_noinc(smem_u32(&bar_full[s]));
+        }
+    } else if (warp == 8) {
+        for (int step = 0; step < n_steps; ++step) {
+            const uint32_t s = step % C::STAGES, ph = (step / C::STAGES) & 1;
+            mbar_wait(smem_u32(&bar_full[s]), ph);
+            fence_proxy_async_smem();
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t sB = base + s * C::STAGE, sA = sB + C::B_BYTES;
+                for (int a = 0; a < n_acc; ++a) {
+#pragma unroll
+                    for (int ks = 0; ks < C::TK / 16; ++ks) {
+                        uint64_t ad = smem_desc(sA + a * C::A_BLK + ks * 2048, C::TK * 128, 1024, kSwizzle128B);
+                        uint64_t bd = C::B_SW128 ? smem_desc(sB + ks * 2048, C::TK * 128, 1024, kSwizzle128B)
+                                                 : smem_desc(sB + ks * 1024, 64, 512, kSwizzle64B);
+                        mma_bf16(tmem + a * COUT, ad, bd, C::IDESC, (step | ks) != 0);
+                    }
+                }
+                mma_commit(smem_u32(&bar_empty[s]));
+            }
+            __syncwarp();
+        }
+        if (lane == 0) mma_commit(smem_u32(&bar_tfull));
+        __syncwarp();
+    } else {
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        if (n_steps > 0) {
+            mbar_wait(smem_u32(&bar_tfull), 0);
+            tc_fence_after();
+        }
+        for (int a = 0; a < n_acc; ++a) {
+            const int d = d0 + a * C::OPB + m / CIN, ci = m % CIN;
+            for (int c0 = 0; c0 < COUT; c0 += 32) {
+                uint32_t v[32];
+                if (n_steps > 0) {
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + a * COUT + c0, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0u;
+                }
+                if (d < 27 && a * C::OPB + m / CIN < n_off) {
+                    uint4* dst = reinterpret_cast<uint4*>(part + (((int64_t)split * 27 + d) * CIN + ci) * COUT + c0);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+}
+
+// gw[co][ci][d] = Σ_s part[s][d][ci][co]   (fixed split order: deterministic)
+__global__ void k_wgrad_tc_reduce(const float* __restrict__ part, int splits, int cin, int cout, float* __restrict__ gw) {
+    const int64_t total = (int64_t)27 * cout * cin;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t co = t / ((int64_t)cin * 27);
+        int64_t rem = t - co * cin * 27;
+        int64_t ci = rem / 27, d = rem - ci * 27;
+        float v = 0.f;
+        for (int s = 0; s < splits; ++s) v += part[(((int64_t)s * 27 + d) * cin + ci) * cout + co];
+        gw[t] = v;
+    }
+}
+
+int sm_count() {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+}
+
+template <int K, int N, bool OB>
+int launch_fwd(const void* in, const void* wimg, const int32_t* nbr, int64_t n_out, void* out, cudaStream_t st) {
+    using C = FwdCfg<K, N>;
+    auto kern = k_conv_fwd_tc<K, N, OB>;
+    FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    int occ = 1;
+    FVDB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreadsTC, C::SMEM));
+    if (occ < 1) occ = 1;
+    const int tiles = (int)ceil_div(n_out, kTile);
+    int grid = sm_count() * occ;
+    if (grid > tiles) grid = tiles;
+    kern<<<grid, kThreadsTC, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, nbr, n_out, out, tiles);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+template <int K, int N>
+int dispatch_out(const void* in, const void* wimg, const int32_t* nbr, int64_t n_out, void* out, int out_dtype,
+                 cudaStream_t st) {
+    if (out_dtype == FVDB_DTYPE_BF16) return launch_fwd<K, N, true>(in, wimg, nbr, n_out, out, st);
+    if (out_dtype == FVDB_DTYPE_F32) return launch_fwd<K, N, false>(in, wimg, nbr, n_out, out, st);
+    return FVDB_ERR_INVALID;
+}
+
+template <int K>
+int dispatch_n(int N, const void* in, const void* wimg, const int32_t* nbr, int64_t n_out, void* out, int od,
+               cudaStream_t st) {
+    switch (N) {
+        case 32: return dispatch_out<K, 32>(in, wimg, nbr, n_out, out, od, st);
+        case 64: return dispatch_out<K, 64>(in, wimg, nbr, n_out, out, od, st);
+        case 128: return dispatch_out<K, 128>(in, wimg, nbr, n_out, out, od, st);
+        default: return FVDB_ERR_INVALID;
+    }
+}
+
+template <int CIN, int COUT>
+struct WgLaunch {
+    using C = WgCfg<CIN, COUT>;
+    static int splits_for(int64_t n_out) {
+        int s = sm_count() / C::GROUPS;
+        if (s < 1) s = 1;
+        int64_t max_s = ceil_div(n_out > 0 ? n_out : 1, (int64_t)C::TK * 4);
+        if (s > max_s) s = (int)max_s;
+        return s;
+    }
+    static int run(const void* in, const void* go, const int32_t* nbr, int64_t n_out, float* gw, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+        const int splits = splits_for(n_out);
+        const size_t need = (size_t)splits * 27 * CIN * COUT * sizeof(float);
+        if (ws_bytes < need) return FVDB_ERR_WORKSPACE;
+        float* part = (float*)ws;
+        int64_t rps = ceil_div(n_out > 0 ? n_out : 1, splits);
+        rps = ceil_div(rps, C::TK) * C::TK;
+        auto kern = k_wgrad_tc<CIN, COUT>;
+        FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        kern<<<splits * C::GROUPS, kThreadsTC, C::SMEM, st>>>((const bf16*)in, (const bf16*)go, nbr, n_out, rps, part);
+        k_wgrad_tc_reduce<<<(unsigned)ceil_div((int64_t)27 * CIN * COUT, 256), 256, 0, st>>>(part, splits, CIN, COUT, gw);
+        FVDB_LAUNCH_CHECK();
+        return FVDB_OK;
+    }
+    static size_t ws(int64_t n_out) { return (size_t)splits_for(n_out) * 27 * CIN * COUT * sizeof(float) + 256; }
+};
+
+template <typename F>
+int wg_dispatch(int cin, int cout, F&& f) {
+#define FVDB_WG_CASE(a, b) \
+    if (cin == a && cout == b) return f(WgLaunch<a, b>{});
+    FVDB_WG_CASE(32, 32) FVDB_WG_CASE(32, 64) FVDB_WG_CASE(32, 128)
+    FVDB_WG_CASE(64, 32) FVDB_WG_CASE(64, 64) FVDB_WG_CASE(64, 128)
+    FVDB_WG_CASE(128, 32) FVDB_WG_CASE(128, 64) FVDB_WG_CASE(128, 128)
+#undef FVDB_WG_CASE
+    return FVDB_ERR_INVALID;
+}
+
+}  // namespace
+}  // namespace fvdb
+
+using namespace fvdb;
+
+extern "C" int fvdb_pack_weights_umma(const float* w, int cout, int cin, int transpose, void* image, void* stream) {
+    const int K = transpose ? cout : cin, N = transpose ? cin : cout;
+    if ((K != 32 && K != 64 && K != 128) || (N != 32 && N != 64 && N != 128)) return FVDB_ERR_INVALID;
+    int64_t total = (int64_t)27 * cout * cin;
+    k_pack_umma<<<(unsigned)ceil_div(total, 256), 256, 0, as_stream(stream)>>>(w, cout, cin, transpose, (uint8_t*)image);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_conv_gather_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
+                                   const int32_t* nbr, int64_t n_out, void* out, int out_dtype, void* stream) {
+    (void)n_in;
+    if (n_out == 0) return FVDB_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (K) {
+        case 32: return dispatch_n<32>(N, in_bf16, w_image, nbr, n_out, out, out_dtype, st);
+        case 64: return dispatch_n<64>(N, in_bf16, w_image, nbr, n_out, out, out_dtype, st);
+        case 128: return dispatch_n<128>(N, in_bf16, w_image, nbr, n_out, out, out_dtype, st);
+        default: return FVDB_ERR_INVALID;
+    }
+}
+
+extern "C" size_t fvdb_wgrad_tc_workspace_bytes(int64_t n_out, int cin, int cout) {
+    size_t r = 0;
+    int rc = wg_dispatch(cin, cout, [&](auto L) {
+        r = decltype(L)::ws(n_out);
+        return 0;
+    });
+    return rc == 0 ? r : 0;
+}
+
+extern "C" int fvdb_conv_wgrad_tc(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,
+                                  const int32_t* nbr, int64_t n_out, float* gw, void* ws, size_t ws_bytes,
+                                  void* stream) {
+    (void)n_in;
+    cudaStream_t st = as_stream(stream);
+    return wg_dispatch(cin, cout, [&](auto L) {
+        return decltype(L)::run(in_bf16, go_bf16, nbr, n_out, gw, ws, ws_bytes, st);
+    });
+}

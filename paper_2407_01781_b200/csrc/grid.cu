@@ -1,0 +1,283 @@
+// grid.cu — index-grid probes and kernel-map generation.
+//
+// Reference: coord_to_index_many (topology.py:253-286) does two binary searches
+// (tile_keys, leaf_keys) + a mask-bit test + popcount rank per query;
+// build_kernel_map (conv.py:105-122) issues 27 such probes per output voxel and
+// compacts per offset.
+//
+// B200 mapping for the kernel map: every output voxel of one 8³ leaf probes
+// input coordinates that fall inside the 3×3×3 block of input leaves around that
+// leaf (for stride 1 around the leaf itself, for stride 2 around the leaf at
+// 2·origin — both are {base + 8e : e ∈ {-1,0,1}³}).  So the expensive tree walk
+// is done once per (output leaf, neighbour leaf) — 27·L binary searches instead
+// of 27·N — and the per-voxel probes become shared-memory bit tests + popcounts
+// against the 27 staged leaf masks.  One CTA per output leaf; the output is the
+// dense offset-major neighbour table nbr[27][N_out] (coalesced writes), from which
+// the reference's per-offset (in_rows, out_rows) lists are a single stable
+// compaction (out_rows ascending by construction).
+#include <cub/cub.cuh>
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace fvdb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* where, cudaError_t e) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+}
+void set_error_msg(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+
+constexpr int kThreads = 256;
+
+int grid_for(int64_t n) {
+    int64_t b = ceil_div(n > 0 ? n : 1, kThreads);
+    return (int)(b < 148 * 16 ? b : 148 * 16);
+}
+
+__global__ void k_coord_to_index(fvdb_grid_view g, const int64_t* __restrict__ coords, int64_t n,
+                                 int64_t* __restrict__ out) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
+        int64_t idx = 0;
+        int64_t l = find_leaf(g, i, j, k);
+        if (l >= 0) {
+            uint32_t m = leaf_off(i, j, k);
+            const uint64_t* w = g.leaf_masks + 8 * l;
+            if ((w[m >> 6] >> (m & 63)) & 1ull)
+                idx = (int64_t)g.leaf_value_offset[l] + leaf_rank(w, g.leaf_prefix[l], m);
+        }
+        out[r] = idx;
+    }
+}
+
+// one block of 128 threads per leaf; row = value_offset-1+rank (topology.py:288-299)
+__global__ void k_active_coords(fvdb_grid_view g, int64_t* __restrict__ out) {
+    const int64_t l = blockIdx.x;
+    const uint64_t* w = g.leaf_masks + 8 * l;
+    const uint64_t pre = g.leaf_prefix[l];
+    const int64_t base = (int64_t)g.leaf_value_offset[l] - 1;
+    const int64_t ox = g.leaf_origins[3 * l], oy = g.leaf_origins[3 * l + 1], oz = g.leaf_origins[3 * l + 2];
+    for (uint32_t m = threadIdx.x; m < 512; m += blockDim.x) {
+        if ((w[m >> 6] >> (m & 63)) & 1ull) {
+            int64_t row = base + leaf_rank(w, pre, m);
+            out[3 * row + 0] = ox + (m >> 6);
+            out[3 * row + 1] = oy + ((m >> 3) & 7);
+            out[3 * row + 2] = oz + (m & 7);
+        }
+    }
+}
+
+// tree walk once per (output leaf, neighbour leaf): nleaf[l][e], e over {-1,0,1}^3
+__global__ void k_neighbor_leaves(fvdb_grid_view gin, fvdb_grid_view gout, int stride,
+                                  int32_t* __restrict__ nleaf) {
+    const int64_t total = gout.num_leaf * 27;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t l = t / 27;
+        int e = (int)(t - l * 27);
+        int64_t bx = stride * gout.leaf_origins[3 * l] + 8 * (e / 9 - 1);
+        int64_t by = stride * gout.leaf_origins[3 * l + 1] + 8 * ((e / 3) % 3 - 1);
+        int64_t bz = stride * gout.leaf_origins[3 * l + 2] + 8 * (e % 3 - 1);
+        nleaf[t] = (int32_t)find_leaf(gin, bx, by, bz);
+    }
+}
+
+// CTA per output leaf: 27 probes per active voxel against staged neighbour-leaf masks
+__global__ void __launch_bounds__(kThreads) k_kernel_map(fvdb_grid_view gin, fvdb_grid_view gout, int stride,
+                                                         const int32_t* __restrict__ nleaf,
+                                                         int32_t* __restrict__ nbr, int64_t n_out,
+                                                         unsigned long long* __restrict__ pair_counts) {
+    __shared__ uint64_t s_mask[27][8];
+    __shared__ uint64_t s_pre[27];
+    __shared__ int64_t s_vo[27];
+    __shared__ int32_t s_nl[27];
+    __shared__ uint16_t s_pos[512];
+    __shared__ int s_cnt[27];
+    __shared__ uint64_t s_own[8];
+
+    const int64_t l = blockIdx.x;
+    const int tid = threadIdx.x;
+    if (tid < 27) {
+        int32_t nl = nleaf[l * 27 + tid];
+        s_nl[tid] = nl;
+        s_cnt[tid] = 0;
+        s_pre[tid] = nl >= 0 ? gin.leaf_prefix[nl] : 0;
+        s_vo[tid] = nl >= 0 ? (int64_t)gin.leaf_value_offset[nl] - 1 : 0;
+    }
+    if (tid < 8) s_own[tid] = gout.leaf_masks[8 * l + tid];
+    for (int q = tid; q < 27 * 8; q += kThreads) {
+        int e = q >> 3;
+        int32_t nl = nleaf[l * 27 + e];
+        s_mask[e][q & 7] = nl >= 0 ? gin.leaf_masks[8 * (int64_t)nl + (q & 7)] : 0ull;
+    }
+    __syncthreads();
+    const uint64_t own_pre = gout.leaf_prefix[l];
+    for (uint32_t m = tid; m < 512; m += kThreads)
+        if ((s_own[m >> 6] >> (m & 63)) & 1ull) s_pos[leaf_rank(s_own, own_pre, m)] = (uint16_t)m;
+    int nvox = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) nvox += __popcll(s_own[w]);
+    __syncthreads();
+
+    const int64_t row0 = (int64_t)gout.leaf_value_offset[l] - 1;
+    const int items = 27 * nvox;
+    for (int f = tid; f < items; f += kThreads) {
+        int d = f / nvox;
+        int r = f - d * nvox;
+        uint32_t m = s_pos[r];
+        int qx = stride * (int)(m >> 6) + (d / 9 - 1);
+        int qy = stride * (int)((m >> 3) & 7) + ((d / 3) % 3 - 1);
+        int qz = stride * (int)(m & 7) + (d % 3 - 1);
+        int e = ((qx >> 3) + 1) * 9 + ((qy >> 3) + 1) * 3 + ((qz >> 3) + 1);
+        int32_t row = -1;
+        if (s_nl[e] >= 0) {
+            uint32_t b = (uint32_t)(((qx & 7) << 6) | ((qy & 7) << 3) | (qz & 7));
+            if ((s_mask[e][b >> 6] >> (b & 63)) & 1ull) {
+                row = (int32_t)(s_vo[e] + leaf_rank(s_mask[e], s_pre[e], b));
+                atomicAdd(&s_cnt[d], 1);
+            }
+        }
+        nbr[(int64_t)d * n_out + row0 + r] = row;
+    }
+    __syncthreads();
+    if (tid < 27 && s_cnt[tid]) atomicAdd(&pair_counts[tid], (unsigned long long)s_cnt[tid]);
+}
+
+__global__ void k_flags(const int32_t* __restrict__ nbr, int64_t n, int* __restrict__ flags) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x)
+        flags[t] = nbr[t] >= 0;
+}
+
+__global__ void k_compact(const int32_t* __restrict__ nbr, int64_t n_out, const int* __restrict__ pos,
+                          int64_t* __restrict__ in_rows, int64_t* __restrict__ out_rows) {
+    const int64_t total = 27 * n_out;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = nbr[t];
+        if (v >= 0) {
+            int p = pos[t];
+            in_rows[p] = v;
+            out_rows[p] = t % n_out;
+        }
+    }
+}
+
+__global__ void k_transpose(const int32_t* __restrict__ nbr, int64_t n_out, int64_t n_in,
+                            int32_t* __restrict__ nbrT) {
+    const int64_t total = 27 * n_out;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = nbr[t];
+        if (v >= 0) {
+            int64_t d = t / n_out;
+            nbrT[d * n_in + v] = (int32_t)(t - d * n_out);
+        }
+    }
+}
+
+__global__ void k_f32_to_bf16(const float* __restrict__ s, int64_t n, __nv_bfloat16* __restrict__ d) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x)
+        d[t] = __float2bfloat16_rn(s[t]);
+}
+
+}  // namespace
+}  // namespace fvdb
+
+using namespace fvdb;
+
+extern "C" const char* fvdb_version(void) { return "fvdb_b200 0.1.0 (sm_100a)"; }
+extern "C" const char* fvdb_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int fvdb_device_sm_count(int device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+    return v;
+}
+
+extern "C" int fvdb_coord_to_index(const fvdb_grid_view* g, const int64_t* coords, int64_t n, int64_t* out,
+                                   void* stream) {
+    if (n == 0) return FVDB_OK;
+    k_coord_to_index<<<grid_for(n), kThreads, 0, as_stream(stream)>>>(*g, coords, n, out);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_active_coords(const fvdb_grid_view* g, int64_t* out, void* stream) {
+    if (g->num_leaf == 0) return FVDB_OK;
+    k_active_coords<<<(unsigned)g->num_leaf, 128, 0, as_stream(stream)>>>(*g, out);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" size_t fvdb_kmap_workspace_bytes(int64_t num_leaf_out) {
+    return (size_t)(num_leaf_out > 0 ? num_leaf_out : 1) * 27 * sizeof(int32_t) + 256;
+}
+
+extern "C" int fvdb_kernel_map(const fvdb_grid_view* gin, const fvdb_grid_view* gout, int stride, int32_t* nbr,
+                               int64_t* pair_counts, void* ws, size_t ws_bytes, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (stride != 1 && stride != 2) return FVDB_ERR_INVALID;
+    if (ws_bytes < fvdb_kmap_workspace_bytes(gout->num_leaf)) return FVDB_ERR_WORKSPACE;
+    FVDB_CUDA_TRY(cudaMemsetAsync(pair_counts, 0, 27 * sizeof(int64_t), st));
+    if (gout->num_leaf == 0) return FVDB_OK;
+    int32_t* nleaf = reinterpret_cast<int32_t*>(ws);
+    k_neighbor_leaves<<<grid_for(gout->num_leaf * 27), kThreads, 0, st>>>(*gin, *gout, stride, nleaf);
+    k_kernel_map<<<(unsigned)gout->num_leaf, kThreads, 0, st>>>(
+        *gin, *gout, stride, nleaf, nbr, gout->num_voxels, reinterpret_cast<unsigned long long*>(pair_counts));
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" size_t fvdb_kmap_compact_workspace_bytes(int64_t n_out) {
+    int64_t n = 27 * (n_out > 0 ? n_out : 1);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (int*)nullptr, (int*)nullptr, (int)n);
+    return 2 * (size_t)n * sizeof(int) + tb + 1024;
+}
+
+extern "C" int fvdb_kmap_compact(const int32_t* nbr, int64_t n_out, int64_t* in_rows, int64_t* out_rows,
+                                 void* ws, size_t ws_bytes, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n_out == 0) return FVDB_OK;
+    const int64_t n = 27 * n_out;
+    if (n >= (int64_t)INT32_MAX) return FVDB_ERR_INVALID;
+    if (ws_bytes < fvdb_kmap_compact_workspace_bytes(n_out)) return FVDB_ERR_WORKSPACE;
+    Carver c(ws, ws_bytes);
+    int* flags = c.take<int>(n);
+    int* pos = c.take<int>(n);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (int*)nullptr, (int*)nullptr, (int)n);
+    void* tmp = c.take<char>(tb);
+    if (!c.ok()) return FVDB_ERR_WORKSPACE;
+    k_flags<<<grid_for(n), kThreads, 0, st>>>(nbr, n, flags);
+    FVDB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flags, pos, (int)n, st));
+    k_compact<<<grid_for(n), kThreads, 0, st>>>(nbr, n_out, pos, in_rows, out_rows);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_kmap_transpose(const int32_t* nbr, int64_t n_out, int64_t n_in, int32_t* nbrT,
+                                   void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n_in > 0) FVDB_CUDA_TRY(cudaMemsetAsync(nbrT, 0xFF, (size_t)27 * n_in * sizeof(int32_t), st));
+    if (n_out == 0 || n_in == 0) return FVDB_OK;
+    k_transpose<<<grid_for(27 * n_out), kThreads, 0, st>>>(nbr, n_out, n_in, nbrT);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream) {
+    if (n == 0) return FVDB_OK;
+    k_f32_to_bf16<<<grid_for(n), kThreads, 0, as_stream(stream)>>>(src, n, (__nv_bfloat16*)dst);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}

@@ -1,0 +1,118 @@
+"""``SparseConv3d`` — autograd module over the device kernels (new).
+
+Forward is ``(GridBatch, JaggedTensor) -> (GridBatch, JaggedTensor)`` as in the
+paper's operator description.  Modes:
+  * stride 1            : output grid = input grid;
+  * stride 2            : output grid = coarsen(grid, 2) per element (conv.py:155-156);
+  * transposed (stride 2 adjoint): pass ``out_grid`` = the fine GridBatch;
+    weight is ``[in_channels(coarse), out_channels(fine), 3, 3, 3]``.
+Backward: dgrad through the transposed neighbour table and tensor-core wgrad;
+``compute_dtype=torch.bfloat16`` (default) runs the tcgen05 kernels, float32 the
+exact CUDA-core kernels.  For data parallelism all-reduce ``weight.grad``
+(``paper_2407_01781_b200.dist.allreduce_gradients``).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+from torch import nn
+
+from .build import coarsen
+from .conv import batch_grid_kernel_map, gather_conv, pack_weights_umma, wgrad
+from .jagged import GridBatch, JaggedTensor
+
+
+class _SparseConvFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, kmap, transposed, cdt):
+        xc = x.to(cdt).contiguous()
+        if transposed:
+            y = gather_conv(xc, kmap.transposed_table(), w, transpose=True, out_dtype=cdt)
+        else:
+            img = pack_weights_umma(w, False) if cdt == torch.bfloat16 and _tc_ok(w) else None
+            y = gather_conv(xc, kmap.nbr, w, transpose=False, out_dtype=cdt, w_image=img)
+        ctx.save_for_backward(xc, w)
+        ctx.kmap, ctx.transposed, ctx.cdt, ctx.x_dtype = kmap, transposed, cdt, x.dtype
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        xc, w = ctx.saved_tensors
+        km, cdt = ctx.kmap, ctx.cdt
+        gy = gy.to(cdt).contiguous()
+        gx = gw = None
+        if ctx.transposed:
+            if ctx.needs_input_grad[0]:
+                gx = gather_conv(gy, km.nbr, w, transpose=False, out_dtype=cdt)
+            if ctx.needs_input_grad[1]:
+                gw = wgrad(gy, xc, km.nbr)
+        else:
+            if ctx.needs_input_grad[0]:
+                gx = gather_conv(gy, km.transposed_table(), w, transpose=True, out_dtype=cdt)
+            if ctx.needs_input_grad[1]:
+                gw = wgrad(xc, gy, km.nbr)
+        if gx is not None:
+            gx = gx.to(ctx.x_dtype)
+        if gw is not None:
+            gw = gw.to(w.dtype)
+        return gx, gw, None, None, None
+
+
+def _tc_ok(w):
+    return int(w.shape[0]) in (32, 64, 128) and int(w.shape[1]) in (32, 64, 128)
+
+
+def coarsen_batch(batch: GridBatch, factor: int = 2) -> GridBatch:
+    key = ("coarse", factor)
+    cached = batch._kmaps.get(key)
+    if cached is None:
+        cached = GridBatch([coarsen(g, factor) for g in batch.grids])
+        batch._kmaps[key] = cached
+    return cached
+
+
+class SparseConv3d(nn.Module):
+    def __init__(self, in_channels, out_channels, kernel_size=3, stride=1, transposed=False, bias=False,
+                 compute_dtype=torch.bfloat16, device=None):
+        super().__init__()
+        if kernel_size != 3:
+            raise NotImplementedError("only 3x3x3 kernels are supported (reference conv.py:36-38, 50-56)")
+        if stride not in (1, 2):
+            raise ValueError(f"stride must be 1 or 2, got {stride}")
+        if transposed and stride != 2:
+            raise ValueError("transposed SparseConv3d is the stride-2 adjoint; use stride=2")
+        self.in_channels, self.out_channels = in_channels, out_channels
+        self.stride, self.transposed, self.compute_dtype = stride, transposed, compute_dtype
+        shape = (in_channels, out_channels, 3, 3, 3) if transposed else (out_channels, in_channels, 3, 3, 3)
+        self.weight = nn.Parameter(torch.empty(shape, device=device))
+        self.bias = nn.Parameter(torch.zeros(out_channels, device=device)) if bias else None
+        self.reset_parameters()
+
+    def reset_parameters(self):
+        with torch.no_grad():
+            self.weight.normal_(0.0, 1.0 / math.sqrt(27 * self.in_channels))
+
+    def forward(self, grid: GridBatch, x, out_grid: GridBatch | None = None):
+        if not isinstance(grid, GridBatch):
+            grid = GridBatch([grid])
+        feats = grid.check_features(x)
+        if self.transposed:
+            if out_grid is None:
+                raise ValueError("transposed SparseConv3d needs out_grid (the fine GridBatch)")
+            kmap = batch_grid_kernel_map(out_grid, grid, 2)   # fine -> coarse stride-2 map
+        elif self.stride == 2:
+            out_grid = out_grid or coarsen_batch(grid, 2)
+            kmap = batch_grid_kernel_map(grid, out_grid, 2)
+        else:
+            out_grid = out_grid or grid
+            kmap = batch_grid_kernel_map(grid, out_grid, 1)
+        y = _SparseConvFn.apply(feats, self.weight, kmap, self.transposed, self.compute_dtype)
+        if self.bias is not None:
+            y = y + self.bias.to(y.dtype)
+        return out_grid, out_grid.jagged(y)
+
+    def extra_repr(self):
+        return (f"{self.in_channels}, {self.out_channels}, kernel_size=3, stride={self.stride}, "
+                f"transposed={self.transposed}, compute_dtype={self.compute_dtype}")
