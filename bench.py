@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""SparseConv3d fwd+bwd throughput on B200 (BASELINE.json metric), plus the reference arm.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2|cfg3|cfg5]
+
+Workload (N=1): BASELINE.json configs[1] — the ScanNet-scale sphere shell
+``sphere_shell_coords(470, band=1.5)`` (1,018,216 voxels, 21,229,376 kernel-map pairs),
+SparseConv3d 3×3×3 64→64, bf16 inputs / fp32 accumulation, forward + input-gradient +
+weight-gradient.  A "step" is one fwd+bwd pass over that grid with inputs resident in HBM;
+the kernel map is built once outside the timed region (as the reference's bench-conv,
+cli.py:353) and its build time is reported separately.  Multi-GPU (torchrun): weak scaling
+— every rank runs its own grid (batch-sharded data parallelism) and the step includes the
+NCCL all-reduce of the fp32 weight gradient.
+
+Timing: W warm-up steps; K timed steps, each preceded by a 256 MB L2-flush write (untimed),
+timed with CUDA events on the launching stream; ms_per_step = mean, max over ranks.
+``e2e`` repeats the step through the public module API with pinned host buffers (H2D of
+features / grad_out / weights, D2H of output / grad_in / grad_w inside the timed region).
+``cpu_baseline`` times the oracle port (numpy restatement of the reference igemm conv,
+BLAS on all host cores) on a leaf-aligned sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SparseConv3d fwd+bwd active voxels/s & TFLOPS at 1/2/4/8 B200 vs CPU ref"
+UNIT = "voxels/s"
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+TRAFFIC_FILE = ROOT / "profiles" / "ncu_traffic.json"
+
+CONFIGS = {
+    "cfg2": dict(desc="ScanNet-scale sphere shell sphere_shell_coords(470, band=1.5), SparseConv3d 3x3x3 64->64 "
+                      "bf16 fwd+bwd", res=470, cin=64, cout=64),
+    "cfg3": dict(desc="KITTI-scale simulated LiDAR grid (128 beams x 2048 az, voxel 0.05 m, seed=rank), "
+                      "SparseConv3d 3x3x3 128->128 bf16 fwd+bwd", lidar=True, cin=128, cout=128),
+    "cfg5": dict(desc="2048^3 surface shell sphere_shell_coords(2048, band=1.5), SparseConv3d 3x3x3 32->32 bf16 "
+                      "fwd+bwd", res=2048, cin=32, cout=32),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        return json.loads(PEAKS_FILE.read_text())
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "_fallback": True}
+
+
+# ----------------------------------------------------------------------------- inputs
+
+def make_coords(cfg, rank):
+    from paper_2407_01781_b200.workloads import lidar_scan_points, sphere_shell_coords
+    if cfg.get("lidar"):
+        return None, lidar_scan_points(rank)
+    return sphere_shell_coords(cfg["res"], band=1.5), None
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """NVML sampling of SM clock + clocks-event reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index, interval=0.005):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self.interval = interval
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.interval)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        reasons = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_01781_b200 as P
+    from paper_2407_01781_b200.conv import gather_conv, pack_weights_umma, wgrad
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = CONFIGS[args.config]
+    cin, cout = cfg["cin"], cfg["cout"]
+
+    coords, points = make_coords(cfg, rank)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if points is not None:
+        grid, _ = P.build_from_points(points, P.VoxelTransform.uniform(0.05))
+    else:
+        grid, _ = P.build_from_coords(coords)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    # kernel map (prebuilt; timed separately with events, best of 3)
+    km = None
+    kms = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        km = P.build_kernel_map(grid, grid, 1)
+        e1.record()
+        torch.cuda.synchronize()
+        kms.append(e0.elapsed_time(e1))
+    n = grid.num_voxels
+    pairs = km.total_pairs
+    nbr = km.nbr
+    nbrT = km.transposed_table()
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    x = torch.randn(n, cin, device=dev, generator=gen).to(torch.bfloat16)
+    gy = torch.randn(n, cout, device=dev, generator=gen).to(torch.bfloat16)
+    w = torch.randn(cout, cin, 3, 3, 3, device=dev, generator=gen) / (27 * cin) ** 0.5
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    use_dist = world > 1
+
+    def step(ev=None):
+        img_f = pack_weights_umma(w, False)
+        img_b = pack_weights_umma(w, True)
+        if ev is not None:
+            ev[0].record()
+        y = gather_conv(x, nbr, w, transpose=False, out_dtype=torch.bfloat16, w_image=img_f)
+        if ev is not None:
+            ev[1].record()
+        gx = gather_conv(gy, nbrT, w, transpose=True, out_dtype=torch.bfloat16, w_image=img_b)
+        if ev is not None:
+            ev[2].record()
+        gw = wgrad(x, gy, nbr)
+        if ev is not None:
+            ev[3].record()
+        if use_dist:
+            dist.all_reduce(gw)
+        if ev is not None:
+            ev[4].record()
+        return y, gx, gw
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if use_dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)          # untimed L2 flush (256 MB > 126 MB L2)
+            starts[k].record()
+            step(evs[k])
+        torch.cuda.synchronize()
+    if use_dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [s.elapsed_time(e[4]) for s, e in zip(starts, evs)]
+    phase = {"fwd": [e[0].elapsed_time(e[1]) for e in evs], "dgrad": [e[1].elapsed_time(e[2]) for e in evs],
+             "wgrad": [e[2].elapsed_time(e[3]) for e in evs], "allreduce": [e[3].elapsed_time(e[4]) for e in evs],
+             "pack": [s.elapsed_time(e[0]) for s, e in zip(starts, evs)]}
+    ms = statistics.mean(step_ms)
+    if use_dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_vox = n * world
+    if use_dist:
+        t = torch.tensor([n], device=dev, dtype=torch.int64)
+        dist.all_reduce(t)
+        total_vox = int(t.item())
+    value = total_vox / (ms / 1e3)
+
+    # ---- end-to-end through the public module API with host buffers ----
+    e2e = run_e2e(args, P, torch, dist, grid, km, cin, cout, dev, use_dist)
+
+    # ---- roofline of the dominant kernel ----
+    pk = peaks()
+    flops_kernel = 2.0 * pairs * cin * cout
+    means = {k: statistics.mean(v) for k, v in phase.items()}
+    dom = max(("fwd", "dgrad", "wgrad"), key=lambda k: means[k])
+    achieved = flops_kernel / (means[dom] / 1e3) / 1e12
+    traffic = None
+    try:
+        tr = json.loads(TRAFFIC_FILE.read_text())
+        traffic = tr.get(args.config, {}).get(dom)
+    except Exception:
+        pass
+    roof = {"bound": "tensor", "kernel": {"fwd": "k_conv_fwd_tc<64,64,bf16>", "dgrad": "k_conv_fwd_tc (dgrad form)",
+                                          "wgrad": "k_wgrad_tc"}[dom],
+            "achieved": round(achieved, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": round(achieved / pk["bf16_tflops"], 4), "traffic": traffic,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if not pk.get("_fallback") else "fallback",
+            "algorithmic_flop_per_launch": flops_kernel}
+    step_tflops = 3 * flops_kernel / (ms / 1e3) / 1e12
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, coords, points, args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "voxels_per_gpu": n, "pairs_per_gpu": pairs,
+                       "cin": cin, "cout": cout, "parallelism": f"dp{world} (batch-sharded, NCCL wgrad all-reduce)"
+                       if world > 1 else "single GPU",
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "kernel_map": "prebuilt outside the timed step (reference cli.py:353)"},
+            "tflops_effective": round(step_tflops, 2),
+            "frac_of_bf16_peak": round(step_tflops / pk["bf16_tflops"], 4),
+            "phases_ms": {k: round(v, 4) for k, v in means.items()},
+            "build_ms": {"grid": round(t_build * 1e3, 3), "kernel_map": round(min(kms), 4)},
+            "roofline": roof,
+            "e2e": e2e,
+            "gpu_launches": 6 * args.steps,
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if use_dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, P, torch, dist, grid, km, cin, cout, dev, use_dist):
+    """Same step through SparseConv3d (autograd) with pinned host inputs/outputs."""
+    n = grid.num_voxels
+    gb = P.GridBatch([grid])
+    gb._kmaps[(id(gb), 1)] = km
+    m = P.SparseConv3d(cin, cout).to(dev)
+    rng = np.random.default_rng(7)
+    x_h = torch.from_numpy(rng.normal(size=(n, cin)).astype(np.float32)).pin_memory()
+    gy_h = torch.from_numpy(rng.normal(size=(n, cout)).astype(np.float32)).pin_memory()
+    w_h = m.weight.detach().cpu().pin_memory()
+    y_h = torch.empty((n, cout), dtype=torch.bfloat16).pin_memory()
+    gx_h = torch.empty((n, cin), dtype=torch.float32).pin_memory()
+    gw_h = torch.empty_like(w_h).pin_memory()
+    steps = args.e2e_steps or max(3, min(args.steps, 20))
+
+    def one():
+        with torch.no_grad():
+            m.weight.copy_(w_h.to(dev, non_blocking=True))
+        m.weight.grad = None
+        x = x_h.to(dev, non_blocking=True).requires_grad_(True)
+        gy = gy_h.to(dev, non_blocking=True)
+        _, y = m(gb, gb.jagged(x))
+        y.jdata.backward(gy.to(y.jdata.dtype))
+        if use_dist:
+            dist.all_reduce(m.weight.grad)
+        y_h.copy_(y.jdata.detach(), non_blocking=True)
+        gx_h.copy_(x.grad, non_blocking=True)
+        gw_h.copy_(m.weight.grad, non_blocking=True)
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if use_dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    world = dist.get_world_size() if use_dist else 1
+    h2d = x_h.numel() * 4 + gy_h.numel() * 4 + w_h.numel() * 4
+    d2h = y_h.numel() * 2 + gx_h.numel() * 4 + gw_h.numel() * 4
+    return {"value": round(n * world / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 4),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "api": "paper_2407_01781_b200.SparseConv3d (autograd) fwd+bwd, fp32 host in, bf16 compute"}
+
+
+# ----------------------------------------------------------------------------- CPU (oracle port)
+
+def _oracle_problem(cfg, coords, points, seed=0):
+    import oracle as O
+    if points is not None:
+        g = O.build_from_points(points, [0.05] * 3, [0.0] * 3)
+    else:
+        g = O.build_from_coords(coords)
+    ins, outs = O.kernel_map(g, g, 1)
+    return O, g, ins, outs
+
+
+def _sample_lists(ins, outs, n, frac):
+    lim = max(1, int(n * frac))
+    si, so = [], []
+    for a, b in zip(ins, outs):
+        k = np.searchsorted(b, lim)  # out rows ascending (conv.py:87)
+        si.append(a[:k])
+        so.append(b[:k])
+    return si, so, lim
+
+
+def cpu_baseline(cfg, coords, points, args, frac=1 / 64, repeats=3):
+    """Oracle port (numpy igemm + BLAS) on a prefix of output rows of the same workload."""
+    O, g, ins, outs = _oracle_problem(cfg, coords, points)
+    n = g.num_voxels
+    cin, cout = cfg["cin"], cfg["cout"]
+    si, so, lim = _sample_lists(ins, outs, n, frac)
+    rng = np.random.default_rng(0)
+    f = rng.normal(size=(n, cin)).astype(np.float32)
+    w = (rng.normal(size=(cout, cin, 3, 3, 3)) / np.sqrt(27 * cin)).astype(np.float32)
+    go = rng.normal(size=(lim, cout)).astype(np.float32)
+    best = float("inf")
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        O.conv_igemm(f, w, si, so, lim)
+        O.conv_backward(si, so, go, f, w)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": round(lim / best, 1), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"first {lim} of {n} output voxels ({frac:.4f} of the grid, leaf-aligned index prefix), "
+                      f"{sum(len(o) for o in so)} pairs, fp32 igemm fwd + conv_backward, best of {repeats}",
+            "seconds_per_sample": round(best, 4)}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port of the reference CPU path on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    coords, points = make_coords(cfg, 0)
+    O, g, ins, outs = _oracle_problem(cfg, coords, points)
+    n = g.num_voxels
+    cin, cout = cfg["cin"], cfg["cout"]
+    frac = 1 / 256 if args.steps + args.warmup > 60 else 1 / 64
+    si, so, lim = _sample_lists(ins, outs, n, frac)
+    rng = np.random.default_rng(0)
+    f = rng.normal(size=(n, cin)).astype(np.float32)
+    w = (rng.normal(size=(cout, cin, 3, 3, 3)) / np.sqrt(27 * cin)).astype(np.float32)
+    go = rng.normal(size=(lim, cout)).astype(np.float32)
+
+    def step():
+        O.conv_igemm(f, w, si, so, lim)
+        O.conv_backward(si, so, go, f, w)
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    ms = statistics.mean(times) * 1e3
+    value = lim / (ms / 1e3)
+    sample = (f"first {lim} of {n} output voxels ({frac:.4f}), {sum(len(o) for o in so)} pairs; fp32 igemm fwd + "
+              f"conv_backward (oracle port of reference conv.py:180-191, 339-368)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "voxels": n, "cin": cin, "cout": cout},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    elif args.gpus > 1:
+        print(json.dumps({"error": "--gpus > 1 needs torchrun (one process per GPU)"}), file=sys.stderr)
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()
