@@ -1,0 +1,332 @@
+// tools/microbench.cu — B200 micro-benchmarks that decide the conv kernel design.
+//   (1) TMA tile::gather4 semantics probe (box height, OOB zero fill, tx byte count)
+//   (2) gather bandwidth of the real cfg2 kernel map: TMA gather4 vs cp.async(.ca/.cg)
+//   (3) tcgen05.mma kind::f16 SS issue rate at M=128, N in {64,128,256}
+// Not part of the product library; built by tools/run_microbench.py.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../paper_2407_01781_b200/csrc/tc_ptx.cuh"
+
+using namespace fvdb::tc;
+using bf16 = __nv_bfloat16;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) return nullptr;
+    return (EncodeTiledFn)fn;
+}
+
+static int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_w, uint32_t box_h,
+                    CUtensorMapSwizzle sw) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return -100;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {box_w, box_h};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return (int)r;
+}
+
+__device__ __forceinline__ void gather4(uint32_t dst, const CUtensorMap* map, int c0, int4 r, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "r"(bar)
+        : "memory");
+}
+
+__device__ bool wait_bounded(uint32_t bar, uint32_t ph, long long spins) {
+    for (long long i = 0; i < spins; ++i)
+        if (mbar_try_wait(bar, ph)) return true;
+    return false;
+}
+
+// ---------------------------------------------------------------- (1) probe
+__global__ void k_probe(const __grid_constant__ CUtensorMap map, int4 rows, int expect, bf16* out, int* status) {
+    __shared__ __align__(1024) uint8_t buf[4096];
+    __shared__ __align__(8) uint64_t bar;
+    uint32_t b = smem_u32(&bar);
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) buf[i] = 0xAB;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_init(b, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(b, expect);
+        gather4(smem_u32(buf), &map, 0, rows, b);
+        bool ok = wait_bounded(b, 0, 20000000);
+        status[0] = ok ? 1 : 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * 64; i += blockDim.x) out[i] = reinterpret_cast<bf16*>(buf)[i];
+}
+
+extern "C" int mb_probe(const void* src, int n_rows, int box_h, int swz, int r0, int r1, int r2, int r3, int expect,
+                        void* out, int* status) {
+    CUtensorMap m;
+    int rc = make_map(&m, src, n_rows, 64, 64, box_h,
+                      swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+    k_probe<<<1, 128>>>(m, make_int4(r0, r1, r2, r3), expect, (bf16*)out, status);
+    return (int)cudaDeviceSynchronize();
+}
+
+// ---------------------------------------------------------------- (2) gather bandwidth
+constexpr int kStages = 8;
+// mode 0: TMA gather4 (1 producer warp); 1: cp.async.ca by 4 warps; 2: cp.async.cg by 4 warps
+template <int MODE>
+__global__ void __launch_bounds__(192, 1) k_gather_bw(const __grid_constant__ CUtensorMap map, const bf16* feat,
+                                                      const int32_t* nbr, long long n_out, int num_tiles) {
+    extern __shared__ uint8_t dsm[];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    const uint32_t base = (smem_u32(dsm) + 1023) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(smem_u32(&full[s]), MODE == 0 ? 1 : 128);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (MODE == 0 && warp == 0) {
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x)
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % kStages, ph = (it / kStages) & 1;
+                int4 r = *reinterpret_cast<const int4*>(nbr + (long long)d * n_out + (long long)t * 128 + 4 * lane);
+                if ((long long)t * 128 + 4 * lane + 3 >= n_out) r = make_int4(-1, -1, -1, -1);
+                mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+                if (lane == 0) mbar_arrive_expect_tx(smem_u32(&full[s]), 128 * 128);
+                __syncwarp();
+                gather4(base + s * 16384 + lane * 512, &map, 0, r, smem_u32(&full[s]));
+            }
+    } else if (MODE != 0 && warp < 4) {
+        const int pt = threadIdx.x, c = pt & 7, rb = pt >> 3;
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x)
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % kStages, ph = (it / kStages) & 1;
+                int idx[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    long long row = (long long)t * 128 + rb + 16 * j;
+                    idx[j] = row < n_out ? nbr[(long long)d * n_out + row] : -1;
+                }
+                mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    int r = rb + 16 * j;
+                    uint32_t dst = base + s * 16384 + r * 128 + ((c ^ (r & 7)) << 4);
+                    const bf16* src = feat + (long long)(idx[j] < 0 ? 0 : idx[j]) * 64 + c * 8;
+                    if (MODE == 1) cp_async_16(dst, src, idx[j] < 0 ? 0 : 16);
+                    else cp_async_16_cg(dst, src, idx[j] < 0 ? 0 : 16);
+                }
+                cp_async_arrive_noinc(smem_u32(&full[s]));
+            }
+    } else if (warp == 5 && lane == 0) {
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x)
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % kStages, ph = (it / kStages) & 1;
+                mbar_wait(smem_u32(&full[s]), ph);
+                mbar_arrive(smem_u32(&empty[s]));
+            }
+    }
+}
+
+extern "C" int mb_gather_bw(int mode, const void* feat, long long n_in, const int32_t* nbr, long long n_out,
+                            int ctas_per_sm, float* ms) {
+    CUtensorMap m;
+    int rc = make_map(&m, feat, n_in, 64, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    int tiles = (int)(n_out / 128);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    size_t smem = kStages * 16384 + 1024;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    void (*k)(CUtensorMap, const bf16*, const int32_t*, long long, int) =
+        mode == 0 ? k_gather_bw<0> : (mode == 1 ? k_gather_bw<1> : k_gather_bw<2>);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(a);
+        k<<<sms * ctas_per_sm, 192, smem>>>(m, (const bf16*)feat, nbr, n_out, tiles);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+    }
+    cudaEventElapsedTime(ms, a, b);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- (2b) gather with index blocks prefetched
+// index block of a tile (27 x 128 int32) arrives by 27 bulk copies into a 2-deep smem ring
+template <int MODE, int STAGES>
+__global__ void __launch_bounds__(192, 1) k_gather_bw2(const __grid_constant__ CUtensorMap map, const bf16* feat,
+                                                       const int32_t* nbr, long long n_out, int num_tiles) {
+    extern __shared__ uint8_t dsm[];
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], ifull[2], iempty[2];
+    const uint32_t base = (smem_u32(dsm) + 1023) & ~1023u;
+    const uint32_t ibase = base + STAGES * 16384;       // 2 x 27 x 512 B
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nprod = MODE == 0 ? 32 : 128;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full[s]), MODE == 0 ? 1 : 128);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&ifull[b]), 1);
+            mbar_init(smem_u32(&iempty[b]), nprod);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 4) {
+        if (lane == 0) {
+            int lt = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+                int b = lt & 1;
+                mbar_wait(smem_u32(&iempty[b]), ((lt >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(smem_u32(&ifull[b]), 27 * 512);
+                for (int d = 0; d < 27; ++d)
+                    bulk_g2s(ibase + b * 27 * 512 + d * 512, nbr + (long long)d * n_out + (long long)t * 128, 512,
+                             smem_u32(&ifull[b]));
+            }
+        }
+    } else if ((MODE == 0 && warp == 0) || (MODE != 0 && warp < 4)) {
+        const int pt = threadIdx.x;
+        uint32_t it = 0;
+        int lt = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+            int b = lt & 1;
+            mbar_wait(smem_u32(&ifull[b]), (lt >> 1) & 1);
+            const int32_t* ib = reinterpret_cast<const int32_t*>(dsm + (ibase - smem_u32(dsm))) + b * 27 * 128;
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+                if (MODE == 0) {
+                    int4 r = *reinterpret_cast<const int4*>(ib + d * 128 + 4 * lane);
+                    if (lane == 0) mbar_arrive_expect_tx(smem_u32(&full[s]), 128 * 128);
+                    __syncwarp();
+                    gather4(base + s * 16384 + lane * 512, &map, 0, r, smem_u32(&full[s]));
+                } else {
+                    const int c = pt & 7, rb = pt >> 3;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        int r = rb + 16 * j;
+                        int idx = ib[d * 128 + r];
+                        uint32_t dst = base + s * 16384 + r * 128 + ((c ^ (r & 7)) << 4);
+                        const bf16* src = feat + (long long)(idx < 0 ? 0 : idx) * 64 + c * 8;
+                        if (MODE == 1) cp_async_16(dst, src, idx < 0 ? 0 : 16);
+                        else cp_async_16_cg(dst, src, idx < 0 ? 0 : 16);
+                    }
+                    cp_async_arrive_noinc(smem_u32(&full[s]));
+                }
+            }
+            mbar_arrive(smem_u32(&iempty[b]));
+        }
+    } else if (warp == 5 && lane == 0) {
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x)
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                mbar_wait(smem_u32(&full[s]), ph);
+                mbar_arrive(smem_u32(&empty[s]));
+            }
+    }
+}
+
+extern "C" int mb_gather_bw2(int mode, int stages, const void* feat, long long n_in, const int32_t* nbr,
+                             long long n_out, float* ms) {
+    CUtensorMap m;
+    int rc = make_map(&m, feat, n_in, 64, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    int tiles = (int)(n_out / 128);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    size_t smem = stages * 16384 + 2 * 27 * 512 + 1024;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    void (*k)(CUtensorMap, const bf16*, const int32_t*, long long, int);
+    if (stages == 8) k = mode == 0 ? k_gather_bw2<0, 8> : (mode == 1 ? k_gather_bw2<1, 8> : k_gather_bw2<2, 8>);
+    else k = mode == 0 ? k_gather_bw2<0, 12> : (mode == 1 ? k_gather_bw2<1, 12> : k_gather_bw2<2, 12>);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(a);
+        k<<<sms, 192, smem>>>(m, (const bf16*)feat, nbr, n_out, tiles);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+    }
+    cudaEventElapsedTime(ms, a, b);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- (3) MMA issue rate
+template <int N>
+__global__ void __launch_bounds__(128, 1) k_mma_rate(int iters, long long* cycles) {
+    extern __shared__ uint8_t dsm[];
+    __shared__ __align__(8) uint64_t done;
+    __shared__ uint32_t slot;
+    const uint32_t base = (smem_u32(dsm) + 1023) & ~1023u;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&done), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(smem_u32(&slot), 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        constexpr uint32_t idesc = idesc_bf16_f32(128, N, false, false);
+        long long t0 = clock64();
+        for (int i = 0; i < iters; ++i)
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                uint64_t ad = smem_desc(base + ks * 32, 16, 1024, kSwizzle128B);
+                uint64_t bd = smem_desc(base + 16384 + ks * 32, 16, 1024, kSwizzle128B);
+                mma_bf16(tmem, ad, bd, idesc, (i | ks) != 0);
+            }
+        mma_commit(smem_u32(&done));
+        mbar_wait(smem_u32(&done), 0);
+        cycles[blockIdx.x] = clock64() - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
+extern "C" int mb_mma_rate(int n, int iters, int blocks, long long* cycles_dev, float* ms) {
+    size_t smem = 16384 + 32768 + 1024;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    void (*k)(int, long long*) = n == 64 ? k_mma_rate<64> : (n == 128 ? k_mma_rate<128> : k_mma_rate<256>);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<blocks, 128, smem>>>(iters, cycles_dev);
+    cudaEventRecord(a);
+    k<<<blocks, 128, smem>>>(iters, cycles_dev);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(ms, a, b);
+    return (int)cudaGetLastError();
+}

@@ -1,0 +1,107 @@
+"""Build and run tools/microbench.cu on the GPU; prints one JSON report."""
+import ctypes as C
+import json
+import pathlib
+import subprocess
+import sys
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+SO = ROOT / "tools" / "_lib" / "libmicrobench.so"
+
+
+def build():
+    SO.parent.mkdir(exist_ok=True)
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo", "-Xcompiler",
+           "-fPIC", "-shared", str(ROOT / "tools" / "microbench.cu"), "-o", str(SO)]
+    subprocess.run(cmd, check=True)
+
+
+def main():
+    if "--build" in sys.argv or not SO.exists():
+        build()
+    if "--build-only" in sys.argv:
+        return
+    L = C.CDLL(str(SO))
+    rep = {}
+    # (1) gather4 probe — each config in its own process (a fault poisons the context)
+    if "--probe" in sys.argv:
+        box_h, swz, r0, r1, r2, r3, expect = (int(v) for v in sys.argv[sys.argv.index("--probe") + 1:][:7])
+        rows = (r0, r1, r2, r3)
+        src = (torch.arange(64 * 16, dtype=torch.float32).reshape(16, 64) / 8).to(torch.bfloat16).cuda()
+        out = torch.zeros(4 * 64, dtype=torch.bfloat16, device="cuda")
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        rc = L.mb_probe(C.c_void_p(src.data_ptr()), 16, box_h, swz, *rows, expect, C.c_void_p(out.data_ptr()),
+                        C.c_void_p(st.data_ptr()))
+        res = {"rc": rc, "completed": int(st.item())}
+        if not swz:
+            got = out.float().reshape(4, 64).cpu()
+            exp = torch.stack([src[r].float().cpu() if 0 <= r < 16 else torch.zeros(64) for r in rows])
+            res["data_ok"] = bool(torch.equal(got, exp))
+            res["got_col0"] = got[:, 0].tolist()
+        print(json.dumps(res))
+        return
+    probes = []
+    for box_h in ((1,) if "--skip-probe" in sys.argv else ()):
+        for swz in (0, 1):
+            for rows, expect in (((3, 0, 7, 15), 512), ((3, -1, 20, 5), 512), ((3, -1, 20, 5), 256)):
+                args = [str(v) for v in (box_h, swz, *rows, expect)]
+                r = subprocess.run([sys.executable, __file__, "--probe", *args], capture_output=True, text=True,
+                                   timeout=120)
+                line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else ""
+                try:
+                    res = json.loads(line)
+                except Exception:
+                    res = {"error": (r.stderr.strip().splitlines() or ["?"])[-1][:200]}
+                res.update({"box_h": box_h, "swizzle128": swz, "rows": rows, "expect_tx": expect})
+                probes.append(res)
+    rep["gather4_probe"] = probes
+    # (2) gather bandwidth on the cfg2 kernel map
+    import paper_2407_01781_b200 as P
+    from paper_2407_01781_b200.workloads import sphere_shell_coords
+    g, _ = P.build_from_coords(sphere_shell_coords(470, 1.5))
+    km = P.build_kernel_map(g, g, 1)
+    n = g.num_voxels
+    n_out = (n // 128) * 128
+    nbr = km.nbr[:, :n_out].contiguous()
+    feat = torch.randn(n, 64, device="cuda").to(torch.bfloat16)
+    valid_bytes = int((nbr >= 0).sum().item()) * 128
+    bw = {}
+    for mode, name in ((0, "tma_gather4"), (1, "cp_async_ca"), (2, "cp_async_cg")):
+        for cps in (1, 2):
+            ms = C.c_float(0)
+            rc = L.mb_gather_bw(mode, C.c_void_p(feat.data_ptr()), C.c_longlong(n), C.c_void_p(nbr.data_ptr()),
+                                C.c_longlong(n_out), cps, C.byref(ms))
+            bw[f"{name}_x{cps}"] = {"rc": rc, "ms": ms.value,
+                                    "valid_GBps": valid_bytes / (ms.value / 1e3) / 1e9 if ms.value else None,
+                                    "all_rows_GBps": 27 * n_out * 128 / (ms.value / 1e3) / 1e9 if ms.value else None}
+    for mode, name in ((0, "tma_gather4"), (1, "cp_async_ca"), (2, "cp_async_cg")):
+        for stages in (8, 12):
+            ms = C.c_float(0)
+            rc = L.mb_gather_bw2(mode, stages, C.c_void_p(feat.data_ptr()), C.c_longlong(n), C.c_void_p(nbr.data_ptr()),
+                                 C.c_longlong(n_out), C.byref(ms))
+            bw[f"{name}_idxprefetch_s{stages}"] = {"rc": rc, "ms": ms.value,
+                                    "valid_GBps": valid_bytes / (ms.value / 1e3) / 1e9 if ms.value else None,
+                                    "all_rows_GBps": 27 * n_out * 128 / (ms.value / 1e3) / 1e9 if ms.value else None}
+    rep["gather_bw_cfg2"] = {"valid_bytes": valid_bytes, "modes": bw}
+    # (3) MMA issue rate
+    cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
+    mm = {}
+    for nn in (64, 128, 256):
+        ms = C.c_float(0)
+        iters = 4000
+        rc = L.mb_mma_rate(nn, iters, 148, C.c_void_p(cyc.data_ptr()), C.byref(ms))
+        flops = 148 * iters * 4 * 2 * 128 * nn * 16
+        c = cyc.float().mean().item()
+        mm[f"N{nn}"] = {"rc": rc, "ms": ms.value, "TFLOPs": flops / (ms.value / 1e3) / 1e12,
+                        "cycles_per_mma": c / (iters * 4)}
+    rep["mma_rate_m128_k16"] = mm
+    print(json.dumps(rep, indent=1))
+
+
+if __name__ == "__main__":
+    main()
