@@ -166,8 +166,8 @@ def run_ours(args, rank, world, local_rank):
         kms.append(e0.elapsed_time(e1))
     n = grid.num_voxels
     pairs = km.total_pairs
-    nbr = km.nbr
-    nbrT = km.transposed_table()
+    nbr = km.fwd
+    nbrT = km.bwd
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     x = torch.randn(n, cin, device=dev, generator=gen).to(torch.bfloat16)
     gy = torch.randn(n, cout, device=dev, generator=gen).to(torch.bfloat16)

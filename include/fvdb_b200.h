@@ -33,6 +33,10 @@ extern "C" {
 #define FVDB_ERR_CUDA (-5)         /* CUDA runtime error; see fvdb_last_error() */
 #define FVDB_ERR_WORKSPACE (-6)    /* workspace smaller than the *_workspace_bytes() query */
 
+/* Neighbour tables nbr[27][ld] are row-padded: ld is a multiple of FVDB_NBR_ALIGN and the
+ * padding columns hold -1, so the tensor-core kernels can stream whole 512-row index blocks. */
+#define FVDB_NBR_ALIGN 512
+
 #define FVDB_DTYPE_F32 0
 #define FVDB_DTYPE_F64 1
 #define FVDB_DTYPE_BF16 2
@@ -97,19 +101,21 @@ int fvdb_coord_to_index(const fvdb_grid_view* grid, const int64_t* coords, int64
 int fvdb_active_coords(const fvdb_grid_view* grid, int64_t* out, void* stream);
 
 /* ---- a7: build_kernel_map (conv.py:105-122) ----
- * nbr[27, n_out] int32: 0-based input row of output o at stencil offset d, -1 if none.
- * pair_counts[27] int64 (device). Works for stride 1 and 2 (conv.py:113, 118). */
+ * nbr[27][ld] int32: nbr[d][o] = 0-based input row of output o at stencil offset d, -1 if none;
+ * columns [n_out, ld) are set to -1.  pair_counts[27] int64 (device). Stride 1 and 2
+ * (conv.py:113, 118). */
 size_t fvdb_kmap_workspace_bytes(int64_t num_leaf_out);
 int fvdb_kernel_map(const fvdb_grid_view* grid_in, const fvdb_grid_view* grid_out, int stride,
-                    int32_t* nbr, int64_t* pair_counts, void* workspace, size_t workspace_bytes,
-                    void* stream);
+                    int32_t* nbr, int64_t ld, int64_t* pair_counts, void* workspace,
+                    size_t workspace_bytes, void* stream);
 /* per-offset (in_rows, out_rows) lists, concatenated in offset order, out ascending */
 size_t fvdb_kmap_compact_workspace_bytes(int64_t n_out);
-int fvdb_kmap_compact(const int32_t* nbr, int64_t n_out, int64_t* in_rows, int64_t* out_rows,
-                      void* workspace, size_t workspace_bytes, void* stream);
-/* inverse table nbrT[27, n_in] (nbrT[d][i] = o  iff  nbr[d][o] = i), for dgrad / transposed conv */
-int fvdb_kmap_transpose(const int32_t* nbr, int64_t n_out, int64_t n_in, int32_t* nbrT,
-                        void* stream);
+int fvdb_kmap_compact(const int32_t* nbr, int64_t ld, int64_t n_out, int64_t* in_rows,
+                      int64_t* out_rows, void* workspace, size_t workspace_bytes, void* stream);
+/* inverse table nbrT[27][ldT] (nbrT[d][i] = o  iff  nbr[d][o] = i; -1 elsewhere incl. padding),
+ * for dgrad / transposed conv */
+int fvdb_kmap_transpose(const int32_t* nbr, int64_t ld, int64_t n_out, int64_t n_in,
+                        int32_t* nbrT, int64_t ldT, void* stream);
 
 /* ---- a9/a11: conv forward, dgrad, wgrad (conv.py:180-191, 339-368) ----
  * Output-stationary gather conv:  out[o,:] = sum_d  in[nbr[d][o],:] @ Wk[d]   (Wk[d] is [K,N]).
@@ -119,7 +125,7 @@ int fvdb_kmap_transpose(const int32_t* nbr, int64_t n_out, int64_t n_in, int32_t
  * SIMT path (FVDB_DTYPE_F32 / F64): exact-precision parity path.
  *   wk: [27, K, N] in the feature dtype (see fvdb_pack_weights_kn). */
 int fvdb_conv_gather_simt(int dtype, const void* in, int64_t n_in, int K, const void* wk, int N,
-                          const int32_t* nbr, int64_t n_out, void* out, void* stream);
+                          const int32_t* nbr, int64_t ld, int64_t n_out, void* out, void* stream);
 /* weight relayout [Cout,Cin,27] -> Wk[27][K][N]; transpose=0: K=Cin,N=Cout; 1: K=Cout,N=Cin */
 int fvdb_pack_weights_kn(int dtype, const void* w, int cout, int cin, int transpose, void* wk,
                          void* stream);
@@ -127,8 +133,8 @@ int fvdb_pack_weights_kn(int dtype, const void* w, int cout, int cin, int transp
  * deterministic split-K (fixed-order reduction over splits). */
 size_t fvdb_wgrad_workspace_bytes(int dtype, int64_t n_out, int cin, int cout);
 int fvdb_conv_wgrad_simt(int dtype, const void* in, int64_t n_in, int cin, const void* go,
-                         int cout, const int32_t* nbr, int64_t n_out, void* gw, void* workspace,
-                         size_t workspace_bytes, void* stream);
+                         int cout, const int32_t* nbr, int64_t ld, int64_t n_out, void* gw,
+                         void* workspace, size_t workspace_bytes, void* stream);
 
 /* Tensor-core path (bf16 in, fp32 accumulate in TMEM, tcgen05.mma):
  *   fvdb_pack_weights_umma: fp32 W[Cout,Cin,27] -> per-offset UMMA B-operand images (bf16,
@@ -138,12 +144,12 @@ int fvdb_conv_wgrad_simt(int dtype, const void* in, int64_t n_in, int cin, const
 int fvdb_pack_weights_umma(const float* w, int cout, int cin, int transpose, void* image,
                            void* stream);
 int fvdb_conv_gather_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
-                        const int32_t* nbr, int64_t n_out, void* out, int out_dtype,
+                        const int32_t* nbr, int64_t ld, int64_t n_out, void* out, int out_dtype,
                         void* stream);
 /* wgrad on tensor cores: gw fp32 [cout][cin][27]. */
 size_t fvdb_wgrad_tc_workspace_bytes(int64_t n_out, int cin, int cout);
 int fvdb_conv_wgrad_tc(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,
-                       const int32_t* nbr, int64_t n_out, float* gw, void* workspace,
+                       const int32_t* nbr, int64_t ld, int64_t n_out, float* gw, void* workspace,
                        size_t workspace_bytes, void* stream);
 
 /* dtype conversion helpers (fp32 -> bf16 RNE), used at the module boundary */

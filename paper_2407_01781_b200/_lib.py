@@ -23,6 +23,7 @@ FVDB_ERR_CUDA = -5
 FVDB_ERR_WORKSPACE = -6
 
 DTYPE_F32, DTYPE_F64, DTYPE_BF16 = 0, 1, 2
+NBR_ALIGN = 512  # FVDB_NBR_ALIGN
 
 _vp, _i64, _i32, _sz = C.c_void_p, C.c_int64, C.c_int, C.c_size_t
 
@@ -55,18 +56,18 @@ SIGNATURES = {
     "fvdb_coord_to_index": (_i32, [C.POINTER(GridView), _vp, _i64, _vp, _vp]),
     "fvdb_active_coords": (_i32, [C.POINTER(GridView), _vp, _vp]),
     "fvdb_kmap_workspace_bytes": (_sz, [_i64]),
-    "fvdb_kernel_map": (_i32, [C.POINTER(GridView), C.POINTER(GridView), _i32, _vp, _vp, _vp, _sz, _vp]),
+    "fvdb_kernel_map": (_i32, [C.POINTER(GridView), C.POINTER(GridView), _i32, _vp, _i64, _vp, _vp, _sz, _vp]),
     "fvdb_kmap_compact_workspace_bytes": (_sz, [_i64]),
-    "fvdb_kmap_compact": (_i32, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),
-    "fvdb_kmap_transpose": (_i32, [_vp, _i64, _i64, _vp, _vp]),
-    "fvdb_conv_gather_simt": (_i32, [_i32, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp]),
+    "fvdb_kmap_compact": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "fvdb_kmap_transpose": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp]),
+    "fvdb_conv_gather_simt": (_i32, [_i32, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp]),
     "fvdb_pack_weights_kn": (_i32, [_i32, _vp, _i32, _i32, _i32, _vp, _vp]),
     "fvdb_wgrad_workspace_bytes": (_sz, [_i32, _i64, _i32, _i32]),
-    "fvdb_conv_wgrad_simt": (_i32, [_i32, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "fvdb_conv_wgrad_simt": (_i32, [_i32, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "fvdb_pack_weights_umma": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp]),
-    "fvdb_conv_gather_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _i32, _vp]),
+    "fvdb_conv_gather_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _i32, _vp]),
     "fvdb_wgrad_tc_workspace_bytes": (_sz, [_i64, _i32, _i32]),
-    "fvdb_conv_wgrad_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "fvdb_conv_wgrad_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "fvdb_f32_to_bf16": (_i32, [_vp, _i64, _vp, _vp]),
 }
 

@@ -78,37 +78,67 @@ def _kernel_weights(kernel):
     return kernel.weights if isinstance(kernel, ConvKernel) else kernel
 
 
+class NbrTable:
+    """Device neighbour table ``t[27, ld]`` (int32, -1 = none; columns >= n are -1 padding)."""
+
+    __slots__ = ("t", "ld", "n")
+
+    def __init__(self, t, n):
+        self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
+
+    @property
+    def view(self):
+        return self.t[:, :self.n]
+
+
+def padded_len(n: int) -> int:
+    a = _lib.NBR_ALIGN
+    return max(a, (int(n) + a - 1) // a * a)
+
+
+def _empty_table(n, device):
+    return torch.full((27, padded_len(n)), -1, dtype=torch.int32, device=device)
+
+
 class KernelMap:
     """Per-offset (input_row, output_row) pairs (conv.py:80-102), device-resident.
 
-    Constructed either from the reference's lists (``KernelMap(in_rows, out_rows,
-    num_in, num_out, stride)``) or from a neighbour table (``nbr=``).
+    Held as the dense offset-major neighbour table (``nbr`` = [27, num_out] view of a
+    row-padded int32 table); the reference's ``in_rows`` / ``out_rows`` lists are
+    materialised lazily.  Constructed from the reference's lists
+    (``KernelMap(in_rows, out_rows, num_in, num_out, stride)``) or from a table.
     """
 
-    __slots__ = ("nbr", "num_in", "num_out", "stride", "_counts", "_lists", "_nbrT")
+    __slots__ = ("fwd", "num_in", "num_out", "stride", "_counts", "_lists", "_bwd")
 
-    def __init__(self, in_rows=None, out_rows=None, num_in=0, num_out=0, stride=1, *, nbr=None,
+    def __init__(self, in_rows=None, out_rows=None, num_in=0, num_out=0, stride=1, *, table=None,
                  pair_counts=None):
         self.num_in, self.num_out, self.stride = int(num_in), int(num_out), int(stride)
         self._lists = None
-        self._nbrT = None
-        if nbr is None:
+        self._bwd = None
+        if table is None:
             from .topology import _device
             dev = _device()
-            nbr = torch.full((27, self.num_out), -1, dtype=torch.int32, device=dev)
+            t = _empty_table(self.num_out, dev)
             ins = [_to_device_tensor(r, dev, torch.int64) for r in in_rows]
             outs = [_to_device_tensor(r, dev, torch.int64) for r in out_rows]
             for d in range(27):
                 if outs[d].numel():
-                    nbr[d, outs[d]] = ins[d].to(torch.int32)
+                    t[d, outs[d]] = ins[d].to(torch.int32)
             self._lists = (ins, outs)
             pair_counts = torch.tensor([int(o.numel()) for o in outs], dtype=torch.int64)
-        self.nbr = nbr
+            table = NbrTable(t, self.num_out)
+        self.fwd = table
         self._counts = pair_counts
 
     @property
+    def nbr(self):
+        """[27, num_out] int32 neighbour table (view; -1 = no pair)."""
+        return self.fwd.view
+
+    @property
     def device(self):
-        return self.nbr.device
+        return self.fwd.t.device
 
     @property
     def pair_counts(self):
@@ -133,7 +163,7 @@ class KernelMap:
                 L = _lib.lib()
                 wsb = L.fvdb_kmap_compact_workspace_bytes(self.num_out)
                 ws = _lib.workspace(wsb, dev)
-                _lib.check(L.fvdb_kmap_compact(self.nbr.data_ptr(), self.num_out, ins.data_ptr(),
+                _lib.check(L.fvdb_kmap_compact(self.fwd.t.data_ptr(), self.fwd.ld, self.num_out, ins.data_ptr(),
                                                outs.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()),
                            "kmap_compact")
             bounds = np.concatenate([[0], np.cumsum(counts)])
@@ -149,15 +179,19 @@ class KernelMap:
     def out_rows(self):
         return self._compact()[1]
 
-    def transposed_table(self):
-        """nbrT[27, num_in]: nbrT[d][i] = o iff nbr[d][o] = i (dgrad / transposed conv)."""
-        if self._nbrT is None:
-            t = torch.empty((27, self.num_in), dtype=torch.int32, device=self.device)
+    @property
+    def bwd(self) -> NbrTable:
+        """Transposed table nbrT[d][i] = o iff nbr[d][o] = i (dgrad / transposed conv), cached."""
+        if self._bwd is None:
+            t = torch.empty((27, padded_len(self.num_in)), dtype=torch.int32, device=self.device)
             L = _lib.lib()
-            _lib.check(L.fvdb_kmap_transpose(self.nbr.data_ptr(), self.num_out, self.num_in, t.data_ptr(),
-                                             _lib.stream_ptr()), "kmap_transpose")
-            self._nbrT = t
-        return self._nbrT
+            _lib.check(L.fvdb_kmap_transpose(self.fwd.t.data_ptr(), self.fwd.ld, self.num_out, self.num_in,
+                                             t.data_ptr(), t.shape[1], _lib.stream_ptr()), "kmap_transpose")
+            self._bwd = NbrTable(t, self.num_in)
+        return self._bwd
+
+    def transposed_table(self):
+        return self.bwd.view
 
     def __repr__(self):
         return f"KernelMap(num_in={self.num_in}, num_out={self.num_out}, stride={self.stride})"
@@ -169,29 +203,31 @@ def build_kernel_map(grid_in, grid_out, stride=1):
     if stride not in (1, 2):
         raise ValueError(f"stride must be 1 or 2, got {stride}")
     dev = grid_out.device
-    nbr = torch.empty((27, grid_out.num_voxels), dtype=torch.int32, device=dev)
+    n_out = grid_out.num_voxels
+    t = torch.empty((27, padded_len(n_out)), dtype=torch.int32, device=dev)
     counts = torch.zeros(27, dtype=torch.int64, device=dev)
-    if grid_out.num_voxels:
-        L = _lib.lib()
-        wsb = L.fvdb_kmap_workspace_bytes(grid_out.num_leaf_nodes)
-        ws = _lib.workspace(wsb, dev)
-        _lib.check(L.fvdb_kernel_map(C.byref(grid_in.view()), C.byref(grid_out.view()), stride, nbr.data_ptr(),
-                                     counts.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()), "kernel_map")
-    return KernelMap(num_in=grid_in.num_voxels, num_out=grid_out.num_voxels, stride=stride, nbr=nbr,
+    L = _lib.lib()
+    wsb = L.fvdb_kmap_workspace_bytes(grid_out.num_leaf_nodes)
+    ws = _lib.workspace(wsb, dev)
+    _lib.check(L.fvdb_kernel_map(C.byref(grid_in.view()), C.byref(grid_out.view()), stride, t.data_ptr(),
+                                 t.shape[1], counts.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()),
+               "kernel_map")
+    return KernelMap(num_in=grid_in.num_voxels, num_out=n_out, stride=stride, table=NbrTable(t, n_out),
                      pair_counts=counts)
 
 
 def batch_kernel_map(kmaps, in_offsets, out_offsets):
     """Concatenate per-grid kernel maps into one batch-global table (row offsets added)."""
-    parts = []
-    for km, io in zip(kmaps, in_offsets):
-        t = km.nbr
-        parts.append(torch.where(t >= 0, t + int(io), t))
-    nbr = torch.cat(parts, dim=1).contiguous() if parts else None
-    counts = torch.stack([km._counts.to(nbr.device) for km in kmaps]).sum(0)
     num_in = sum(km.num_in for km in kmaps)
     num_out = sum(km.num_out for km in kmaps)
-    return KernelMap(num_in=num_in, num_out=num_out, stride=kmaps[0].stride, nbr=nbr, pair_counts=counts)
+    dev = kmaps[0].device
+    t = _empty_table(num_out, dev)
+    for km, io, oo in zip(kmaps, in_offsets, out_offsets):
+        v = km.nbr
+        t[:, int(oo):int(oo) + km.num_out] = torch.where(v >= 0, v + int(io), v)
+    counts = torch.stack([km._counts.to(dev) for km in kmaps]).sum(0)
+    return KernelMap(num_in=num_in, num_out=num_out, stride=kmaps[0].stride, table=NbrTable(t, num_out),
+                     pair_counts=counts)
 
 
 def choose_variant(grid, c_in, c_out):
@@ -259,13 +295,13 @@ def _tc_width(c: int) -> int:
     raise ValueError(f"bf16 tensor-core path supports up to 128 channels per operand, got {c}")
 
 
-def gather_conv(x: torch.Tensor, nbr: torch.Tensor, w: torch.Tensor, transpose: bool = False,
+def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool = False,
                 out_dtype=None, w_image=None) -> torch.Tensor:
     """out[o] = Σ_d x[nbr[d][o]] @ Wk[d]; Wk from w [Cout,Cin,3,3,3] (transpose → dgrad form).
 
-    x: [n_in, K] float32 / float64 / bfloat16 CUDA tensor.  Returns [n_out, N].
+    x: [n_in, K] float32 / float64 / bfloat16 CUDA tensor; nbr: padded NbrTable.  Returns [n_out, N].
     """
-    n_out = int(nbr.shape[1])
+    n_out = nbr.n
     cout, cin = int(w.shape[0]), int(w.shape[1])
     K, N = (cout, cin) if transpose else (cin, cout)
     if x.shape[1] != K:
@@ -278,7 +314,8 @@ def gather_conv(x: torch.Tensor, nbr: torch.Tensor, w: torch.Tensor, transpose: 
         out = torch.empty((n_out, N), dtype=x.dtype, device=x.device)
         if n_out:
             _lib.check(L.fvdb_conv_gather_simt(_dtype_code(x.dtype), x.data_ptr(), x.shape[0], K, wk.data_ptr(), N,
-                                               nbr.data_ptr(), n_out, out.data_ptr(), st), "conv_gather_simt")
+                                               nbr.t.data_ptr(), nbr.ld, n_out, out.data_ptr(), st),
+                       "conv_gather_simt")
         return out
     if x.dtype != torch.bfloat16:
         raise TypeError(f"unsupported feature dtype {x.dtype}")
@@ -293,14 +330,14 @@ def gather_conv(x: torch.Tensor, nbr: torch.Tensor, w: torch.Tensor, transpose: 
     img = w_image if w_image is not None else pack_weights_umma(w, transpose)
     out = torch.empty((n_out, N), dtype=out_dtype, device=x.device)
     if n_out:
-        _lib.check(L.fvdb_conv_gather_tc(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, nbr.data_ptr(), n_out,
-                                         out.data_ptr(), _dtype_code(out_dtype), st), "conv_gather_tc")
+        _lib.check(L.fvdb_conv_gather_tc(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, nbr.t.data_ptr(), nbr.ld,
+                                         n_out, out.data_ptr(), _dtype_code(out_dtype), st), "conv_gather_tc")
     return out
 
 
-def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: torch.Tensor) -> torch.Tensor:
+def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: NbrTable) -> torch.Tensor:
     """gw[co][ci][d] = Σ_o go[o,co]·x[nbr[d][o],ci]  → [Cout, Cin, 3, 3, 3] (fp32 for bf16 inputs)."""
-    n_out = int(nbr.shape[1])
+    n_out = nbr.n
     cin, cout = int(x.shape[1]), int(go.shape[1])
     L = _lib.lib()
     st = _lib.stream_ptr()
@@ -310,8 +347,8 @@ def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: torch.Tensor) -> torch.Tensor:
         code = _dtype_code(x.dtype)
         wsb = L.fvdb_wgrad_workspace_bytes(code, n_out, cin, cout)
         ws = _lib.workspace(wsb, x.device)
-        _lib.check(L.fvdb_conv_wgrad_simt(code, x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, nbr.data_ptr(),
-                                          n_out, gw.data_ptr(), ws.data_ptr(), wsb, st), "conv_wgrad_simt")
+        _lib.check(L.fvdb_conv_wgrad_simt(code, x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, nbr.t.data_ptr(),
+                                          nbr.ld, n_out, gw.data_ptr(), ws.data_ptr(), wsb, st), "conv_wgrad_simt")
         return gw
     ci_p, co_p = _tc_width(cin), _tc_width(cout)
     if (ci_p, co_p) != (cin, cout):
@@ -320,12 +357,12 @@ def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: torch.Tensor) -> torch.Tensor:
     gw = torch.empty((cout, cin, 3, 3, 3), dtype=torch.float32, device=x.device)
     wsb = L.fvdb_wgrad_tc_workspace_bytes(n_out, cin, cout)
     ws = _lib.workspace(wsb, x.device)
-    _lib.check(L.fvdb_conv_wgrad_tc(x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, nbr.data_ptr(), n_out,
-                                    gw.data_ptr(), ws.data_ptr(), wsb, st), "conv_wgrad_tc")
+    _lib.check(L.fvdb_conv_wgrad_tc(x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, nbr.t.data_ptr(), nbr.ld,
+                                    n_out, gw.data_ptr(), ws.data_ptr(), wsb, st), "conv_wgrad_tc")
     return gw
 
 
-def lggs_stats(nbr: torch.Tensor, stats: dict):
+def lggs_stats(nbr: torch.Tensor, stats: dict):  # nbr: [27, n_out] view
     """LGGS instrumentation counters (conv.py:264-301): 64-row blocks, per-offset pad to 16."""
     n = int(nbr.shape[1])
     nblocks = (n + LGGS_BLOCK - 1) // LGGS_BLOCK
@@ -371,7 +408,7 @@ def conv(grid_in, features, kernel, grid_out=None, variant="igemm", stride=1, km
         w = w.to(features.dtype)  # conv.py:164
     if kmap is None:
         kmap = build_kernel_map(grid_in, grid_out, stride)
-    out = gather_conv(features, kmap.nbr, w, transpose=False)
+    out = gather_conv(features, kmap.fwd, w, transpose=False)
     if variant == "lggs" and stats is not None:
         lggs_stats(kmap.nbr, stats)
     return out
@@ -392,11 +429,11 @@ def conv_backward(kmap, grad_out, features_in, kernel):
     w_dtype = w.dtype
     if grad_out.dtype != torch.bfloat16:
         w = w.to(grad_out.dtype)
-    grad_in = gather_conv(grad_out, kmap.transposed_table(), w, transpose=True,
+    grad_in = gather_conv(grad_out, kmap.bwd, w, transpose=True,
                           out_dtype=features_in.dtype if features_in.dtype == torch.bfloat16 else None)
     grad_in = grad_in.to(features_in.dtype)
     gw = wgrad(features_in.to(grad_out.dtype) if grad_out.dtype != torch.bfloat16 else features_in.to(torch.bfloat16),
-               grad_out, kmap.nbr)
+               grad_out, kmap.fwd)
     return grad_in, gw.to(w_dtype)
 
 
@@ -415,7 +452,7 @@ def conv_transpose(kmap, x_coarse, kernel, out_dtype=None):
     w = _to_device_tensor(weights, dev)
     if x.dtype != torch.bfloat16:
         w = w.to(x.dtype)
-    return gather_conv(x, kmap.transposed_table(), w, transpose=True, out_dtype=out_dtype)
+    return gather_conv(x, kmap.bwd, w, transpose=True, out_dtype=out_dtype)
 
 
 def conv_batch(batch, features, kernel, variant="igemm"):
@@ -435,7 +472,7 @@ def conv_batch(batch, features, kernel, variant="igemm"):
     w = _to_device_tensor(weights, feats.device)
     if feats.dtype != torch.bfloat16:
         w = w.to(feats.dtype)
-    return batch.jagged(gather_conv(feats, km.nbr, w))
+    return batch.jagged(gather_conv(feats, km.fwd, w))
 
 
 def batch_grid_kernel_map(batch_in, batch_out, stride):

@@ -20,8 +20,8 @@ constexpr int kMaxAcc = 32;  // kRows * N / kThr for N <= 256
 
 template <typename T>
 __global__ void __launch_bounds__(kThr) k_conv_gather(const T* __restrict__ in, int K, const T* __restrict__ wk,
-                                                      int N, const int32_t* __restrict__ nbr, int64_t n_out,
-                                                      T* __restrict__ out) {
+                                                      int N, const int32_t* __restrict__ nbr, int64_t ld,
+                                                      int64_t n_out, T* __restrict__ out) {
     __shared__ T s_in[kRows][kKC + 1];
     __shared__ T s_w[kKC][256];
     __shared__ int32_t s_idx[kRows];
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kThr) k_conv_gather(const T* __restrict__ in, 
         __syncthreads();
         if (tid < kRows) {
             int64_t o = o0 + tid;
-            s_idx[tid] = o < n_out ? nbr[(int64_t)d * n_out + o] : -1;
+            s_idx[tid] = o < n_out ? nbr[(int64_t)d * ld + o] : -1;
         }
         __syncthreads();
         for (int k0 = 0; k0 < K; k0 += kKC) {
@@ -94,8 +94,8 @@ __global__ void k_pack_kn(const T* __restrict__ w, int cout, int cin, int transp
 constexpr int kWB = 32;  // output-channel and input-channel block edge
 template <typename T>
 __global__ void __launch_bounds__(kThr) k_wgrad_part(const T* __restrict__ in, int cin, const T* __restrict__ go,
-                                                     int cout, const int32_t* __restrict__ nbr, int64_t n_out,
-                                                     int64_t rows_per_split, T* __restrict__ part) {
+                                                     int cout, const int32_t* __restrict__ nbr, int64_t ld,
+                                                     int64_t n_out, int64_t rows_per_split, T* __restrict__ part) {
     __shared__ T s_go[kRows][kWB + 1];
     __shared__ T s_in[kRows][kWB + 1];
     __shared__ int32_t s_idx[kRows];
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThr) k_wgrad_part(const T* __restrict__ in, i
         __syncthreads();
         if (tid < kRows) {
             int64_t o = o0 + tid;
-            s_idx[tid] = o < end ? nbr[(int64_t)d * n_out + o] : -1;
+            s_idx[tid] = o < end ? nbr[(int64_t)d * ld + o] : -1;
         }
         __syncthreads();
         for (int t = tid; t < kRows * kWB; t += kThr) {
@@ -163,18 +163,18 @@ int wgrad_splits(int64_t n_out) {
 }
 
 template <typename T>
-int run_gather(const void* in, int K, const void* wk, int N, const int32_t* nbr, int64_t n_out, void* out,
+int run_gather(const void* in, int K, const void* wk, int N, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
                cudaStream_t st) {
     if (n_out == 0) return FVDB_OK;
     unsigned blocks = (unsigned)ceil_div(n_out, kRows);
-    k_conv_gather<T><<<blocks, kThr, 0, st>>>((const T*)in, K, (const T*)wk, N, nbr, n_out, (T*)out);
+    k_conv_gather<T><<<blocks, kThr, 0, st>>>((const T*)in, K, (const T*)wk, N, nbr, ld, n_out, (T*)out);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
 
 template <typename T>
-int run_wgrad(const void* in, int cin, const void* go, int cout, const int32_t* nbr, int64_t n_out, void* gw,
-              void* ws, size_t ws_bytes, cudaStream_t st) {
+int run_wgrad(const void* in, int cin, const void* go, int cout, const int32_t* nbr, int64_t ld, int64_t n_out,
+              void* gw, void* ws, size_t ws_bytes, cudaStream_t st) {
     const int splits = wgrad_splits(n_out);
     size_t need = (size_t)splits * 27 * cout * cin * sizeof(T);
     if (ws_bytes < need) return FVDB_ERR_WORKSPACE;
@@ -182,7 +182,7 @@ int run_wgrad(const void* in, int cin, const void* go, int cout, const int32_t* 
     int64_t rps = ceil_div(n_out > 0 ? n_out : 1, splits);
     rps = ceil_div(rps, kRows) * kRows;
     dim3 grid(splits, 27, ((cout + kWB - 1) / kWB) * ((cin + kWB - 1) / kWB));
-    k_wgrad_part<T><<<grid, kThr, 0, st>>>((const T*)in, cin, (const T*)go, cout, nbr, n_out, rps, part);
+    k_wgrad_part<T><<<grid, kThr, 0, st>>>((const T*)in, cin, (const T*)go, cout, nbr, ld, n_out, rps, part);
     k_wgrad_reduce<T><<<(unsigned)ceil_div((int64_t)27 * cout * cin, 256), 256, 0, st>>>(part, splits, cout, cin,
                                                                                        (T*)gw);
     FVDB_LAUNCH_CHECK();
@@ -195,12 +195,12 @@ int run_wgrad(const void* in, int cin, const void* go, int cout, const int32_t* 
 using namespace fvdb;
 
 extern "C" int fvdb_conv_gather_simt(int dtype, const void* in, int64_t n_in, int K, const void* wk, int N,
-                                     const int32_t* nbr, int64_t n_out, void* out, void* stream) {
+                                     const int32_t* nbr, int64_t ld, int64_t n_out, void* out, void* stream) {
     (void)n_in;
-    if (K <= 0 || N <= 0 || N > 256) return FVDB_ERR_INVALID;
+    if (K <= 0 || N <= 0 || N > 256 || ld < n_out) return FVDB_ERR_INVALID;
     cudaStream_t st = as_stream(stream);
-    if (dtype == FVDB_DTYPE_F32) return run_gather<float>(in, K, wk, N, nbr, n_out, out, st);
-    if (dtype == FVDB_DTYPE_F64) return run_gather<double>(in, K, wk, N, nbr, n_out, out, st);
+    if (dtype == FVDB_DTYPE_F32) return run_gather<float>(in, K, wk, N, nbr, ld, n_out, out, st);
+    if (dtype == FVDB_DTYPE_F64) return run_gather<double>(in, K, wk, N, nbr, ld, n_out, out, st);
     return FVDB_ERR_INVALID;
 }
 
@@ -225,11 +225,12 @@ extern "C" size_t fvdb_wgrad_workspace_bytes(int dtype, int64_t n_out, int cin, 
 }
 
 extern "C" int fvdb_conv_wgrad_simt(int dtype, const void* in, int64_t n_in, int cin, const void* go, int cout,
-                                    const int32_t* nbr, int64_t n_out, void* gw, void* ws, size_t ws_bytes,
-                                    void* stream) {
+                                    const int32_t* nbr, int64_t ld, int64_t n_out, void* gw, void* ws,
+                                    size_t ws_bytes, void* stream) {
     (void)n_in;
+    if (ld < n_out) return FVDB_ERR_INVALID;
     cudaStream_t st = as_stream(stream);
-    if (dtype == FVDB_DTYPE_F32) return run_wgrad<float>(in, cin, go, cout, nbr, n_out, gw, ws, ws_bytes, st);
-    if (dtype == FVDB_DTYPE_F64) return run_wgrad<double>(in, cin, go, cout, nbr, n_out, gw, ws, ws_bytes, st);
+    if (dtype == FVDB_DTYPE_F32) return run_wgrad<float>(in, cin, go, cout, nbr, ld, n_out, gw, ws, ws_bytes, st);
+    if (dtype == FVDB_DTYPE_F64) return run_wgrad<double>(in, cin, go, cout, nbr, ld, n_out, gw, ws, ws_bytes, st);
     return FVDB_ERR_INVALID;
 }

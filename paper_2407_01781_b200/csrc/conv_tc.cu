@@ -38,7 +38,6 @@ using bf16 = __nv_bfloat16;
 using namespace tc;
 
 constexpr int kTile = 128;        // output rows per tile (UMMA M)
-constexpr int kThreadsTC = 288;   // 4 producer + 4 epilogue + 1 MMA warp
 
 __host__ __device__ constexpr int pow2_cols(int c) {
     return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
@@ -52,37 +51,62 @@ __host__ __device__ __forceinline__ uint32_t swz_off(int r, int c, int rowb) {
 
 template <int K, int N>
 struct FwdCfg {
-    static constexpr int KB = K >= 64 ? 64 : K;  // K elements per swizzle row
-    static constexpr int ROWB = KB * 2;
+    static constexpr int KB = K >= 64 ? 64 : K;       // K elements per swizzle row
+    static constexpr int ROWB = KB * 2;                // bytes per swizzled row segment
     static constexpr int NKB = K / KB;
-    static constexpr int A_BYTES = kTile * K * 2;
-    static constexpr int B_BYTES = N * K * 2;
-    static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (STAGE * 4 <= 100 * 1024) ? 4 : ((STAGE * 3 <= 200 * 1024) ? 3 : 2);
-    static constexpr int SMEM = STAGES * STAGE + 1024;
+    static constexpr int A_BYTES = kTile * K * 2;      // one gathered 128-row A tile
+    static constexpr int B_BYTES = N * K * 2;          // one offset's weight image
+    static constexpr int TPS = N <= 64 ? 4 : 2;        // 128-row tiles per super-tile (share one B load)
+    static constexpr int SUPER = TPS * kTile;
+    static constexpr int IDX_BYTES = SUPER * 4;        // index block of one (super-tile, offset)
+    static constexpr int ISLOTS = 8;
+    static constexpr int BSLOTS = B_BYTES <= 8192 ? 3 : 2;
+    static constexpr int FIXED = BSLOTS * B_BYTES + ISLOTS * IDX_BYTES + 1024;
+    static constexpr int STAGES0 = (222 * 1024 - FIXED) / A_BYTES;
+    static constexpr int STAGES = STAGES0 > 10 ? 10 : STAGES0;
+    static constexpr int SMEM = FIXED + STAGES * A_BYTES;
     static constexpr uint32_t LAYOUT = ROWB == 128 ? kSwizzle128B : kSwizzle64B;
-    static constexpr int CPR = K / 8;           // 16-B chunks per gathered row
-    static constexpr int RSTEP = kTile / CPR;   // rows per producer pass
-    static constexpr int TMEM_COLS = pow2_cols(2 * N);
+    static constexpr int CPR = K / 8;                  // 16-B chunks per gathered row
+    static constexpr int RSTEP = kTile / CPR;          // rows per producer pass
+    static constexpr int TMEM_COLS = pow2_cols(2 * TPS * N);
     static constexpr uint32_t IDESC = idesc_bf16_f32(kTile, N, false, false);
+    static_assert(2 * TPS * N <= 512, "TMEM budget");
+    static_assert(FVDB_NBR_ALIGN % SUPER == 0, "index blocks must tile the padded table");
 };
 
+constexpr int kFwdThreads = 320;  // warps 0-3 gather, 4 loader, 5 MMA, 6-9 epilogue
+
 template <int K, int N, bool OUT_BF16>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     k_conv_fwd_tc(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, const int32_t* __restrict__ nbr,
-                  int64_t n_out, void* __restrict__ out, int num_tiles) {
+                  int64_t ld, int64_t n_out, void* __restrict__ out, int num_super) {
     using C = FwdCfg<K, N>;
     extern __shared__ uint8_t dsmem[];
-    __shared__ __align__(8) uint64_t bar_full[C::STAGES], bar_empty[C::STAGES], bar_tfull[2], bar_tempty[2];
+    __shared__ __align__(8) uint64_t bar_full[C::STAGES], bar_empty[C::STAGES];
+    __shared__ __align__(8) uint64_t bar_ifull[C::ISLOTS], bar_iempty[C::ISLOTS];
+    __shared__ __align__(8) uint64_t bar_bfull[C::BSLOTS], bar_bempty[C::BSLOTS];
+    __shared__ __align__(8) uint64_t bar_tfull[2], bar_tempty[2];
     __shared__ uint32_t tmem_slot;
 
-    const uint32_t base = (smem_u32(dsmem) + 1023u) & ~1023u;
+    const uint32_t sbase = smem_u32(dsmem);
+    const uint32_t base = (sbase + 1023u) & ~1023u;                  // A stages (1024-aligned)
+    const uint32_t bbase = base + C::STAGES * C::A_BYTES;            // weight images
+    const uint32_t ibase = bbase + C::BSLOTS * C::B_BYTES;           // index blocks
+    const int32_t* idx_smem = reinterpret_cast<const int32_t*>(dsmem + (ibase - sbase));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
-            mbar_init(smem_u32(&bar_full[s]), kTile + 1);  // 128 cp.async arrivals + 1 expect_tx
+            mbar_init(smem_u32(&bar_full[s]), 128);   // one cp.async arrival per gather thread
             mbar_init(smem_u32(&bar_empty[s]), 1);
+        }
+        for (int s = 0; s < C::ISLOTS; ++s) {
+            mbar_init(smem_u32(&bar_ifull[s]), 1);
+            mbar_init(smem_u32(&bar_iempty[s]), 128);
+        }
+        for (int s = 0; s < C::BSLOTS; ++s) {
+            mbar_init(smem_u32(&bar_bfull[s]), 1);
+            mbar_init(smem_u32(&bar_bempty[s]), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(smem_u32(&bar_tfull[a]), 1);
@@ -90,116 +114,143 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 8) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
+    if (warp == 5) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
 
     if (warp < 4) {
-        // ------------------------------ producers ------------------------------
+        // ---------------- gather producers: 16-B cp.async per (row, chunk), 8 lanes per row --------
         const int pt = threadIdx.x;
         const int cchunk = pt % C::CPR, rbase = pt / C::CPR;
         const int kb = cchunk / (C::KB / 8), cc = cchunk % (C::KB / 8);
-        uint32_t it = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const int64_t row0 = (int64_t)tile * kTile;
-            for (int d = 0; d < 27; ++d, ++it) {
-                const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
-                int32_t idx[C::CPR];
+        uint32_t it = 0, ic = 0;
+        for (int st = blockIdx.x; st < num_super; st += gridDim.x) {
+            for (int d = 0; d < 27; ++d, ++ic) {
+                const uint32_t islot = ic % C::ISLOTS;
+                mbar_wait(smem_u32(&bar_ifull[islot]), (ic / C::ISLOTS) & 1);
+                const int32_t* ib = idx_smem + islot * C::SUPER;
+                for (int t = 0; t < C::TPS; ++t, ++it) {
+                    const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
+                    int32_t idx[C::CPR];
 #pragma unroll
-                for (int j = 0; j < C::CPR; ++j) {
-                    int64_t row = row0 + rbase + j * C::RSTEP;
-                    idx[j] = row < n_out ? __ldg(nbr + (int64_t)d * n_out + row) : -1;
-                }
-                mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
-                const uint32_t sA = base + s * C::STAGE;
+                    for (int j = 0; j < C::CPR; ++j) idx[j] = ib[t * kTile + rbase + j * C::RSTEP];
+                    mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+                    const uint32_t sA = base + s * C::A_BYTES;
 #pragma unroll
-                for (int j = 0; j < C::CPR; ++j) {
-                    const int r = rbase + j * C::RSTEP;
-                    const uint32_t dst = sA + kb * (kTile * C::ROWB) + swz_off(r, cc, C::ROWB);
-                    const int32_t i = idx[j] < 0 ? 0 : idx[j];
-                    cp_async_16(dst, in + (int64_t)i * K + cchunk * 8, idx[j] < 0 ? 0u : 16u);
+                    for (int j = 0; j < C::CPR; ++j) {
+                        const int r = rbase + j * C::RSTEP;
+                        const uint32_t dst = sA + kb * (kTile * C::ROWB) + swz_off(r, cc, C::ROWB);
+                        const int32_t i = idx[j] < 0 ? 0 : idx[j];
+                        cp_async_16(dst, in + (int64_t)i * K + cchunk * 8, idx[j] < 0 ? 0u : 16u);
+                    }
+                    cp_async_arrive_noinc(smem_u32(&bar_full[s]));
                 }
-                const uint32_t fb = smem_u32(&bar_full[s]);
-                if (pt == 0) {
-                    mbar_arrive_expect_tx(fb, C::B_BYTES);
-                    bulk_g2s(sA + C::A_BYTES, wimg + (size_t)d * C::B_BYTES, C::B_BYTES, fb);
-                }
-                cp_async_arrive_noinc(fb);
+                mbar_arrive(smem_u32(&bar_iempty[islot]));
             }
         }
-    } else if (warp == 8) {
-        // ------------------------------ MMA issuer -----------------------------
-        uint32_t it = 0, lt = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
-            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
-            mbar_wait(smem_u32(&bar_tempty[acc]), aph ^ 1);
-            tc_fence_after();
-            const uint32_t dt = tmem + acc * N;
-            for (int d = 0; d < 27; ++d, ++it) {
-                const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
-                mbar_wait(smem_u32(&bar_full[s]), ph);
-                fence_proxy_async_smem();
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t sA = base + s * C::STAGE, sB = sA + C::A_BYTES;
-#pragma unroll
-                    for (int kb = 0; kb < C::NKB; ++kb)
-#pragma unroll
-                        for (int ks = 0; ks < C::KB / 16; ++ks) {
-                            uint64_t ad = smem_desc(sA + kb * kTile * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
-                            uint64_t bd = smem_desc(sB + kb * N * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
-                            mma_bf16(dt, ad, bd, C::IDESC, (d | kb | ks) != 0);
-                        }
-                    mma_commit(smem_u32(&bar_empty[s]));
+    } else if (warp == 4) {
+        // ---------------- loader: index blocks + weight images by TMA bulk copies ---------------
+        if (lane == 0) {
+            uint32_t ic = 0, bc = 0;
+            for (int st = blockIdx.x; st < num_super; st += gridDim.x) {
+                for (int d = 0; d < 27; ++d, ++ic, ++bc) {
+                    const uint32_t islot = ic % C::ISLOTS;
+                    mbar_wait(smem_u32(&bar_iempty[islot]), ((ic / C::ISLOTS) & 1) ^ 1);
+                    mbar_arrive_expect_tx(smem_u32(&bar_ifull[islot]), C::IDX_BYTES);
+                    bulk_g2s(ibase + islot * C::IDX_BYTES, nbr + (int64_t)d * ld + (int64_t)st * C::SUPER,
+                             C::IDX_BYTES, smem_u32(&bar_ifull[islot]));
+                    const uint32_t bslot = bc % C::BSLOTS;
+                    mbar_wait(smem_u32(&bar_bempty[bslot]), ((bc / C::BSLOTS) & 1) ^ 1);
+                    mbar_arrive_expect_tx(smem_u32(&bar_bfull[bslot]), C::B_BYTES);
+                    bulk_g2s(bbase + bslot * C::B_BYTES, wimg + (size_t)d * C::B_BYTES, C::B_BYTES,
+                             smem_u32(&bar_bfull[bslot]));
                 }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        uint32_t it = 0, bc = 0, lt = 0;
+        for (int st = blockIdx.x; st < num_super; st += gridDim.x, ++lt) {
+            const uint32_t buf = lt & 1;
+            mbar_wait(smem_u32(&bar_tempty[buf]), ((lt >> 1) & 1) ^ 1);
+            tc_fence_after();
+            for (int d = 0; d < 27; ++d, ++bc) {
+                const uint32_t bslot = bc % C::BSLOTS;
+                mbar_wait(smem_u32(&bar_bfull[bslot]), (bc / C::BSLOTS) & 1);
+                const uint32_t sB = bbase + bslot * C::B_BYTES;
+                for (int t = 0; t < C::TPS; ++t, ++it) {
+                    const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
+                    mbar_wait(smem_u32(&bar_full[s]), ph);
+                    fence_proxy_async_smem();
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t sA = base + s * C::A_BYTES;
+                        const uint32_t dt = tmem + (buf * C::TPS + t) * N;
+#pragma unroll
+                        for (int kb = 0; kb < C::NKB; ++kb)
+#pragma unroll
+                            for (int ks = 0; ks < C::KB / 16; ++ks) {
+                                uint64_t ad = smem_desc(sA + kb * kTile * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
+                                uint64_t bd = smem_desc(sB + kb * N * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
+                                mma_bf16(dt, ad, bd, C::IDESC, (d | kb | ks) != 0);
+                            }
+                        mma_commit(smem_u32(&bar_empty[s]));
+                    }
+                    __syncwarp();
+                }
+                if (lane == 0) mma_commit(smem_u32(&bar_bempty[bslot]));
                 __syncwarp();
             }
-            if (lane == 0) mma_commit(smem_u32(&bar_tfull[acc]));
+            if (lane == 0) mma_commit(smem_u32(&bar_tfull[buf]));
             __syncwarp();
         }
     } else {
-        // ------------------------------ epilogue -------------------------------
+        // ---------------- epilogue: TMEM -> registers -> global ----------------
         const int q = warp & 3;
         uint32_t lt = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
-            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
-            mbar_wait(smem_u32(&bar_tfull[acc]), aph);
+        for (int st = blockIdx.x; st < num_super; st += gridDim.x, ++lt) {
+            const uint32_t buf = lt & 1;
+            mbar_wait(smem_u32(&bar_tfull[buf]), (lt >> 1) & 1);
             tc_fence_after();
-            const int64_t row = (int64_t)tile * kTile + q * 32 + lane;
+            for (int t = 0; t < C::TPS; ++t) {
+                const int64_t row = (int64_t)st * C::SUPER + t * kTile + q * 32 + lane;
 #pragma unroll
-            for (int c0 = 0; c0 < N; c0 += 32) {
-                uint32_t v[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * N + c0, v);
-                tmem_ld_wait();
-                if (row < n_out) {
-                    if constexpr (OUT_BF16) {
-                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(out) + row * N + c0);
+                for (int c0 = 0; c0 < N; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (buf * C::TPS + t) * N + c0, v);
+                    tmem_ld_wait();
+                    if (row < n_out) {
+                        if constexpr (OUT_BF16) {
+                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(out) + row * N + c0);
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            uint32_t p[4];
+                            for (int j = 0; j < 4; ++j) {
+                                uint32_t p[4];
 #pragma unroll
-                            for (int h = 0; h < 4; ++h) {
-                                __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * h]),
-                                                                          __uint_as_float(v[8 * j + 2 * h + 1]));
-                                p[h] = *reinterpret_cast<uint32_t*>(&b2);
+                                for (int h = 0; h < 4; ++h) {
+                                    __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * h]),
+                                                                              __uint_as_float(v[8 * j + 2 * h + 1]));
+                                    p[h] = *reinterpret_cast<uint32_t*>(&b2);
+                                }
+                                dst[j] = make_uint4(p[0], p[1], p[2], p[3]);
                             }
-                            dst[j] = make_uint4(p[0], p[1], p[2], p[3]);
-                        }
-                    } else {
-                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(out) + row * N + c0);
+                        } else {
+                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(out) + row * N + c0);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            for (int j = 0; j < 8; ++j)
+                                dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        }
                     }
                 }
             }
             tc_fence_before();
-            mbar_arrive(smem_u32(&bar_tempty[acc]));
+            mbar_arrive(smem_u32(&bar_tempty[buf]));
         }
     }
+    tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == 5) {
         tc_fence_after();
         tmem_dealloc(tmem, C::TMEM_COLS);
     }
@@ -233,44 +284,61 @@ struct WgCfg {
     static constexpr int NACC = NACC0 < 8 ? NACC0 : 8;         // M-blocks (TMEM accumulators) per CTA
     static constexpr int OFFS = NACC * OPB;                    // offsets per CTA
     static constexpr int GROUPS = (27 + OFFS - 1) / OFFS;
-    static constexpr int TK = 32;                              // output rows (K) per stage
-    static constexpr int A_BLK = TK * 256;                     // one M-block: TK k-rows x 128 m bf16
+    static constexpr int TK = 32;                              // output rows (MMA K) per stage
+    static constexpr int CHUNK = 128;                          // output rows per index block
+    static constexpr int A_BLK = TK * 256;                     // one M-block: TK k-rows x 128 m (bf16)
     static constexpr int B_BYTES = TK * COUT * 2;
     static constexpr int STAGE = B_BYTES + NACC * A_BLK;
-    static constexpr int STAGES = (STAGE * 4 <= 200 * 1024) ? 4 : ((STAGE * 3 <= 216 * 1024) ? 3 : 2);
-    static constexpr int SMEM = STAGES * STAGE + 1024;
+    static constexpr int IDX_BYTES = OFFS * CHUNK * 4;
+    static constexpr int ISLOTS = 2;
+    static constexpr int FIXED = ISLOTS * IDX_BYTES + 1024;
+    static constexpr int STAGES0 = (222 * 1024 - FIXED) / STAGE;
+    static constexpr int STAGES = STAGES0 > 4 ? 4 : STAGES0;
+    static constexpr int SMEM = FIXED + STAGES * STAGE;
     static constexpr int TMEM_COLS = pow2_cols(NACC * COUT);
     static constexpr bool B_SW128 = (COUT % 64) == 0;
     static constexpr uint32_t IDESC = idesc_bf16_f32(128, COUT, true, true);
+    static_assert(STAGES >= 2, "wgrad pipeline needs >= 2 stages");
 };
 
+constexpr int kWgThreads = 320;  // warps 0-3 gather, 4 loader, 5 MMA, 6-9 epilogue
+
 template <int CIN, int COUT>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+__global__ void __launch_bounds__(kWgThreads, 1)
     k_wgrad_tc(const bf16* __restrict__ in, const bf16* __restrict__ go, const int32_t* __restrict__ nbr,
-               int64_t n_out, int64_t rows_per_split, float* __restrict__ part) {
+               int64_t ld, int64_t n_out, int64_t rows_per_split, float* __restrict__ part) {
     using C = WgCfg<CIN, COUT>;
     extern __shared__ uint8_t dsmem[];
-    __shared__ __align__(8) uint64_t bar_full[C::STAGES], bar_empty[C::STAGES], bar_tfull;
+    __shared__ __align__(8) uint64_t bar_full[C::STAGES], bar_empty[C::STAGES], bar_ifull[C::ISLOTS],
+        bar_iempty[C::ISLOTS], bar_tfull;
     __shared__ uint32_t tmem_slot;
-    const uint32_t base = (smem_u32(dsmem) + 1023u) & ~1023u;
+    const uint32_t sbase = smem_u32(dsmem);
+    const uint32_t base = (sbase + 1023u) & ~1023u;
+    const uint32_t ibase = base + C::STAGES * C::STAGE;
+    const int32_t* idx_smem = reinterpret_cast<const int32_t*>(dsmem + (ibase - sbase));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int group = blockIdx.x % C::GROUPS, split = blockIdx.x / C::GROUPS;
     const int d0 = group * C::OFFS;
     const int n_off = (27 - d0) < C::OFFS ? (27 - d0) : C::OFFS;     // offsets of this CTA
     const int n_acc = (n_off + C::OPB - 1) / C::OPB;                  // live M-blocks
-    const int64_t o_begin = (int64_t)split * rows_per_split;
+    const int64_t o_begin = (int64_t)split * rows_per_split;          // multiple of CHUNK
     const int64_t o_end = (o_begin + rows_per_split) < n_out ? (o_begin + rows_per_split) : n_out;
-    const int n_steps = o_end > o_begin ? (int)ceil_div(o_end - o_begin, C::TK) : 0;
+    const int n_chunks = o_end > o_begin ? (int)ceil_div(o_end - o_begin, C::CHUNK) : 0;
+    constexpr int SPC = C::CHUNK / C::TK;                             // stages per chunk
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(smem_u32(&bar_full[s]), 128);
             mbar_init(smem_u32(&bar_empty[s]), 1);
         }
+        for (int s = 0; s < C::ISLOTS; ++s) {
+            mbar_init(smem_u32(&bar_ifull[s]), 1);
+            mbar_init(smem_u32(&bar_iempty[s]), 128);
+        }
         mbar_init(smem_u32(&bar_tfull), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 8) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
+    if (warp == 5) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -278,44 +346,55 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
     if (warp < 4) {
         const int pt = threadIdx.x;
-        const int a_rows = n_off * C::TK;
-        for (int step = 0; step < n_steps; ++step) {
-            const uint32_t s = step % C::STAGES, ph = (step / C::STAGES) & 1;
-            const int64_t o0 = o_begin + (int64_t)step * C::TK;
-            mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
-            const uint32_t sB = base + s * C::STAGE, sA = sB + C::B_BYTES;
-            for (int t = pt; t < a_rows + C::TK; t += 128) {
-                if (t < a_rows) {
-                    const int u = t / C::TK, r = t % C::TK;
-                    const int64_t o = o0 + r;
-                    const int32_t i = o < o_end ? __ldg(nbr + (int64_t)(d0 + u) * n_out + o) : -1;
-                    const int a = u / C::OPB, m0 = (u % C::OPB) * CIN;
-                    const bf16* src = in + (int64_t)(i < 0 ? 0 : i) * CIN;
-#pragma unroll
-                    for (int c = 0; c < CIN / 8; ++c) {
-                        const int m = m0 + c * 8;
-                        const uint32_t dst = sA + a * C::A_BLK + (m >> 6) * (C::TK * 128) + swz_off(r, (m & 63) >> 3, 128);
-                        cp_async_16(dst, src + c * 8, i < 0 ? 0u : 16u);
-                    }
-                } else {
-                    const int r = t - a_rows;
+        constexpr int ACH = CIN / 8, BCH = COUT / 8;                  // 16-B chunks per row
+        const int a_items = n_off * C::TK * ACH;
+        uint32_t it = 0;
+        for (int ch = 0; ch < n_chunks; ++ch) {
+            const uint32_t islot = ch % C::ISLOTS;
+            mbar_wait(smem_u32(&bar_ifull[islot]), (ch / C::ISLOTS) & 1);
+            const int32_t* ib = idx_smem + islot * (C::OFFS * C::CHUNK);
+            for (int sub = 0; sub < SPC; ++sub, ++it) {
+                const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
+                const int64_t o0 = o_begin + (int64_t)ch * C::CHUNK + sub * C::TK;
+                mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+                const uint32_t sB = base + s * C::STAGE, sA = sB + C::B_BYTES;
+                for (int i = pt; i < a_items; i += 128) {
+                    const int task = i / ACH, c = i % ACH;
+                    const int u = task / C::TK, r = task % C::TK;
+                    const int32_t idx = ib[u * C::CHUNK + sub * C::TK + r];
+                    const int a = u / C::OPB, m = (u % C::OPB) * CIN + c * 8;
+                    const uint32_t dst = sA + a * C::A_BLK + (m >> 6) * (C::TK * 128) + swz_off(r, (m & 63) >> 3, 128);
+                    cp_async_16(dst, in + (int64_t)(idx < 0 ? 0 : idx) * CIN + c * 8, idx < 0 ? 0u : 16u);
+                }
+                for (int i = pt; i < C::TK * BCH; i += 128) {
+                    const int r = i / BCH, c = i % BCH;
                     const int64_t o = o0 + r;
                     const bool ok = o < o_end;
-                    const bf16* src = go + (ok ? o : 0) * COUT;
-#pragma unroll
-                    for (int c = 0; c < COUT / 8; ++c) {
-                        uint32_t dst;
-                        if constexpr (C::B_SW128)
-                            dst = sB + (c >> 3) * (C::TK * 128) + swz_off(r, c & 7, 128);
-                        else
-                            dst = sB + swz_off(r, c, 64);
-                        cp_async_16(dst, src + c * 8, ok ? 16u : 0u);
-                    }
+                    uint32_t dst;
+                    if constexpr (C::B_SW128)
+                        dst = sB + (c >> 3) * (C::TK * 128) + swz_off(r, c & 7, 128);
+                    else
+                        dst = sB + swz_off(r, c, 64);
+                    cp_async_16(dst, go + (ok ? o : 0) * COUT + c * 8, ok ? 16u : 0u);
                 }
+                cp_async_arrive_noinc(smem_u32(&bar_full[s]));
             }
-            cp_async_arrive_noinc(smem_u32(&bar_full[s]));
+            mbar_arrive(smem_u32(&bar_iempty[islot]));
         }
-    } else if (warp == 8) {
+    } else if (warp == 4) {
+        if (lane == 0) {
+            for (int ch = 0; ch < n_chunks; ++ch) {
+                const uint32_t islot = ch % C::ISLOTS;
+                mbar_wait(smem_u32(&bar_iempty[islot]), ((ch / C::ISLOTS) & 1) ^ 1);
+                const uint32_t fb = smem_u32(&bar_ifull[islot]);
+                mbar_arrive_expect_tx(fb, n_off * C::CHUNK * 4);
+                for (int u = 0; u < n_off; ++u)
+                    bulk_g2s(ibase + islot * C::IDX_BYTES + u * C::CHUNK * 4,
+                             nbr + (int64_t)(d0 + u) * ld + o_begin + (int64_t)ch * C::CHUNK, C::CHUNK * 4, fb);
+            }
+        }
+    } else if (warp == 5) {
+        const int n_steps = n_chunks * SPC;
         for (int step = 0; step < n_steps; ++step) {
             const uint32_t s = step % C::STAGES, ph = (step / C::STAGES) & 1;
             mbar_wait(smem_u32(&bar_full[s]), ph);
@@ -336,28 +415,28 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
             __syncwarp();
         }
-        if (lane == 0) mma_commit(smem_u32(&bar_tfull));
+        if (lane == 0 && n_steps > 0) mma_commit(smem_u32(&bar_tfull));
         __syncwarp();
     } else {
         const int q = warp & 3;
         const int m = q * 32 + lane;
-        if (n_steps > 0) {
+        if (n_chunks > 0) {
             mbar_wait(smem_u32(&bar_tfull), 0);
             tc_fence_after();
         }
         for (int a = 0; a < n_acc; ++a) {
-            const int d = d0 + a * C::OPB + m / CIN, ci = m % CIN;
+            const int u = a * C::OPB + m / CIN, ci = m % CIN;
             for (int c0 = 0; c0 < COUT; c0 += 32) {
                 uint32_t v[32];
-                if (n_steps > 0) {
+                if (n_chunks > 0) {
                     tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + a * COUT + c0, v);
                     tmem_ld_wait();
                 } else {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = 0u;
                 }
-                if (d < 27 && a * C::OPB + m / CIN < n_off) {
-                    uint4* dst = reinterpret_cast<uint4*>(part + (((int64_t)split * 27 + d) * CIN + ci) * COUT + c0);
+                if (u < n_off) {
+                    uint4* dst = reinterpret_cast<uint4*>(part + (((int64_t)split * 27 + d0 + u) * CIN + ci) * COUT + c0);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                 }
@@ -366,7 +445,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == 5) {
         tc_fence_after();
         tmem_dealloc(tmem, C::TMEM_COLS);
     }
@@ -394,36 +473,34 @@ int sm_count() {
 }
 
 template <int K, int N, bool OB>
-int launch_fwd(const void* in, const void* wimg, const int32_t* nbr, int64_t n_out, void* out, cudaStream_t st) {
+int launch_fwd(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
+               cudaStream_t st) {
     using C = FwdCfg<K, N>;
     auto kern = k_conv_fwd_tc<K, N, OB>;
     FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    int occ = 1;
-    FVDB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreadsTC, C::SMEM));
-    if (occ < 1) occ = 1;
-    const int tiles = (int)ceil_div(n_out, kTile);
-    int grid = sm_count() * occ;
-    if (grid > tiles) grid = tiles;
-    kern<<<grid, kThreadsTC, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, nbr, n_out, out, tiles);
+    const int supers = (int)ceil_div(n_out, C::SUPER);
+    int grid = sm_count();
+    if (grid > supers) grid = supers;
+    kern<<<grid, kFwdThreads, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, nbr, ld, n_out, out, supers);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
 
 template <int K, int N>
-int dispatch_out(const void* in, const void* wimg, const int32_t* nbr, int64_t n_out, void* out, int out_dtype,
-                 cudaStream_t st) {
-    if (out_dtype == FVDB_DTYPE_BF16) return launch_fwd<K, N, true>(in, wimg, nbr, n_out, out, st);
-    if (out_dtype == FVDB_DTYPE_F32) return launch_fwd<K, N, false>(in, wimg, nbr, n_out, out, st);
+int dispatch_out(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
+                 int out_dtype, cudaStream_t st) {
+    if (out_dtype == FVDB_DTYPE_BF16) return launch_fwd<K, N, true>(in, wimg, nbr, ld, n_out, out, st);
+    if (out_dtype == FVDB_DTYPE_F32) return launch_fwd<K, N, false>(in, wimg, nbr, ld, n_out, out, st);
     return FVDB_ERR_INVALID;
 }
 
 template <int K>
-int dispatch_n(int N, const void* in, const void* wimg, const int32_t* nbr, int64_t n_out, void* out, int od,
-               cudaStream_t st) {
+int dispatch_n(int N, const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
+               int od, cudaStream_t st) {
     switch (N) {
-        case 32: return dispatch_out<K, 32>(in, wimg, nbr, n_out, out, od, st);
-        case 64: return dispatch_out<K, 64>(in, wimg, nbr, n_out, out, od, st);
-        case 128: return dispatch_out<K, 128>(in, wimg, nbr, n_out, out, od, st);
+        case 32: return dispatch_out<K, 32>(in, wimg, nbr, ld, n_out, out, od, st);
+        case 64: return dispatch_out<K, 64>(in, wimg, nbr, ld, n_out, out, od, st);
+        case 128: return dispatch_out<K, 128>(in, wimg, nbr, ld, n_out, out, od, st);
         default: return FVDB_ERR_INVALID;
     }
 }
@@ -434,21 +511,23 @@ struct WgLaunch {
     static int splits_for(int64_t n_out) {
         int s = sm_count() / C::GROUPS;
         if (s < 1) s = 1;
-        int64_t max_s = ceil_div(n_out > 0 ? n_out : 1, (int64_t)C::TK * 4);
+        int64_t max_s = ceil_div(n_out > 0 ? n_out : 1, (int64_t)C::CHUNK * 2);
         if (s > max_s) s = (int)max_s;
         return s;
     }
-    static int run(const void* in, const void* go, const int32_t* nbr, int64_t n_out, float* gw, void* ws,
+    static int run(const void* in, const void* go, const int32_t* nbr, int64_t ld, int64_t n_out, float* gw, void* ws,
                    size_t ws_bytes, cudaStream_t st) {
         const int splits = splits_for(n_out);
         const size_t need = (size_t)splits * 27 * CIN * COUT * sizeof(float);
         if (ws_bytes < need) return FVDB_ERR_WORKSPACE;
+        if (ld % FVDB_NBR_ALIGN != 0 || ld < n_out) return FVDB_ERR_INVALID;
         float* part = (float*)ws;
         int64_t rps = ceil_div(n_out > 0 ? n_out : 1, splits);
-        rps = ceil_div(rps, C::TK) * C::TK;
+        rps = ceil_div(rps, C::CHUNK) * C::CHUNK;
         auto kern = k_wgrad_tc<CIN, COUT>;
         FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        kern<<<splits * C::GROUPS, kThreadsTC, C::SMEM, st>>>((const bf16*)in, (const bf16*)go, nbr, n_out, rps, part);
+        kern<<<splits * C::GROUPS, kWgThreads, C::SMEM, st>>>((const bf16*)in, (const bf16*)go, nbr, ld, n_out, rps,
+                                                              part);
         k_wgrad_tc_reduce<<<(unsigned)ceil_div((int64_t)27 * CIN * COUT, 256), 256, 0, st>>>(part, splits, CIN, COUT, gw);
         FVDB_LAUNCH_CHECK();
         return FVDB_OK;
@@ -482,14 +561,16 @@ extern "C" int fvdb_pack_weights_umma(const float* w, int cout, int cin, int tra
 }
 
 extern "C" int fvdb_conv_gather_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
-                                   const int32_t* nbr, int64_t n_out, void* out, int out_dtype, void* stream) {
+                                   const int32_t* nbr, int64_t ld, int64_t n_out, void* out, int out_dtype,
+                                   void* stream) {
     (void)n_in;
     if (n_out == 0) return FVDB_OK;
+    if (ld % FVDB_NBR_ALIGN != 0 || ld < n_out) return FVDB_ERR_INVALID;
     cudaStream_t st = as_stream(stream);
     switch (K) {
-        case 32: return dispatch_n<32>(N, in_bf16, w_image, nbr, n_out, out, out_dtype, st);
-        case 64: return dispatch_n<64>(N, in_bf16, w_image, nbr, n_out, out, out_dtype, st);
-        case 128: return dispatch_n<128>(N, in_bf16, w_image, nbr, n_out, out, out_dtype, st);
+        case 32: return dispatch_n<32>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st);
+        case 64: return dispatch_n<64>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st);
+        case 128: return dispatch_n<128>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st);
         default: return FVDB_ERR_INVALID;
     }
 }
@@ -504,11 +585,11 @@ extern "C" size_t fvdb_wgrad_tc_workspace_bytes(int64_t n_out, int cin, int cout
 }
 
 extern "C" int fvdb_conv_wgrad_tc(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,
-                                  const int32_t* nbr, int64_t n_out, float* gw, void* ws, size_t ws_bytes,
-                                  void* stream) {
+                                  const int32_t* nbr, int64_t ld, int64_t n_out, float* gw, void* ws,
+                                  size_t ws_bytes, void* stream) {
     (void)n_in;
     cudaStream_t st = as_stream(stream);
     return wg_dispatch(cin, cout, [&](auto L) {
-        return decltype(L)::run(in_bf16, go_bf16, nbr, n_out, gw, ws, ws_bytes, st);
+        return decltype(L)::run(in_bf16, go_bf16, nbr, ld, n_out, gw, ws, ws_bytes, st);
     });
 }

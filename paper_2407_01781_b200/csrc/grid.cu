@@ -92,7 +92,7 @@ __global__ void k_neighbor_leaves(fvdb_grid_view gin, fvdb_grid_view gout, int s
 // CTA per output leaf: 27 probes per active voxel against staged neighbour-leaf masks
 __global__ void __launch_bounds__(kThreads) k_kernel_map(fvdb_grid_view gin, fvdb_grid_view gout, int stride,
                                                          const int32_t* __restrict__ nleaf,
-                                                         int32_t* __restrict__ nbr, int64_t n_out,
+                                                         int32_t* __restrict__ nbr, int64_t ld,
                                                          unsigned long long* __restrict__ pair_counts) {
     __shared__ uint64_t s_mask[27][8];
     __shared__ uint64_t s_pre[27];
@@ -144,42 +144,49 @@ __global__ void __launch_bounds__(kThreads) k_kernel_map(fvdb_grid_view gin, fvd
                 atomicAdd(&s_cnt[d], 1);
             }
         }
-        nbr[(int64_t)d * n_out + row0 + r] = row;
+        nbr[(int64_t)d * ld + row0 + r] = row;
     }
     __syncthreads();
     if (tid < 27 && s_cnt[tid]) atomicAdd(&pair_counts[tid], (unsigned long long)s_cnt[tid]);
 }
 
-__global__ void k_flags(const int32_t* __restrict__ nbr, int64_t n, int* __restrict__ flags) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+// padding columns [n_out, ld) of every offset row := -1
+__global__ void k_pad(int32_t* __restrict__ nbr, int64_t ld, int64_t n_out) {
+    const int64_t w = ld - n_out;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 27 * w;
          t += (int64_t)gridDim.x * blockDim.x)
-        flags[t] = nbr[t] >= 0;
+        nbr[(t / w) * ld + n_out + (t % w)] = -1;
 }
 
-__global__ void k_compact(const int32_t* __restrict__ nbr, int64_t n_out, const int* __restrict__ pos,
-                          int64_t* __restrict__ in_rows, int64_t* __restrict__ out_rows) {
-    const int64_t total = 27 * n_out;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+__global__ void k_flags(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out, int* __restrict__ flags) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 27 * n_out;
          t += (int64_t)gridDim.x * blockDim.x) {
-        int32_t v = nbr[t];
+        int64_t d = t / n_out;
+        flags[t] = nbr[d * ld + (t - d * n_out)] >= 0;
+    }
+}
+
+__global__ void k_compact(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out, const int* __restrict__ pos,
+                          int64_t* __restrict__ in_rows, int64_t* __restrict__ out_rows) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 27 * n_out;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t d = t / n_out, o = t - d * n_out;
+        int32_t v = nbr[d * ld + o];
         if (v >= 0) {
             int p = pos[t];
             in_rows[p] = v;
-            out_rows[p] = t % n_out;
+            out_rows[p] = o;
         }
     }
 }
 
-__global__ void k_transpose(const int32_t* __restrict__ nbr, int64_t n_out, int64_t n_in,
-                            int32_t* __restrict__ nbrT) {
-    const int64_t total = 27 * n_out;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+__global__ void k_transpose(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out, int32_t* __restrict__ nbrT,
+                            int64_t ldT) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 27 * n_out;
          t += (int64_t)gridDim.x * blockDim.x) {
-        int32_t v = nbr[t];
-        if (v >= 0) {
-            int64_t d = t / n_out;
-            nbrT[d * n_in + v] = (int32_t)(t - d * n_out);
-        }
+        int64_t d = t / n_out, o = t - d * n_out;
+        int32_t v = nbr[d * ld + o];
+        if (v >= 0) nbrT[d * ldT + v] = (int32_t)o;
     }
 }
 
@@ -223,16 +230,19 @@ extern "C" size_t fvdb_kmap_workspace_bytes(int64_t num_leaf_out) {
 }
 
 extern "C" int fvdb_kernel_map(const fvdb_grid_view* gin, const fvdb_grid_view* gout, int stride, int32_t* nbr,
-                               int64_t* pair_counts, void* ws, size_t ws_bytes, void* stream_) {
+                               int64_t ld, int64_t* pair_counts, void* ws, size_t ws_bytes, void* stream_) {
     cudaStream_t st = as_stream(stream_);
     if (stride != 1 && stride != 2) return FVDB_ERR_INVALID;
+    if (ld < gout->num_voxels) return FVDB_ERR_INVALID;
     if (ws_bytes < fvdb_kmap_workspace_bytes(gout->num_leaf)) return FVDB_ERR_WORKSPACE;
     FVDB_CUDA_TRY(cudaMemsetAsync(pair_counts, 0, 27 * sizeof(int64_t), st));
+    if (ld > gout->num_voxels)
+        k_pad<<<grid_for(27 * (ld - gout->num_voxels)), kThreads, 0, st>>>(nbr, ld, gout->num_voxels);
     if (gout->num_leaf == 0) return FVDB_OK;
     int32_t* nleaf = reinterpret_cast<int32_t*>(ws);
     k_neighbor_leaves<<<grid_for(gout->num_leaf * 27), kThreads, 0, st>>>(*gin, *gout, stride, nleaf);
     k_kernel_map<<<(unsigned)gout->num_leaf, kThreads, 0, st>>>(
-        *gin, *gout, stride, nleaf, nbr, gout->num_voxels, reinterpret_cast<unsigned long long*>(pair_counts));
+        *gin, *gout, stride, nleaf, nbr, ld, reinterpret_cast<unsigned long long*>(pair_counts));
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
@@ -244,7 +254,7 @@ extern "C" size_t fvdb_kmap_compact_workspace_bytes(int64_t n_out) {
     return 2 * (size_t)n * sizeof(int) + tb + 1024;
 }
 
-extern "C" int fvdb_kmap_compact(const int32_t* nbr, int64_t n_out, int64_t* in_rows, int64_t* out_rows,
+extern "C" int fvdb_kmap_compact(const int32_t* nbr, int64_t ld, int64_t n_out, int64_t* in_rows, int64_t* out_rows,
                                  void* ws, size_t ws_bytes, void* stream_) {
     cudaStream_t st = as_stream(stream_);
     if (n_out == 0) return FVDB_OK;
@@ -258,19 +268,20 @@ extern "C" int fvdb_kmap_compact(const int32_t* nbr, int64_t n_out, int64_t* in_
     cub::DeviceScan::ExclusiveSum(nullptr, tb, (int*)nullptr, (int*)nullptr, (int)n);
     void* tmp = c.take<char>(tb);
     if (!c.ok()) return FVDB_ERR_WORKSPACE;
-    k_flags<<<grid_for(n), kThreads, 0, st>>>(nbr, n, flags);
+    k_flags<<<grid_for(n), kThreads, 0, st>>>(nbr, ld, n_out, flags);
     FVDB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flags, pos, (int)n, st));
-    k_compact<<<grid_for(n), kThreads, 0, st>>>(nbr, n_out, pos, in_rows, out_rows);
+    k_compact<<<grid_for(n), kThreads, 0, st>>>(nbr, ld, n_out, pos, in_rows, out_rows);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
 
-extern "C" int fvdb_kmap_transpose(const int32_t* nbr, int64_t n_out, int64_t n_in, int32_t* nbrT,
-                                   void* stream_) {
+extern "C" int fvdb_kmap_transpose(const int32_t* nbr, int64_t ld, int64_t n_out, int64_t n_in, int32_t* nbrT,
+                                   int64_t ldT, void* stream_) {
     cudaStream_t st = as_stream(stream_);
-    if (n_in > 0) FVDB_CUDA_TRY(cudaMemsetAsync(nbrT, 0xFF, (size_t)27 * n_in * sizeof(int32_t), st));
+    if (ldT < n_in || ld < n_out) return FVDB_ERR_INVALID;
+    if (ldT > 0) FVDB_CUDA_TRY(cudaMemsetAsync(nbrT, 0xFF, (size_t)27 * ldT * sizeof(int32_t), st));
     if (n_out == 0 || n_in == 0) return FVDB_OK;
-    k_transpose<<<grid_for(27 * n_out), kThreads, 0, st>>>(nbr, n_out, n_in, nbrT);
+    k_transpose<<<grid_for(27 * n_out), kThreads, 0, st>>>(nbr, ld, n_out, nbrT, ldT);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

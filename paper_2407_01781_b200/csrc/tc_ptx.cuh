@@ -33,8 +33,11 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t n = 0;
     while (!mbar_try_wait(bar, parity)) {
+        if (++n == (1u << 24)) asm volatile("trap;");
     }
 }
 

@@ -29,10 +29,10 @@ class _SparseConvFn(torch.autograd.Function):
     def forward(ctx, x, w, kmap, transposed, cdt):
         xc = x.to(cdt).contiguous()
         if transposed:
-            y = gather_conv(xc, kmap.transposed_table(), w, transpose=True, out_dtype=cdt)
+            y = gather_conv(xc, kmap.bwd, w, transpose=True, out_dtype=cdt)
         else:
             img = pack_weights_umma(w, False) if cdt == torch.bfloat16 and _tc_ok(w) else None
-            y = gather_conv(xc, kmap.nbr, w, transpose=False, out_dtype=cdt, w_image=img)
+            y = gather_conv(xc, kmap.fwd, w, transpose=False, out_dtype=cdt, w_image=img)
         ctx.save_for_backward(xc, w)
         ctx.kmap, ctx.transposed, ctx.cdt, ctx.x_dtype = kmap, transposed, cdt, x.dtype
         return y
@@ -45,14 +45,14 @@ class _SparseConvFn(torch.autograd.Function):
         gx = gw = None
         if ctx.transposed:
             if ctx.needs_input_grad[0]:
-                gx = gather_conv(gy, km.nbr, w, transpose=False, out_dtype=cdt)
+                gx = gather_conv(gy, km.fwd, w, transpose=False, out_dtype=cdt)
             if ctx.needs_input_grad[1]:
-                gw = wgrad(gy, xc, km.nbr)
+                gw = wgrad(gy, xc, km.fwd)
         else:
             if ctx.needs_input_grad[0]:
-                gx = gather_conv(gy, km.transposed_table(), w, transpose=True, out_dtype=cdt)
+                gx = gather_conv(gy, km.bwd, w, transpose=True, out_dtype=cdt)
             if ctx.needs_input_grad[1]:
-                gw = wgrad(xc, gy, km.nbr)
+                gw = wgrad(xc, gy, km.fwd)
         if gx is not None:
             gx = gx.to(ctx.x_dtype)
         if gw is not None:

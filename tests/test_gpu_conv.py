@@ -178,19 +178,19 @@ def test_tc_forward_dgrad_wgrad(shell, cin, cout):
     # forward
     ref_r = O.conv_igemm(xr, wr, ins, outs, n)
     ref = O.conv_igemm(x.astype(np.float64), w.astype(np.float64), ins, outs, n)
-    y32 = gather_conv(xb, km.nbr, wt, out_dtype=torch.float32)
+    y32 = gather_conv(xb, km.fwd, wt, out_dtype=torch.float32)
     assert rel(y32, ref_r) < 2e-5
-    y16 = gather_conv(xb, km.nbr, wt)
+    y16 = gather_conv(xb, km.fwd, wt)
     assert y16.dtype == torch.bfloat16
     assert rel(y16, ref) < 1e-2
     # dgrad
     gi_r, gw_r = O.conv_backward(ins, outs, gyr, xr, wr)
-    gi32 = gather_conv(gyb, km.transposed_table(), wt, transpose=True, out_dtype=torch.float32)
+    gi32 = gather_conv(gyb, km.bwd, wt, transpose=True, out_dtype=torch.float32)
     assert rel(gi32, gi_r) < 2e-5
     gi_ref, gw_ref = O.conv_backward(ins, outs, gy.astype(np.float64), x.astype(np.float64), w.astype(np.float64))
-    assert rel(gather_conv(gyb, km.transposed_table(), wt, transpose=True), gi_ref) < 1e-2
+    assert rel(gather_conv(gyb, km.bwd, wt, transpose=True), gi_ref) < 1e-2
     # wgrad
-    gw = wgrad(xb, gyb, km.nbr)
+    gw = wgrad(xb, gyb, km.fwd)
     assert gw.dtype == torch.float32 and tuple(gw.shape) == (cout, cin, 3, 3, 3)
     assert rel(gw, gw_r) < 2e-5
     assert rel(gw, gw_ref) < 1e-2
@@ -202,10 +202,10 @@ def test_tc_deterministic(shell):
     xb = torch.from_numpy(rng.normal(size=(g.num_voxels, 64)).astype(np.float32)).cuda().to(torch.bfloat16)
     gyb = torch.from_numpy(rng.normal(size=(g.num_voxels, 64)).astype(np.float32)).cuda().to(torch.bfloat16)
     w = torch.randn(64, 64, 3, 3, 3, device="cuda")
-    a = gather_conv(xb, km.nbr, w, out_dtype=torch.float32)
-    b = gather_conv(xb, km.nbr, w, out_dtype=torch.float32)
+    a = gather_conv(xb, km.fwd, w, out_dtype=torch.float32)
+    b = gather_conv(xb, km.fwd, w, out_dtype=torch.float32)
     assert torch.equal(a, b)
-    assert torch.equal(wgrad(xb, gyb, km.nbr), wgrad(xb, gyb, km.nbr))
+    assert torch.equal(wgrad(xb, gyb, km.fwd), wgrad(xb, gyb, km.fwd))
 
 
 def test_tc_unaligned_channels_pad(shell):
@@ -317,9 +317,9 @@ def test_cfg2_full_size_tc_vs_torch_fp64():
     wr = w.to(torch.bfloat16).double()
     xd, gyd = x.double(), gy.double()
     nbr = km.nbr.long()
-    y = gather_conv(x, km.nbr, w, out_dtype=torch.float32)
-    gi = gather_conv(gy, km.transposed_table(), w, transpose=True, out_dtype=torch.float32)
-    gw = wgrad(x, gy, km.nbr)
+    y = gather_conv(x, km.fwd, w, out_dtype=torch.float32)
+    gi = gather_conv(gy, km.bwd, w, transpose=True, out_dtype=torch.float32)
+    gw = wgrad(x, gy, km.fwd)
     ref_y = torch.zeros(n, 64, dtype=torch.float64, device="cuda")
     ref_gi = torch.zeros_like(ref_y)
     ref_gw = torch.zeros(64, 64, 27, dtype=torch.float64, device="cuda")
