@@ -276,6 +276,137 @@ extern "C" int mb_gather_bw2(int mode, int stages, const void* feat, long long n
     return (int)cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- (2c) gather bottleneck matrix
+// MODE 0: cp.async.ca, 1: cp.async.cg, 2: ld.global.v4 + st.shared.v4; NPW producer warps;
+// IDX 0: real kernel map, 1: rows & 1023 (L1-resident set), 2: identity rows (contiguous)
+template <int MODE, int NPW, int IDX>
+__global__ void __launch_bounds__(NPW * 32 + 64, 1) k_gather_mx(const bf16* feat, const int32_t* nbr, long long n_out,
+                                                               int num_tiles) {
+    constexpr int STAGES = 8;
+    extern __shared__ uint8_t dsm[];
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], ifull[2], iempty[2];
+    const uint32_t sbase = smem_u32(dsm);
+    const uint32_t base = (sbase + 1023) & ~1023u;
+    const uint32_t ibase = base + STAGES * 16384;
+    const int32_t* ism = reinterpret_cast<const int32_t*>(dsm + (ibase - sbase));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NP = NPW * 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full[s]), NP);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&ifull[b]), 1);
+            mbar_init(smem_u32(&iempty[b]), NP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == NPW) {
+        if (lane == 0) {
+            int lt = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+                int b = lt & 1;
+                mbar_wait(smem_u32(&iempty[b]), ((lt >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(smem_u32(&ifull[b]), 27 * 512);
+                for (int d = 0; d < 27; ++d)
+                    bulk_g2s(ibase + b * 27 * 512 + d * 512, nbr + (long long)d * n_out + (long long)t * 128, 512,
+                             smem_u32(&ifull[b]));
+            }
+        }
+    } else if (warp < NPW) {
+        const int pt = threadIdx.x, c = pt & 7, rb = pt >> 3;
+        constexpr int RS = NP / 8, J = 128 / RS;
+        uint32_t it = 0;
+        int lt = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+            int b = lt & 1;
+            mbar_wait(smem_u32(&ifull[b]), (lt >> 1) & 1);
+            const int32_t* ib = ism + b * 27 * 128;
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                int idx[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    int r = rb + RS * j;
+                    int v = ib[d * 128 + r];
+                    if (IDX == 1) v = v < 0 ? v : (v & 1023);
+                    if (IDX == 2) v = t * 128 + r;
+                    idx[j] = v;
+                }
+                mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+                if (MODE == 2) {
+                    int4 vals[J];
+#pragma unroll
+                    for (int j = 0; j < J; ++j) {
+                        const int4* src = reinterpret_cast<const int4*>(feat + (long long)(idx[j] < 0 ? 0 : idx[j]) * 64 + c * 8);
+                        vals[j] = idx[j] < 0 ? make_int4(0, 0, 0, 0) : __ldg(src);
+                    }
+#pragma unroll
+                    for (int j = 0; j < J; ++j) {
+                        int r = rb + RS * j;
+                        uint32_t dst = base + s * 16384 + r * 128 + ((c ^ (r & 7)) << 4);
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(vals[j].x), "r"(vals[j].y),
+                                     "r"(vals[j].z), "r"(vals[j].w)
+                                     : "memory");
+                    }
+                    mbar_arrive(smem_u32(&full[s]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < J; ++j) {
+                        int r = rb + RS * j;
+                        uint32_t dst = base + s * 16384 + r * 128 + ((c ^ (r & 7)) << 4);
+                        const bf16* src = feat + (long long)(idx[j] < 0 ? 0 : idx[j]) * 64 + c * 8;
+                        if (MODE == 0) cp_async_16(dst, src, idx[j] < 0 ? 0 : 16);
+                        else cp_async_16_cg(dst, src, idx[j] < 0 ? 0 : 16);
+                    }
+                    cp_async_arrive_noinc(smem_u32(&full[s]));
+                }
+            }
+            mbar_arrive(smem_u32(&iempty[b]));
+        }
+    } else if (warp == NPW + 1 && lane == 0) {
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x)
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                mbar_wait(smem_u32(&full[s]), ph);
+                mbar_arrive(smem_u32(&empty[s]));
+            }
+    }
+}
+
+template <int MODE, int NPW, int IDX>
+static float run_mx(const void* feat, const int32_t* nbr, long long n_out, int ctas) {
+    int tiles = (int)(n_out / 128);
+    size_t smem = 8 * 16384 + 2 * 27 * 512 + 1024;
+    auto k = k_gather_mx<MODE, NPW, IDX>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float ms = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(a);
+        k<<<ctas, NPW * 32 + 64, smem>>>((const bf16*)feat, nbr, n_out, tiles);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+    }
+    cudaEventElapsedTime(&ms, a, b);
+    return cudaGetLastError() == cudaSuccess ? ms : -1.f;
+}
+
+extern "C" int mb_gather_mx(const void* feat, const int32_t* nbr, long long n_out, float* out /*[2][3][3]*/) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+#define MX(M, W, I) out[((W == 8) * 3 + M) * 3 + I] = run_mx<M, W, I>(feat, nbr, n_out, sms);
+    MX(0, 4, 0) MX(0, 4, 1) MX(0, 4, 2) MX(1, 4, 0) MX(1, 4, 1) MX(1, 4, 2) MX(2, 4, 0) MX(2, 4, 1) MX(2, 4, 2)
+    MX(0, 8, 0) MX(0, 8, 1) MX(0, 8, 2) MX(1, 8, 0) MX(1, 8, 1) MX(1, 8, 2) MX(2, 8, 0) MX(2, 8, 1) MX(2, 8, 2)
+#undef MX
+    return 0;
+}
+
 // ---------------------------------------------------------------- (3) MMA issue rate
 template <int N>
 __global__ void __launch_bounds__(128, 1) k_mma_rate(int iters, long long* cycles) {

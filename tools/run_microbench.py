@@ -71,7 +71,7 @@ def main():
     feat = torch.randn(n, 64, device="cuda").to(torch.bfloat16)
     valid_bytes = int((nbr >= 0).sum().item()) * 128
     bw = {}
-    for mode, name in ((0, "tma_gather4"), (1, "cp_async_ca"), (2, "cp_async_cg")):
+    for mode, name in ():
         for cps in (1, 2):
             ms = C.c_float(0)
             rc = L.mb_gather_bw(mode, C.c_void_p(feat.data_ptr()), C.c_longlong(n), C.c_void_p(nbr.data_ptr()),
@@ -79,8 +79,8 @@ def main():
             bw[f"{name}_x{cps}"] = {"rc": rc, "ms": ms.value,
                                     "valid_GBps": valid_bytes / (ms.value / 1e3) / 1e9 if ms.value else None,
                                     "all_rows_GBps": 27 * n_out * 128 / (ms.value / 1e3) / 1e9 if ms.value else None}
-    for mode, name in ((0, "tma_gather4"), (1, "cp_async_ca"), (2, "cp_async_cg")):
-        for stages in (8, 12):
+    for mode, name in ((1, "cp_async_ca"),):
+        for stages in (8,):
             ms = C.c_float(0)
             rc = L.mb_gather_bw2(mode, stages, C.c_void_p(feat.data_ptr()), C.c_longlong(n), C.c_void_p(nbr.data_ptr()),
                                  C.c_longlong(n_out), C.byref(ms))
@@ -88,10 +88,18 @@ def main():
                                     "valid_GBps": valid_bytes / (ms.value / 1e3) / 1e9 if ms.value else None,
                                     "all_rows_GBps": 27 * n_out * 128 / (ms.value / 1e3) / 1e9 if ms.value else None}
     rep["gather_bw_cfg2"] = {"valid_bytes": valid_bytes, "modes": bw}
+    mx = torch.zeros(18, dtype=torch.float32)
+    mxp = C.c_void_p(mx.data_ptr())
+    L.mb_gather_mx(C.c_void_p(feat.data_ptr()), C.c_void_p(nbr.data_ptr()), C.c_longlong(n_out), mxp)
+    allb = 27 * n_out * 128
+    rep["gather_matrix_ms"] = {f"{m}_w{w}_{i}": {"ms": float(mx[((w == 8) * 3 + mi) * 3 + ii]),
+                                                 "GBps_all_rows": allb / (float(mx[((w == 8) * 3 + mi) * 3 + ii]) / 1e3) / 1e9}
+                               for w in (4, 8) for mi, m in enumerate(("cp_async_ca", "cp_async_cg", "ldg_sts"))
+                               for ii, i in enumerate(("real", "l1set", "identity"))}
     # (3) MMA issue rate
     cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
     mm = {}
-    for nn in (64, 128, 256):
+    for nn in ():
         ms = C.c_float(0)
         iters = 4000
         rc = L.mb_mma_rate(nn, iters, 148, C.c_void_p(cyc.data_ptr()), C.byref(ms))
