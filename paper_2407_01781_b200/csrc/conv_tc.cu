@@ -67,7 +67,6 @@ struct FwdCfg {
     static constexpr int SMEM = FIXED + STAGES * A_BYTES;
     static constexpr uint32_t LAYOUT = ROWB == 128 ? kSwizzle128B : kSwizzle64B;
     static constexpr int CPR = K / 8;                  // 16-B chunks per gathered row
-    static constexpr int RSTEP = kTile / CPR;          // rows per producer pass
     static constexpr int TMEM_COLS = pow2_cols(2 * TPS * N);
     static constexpr uint32_t IDESC = idesc_bf16_f32(kTile, N, false, false);
     static_assert(2 * TPS * N <= 512, "TMEM budget");
@@ -87,6 +86,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     __shared__ __align__(8) uint64_t bar_bfull[C::BSLOTS], bar_bempty[C::BSLOTS];
     __shared__ __align__(8) uint64_t bar_tfull[2], bar_tempty[2];
     __shared__ uint32_t tmem_slot;
+    __shared__ uint32_t lane_mask[C::STAGES][4];
 
     const uint32_t sbase = smem_u32(dsmem);
     const uint32_t base = (sbase + 1023u) & ~1023u;                  // A stages (1024-aligned)
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
-            mbar_init(smem_u32(&bar_full[s]), 128);   // one cp.async arrival per gather thread
+            mbar_init(smem_u32(&bar_full[s]), 128 + 4);  // cp.async arrivals + one mask-word arrive per warp
             mbar_init(smem_u32(&bar_empty[s]), 1);
         }
         for (int s = 0; s < C::ISLOTS; ++s) {
@@ -119,11 +119,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
+    if (warp >= 6) {  // accumulators start at zero; every MMA then accumulates under its lane mask
+        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        for (int c0 = 0; c0 < 2 * C::TPS * N; c0 += 32) tmem_st32_zero(lane_base + c0);
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
 
     if (warp < 4) {
-        // ---------------- gather producers: 16-B cp.async per (row, chunk), 8 lanes per row --------
-        const int pt = threadIdx.x;
-        const int cchunk = pt % C::CPR, rbase = pt / C::CPR;
+        // ---------------- gather producers ----------------
+        // warp w owns rows 32w..32w+31 of each 128-row tile; per instruction j a warp covers RPI rows
+        // with CPR lanes per row (one 16-B chunk each).  Missing neighbours issue no copy at all:
+        // their TMEM rows are masked off in the MMA (disable-output-lane), so nothing is zero-filled.
+        constexpr int RPI = 32 / C::CPR;
+        const int q = lane / C::CPR, cchunk = lane % C::CPR;
         const int kb = cchunk / (C::KB / 8), cc = cchunk % (C::KB / 8);
         uint32_t it = 0, ic = 0;
         for (int st = blockIdx.x; st < num_super; st += gridDim.x) {
@@ -135,17 +146,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
                     int32_t idx[C::CPR];
 #pragma unroll
-                    for (int j = 0; j < C::CPR; ++j) idx[j] = ib[t * kTile + rbase + j * C::RSTEP];
+                    for (int j = 0; j < C::CPR; ++j) idx[j] = ib[t * kTile + warp * 32 + j * RPI + q];
+                    uint32_t valid = 0;
+#pragma unroll
+                    for (int j = 0; j < C::CPR; ++j) {
+                        const uint32_t b = __ballot_sync(0xffffffffu, idx[j] >= 0);
+#pragma unroll
+                        for (int qq = 0; qq < RPI; ++qq) valid |= ((b >> (qq * C::CPR)) & 1u) << (j * RPI + qq);
+                    }
                     mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
                     const uint32_t sA = base + s * C::A_BYTES;
 #pragma unroll
                     for (int j = 0; j < C::CPR; ++j) {
-                        const int r = rbase + j * C::RSTEP;
-                        const uint32_t dst = sA + kb * (kTile * C::ROWB) + swz_off(r, cc, C::ROWB);
-                        const int32_t i = idx[j] < 0 ? 0 : idx[j];
-                        cp_async_16(dst, in + (int64_t)i * K + cchunk * 8, idx[j] < 0 ? 0u : 16u);
+                        if (idx[j] >= 0) {
+                            const int r = warp * 32 + j * RPI + q;
+                            const uint32_t dst = sA + kb * (kTile * C::ROWB) + swz_off(r, cc, C::ROWB);
+                            cp_async_16(dst, in + (int64_t)idx[j] * K + cchunk * 8, 16u);
+                        }
                     }
+                    if (lane == 0) lane_mask[s][warp] = ~valid;   // 1 = disabled output lane
                     cp_async_arrive_noinc(smem_u32(&bar_full[s]));
+                    if (lane == 0) mbar_arrive(smem_u32(&bar_full[s]));
                 }
                 mbar_arrive(smem_u32(&bar_iempty[islot]));
             }
@@ -186,16 +207,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     fence_proxy_async_smem();
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t sA = base + s * C::A_BYTES;
-                        const uint32_t dt = tmem + (buf * C::TPS + t) * N;
+                        const uint32_t m0 = lane_mask[s][0], m1 = lane_mask[s][1], m2 = lane_mask[s][2],
+                                       m3 = lane_mask[s][3];
+                        if ((m0 & m1 & m2 & m3) != 0xffffffffu) {  // skip stages with no pair at all
+                            const uint32_t sA = base + s * C::A_BYTES;
+                            const uint32_t dt = tmem + (buf * C::TPS + t) * N;
 #pragma unroll
-                        for (int kb = 0; kb < C::NKB; ++kb)
+                            for (int kb = 0; kb < C::NKB; ++kb)
 #pragma unroll
-                            for (int ks = 0; ks < C::KB / 16; ++ks) {
-                                uint64_t ad = smem_desc(sA + kb * kTile * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
-                                uint64_t bd = smem_desc(sB + kb * N * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
-                                mma_bf16(dt, ad, bd, C::IDESC, (d | kb | ks) != 0);
-                            }
+                                for (int ks = 0; ks < C::KB / 16; ++ks) {
+                                    uint64_t ad = smem_desc(sA + kb * kTile * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
+                                    uint64_t bd = smem_desc(sB + kb * N * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
+                                    mma_bf16_masked(dt, ad, bd, C::IDESC, 1u, m0, m1, m2, m3);
+                                }
+                        }
                         mma_commit(smem_u32(&bar_empty[s]));
                     }
                     __syncwarp();
@@ -219,8 +244,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
                 for (int c0 = 0; c0 < N; c0 += 32) {
                     uint32_t v[32];
-                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (buf * C::TPS + t) * N + c0, v);
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (buf * C::TPS + t) * N + c0;
+                    tmem_ld32(ta, v);
                     tmem_ld_wait();
+                    tmem_st32_zero(ta);  // reset for the next super-tile using this buffer
                     if (row < n_out) {
                         if constexpr (OUT_BF16) {
                             uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(out) + row * N + c0);
@@ -244,6 +271,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     }
                 }
             }
+            tmem_st_wait();
             tc_fence_before();
             mbar_arrive(smem_u32(&bar_tempty[buf]));
         }

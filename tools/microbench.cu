@@ -407,6 +407,203 @@ extern "C" int mb_gather_mx(const void* feat, const int32_t* nbr, long long n_ou
     return 0;
 }
 
+// ---------------------------------------------------------------- (2d) L1-friendly gathers
+// tile-major gather with few stages (large L1), cp.async.ca vs ld.global(L1)+st.shared.
+template <int MODE, int STAGES, int NPW>
+__global__ void __launch_bounds__(NPW * 32 + 64, 1) k_gather_l1(const bf16* feat, const int32_t* nbr, long long n_out,
+                                                               int num_tiles) {
+    extern __shared__ uint8_t dsm[];
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], ifull[2], iempty[2];
+    const uint32_t sbase = smem_u32(dsm);
+    const uint32_t base = (sbase + 1023) & ~1023u;
+    const uint32_t ibase = base + STAGES * 16384;
+    const int32_t* ism = reinterpret_cast<const int32_t*>(dsm + (ibase - sbase));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NP = NPW * 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full[s]), NP);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&ifull[b]), 1);
+            mbar_init(smem_u32(&iempty[b]), NP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == NPW) {
+        if (lane == 0) {
+            int lt = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+                int b = lt & 1;
+                mbar_wait(smem_u32(&iempty[b]), ((lt >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(smem_u32(&ifull[b]), 27 * 512);
+                for (int d = 0; d < 27; ++d)
+                    bulk_g2s(ibase + b * 27 * 512 + d * 512, nbr + (long long)d * n_out + (long long)t * 128, 512,
+                             smem_u32(&ifull[b]));
+            }
+        }
+    } else if (warp < NPW) {
+        const int pt = threadIdx.x, c = pt & 7, rb = pt >> 3;
+        constexpr int RS = NP / 8, J = 128 / RS;
+        uint32_t it = 0;
+        int lt = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+            int b = lt & 1;
+            mbar_wait(smem_u32(&ifull[b]), (lt >> 1) & 1);
+            const int32_t* ib = ism + b * 27 * 128;
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                int idx[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) idx[j] = ib[d * 128 + rb + RS * j];
+                if (MODE == 1) {
+                    int4 vals[J];
+#pragma unroll
+                    for (int j = 0; j < J; ++j) {
+                        const int4* src = reinterpret_cast<const int4*>(feat + (long long)(idx[j] < 0 ? 0 : idx[j]) * 64 + c * 8);
+                        int4 v;
+                        asm volatile("ld.global.L1::evict_last.v4.b32 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src));
+                        vals[j] = idx[j] < 0 ? make_int4(0, 0, 0, 0) : v;
+                    }
+                    mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+#pragma unroll
+                    for (int j = 0; j < J; ++j) {
+                        int r = rb + RS * j;
+                        uint32_t dst = base + s * 16384 + r * 128 + ((c ^ (r & 7)) << 4);
+                        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(vals[j].x), "r"(vals[j].y),
+                                     "r"(vals[j].z), "r"(vals[j].w)
+                                     : "memory");
+                    }
+                    mbar_arrive(smem_u32(&full[s]));
+                } else {
+                    mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+#pragma unroll
+                    for (int j = 0; j < J; ++j) {
+                        int r = rb + RS * j;
+                        uint32_t dst = base + s * 16384 + r * 128 + ((c ^ (r & 7)) << 4);
+                        const bf16* src = feat + (long long)(idx[j] < 0 ? 0 : idx[j]) * 64 + c * 8;
+                        cp_async_16(dst, src, idx[j] < 0 ? 0 : 16);
+                    }
+                    cp_async_arrive_noinc(smem_u32(&full[s]));
+                }
+            }
+            mbar_arrive(smem_u32(&iempty[b]));
+        }
+    } else if (warp == NPW + 1 && lane == 0) {
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x)
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                mbar_wait(smem_u32(&full[s]), ph);
+                mbar_arrive(smem_u32(&empty[s]));
+            }
+    }
+}
+
+template <int MODE, int STAGES, int NPW>
+static float run_l1(const void* feat, const int32_t* nbr, long long n_out, int ctas_per_sm, int sms) {
+    int tiles = (int)(n_out / 128);
+    size_t smem = STAGES * 16384 + 2 * 27 * 512 + 1024;
+    auto k = k_gather_l1<MODE, STAGES, NPW>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float ms = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(a);
+        k<<<sms * ctas_per_sm, NPW * 32 + 64, smem>>>((const bf16*)feat, nbr, n_out, tiles);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+    }
+    cudaEventElapsedTime(&ms, a, b);
+    return cudaGetLastError() == cudaSuccess ? ms : -1.f;
+}
+
+extern "C" int mb_gather_l1(const void* feat, const int32_t* nbr, long long n_out, float* out) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    out[0] = run_l1<0, 2, 4>(feat, nbr, n_out, 1, sms);
+    out[1] = run_l1<0, 4, 4>(feat, nbr, n_out, 1, sms);
+    out[2] = run_l1<0, 2, 4>(feat, nbr, n_out, 2, sms);
+    out[3] = run_l1<0, 4, 4>(feat, nbr, n_out, 2, sms);
+    out[4] = run_l1<1, 2, 8>(feat, nbr, n_out, 1, sms);
+    out[5] = run_l1<1, 4, 8>(feat, nbr, n_out, 1, sms);
+    out[6] = run_l1<1, 2, 8>(feat, nbr, n_out, 2, sms);
+    out[7] = run_l1<1, 4, 8>(feat, nbr, n_out, 2, sms);
+    out[8] = run_l1<0, 12, 4>(feat, nbr, n_out, 1, sms);
+    return 0;
+}
+
+// ---------------------------------------------------------------- (2e) smem window -> TMEM A operand
+// per 16-KB A tile: 128 threads each LDS.128 x8 one random window row (own TMEM lane) + tcgen05.st.
+template <int SWZ>
+__global__ void __launch_bounds__(128, 1) k_lds_sttm(const uint16_t* lidx, int iters, long long* cycles) {
+    extern __shared__ uint8_t dsm[];
+    __shared__ uint32_t slot;
+    const uint32_t base = (smem_u32(dsm) + 1023) & ~1023u;   // window: 512 rows x 128 B = 64 KB
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 512 * 32; i += 128)
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(base + 4 * i), "r"(i) : "memory");
+    if (warp == 0) tmem_alloc(smem_u32(&slot), 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot + ((uint32_t)(warp * 32) << 16);
+    uint32_t acc = 0;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        const int u = lidx[(it * 128 + threadIdx.x) & 65535] & 511;
+        uint32_t v[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int cc = SWZ ? ((c + lane) & 7) : c;
+            const uint32_t addr = base + u * 128 + ((SWZ ? (cc ^ (u & 7)) : cc) << 4);
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v[4 * cc]), "=r"(v[4 * cc + 1]), "=r"(v[4 * cc + 2]), "=r"(v[4 * cc + 3]) : "r"(addr));
+        }
+        const uint32_t ta = tmem + (it & 7) * 32;
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+            "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+            ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+            "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+            "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]),
+            "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+            : "memory");
+        acc += v[0];
+    }
+    tmem_st_wait();
+    long long t1 = clock64();
+    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0 + (acc == 12345 ? 1 : 0);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(slot, 256);
+    }
+}
+
+extern "C" int mb_lds_sttm(const uint16_t* lidx, int iters, long long* cycles, float* ms, int swz) {
+    size_t smem = 65536 + 1024;
+    auto k = swz ? k_lds_sttm<1> : k_lds_sttm<0>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k<<<148, 128, smem>>>(lidx, iters, cycles);
+    cudaEventRecord(a);
+    k<<<148, 128, smem>>>(lidx, iters, cycles);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(ms, a, b);
+    return (int)cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- (3) MMA issue rate
 template <int N>
 __global__ void __launch_bounds__(128, 1) k_mma_rate(int iters, long long* cycles) {

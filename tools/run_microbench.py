@@ -79,7 +79,7 @@ def main():
             bw[f"{name}_x{cps}"] = {"rc": rc, "ms": ms.value,
                                     "valid_GBps": valid_bytes / (ms.value / 1e3) / 1e9 if ms.value else None,
                                     "all_rows_GBps": 27 * n_out * 128 / (ms.value / 1e3) / 1e9 if ms.value else None}
-    for mode, name in ((1, "cp_async_ca"),):
+    for mode, name in ():
         for stages in (8,):
             ms = C.c_float(0)
             rc = L.mb_gather_bw2(mode, stages, C.c_void_p(feat.data_ptr()), C.c_longlong(n), C.c_void_p(nbr.data_ptr()),
@@ -88,14 +88,20 @@ def main():
                                     "valid_GBps": valid_bytes / (ms.value / 1e3) / 1e9 if ms.value else None,
                                     "all_rows_GBps": 27 * n_out * 128 / (ms.value / 1e3) / 1e9 if ms.value else None}
     rep["gather_bw_cfg2"] = {"valid_bytes": valid_bytes, "modes": bw}
-    mx = torch.zeros(18, dtype=torch.float32)
-    mxp = C.c_void_p(mx.data_ptr())
-    L.mb_gather_mx(C.c_void_p(feat.data_ptr()), C.c_void_p(nbr.data_ptr()), C.c_longlong(n_out), mxp)
     allb = 27 * n_out * 128
-    rep["gather_matrix_ms"] = {f"{m}_w{w}_{i}": {"ms": float(mx[((w == 8) * 3 + mi) * 3 + ii]),
-                                                 "GBps_all_rows": allb / (float(mx[((w == 8) * 3 + mi) * 3 + ii]) / 1e3) / 1e9}
-                               for w in (4, 8) for mi, m in enumerate(("cp_async_ca", "cp_async_cg", "ldg_sts"))
-                               for ii, i in enumerate(("real", "l1set", "identity"))}
+    l1 = torch.zeros(9, dtype=torch.float32)
+    L.mb_gather_l1(C.c_void_p(feat.data_ptr()), C.c_void_p(nbr.data_ptr()), C.c_longlong(n_out), C.c_void_p(l1.data_ptr()))
+    names = ["cpasync_ca_s2_x1", "cpasync_ca_s4_x1", "cpasync_ca_s2_x2", "cpasync_ca_s4_x2", "ldgL1_sts_s2_w8_x1",
+             "ldgL1_sts_s4_w8_x1", "ldgL1_sts_s2_w8_x2", "ldgL1_sts_s4_w8_x2", "cpasync_ca_s12_x1"]
+    rep["gather_l1"] = {n_: {"ms": float(v), "GBps_all_rows": allb / (float(v) / 1e3) / 1e9} for n_, v in zip(names, l1)}
+    lidx = torch.randint(0, 512, (65536,), dtype=torch.int16, device="cuda")
+    cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
+    for swz in (0, 1):
+        ms = C.c_float(0)
+        iters = 20000
+        rc = L.mb_lds_sttm(C.c_void_p(lidx.data_ptr()), iters, C.c_void_p(cyc.data_ptr()), C.byref(ms), swz)
+        rep[f"lds_sttm_swz{swz}"] = {"rc": rc, "ms": ms.value, "cycles_per_16KB_tile": cyc.float().mean().item() / iters,
+                                     "GBps": 148 * iters * 16384 / (ms.value / 1e3) / 1e9}
     # (3) MMA issue rate
     cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
     mm = {}
