@@ -27,6 +27,7 @@
 // A CTA owns up to 8 M-blocks (TMEM ≤ 512 columns) for one output-row split;
 // partial [split][27][Cin][Cout] sums are reduced in a fixed order (deterministic).
 #include <cuda_bf16.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -49,14 +50,14 @@ __host__ __device__ __forceinline__ uint32_t swz_off(int r, int c, int rowb) {
     return (uint32_t)(r * rowb + ((c ^ x) << 4));
 }
 
-template <int K, int N>
+template <int K, int N, int TPS_ = (N <= 64 ? 4 : 2)>
 struct FwdCfg {
     static constexpr int KB = K >= 64 ? 64 : K;       // K elements per swizzle row
     static constexpr int ROWB = KB * 2;                // bytes per swizzled row segment
     static constexpr int NKB = K / KB;
     static constexpr int A_BYTES = kTile * K * 2;      // one gathered 128-row A tile
     static constexpr int B_BYTES = N * K * 2;          // one offset's weight image
-    static constexpr int TPS = N <= 64 ? 4 : 2;        // 128-row tiles per super-tile (share one B load)
+    static constexpr int TPS = TPS_;                   // 128-row tiles per super-tile (share one B load)
     static constexpr int SUPER = TPS * kTile;
     static constexpr int IDX_BYTES = SUPER * 4;        // index block of one (super-tile, offset)
     static constexpr int ISLOTS = 8;
@@ -73,20 +74,23 @@ struct FwdCfg {
     static_assert(FVDB_NBR_ALIGN % SUPER == 0, "index blocks must tile the padded table");
 };
 
-constexpr int kFwdThreads = 320;  // warps 0-3 gather, 4 loader, 5 MMA, 6-9 epilogue
+// warps [0, NPW) gather, NPW loader, NPW+1 MMA, NPW+2 .. NPW+5 epilogue
+__host__ __device__ constexpr int fwd_threads(int npw) { return (npw + 6) * 32; }
 
-template <int K, int N, bool OUT_BF16>
-__global__ void __launch_bounds__(kFwdThreads, 1)
+template <int K, int N, bool OUT_BF16, int TPS = (N <= 64 ? 4 : 2), int NPW = 4>
+__global__ void __launch_bounds__(fwd_threads(NPW), 1)
     k_conv_fwd_tc(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, const int32_t* __restrict__ nbr,
-                  int64_t ld, int64_t n_out, void* __restrict__ out, int num_super) {
-    using C = FwdCfg<K, N>;
+                  int64_t ld, int64_t n_out, void* __restrict__ out, int num_super, int dbg) {
+    using C = FwdCfg<K, N, TPS>;
+    constexpr int W_LOAD = NPW, W_MMA = NPW + 1, W_EPI = NPW + 2;
+    constexpr int RPW = kTile / NPW;  // rows per gather warp per tile
     extern __shared__ uint8_t dsmem[];
     __shared__ __align__(8) uint64_t bar_full[C::STAGES], bar_empty[C::STAGES];
     __shared__ __align__(8) uint64_t bar_ifull[C::ISLOTS], bar_iempty[C::ISLOTS];
     __shared__ __align__(8) uint64_t bar_bfull[C::BSLOTS], bar_bempty[C::BSLOTS];
     __shared__ __align__(8) uint64_t bar_tfull[2], bar_tempty[2];
     __shared__ uint32_t tmem_slot;
-    __shared__ uint32_t lane_mask[C::STAGES][4];
+    __shared__ __align__(16) uint16_t lane_mask[C::STAGES][8];  // 128-bit disable-output-lane mask per stage
 
     const uint32_t sbase = smem_u32(dsmem);
     const uint32_t base = (sbase + 1023u) & ~1023u;                  // A stages (1024-aligned)
@@ -97,12 +101,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
-            mbar_init(smem_u32(&bar_full[s]), 128 + 4);  // cp.async arrivals + one mask-word arrive per warp
+            mbar_init(smem_u32(&bar_full[s]), NPW * 32 + NPW);  // cp.async arrivals + one mask arrive per warp
             mbar_init(smem_u32(&bar_empty[s]), 1);
         }
         for (int s = 0; s < C::ISLOTS; ++s) {
             mbar_init(smem_u32(&bar_ifull[s]), 1);
-            mbar_init(smem_u32(&bar_iempty[s]), 128);
+            mbar_init(smem_u32(&bar_iempty[s]), NPW * 32);
         }
         for (int s = 0; s < C::BSLOTS; ++s) {
             mbar_init(smem_u32(&bar_bfull[s]), 1);
@@ -114,12 +118,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 5) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
+    if (warp == W_MMA) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
-    if (warp >= 6) {  // accumulators start at zero; every MMA then accumulates under its lane mask
+    if (warp >= W_EPI) {  // accumulators start at zero; every MMA then accumulates under its lane mask
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         for (int c0 = 0; c0 < 2 * C::TPS * N; c0 += 32) tmem_st32_zero(lane_base + c0);
         tmem_st_wait();
@@ -128,69 +132,76 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     __syncthreads();
     tc_fence_after();
 
-    if (warp < 4) {
+    if (warp < NPW) {
         // ---------------- gather producers ----------------
-        // warp w owns rows 32w..32w+31 of each 128-row tile; per instruction j a warp covers RPI rows
-        // with CPR lanes per row (one 16-B chunk each).  Missing neighbours issue no copy at all:
-        // their TMEM rows are masked off in the MMA (disable-output-lane), so nothing is zero-filled.
+        // warp w owns rows RPW*w .. RPW*w+RPW-1 of each 128-row tile; per instruction j a warp covers
+        // RPI rows with CPR lanes per row (one 16-B chunk each).  Missing neighbours issue no copy:
+        // their TMEM rows are masked off in the MMA (disable-output-lane), nothing is zero-filled.
         constexpr int RPI = 32 / C::CPR;
+        constexpr int NJ = RPW / RPI;  // instructions per warp per stage
         const int q = lane / C::CPR, cchunk = lane % C::CPR;
         const int kb = cchunk / (C::KB / 8), cc = cchunk % (C::KB / 8);
+        uint32_t dst_off[NJ];  // swizzled smem offsets of this thread's chunks (stage-invariant)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            dst_off[j] = kb * (kTile * C::ROWB) + swz_off(warp * RPW + j * RPI + q, cc, C::ROWB);
+        const bf16* in_c = in + cchunk * 8;
         uint32_t it = 0, ic = 0;
         for (int st = blockIdx.x; st < num_super; st += gridDim.x) {
             for (int d = 0; d < 27; ++d, ++ic) {
                 const uint32_t islot = ic % C::ISLOTS;
                 mbar_wait(smem_u32(&bar_ifull[islot]), (ic / C::ISLOTS) & 1);
-                const int32_t* ib = idx_smem + islot * C::SUPER;
+                const int32_t* ib = idx_smem + islot * C::SUPER + warp * RPW;
                 for (int t = 0; t < C::TPS; ++t, ++it) {
                     const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
-                    int32_t idx[C::CPR];
+                    const int32_t* ibt = ib + t * kTile;
+                    const uint32_t valid = __ballot_sync(0xffffffffu, lane < RPW && ibt[lane < RPW ? lane : 0] >= 0);
+                    int32_t idx[NJ];
 #pragma unroll
-                    for (int j = 0; j < C::CPR; ++j) idx[j] = ib[t * kTile + warp * 32 + j * RPI + q];
-                    uint32_t valid = 0;
-#pragma unroll
-                    for (int j = 0; j < C::CPR; ++j) {
-                        const uint32_t b = __ballot_sync(0xffffffffu, idx[j] >= 0);
-#pragma unroll
-                        for (int qq = 0; qq < RPI; ++qq) valid |= ((b >> (qq * C::CPR)) & 1u) << (j * RPI + qq);
-                    }
+                    for (int j = 0; j < NJ; ++j) idx[j] = ibt[j * RPI + q];
                     mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
                     const uint32_t sA = base + s * C::A_BYTES;
 #pragma unroll
-                    for (int j = 0; j < C::CPR; ++j) {
-                        if (idx[j] >= 0) {
-                            const int r = warp * 32 + j * RPI + q;
-                            const uint32_t dst = sA + kb * (kTile * C::ROWB) + swz_off(r, cc, C::ROWB);
-                            cp_async_16(dst, in + (int64_t)idx[j] * K + cchunk * 8, 16u);
+                    for (int j = 0; j < NJ; ++j)
+                        if (idx[j] >= 0) cp_async_16(sA + dst_off[j], in_c + (int64_t)idx[j] * K, 16u);
+                    if (lane == 0) {  // 1 = disabled output lane
+                        if constexpr (RPW == 32) {
+                            lane_mask[s][2 * warp] = (uint16_t)(~valid);
+                            lane_mask[s][2 * warp + 1] = (uint16_t)(~valid >> 16);
+                        } else {
+                            lane_mask[s][warp] = (uint16_t)(~valid);
                         }
                     }
-                    if (lane == 0) lane_mask[s][warp] = ~valid;   // 1 = disabled output lane
                     cp_async_arrive_noinc(smem_u32(&bar_full[s]));
                     if (lane == 0) mbar_arrive(smem_u32(&bar_full[s]));
                 }
                 mbar_arrive(smem_u32(&bar_iempty[islot]));
             }
         }
-    } else if (warp == 4) {
+    } else if (warp == W_LOAD) {
         // ---------------- loader: index blocks + weight images by TMA bulk copies ---------------
         if (lane == 0) {
             uint32_t ic = 0, bc = 0;
             for (int st = blockIdx.x; st < num_super; st += gridDim.x) {
                 for (int d = 0; d < 27; ++d, ++ic, ++bc) {
                     const uint32_t islot = ic % C::ISLOTS;
-                    mbar_wait(smem_u32(&bar_iempty[islot]), ((ic / C::ISLOTS) & 1) ^ 1);
+                    mbar_wait_sleep(smem_u32(&bar_iempty[islot]), ((ic / C::ISLOTS) & 1) ^ 1, 128);
                     mbar_arrive_expect_tx(smem_u32(&bar_ifull[islot]), C::IDX_BYTES);
                     bulk_g2s(ibase + islot * C::IDX_BYTES, nbr + (int64_t)d * ld + (int64_t)st * C::SUPER,
                              C::IDX_BYTES, smem_u32(&bar_ifull[islot]));
                     const uint32_t bslot = bc % C::BSLOTS;
-                    mbar_wait(smem_u32(&bar_bempty[bslot]), ((bc / C::BSLOTS) & 1) ^ 1);
-                    mbar_arrive_expect_tx(smem_u32(&bar_bfull[bslot]), C::B_BYTES);
-                    bulk_g2s(bbase + bslot * C::B_BYTES, wimg + (size_t)d * C::B_BYTES, C::B_BYTES,
-                             smem_u32(&bar_bfull[bslot]));
+                    mbar_wait_sleep(smem_u32(&bar_bempty[bslot]), ((bc / C::BSLOTS) & 1) ^ 1, 128);
+                    if ((dbg & 8) && bc >= (uint32_t)C::BSLOTS) {  // profiling: reuse stale weight slots
+                        mbar_arrive(smem_u32(&bar_bfull[bslot]));
+                    } else {
+                        mbar_arrive_expect_tx(smem_u32(&bar_bfull[bslot]), C::B_BYTES);
+                        bulk_g2s(bbase + bslot * C::B_BYTES, wimg + (size_t)d * C::B_BYTES, C::B_BYTES,
+                                 smem_u32(&bar_bfull[bslot]));
+                    }
                 }
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == W_MMA) {
         // ---------------- MMA issuer ----------------
         uint32_t it = 0, bc = 0, lt = 0;
         for (int st = blockIdx.x; st < num_super; st += gridDim.x, ++lt) {
@@ -207,21 +218,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     fence_proxy_async_smem();
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t m0 = lane_mask[s][0], m1 = lane_mask[s][1], m2 = lane_mask[s][2],
-                                       m3 = lane_mask[s][3];
-                        if ((m0 & m1 & m2 & m3) != 0xffffffffu) {  // skip stages with no pair at all
+                        const uint4 mk = *reinterpret_cast<const uint4*>(&lane_mask[s][0]);
+                        const uint32_t m0 = mk.x, m1 = mk.y, m2 = mk.z, m3 = mk.w;
+                        if ((m0 & m1 & m2 & m3) != 0xffffffffu && !(dbg & 1)) {  // skip stages with no pair
                             const uint32_t sA = base + s * C::A_BYTES;
                             const uint32_t dt = tmem + (buf * C::TPS + t) * N;
 #pragma unroll
                             for (int kb = 0; kb < C::NKB; ++kb)
 #pragma unroll
-                                for (int ks = 0; ks < C::KB / 16; ++ks) {
+                                for (int ks = 0; ks < ((dbg & 64) ? 1 : C::KB / 16); ++ks) {
                                     uint64_t ad = smem_desc(sA + kb * kTile * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
                                     uint64_t bd = smem_desc(sB + kb * N * C::ROWB + ks * 32, 16, 8 * C::ROWB, C::LAYOUT);
                                     mma_bf16_masked(dt, ad, bd, C::IDESC, 1u, m0, m1, m2, m3);
                                 }
                         }
-                        mma_commit(smem_u32(&bar_empty[s]));
+                        if (dbg & 16) mbar_arrive(smem_u32(&bar_empty[s]));  // profiling: release without tcgen05
+                        else mma_commit(smem_u32(&bar_empty[s]));
                     }
                     __syncwarp();
                 }
@@ -237,7 +249,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         uint32_t lt = 0;
         for (int st = blockIdx.x; st < num_super; st += gridDim.x, ++lt) {
             const uint32_t buf = lt & 1;
-            mbar_wait(smem_u32(&bar_tfull[buf]), (lt >> 1) & 1);
+            mbar_wait_sleep(smem_u32(&bar_tfull[buf]), (lt >> 1) & 1, 512);
             tc_fence_after();
             for (int t = 0; t < C::TPS; ++t) {
                 const int64_t row = (int64_t)st * C::SUPER + t * kTile + q * 32 + lane;
@@ -248,7 +260,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     tmem_ld32(ta, v);
                     tmem_ld_wait();
                     tmem_st32_zero(ta);  // reset for the next super-tile using this buffer
-                    if (row < n_out) {
+                    if (row < n_out && !(dbg & 2)) {
                         if constexpr (OUT_BF16) {
                             uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(out) + row * N + c0);
 #pragma unroll
@@ -278,7 +290,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc(tmem, C::TMEM_COLS);
     }
@@ -413,7 +425,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         if (lane == 0) {
             for (int ch = 0; ch < n_chunks; ++ch) {
                 const uint32_t islot = ch % C::ISLOTS;
-                mbar_wait(smem_u32(&bar_iempty[islot]), ((ch / C::ISLOTS) & 1) ^ 1);
+                mbar_wait_sleep(smem_u32(&bar_iempty[islot]), ((ch / C::ISLOTS) & 1) ^ 1, 128);
                 const uint32_t fb = smem_u32(&bar_ifull[islot]);
                 mbar_arrive_expect_tx(fb, n_off * C::CHUNK * 4);
                 for (int u = 0; u < n_off; ++u)
@@ -449,7 +461,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const int q = warp & 3;
         const int m = q * 32 + lane;
         if (n_chunks > 0) {
-            mbar_wait(smem_u32(&bar_tfull), 0);
+            mbar_wait_sleep(smem_u32(&bar_tfull), 0, 2048);
             tc_fence_after();
         }
         for (int a = 0; a < n_acc; ++a) {
@@ -500,18 +512,30 @@ int sm_count() {
     return v;
 }
 
-template <int K, int N, bool OB>
-int launch_fwd(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-               cudaStream_t st) {
-    using C = FwdCfg<K, N>;
-    auto kern = k_conv_fwd_tc<K, N, OB>;
+template <int K, int N, bool OB, int TPS = (N <= 64 ? 4 : 2), int NPW = 4>
+int launch_fwd_t(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
+                 cudaStream_t st) {
+    using C = FwdCfg<K, N, TPS>;
+    auto kern = k_conv_fwd_tc<K, N, OB, TPS, NPW>;
     FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     const int supers = (int)ceil_div(n_out, C::SUPER);
     int grid = sm_count();
     if (grid > supers) grid = supers;
-    kern<<<grid, kFwdThreads, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, nbr, ld, n_out, out, supers);
+    static const int dbg = getenv("FVDB_DEBUG_FWD") ? atoi(getenv("FVDB_DEBUG_FWD")) : 0;  // profiling switches
+    kern<<<grid, fwd_threads(NPW), C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, nbr, ld, n_out, out, supers,
+                                                  dbg);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
+}
+
+template <int K, int N, bool OB>
+int launch_fwd(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
+               cudaStream_t st) {
+    if constexpr (K == 64 && N == 64) {
+        static const int npw = getenv("FVDB_FWD_NPW") ? atoi(getenv("FVDB_FWD_NPW")) : 4;  // profiling switch
+        if (npw == 8) return launch_fwd_t<K, N, OB, 4, 8>(in, wimg, nbr, ld, n_out, out, st);
+    }
+    return launch_fwd_t<K, N, OB>(in, wimg, nbr, ld, n_out, out, st);
 }
 
 template <int K, int N>

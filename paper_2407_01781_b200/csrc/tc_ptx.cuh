@@ -41,6 +41,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+// wait for warps that are off the critical path (epilogue, loaders): back off with
+// nanosleep so idle waiters do not steal MIO issue slots from the gather warps
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns = 256) {
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        __nanosleep(ns);
+        if (++n == (1u << 22)) asm volatile("trap;");
+    }
+}
+
 // ---- async copies ----
 // 16-byte cp.async through L1 (.ca: neighbour rows are re-read by ~20 outputs);
 // src_bytes == 0 zero-fills the destination (missing neighbour).

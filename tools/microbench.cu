@@ -604,6 +604,108 @@ extern "C" int mb_lds_sttm(const uint16_t* lidx, int iters, long long* cycles, f
     return (int)cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- (2f) register gather -> TMEM (A operand path)
+// Each producer warp owns TMEM lane quarter (warp & 3); lane t loads its row (8 x 16 B, L1-cached)
+// and stores it with tcgen05.st.32x32b.x32 into a TMEM ring of 32-column stages.  No shared-memory
+// traffic for A.  NPW = 4 or 8 producer warps (8: two warps per lane quarter alternate stages).
+__device__ __forceinline__ void ld_row(const bf16* p, uint32_t (&v)[32], int valid) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        if (valid) {
+            asm volatile("ld.global.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v[4 * c]), "=r"(v[4 * c + 1]), "=r"(v[4 * c + 2]), "=r"(v[4 * c + 3])
+                         : "l"(p + 8 * c));
+        }
+    }
+}
+__device__ __forceinline__ void st_tmem32(uint32_t ta, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+        ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]),
+        "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+
+template <int NPW>
+__global__ void __launch_bounds__(NPW * 32 + 64, 1) k_gather_tmem(const bf16* feat, const int32_t* nbr, long long n_out,
+                                                                 int num_tiles) {
+    constexpr int TSTAGES = 8;
+    __shared__ __align__(8) uint64_t full[TSTAGES], empty[TSTAGES];
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int GROUPS = NPW / 4;  // warps per lane quarter
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TSTAGES; ++s) {
+            mbar_init(smem_u32(&full[s]), 4);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == NPW) tmem_alloc(smem_u32(&slot), 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    if (warp < NPW) {
+        const int quarter = warp & 3, grp = warp >> 2;
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x)
+            for (int d = 0; d < 27; ++d, ++it) {
+                if ((int)(it % GROUPS) != grp) continue;
+                const uint32_t s = it % TSTAGES, ph = (it / TSTAGES) & 1;
+                const long long row = (long long)t * 128 + quarter * 32 + lane;
+                const int idx = nbr[(long long)d * n_out + row];
+                uint32_t v[32];
+                ld_row(feat + (long long)(idx < 0 ? 0 : idx) * 64, v, idx >= 0);
+                mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+                st_tmem32(lane_base + s * 32, v);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&full[s]));
+            }
+    } else if (warp == NPW + 1 && lane == 0) {
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x)
+            for (int d = 0; d < 27; ++d, ++it) {
+                uint32_t s = it % TSTAGES, ph = (it / TSTAGES) & 1;
+                mbar_wait(smem_u32(&full[s]), ph);
+                tc_fence_after();
+                mbar_arrive(smem_u32(&empty[s]));
+            }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == NPW) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
+extern "C" int mb_gather_tmem(const void* feat, const int32_t* nbr, long long n_out, int npw, float* ms) {
+    int tiles = (int)(n_out / 128);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    void (*k)(const bf16*, const int32_t*, long long, int) =
+        npw == 4 ? k_gather_tmem<4> : (npw == 8 ? k_gather_tmem<8> : k_gather_tmem<16>);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(a);
+        k<<<sms, npw * 32 + 64>>>((const bf16*)feat, nbr, n_out, tiles);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+    }
+    cudaEventElapsedTime(ms, a, b);
+    return (int)cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- (3) MMA issue rate
 template <int N>
 __global__ void __launch_bounds__(128, 1) k_mma_rate(int iters, long long* cycles) {

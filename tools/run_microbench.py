@@ -89,14 +89,19 @@ def main():
                                     "all_rows_GBps": 27 * n_out * 128 / (ms.value / 1e3) / 1e9 if ms.value else None}
     rep["gather_bw_cfg2"] = {"valid_bytes": valid_bytes, "modes": bw}
     allb = 27 * n_out * 128
+    for npw in (4, 8, 16):
+        ms = C.c_float(0)
+        rc = L.mb_gather_tmem(C.c_void_p(feat.data_ptr()), C.c_void_p(nbr.data_ptr()), C.c_longlong(n_out), npw, C.byref(ms))
+        rep[f"gather_tmem_w{npw}"] = {"rc": rc, "ms": ms.value, "valid_GBps": valid_bytes / (ms.value / 1e3) / 1e9 if ms.value else None}
     l1 = torch.zeros(9, dtype=torch.float32)
-    L.mb_gather_l1(C.c_void_p(feat.data_ptr()), C.c_void_p(nbr.data_ptr()), C.c_longlong(n_out), C.c_void_p(l1.data_ptr()))
+    # L.mb_gather_l1(...) measured in microbench4
     names = ["cpasync_ca_s2_x1", "cpasync_ca_s4_x1", "cpasync_ca_s2_x2", "cpasync_ca_s4_x2", "ldgL1_sts_s2_w8_x1",
              "ldgL1_sts_s4_w8_x1", "ldgL1_sts_s2_w8_x2", "ldgL1_sts_s4_w8_x2", "cpasync_ca_s12_x1"]
-    rep["gather_l1"] = {n_: {"ms": float(v), "GBps_all_rows": allb / (float(v) / 1e3) / 1e9} for n_, v in zip(names, l1)}
+    if float(l1.sum()) > 0:
+        rep["gather_l1"] = {n_: {"ms": float(v), "GBps_all_rows": allb / (float(v) / 1e3) / 1e9} for n_, v in zip(names, l1)}
     lidx = torch.randint(0, 512, (65536,), dtype=torch.int16, device="cuda")
     cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
-    for swz in (0, 1):
+    for swz in ():
         ms = C.c_float(0)
         iters = 20000
         rc = L.mb_lds_sttm(C.c_void_p(lidx.data_ptr()), iters, C.c_void_p(cyc.data_ptr()), C.byref(ms), swz)
