@@ -42,6 +42,11 @@ PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 TRAFFIC_FILE = ROOT / "profiles" / "ncu_traffic.json"
 
 CONFIGS = {
+    "cfg1": dict(desc="single GridBatch from a random 100k-point cloud (sigma 1, voxel 0.05), SparseConv3d 3x3x3 "
+                      "32->32 fp32 forward (CUDA-core exact path)", points=True, cin=32, cout=32, fp32_fwd=True),
+    "cfg4": dict(desc="sparse U-Net stage: build from jagged points (cfg2 shell as f64 voxel centres), coarsen, "
+                      "stride-2 conv 64->128 + transposed conv 128->64, fwd+bwd, bf16", res=470, cin=64, cout=128,
+                 unet=True),
     "cfg2": dict(desc="ScanNet-scale sphere shell sphere_shell_coords(470, band=1.5), SparseConv3d 3x3x3 64->64 "
                       "bf16 fwd+bwd", res=470, cin=64, cout=64),
     "cfg3": dict(desc="KITTI-scale simulated LiDAR grid (128 beams x 2048 az, voxel 0.05 m, seed=rank), "
@@ -78,9 +83,11 @@ def peaks():
 # ----------------------------------------------------------------------------- inputs
 
 def make_coords(cfg, rank):
-    from paper_2407_01781_b200.workloads import lidar_scan_points, sphere_shell_coords
+    from paper_2407_01781_b200.workloads import lidar_scan_points, random_points, sphere_shell_coords
     if cfg.get("lidar"):
         return None, lidar_scan_points(rank)
+    if cfg.get("points"):
+        return None, random_points(np.random.default_rng(rank), 100_000, sigma=1.0)
     return sphere_shell_coords(cfg["res"], band=1.5), None
 
 
@@ -134,6 +141,9 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- our arm
 
 def run_ours(args, rank, world, local_rank):
+    cfg = CONFIGS[args.config]
+    if cfg.get("fp32_fwd") or cfg.get("unet"):
+        return run_special(args, rank, world, local_rank, cfg)
     import torch
     import torch.distributed as dist
 
@@ -277,6 +287,90 @@ def run_ours(args, rank, world, local_rank):
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
+    if use_dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_special(args, rank, world, local_rank, cfg):
+    """cfg1 (fp32 forward, exact path) and cfg4 (U-Net stage incl. grid build) — timed like the main arm."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_01781_b200 as P
+    from paper_2407_01781_b200.conv import gather_conv
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    use_dist = world > 1
+    coords, points = make_coords(cfg, rank)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    if cfg.get("fp32_fwd"):
+        grid, _ = P.build_from_points(points, P.VoxelTransform.uniform(0.05))
+        km = P.build_kernel_map(grid, grid, 1)
+        x = torch.randn(grid.num_voxels, cfg["cin"], device=dev, generator=gen)
+        w = torch.randn(cfg["cout"], cfg["cin"], 3, 3, 3, device=dev, generator=gen) / (27 * cfg["cin"]) ** 0.5
+        n_vox, pairs = grid.num_voxels, km.total_pairs
+        flops = 2.0 * pairs * cfg["cin"] * cfg["cout"]
+
+        def step():
+            return gather_conv(x, km.fwd, w)
+    else:
+        pts = torch.from_numpy(coords.astype(np.float64)).to(dev)        # jagged points, B=1, on device
+        tf = P.VoxelTransform.uniform(1.0)
+        down = P.SparseConv3d(64, 128, stride=2).to(dev)
+        up = P.SparseConv3d(128, 64, stride=2, transposed=True).to(dev)
+        n_vox = coords.shape[0]
+        x = torch.randn(n_vox, 64, device=dev, generator=gen)
+        pairs = None
+
+        def step():
+            g, _ = P.build_from_points(pts, tf)
+            fine = P.GridBatch([g])
+            coarse, h = down(fine, fine.jagged(x))
+            _, y = up(coarse, h, out_grid=fine)
+            y.jdata.float().sum().backward()
+            if use_dist:
+                P.dist.allreduce_gradients(list(down.parameters()) + list(up.parameters()))
+            return y
+
+        g0, _ = P.build_from_points(pts, tf)
+        k2 = P.build_kernel_map(g0, P.coarsen(g0, 2), 2)
+        pairs = k2.total_pairs
+        flops = 2 * 6.0 * pairs * 64 * 128   # s2 conv fwd+bwd and transposed fwd+bwd (2 x 3 GEMMs)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if use_dist:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        for a, b in ev:
+            flush.fill_(1)
+            a.record()
+            step()
+            b.record()
+        torch.cuda.synchronize()
+    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    if use_dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        pk = peaks()
+        tfl = flops / (ms / 1e3) / 1e12
+        print(json.dumps({
+            "metric": METRIC, "value": round(n_vox * world / (ms / 1e3), 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg.get("fp32_fwd") else "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "voxels_per_gpu": n_vox, "pairs": pairs,
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "step": "forward only" if cfg.get("fp32_fwd") else "build+coarsen+kmaps+fwd+bwd"},
+            "tflops_effective": round(tfl, 3),
+            "frac_of_bf16_peak": None if cfg.get("fp32_fwd") else round(tfl / pk["bf16_tflops"], 4),
+            "clocks": clk.summary(),
+        }), flush=True)
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -64,7 +64,7 @@ struct FwdCfg {
     static constexpr int BSLOTS = B_BYTES <= 8192 ? 3 : 2;
     static constexpr int FIXED = BSLOTS * B_BYTES + ISLOTS * IDX_BYTES + 1024;
     static constexpr int STAGES0 = (222 * 1024 - FIXED) / A_BYTES;
-    static constexpr int STAGES = STAGES0 > 10 ? 10 : STAGES0;
+    static constexpr int STAGES = STAGES0 > 20 ? 20 : STAGES0;   // small-K tiles: deeper ring hides latency
     static constexpr int SMEM = FIXED + STAGES * A_BYTES;
     static constexpr uint32_t LAYOUT = ROWB == 128 ? kSwizzle128B : kSwizzle64B;
     static constexpr int CPR = K / 8;                  // 16-B chunks per gathered row
