@@ -152,6 +152,55 @@ int fvdb_conv_wgrad_tc(const void* in_bf16, int64_t n_in, int cin, const void* g
                        const int32_t* nbr, int64_t ld, int64_t n_out, float* gw, void* workspace,
                        size_t workspace_bytes, void* stream);
 
+/* ---- Halo-staged tensor-core conv (same operator as fvdb_conv_gather_tc, conv.py:180-191) ----
+ * The output rows are cut into 128-row tiles.  For each tile a "halo plan" (built once per kernel
+ * map and cached by the caller) lists the unique input rows its 27 offsets touch; the conv kernel
+ * stages those rows in shared memory once (instead of re-reading each row from L2 for every pair),
+ * builds each offset's A operand from them into TMEM and runs tcgen05.mma with A in TMEM.
+ * A tile whose halo exceeds the kernel's capacity is split into 3, 9 or 27 offset phases.
+ *   perm[l]         output row of TMEM lane l of its tile (rows are paired so that the two lanes
+ *                   of every shared-memory phase read halo rows of opposite parity: no bank conflicts)
+ *   tile_rec[t]     FVDB_HALO_REC_BYTES per tile, loaded by one TMA:
+ *                     u16 lnbr[27][128]  halo slot of (offset d, lane l) inside the phase holding d,
+ *                                        0xFFFF = no pair;
+ *                     u32 mask[27][4]    (byte 6912) disable-output-lane mask per offset, bit = no pair
+ *   phase[t][g]     {first slot relative to tile_base[t], slot count} of phase g of tile t
+ * Colors: color_in[i] = parity of input row i's (possibly halved) coordinate sum, q_out[o] the
+ * matching parity of output row o (fvdb_parity_colors); they only affect bank conflicts. */
+typedef struct fvdb_halo_plan {
+    int32_t num_tiles;   /* ceil(n_out / 128) */
+    int32_t halo_cap;    /* max slots per phase (fvdb_halo_cap) */
+    int32_t* tile_level; /* [T]  1, 3, 9 or 27 phases */
+    int32_t* tile_base;  /* [T]  first halo slot of the tile */
+    int32_t* phase;      /* [T][27][2] */
+    int32_t* halo_rows;  /* [total] input row per slot, -1 = padding */
+    int32_t* perm;       /* [T*128] */
+    uint8_t* tile_rec;   /* [T][FVDB_HALO_REC_BYTES] */
+} fvdb_halo_plan;
+
+/* color[i] = ((c.x >> shift) + (c.y >> shift) + (c.z >> shift)) & 1, coords int64 [n,3] */
+int fvdb_parity_colors(const int64_t* coords, int64_t n, int shift, uint8_t* color, void* stream);
+/* halo capacity (slots per phase) of the conv kernel for K input / N output channels; 0 = unsupported */
+int fvdb_halo_cap(int K, int N);
+/* count pass: writes tile_level, tile_base, phase; total slots -> *total (host). Synchronizes. */
+size_t fvdb_halo_plan_workspace_bytes(int64_t n_out);
+int fvdb_halo_plan_count(const int32_t* nbr, int64_t ld, int64_t n_out, const uint8_t* color_in,
+                         const fvdb_halo_plan* plan, int64_t* total, void* workspace,
+                         size_t workspace_bytes, void* stream);
+#define FVDB_HALO_REC_BYTES 7424
+/* fill pass: writes halo_rows, perm, tile_rec */
+int fvdb_halo_plan_fill(const int32_t* nbr, int64_t ld, int64_t n_out, const uint8_t* color_in,
+                        const uint8_t* q_out, const fvdb_halo_plan* plan, void* stream);
+/* B images for the halo kernel: as fvdb_pack_weights_umma with the K index permuted to the
+ * TMEM A layout the kernel's tcgen05.st produces, followed by copies of offsets 0..6 so that any
+ * run of up to 8 consecutive offsets (mod 27) is one contiguous TMA copy.
+ * Image bytes: FVDB_HALO_IMAGES*K*N*2. */
+#define FVDB_HALO_IMAGES 34
+int fvdb_pack_weights_halo(const float* w, int cout, int cin, int transpose, void* image, void* stream);
+int fvdb_conv_halo_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
+                      const fvdb_halo_plan* plan, int64_t n_out, void* out, int out_dtype,
+                      void* stream);
+
 /* dtype conversion helpers (fp32 -> bf16 RNE), used at the module boundary */
 int fvdb_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream);
 

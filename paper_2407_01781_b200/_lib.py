@@ -24,6 +24,8 @@ FVDB_ERR_WORKSPACE = -6
 
 DTYPE_F32, DTYPE_F64, DTYPE_BF16 = 0, 1, 2
 NBR_ALIGN = 512  # FVDB_NBR_ALIGN
+HALO_IMAGES = 34  # FVDB_HALO_IMAGES
+HALO_REC_BYTES = 7424  # FVDB_HALO_REC_BYTES
 
 _vp, _i64, _i32, _sz = C.c_void_p, C.c_int64, C.c_int, C.c_size_t
 
@@ -33,6 +35,12 @@ class GridView(C.Structure):
     _fields_ = [("tile_keys", _vp), ("leaf_keys", _vp), ("leaf_origins", _vp), ("leaf_masks", _vp),
                 ("leaf_prefix", _vp), ("leaf_value_offset", _vp), ("num_upper", _i64),
                 ("num_leaf", _i64), ("num_voxels", _i64)]
+
+
+class HaloPlan(C.Structure):
+    """fvdb_halo_plan"""
+    _fields_ = [("num_tiles", C.c_int32), ("halo_cap", C.c_int32)] + [(n, _vp) for n in (
+        "tile_level", "tile_base", "phase", "halo_rows", "perm", "tile_rec")]
 
 
 class GridArrays(C.Structure):
@@ -69,6 +77,13 @@ SIGNATURES = {
     "fvdb_wgrad_tc_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "fvdb_conv_wgrad_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "fvdb_f32_to_bf16": (_i32, [_vp, _i64, _vp, _vp]),
+    "fvdb_parity_colors": (_i32, [_vp, _i64, _i32, _vp, _vp]),
+    "fvdb_halo_cap": (_i32, [_i32, _i32]),
+    "fvdb_halo_plan_workspace_bytes": (_sz, [_i64]),
+    "fvdb_halo_plan_count": (_i32, [_vp, _i64, _i64, _vp, C.POINTER(HaloPlan), C.POINTER(_i64), _vp, _sz, _vp]),
+    "fvdb_halo_plan_fill": (_i32, [_vp, _i64, _i64, _vp, _vp, C.POINTER(HaloPlan), _vp]),
+    "fvdb_pack_weights_halo": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp]),
+    "fvdb_conv_halo_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, C.POINTER(HaloPlan), _i64, _vp, _i32, _vp]),
 }
 
 _LIB = None

@@ -17,6 +17,7 @@ The kernel map is kept on the device as a dense offset-major table
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -78,17 +79,83 @@ def _kernel_weights(kernel):
     return kernel.weights if isinstance(kernel, ConvKernel) else kernel
 
 
+class HaloPlan:
+    """Device halo plan of one neighbour table for one kernel capacity (include/fvdb_b200.h)."""
+
+    __slots__ = ("cap", "tensors", "c")
+
+    def __init__(self, table: "NbrTable", cap: int):
+        L = _lib.lib()
+        dev = table.t.device
+        n = table.n
+        T = (n + 127) // 128
+        ci, qo = table.colors()
+        z = lambda *shape, dt=torch.int32: torch.empty(shape, dtype=dt, device=dev)  # noqa: E731
+        t = {"tile_level": z(T), "tile_base": z(T), "phase": z(T, 27, 2), "perm": z(T * 128),
+             "tile_rec": z(T, _lib.HALO_REC_BYTES, dt=torch.uint8)}
+        c = _lib.HaloPlan(T, cap, *(t[k].data_ptr() for k in ("tile_level", "tile_base", "phase")), None,
+                          t["perm"].data_ptr(), t["tile_rec"].data_ptr())
+        wsb = L.fvdb_halo_plan_workspace_bytes(n)
+        ws = _lib.workspace(wsb, dev)
+        total = C.c_int64(0)
+        st = _lib.stream_ptr()
+        cp = _lib.ptr(ci)
+        _lib.check(L.fvdb_halo_plan_count(table.t.data_ptr(), table.ld, n, cp, C.byref(c), C.byref(total),
+                                          ws.data_ptr(), wsb, st), "halo_plan_count")
+        t["halo_rows"] = z(max(int(total.value), 8))
+        c.halo_rows = t["halo_rows"].data_ptr()
+        _lib.check(L.fvdb_halo_plan_fill(table.t.data_ptr(), table.ld, n, cp, _lib.ptr(qo), C.byref(c), st),
+                   "halo_plan_fill")
+        self.cap, self.tensors, self.c = cap, t, c
+
+    @property
+    def total_slots(self):
+        return int(self.tensors["halo_rows"].numel())
+
+
 class NbrTable:
-    """Device neighbour table ``t[27, ld]`` (int32, -1 = none; columns >= n are -1 padding)."""
+    """Device neighbour table ``t[27, ld]`` (int32, -1 = none; columns >= n are -1 padding).
 
-    __slots__ = ("t", "ld", "n")
+    ``colors_fn`` (optional) returns the (input-row, output-row) parity colours the halo plan
+    uses to pair lanes; halo plans are built lazily per kernel capacity and cached.
+    """
 
-    def __init__(self, t, n):
+    __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans")
+
+    def __init__(self, t, n, colors_fn=None):
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
+        self._colors_fn, self._colors, self._plans = colors_fn, None, {}
 
     @property
     def view(self):
         return self.t[:, :self.n]
+
+    def colors(self):
+        if self._colors is None:
+            self._colors = self._colors_fn() if self._colors_fn is not None else (None, None)
+        return self._colors
+
+    def halo_plan(self, K: int, N: int) -> HaloPlan:
+        cap = int(_lib.lib().fvdb_halo_cap(K, N))
+        if cap <= 0:
+            raise ValueError(f"halo conv does not support K={K}, N={N}")
+        p = self._plans.get(cap)
+        if p is None:
+            p = self._plans[cap] = HaloPlan(self, cap)
+        return p
+
+
+def parity_colors(coords: torch.Tensor, shift: int) -> torch.Tensor:
+    """uint8 ((x>>shift) + (y>>shift) + (z>>shift)) & 1 of device int64 [n, 3] coordinates."""
+    out = torch.empty(coords.shape[0], dtype=torch.uint8, device=coords.device)
+    if coords.shape[0]:
+        _lib.check(_lib.lib().fvdb_parity_colors(coords.contiguous().data_ptr(), coords.shape[0], int(shift),
+                                                 out.data_ptr(), _lib.stream_ptr()), "parity_colors")
+    return out
+
+
+def _grid_colors(grids, shift):
+    return torch.cat([parity_colors(g.active_coords(), shift) for g in grids]) if grids else None
 
 
 def padded_len(n: int) -> int:
@@ -109,13 +176,14 @@ class KernelMap:
     (``KernelMap(in_rows, out_rows, num_in, num_out, stride)``) or from a table.
     """
 
-    __slots__ = ("fwd", "num_in", "num_out", "stride", "_counts", "_lists", "_bwd")
+    __slots__ = ("fwd", "num_in", "num_out", "stride", "_counts", "_lists", "_bwd", "_grids")
 
     def __init__(self, in_rows=None, out_rows=None, num_in=0, num_out=0, stride=1, *, table=None,
-                 pair_counts=None):
+                 pair_counts=None, grids=None):
         self.num_in, self.num_out, self.stride = int(num_in), int(num_out), int(stride)
         self._lists = None
         self._bwd = None
+        self._grids = grids  # (grids_in, grids_out) lists, for the halo plan's lane colours
         if table is None:
             from .topology import _device
             dev = _device()
@@ -128,8 +196,20 @@ class KernelMap:
             self._lists = (ins, outs)
             pair_counts = torch.tensor([int(o.numel()) for o in outs], dtype=torch.int64)
             table = NbrTable(t, self.num_out)
+        if table._colors_fn is None and grids is not None:
+            table._colors_fn = self._fwd_colors
         self.fwd = table
         self._counts = pair_counts
+
+    # Lane colours (fvdb_halo_plan): forward map: inputs P(c >> (stride-1)), outputs P(c);
+    # transposed map: inputs P(c), outputs P(c >> (stride-1)).  P = coordinate-sum parity.
+    def _fwd_colors(self):
+        gi, go = self._grids
+        return _grid_colors(gi, self.stride - 1), _grid_colors(go, 0)
+
+    def _bwd_colors(self):
+        gi, go = self._grids
+        return _grid_colors(go, 0), _grid_colors(gi, self.stride - 1)
 
     @property
     def nbr(self):
@@ -187,7 +267,7 @@ class KernelMap:
             L = _lib.lib()
             _lib.check(L.fvdb_kmap_transpose(self.fwd.t.data_ptr(), self.fwd.ld, self.num_out, self.num_in,
                                              t.data_ptr(), t.shape[1], _lib.stream_ptr()), "kmap_transpose")
-            self._bwd = NbrTable(t, self.num_in)
+            self._bwd = NbrTable(t, self.num_in, self._bwd_colors if self._grids is not None else None)
         return self._bwd
 
     def transposed_table(self):
@@ -213,7 +293,7 @@ def build_kernel_map(grid_in, grid_out, stride=1):
                                  t.shape[1], counts.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()),
                "kernel_map")
     return KernelMap(num_in=grid_in.num_voxels, num_out=n_out, stride=stride, table=NbrTable(t, n_out),
-                     pair_counts=counts)
+                     pair_counts=counts, grids=([grid_in], [grid_out]))
 
 
 def batch_kernel_map(kmaps, in_offsets, out_offsets):
@@ -226,8 +306,11 @@ def batch_kernel_map(kmaps, in_offsets, out_offsets):
         v = km.nbr
         t[:, int(oo):int(oo) + km.num_out] = torch.where(v >= 0, v + int(io), v)
     counts = torch.stack([km._counts.to(dev) for km in kmaps]).sum(0)
+    grids = None
+    if all(km._grids is not None for km in kmaps):
+        grids = ([g for km in kmaps for g in km._grids[0]], [g for km in kmaps for g in km._grids[1]])
     return KernelMap(num_in=num_in, num_out=num_out, stride=kmaps[0].stride, table=NbrTable(t, num_out),
-                     pair_counts=counts)
+                     pair_counts=counts, grids=grids)
 
 
 def choose_variant(grid, c_in, c_out):
@@ -268,15 +351,25 @@ def pack_weights_kn(w: torch.Tensor, transpose: bool, dtype) -> torch.Tensor:
     return out
 
 
-def pack_weights_umma(w: torch.Tensor, transpose: bool) -> torch.Tensor:
-    """fp32 [Cout,Cin,3,3,3] -> bf16 UMMA B-operand images (27 x K x N, swizzled)."""
+def conv_impl() -> str:
+    """Tensor-core conv kernel: "halo" (default; conv_halo.cu) or "gather" (conv_tc.cu), env FVDB_CONV_IMPL."""
+    v = os.environ.get("FVDB_CONV_IMPL", "halo")
+    if v not in ("halo", "gather"):
+        raise ValueError(f"FVDB_CONV_IMPL must be 'halo' or 'gather', got {v!r}")
+    return v
+
+
+def pack_weights_umma(w: torch.Tensor, transpose: bool, impl: str | None = None) -> torch.Tensor:
+    """fp32 [Cout,Cin,3,3,3] -> bf16 UMMA B-operand images (27 x K x N, swizzled) for ``impl``'s kernel."""
     from .topology import _device
+    impl = impl or conv_impl()
     w = w.to(device=_device(), dtype=torch.float32).contiguous()
     cout, cin = int(w.shape[0]), int(w.shape[1])
-    img = torch.empty(27 * cout * cin * 2, dtype=torch.uint8, device=w.device)
+    img = torch.empty((_lib.HALO_IMAGES if impl == "halo" else 27) * cout * cin * 2, dtype=torch.uint8,
+                      device=w.device)
     L = _lib.lib()
-    _lib.check(L.fvdb_pack_weights_umma(w.data_ptr(), cout, cin, int(transpose), img.data_ptr(), _lib.stream_ptr()),
-               "pack_weights_umma")
+    fn = L.fvdb_pack_weights_halo if impl == "halo" else L.fvdb_pack_weights_umma
+    _lib.check(fn(w.data_ptr(), cout, cin, int(transpose), img.data_ptr(), _lib.stream_ptr()), f"pack_weights ({impl})")
     return img
 
 
@@ -296,7 +389,7 @@ def _tc_width(c: int) -> int:
 
 
 def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool = False,
-                out_dtype=None, w_image=None) -> torch.Tensor:
+                out_dtype=None, w_image=None, impl: str | None = None) -> torch.Tensor:
     """out[o] = Σ_d x[nbr[d][o]] @ Wk[d]; Wk from w [Cout,Cin,3,3,3] (transpose → dgrad form).
 
     x: [n_in, K] float32 / float64 / bfloat16 CUDA tensor; nbr: padded NbrTable.  Returns [n_out, N].
@@ -325,11 +418,18 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
         wp = torch.zeros(((Np, Kp) if not transpose else (Kp, Np)) + (3, 3, 3), dtype=torch.float32,
                          device=x.device)
         wp[:cout, :cin] = w.to(device=x.device, dtype=torch.float32)
-        y = gather_conv(_pad_cols(x, Kp), nbr, wp, transpose, out_dtype)
+        y = gather_conv(_pad_cols(x, Kp), nbr, wp, transpose, out_dtype, impl=impl)
         return y[:, :N].contiguous()
-    img = w_image if w_image is not None else pack_weights_umma(w, transpose)
+    impl = impl or conv_impl()
+    img = w_image if w_image is not None else pack_weights_umma(w, transpose, impl)
     out = torch.empty((n_out, N), dtype=out_dtype, device=x.device)
-    if n_out:
+    if not n_out:
+        return out
+    if impl == "halo":
+        plan = nbr.halo_plan(K, N)
+        _lib.check(L.fvdb_conv_halo_tc(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, C.byref(plan.c), n_out,
+                                       out.data_ptr(), _dtype_code(out_dtype), st), "conv_halo_tc")
+    else:
         _lib.check(L.fvdb_conv_gather_tc(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, nbr.t.data_ptr(), nbr.ld,
                                          n_out, out.data_ptr(), _dtype_code(out_dtype), st), "conv_gather_tc")
     return out

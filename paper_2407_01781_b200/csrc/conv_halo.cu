@@ -1,0 +1,816 @@
+// conv_halo.cu — halo-staged tensor-core sparse convolution for sm_100a.
+//
+// Operator (reference conv.py:180-191 forward; conv.py:358-366 dgrad form):
+//   out[o,:] = Σ_d in[nbr[d][o],:] · Wk[d]
+//
+// Why: the gather-GEMM kernel (conv_tc.cu) re-reads every (output, offset) pair's input row
+// from L2 — 27 × 128 rows per 128-row tile, 2.7 GB per pass at cfg2 — and is bound by the
+// chip's L2 throughput (~42 B/clk/SM).  The rows a tile touches are few: a 128-row tile of a
+// surface grid references ~300 unique input rows (its "halo").  This kernel stages each tile's
+// halo in shared memory ONCE (cp.async, double-buffered across tiles), then builds each offset's
+// 128×K A operand from it with conflict-free 128-bit shared loads straight into TMEM
+// (tcgen05.st.16x256b) and issues tcgen05.mma with A in TMEM, B (the offset's weights) in
+// shared memory, fp32 accumulators in TMEM.  L2 traffic drops ~9× and the A operand never
+// passes through shared memory as an MMA operand.
+//
+// Halo plan (k_halo_plan, once per kernel map; cached by the caller):
+//   * per tile, the 27×128 neighbour entries are block-radix-sorted and deduplicated;
+//   * unique rows get slots 2·rank + color (color = coordinate-sum parity, see
+//     fvdb_parity_colors), so a slot's parity is its color;
+//   * output rows are permuted into lanes so that lanes 2p, 2p+1 hold rows of opposite
+//     output parity — their halo rows at any offset then have opposite slot parity, and the
+//     two rows a shared-memory phase (8 threads) reads fall into disjoint bank halves;
+//   * a tile whose halo exceeds the kernel's capacity is split into 3 / 9 / 27 offset phases.
+//
+// Warp roles (11 warps): 0 halo loader, 1 MMA, 2-5 A builders, 6-9 epilogue, 10 weight loader.
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cuda_bf16.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace fvdb {
+namespace {
+
+using bf16 = __nv_bfloat16;
+using namespace tc;
+
+constexpr int kTileRows = 128;
+constexpr int kSmemMax = 227 * 1024;
+constexpr uint16_t kNoSlot = 0xFFFF;
+constexpr int kIdxBytes = 7424;  // tile record: 27 × 128 u16 slots (6912 B) + 27 × 16 B masks, padded
+constexpr int kRecBytes = 6912 + 27 * 16;
+
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+
+// ---------------------------------------------------------------------------------------------
+// K permutation.  Builder thread t0 (= lane & 3) of a 4-thread row group loads 16-byte chunks
+// c(t0, j), j < K/32, of its halo row; word e of load j is register i = 4j + e, which the
+// 16x256b store puts in TMEM column 8(i>>1) + 2·t0 + (i&1).  Column col holds MMA K indices
+// 2col, 2col+1.  (Layout verified by tools/tmem_a_probe.cu.)
+// ---------------------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int halo_chunk(int K, int t0, int j) {
+    return K == 32 ? t0 : (K == 64 ? 2 * t0 + j : 4 * j + t0);
+}
+// channel -> MMA K index
+__host__ __device__ __forceinline__ int halo_k_of_channel(int K, int ch) {
+    const int c = ch >> 3, e = (ch >> 1) & 3, h = ch & 1;
+    int t0, j;
+    if (K == 32) { t0 = c; j = 0; }
+    else if (K == 64) { t0 = c >> 1; j = c & 1; }
+    else { t0 = c & 3; j = c >> 2; }
+    const int i = 4 * j + e;
+    const int col = 8 * (i >> 1) + 2 * t0 + (i & 1);
+    return 2 * col + h;
+}
+// physical 16-B chunk of logical chunk c in halo slot s: odd slots flip the bank half
+__host__ __device__ __forceinline__ int halo_phys(int K, int s, int c) {
+    return K == 64 ? (c ^ (s & 1)) : (K == 128 ? (c ^ ((s & 1) << 2)) : c);
+}
+
+constexpr int kImgExt = 34;  // weight images per layer: 27 offsets + 7 wrap-around copies (d = 0..6)
+
+// Two half-pipelines (builder warps of half h -> MMA warp h -> accumulator set h) take alternate
+// batches of BATCH consecutive (tile, offset) stages.  Why two MMA issuers: at N <= 128 a single
+// issuing thread sustains only ~100 cycles per A-in-TMEM tcgen05.mma (M=128, K=16), several issuing
+// warps reach the ~32-36-cycle hardware rate (profiles/r01_halo_kernel.md).  Every hand-off is per
+// batch: an mbarrier wait costs ~150-190 cycles even when its phase has already completed.
+template <int K, int N>
+struct HaloCfg {
+    static constexpr int ROWB = 2 * K;                      // halo row bytes
+    static constexpr int CPR = K / 8;                       // 16-B chunks per row
+    static constexpr int LJ = K / 32;                       // 16-B loads per row per builder thread
+    static constexpr int NX = K / 16;                       // 16x256b .x multiplier
+    static constexpr int KB = K >= 64 ? 64 : K;             // B image swizzle-row elements
+    static constexpr int BROWB = KB * 2;
+    static constexpr uint32_t BLAYOUT = BROWB == 128 ? kSwizzle128B : kSwizzle64B;
+    static constexpr int B_BYTES = N * K * 2;               // one offset's weight image
+    static constexpr int ACOLS = K / 2;                     // TMEM columns of one A stage
+    // accumulator buffers per half: 2 (epilogue overlaps the next tile) when TMEM allows
+    static constexpr int NACC = 4 * N + 2 * ACOLS <= 512 ? 2 : 1;
+    static constexpr int ACC = 2 * NACC * N;                // accumulator columns (both halves)
+    static constexpr int fits(int b) {
+        return ACC + 2 * b * ACOLS <= 512 &&
+               (kSmemMax - 2048 - (1024 + 2 * b * B_BYTES + 2 * kIdxBytes)) / (2 * (ROWB + 4)) >= 256;
+    }
+    static constexpr int BATCH = fits(4) ? 4 : (fits(2) ? 2 : 1);  // stages per batch (= weight images per TMA)
+    static constexpr int FIXED = 1024 + 2 * BATCH * B_BYTES + 2 * kIdxBytes;
+    static constexpr int CAP = ((kSmemMax - 2048 - FIXED) / (2 * (ROWB + 4))) & ~7;
+    static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4);
+    static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, N, false, false);
+    static_assert(fits(BATCH) && CAP >= 256, "halo capacity must hold one offset phase (2 x 128 slots)");
+    static_assert(27 + BATCH - 1 <= kImgExt, "weight batch wraps past the extended image array");
+};
+
+constexpr int kHalves = 2;
+constexpr int kBuilders = 4 * kHalves;
+// warps: 0 halo loader, 1-2 MMA (half 0, 1), 3-10 builders, 11-14 epilogue, 15 weight loader
+constexpr int kHaloWarps = 3 + kBuilders + 4 + 1;
+constexpr int kHaloThreads = kHaloWarps * 32;
+
+// profiling trace (FVDB_DEBUG_HALO & 64): clock64 stamps of CTA 0, kTraceN events per channel
+constexpr int kTraceCh = 12, kTraceN = 2048;
+__device__ long long g_halo_trace[kTraceCh][kTraceN];
+__device__ __forceinline__ void trace(int dbg, int ch, uint32_t i) {
+    if ((dbg & 64) && blockIdx.x == 0 && i < (uint32_t)kTraceN) g_halo_trace[ch][i] = clock64();
+}
+
+// ---------------------------------------------------------------------------------------------
+// conv kernel
+// ---------------------------------------------------------------------------------------------
+template <int K, int N, bool OUT_BF16>
+__global__ void __launch_bounds__(kHaloThreads, 1)
+    k_conv_halo(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, fvdb_halo_plan P,
+                int64_t n_out, void* __restrict__ out, int dbg) {
+    using C = HaloCfg<K, N>;
+    constexpr int W_LOAD = 0, W_MMA = 1, W_BLD = 3, W_EPI = 3 + kBuilders, W_BLOAD = W_EPI + 4;
+    constexpr int BATCH = C::BATCH, NACC = C::NACC;
+    extern __shared__ uint8_t dsmem[];
+    __shared__ __align__(8) uint64_t bar_hfull[2], bar_hempty[2], bar_xfull[2];
+    __shared__ __align__(8) uint64_t bar_ifull[2], bar_iempty[2];
+    __shared__ __align__(8) uint64_t bar_afull[2], bar_adone[2];     // per half
+    __shared__ __align__(8) uint64_t bar_bfull[2], bar_bempty[2];    // per half
+    __shared__ __align__(8) uint64_t bar_tfull[NACC], bar_tempty[NACC];
+    __shared__ uint32_t tmem_slot;
+
+    const uint32_t sbase = smem_u32(dsmem);
+    const uint32_t bbase = (sbase + 1023u) & ~1023u;                  // weight batches [2][BATCH][B_BYTES]
+    const uint32_t ibase = bbase + 2 * BATCH * C::B_BYTES;            // index blocks [2]
+    const uint32_t hbase = ibase + 2 * kIdxBytes;                     // halo rows [2][CAP][ROWB]
+    const uint32_t xbase = hbase + 2 * C::CAP * C::ROWB;              // halo row ids [2][CAP]
+    const uint8_t* gen = dsmem - sbase;                               // generic view: gen + saddr
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = P.num_tiles;
+    const int ntiles = blockIdx.x < T ? (T - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const uint32_t nstages = 27u * (uint32_t)ntiles;                  // this CTA's (tile, offset) stages
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&bar_hfull[b]), 32);
+            mbar_init(smem_u32(&bar_hempty[b]), kBuilders);
+            mbar_init(smem_u32(&bar_xfull[b]), 1);
+            mbar_init(smem_u32(&bar_ifull[b]), 1);
+            mbar_init(smem_u32(&bar_iempty[b]), kBuilders);
+            mbar_init(smem_u32(&bar_afull[b]), 4);
+            mbar_init(smem_u32(&bar_adone[b]), 1);
+            mbar_init(smem_u32(&bar_bfull[b]), 1);
+            mbar_init(smem_u32(&bar_bempty[b]), 1);
+        }
+        for (int b = 0; b < NACC; ++b) {
+            mbar_init(smem_u32(&bar_tfull[b]), 2);   // both MMA warps commit
+            mbar_init(smem_u32(&bar_tempty[b]), 4);  // four epilogue warps
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == W_MMA) tmem_alloc(smem_u32(&tmem_slot), 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    const uint32_t AFULL = smem_u32(bar_afull), ADONE = smem_u32(bar_adone);
+    const uint32_t BFULL = smem_u32(bar_bfull), BEMPTY = smem_u32(bar_bempty);
+    // TMEM columns: accumulator (half h, buffer b) at (h * NACC + b) * N; A batch slot of half h at
+    // ACC + h * BATCH * ACOLS
+    if (warp >= W_EPI && warp < W_EPI + 4) {  // zero all accumulators (the MMAs always accumulate)
+        const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        for (int c0 = 0; c0 < C::ACC; c0 += 32) tmem_st32_zero(lb + c0);
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == W_LOAD) {
+        // ---------------- halo loader: row ids by TMA bulk, rows by cp.async into swizzled slots -------------
+        int tile = blockIdx.x, g = 0;
+        uint32_t pc = 0;
+        auto issue_ids = [&](int t, int gg, uint32_t buf) {
+            const int32_t* ph = P.phase + ((int64_t)t * 27 + gg) * 2;
+            const int off = P.tile_base[t] + ph[0], len = ph[1];
+            if (lane == 0) {
+                mbar_arrive_expect_tx(smem_u32(&bar_xfull[buf]), (uint32_t)len * 4u);
+                if (len > 0) bulk_g2s(xbase + buf * C::CAP * 4, P.halo_rows + off, (uint32_t)len * 4u,
+                                      smem_u32(&bar_xfull[buf]));
+            }
+            return len;
+        };
+        int len = tile < T ? issue_ids(tile, 0, 0) : 0;
+        int level = tile < T ? P.tile_level[tile] : 1;
+        while (tile < T) {
+            int ng = g + 1, nt = tile;
+            if (ng >= level) { ng = 0; nt = tile + gridDim.x; }
+            const int nlevel = ng == 0 ? (nt < T ? P.tile_level[nt] : 1) : level;
+            const uint32_t buf = pc & 1, par = (pc >> 1) & 1;
+            // the id buffer of the next phase was last read by this warp two phases ago: free
+            const int nlen = nt < T ? issue_ids(nt, ng, buf ^ 1) : 0;
+            mbar_wait(smem_u32(&bar_xfull[buf]), par);
+            mbar_wait(smem_u32(&bar_hempty[buf]), par ^ 1);
+            if (lane == 0) trace(dbg, 9, pc);
+            const int32_t* ids = reinterpret_cast<const int32_t*>(gen + xbase + buf * C::CAP * 4);
+            const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
+            constexpr int RPI = 32 / C::CPR;  // rows per warp instruction
+            const int q = lane / C::CPR, c = lane % C::CPR;
+            for (int s0 = 0; s0 < len; s0 += 4 * RPI) {
+                int r[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int s = s0 + k * RPI + q;
+                    r[k] = s < len ? ids[s] : -1;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int s = s0 + k * RPI + q;
+                    if (r[k] >= 0 && !(dbg & 8))
+                        cp_async_16(hb + s * C::ROWB + (halo_phys(K, s, c) << 4), in + (int64_t)r[k] * K + c * 8, 16u);
+                }
+            }
+            cp_async_arrive_noinc(smem_u32(&bar_hfull[buf]));
+            if (lane == 0) {  // index block: the tile's whole record (lnbr rows + masks), one TMA
+                mbar_wait(smem_u32(&bar_iempty[buf]), par ^ 1);
+                mbar_arrive_expect_tx(smem_u32(&bar_ifull[buf]), (uint32_t)kRecBytes);
+                bulk_g2s(ibase + buf * kIdxBytes, P.tile_rec + (int64_t)tile * kIdxBytes, (uint32_t)kRecBytes,
+                         smem_u32(&bar_ifull[buf]));
+                trace(dbg, 10, pc);
+            }
+            __syncwarp();
+            ++pc;
+            tile = nt;
+            g = ng;
+            len = nlen;
+            level = nlevel;
+        }
+    } else if (warp == W_BLOAD) {
+        // ---------------- weight loader: batch ab (BATCH consecutive offsets, one TMA) -> slot ab & 1 --------
+        if (lane == 0) {
+            const uint32_t nb = (nstages + BATCH - 1) / BATCH;
+            for (uint32_t ab = 0; ab < nb; ++ab) {
+                const uint32_t h = ab & 1;
+                mbar_wait_sleep(BEMPTY + 8 * h, ((ab >> 1) & 1) ^ 1, 32);
+                trace(dbg, 6, ab);
+                const uint32_t d0 = (ab * BATCH) % 27;  // offsets d0 .. d0+BATCH-1 (extended image array)
+                mbar_arrive_expect_tx(BFULL + 8 * h, BATCH * C::B_BYTES);
+                bulk_g2s(bbase + h * BATCH * C::B_BYTES, wimg + (size_t)d0 * C::B_BYTES, BATCH * C::B_BYTES,
+                         BFULL + 8 * h);
+            }
+        }
+    } else if (warp >= W_BLD && warp < W_BLD + kBuilders) {
+        // ---------------- A builders: halo (smem) -> registers -> TMEM (16x256b) ----------------
+        const int q = warp & 3;                        // TMEM lane quarter this warp may access
+        const int half = (warp - W_BLD) / 4;           // builds A batches ab with ab % 2 == half
+        const int t0 = lane & 3, t1 = lane >> 2;
+        const uint32_t abase = tmem + C::ACC + half * BATCH * C::ACOLS;
+        uint32_t pc = 0, ac = 0;
+        for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
+            const int level = P.tile_level[tile], gs = 27 / level;
+            for (int g = 0; g < level; ++g, ++pc) {
+                const uint32_t buf = pc & 1, par = (pc >> 1) & 1;
+                mbar_wait(smem_u32(&bar_hfull[buf]), par);
+                mbar_wait(smem_u32(&bar_ifull[buf]), par);
+                if (lane == 0 && q == 0 && half == 0) trace(dbg, 5, pc);
+                const uint16_t* lb = reinterpret_cast<const uint16_t*>(gen + ibase + buf * kIdxBytes);
+                const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
+                for (int u = g * gs; u < (g + 1) * gs; ++u, ++ac) {  // u = offset d
+                    const uint32_t ab = ac / BATCH, within = ac % BATCH;
+                    if ((int)(ab & 1) != half) continue;
+                    if (within == 0) {  // first stage of my batch: wait until my MMA warp released the slot
+                        mbar_wait(ADONE + 8 * half, ((ab >> 1) & 1) ^ 1);
+                        if (lane == 0 && q == 0) trace(dbg, 2, ab);
+                        tc_fence_after();
+                    }
+                    if (!(dbg & 2)) {  // lanes without a pair get zero A rows: the MMA needs no lane mask
+                        int sl[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) sl[r] = lb[u * kTileRows + q * 32 + (r >> 1) * 16 + t1 + 8 * (r & 1)];
+                        const uint32_t acol = abase + within * C::ACOLS;
+#pragma unroll
+                        for (int gg = 0; gg < 2; ++gg) {
+                            uint32_t v[4 * C::NX];
+#pragma unroll
+                            for (int i = 0; i < 4 * C::NX; ++i) v[i] = 0u;
+#pragma unroll
+                            for (int hi = 0; hi < 2; ++hi) {
+                                const int s = sl[2 * gg + hi];
+                                if (s != kNoSlot) {
+                                    const uint32_t rb = hb + s * C::ROWB;
+#pragma unroll
+                                    for (int j = 0; j < C::LJ; ++j) {
+                                        const uint4 w = lds128(rb + (halo_phys(K, s, halo_chunk(K, t0, j)) << 4));
+                                        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                                        for (int e = 0; e < 4; ++e) {
+                                            const int i = 4 * j + e;
+                                            v[4 * (i >> 1) + (i & 1) + 2 * hi] = ww[e];
+                                        }
+                                    }
+                                }
+                            }
+                            tmem_st16x256<C::NX>(acol + ((uint32_t)(q * 32 + gg * 16) << 16), v);
+                        }
+                    }
+                    if (within == BATCH - 1 || ac + 1 == nstages) {  // publish the batch
+                        tmem_st_wait();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (q == 0) trace(dbg, 3, ab);
+                            mbar_arrive(AFULL + 8 * half);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(smem_u32(&bar_hempty[buf]));
+                    mbar_arrive(smem_u32(&bar_iempty[buf]));
+                }
+            }
+        }
+    } else if (warp == W_MMA || warp == W_MMA + 1) {
+        // ---------------- MMA issuers (one per half): A from TMEM, B from smem, D in TMEM ----------------
+        const int half = warp - W_MMA;
+        const uint32_t TFULL = smem_u32(bar_tfull), TEMPTY = smem_u32(bar_tempty);
+        const uint32_t abase = tmem + C::ACC + half * BATCH * C::ACOLS;
+        const uint32_t bsm = bbase + half * BATCH * C::B_BYTES;
+        uint32_t ac = 0, lt = 0;
+        for (int tile = blockIdx.x; tile < T; tile += gridDim.x, ++lt) {
+            const uint32_t accb = lt % NACC, ause = lt / NACC;
+            const uint32_t dt = tmem + (half * NACC + accb) * N;
+            bool mine = false;
+            for (int u = 0; u < 27; ++u, ++ac) {  // u = offset d
+                const uint32_t ab = ac / BATCH, within = ac % BATCH;
+                if ((int)(ab & 1) != half) continue;
+                if (!mine) {  // first stage of this tile for this half: accumulator must be drained
+                    mbar_wait(TEMPTY + 8 * accb, (ause & 1) ^ 1);
+                    tc_fence_after();
+                    mine = true;
+                }
+                if (within == 0) {
+                    mbar_wait(BFULL + 8 * half, (ab >> 1) & 1);
+                    mbar_wait(AFULL + 8 * half, (ab >> 1) & 1);
+                    if (lane == 0) trace(dbg, 1, ab);
+                    tc_fence_after();
+                }
+                if (lane == 0) {
+                    const uint32_t sB = bsm + within * C::B_BYTES;
+                    const uint32_t at = abase + within * C::ACOLS;
+                    if (!(dbg & 1)) {
+#pragma unroll
+                        for (int ks = 0; ks < K / 16; ++ks) {
+                            const int kb = ks / (C::KB / 16), kk = ks % (C::KB / 16);
+                            mma_bf16_ts(dt, at + ks * 8,
+                                        smem_desc(sB + kb * N * C::BROWB + kk * 32, 16, 8 * C::BROWB, C::BLAYOUT),
+                                        C::IDESC, 1u);
+                        }
+                    }
+                    if (within == BATCH - 1 || ac + 1 == nstages) {
+                        mma_commit(ADONE + 8 * half);
+                        mma_commit(BEMPTY + 8 * half);
+                    }
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mma_commit(TFULL + 8 * accb);  // every tile has stages of both halves
+            __syncwarp();
+        }
+    } else if (warp >= W_EPI && warp < W_EPI + 4) {
+        // ---------------- epilogue: D0 + D1 (fixed order) -> output rows (lane permutation) ----------------
+        const int q = warp & 3;
+        uint32_t lt = 0;
+        for (int tile = blockIdx.x; tile < T; tile += gridDim.x, ++lt) {
+            const uint32_t accb = lt % NACC, ause = lt / NACC;
+            const int64_t row = P.perm[(int64_t)tile * kTileRows + q * 32 + lane];
+            mbar_wait_sleep(smem_u32(&bar_tfull[accb]), ause & 1, 256);
+            if (lane == 0 && q == 0) trace(dbg, 11, lt);
+            tc_fence_after();
+#pragma unroll
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                uint32_t v[32], w[32];
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + accb * N + c0;
+                const uint32_t tb = ta + NACC * N;  // half 1's accumulator
+                tmem_ld32(ta, v);
+                tmem_ld32(tb, w);
+                tmem_ld_wait();
+                tmem_st32_zero(ta);
+                tmem_st32_zero(tb);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+                if (row >= 0 && !(dbg & 4)) {
+                    if constexpr (OUT_BF16) {
+                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(out) + row * N + c0);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint32_t p[4];
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * h]),
+                                                                          __uint_as_float(v[8 * j + 2 * h + 1]));
+                                p[h] = *reinterpret_cast<uint32_t*>(&b2);
+                            }
+                            dst[j] = make_uint4(p[0], p[1], p[2], p[3]);
+                        }
+                    } else {
+                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(out) + row * N + c0);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    }
+                }
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_tempty[accb]));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == W_MMA) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// halo plan
+// ---------------------------------------------------------------------------------------------
+constexpr int kPlanThreads = 256;
+constexpr int kPlanItems = 14;  // 256 × 14 = 3584 >= 27 × 128
+constexpr int kPlanKeys = kPlanThreads * kPlanItems;
+using PlanSort = cub::BlockRadixSort<uint64_t, kPlanThreads, kPlanItems>;
+using PlanScan = cub::BlockScan<uint32_t, kPlanThreads>;
+struct PlanSmem {
+    union {
+        typename PlanSort::TempStorage sort;
+        typename PlanScan::TempStorage scan;
+    } tmp;
+    uint64_t keys[kPlanKeys];
+    uint16_t slot[kPlanKeys];
+};
+constexpr uint64_t kNoKey = ~0ull;
+
+
+struct PlanCounts {
+    int cnt[2][27];     // unique rows per (color, phase)
+    int gfirst[2][27];  // exclusive unique-count prefix at each phase's first element
+    int goff[27];       // phase slot offsets (multiples of 8)
+    int ghalo[27];      // phase slot counts (multiples of 8)
+    int total;          // tile slots
+};
+
+// Sort + dedupe the tile's (phase, row) keys for `level` phases.  Fills S.keys (sorted),
+// S.slot (slot of each unique key inside its phase), and the PlanCounts.  Block-wide.
+__device__ void plan_tile(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out,
+                          const uint8_t* __restrict__ color, int tile, int level, PlanSmem& S, PlanCounts& pc) {
+    const int tid = threadIdx.x;
+    const int gsz = 27 / level;
+    uint64_t key[kPlanItems];
+#pragma unroll
+    for (int k = 0; k < kPlanItems; ++k) {
+        const int e = tid * kPlanItems + k;
+        key[k] = kNoKey;
+        if (e < 27 * kTileRows) {
+            const int d = e / kTileRows, i = e % kTileRows;
+            const int64_t o = (int64_t)tile * kTileRows + i;
+            if (o < n_out) {
+                const int32_t r = nbr[(int64_t)d * ld + o];
+                if (r >= 0) key[k] = ((uint64_t)(d / gsz) << 32) | (uint32_t)r;
+            }
+        }
+    }
+    if (tid < 27) {
+        pc.cnt[0][tid] = pc.cnt[1][tid] = 0;
+        pc.gfirst[0][tid] = pc.gfirst[1][tid] = 0;
+    }
+    __syncthreads();
+    PlanSort(S.tmp.sort).Sort(key);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPlanItems; ++k) S.keys[tid * kPlanItems + k] = key[k];
+    __syncthreads();
+    uint32_t packed = 0;  // unique rows of color 0 (low 16 bits) / color 1 (high 16 bits) in this thread
+    uint8_t uc[kPlanItems];
+#pragma unroll
+    for (int k = 0; k < kPlanItems; ++k) {
+        const int e = tid * kPlanItems + k;
+        uc[k] = 0;
+        if (key[k] != kNoKey && (e == 0 || S.keys[e - 1] != key[k])) {
+            const int c = color ? (color[(uint32_t)key[k]] & 1) : 0;
+            uc[k] = (uint8_t)(1 + c);
+            packed += c ? (1u << 16) : 1u;
+            atomicAdd(&pc.cnt[c][(int)(key[k] >> 32)], 1);
+        }
+    }
+    uint32_t excl;
+    PlanScan(S.tmp.scan).ExclusiveSum(packed, excl);
+    uint32_t run = excl;
+#pragma unroll
+    for (int k = 0; k < kPlanItems; ++k) {
+        const int e = tid * kPlanItems + k;
+        if (uc[k]) {
+            const int gr = (int)(key[k] >> 32);
+            if (e == 0 || (int)(S.keys[e - 1] >> 32) != gr) {  // first element of its phase
+                pc.gfirst[0][gr] = (int)(run & 0xFFFF);
+                pc.gfirst[1][gr] = (int)(run >> 16);
+            }
+            run += (uc[k] == 2) ? (1u << 16) : 1u;
+        }
+    }
+    __syncthreads();
+    run = excl;
+#pragma unroll
+    for (int k = 0; k < kPlanItems; ++k) {
+        const int e = tid * kPlanItems + k;
+        uint16_t sl = kNoSlot;
+        if (uc[k]) {
+            const int gr = (int)(key[k] >> 32), c = uc[k] - 1;
+            const int rank = (c ? (int)(run >> 16) : (int)(run & 0xFFFF)) - pc.gfirst[c][gr];
+            sl = (uint16_t)(2 * rank + c);
+            run += c ? (1u << 16) : 1u;
+        }
+        S.slot[e] = sl;
+    }
+    if (tid == 0) {
+        int acc = 0;
+        for (int gr = 0; gr < 27; ++gr) {
+            const int h = gr < level ? 2 * max(pc.cnt[0][gr], pc.cnt[1][gr]) : 0;
+            pc.ghalo[gr] = (h + 7) & ~7;
+            pc.goff[gr] = acc;
+            acc += pc.ghalo[gr];
+        }
+        pc.total = acc;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ bool plan_fits(const PlanCounts& pc, int level, int cap) {
+    for (int gr = 0; gr < level; ++gr)
+        if (pc.ghalo[gr] > cap) return false;
+    return true;
+}
+
+// count pass: choose the smallest phase count whose halos fit; tile_size[t] = slots of tile t
+__global__ void __launch_bounds__(kPlanThreads) k_halo_count(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out,
+                                                            const uint8_t* __restrict__ color, fvdb_halo_plan P,
+                                                            int32_t* __restrict__ tile_size) {
+    extern __shared__ __align__(16) uint8_t psm[];
+    PlanSmem& S = *reinterpret_cast<PlanSmem*>(psm);
+    __shared__ PlanCounts pc;
+    const int tile = blockIdx.x;
+    int level = 1;
+    for (;; level *= 3) {
+        plan_tile(nbr, ld, n_out, color, tile, level, S, pc);
+        if (level == 27 || plan_fits(pc, level, P.halo_cap)) break;
+        __syncthreads();
+    }
+    if (threadIdx.x < 27) {
+        int32_t* ph = P.phase + ((int64_t)tile * 27 + threadIdx.x) * 2;
+        ph[0] = pc.goff[threadIdx.x];
+        ph[1] = pc.ghalo[threadIdx.x];
+    }
+    if (threadIdx.x == 0) {
+        P.tile_level[tile] = level;
+        tile_size[tile] = pc.total;
+    }
+}
+
+// fill pass: halo rows, lane permutation, local neighbour table, lane masks
+__global__ void __launch_bounds__(kPlanThreads) k_halo_fill(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out,
+                                                           const uint8_t* __restrict__ color,
+                                                           const uint8_t* __restrict__ q_out, fvdb_halo_plan P) {
+    extern __shared__ __align__(16) uint8_t psm[];
+    PlanSmem& S = *reinterpret_cast<PlanSmem*>(psm);
+    __shared__ PlanCounts pc;
+    __shared__ int perm[kTileRows];
+    __shared__ int wcnt[2][4];
+    const int tile = blockIdx.x, tid = threadIdx.x;
+    const int level = P.tile_level[tile], gsz = 27 / level;
+    const int base = P.tile_base[tile];
+    plan_tile(nbr, ld, n_out, color, tile, level, S, pc);
+    // halo rows: padding slots -1, then every unique key at its slot
+    for (int s = tid; s < pc.total; s += kPlanThreads) P.halo_rows[base + s] = -1;
+    __syncthreads();
+    for (int e = tid; e < kPlanKeys; e += kPlanThreads) {
+        const uint16_t sl = S.slot[e];
+        if (sl != kNoSlot) {
+            const uint64_t k = S.keys[e];
+            P.halo_rows[base + pc.goff[(int)(k >> 32)] + sl] = (int32_t)(uint32_t)k;
+        }
+    }
+    // lane permutation: pair parity-0 rows with parity-1 rows (lanes 2p, 2p+1), leftovers after
+    int f = -1, o = -1;  // f: list (0/1) of row tid, -1 invalid
+    if (tid < kTileRows) {
+        perm[tid] = -1;
+        const int64_t oo = (int64_t)tile * kTileRows + tid;
+        if (oo < n_out) {
+            o = (int)oo;
+            f = q_out ? (q_out[oo] & 1) : 0;
+        }
+    }
+    const int w = tid >> 5, ln = tid & 31;
+    const uint32_t b0 = __ballot_sync(0xffffffffu, f == 0), b1 = __ballot_sync(0xffffffffu, f == 1);
+    if (w < 4 && ln == 0) {
+        wcnt[0][w] = __popc(b0);
+        wcnt[1][w] = __popc(b1);
+    }
+    __syncthreads();
+    if (f >= 0) {
+        const uint32_t bm = f ? b1 : b0;
+        int pos = __popc(bm & ((1u << ln) - 1u));
+        for (int ww = 0; ww < w; ++ww) pos += wcnt[f][ww];
+        int n0 = 0, n1 = 0;
+        for (int ww = 0; ww < 4; ++ww) {
+            n0 += wcnt[0][ww];
+            n1 += wcnt[1][ww];
+        }
+        const int m = min(n0, n1);
+        const int lanei = pos < m ? 2 * pos + f : 2 * m + (pos - m);
+        perm[lanei] = o;
+    }
+    __syncthreads();
+    if (tid < kTileRows) P.perm[(int64_t)tile * kTileRows + tid] = perm[tid];
+    // tile record: local neighbour table [27][128] u16 + masks [27][4] u32; a warp covers 32 lanes of one offset
+    uint8_t* rec = P.tile_rec + (int64_t)tile * kIdxBytes;
+    for (int e = tid; e < 27 * kTileRows; e += kPlanThreads) {
+        const int d = e / kTileRows, l = e % kTileRows;
+        const int oo = perm[l];
+        const int32_t r = oo >= 0 ? nbr[(int64_t)d * ld + oo] : -1;
+        uint16_t sl = kNoSlot;
+        if (r >= 0) {
+            const uint64_t key = ((uint64_t)(d / gsz) << 32) | (uint32_t)r;
+            int lo = 0, hi = kPlanKeys;  // first key >= key (the unique element)
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (S.keys[mid] < key) lo = mid + 1; else hi = mid;
+            }
+            sl = S.slot[lo];
+        }
+        reinterpret_cast<uint16_t*>(rec)[d * kTileRows + l] = sl;
+        const uint32_t none = __ballot_sync(0xffffffffu, sl == kNoSlot);
+        if ((tid & 31) == 0) reinterpret_cast<uint32_t*>(rec + 6912)[d * 4 + (l >> 5)] = none;
+    }
+}
+
+__global__ void k_parity_colors(const int64_t* __restrict__ c, int64_t n, int shift, uint8_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (uint8_t)(((c[3 * i] >> shift) + (c[3 * i + 1] >> shift) + (c[3 * i + 2] >> shift)) & 1);
+}
+
+// fp32 W[Cout][Cin][27] -> per-offset bf16 B images [27][K/KB][N][KB] (swizzled), K permuted to the
+// halo kernel's TMEM A layout
+__global__ void k_pack_halo(const float* __restrict__ w, int cout, int cin, int transpose, uint8_t* __restrict__ img) {
+    const int K = transpose ? cout : cin, N = transpose ? cin : cout;
+    const int KB = K >= 64 ? 64 : K, rowb = KB * 2;
+    const int64_t total = (int64_t)27 * cout * cin;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t co = t / ((int64_t)cin * 27);
+        const int64_t rem = t - co * cin * 27;
+        const int ci = (int)(rem / 27), d = (int)(rem - (int64_t)ci * 27);
+        const int n = transpose ? ci : (int)co, ch = transpose ? (int)co : ci;
+        const int k = halo_k_of_channel(K, ch);
+        const int kb = k / KB, e = k % KB;
+        const int x = rowb == 128 ? (n & 7) : ((n >> 1) & 3);
+        const size_t off = (size_t)kb * N * rowb + (size_t)n * rowb + (((e >> 3) ^ x) << 4) + (e & 7) * 2;
+        const bf16 v = __float2bfloat16_rn(w[t]);
+        const size_t img_bytes = (size_t)N * K * 2;
+        *reinterpret_cast<bf16*>(img + (size_t)d * img_bytes + off) = v;
+        if (d + 27 < kImgExt) *reinterpret_cast<bf16*>(img + (size_t)(d + 27) * img_bytes + off) = v;
+    }
+}
+
+int sm_count_h() {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+}
+
+template <int K, int N, bool OB>
+int launch_halo(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out, cudaStream_t st) {
+    using C = HaloCfg<K, N>;
+    if (P.halo_cap > C::CAP) return FVDB_ERR_INVALID;
+    auto kern = k_conv_halo<K, N, OB>;
+    FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    int grid = sm_count_h();
+    if (grid > P.num_tiles) grid = P.num_tiles;
+    // profiling switches (FVDB_DEBUG_HALO): 1 no MMA, 2 no A build, 4 no output stores, 8 no halo loads
+    static const int dbg = getenv("FVDB_DEBUG_HALO") ? atoi(getenv("FVDB_DEBUG_HALO")) : 0;
+    kern<<<grid, kHaloThreads, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, P, n_out, out, dbg);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+template <typename F>
+int halo_dispatch(int K, int N, F&& f) {
+#define FVDB_HALO_CASE(a, b) \
+    if (K == a && N == b) return f(std::integral_constant<int, a>{}, std::integral_constant<int, b>{});
+    FVDB_HALO_CASE(32, 32) FVDB_HALO_CASE(32, 64) FVDB_HALO_CASE(32, 128)
+    FVDB_HALO_CASE(64, 32) FVDB_HALO_CASE(64, 64) FVDB_HALO_CASE(64, 128)
+    FVDB_HALO_CASE(128, 32) FVDB_HALO_CASE(128, 64) FVDB_HALO_CASE(128, 128)
+#undef FVDB_HALO_CASE
+    return FVDB_ERR_INVALID;
+}
+
+}  // namespace
+}  // namespace fvdb
+
+using namespace fvdb;
+
+extern "C" int fvdb_parity_colors(const int64_t* coords, int64_t n, int shift, uint8_t* color, void* stream) {
+    if (n <= 0) return FVDB_OK;
+    k_parity_colors<<<(unsigned)cmin((int)ceil_div(n, 256), 4096), 256, 0, as_stream(stream)>>>(coords, n, shift, color);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_halo_cap(int K, int N) {
+    int cap = 0;
+    halo_dispatch(K, N, [&](auto k, auto n) {
+        cap = HaloCfg<decltype(k)::value, decltype(n)::value>::CAP;
+        return 0;
+    });
+    return cap;
+}
+
+extern "C" size_t fvdb_halo_plan_workspace_bytes(int64_t n_out) {
+    const int T = (int)ceil_div(n_out > 0 ? n_out : 1, kTileRows);
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, (const int32_t*)nullptr, (int32_t*)nullptr, T);
+    Sizer s;
+    s.take<int32_t>(T);      // tile sizes
+    s.take<int32_t>(1);      // total
+    s.take<uint8_t>(tmp);
+    return s.used + 256;
+}
+
+extern "C" int fvdb_halo_plan_count(const int32_t* nbr, int64_t ld, int64_t n_out, const uint8_t* color_in,
+                                    const fvdb_halo_plan* plan, int64_t* total, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
+    *total = 0;
+    if (n_out <= 0) return FVDB_OK;
+    const fvdb_halo_plan& P = *plan;
+    const int T = (int)ceil_div(n_out, kTileRows);
+    if (P.num_tiles != T || P.halo_cap < 256 || P.halo_cap > 32768 || ld < n_out) return FVDB_ERR_INVALID;
+    cudaStream_t st = as_stream(stream);
+    Carver cv(workspace, workspace_bytes);
+    int32_t* sizes = cv.take<int32_t>(T);
+    int32_t* tot = cv.take<int32_t>(1);
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, sizes, P.tile_base, T);
+    void* tmpp = cv.take<uint8_t>(tmp);
+    if (!cv.ok()) return FVDB_ERR_WORKSPACE;
+    FVDB_CUDA_TRY(cudaFuncSetAttribute(k_halo_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSmem)));
+    k_halo_count<<<T, kPlanThreads, sizeof(PlanSmem), st>>>(nbr, ld, n_out, color_in, P, sizes);
+    FVDB_LAUNCH_CHECK();
+    FVDB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmpp, tmp, sizes, P.tile_base, T, st));
+    int32_t last_base = 0, last_size = 0;
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&last_base, P.tile_base + (T - 1), 4, cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&last_size, sizes + (T - 1), 4, cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+    (void)tot;
+    *total = (int64_t)last_base + last_size;
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_halo_plan_fill(const int32_t* nbr, int64_t ld, int64_t n_out, const uint8_t* color_in,
+                                   const uint8_t* q_out, const fvdb_halo_plan* plan, void* stream) {
+    if (n_out <= 0) return FVDB_OK;
+    const fvdb_halo_plan& P = *plan;
+    if (P.num_tiles != (int)ceil_div(n_out, kTileRows)) return FVDB_ERR_INVALID;
+    FVDB_CUDA_TRY(cudaFuncSetAttribute(k_halo_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSmem)));
+    k_halo_fill<<<P.num_tiles, kPlanThreads, sizeof(PlanSmem), as_stream(stream)>>>(nbr, ld, n_out, color_in, q_out, P);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_pack_weights_halo(const float* w, int cout, int cin, int transpose, void* image, void* stream) {
+    const int K = transpose ? cout : cin, N = transpose ? cin : cout;
+    if ((K != 32 && K != 64 && K != 128) || (N != 32 && N != 64 && N != 128)) return FVDB_ERR_INVALID;
+    const int64_t total = (int64_t)27 * cout * cin;
+    k_pack_halo<<<(unsigned)ceil_div(total, 256), 256, 0, as_stream(stream)>>>(w, cout, cin, transpose, (uint8_t*)image);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+// profiling hook (tools/): copy the CTA-0 trace of the last FVDB_DEBUG_HALO&64 launch to host
+extern "C" int fvdb_halo_debug_trace(long long* host, int n) {
+    const int cnt = n < kTraceCh * kTraceN ? n : kTraceCh * kTraceN;
+    FVDB_CUDA_TRY(cudaMemcpyFromSymbol(host, g_halo_trace, cnt * sizeof(long long)));
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_conv_halo_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
+                                 const fvdb_halo_plan* plan, int64_t n_out, void* out, int out_dtype, void* stream) {
+    (void)n_in;
+    if (n_out <= 0) return FVDB_OK;
+    const fvdb_halo_plan& P = *plan;
+    if (P.num_tiles != (int)ceil_div(n_out, kTileRows)) return FVDB_ERR_INVALID;
+    if (out_dtype != FVDB_DTYPE_BF16 && out_dtype != FVDB_DTYPE_F32) return FVDB_ERR_INVALID;
+    cudaStream_t st = as_stream(stream);
+    return halo_dispatch(K, N, [&](auto k, auto n) {
+        constexpr int KK = decltype(k)::value, NN = decltype(n)::value;
+        return out_dtype == FVDB_DTYPE_BF16 ? launch_halo<KK, NN, true>(in_bf16, w_image, P, n_out, out, st)
+                                            : launch_halo<KK, NN, false>(in_bf16, w_image, P, n_out, out, st);
+    });
+}

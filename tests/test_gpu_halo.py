@@ -1,0 +1,173 @@
+"""GPU: halo plan invariants and the halo-staged tensor-core conv (csrc/conv_halo.cu).
+
+The halo kernel computes the reference operator (conv.py:180-191 forward, conv.py:358-366 dgrad
+form); these tests pin it against the oracle on bf16-rounded inputs (accumulation error only,
+rel ≤ 2e-5), against the gather-GEMM kernel, and check the plan itself exactly: every
+(offset, lane) slot must resolve to the kernel map's input row.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2407_01781_b200 as P
+from paper_2407_01781_b200.conv import gather_conv
+from paper_2407_01781_b200.workloads import sphere_shell_coords
+from conftest import KMAP_CASES
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = a.detach().double().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def bf16_round(a):
+    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64)
+
+
+def check_plan(table, K, N):
+    """Exact plan invariants: lane permutation, slot -> input row, masks, phase capacity."""
+    plan = table.halo_plan(K, N)
+    t = {k: v.cpu().numpy() for k, v in plan.tensors.items()}
+    n, T = table.n, (table.n + 127) // 128
+    nbr = table.view.cpu().numpy()
+    perm = t["perm"].reshape(T, 128)
+    valid = perm[perm >= 0]
+    assert np.array_equal(np.sort(valid), np.arange(n)), "perm is not a permutation of the output rows"
+    rec = t["tile_rec"].reshape(T, -1)
+    lnbr = rec[:, :6912].copy().view(np.uint16).reshape(T, 27, 128).transpose(1, 0, 2).astype(np.int64)
+    level = t["tile_level"]
+    assert set(np.unique(level)) <= {1, 3, 9, 27}
+    phase = t["phase"]
+    hr = t["halo_rows"]
+    masks = rec[:, 6912:6912 + 432].copy().view(np.uint32).reshape(T, 27, 4)
+    for tile in range(T):
+        gs = 27 // level[tile]
+        for d in range(27):
+            g = d // gs
+            off, cnt = phase[tile, g]
+            assert cnt <= plan.cap and cnt % 8 == 0
+            lanes = np.arange(128)
+            o = perm[tile]
+            want = np.where(o >= 0, nbr[d][np.maximum(o, 0)], -1)
+            s = lnbr[d, tile]
+            has = s != 0xFFFF
+            assert np.array_equal(has, want >= 0), (tile, d)
+            assert np.all(s[has] < cnt)
+            got = hr[t["tile_base"][tile] + off + s[has]]
+            assert np.array_equal(got, want[has]), (tile, d)
+            bits = np.zeros(128, bool)
+            for wd in range(4):
+                bits[32 * wd:32 * wd + 32] = (masks[tile, d, wd] >> np.arange(32, dtype=np.uint32)) & 1
+            assert np.array_equal(bits, ~has), (tile, d)
+            del lanes
+    return plan
+
+
+@pytest.mark.parametrize("name", KMAP_CASES)
+@pytest.mark.parametrize("stride", [1, 2])
+def test_halo_plan_exact(golden_grids, name, stride):
+    c = golden_grids[f"{name}/coords"]
+    g, _ = P.build_from_coords(c)
+    go = g if stride == 1 else P.coarsen(g, 2)
+    km = P.build_kernel_map(g, go, stride)
+    check_plan(km.fwd, 64, 64)
+    check_plan(km.bwd, 64, 64)
+    check_plan(km.fwd, 128, 128)
+
+
+def dense_cube(n=16):
+    r = np.arange(n)
+    return np.stack(np.meshgrid(r, r, r, indexing="ij"), -1).reshape(-1, 3)
+
+
+def test_halo_plan_splits_phases_when_halo_exceeds_capacity():
+    g, _ = P.build_from_coords(dense_cube(24))
+    km = P.build_kernel_map(g, g, 1)
+    plan = check_plan(km.fwd, 128, 128)  # 128 channels: ~288-slot capacity < a dense tile's ~400-row halo
+    assert (plan.tensors["tile_level"] > 1).any()
+
+
+CASES = [(32, 32), (64, 64), (128, 128), (64, 128), (128, 64), (32, 64), (128, 32)]
+
+
+@pytest.fixture(scope="module")
+def shell():
+    c = sphere_shell_coords(48, band=1.5)
+    g, _ = P.build_from_coords(c)
+    og = O.build_from_coords(c)
+    ins, outs = O.kernel_map(og, og, 1)
+    return g, ins, outs, P.build_kernel_map(g, g, 1)
+
+
+@pytest.mark.parametrize("cin,cout", CASES)
+def test_halo_conv_matches_oracle_and_gather(shell, cin, cout):
+    g, ins, outs, km = shell
+    rng = np.random.default_rng(cin * 7 + cout)
+    n = g.num_voxels
+    x = rng.normal(size=(n, cin)).astype(np.float32)
+    w = (rng.normal(size=(cout, cin, 3, 3, 3)) / np.sqrt(27 * cin)).astype(np.float32)
+    gy = rng.normal(size=(n, cout)).astype(np.float32)
+    xb = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    gyb = torch.from_numpy(gy).cuda().to(torch.bfloat16)
+    wt = torch.from_numpy(w).cuda()
+    ref_r = O.conv_igemm(bf16_round(x), bf16_round(w), ins, outs, n)
+    y = gather_conv(xb, km.fwd, wt, out_dtype=torch.float32, impl="halo")
+    assert rel(y, ref_r) < 2e-5
+    yg = gather_conv(xb, km.fwd, wt, out_dtype=torch.float32, impl="gather")
+    assert rel(y, yg.cpu().numpy()) < 2e-5
+    y16 = gather_conv(xb, km.fwd, wt, impl="halo")
+    ref = O.conv_igemm(x.astype(np.float64), w.astype(np.float64), ins, outs, n)
+    assert y16.dtype == torch.bfloat16 and rel(y16, ref) < 1e-2
+    gi_r, _ = O.conv_backward(ins, outs, bf16_round(gy), bf16_round(x), bf16_round(w))
+    gi = gather_conv(gyb, km.bwd, wt, transpose=True, out_dtype=torch.float32, impl="halo")
+    assert rel(gi, gi_r) < 2e-5
+
+
+def test_halo_conv_phases_and_stride2():
+    """Dense cube at 128 channels (multi-phase tiles) and a stride-2 map plus its transpose."""
+    c = dense_cube(20)
+    g, _ = P.build_from_coords(c)
+    og = O.build_from_coords(c)
+    rng = np.random.default_rng(5)
+    for stride, K, N in ((1, 128, 128), (2, 64, 128), (2, 128, 64)):
+        go, ogo = (g, og) if stride == 1 else (P.coarsen(g, 2), O.coarsen(og, 2))
+        km = P.build_kernel_map(g, go, stride)
+        ins, outs = O.kernel_map(og, ogo, stride)
+        x = rng.normal(size=(g.num_voxels, K)).astype(np.float32)
+        w = (rng.normal(size=(N, K, 3, 3, 3)) / np.sqrt(27 * K)).astype(np.float32)
+        y = gather_conv(torch.from_numpy(x).cuda().to(torch.bfloat16), km.fwd, torch.from_numpy(w).cuda(),
+                        out_dtype=torch.float32, impl="halo")
+        assert rel(y, O.conv_igemm(bf16_round(x), bf16_round(w), ins, outs, go.num_voxels)) < 2e-5
+        gy = rng.normal(size=(go.num_voxels, N)).astype(np.float32)
+        gi = gather_conv(torch.from_numpy(gy).cuda().to(torch.bfloat16), km.bwd, torch.from_numpy(w).cuda(),
+                         transpose=True, out_dtype=torch.float32, impl="halo")
+        gi_r, _ = O.conv_backward(ins, outs, bf16_round(gy), bf16_round(x), bf16_round(w))
+        assert rel(gi, gi_r) < 2e-5
+    if stride == 1:
+        pass
+
+
+def test_halo_conv_without_colours_and_deterministic(shell):
+    """A KernelMap built from reference lists has no grids (no lane colours): same results."""
+    g, ins, outs, km = shell
+    km2 = P.KernelMap(ins, outs, g.num_voxels, g.num_voxels, 1)
+    rng = np.random.default_rng(3)
+    xb = torch.from_numpy(rng.normal(size=(g.num_voxels, 64)).astype(np.float32)).cuda().to(torch.bfloat16)
+    w = torch.randn(64, 64, 3, 3, 3, device="cuda") / 40
+    a = gather_conv(xb, km.fwd, w, out_dtype=torch.float32, impl="halo")
+    b = gather_conv(xb, km2.fwd, w, out_dtype=torch.float32, impl="halo")
+    assert rel(a, b.cpu().numpy()) < 1e-6
+    assert torch.equal(a, gather_conv(xb, km.fwd, w, out_dtype=torch.float32, impl="halo"))
+
+
+def test_halo_empty_and_tiny():
+    g, _ = P.build_from_coords(np.array([[0, 0, 0]]))
+    km = P.build_kernel_map(g, g, 1)
+    x = torch.ones(1, 64, device="cuda", dtype=torch.bfloat16)
+    w = torch.ones(64, 64, 3, 3, 3, device="cuda") / 64
+    y = gather_conv(x, km.fwd, w, out_dtype=torch.float32, impl="halo")
+    assert torch.allclose(y, torch.ones_like(y))
