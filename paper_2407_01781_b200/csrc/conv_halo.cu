@@ -92,16 +92,19 @@ struct HaloCfg {
     // accumulator buffers per half: 2 (epilogue overlaps the next tile) when TMEM allows
     static constexpr int NACC = 4 * N + 2 * ACOLS <= 512 ? 2 : 1;
     static constexpr int ACC = 2 * NACC * N;                // accumulator columns (both halves)
-    static constexpr int fits(int b) {
-        return ACC + 2 * b * ACOLS <= 512 &&
-               (kSmemMax - 2048 - (1024 + 2 * b * B_BYTES + 2 * kIdxBytes)) / (2 * (ROWB + 4)) >= 256;
+    // NSL slots per half (2: a half's builders fill one slot while its MMA warp drains the other)
+    static constexpr int fits(int nsl, int b) {
+        return ACC + 2 * nsl * b * ACOLS <= 512 &&
+               (kSmemMax - 2048 - (1024 + 2 * nsl * b * B_BYTES + 2 * kIdxBytes)) / (2 * (ROWB + 4)) >= 256;
     }
-    static constexpr int BATCH = fits(4) ? 4 : (fits(2) ? 2 : 1);  // stages per batch (= weight images per TMA)
-    static constexpr int FIXED = 1024 + 2 * BATCH * B_BYTES + 2 * kIdxBytes;
+    static constexpr int NSL = fits(2, 1) ? 2 : 1;
+    static constexpr int BATCH = fits(NSL, 4) ? 4 : (fits(NSL, 2) ? 2 : 1);  // stages per batch (= images per TMA)
+    static constexpr int SLOT_B = BATCH * B_BYTES;          // weight bytes of one slot
+    static constexpr int FIXED = 1024 + 2 * NSL * SLOT_B + 2 * kIdxBytes;
     static constexpr int CAP = ((kSmemMax - 2048 - FIXED) / (2 * (ROWB + 4))) & ~7;
     static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4);
     static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, N, false, false);
-    static_assert(fits(BATCH) && CAP >= 256, "halo capacity must hold one offset phase (2 x 128 slots)");
+    static_assert(fits(NSL, BATCH) && CAP >= 256, "halo capacity must hold one offset phase (2 x 128 slots)");
     static_assert(27 + BATCH - 1 <= kImgExt, "weight batch wraps past the extended image array");
 };
 
@@ -127,18 +130,18 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 int64_t n_out, void* __restrict__ out, int dbg) {
     using C = HaloCfg<K, N>;
     constexpr int W_LOAD = 0, W_MMA = 1, W_BLD = 3, W_EPI = 3 + kBuilders, W_BLOAD = W_EPI + 4;
-    constexpr int BATCH = C::BATCH, NACC = C::NACC;
+    constexpr int BATCH = C::BATCH, NACC = C::NACC, NSL = C::NSL;
     extern __shared__ uint8_t dsmem[];
     __shared__ __align__(8) uint64_t bar_hfull[2], bar_hempty[2], bar_xfull[2];
     __shared__ __align__(8) uint64_t bar_ifull[2], bar_iempty[2];
-    __shared__ __align__(8) uint64_t bar_afull[2], bar_adone[2];     // per half
-    __shared__ __align__(8) uint64_t bar_bfull[2], bar_bempty[2];    // per half
+    __shared__ __align__(8) uint64_t bar_afull[2 * NSL], bar_adone[2 * NSL];   // per (half, slot)
+    __shared__ __align__(8) uint64_t bar_bfull[2 * NSL];  // per (half, slot); released via bar_adone
     __shared__ __align__(8) uint64_t bar_tfull[NACC], bar_tempty[NACC];
     __shared__ uint32_t tmem_slot;
 
     const uint32_t sbase = smem_u32(dsmem);
-    const uint32_t bbase = (sbase + 1023u) & ~1023u;                  // weight batches [2][BATCH][B_BYTES]
-    const uint32_t ibase = bbase + 2 * BATCH * C::B_BYTES;            // index blocks [2]
+    const uint32_t bbase = (sbase + 1023u) & ~1023u;                  // weight slots [2 halves][NSL][SLOT_B]
+    const uint32_t ibase = bbase + 2 * NSL * C::SLOT_B;               // index blocks [2]
     const uint32_t hbase = ibase + 2 * kIdxBytes;                     // halo rows [2][CAP][ROWB]
     const uint32_t xbase = hbase + 2 * C::CAP * C::ROWB;              // halo row ids [2][CAP]
     const uint8_t* gen = dsmem - sbase;                               // generic view: gen + saddr
@@ -154,10 +157,11 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             mbar_init(smem_u32(&bar_xfull[b]), 1);
             mbar_init(smem_u32(&bar_ifull[b]), 1);
             mbar_init(smem_u32(&bar_iempty[b]), kBuilders);
+        }
+        for (int b = 0; b < 2 * NSL; ++b) {
             mbar_init(smem_u32(&bar_afull[b]), 4);
             mbar_init(smem_u32(&bar_adone[b]), 1);
             mbar_init(smem_u32(&bar_bfull[b]), 1);
-            mbar_init(smem_u32(&bar_bempty[b]), 1);
         }
         for (int b = 0; b < NACC; ++b) {
             mbar_init(smem_u32(&bar_tfull[b]), 2);   // both MMA warps commit
@@ -171,9 +175,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
     const uint32_t AFULL = smem_u32(bar_afull), ADONE = smem_u32(bar_adone);
-    const uint32_t BFULL = smem_u32(bar_bfull), BEMPTY = smem_u32(bar_bempty);
-    // TMEM columns: accumulator (half h, buffer b) at (h * NACC + b) * N; A batch slot of half h at
-    // ACC + h * BATCH * ACOLS
+    const uint32_t BFULL = smem_u32(bar_bfull);
+    // TMEM columns: accumulator (half h, buffer b) at (h * NACC + b) * N; A slot (h, sl) at
+    // ACC + (h * NSL + sl) * BATCH * ACOLS.  Batch ab -> half ab & 1, half-local index hb = ab >> 1,
+    // slot hb % NSL, use count hb / NSL.
     if (warp >= W_EPI && warp < W_EPI + 4) {  // zero all accumulators (the MMAs always accumulate)
         const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         for (int c0 = 0; c0 < C::ACC; c0 += 32) tmem_st32_zero(lb + c0);
@@ -247,76 +252,89 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         if (lane == 0) {
             const uint32_t nb = (nstages + BATCH - 1) / BATCH;
             for (uint32_t ab = 0; ab < nb; ++ab) {
-                const uint32_t h = ab & 1;
-                mbar_wait_sleep(BEMPTY + 8 * h, ((ab >> 1) & 1) ^ 1, 32);
+                const uint32_t hbi = ab >> 1, k = (ab & 1) * NSL + hbi % NSL, use = hbi / NSL;
+                mbar_wait_sleep(ADONE + 8 * k, (use & 1) ^ 1, 32);  // slot k's previous batch is done
                 trace(dbg, 6, ab);
+                if ((dbg & 16) && ab >= 2u * NSL) {  // profiling: reuse stale weight slots
+                    mbar_arrive(BFULL + 8 * k);
+                    continue;
+                }
                 const uint32_t d0 = (ab * BATCH) % 27;  // offsets d0 .. d0+BATCH-1 (extended image array)
-                mbar_arrive_expect_tx(BFULL + 8 * h, BATCH * C::B_BYTES);
-                bulk_g2s(bbase + h * BATCH * C::B_BYTES, wimg + (size_t)d0 * C::B_BYTES, BATCH * C::B_BYTES,
-                         BFULL + 8 * h);
+                mbar_arrive_expect_tx(BFULL + 8 * k, C::SLOT_B);
+                bulk_g2s(bbase + k * C::SLOT_B, wimg + (size_t)d0 * C::B_BYTES, C::SLOT_B, BFULL + 8 * k);
             }
         }
     } else if (warp >= W_BLD && warp < W_BLD + kBuilders) {
         // ---------------- A builders: halo (smem) -> registers -> TMEM (16x256b) ----------------
+        // Each builder walks only its half's stages (batches ab with ab % 2 == half) inside every phase.
         const int q = warp & 3;                        // TMEM lane quarter this warp may access
-        const int half = (warp - W_BLD) / 4;           // builds A batches ab with ab % 2 == half
+        const int half = (warp - W_BLD) / 4;
         const int t0 = lane & 3, t1 = lane >> 2;
-        const uint32_t abase = tmem + C::ACC + half * BATCH * C::ACOLS;
-        uint32_t pc = 0, ac = 0;
+        const int lrow = q * 32 + t1;                  // first of this thread's 4 lanes (+8, +16, +24)
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        uint32_t pc = 0, s0 = 0;                       // phase counter, first stage of the phase
+        uint32_t ac = (uint32_t)half * BATCH;          // next own stage
         for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
             const int level = P.tile_level[tile], gs = 27 / level;
-            for (int g = 0; g < level; ++g, ++pc) {
+            for (int g = 0; g < level; ++g, ++pc, s0 += gs) {
                 const uint32_t buf = pc & 1, par = (pc >> 1) & 1;
+                const uint32_t s1 = s0 + gs;
+                // wait for the phase's fill even without own stages in it: the release below must not run
+                // ahead of the loader, or it would count toward a later use of the same buffer
                 mbar_wait(smem_u32(&bar_hfull[buf]), par);
                 mbar_wait(smem_u32(&bar_ifull[buf]), par);
-                if (lane == 0 && q == 0 && half == 0) trace(dbg, 5, pc);
-                const uint16_t* lb = reinterpret_cast<const uint16_t*>(gen + ibase + buf * kIdxBytes);
-                const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
-                for (int u = g * gs; u < (g + 1) * gs; ++u, ++ac) {  // u = offset d
-                    const uint32_t ab = ac / BATCH, within = ac % BATCH;
-                    if ((int)(ab & 1) != half) continue;
-                    if (within == 0) {  // first stage of my batch: wait until my MMA warp released the slot
-                        mbar_wait(ADONE + 8 * half, ((ab >> 1) & 1) ^ 1);
-                        if (lane == 0 && q == 0) trace(dbg, 2, ab);
-                        tc_fence_after();
-                    }
-                    if (!(dbg & 2)) {  // lanes without a pair get zero A rows: the MMA needs no lane mask
-                        int sl[4];
+                if (ac < s1) {
+                    if (lane == 0 && q == 0 && half == 0) trace(dbg, 5, pc);
+                    const uint16_t* lb = reinterpret_cast<const uint16_t*>(gen + ibase + buf * kIdxBytes) -
+                                         (int)(s0 - g * gs) * kTileRows;  // indexed by stage: (ac - 27·lt) = d
+                    const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
+                    for (; ac < s1;) {
+                        const uint32_t ab = ac / BATCH, within = ac % BATCH;
+                        const uint32_t hbi = ab >> 1, k = half * NSL + hbi % NSL, use = hbi / NSL;
+                        if (within == 0) {  // first stage of my batch: wait until my MMA warp released the slot
+                            mbar_wait(ADONE + 8 * k, (use & 1) ^ 1);
+                            if (lane == 0 && q == 0) trace(dbg, 2, ab);
+                            tc_fence_after();
+                        }
+                        if (!(dbg & 2)) {  // lanes without a pair get zero A rows: the MMA needs no lane mask
+                            const uint16_t* lr = lb + (int)ac * kTileRows + lrow;
+                            const int sl[4] = {lr[0], lr[8], lr[16], lr[24]};
+                            const uint32_t acol = tmem + lane_off + C::ACC + (k * BATCH + within) * C::ACOLS;
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) sl[r] = lb[u * kTileRows + q * 32 + (r >> 1) * 16 + t1 + 8 * (r & 1)];
-                        const uint32_t acol = abase + within * C::ACOLS;
+                            for (int gg = 0; gg < 2; ++gg) {
+                                uint32_t v[4 * C::NX];
 #pragma unroll
-                        for (int gg = 0; gg < 2; ++gg) {
-                            uint32_t v[4 * C::NX];
+                                for (int i = 0; i < 4 * C::NX; ++i) v[i] = 0u;
 #pragma unroll
-                            for (int i = 0; i < 4 * C::NX; ++i) v[i] = 0u;
+                                for (int hi = 0; hi < 2; ++hi) {
+                                    const int sv = sl[2 * gg + hi];
+                                    if (sv != kNoSlot) {
+                                        const uint32_t rb = hb + sv * C::ROWB;
 #pragma unroll
-                            for (int hi = 0; hi < 2; ++hi) {
-                                const int s = sl[2 * gg + hi];
-                                if (s != kNoSlot) {
-                                    const uint32_t rb = hb + s * C::ROWB;
+                                        for (int j = 0; j < C::LJ; ++j) {
+                                            const uint4 w = lds128(rb + (halo_phys(K, sv, halo_chunk(K, t0, j)) << 4));
+                                            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-                                    for (int j = 0; j < C::LJ; ++j) {
-                                        const uint4 w = lds128(rb + (halo_phys(K, s, halo_chunk(K, t0, j)) << 4));
-                                        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                                        for (int e = 0; e < 4; ++e) {
-                                            const int i = 4 * j + e;
-                                            v[4 * (i >> 1) + (i & 1) + 2 * hi] = ww[e];
+                                            for (int e = 0; e < 4; ++e) {
+                                                const int i = 4 * j + e;
+                                                v[4 * (i >> 1) + (i & 1) + 2 * hi] = ww[e];
+                                            }
                                         }
                                     }
                                 }
+                                tmem_st16x256<C::NX>(acol + ((uint32_t)(gg * 16) << 16), v);
                             }
-                            tmem_st16x256<C::NX>(acol + ((uint32_t)(q * 32 + gg * 16) << 16), v);
                         }
-                    }
-                    if (within == BATCH - 1 || ac + 1 == nstages) {  // publish the batch
-                        tmem_st_wait();
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (q == 0) trace(dbg, 3, ab);
-                            mbar_arrive(AFULL + 8 * half);
+                        ++ac;
+                        if (within == BATCH - 1 || ac == nstages) {  // publish the batch, skip the other half's
+                            tmem_st_wait();
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) {
+                                if (q == 0) trace(dbg, 3, ab);
+                                mbar_arrive(AFULL + 8 * k);
+                            }
+                            ac += BATCH;
                         }
                     }
                 }
@@ -329,51 +347,47 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
     } else if (warp == W_MMA || warp == W_MMA + 1) {
         // ---------------- MMA issuers (one per half): A from TMEM, B from smem, D in TMEM ----------------
+        // Iterates only this half's batches; barrier addresses and descriptors are loop-invariant bases
+        // plus offsets (the issuing warp's instruction stream is the critical path at N <= 128).
         const int half = warp - W_MMA;
         const uint32_t TFULL = smem_u32(bar_tfull), TEMPTY = smem_u32(bar_tempty);
-        const uint32_t abase = tmem + C::ACC + half * BATCH * C::ACOLS;
-        const uint32_t bsm = bbase + half * BATCH * C::B_BYTES;
-        uint32_t ac = 0, lt = 0;
-        for (int tile = blockIdx.x; tile < T; tile += gridDim.x, ++lt) {
-            const uint32_t accb = lt % NACC, ause = lt / NACC;
-            const uint32_t dt = tmem + (half * NACC + accb) * N;
-            bool mine = false;
-            for (int u = 0; u < 27; ++u, ++ac) {  // u = offset d
-                const uint32_t ab = ac / BATCH, within = ac % BATCH;
-                if ((int)(ab & 1) != half) continue;
-                if (!mine) {  // first stage of this tile for this half: accumulator must be drained
-                    mbar_wait(TEMPTY + 8 * accb, (ause & 1) ^ 1);
-                    tc_fence_after();
-                    mine = true;
-                }
-                if (within == 0) {
-                    mbar_wait(BFULL + 8 * half, (ab >> 1) & 1);
-                    mbar_wait(AFULL + 8 * half, (ab >> 1) & 1);
-                    if (lane == 0) trace(dbg, 1, ab);
-                    tc_fence_after();
-                }
-                if (lane == 0) {
-                    const uint32_t sB = bsm + within * C::B_BYTES;
-                    const uint32_t at = abase + within * C::ACOLS;
-                    if (!(dbg & 1)) {
+        const uint64_t bdesc0 = smem_desc(bbase, 16, 8 * C::BROWB, C::BLAYOUT);  // + (byte offset >> 4)
+        const uint32_t nb = (nstages + BATCH - 1) / BATCH;
+        int cur = -1;  // local tile whose accumulator this warp is filling
+        for (uint32_t ab = half; ab < nb; ab += 2) {
+            const uint32_t hbi = ab >> 1, k = half * NSL + hbi % NSL, use = hbi / NSL;
+            mbar_wait(BFULL + 8 * k, use & 1);
+            mbar_wait(AFULL + 8 * k, use & 1);
+            if (lane == 0) trace(dbg, 1, ab);
+            tc_fence_after();
 #pragma unroll
-                        for (int ks = 0; ks < K / 16; ++ks) {
-                            const int kb = ks / (C::KB / 16), kk = ks % (C::KB / 16);
-                            mma_bf16_ts(dt, at + ks * 8,
-                                        smem_desc(sB + kb * N * C::BROWB + kk * 32, 16, 8 * C::BROWB, C::BLAYOUT),
-                                        C::IDESC, 1u);
-                        }
-                    }
-                    if (within == BATCH - 1 || ac + 1 == nstages) {
-                        mma_commit(ADONE + 8 * half);
-                        mma_commit(BEMPTY + 8 * half);
+            for (int w = 0; w < BATCH; ++w) {
+                const uint32_t ac = ab * BATCH + w;
+                if (ac >= nstages) break;
+                const int lt = (int)(ac / 27u);
+                if (lt != cur) {  // tile boundary: publish the finished tile, claim the next accumulator
+                    if (cur >= 0 && lane == 0) mma_commit(TFULL + 8 * (cur % NACC));
+                    __syncwarp();
+                    mbar_wait(TEMPTY + 8 * (lt % NACC), ((lt / NACC) & 1) ^ 1);
+                    tc_fence_after();
+                    cur = lt;
+                }
+                if (lane == 0 && !(dbg & 1)) {
+                    const uint32_t dt = tmem + (half * NACC + lt % NACC) * N;
+                    const uint32_t at = tmem + C::ACC + (k * BATCH + w) * C::ACOLS;
+                    const uint32_t boff = k * C::SLOT_B + w * C::B_BYTES;
+#pragma unroll
+                    for (int ks = 0; ks < K / 16; ++ks) {
+                        const int kb = ks / (C::KB / 16), kk = ks % (C::KB / 16);
+                        mma_bf16_ts(dt, at + ks * 8, bdesc0 + ((boff + kb * N * C::BROWB + kk * 32) >> 4), C::IDESC, 1u);
                     }
                 }
-                __syncwarp();
             }
-            if (lane == 0) mma_commit(TFULL + 8 * accb);  // every tile has stages of both halves
+            if (lane == 0) mma_commit(ADONE + 8 * k);  // frees A slot k and weight slot k
             __syncwarp();
         }
+        if (cur >= 0 && lane == 0) mma_commit(TFULL + 8 * (cur % NACC));
+        __syncwarp();
     } else if (warp >= W_EPI && warp < W_EPI + 4) {
         // ---------------- epilogue: D0 + D1 (fixed order) -> output rows (lane permutation) ----------------
         const int q = warp & 3;

@@ -23,19 +23,16 @@ t0 = t[t > 0].min()
 t = t.astype(np.int64)
 def col(ch, n):
     return [int(t[ch, i] - t0) if t[ch, i] else -1 for i in range(n)]
-print("A batches: mma_afull(ab) bld_adone(ab) bld_publish(ab)")
-for ab in range(40):
-    print(ab, int(t[1, ab] - t0) if t[1, ab] else -1, int(t[2, ab] - t0) if t[2, ab] else -1,
-          int(t[3, ab] - t0) if t[3, ab] else -1)
-print("MMA stages: start(ac) before_commit(ac)")
-for a in range(60):
-    print(a, int(t[4, a] - t0) if t[4, a] else -1, int(t[7, a] - t0) if t[7, a] else -1)
-print("B batches: mma_bfull(bb) bload(bb)")
-for bb in range(20):
-    print(bb, int(t[0, bb] - t0) if t[0, bb] else -1, int(t[6, bb] - t0) if t[6, bb] else -1)
-print("phase  ld_xfull ld_hempty ld_idx bld_phase epi_tfull")
-for p in range(8):
-    print(p, [(int(t[c, p] - t0) if t[c, p] else -1) for c in (8, 9, 10, 5, 11)])
+print("A batches: mma_afull(ab) bld_adone(ab) bld_publish(ab) bload(ab)")
+for ab in range(48):
+    print(ab, *[int(t[c, ab] - t0) if t[c, ab] else -1 for c in (1, 2, 3, 6)])
+print("MMA half0 stages: start(ac) end(ac) | after_bfull(ab) after_afull(ab)")
+for a in range(40):
+    print(a, *[int(t[c, a] - t0) if t[c, a] else -1 for c in (4, 7)], "|", *[int(t[c, a // 2] - t0) if t[c, a // 2] else -1 for c in (0, 1)])
+print("MMA tempty(lt)", [int(t[8, i] - t0) if t[8, i] else -1 for i in range(6)])
+print("phase  ld_hempty ld_idx bld_phase epi_tfull(tile)")
+for p in range(10):
+    print(p, [(int(t[c, p] - t0) if t[c, p] else -1) for c in (9, 10, 5, 11)])
 d = np.diff(t[1, :300])
 print(json.dumps({"dbg": os.environ.get("FVDB_DEBUG_HALO"), "mean_cycles_per_A_batch": float(d[d > 0].mean()),
                   "median": float(np.median(d))}))

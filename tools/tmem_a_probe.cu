@@ -238,3 +238,46 @@ extern "C" int probe_rate(int n, int iters, int mode, long long* cycles, float* 
     cudaEventElapsedTime(ms, a, b);
     return (int)cudaGetLastError();
 }
+
+// ---- cost of waiting on an already-completed mbarrier phase: try_wait vs test_wait
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__global__ void k_wait_cost(int iters, long long* out) {
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&bar), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_arrive(smem_u32(&bar));  // phase 0 complete
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const uint32_t b = smem_u32(&bar);
+        uint32_t acc = 0;
+        long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) acc += mbar_try_wait(b, 0) ? 1u : 0u;
+        long long t1 = clock64();
+        for (int i = 0; i < iters; ++i) acc += mbar_test(b, 0) ? 1u : 0u;
+        long long t2 = clock64();
+        for (int i = 0; i < iters; ++i) mbar_wait(b, 0);
+        long long t3 = clock64();
+        if (threadIdx.x == 0) {
+            out[0] = t1 - t0;
+            out[1] = t2 - t1;
+            out[2] = t3 - t2;
+            out[3] = acc;
+        }
+    }
+}
+extern "C" int probe_wait_cost(int iters, long long* out) {
+    k_wait_cost<<<1, 32>>>(iters, out);
+    return (int)cudaDeviceSynchronize();
+}

@@ -58,7 +58,7 @@ def main():
         err = float((out.cpu().double() - ref).abs().max() / ref.abs().max())
         rep[f"mode{mode}"] = {"rc": rc, "rel_err": err}
     cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
-    for n in (64, 128):
+    for n in (64,):
         for mode, name in enumerate(("ss", "ts", "ts_mask0", "ts_mask_half", "ss_elect", "ts_elect", "ss_2warps", "ss_4warps", "ts_2warps", "ts_4warps")):
             ms = C.c_float(0)
             iters = 20000
@@ -66,6 +66,11 @@ def main():
             c = float(cyc.float().mean()) / (iters * 4)
             rep[f"rate_n{n}_{name}"] = {"rc": rc, "cycles_per_mma": round(c, 1),
                                         "tflops": round(148 * iters * 4 * 2 * 128 * n * 16 / (ms.value * 1e-3) / 1e12)}
+    wc = torch.zeros(4, dtype=torch.int64, device="cuda")
+    it = 10000
+    rc = L.probe_wait_cost(it, C.c_void_p(wc.data_ptr()))
+    w = wc.cpu().tolist()
+    rep["wait_cost_cycles"] = {"rc": rc, "try_wait": w[0] / it, "test_wait": w[1] / it, "mbar_wait_loop": w[2] / it}
     print(json.dumps(rep))
 
 
