@@ -324,7 +324,9 @@ struct WgCfg {
     static constexpr int NACC = NACC0 < 8 ? NACC0 : 8;         // M-blocks (TMEM accumulators) per CTA
     static constexpr int OFFS = NACC * OPB;                    // offsets per CTA
     static constexpr int GROUPS = (27 + OFFS - 1) / OFFS;
-    static constexpr int TK = 32;                              // output rows (MMA K) per stage
+    // output rows (MMA K) per stage.  16 (twice the stages in flight) measured slower: the per-stage
+    // fixed cost in the MMA warps (wait, proxy fence, commit) dominates, not the stage round trip.
+    static constexpr int TK = 32;
     static constexpr int CHUNK = 128;                          // output rows per index block
     static constexpr int A_BLK = TK * 256;                     // one M-block: TK k-rows x 128 m (bf16)
     static constexpr int B_BYTES = TK * COUT * 2;
@@ -341,12 +343,12 @@ struct WgCfg {
     static_assert(STAGES >= 2, "wgrad pipeline needs >= 2 stages");
 };
 
-constexpr int kWgThreads = 320;  // warps 0-3 gather, 4 loader, 5 MMA, 6-9 epilogue
+constexpr int kWgThreads = 352;  // warps 0-3 gather, 4 loader, 5 and 10 MMA (half the M-blocks each), 6-9 epilogue
 
 template <int CIN, int COUT>
 __global__ void __launch_bounds__(kWgThreads, 1)
     k_wgrad_tc(const bf16* __restrict__ in, const bf16* __restrict__ go, const int32_t* __restrict__ nbr,
-               int64_t ld, int64_t n_out, int64_t rows_per_split, float* __restrict__ part) {
+               int64_t ld, int64_t n_out, int64_t rows_per_split, float* __restrict__ part, int dbg) {
     using C = WgCfg<CIN, COUT>;
     extern __shared__ uint8_t dsmem[];
     __shared__ __align__(8) uint64_t bar_full[C::STAGES], bar_empty[C::STAGES], bar_ifull[C::ISLOTS],
@@ -369,13 +371,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(smem_u32(&bar_full[s]), 128);
-            mbar_init(smem_u32(&bar_empty[s]), 1);
+            mbar_init(smem_u32(&bar_empty[s]), 2);  // both MMA warps commit
         }
         for (int s = 0; s < C::ISLOTS; ++s) {
             mbar_init(smem_u32(&bar_ifull[s]), 1);
             mbar_init(smem_u32(&bar_iempty[s]), 128);
         }
-        mbar_init(smem_u32(&bar_tfull), 1);
+        mbar_init(smem_u32(&bar_tfull), 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 5) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
@@ -387,7 +389,20 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     if (warp < 4) {
         const int pt = threadIdx.x;
         constexpr int ACH = CIN / 8, BCH = COUT / 8;                  // 16-B chunks per row
-        const int a_items = n_off * C::TK * ACH;
+        // thread -> (chunk c, rows r0 + p*RPP): loop-invariant smem offsets; all of a stage's indices are
+        // loaded before its copies are issued (a runtime-trip loop serialised one LDS latency per copy)
+        constexpr int RPP = 128 / ACH, NPASS = C::TK / RPP;
+        static_assert(RPP * NPASS == C::TK, "gather mapping");
+        const int c = pt % ACH, r0 = pt / ACH;
+        uint32_t roff[NPASS][C::OPB];                                 // swizzled offset inside an M-block
+#pragma unroll
+        for (int p = 0; p < NPASS; ++p)
+#pragma unroll
+            for (int v = 0; v < C::OPB; ++v) {
+                const int r = r0 + p * RPP, m = v * CIN + c * 8;
+                roff[p][v] = (m >> 6) * (C::TK * 128) + swz_off(r, (m & 63) >> 3, 128);
+            }
+        const bf16* in_c = in + c * 8;
         uint32_t it = 0;
         for (int ch = 0; ch < n_chunks; ++ch) {
             const uint32_t islot = ch % C::ISLOTS;
@@ -396,16 +411,23 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             for (int sub = 0; sub < SPC; ++sub, ++it) {
                 const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
                 const int64_t o0 = o_begin + (int64_t)ch * C::CHUNK + sub * C::TK;
+                int32_t idx[C::OFFS][NPASS];
+#pragma unroll
+                for (int u = 0; u < C::OFFS; ++u)
+#pragma unroll
+                    for (int p = 0; p < NPASS; ++p)
+                        idx[u][p] = u < n_off ? ib[u * C::CHUNK + sub * C::TK + r0 + p * RPP] : -1;
                 mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
                 const uint32_t sB = base + s * C::STAGE, sA = sB + C::B_BYTES;
-                for (int i = pt; i < a_items; i += 128) {
-                    const int task = i / ACH, c = i % ACH;
-                    const int u = task / C::TK, r = task % C::TK;
-                    const int32_t idx = ib[u * C::CHUNK + sub * C::TK + r];
-                    const int a = u / C::OPB, m = (u % C::OPB) * CIN + c * 8;
-                    const uint32_t dst = sA + a * C::A_BLK + (m >> 6) * (C::TK * 128) + swz_off(r, (m & 63) >> 3, 128);
-                    cp_async_16(dst, in + (int64_t)(idx < 0 ? 0 : idx) * CIN + c * 8, idx < 0 ? 0u : 16u);
-                }
+#pragma unroll
+                for (int u = 0; u < C::OFFS; ++u)
+#pragma unroll
+                    for (int p = 0; p < NPASS; ++p) {
+                        const int32_t x = idx[u][p];  // missing neighbour: zero-fill (src-size 0, no read)
+                        if (u < n_off && !(dbg & 2))
+                            cp_async_16(sA + (u / C::OPB) * C::A_BLK + roff[p][u % C::OPB],
+                                        in_c + (int64_t)(x < 0 ? 0 : x) * CIN, x < 0 ? 0u : 16u);
+                    }
                 for (int i = pt; i < C::TK * BCH; i += 128) {
                     const int r = i / BCH, c = i % BCH;
                     const int64_t o = o0 + r;
@@ -427,35 +449,40 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const uint32_t islot = ch % C::ISLOTS;
                 mbar_wait_sleep(smem_u32(&bar_iempty[islot]), ((ch / C::ISLOTS) & 1) ^ 1, 128);
                 const uint32_t fb = smem_u32(&bar_ifull[islot]);
-                mbar_arrive_expect_tx(fb, n_off * C::CHUNK * 4);
-                for (int u = 0; u < n_off; ++u)
+                const int nc = (dbg & 4) ? 1 : n_off;  // profiling: one index row per chunk
+                mbar_arrive_expect_tx(fb, nc * C::CHUNK * 4);
+                for (int u = 0; u < nc; ++u)
                     bulk_g2s(ibase + islot * C::IDX_BYTES + u * C::CHUNK * 4,
                              nbr + (int64_t)(d0 + u) * ld + o_begin + (int64_t)ch * C::CHUNK, C::CHUNK * 4, fb);
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 5 || warp == 10) {
+        // two MMA issuers on disjoint accumulators (M-blocks): one thread issues ~1 MMA per 60-100 cycles
+        const int a_lo = warp == 5 ? 0 : (n_acc + 1) / 2, a_hi = warp == 5 ? (n_acc + 1) / 2 : n_acc;
         const int n_steps = n_chunks * SPC;
+        const uint64_t adesc0 = smem_desc(base + C::B_BYTES, C::TK * 128, 1024, kSwizzle128B);
+        const uint64_t bdesc0 = C::B_SW128 ? smem_desc(base, C::TK * 128, 1024, kSwizzle128B)
+                                           : smem_desc(base, 64, 512, kSwizzle64B);
         for (int step = 0; step < n_steps; ++step) {
             const uint32_t s = step % C::STAGES, ph = (step / C::STAGES) & 1;
             mbar_wait(smem_u32(&bar_full[s]), ph);
             fence_proxy_async_smem();
             tc_fence_after();
             if (lane == 0) {
-                const uint32_t sB = base + s * C::STAGE, sA = sB + C::B_BYTES;
-                for (int a = 0; a < n_acc; ++a) {
+                const uint32_t so = s * C::STAGE;
+                for (int a = a_lo; a < a_hi; ++a) {
 #pragma unroll
                     for (int ks = 0; ks < C::TK / 16; ++ks) {
-                        uint64_t ad = smem_desc(sA + a * C::A_BLK + ks * 2048, C::TK * 128, 1024, kSwizzle128B);
-                        uint64_t bd = C::B_SW128 ? smem_desc(sB + ks * 2048, C::TK * 128, 1024, kSwizzle128B)
-                                                 : smem_desc(sB + ks * 1024, 64, 512, kSwizzle64B);
-                        mma_bf16(tmem + a * COUT, ad, bd, C::IDESC, (step | ks) != 0);
+                        const uint64_t ad = adesc0 + ((so + a * C::A_BLK + ks * 2048) >> 4);
+                        const uint64_t bd = bdesc0 + ((so + (C::B_SW128 ? ks * 2048 : ks * 1024)) >> 4);
+                        if (!(dbg & 1)) mma_bf16(tmem + a * COUT, ad, bd, C::IDESC, (step | ks) != 0);
                     }
                 }
                 mma_commit(smem_u32(&bar_empty[s]));
             }
             __syncwarp();
         }
-        if (lane == 0 && n_steps > 0) mma_commit(smem_u32(&bar_tfull));
+        if (lane == 0) mma_commit(smem_u32(&bar_tfull));
         __syncwarp();
     } else {
         const int q = warp & 3;
@@ -578,8 +605,10 @@ struct WgLaunch {
         rps = ceil_div(rps, C::CHUNK) * C::CHUNK;
         auto kern = k_wgrad_tc<CIN, COUT>;
         FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        // profiling switches (FVDB_DEBUG_WG): 1 no MMA, 2 no A gather, 4 one index row per chunk
+        static const int dbg = getenv("FVDB_DEBUG_WG") ? atoi(getenv("FVDB_DEBUG_WG")) : 0;
         kern<<<splits * C::GROUPS, kWgThreads, C::SMEM, st>>>((const bf16*)in, (const bf16*)go, nbr, ld, n_out, rps,
-                                                              part);
+                                                              part, dbg);
         k_wgrad_tc_reduce<<<(unsigned)ceil_div((int64_t)27 * CIN * COUT, 256), 256, 0, st>>>(part, splits, CIN, COUT, gw);
         FVDB_LAUNCH_CHECK();
         return FVDB_OK;
