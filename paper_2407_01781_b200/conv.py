@@ -120,11 +120,16 @@ class NbrTable:
     uses to pair lanes; halo plans are built lazily per kernel capacity and cached.
     """
 
-    __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans")
+    __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses")
 
     def __init__(self, t, n, colors_fn=None):
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
         self._colors_fn, self._colors, self._plans = colors_fn, None, {}
+        self.uses = 0  # bf16 tensor-core convolutions run over this table (conv_impl "auto")
+
+    def has_plan(self, K: int, N: int) -> bool:
+        cap = int(_lib.lib().fvdb_halo_cap(K, N))
+        return cap in self._plans
 
     @property
     def view(self):
@@ -352,17 +357,31 @@ def pack_weights_kn(w: torch.Tensor, transpose: bool, dtype) -> torch.Tensor:
 
 
 def conv_impl() -> str:
-    """Tensor-core conv kernel: "halo" (default; conv_halo.cu) or "gather" (conv_tc.cu), env FVDB_CONV_IMPL."""
-    v = os.environ.get("FVDB_CONV_IMPL", "halo")
-    if v not in ("halo", "gather"):
-        raise ValueError(f"FVDB_CONV_IMPL must be 'halo' or 'gather', got {v!r}")
+    """Tensor-core conv kernel policy, env FVDB_CONV_IMPL:
+
+    * "auto" (default): the gather-GEMM kernel (conv_tc.cu) on a neighbour table's first bf16 use,
+      the halo-staged kernel (conv_halo.cu) from its second use on.  The halo plan costs a few
+      conv launches to build, so it pays off only for maps that are reused (layers sharing a grid,
+      training iterations, the backward pass of a cached map), not for one-shot maps;
+    * "halo" / "gather": always that kernel.
+    """
+    v = os.environ.get("FVDB_CONV_IMPL", "auto")
+    if v not in ("auto", "halo", "gather"):
+        raise ValueError(f"FVDB_CONV_IMPL must be 'auto', 'halo' or 'gather', got {v!r}")
     return v
+
+
+def _image_impl(img: torch.Tensor, K: int, N: int) -> str:
+    """Which kernel a packed weight image was made for (the halo layout carries extra copies)."""
+    return "halo" if img.numel() == _lib.HALO_IMAGES * K * N * 2 else "gather"
 
 
 def pack_weights_umma(w: torch.Tensor, transpose: bool, impl: str | None = None) -> torch.Tensor:
     """fp32 [Cout,Cin,3,3,3] -> bf16 UMMA B-operand images (27 x K x N, swizzled) for ``impl``'s kernel."""
     from .topology import _device
     impl = impl or conv_impl()
+    if impl == "auto":
+        impl = "halo"
     w = w.to(device=_device(), dtype=torch.float32).contiguous()
     cout, cin = int(w.shape[0]), int(w.shape[1])
     img = torch.empty((_lib.HALO_IMAGES if impl == "halo" else 27) * cout * cin * 2, dtype=torch.uint8,
@@ -420,7 +439,13 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
         wp[:cout, :cin] = w.to(device=x.device, dtype=torch.float32)
         y = gather_conv(_pad_cols(x, Kp), nbr, wp, transpose, out_dtype, impl=impl)
         return y[:, :N].contiguous()
-    impl = impl or conv_impl()
+    if w_image is not None:
+        impl = _image_impl(w_image, K, N)  # the image decides
+    else:
+        impl = impl or conv_impl()
+        if impl == "auto":
+            impl = "halo" if nbr.uses > 0 or nbr.has_plan(K, N) else "gather"
+    nbr.uses += 1
     img = w_image if w_image is not None else pack_weights_umma(w, transpose, impl)
     out = torch.empty((n_out, N), dtype=out_dtype, device=x.device)
     if not n_out:

@@ -20,7 +20,7 @@ import torch
 from torch import nn
 
 from .build import coarsen
-from .conv import batch_grid_kernel_map, gather_conv, pack_weights_umma, wgrad
+from .conv import batch_grid_kernel_map, gather_conv, wgrad
 from .jagged import GridBatch, JaggedTensor
 
 
@@ -31,8 +31,7 @@ class _SparseConvFn(torch.autograd.Function):
         if transposed:
             y = gather_conv(xc, kmap.bwd, w, transpose=True, out_dtype=cdt)
         else:
-            img = pack_weights_umma(w, False) if cdt == torch.bfloat16 and _tc_ok(w) else None
-            y = gather_conv(xc, kmap.fwd, w, transpose=False, out_dtype=cdt, w_image=img)
+            y = gather_conv(xc, kmap.fwd, w, transpose=False, out_dtype=cdt)
         ctx.save_for_backward(xc, w)
         ctx.kmap, ctx.transposed, ctx.cdt, ctx.x_dtype = kmap, transposed, cdt, x.dtype
         return y
