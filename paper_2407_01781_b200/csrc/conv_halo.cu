@@ -78,7 +78,9 @@ constexpr int kImgExt = 34;  // weight images per layer: 27 offsets + 7 wrap-aro
 // issuing thread sustains only ~100 cycles per A-in-TMEM tcgen05.mma (M=128, K=16), several issuing
 // warps reach the ~32-36-cycle hardware rate (profiles/r01_halo_kernel.md).  Every hand-off is per
 // batch: an mbarrier wait costs ~150-190 cycles even when its phase has already completed.
-template <int K, int N>
+// V selects the TMEM/smem split (profiling experiments): 0 = double-buffered accumulators;
+// 1 = single-buffered accumulators, 2 slots x 3-stage batches; 2 = single-buffered, 3 slots x 2 stages
+template <int K, int N, int V = 0>
 struct HaloCfg {
     static constexpr int ROWB = 2 * K;                      // halo row bytes
     static constexpr int CPR = K / 8;                       // 16-B chunks per row
@@ -90,19 +92,19 @@ struct HaloCfg {
     static constexpr int B_BYTES = N * K * 2;               // one offset's weight image
     static constexpr int ACOLS = K / 2;                     // TMEM columns of one A stage
     // accumulator buffers per half: 2 (epilogue overlaps the next tile) when TMEM allows
-    static constexpr int NACC = 4 * N + 2 * ACOLS <= 512 ? 2 : 1;
+    static constexpr int NACC = V != 0 ? 1 : (4 * N + 2 * ACOLS <= 512 ? 2 : 1);
     static constexpr int ACC = 2 * NACC * N;                // accumulator columns (both halves)
     // NSL slots per half (2: a half's builders fill one slot while its MMA warp drains the other)
     static constexpr int fits(int nsl, int b) {
         return ACC + 2 * nsl * b * ACOLS <= 512 &&
                (kSmemMax - 2048 - (1024 + 2 * nsl * b * B_BYTES + 2 * kIdxBytes)) / (2 * (ROWB + 4)) >= 256;
     }
-    static constexpr int NSL = fits(2, 1) ? 2 : 1;
-    static constexpr int BATCH = fits(NSL, 4) ? 4 : (fits(NSL, 2) ? 2 : 1);  // stages per batch (= images per TMA)
+    static constexpr int NSL = V == 2 ? 3 : (fits(2, 1) ? 2 : 1);
+    static constexpr int BATCH = V == 1 ? 3 : (V == 2 ? 2 : (fits(NSL, 4) ? 4 : (fits(NSL, 2) ? 2 : 1)));
     static constexpr int SLOT_B = BATCH * B_BYTES;          // weight bytes of one slot
     static constexpr int FIXED = 1024 + 2 * NSL * SLOT_B + 2 * kIdxBytes;
-    static constexpr int CAP = ((kSmemMax - 2048 - FIXED) / (2 * (ROWB + 4))) & ~7;
-    static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4);
+    static constexpr int CAP = ((kSmemMax - 2048 - FIXED - ROWB) / (2 * (ROWB + 4))) & ~7;
+    static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4) + ROWB;  // + one zero row
     static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, N, false, false);
     static_assert(fits(NSL, BATCH) && CAP >= 256, "halo capacity must hold one offset phase (2 x 128 slots)");
     static_assert(27 + BATCH - 1 <= kImgExt, "weight batch wraps past the extended image array");
@@ -124,11 +126,11 @@ __device__ __forceinline__ void trace(int dbg, int ch, uint32_t i) {
 // ---------------------------------------------------------------------------------------------
 // conv kernel
 // ---------------------------------------------------------------------------------------------
-template <int K, int N, bool OUT_BF16>
+template <int K, int N, bool OUT_BF16, int V = 0>
 __global__ void __launch_bounds__(kHaloThreads, 1)
     k_conv_halo(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, fvdb_halo_plan P,
                 int64_t n_out, void* __restrict__ out, int dbg) {
-    using C = HaloCfg<K, N>;
+    using C = HaloCfg<K, N, V>;
     constexpr int W_LOAD = 0, W_MMA = 1, W_BLD = 3, W_EPI = 3 + kBuilders, W_BLOAD = W_EPI + 4;
     constexpr int BATCH = C::BATCH, NACC = C::NACC, NSL = C::NSL;
     extern __shared__ uint8_t dsmem[];
@@ -144,6 +146,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     const uint32_t ibase = bbase + 2 * NSL * C::SLOT_B;               // index blocks [2]
     const uint32_t hbase = ibase + 2 * kIdxBytes;                     // halo rows [2][CAP][ROWB]
     const uint32_t xbase = hbase + 2 * C::CAP * C::ROWB;              // halo row ids [2][CAP]
+    const uint32_t zrow = xbase + 2 * C::CAP * 4;                     // one zero row (missing neighbours)
     const uint8_t* gen = dsmem - sbase;                               // generic view: gen + saddr
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int T = P.num_tiles;
@@ -170,6 +173,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == W_MMA) tmem_alloc(smem_u32(&tmem_slot), 512);
+    for (int i = threadIdx.x; i < C::ROWB / 16; i += blockDim.x)
+        *reinterpret_cast<uint4*>(dsmem + (zrow - sbase) + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -196,9 +201,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             const int32_t* ph = P.phase + ((int64_t)t * 27 + gg) * 2;
             const int off = P.tile_base[t] + ph[0], len = ph[1];
             if (lane == 0) {
-                mbar_arrive_expect_tx(smem_u32(&bar_xfull[buf]), (uint32_t)len * 4u);
-                if (len > 0) bulk_g2s(xbase + buf * C::CAP * 4, P.halo_rows + off, (uint32_t)len * 4u,
-                                      smem_u32(&bar_xfull[buf]));
+                const bool skip = (dbg & 32) != 0;  // profiling: no id/record TMAs (use with 8 and 2)
+                mbar_arrive_expect_tx(smem_u32(&bar_xfull[buf]), skip ? 0u : (uint32_t)len * 4u);
+                if (len > 0 && !skip)
+                    bulk_g2s(xbase + buf * C::CAP * 4, P.halo_rows + off, (uint32_t)len * 4u, smem_u32(&bar_xfull[buf]));
             }
             return len;
         };
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
             constexpr int RPI = 32 / C::CPR;  // rows per warp instruction
             const int q = lane / C::CPR, c = lane % C::CPR;
-            for (int s0 = 0; s0 < len; s0 += 4 * RPI) {
+            for (int s0 = 0; s0 < ((dbg & 32) ? 0 : len); s0 += 4 * RPI) {
                 int r[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -235,9 +241,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             cp_async_arrive_noinc(smem_u32(&bar_hfull[buf]));
             if (lane == 0) {  // index block: the tile's whole record (lnbr rows + masks), one TMA
                 mbar_wait(smem_u32(&bar_iempty[buf]), par ^ 1);
-                mbar_arrive_expect_tx(smem_u32(&bar_ifull[buf]), (uint32_t)kRecBytes);
-                bulk_g2s(ibase + buf * kIdxBytes, P.tile_rec + (int64_t)tile * kIdxBytes, (uint32_t)kRecBytes,
-                         smem_u32(&bar_ifull[buf]));
+                mbar_arrive_expect_tx(smem_u32(&bar_ifull[buf]), (dbg & 32) ? 0u : (uint32_t)kRecBytes);
+                if (!(dbg & 32))
+                    bulk_g2s(ibase + buf * kIdxBytes, P.tile_rec + (int64_t)tile * kIdxBytes, (uint32_t)kRecBytes,
+                             smem_u32(&bar_ifull[buf]));
                 trace(dbg, 10, pc);
             }
             __syncwarp();
@@ -300,30 +307,32 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                             const uint16_t* lr = lb + (int)ac * kTileRows + lrow;
                             const int sl[4] = {lr[0], lr[8], lr[16], lr[24]};
                             const uint32_t acol = tmem + lane_off + C::ACC + (k * BATCH + within) * C::ACOLS;
+                            // all loads of the stage first, then both TMEM stores (asm volatile keeps order,
+                            // so interleaving them serialised one shared-memory latency per store)
+                            uint32_t v[2][4 * C::NX];
 #pragma unroll
                             for (int gg = 0; gg < 2; ++gg) {
-                                uint32_t v[4 * C::NX];
-#pragma unroll
-                                for (int i = 0; i < 4 * C::NX; ++i) v[i] = 0u;
 #pragma unroll
                                 for (int hi = 0; hi < 2; ++hi) {
                                     const int sv = sl[2 * gg + hi];
-                                    if (sv != kNoSlot) {
-                                        const uint32_t rb = hb + sv * C::ROWB;
+                                    // missing neighbour: read the zero row (no branch, no register zeroing)
+                                    const uint32_t rb = sv != kNoSlot ? hb + sv * C::ROWB : zrow;
+                                    const int par = sv & 1;
 #pragma unroll
-                                        for (int j = 0; j < C::LJ; ++j) {
-                                            const uint4 w = lds128(rb + (halo_phys(K, sv, halo_chunk(K, t0, j)) << 4));
-                                            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+                                    for (int j = 0; j < C::LJ; ++j) {
+                                        const uint4 w = lds128(rb + (halo_phys(K, par, halo_chunk(K, t0, j)) << 4));
+                                        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-                                            for (int e = 0; e < 4; ++e) {
-                                                const int i = 4 * j + e;
-                                                v[4 * (i >> 1) + (i & 1) + 2 * hi] = ww[e];
-                                            }
+                                        for (int e = 0; e < 4; ++e) {
+                                            const int i = 4 * j + e;
+                                            v[gg][4 * (i >> 1) + (i & 1) + 2 * hi] = ww[e];
                                         }
                                     }
                                 }
-                                tmem_st16x256<C::NX>(acol + ((uint32_t)(gg * 16) << 16), v);
                             }
+#pragma unroll
+                            for (int gg = 0; gg < 2; ++gg)
+                                tmem_st16x256<C::NX>(acol + ((uint32_t)(gg * 16) << 16), v[gg]);
                         }
                         ++ac;
                         if (within == BATCH - 1 || ac == nstages) {  // publish the batch, skip the other half's
@@ -358,7 +367,6 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             const uint32_t hbi = ab >> 1, k = half * NSL + hbi % NSL, use = hbi / NSL;
             mbar_wait(BFULL + 8 * k, use & 1);
             mbar_wait(AFULL + 8 * k, use & 1);
-            if (lane == 0) trace(dbg, 1, ab);
             tc_fence_after();
 #pragma unroll
             for (int w = 0; w < BATCH; ++w) {
@@ -366,27 +374,26 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 if (ac >= nstages) break;
                 const int lt = (int)(ac / 27u);
                 if (lt != cur) {  // tile boundary: publish the finished tile, claim the next accumulator
-                    if (cur >= 0 && lane == 0) mma_commit(TFULL + 8 * (cur % NACC));
-                    __syncwarp();
+                    if (cur >= 0) mma_commit_elect(TFULL + 8 * (cur % NACC));
                     mbar_wait(TEMPTY + 8 * (lt % NACC), ((lt / NACC) & 1) ^ 1);
                     tc_fence_after();
                     cur = lt;
                 }
-                if (lane == 0 && !(dbg & 1)) {
+                if (!(dbg & 1)) {  // the whole warp runs this (uniform operands); one elected lane issues
                     const uint32_t dt = tmem + (half * NACC + lt % NACC) * N;
                     const uint32_t at = tmem + C::ACC + (k * BATCH + w) * C::ACOLS;
                     const uint32_t boff = k * C::SLOT_B + w * C::B_BYTES;
 #pragma unroll
                     for (int ks = 0; ks < K / 16; ++ks) {
                         const int kb = ks / (C::KB / 16), kk = ks % (C::KB / 16);
-                        mma_bf16_ts(dt, at + ks * 8, bdesc0 + ((boff + kb * N * C::BROWB + kk * 32) >> 4), C::IDESC, 1u);
+                        mma_bf16_ts_elect(dt, at + ks * 8, bdesc0 + ((boff + kb * N * C::BROWB + kk * 32) >> 4),
+                                          C::IDESC, 1u);
                     }
                 }
             }
-            if (lane == 0) mma_commit(ADONE + 8 * k);  // frees A slot k and weight slot k
-            __syncwarp();
+            mma_commit_elect(ADONE + 8 * k);  // frees A slot k and weight slot k
         }
-        if (cur >= 0 && lane == 0) mma_commit(TFULL + 8 * (cur % NACC));
+        if (cur >= 0) mma_commit_elect(TFULL + 8 * (cur % NACC));
         __syncwarp();
     } else if (warp >= W_EPI && warp < W_EPI + 4) {
         // ---------------- epilogue: D0 + D1 (fixed order) -> output rows (lane permutation) ----------------
@@ -700,11 +707,17 @@ int sm_count_h() {
     return v;
 }
 
-template <int K, int N, bool OB>
-int launch_halo(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out, cudaStream_t st) {
-    using C = HaloCfg<K, N>;
+int halo_variant() {
+    static const int v = getenv("FVDB_HALO_VARIANT") ? atoi(getenv("FVDB_HALO_VARIANT")) : 0;  // profiling
+    return v;
+}
+
+template <int K, int N, bool OB, int V = 0>
+int launch_halo_v(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out,
+                  cudaStream_t st) {
+    using C = HaloCfg<K, N, V>;
     if (P.halo_cap > C::CAP) return FVDB_ERR_INVALID;
-    auto kern = k_conv_halo<K, N, OB>;
+    auto kern = k_conv_halo<K, N, OB, V>;
     FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     int grid = sm_count_h();
     if (grid > P.num_tiles) grid = P.num_tiles;
@@ -713,6 +726,15 @@ int launch_halo(const void* in, const void* wimg, const fvdb_halo_plan& P, int64
     kern<<<grid, kHaloThreads, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, P, n_out, out, dbg);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
+}
+
+template <int K, int N, bool OB>
+int launch_halo(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out, cudaStream_t st) {
+    if constexpr (K == 64 && N == 64) {
+        if (halo_variant() == 1) return launch_halo_v<K, N, OB, 1>(in, wimg, P, n_out, out, st);
+        if (halo_variant() == 2) return launch_halo_v<K, N, OB, 2>(in, wimg, P, n_out, out, st);
+    }
+    return launch_halo_v<K, N, OB, 0>(in, wimg, P, n_out, out, st);
 }
 
 template <typename F>
@@ -741,7 +763,12 @@ extern "C" int fvdb_parity_colors(const int64_t* coords, int64_t n, int shift, u
 extern "C" int fvdb_halo_cap(int K, int N) {
     int cap = 0;
     halo_dispatch(K, N, [&](auto k, auto n) {
-        cap = HaloCfg<decltype(k)::value, decltype(n)::value>::CAP;
+        constexpr int KK = decltype(k)::value, NN = decltype(n)::value;
+        cap = HaloCfg<KK, NN>::CAP;
+        if constexpr (KK == 64 && NN == 64) {
+            if (halo_variant() == 1) cap = HaloCfg<KK, NN, 1>::CAP;
+            if (halo_variant() == 2) cap = HaloCfg<KK, NN, 2>::CAP;
+        }
         return 0;
     });
     return cap;

@@ -518,17 +518,19 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
 }
 
-// gw[co][ci][d] = Σ_s part[s][d][ci][co]   (fixed split order: deterministic)
+// gw[co][ci][d] = Σ_s part[s][d][ci][co]   (fixed split order: deterministic).  Threads walk the
+// partials' own layout (co fastest) so the split-strided reads are coalesced; the scattered writes are
+// only 27·Cin·Cout elements.
 __global__ void k_wgrad_tc_reduce(const float* __restrict__ part, int splits, int cin, int cout, float* __restrict__ gw) {
-    const int64_t total = (int64_t)27 * cout * cin;
+    const int64_t total = (int64_t)27 * cout * cin, stride = total;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t co = t / ((int64_t)cin * 27);
-        int64_t rem = t - co * cin * 27;
-        int64_t ci = rem / 27, d = rem - ci * 27;
+        const int64_t d = t / ((int64_t)cin * cout);
+        const int64_t rem = t - d * cin * cout;
+        const int64_t ci = rem / cout, co = rem - ci * cout;
         float v = 0.f;
-        for (int s = 0; s < splits; ++s) v += part[(((int64_t)s * 27 + d) * cin + ci) * cout + co];
-        gw[t] = v;
+        for (int s = 0; s < splits; ++s) v += part[s * stride + t];
+        gw[(co * cin + ci) * 27 + d] = v;
     }
 }
 

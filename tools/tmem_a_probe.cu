@@ -281,3 +281,78 @@ extern "C" int probe_wait_cost(int iters, long long* out) {
     k_wait_cost<<<1, 32>>>(iters, out);
     return (int)cudaDeviceSynchronize();
 }
+
+// ---- cta_group::2 issue rate: 2-CTA cluster, leader thread issues M=256 (128 rows per CTA) N=64 K=16 MMAs
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_rate2(int iters, int ts, long long* cycles) {
+    __shared__ __align__(1024) uint8_t sm[32768];
+    __shared__ __align__(8) uint64_t done;
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t rank = cluster_rank();
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&done), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    if (rank == 0 && threadIdx.x == 0) {
+        const uint32_t idesc = idesc_bf16_f32(256, 64, false, false);
+        const uint32_t sA = smem_u32(sm), sB = sA;
+        long long t0 = clock64();
+        for (int i = 0; i < iters; ++i)
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const uint64_t bd = smem_desc(sB + ks * 32, 16, 1024, kSwizzle128B);
+                const uint32_t acc = (i | ks) != 0;
+                if (ts) {
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                                 "r"(tmem + 256 + ks * 8), "l"(bd), "r"(idesc), "r"(acc)
+                                 : "memory");
+                } else {
+                    const uint64_t ad = smem_desc(sA + ks * 32, 16, 1024, kSwizzle128B);
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+                                 : "memory");
+                }
+            }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     ::"r"(smem_u32(&done)), "h"((uint16_t)3)
+                     : "memory");
+        mbar_wait(smem_u32(&done), 0);
+        cycles[blockIdx.x / 2] = clock64() - t0;
+    } else if (rank == 1 && threadIdx.x == 0) {
+        mbar_wait(smem_u32(&done), 0);
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    }
+}
+extern "C" int probe_rate2(int iters, int ts, long long* cycles, float* ms) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_rate2<<<148, 128>>>(iters, ts, cycles);
+    cudaEventRecord(a);
+    k_rate2<<<148, 128>>>(iters, ts, cycles);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(ms, a, b);
+    return (int)cudaGetLastError();
+}

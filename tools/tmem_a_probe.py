@@ -66,6 +66,13 @@ def main():
             c = float(cyc.float().mean()) / (iters * 4)
             rep[f"rate_n{n}_{name}"] = {"rc": rc, "cycles_per_mma": round(c, 1),
                                         "tflops": round(148 * iters * 4 * 2 * 128 * n * 16 / (ms.value * 1e-3) / 1e12)}
+    for ts, name in ((0, "ss"), (1, "ts")):
+        ms = C.c_float(0)
+        iters = 20000
+        rc = L.probe_rate2(iters, ts, C.c_void_p(cyc.data_ptr()), C.byref(ms))
+        c = float(cyc[:74].float().mean()) / (iters * 4)
+        rep[f"rate_cta2_m256_n64_{name}"] = {"rc": rc, "cycles_per_mma": round(c, 1),
+                                             "tflops": round(74 * iters * 4 * 2 * 256 * 64 * 16 / (ms.value * 1e-3) / 1e12)}
     wc = torch.zeros(4, dtype=torch.int64, device="cuda")
     it = 10000
     rc = L.probe_wait_cost(it, C.c_void_p(wc.data_ptr()))
