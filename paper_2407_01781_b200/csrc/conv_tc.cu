@@ -468,21 +468,19 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             mbar_wait(smem_u32(&bar_full[s]), ph);
             fence_proxy_async_smem();
             tc_fence_after();
-            if (lane == 0) {
-                const uint32_t so = s * C::STAGE;
-                for (int a = a_lo; a < a_hi; ++a) {
+            // whole warp runs the issue loop (warp-uniform operands); one elected lane issues
+            const uint32_t so = s * C::STAGE;
+            for (int a = a_lo; a < a_hi; ++a) {
 #pragma unroll
-                    for (int ks = 0; ks < C::TK / 16; ++ks) {
-                        const uint64_t ad = adesc0 + ((so + a * C::A_BLK + ks * 2048) >> 4);
-                        const uint64_t bd = bdesc0 + ((so + (C::B_SW128 ? ks * 2048 : ks * 1024)) >> 4);
-                        if (!(dbg & 1)) mma_bf16(tmem + a * COUT, ad, bd, C::IDESC, (step | ks) != 0);
-                    }
+                for (int ks = 0; ks < C::TK / 16; ++ks) {
+                    const uint64_t ad = adesc0 + ((so + a * C::A_BLK + ks * 2048) >> 4);
+                    const uint64_t bd = bdesc0 + ((so + (C::B_SW128 ? ks * 2048 : ks * 1024)) >> 4);
+                    if (!(dbg & 1)) mma_bf16_elect(tmem + a * COUT, ad, bd, C::IDESC, (step | ks) != 0);
                 }
-                mma_commit(smem_u32(&bar_empty[s]));
             }
-            __syncwarp();
+            mma_commit_elect(smem_u32(&bar_empty[s]));
         }
-        if (lane == 0) mma_commit(smem_u32(&bar_tfull));
+        mma_commit_elect(smem_u32(&bar_tfull));
         __syncwarp();
     } else {
         const int q = warp & 3;
