@@ -201,6 +201,25 @@ int fvdb_conv_halo_tc(const void* in_bf16, int64_t n_in, int K, const void* w_im
                       const fvdb_halo_plan* plan, int64_t n_out, void* out, int out_dtype,
                       void* stream);
 
+/* ---- U-Net glue (build.py:310-360, conv.py:401-446) ----
+ * expand: out[i*w^3 + j] = coords[i]*scale + (lo + j/w^2, lo + (j/w)%w, lo + j%w)  (k fastest)
+ *   subdivide(f): scale=f, lo=0, w=f (build.py:342-360);  dilate(r): scale=1, lo=-r, w=2r+1 (build.py:310-322)
+ * pool: out[c] = avg (float64 sum over the children in ascending fine-row order / child count, then
+ *   cast: np.add.at order, bit-identical for f32/f64) or max (NaN-propagating) of features[i] over the
+ *   fine rows i with prow1[i] == c+1 (conv.py:401-426).  prow1: 1-based parent rows (fvdb_coord_to_index).
+ *   Synchronizes; a fine row without parent -> FVDB_ERR_INVALID, detail = its row.
+ * gather_rows: dst[i] = src[idx1[i]-1] (row_bytes each); idx1[i] == 0 -> FVDB_ERR_INVALID with
+ *   detail = the first such i (upsample_nearest's orphan, conv.py:429-446).  workspace >= 4 bytes.
+ *   Synchronizes. */
+int fvdb_expand_coords(const int64_t* coords, int64_t n, int64_t scale, int64_t lo, int64_t width,
+                       int64_t* out, void* stream);
+size_t fvdb_pool_workspace_bytes(int64_t n_fine, int64_t n_coarse);
+int fvdb_pool(int dtype, const void* features, int64_t n_fine, int64_t channels, const int64_t* prow1,
+              int64_t n_coarse, int mode_max, void* out, int64_t* detail, void* workspace,
+              size_t workspace_bytes, void* stream);
+int fvdb_gather_rows(const void* src, int64_t row_bytes, const int64_t* idx1, int64_t n, void* dst,
+                     int64_t* detail, void* workspace, size_t workspace_bytes, void* stream);
+
 /* dtype conversion helpers (fp32 -> bf16 RNE), used at the module boundary */
 int fvdb_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream);
 

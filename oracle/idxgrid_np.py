@@ -22,6 +22,7 @@ __all__ = [
     "quantize", "build_from_coords", "build_from_points", "coarsen", "empty",
     "coord_to_index", "active_coords", "kernel_map", "kernel_map_table",
     "conv_igemm", "conv_backward", "conv_transpose", "conv_dense",
+    "subdivide", "dilate", "pool", "upsample_nearest",
 ]
 
 COORD_LIMIT = 1 << 30          # topology.py:24
@@ -375,3 +376,71 @@ def conv_dense(grid_in, features, weights, grid_out, stride=1):
         if ok.any():
             out[ok] += dense[q[ok, 0], q[ok, 1], q[ok, 2]] @ w[:, :, a + 1, b + 1, c + 1].astype(np.float64).T
     return out
+
+
+# ---------------------------------------------------------------------------
+# U-Net glue: subdivide / dilate (build.py:310-360), pool / upsample (conv.py:401-446)
+# ---------------------------------------------------------------------------
+
+def _cube(lo, width):
+    r = np.arange(lo, lo + width, dtype=np.int64)
+    return np.stack(np.meshgrid(r, r, r, indexing="ij"), -1).reshape(-1, 3)
+
+
+def subdivide(grid, factor):
+    """Every active voxel -> its factor^3 children; voxel size / factor, origin shifted (build.py:342-360)."""
+    factor = int(factor)
+    if factor < 1:
+        raise ValueError("subdivision factor must be >= 1")
+    c = active_coords(grid)
+    vs, og = grid.voxel_size, grid.origin
+    if factor > 1:
+        vs = vs / factor
+        og = og - vs * (factor - 1) / 2.0
+        c = (c[:, None, :] * factor + _cube(0, factor)[None]).reshape(-1, 3)
+    if len(c) == 0:
+        return empty(vs, og)
+    return build_from_coords(c, vs, og)
+
+
+def dilate(grid, radius):
+    """Union of the active set shifted by [-r, r]^3 (build.py:310-322)."""
+    radius = int(radius)
+    if radius < 1:
+        raise ValueError("dilation radius must be >= 1")
+    c = active_coords(grid)
+    if len(c) == 0:
+        return empty(grid.voxel_size, grid.origin)
+    c = (c[:, None, :] + _cube(-radius, 2 * radius + 1)[None]).reshape(-1, 3)
+    return build_from_coords(c, grid.voxel_size, grid.origin)
+
+
+def pool(grid, features, factor, mode="avg"):
+    """Average (float64, np.add.at row order, / active-child count) or max over active children (conv.py:401-426)."""
+    if mode not in ("avg", "max"):
+        raise ValueError(f"pool mode must be 'avg' or 'max', got {mode!r}")
+    factor = int(factor)
+    f = np.asarray(features)
+    coarse = coarsen(grid, factor)
+    if factor == 1:
+        return coarse, f.copy()
+    prow = coord_to_index(coarse, np.floor_divide(active_coords(grid), factor)) - 1
+    if mode == "avg":
+        acc = np.zeros((coarse.num_voxels,) + f.shape[1:], np.float64)
+        np.add.at(acc, prow, f)
+        cnt = np.bincount(prow, minlength=coarse.num_voxels).astype(np.float64)
+        return coarse, (acc / cnt.reshape(-1, *([1] * (f.ndim - 1)))).astype(f.dtype)
+    acc = np.full((coarse.num_voxels,) + f.shape[1:], -np.inf)
+    np.maximum.at(acc, prow, f)
+    return coarse, acc.astype(f.dtype)
+
+
+def upsample_nearest(coarse, features, factor, fine):
+    """Each fine voxel copies its floor-division parent's row; orphans raise (conv.py:429-446)."""
+    factor = int(factor)
+    fc = active_coords(fine)
+    prow = coord_to_index(coarse, np.floor_divide(fc, factor) if factor > 1 else fc) - 1
+    if (prow < 0).any():
+        bad = fc[int(np.flatnonzero(prow < 0)[0])]
+        raise ValueError(f"fine voxel {tuple(bad.tolist())} has no active parent")
+    return np.asarray(features)[prow]

@@ -84,6 +84,10 @@ SIGNATURES = {
     "fvdb_halo_plan_fill": (_i32, [_vp, _i64, _i64, _vp, _vp, C.POINTER(HaloPlan), _vp]),
     "fvdb_pack_weights_halo": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp]),
     "fvdb_conv_halo_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, C.POINTER(HaloPlan), _i64, _vp, _i32, _vp]),
+    "fvdb_expand_coords": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "fvdb_pool_workspace_bytes": (_sz, [_i64, _i64]),
+    "fvdb_pool": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _i32, _vp, C.POINTER(_i64), _vp, _sz, _vp]),
+    "fvdb_gather_rows": (_i32, [_vp, _i64, _vp, _i64, _vp, C.POINTER(_i64), _vp, _sz, _vp]),
 }
 
 _LIB = None

@@ -143,3 +143,43 @@ def coarsen(grid, factor):
         return empty_grid(tc, grid.name)
     g, _ = build_from_coords(coords, tc, grid.name)
     return g
+
+
+def _expand(coords: torch.Tensor, scale: int, lo: int, width: int) -> torch.Tensor:
+    n = coords.shape[0]
+    out = torch.empty((n * width ** 3, 3), dtype=torch.int64, device=coords.device)
+    if n:
+        _lib.check(_lib.lib().fvdb_expand_coords(coords.contiguous().data_ptr(), n, int(scale), int(lo), int(width),
+                                                 out.data_ptr(), _lib.stream_ptr()), "expand_coords")
+    return out
+
+
+def subdivide(grid, factor):
+    """Every active voxel expands to its factor^3 children (build.py:342-360)."""
+    factor = int(factor)
+    if factor < 1:
+        raise ValueError("subdivision factor must be >= 1")
+    coords = grid.active_coords()
+    t = grid.transform
+    if factor == 1:
+        tf = t
+    else:
+        vs = t.voxel_size / factor
+        tf = VoxelTransform(vs, t.origin - vs * (factor - 1) / 2.0)
+        coords = _expand(coords, factor, 0, factor)
+    if coords.shape[0] == 0:
+        return empty_grid(tf, grid.name)
+    g, _ = build_from_coords(coords, tf, grid.name)
+    return g
+
+
+def dilate(grid, radius):
+    """Morphological dilation by the cubic structuring element [-r, r]^3 (build.py:310-322)."""
+    radius = int(radius)
+    if radius < 1:
+        raise ValueError("dilation radius must be >= 1")
+    coords = grid.active_coords()
+    if coords.shape[0] == 0:
+        return empty_grid(grid.transform, grid.name)
+    g, _ = build_from_coords(_expand(coords, 1, -radius, 2 * radius + 1), grid.transform, grid.name)
+    return g

@@ -611,3 +611,88 @@ def batch_grid_kernel_map(batch_in, batch_out, stride):
                                                        batch_out.voxel_joffsets[:, 0].tolist())
     batch_out._kmaps[key] = km
     return km
+
+
+# ---------------------------------------------------------------------------
+# U-Net glue: pool / upsample_nearest (conv.py:386-446)
+# ---------------------------------------------------------------------------
+
+def _floor_div(coords: torch.Tensor, factor: int) -> torch.Tensor:
+    if factor == 1 or coords.shape[0] == 0:
+        return coords
+    out = torch.empty_like(coords)
+    _lib.check(_lib.lib().fvdb_floor_div_coords(coords.data_ptr(), coords.shape[0], int(factor), out.data_ptr(),
+                                                _lib.stream_ptr()), "floor_div")
+    return out
+
+
+def pool(grid, features, factor, mode="avg"):
+    """Reduce features onto the coarsened grid over active fine children only (conv.py:401-426).
+
+    ``avg`` divides by the count of active children (not factor^3), accumulating in float64 in the
+    reference's order; ``max`` takes their componentwise maximum.  Returns (coarse_grid, coarse_features).
+    """
+    if mode not in ("avg", "max"):
+        raise ValueError(f"pool mode must be 'avg' or 'max', got {mode!r}")
+    factor = int(factor)
+    dev = grid.device
+    feats = _to_device_tensor(features, dev)
+    if feats.shape[0] != grid.num_voxels:
+        raise ValueError(f"features rows {feats.shape[0]} != voxel count {grid.num_voxels}")
+    coarse = _coarsen_grid(grid, factor)
+    if factor == 1:
+        return coarse, feats.clone()
+    prow = coarse.coord_to_index_many(_floor_div(grid.active_coords(), factor))
+    chans = int(np.prod(feats.shape[1:])) if feats.ndim > 1 else 1
+    out = torch.empty((coarse.num_voxels,) + tuple(feats.shape[1:]), dtype=feats.dtype, device=dev)
+    if grid.num_voxels:
+        L = _lib.lib()
+        wsb = L.fvdb_pool_workspace_bytes(grid.num_voxels, coarse.num_voxels)
+        ws = _lib.workspace(wsb, dev)
+        detail = C.c_int64(-1)
+        f = feats.contiguous()
+        _lib.check(L.fvdb_pool(_dtype_code(f.dtype), f.data_ptr(), grid.num_voxels, chans, prow.data_ptr(),
+                               coarse.num_voxels, int(mode == "max"), out.data_ptr(), C.byref(detail),
+                               ws.data_ptr(), wsb, _lib.stream_ptr()), "pool")
+    return coarse, out
+
+
+def upsample_nearest(coarse_grid, features, factor, fine_grid):
+    """Copy each fine active voxel's feature from its floor-division parent (conv.py:429-446)."""
+    factor = int(factor)
+    dev = fine_grid.device
+    feats = _to_device_tensor(features, dev).contiguous()
+    if feats.shape[0] != coarse_grid.num_voxels:
+        raise ValueError(
+            f"features rows {feats.shape[0]} != coarse voxel count {coarse_grid.num_voxels}")
+    fine_coords = fine_grid.active_coords()
+    prow = coarse_grid.coord_to_index_many(_floor_div(fine_coords, factor) if factor > 1 else fine_coords)
+    out = torch.empty((fine_grid.num_voxels,) + tuple(feats.shape[1:]), dtype=feats.dtype, device=dev)
+    n = fine_grid.num_voxels
+    if n:
+        L = _lib.lib()
+        ws = _lib.workspace(256, dev)
+        detail = C.c_int64(-1)
+        row_bytes = feats[0].numel() * feats.element_size() if feats.shape[0] else 1
+        rc = L.fvdb_gather_rows(feats.data_ptr(), row_bytes, prow.data_ptr(), n, out.data_ptr(), C.byref(detail),
+                                ws.data_ptr(), 256, _lib.stream_ptr())
+        if rc == _lib.FVDB_ERR_INVALID and detail.value >= 0:
+            bad = fine_coords[int(detail.value)].tolist()
+            raise ValueError(f"fine voxel {tuple(bad)} has no active parent")
+        _lib.check(rc, "upsample_nearest")
+    return out
+
+
+def pool_batch(batch, features, factor, mode="avg"):
+    """Pooling applied per batch element; returns (coarse GridBatch, features) (conv.py:386-398)."""
+    from .jagged import GridBatch
+    if not isinstance(batch, GridBatch):
+        raise TypeError("pool_batch needs a GridBatch; use pool() for a single grid")
+    feats = _to_device_tensor(batch.check_features(features), batch.device)
+    coarse, parts = [], []
+    for b, g in enumerate(batch.grids):
+        cg, cf = pool(g, feats[batch.voxel_slice(b)], factor, mode)
+        coarse.append(cg)
+        parts.append(cf)
+    out = GridBatch(coarse)
+    return out, out.jagged(torch.cat(parts, 0))
