@@ -220,6 +220,24 @@ int fvdb_pool(int dtype, const void* features, int64_t n_fine, int64_t channels,
 int fvdb_gather_rows(const void* src, int64_t row_bytes, const int64_t* idx1, int64_t n, void* dst,
                      int64_t* detail, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- grid <-> point transfer (interp.py:44-203) ----
+ * stencil: u = (p - origin) / voxel_size (IEEE f64), mode 0 trilinear (8 taps) / 1 bezier (27 taps);
+ *   rows[n][S] 0-based voxel row or -1, weights[n][S] f64, dweights[n][S][3] (world-space d/dp) or NULL.
+ *   voxel_size3 / origin3 are HOST arrays.
+ * sample: out[p][c] = sum_s w*f[row] in f64, s ascending; grads[p][c][3] likewise (or NULL).  f32/f64.
+ * splat : out[v][c] = sum over (p,s) with row == v of w*f[p][c], f64, in (p,s) order (stable sort by
+ *   destination, interp.py:195-202): bitwise reproducible.  out must hold n_vox*channels elements. */
+int fvdb_interp_stencil(const fvdb_grid_view* grid, const double* points, int64_t n,
+                        const double* voxel_size3, const double* origin3, int mode, int64_t* rows,
+                        double* weights, double* dweights, void* stream);
+int fvdb_interp_sample(int dtype, const void* features, int64_t channels, const int64_t* rows,
+                       const double* weights, const double* dweights, int64_t n, int stencil, void* out,
+                       void* grads, void* stream);
+size_t fvdb_splat_workspace_bytes(int64_t n_points, int stencil, int64_t n_vox);
+int fvdb_interp_splat(int dtype, const void* point_features, int64_t channels, const int64_t* rows,
+                      const double* weights, int64_t n_points, int stencil, int64_t n_vox, void* out,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
 /* dtype conversion helpers (fp32 -> bf16 RNE), used at the module boundary */
 int fvdb_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream);
 

@@ -22,7 +22,7 @@ __all__ = [
     "quantize", "build_from_coords", "build_from_points", "coarsen", "empty",
     "coord_to_index", "active_coords", "kernel_map", "kernel_map_table",
     "conv_igemm", "conv_backward", "conv_transpose", "conv_dense",
-    "subdivide", "dilate", "pool", "upsample_nearest",
+    "subdivide", "dilate", "pool", "upsample_nearest", "interp_stencil", "sample", "splat",
 ]
 
 COORD_LIMIT = 1 << 30          # topology.py:24
@@ -444,3 +444,70 @@ def upsample_nearest(coarse, features, factor, fine):
         bad = fc[int(np.flatnonzero(prow < 0)[0])]
         raise ValueError(f"fine voxel {tuple(bad.tolist())} has no active parent")
     return np.asarray(features)[prow]
+
+
+# ---------------------------------------------------------------------------
+# grid <-> point transfer (interp.py:44-203)
+# ---------------------------------------------------------------------------
+
+def _axis_weights(u, mode):
+    """Per-axis taps: trilinear 2 (floor base), bezier 3 (quadratic B-spline, round base) (interp.py:44-72)."""
+    if mode == "trilinear":
+        base = np.floor(u)
+        f = u - base
+        w = np.stack([1.0 - f, f], axis=2)
+        dw = np.stack([-np.ones_like(f), np.ones_like(f)], axis=2)
+        offs = np.array([0, 1], np.int64)
+    else:
+        base = np.floor(u + 0.5)
+        offs = np.array([-1, 0, 1], np.int64)
+        x = u[:, :, None] - (base[:, :, None] + offs)
+        ax = np.abs(x)
+        outer = np.maximum(1.5 - ax, 0.0)
+        w = np.where(ax <= 0.5, 0.75 - x * x, 0.5 * outer * outer)
+        dw = np.where(ax <= 0.5, -2.0 * x, -np.sign(x) * outer)
+    return base.astype(np.int64), offs, w, dw
+
+
+def interp_stencil(grid, points, mode):
+    """rows [n,S] (-1 background), weights [n,S], world-space weight gradients [n,S,3] (interp.py:75-107)."""
+    u = (np.asarray(points, np.float64) - grid.origin) / grid.voxel_size
+    base, offs, w, dw = _axis_weights(u, mode)
+    k = len(offs)
+    sten = np.stack(np.meshgrid(offs, offs, offs, indexing="ij"), -1).reshape(-1, 3)
+    rows = coord_to_index(grid, (base[:, None, :] + sten[None]).reshape(-1, 3)).reshape(len(u), -1) - 1
+    wx, wy, wz = w[:, 0, :, None, None], w[:, 1, None, :, None], w[:, 2, None, None, :]
+    dx, dy, dz = dw[:, 0, :, None, None], dw[:, 1, None, :, None], dw[:, 2, None, None, :]
+    inv = 1.0 / grid.voxel_size
+    weights = (wx * wy * wz).reshape(len(u), k ** 3)
+    dweights = np.stack([(dx * wy * wz).reshape(len(u), k ** 3) * inv[0],
+                         (wx * dy * wz).reshape(len(u), k ** 3) * inv[1],
+                         (wx * wy * dz).reshape(len(u), k ** 3) * inv[2]], axis=2)
+    return rows, weights, dweights
+
+
+def sample(grid, features, points, mode="trilinear"):
+    """Values [n,C] and gradients [n,C,3]: f64 sums over the stencil (interp.py:142-164)."""
+    f = np.asarray(features)
+    rows, w, dw = interp_stencil(grid, points, mode)
+    padded = np.concatenate([f.astype(np.float64), np.zeros((1, f.shape[1]))])
+    neigh = padded[rows]
+    return (np.einsum("ns,nsc->nc", w, neigh).astype(f.dtype),
+            np.einsum("nsx,nsc->ncx", dw, neigh).astype(f.dtype))
+
+
+def splat(grid, points, point_features, mode="trilinear"):
+    """Per-voxel sums of w * f over (point, tap) in stable destination order (interp.py:167-203)."""
+    pf = np.asarray(point_features)
+    rows, w, _ = interp_stencil(grid, points, mode)
+    contrib = (w[:, :, None] * pf.astype(np.float64)[:, None, :]).reshape(-1, pf.shape[1])
+    rows = rows.ravel()
+    keep = rows >= 0
+    rows, contrib = rows[keep], contrib[keep]
+    out = np.zeros((grid.num_voxels, pf.shape[1]), np.float64)
+    if len(rows):
+        order = np.argsort(rows, kind="stable")
+        rows, contrib = rows[order], contrib[order]
+        starts = np.concatenate(([0], np.flatnonzero(rows[1:] != rows[:-1]) + 1))
+        out[rows[starts]] += np.add.reduceat(contrib, starts, axis=0)
+    return out.astype(pf.dtype)

@@ -88,6 +88,11 @@ SIGNATURES = {
     "fvdb_pool_workspace_bytes": (_sz, [_i64, _i64]),
     "fvdb_pool": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _i32, _vp, C.POINTER(_i64), _vp, _sz, _vp]),
     "fvdb_gather_rows": (_i32, [_vp, _i64, _vp, _i64, _vp, C.POINTER(_i64), _vp, _sz, _vp]),
+    "fvdb_interp_stencil": (_i32, [C.POINTER(GridView), _vp, _i64, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                   _i32, _vp, _vp, _vp, _vp]),
+    "fvdb_interp_sample": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp]),
+    "fvdb_splat_workspace_bytes": (_sz, [_i64, _i32, _i64]),
+    "fvdb_interp_splat": (_i32, [_i32, _vp, _i64, _vp, _vp, _i64, _i32, _i64, _vp, _vp, _sz, _vp]),
 }
 
 _LIB = None
