@@ -71,7 +71,8 @@ __host__ __device__ __forceinline__ int halo_phys(int K, int s, int c) {
     return K == 64 ? (c ^ (s & 1)) : (K == 128 ? (c ^ ((s & 1) << 2)) : c);
 }
 
-constexpr int kImgExt = 34;  // weight images per layer: 27 offsets + 7 wrap-around copies (d = 0..6)
+constexpr int kImgExt = 34;
+constexpr int kHalves = 2;  // builder/MMA half-pipelines  // weight images per layer: 27 offsets + 7 wrap-around copies (d = 0..6)
 
 // Two half-pipelines (builder warps of half h -> MMA warp h -> accumulator set h) take alternate
 // batches of BATCH consecutive (tile, offset) stages.  Why two MMA issuers: at N <= 128 a single
@@ -108,13 +109,15 @@ struct HaloCfg {
     static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, N, false, false);
     static_assert(fits(NSL, BATCH) && CAP >= 256, "halo capacity must hold one offset phase (2 x 128 slots)");
     static_assert(27 + BATCH - 1 <= kImgExt, "weight batch wraps past the extended image array");
+    // builder warps per (half, lane quarter), building alternate stages of a batch (K=128 builders hold
+    // 64 data registers: one per slot keeps them within the register budget)
+    static constexpr int SUBS = (K >= 128 || BATCH < 2) ? 1 : 2;
+    static constexpr int BUILDERS = 4 * kHalves * SUBS;
+    static constexpr int THREADS = (3 + BUILDERS + 4 + 1) * 32;
 };
 
-constexpr int kHalves = 2;
-constexpr int kBuilders = 4 * kHalves;
-// warps: 0 halo loader, 1-2 MMA (half 0, 1), 3-10 builders, 11-14 epilogue, 15 weight loader
-constexpr int kHaloWarps = 3 + kBuilders + 4 + 1;
-constexpr int kHaloThreads = kHaloWarps * 32;
+// warps: 0 halo loader, 1-2 MMA (half 0, 1), 3.. builders (4 quarters x 2 halves x SUBS), 4 epilogue,
+// 1 weight loader
 
 // profiling trace (FVDB_DEBUG_HALO & 64): clock64 stamps of CTA 0, kTraceN events per channel
 constexpr int kTraceCh = 12, kTraceN = 2048;
@@ -127,10 +130,11 @@ __device__ __forceinline__ void trace(int dbg, int ch, uint32_t i) {
 // conv kernel
 // ---------------------------------------------------------------------------------------------
 template <int K, int N, bool OUT_BF16, int V = 0>
-__global__ void __launch_bounds__(kHaloThreads, 1)
+__global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
     k_conv_halo(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, fvdb_halo_plan P,
                 int64_t n_out, void* __restrict__ out, int dbg) {
     using C = HaloCfg<K, N, V>;
+    constexpr int kSubs = C::SUBS, kBuilders = C::BUILDERS;
     constexpr int W_LOAD = 0, W_MMA = 1, W_BLD = 3, W_EPI = 3 + kBuilders, W_BLOAD = W_EPI + 4;
     constexpr int BATCH = C::BATCH, NACC = C::NACC, NSL = C::NSL;
     extern __shared__ uint8_t dsmem[];
@@ -162,7 +166,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             mbar_init(smem_u32(&bar_iempty[b]), kBuilders);
         }
         for (int b = 0; b < 2 * NSL; ++b) {
-            mbar_init(smem_u32(&bar_afull[b]), 4);
+            mbar_init(smem_u32(&bar_afull[b]), 4 * (kSubs < BATCH ? kSubs : BATCH));
             mbar_init(smem_u32(&bar_adone[b]), 1);
             mbar_init(smem_u32(&bar_bfull[b]), 1);
         }
@@ -275,7 +279,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         // ---------------- A builders: halo (smem) -> registers -> TMEM (16x256b) ----------------
         // Each builder walks only its half's stages (batches ab with ab % 2 == half) inside every phase.
         const int q = warp & 3;                        // TMEM lane quarter this warp may access
-        const int half = (warp - W_BLD) / 4;
+        const int half = ((warp - W_BLD) / 4) % 2;
+        const int sub = (warp - W_BLD) / 8;            // builds the stages with within % kSubs == sub
         const int t0 = lane & 3, t1 = lane >> 2;
         const int lrow = q * 32 + t1;                  // first of this thread's 4 lanes (+8, +16, +24)
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 mbar_wait(smem_u32(&bar_hfull[buf]), par);
                 mbar_wait(smem_u32(&bar_ifull[buf]), par);
                 if (ac < s1) {
-                    if (lane == 0 && q == 0 && half == 0) trace(dbg, 5, pc);
+                    if (lane == 0 && q == 0 && half == 0 && sub == 0) trace(dbg, 5, pc);
                     const uint16_t* lb = reinterpret_cast<const uint16_t*>(gen + ibase + buf * kIdxBytes) -
                                          (int)(s0 - g * gs) * kTileRows;  // indexed by stage: (ac - 27·lt) = d
                     const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
@@ -300,10 +305,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                         const uint32_t hbi = ab >> 1, k = half * NSL + hbi % NSL, use = hbi / NSL;
                         if (within == 0) {  // first stage of my batch: wait until my MMA warp released the slot
                             mbar_wait(ADONE + 8 * k, (use & 1) ^ 1);
-                            if (lane == 0 && q == 0) trace(dbg, 2, ab);
+                            if (lane == 0 && q == 0 && sub == 0) trace(dbg, 2, ab);
                             tc_fence_after();
                         }
-                        if (!(dbg & 2)) {  // lanes without a pair get zero A rows: the MMA needs no lane mask
+                        if ((int)(within % kSubs) == sub && !(dbg & 2)) {  // zero A rows for lanes without a pair
                             const uint16_t* lr = lb + (int)ac * kTileRows + lrow;
                             const int sl[4] = {lr[0], lr[8], lr[16], lr[24]};
                             const uint32_t acol = tmem + lane_off + C::ACC + (k * BATCH + within) * C::ACOLS;
@@ -330,17 +335,20 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                                     }
                                 }
                             }
+                            if (lane == 0 && q == 0 && sub == 0 && half == 0) trace(dbg, 4, ac);
 #pragma unroll
                             for (int gg = 0; gg < 2; ++gg)
                                 tmem_st16x256<C::NX>(acol + ((uint32_t)(gg * 16) << 16), v[gg]);
+                            if (lane == 0 && q == 0 && sub == 0 && half == 0) trace(dbg, 7, ac);
                         }
                         ++ac;
                         if (within == BATCH - 1 || ac == nstages) {  // publish the batch, skip the other half's
                             tmem_st_wait();
+                            if (lane == 0 && q == 0 && sub == 0 && half == 0) trace(dbg, 8, ab);
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) {
-                                if (q == 0) trace(dbg, 3, ab);
+                                if (q == 0 && sub == 0) trace(dbg, 3, ab);
                                 mbar_arrive(AFULL + 8 * k);
                             }
                             ac += BATCH;
@@ -723,7 +731,7 @@ int launch_halo_v(const void* in, const void* wimg, const fvdb_halo_plan& P, int
     if (grid > P.num_tiles) grid = P.num_tiles;
     // profiling switches (FVDB_DEBUG_HALO): 1 no MMA, 2 no A build, 4 no output stores, 8 no halo loads
     static const int dbg = getenv("FVDB_DEBUG_HALO") ? atoi(getenv("FVDB_DEBUG_HALO")) : 0;
-    kern<<<grid, kHaloThreads, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, P, n_out, out, dbg);
+    kern<<<grid, C::THREADS, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, P, n_out, out, dbg);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

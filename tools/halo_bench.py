@@ -35,8 +35,15 @@ def timed(fn, reps=10):
 
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-    res, C = {"cfg2": (470, 64), "cfg5": (2048, 32), "cfg2_128": (470, 128)}[cfg]
-    g, _ = P.build_from_coords(sphere_shell_coords(res, 1.5))
+    import numpy as np
+    if cfg.startswith("dense"):  # dense block (100% leaf occupancy): the reference's leaf/brick regime
+        side, C = {"dense": (128, 64), "dense128": (96, 128), "dense32": (160, 32)}[cfg]
+        r = np.arange(side)
+        coords = np.stack(np.meshgrid(r, r, r, indexing="ij"), -1).reshape(-1, 3)
+    else:
+        res, C = {"cfg2": (470, 64), "cfg5": (2048, 32), "cfg2_128": (470, 128)}[cfg]
+        coords = sphere_shell_coords(res, 1.5)
+    g, _ = P.build_from_coords(coords)
     km = P.build_kernel_map(g, g, 1)
     n = g.num_voxels
     pairs = km.total_pairs

@@ -30,6 +30,11 @@ print("MMA half0 stages: start(ac) end(ac) | after_bfull(ab) after_afull(ab)")
 for a in range(40):
     print(a, *[int(t[c, a] - t0) if t[c, a] else -1 for c in (4, 7)], "|", *[int(t[c, a // 2] - t0) if t[c, a // 2] else -1 for c in (0, 1)])
 print("MMA tempty(lt)", [int(t[8, i] - t0) if t[8, i] else -1 for i in range(6)])
+print("builder half0 sub0 q0: stage ac: after_loads after_sttm | batch: adone st_waited publish")
+for a in range(0, 40, 4):
+    ab = a // 2
+    print(a, *[int(t[c, a] - t0) if t[c, a] else -1 for c in (4, 7)], "|",
+          *[int(t[c, ab] - t0) if t[c, ab] else -1 for c in (2, 8, 3)])
 print("phase  ld_hempty ld_idx bld_phase epi_tfull(tile)")
 for p in range(10):
     print(p, [(int(t[c, p] - t0) if t[c, p] else -1) for c in (9, 10, 5, 11)])
