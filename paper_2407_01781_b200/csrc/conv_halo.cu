@@ -93,7 +93,7 @@ struct HaloCfg {
     static constexpr int B_BYTES = N * K * 2;               // one offset's weight image
     static constexpr int ACOLS = K / 2;                     // TMEM columns of one A stage
     // accumulator buffers per half: 2 (epilogue overlaps the next tile) when TMEM allows
-    static constexpr int NACC = V != 0 ? 1 : (4 * N + 2 * ACOLS <= 512 ? 2 : 1);
+    static constexpr int NACC = (V == 1 || V == 2) ? 1 : (4 * N + 2 * ACOLS <= 512 ? 2 : 1);
     static constexpr int ACC = 2 * NACC * N;                // accumulator columns (both halves)
     // NSL slots per half (2: a half's builders fill one slot while its MMA warp drains the other)
     static constexpr int fits(int nsl, int b) {
@@ -111,7 +111,7 @@ struct HaloCfg {
     static_assert(27 + BATCH - 1 <= kImgExt, "weight batch wraps past the extended image array");
     // builder warps per (half, lane quarter), building alternate stages of a batch (K=128 builders hold
     // 64 data registers: one per slot keeps them within the register budget)
-    static constexpr int SUBS = (K >= 128 || BATCH < 2) ? 1 : 2;
+    static constexpr int SUBS = (K >= 128 || BATCH < 2 || (K == 32 && V == 3)) ? 1 : 2;
     static constexpr int BUILDERS = 4 * kHalves * SUBS;
     static constexpr int THREADS = (3 + BUILDERS + 4 + 1) * 32;
 };
@@ -741,6 +741,9 @@ int launch_halo(const void* in, const void* wimg, const fvdb_halo_plan& P, int64
     if constexpr (K == 64 && N == 64) {
         if (halo_variant() == 1) return launch_halo_v<K, N, OB, 1>(in, wimg, P, n_out, out, st);
         if (halo_variant() == 2) return launch_halo_v<K, N, OB, 2>(in, wimg, P, n_out, out, st);
+    }
+    if constexpr (K == 32 && N == 32) {
+        if (halo_variant() == 3) return launch_halo_v<K, N, OB, 3>(in, wimg, P, n_out, out, st);
     }
     return launch_halo_v<K, N, OB, 0>(in, wimg, P, n_out, out, st);
 }
