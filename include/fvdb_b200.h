@@ -146,6 +146,17 @@ int fvdb_pack_weights_umma(const float* w, int cout, int cin, int transpose, voi
 int fvdb_conv_gather_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
                         const int32_t* nbr, int64_t ld, int64_t n_out, void* out, int out_dtype,
                         void* stream);
+/* Signature-sorted tables for sparse maps: perm[i] = output row of table column i, rows stably sorted by
+ * their 27-bit signature (bit d = offset d has a pair), and nbr_perm[d][i] = nbr[d][perm[i]].  Run over
+ * nbr_perm, the gather kernel's 128-row tiles are homogeneous, so (tile, offset) stages without any pair
+ * skip their copies and MMAs (transposed stride-2 maps: ~3 of 27 offsets per row).
+ * fvdb_conv_gather_tc_perm = fvdb_conv_gather_tc writing table column i to output row perm[i]. */
+size_t fvdb_kmap_signature_workspace_bytes(int64_t n_out);
+int fvdb_kmap_signature_order(const int32_t* nbr, int64_t ld, int64_t n_out, int32_t* perm, int32_t* nbr_perm,
+                              void* workspace, size_t workspace_bytes, void* stream);
+int fvdb_conv_gather_tc_perm(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
+                             const int32_t* nbr_perm, int64_t ld, int64_t n_out, const int32_t* row_perm,
+                             void* out, int out_dtype, void* stream);
 /* wgrad on tensor cores: gw fp32 [cout][cin][27]. */
 size_t fvdb_wgrad_tc_workspace_bytes(int64_t n_out, int cin, int cout);
 int fvdb_conv_wgrad_tc(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,

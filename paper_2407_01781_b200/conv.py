@@ -120,12 +120,38 @@ class NbrTable:
     uses to pair lanes; halo plans are built lazily per kernel capacity and cached.
     """
 
-    __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses")
+    __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted")
 
-    def __init__(self, t, n, colors_fn=None):
+    def __init__(self, t, n, colors_fn=None, counts=None):
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
         self._colors_fn, self._colors, self._plans = colors_fn, None, {}
         self.uses = 0  # bf16 tensor-core convolutions run over this table (conv_impl "auto")
+        self.counts = counts  # per-offset pair counts (device or host int64 [27]), when known
+        self._density = None
+        self._sorted = None
+
+    def density(self) -> float:
+        """Mean pairs per output row (27 = every offset active); 27 when unknown."""
+        if self._density is None:
+            if self.counts is None or self.n == 0:
+                self._density = 27.0
+            else:
+                self._density = float(self.counts.sum().item()) / self.n
+        return self._density
+
+    def signature_sorted(self):
+        """(nbr_perm table, perm): rows stably sorted by their 27-bit offset signature, cached."""
+        if self._sorted is None:
+            L = _lib.lib()
+            perm = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.t.device)
+            tp = torch.empty_like(self.t)
+            wsb = L.fvdb_kmap_signature_workspace_bytes(self.n)
+            ws = _lib.workspace(wsb, self.t.device)
+            _lib.check(L.fvdb_kmap_signature_order(self.t.data_ptr(), self.ld, self.n, perm.data_ptr(),
+                                                   tp.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()),
+                       "kmap_signature_order")
+            self._sorted = (tp, perm)
+        return self._sorted
 
     def has_plan(self, K: int, N: int) -> bool:
         cap = int(_lib.lib().fvdb_halo_cap(K, N))
@@ -201,6 +227,8 @@ class KernelMap:
             self._lists = (ins, outs)
             pair_counts = torch.tensor([int(o.numel()) for o in outs], dtype=torch.int64)
             table = NbrTable(t, self.num_out)
+        if table.counts is None:
+            table.counts = pair_counts
         if table._colors_fn is None and grids is not None:
             table._colors_fn = self._fwd_colors
         self.fwd = table
@@ -272,7 +300,8 @@ class KernelMap:
             L = _lib.lib()
             _lib.check(L.fvdb_kmap_transpose(self.fwd.t.data_ptr(), self.fwd.ld, self.num_out, self.num_in,
                                              t.data_ptr(), t.shape[1], _lib.stream_ptr()), "kmap_transpose")
-            self._bwd = NbrTable(t, self.num_in, self._bwd_colors if self._grids is not None else None)
+            self._bwd = NbrTable(t, self.num_in, self._bwd_colors if self._grids is not None else None,
+                                 counts=self._counts)
         return self._bwd
 
     def transposed_table(self):
@@ -356,13 +385,36 @@ def pack_weights_kn(w: torch.Tensor, transpose: bool, dtype) -> torch.Tensor:
     return out
 
 
+HALO_AFTER_USES = 4  # conv_impl "auto": uses of a table before its halo plan is built
+SORT_BELOW_DENSITY = 10.0  # gather kernel: signature-sort tables with fewer mean pairs per row
+
+
+def sig_sort_enabled(nbr: "NbrTable") -> bool:
+    """Run the gather kernel over the signature-sorted table?
+
+    Sorting output rows by which offsets they have (fvdb_kmap_signature_order) makes 128-row tiles
+    homogeneous, so the kernel skips the copies and MMAs of (tile, offset) stages with no pair.
+    Sparse maps gain (a transposed stride-2 map has ~3 of 27 offsets per row); dense ones
+    only pay the sort.  Opt-in: env FVDB_SIG_SORT=1 sorts tables below ``SORT_BELOW_DENSITY``,
+    "force" sorts every table.  Measured on B200 (tools/sigsort_bench.py), cfg4's transposed map
+    at 3.1 pairs/row runs 0.858 -> 0.645 ms per conv after a 0.21 ms one-off sort, while the halo
+    kernel runs the same map in 0.526 ms, so "auto" does not sort.
+    """
+    v = os.environ.get("FVDB_SIG_SORT", "0")
+    if v == "force":
+        return True
+    return v == "1" and nbr.density() < SORT_BELOW_DENSITY
+
+
 def conv_impl() -> str:
     """Tensor-core conv kernel policy, env FVDB_CONV_IMPL:
 
-    * "auto" (default): the gather-GEMM kernel (conv_tc.cu) on a neighbour table's first bf16 use,
-      the halo-staged kernel (conv_halo.cu) from its second use on.  The halo plan costs a few
-      conv launches to build, so it pays off only for maps that are reused (layers sharing a grid,
-      training iterations, the backward pass of a cached map), not for one-shot maps;
+    * "auto" (default): the gather-GEMM kernel (conv_tc.cu) for a neighbour table's first
+      ``HALO_AFTER_USES`` bf16 uses, then the halo-staged kernel (conv_halo.cu); immediately if the
+      table already has a plan.  Building the plan costs ~3-6 gather convolutions (cfg2: 2.2 ms vs
+      0.67 ms per conv, saving ~0.3 ms per use), so it pays off for maps reused across layers and
+      training iterations, not for maps used once or twice (cfg4 rebuilds its maps every step and uses
+      each in one forward and one backward);
     * "halo" / "gather": always that kernel.
     """
     v = os.environ.get("FVDB_CONV_IMPL", "auto")
@@ -444,7 +496,7 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
     else:
         impl = impl or conv_impl()
         if impl == "auto":
-            impl = "halo" if nbr.uses > 0 or nbr.has_plan(K, N) else "gather"
+            impl = "halo" if nbr.uses >= HALO_AFTER_USES or nbr.has_plan(K, N) else "gather"
     nbr.uses += 1
     img = w_image if w_image is not None else pack_weights_umma(w, transpose, impl)
     out = torch.empty((n_out, N), dtype=out_dtype, device=x.device)
@@ -454,6 +506,11 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
         plan = nbr.halo_plan(K, N)
         _lib.check(L.fvdb_conv_halo_tc(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, C.byref(plan.c), n_out,
                                        out.data_ptr(), _dtype_code(out_dtype), st), "conv_halo_tc")
+    elif sig_sort_enabled(nbr):
+        tp, perm = nbr.signature_sorted()
+        _lib.check(L.fvdb_conv_gather_tc_perm(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, tp.data_ptr(), nbr.ld,
+                                              n_out, perm.data_ptr(), out.data_ptr(), _dtype_code(out_dtype), st),
+                   "conv_gather_tc_perm")
     else:
         _lib.check(L.fvdb_conv_gather_tc(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, nbr.t.data_ptr(), nbr.ld,
                                          n_out, out.data_ptr(), _dtype_code(out_dtype), st), "conv_gather_tc")

@@ -26,6 +26,7 @@
 // (MN-major B = grad_out rows, shared by every offset of the CTA), K = output rows.
 // A CTA owns up to 8 M-blocks (TMEM ≤ 512 columns) for one output-row split;
 // partial [split][27][Cin][Cout] sums are reduced in a fixed order (deterministic).
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_bf16.h>
 #include <stdlib.h>
 
@@ -80,7 +81,8 @@ __host__ __device__ constexpr int fwd_threads(int npw) { return (npw + 6) * 32; 
 template <int K, int N, bool OUT_BF16, int TPS = (N <= 64 ? 4 : 2), int NPW = 4>
 __global__ void __launch_bounds__(fwd_threads(NPW), 1)
     k_conv_fwd_tc(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, const int32_t* __restrict__ nbr,
-                  int64_t ld, int64_t n_out, void* __restrict__ out, int num_super, int dbg) {
+                  int64_t ld, int64_t n_out, void* __restrict__ out, int num_super, int dbg,
+                  const int32_t* __restrict__ row_perm) {
     using C = FwdCfg<K, N, TPS>;
     constexpr int W_LOAD = NPW, W_MMA = NPW + 1, W_EPI = NPW + 2;
     constexpr int RPW = kTile / NPW;  // rows per gather warp per tile
@@ -252,7 +254,9 @@ __global__ void __launch_bounds__(fwd_threads(NPW), 1)
             mbar_wait_sleep(smem_u32(&bar_tfull[buf]), (lt >> 1) & 1, 512);
             tc_fence_after();
             for (int t = 0; t < C::TPS; ++t) {
-                const int64_t row = (int64_t)st * C::SUPER + t * kTile + q * 32 + lane;
+                const int64_t slot = (int64_t)st * C::SUPER + t * kTile + q * 32 + lane;
+                // row_perm: table column -> output row (signature-sorted tables, fvdb_kmap_signature_order)
+                const int64_t row = row_perm ? (slot < n_out ? (int64_t)row_perm[slot] : n_out) : slot;
 #pragma unroll
                 for (int c0 = 0; c0 < N; c0 += 32) {
                     uint32_t v[32];
@@ -541,7 +545,7 @@ int sm_count() {
 
 template <int K, int N, bool OB, int TPS = (N <= 64 ? 4 : 2), int NPW = 4>
 int launch_fwd_t(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-                 cudaStream_t st) {
+                 cudaStream_t st, const int32_t* perm) {
     using C = FwdCfg<K, N, TPS>;
     auto kern = k_conv_fwd_tc<K, N, OB, TPS, NPW>;
     FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -550,37 +554,57 @@ int launch_fwd_t(const void* in, const void* wimg, const int32_t* nbr, int64_t l
     if (grid > supers) grid = supers;
     static const int dbg = getenv("FVDB_DEBUG_FWD") ? atoi(getenv("FVDB_DEBUG_FWD")) : 0;  // profiling switches
     kern<<<grid, fwd_threads(NPW), C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, nbr, ld, n_out, out, supers,
-                                                  dbg);
+                                                  dbg, perm);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
 
 template <int K, int N, bool OB>
 int launch_fwd(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-               cudaStream_t st) {
+               cudaStream_t st, const int32_t* perm) {
     if constexpr (K == 64 && N == 64) {
         static const int npw = getenv("FVDB_FWD_NPW") ? atoi(getenv("FVDB_FWD_NPW")) : 4;  // profiling switch
-        if (npw == 8) return launch_fwd_t<K, N, OB, 4, 8>(in, wimg, nbr, ld, n_out, out, st);
+        if (npw == 8) return launch_fwd_t<K, N, OB, 4, 8>(in, wimg, nbr, ld, n_out, out, st, perm);
     }
-    return launch_fwd_t<K, N, OB>(in, wimg, nbr, ld, n_out, out, st);
+    return launch_fwd_t<K, N, OB>(in, wimg, nbr, ld, n_out, out, st, perm);
 }
 
 template <int K, int N>
 int dispatch_out(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-                 int out_dtype, cudaStream_t st) {
-    if (out_dtype == FVDB_DTYPE_BF16) return launch_fwd<K, N, true>(in, wimg, nbr, ld, n_out, out, st);
-    if (out_dtype == FVDB_DTYPE_F32) return launch_fwd<K, N, false>(in, wimg, nbr, ld, n_out, out, st);
+                 int out_dtype, cudaStream_t st, const int32_t* perm) {
+    if (out_dtype == FVDB_DTYPE_BF16) return launch_fwd<K, N, true>(in, wimg, nbr, ld, n_out, out, st, perm);
+    if (out_dtype == FVDB_DTYPE_F32) return launch_fwd<K, N, false>(in, wimg, nbr, ld, n_out, out, st, perm);
     return FVDB_ERR_INVALID;
 }
 
 template <int K>
 int dispatch_n(int N, const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-               int od, cudaStream_t st) {
+               int od, cudaStream_t st, const int32_t* perm) {
     switch (N) {
-        case 32: return dispatch_out<K, 32>(in, wimg, nbr, ld, n_out, out, od, st);
-        case 64: return dispatch_out<K, 64>(in, wimg, nbr, ld, n_out, out, od, st);
-        case 128: return dispatch_out<K, 128>(in, wimg, nbr, ld, n_out, out, od, st);
+        case 32: return dispatch_out<K, 32>(in, wimg, nbr, ld, n_out, out, od, st, perm);
+        case 64: return dispatch_out<K, 64>(in, wimg, nbr, ld, n_out, out, od, st, perm);
+        case 128: return dispatch_out<K, 128>(in, wimg, nbr, ld, n_out, out, od, st, perm);
         default: return FVDB_ERR_INVALID;
+    }
+}
+
+// 27-bit signature of each output row (bit d = offset d has a pair); padding columns get ~0u
+__global__ void k_signature(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out, uint32_t* __restrict__ key,
+                            int32_t* __restrict__ val) {
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n_out; o += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t sig = 0;
+        for (int d = 0; d < 27; ++d) sig |= (nbr[(int64_t)d * ld + o] >= 0 ? 1u : 0u) << d;
+        key[o] = sig;
+        val[o] = (int32_t)o;
+    }
+}
+// nbrP[d][i] = nbr[d][perm[i]] for i < n_out, -1 in the padding
+__global__ void k_permute_table(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out,
+                                const int32_t* __restrict__ perm, int32_t* __restrict__ nbrP) {
+    const int64_t total = 27 * ld;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = t / ld, i = t - d * ld;
+        nbrP[t] = i < n_out ? nbr[d * ld + perm[i]] : -1;
     }
 }
 
@@ -649,11 +673,63 @@ extern "C" int fvdb_conv_gather_tc(const void* in_bf16, int64_t n_in, int K, con
     if (ld % FVDB_NBR_ALIGN != 0 || ld < n_out) return FVDB_ERR_INVALID;
     cudaStream_t st = as_stream(stream);
     switch (K) {
-        case 32: return dispatch_n<32>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st);
-        case 64: return dispatch_n<64>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st);
-        case 128: return dispatch_n<128>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st);
+        case 32: return dispatch_n<32>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st, nullptr);
+        case 64: return dispatch_n<64>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st, nullptr);
+        case 128: return dispatch_n<128>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st, nullptr);
         default: return FVDB_ERR_INVALID;
     }
+}
+
+extern "C" int fvdb_conv_gather_tc_perm(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
+                                        const int32_t* nbr_perm, int64_t ld, int64_t n_out, const int32_t* row_perm,
+                                        void* out, int out_dtype, void* stream) {
+    (void)n_in;
+    if (n_out == 0) return FVDB_OK;
+    if (ld % FVDB_NBR_ALIGN != 0 || ld < n_out || !row_perm) return FVDB_ERR_INVALID;
+    cudaStream_t st = as_stream(stream);
+    switch (K) {
+        case 32: return dispatch_n<32>(N, in_bf16, w_image, nbr_perm, ld, n_out, out, out_dtype, st, row_perm);
+        case 64: return dispatch_n<64>(N, in_bf16, w_image, nbr_perm, ld, n_out, out, out_dtype, st, row_perm);
+        case 128: return dispatch_n<128>(N, in_bf16, w_image, nbr_perm, ld, n_out, out, out_dtype, st, row_perm);
+        default: return FVDB_ERR_INVALID;
+    }
+}
+
+extern "C" size_t fvdb_kmap_signature_workspace_bytes(int64_t n_out) {
+    const int n = (int)(n_out > 0 ? n_out : 1);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, n);
+    Sizer sz;
+    sz.take<uint32_t>(n);
+    sz.take<uint32_t>(n);
+    sz.take<int32_t>(n);
+    sz.take<uint8_t>(tmp);
+    return sz.used + 256;
+}
+
+extern "C" int fvdb_kmap_signature_order(const int32_t* nbr, int64_t ld, int64_t n_out, int32_t* perm,
+                                         int32_t* nbr_perm, void* workspace, size_t workspace_bytes, void* stream) {
+    if (n_out < 0 || n_out > 0x7fffffffLL || ld < n_out) return FVDB_ERR_INVALID;
+    cudaStream_t st = as_stream(stream);
+    if (n_out > 0) {
+        Carver cv(workspace, workspace_bytes);
+        uint32_t* key = cv.take<uint32_t>(n_out);
+        uint32_t* skey = cv.take<uint32_t>(n_out);
+        int32_t* val = cv.take<int32_t>(n_out);
+        size_t tmp = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, skey, val, perm, (int)n_out);
+        void* tmpp = cv.take<uint8_t>(tmp);
+        if (!cv.ok()) return FVDB_ERR_WORKSPACE;
+        const unsigned g = (unsigned)ceil_div(n_out, 256) < 8192 ? (unsigned)ceil_div(n_out, 256) : 8192;
+        k_signature<<<g, 256, 0, st>>>(nbr, ld, n_out, key, val);
+        FVDB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmpp, tmp, key, skey, val, perm, (int)n_out, 0, 27, st));
+    }
+    const int64_t total = 27 * ld;
+    const unsigned g2 = (unsigned)(ceil_div(total, 256) < 8192 ? ceil_div(total, 256) : 8192);
+    k_permute_table<<<g2, 256, 0, st>>>(nbr, ld, n_out, perm, nbr_perm);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
 }
 
 extern "C" size_t fvdb_wgrad_tc_workspace_bytes(int64_t n_out, int cin, int cout) {

@@ -1,0 +1,39 @@
+"""Host-side profile of the cfg4 step (cProfile, cumulative), to find Python / sync overhead."""
+import cProfile, pathlib, pstats, sys, time
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
+import numpy as np, torch
+import paper_2407_01781_b200 as P
+from paper_2407_01781_b200.workloads import sphere_shell_coords
+
+coords = sphere_shell_coords(470, 1.5)
+pts = torch.from_numpy(coords.astype(np.float64)).cuda()
+tf = P.VoxelTransform.uniform(1.0)
+down = P.SparseConv3d(64, 128, stride=2).cuda()
+up = P.SparseConv3d(128, 64, stride=2, transposed=True).cuda()
+x = torch.randn(coords.shape[0], 64, device="cuda")
+
+
+def step():
+    g, _ = P.build_from_points(pts, tf)
+    fine = P.GridBatch([g])
+    coarse, h = down(fine, fine.jagged(x))
+    _, y = up(coarse, h, out_grid=fine)
+    y.jdata.float().sum().backward()
+
+
+for _ in range(5):
+    step()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(20):
+    step()
+torch.cuda.synchronize()
+print("wall ms/step", (time.perf_counter() - t0) / 20 * 1e3)
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(20):
+    step()
+torch.cuda.synchronize()
+pr.disable()
+st = pstats.Stats(pr)
+st.sort_stats("tottime").print_stats(30)
