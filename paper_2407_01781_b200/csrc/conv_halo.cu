@@ -92,18 +92,37 @@ struct HaloCfg {
     static constexpr uint32_t BLAYOUT = BROWB == 128 ? kSwizzle128B : kSwizzle64B;
     static constexpr int B_BYTES = N * K * 2;               // one offset's weight image
     static constexpr int ACOLS = K / 2;                     // TMEM columns of one A stage
-    // accumulator buffers per half: 2 (epilogue overlaps the next tile) when TMEM allows
-    static constexpr int NACC = (V == 1 || V == 2) ? 1 : (4 * N + 2 * ACOLS <= 512 ? 2 : 1);
-    static constexpr int ACC = 2 * NACC * N;                // accumulator columns (both halves)
-    // NSL slots per half (2: a half's builders fill one slot while its MMA warp drains the other)
+    // V = 0: two half-pipelines (MMA warp h takes the batches ab with ab % 2 == h into accumulator set h,
+    //        NSL slots each; the epilogue sums both sets in a fixed order).
+    // V = 1: one MMA issuer consuming one ring of NSL slots in batch order into one accumulator set.  A
+    //        convergent warp issues TS MMAs at the 32-cycle floor; what costs is the issuer's per-batch
+    //        mbarrier / fence / commit round trips (~150-300 cycles each), amortised over BATCH = 4 stages,
+    //        and one accumulator set leaves TMEM for the deepest A ring (64x64: 12 stages vs 8).
+    static constexpr bool ONE = V == 1;
+    static constexpr int NISS = ONE ? 1 : 2;                // MMA issuers = accumulator sets
+    // accumulator buffers per set: 2 (epilogue overlaps the next tile) when TMEM allows
+    static constexpr int NACC = (ONE || 4 * N + 2 * ACOLS <= 512) ? 2 : 1;
+    static constexpr int ACC = NISS * NACC * N;             // accumulator columns
     static constexpr int fits(int nsl, int b) {
-        return ACC + 2 * nsl * b * ACOLS <= 512 &&
-               (kSmemMax - 2048 - (1024 + 2 * nsl * b * B_BYTES + 2 * kIdxBytes)) / (2 * (ROWB + 4)) >= 256;
+        return ACC + NISS * nsl * b * ACOLS <= 512 &&
+               (kSmemMax - 2048 - (1024 + NISS * nsl * b * B_BYTES + 2 * kIdxBytes)) / (2 * (ROWB + 4)) >= 256;
     }
-    static constexpr int NSL = V == 2 ? 3 : (fits(2, 1) ? 2 : 1);
-    static constexpr int BATCH = V == 1 ? 3 : (V == 2 ? 2 : (fits(NSL, 4) ? 4 : (fits(NSL, 2) ? 2 : 1)));
+    static constexpr int deepest(int b) {
+        int n = 8;
+        while (n > 1 && !fits(n, b)) --n;
+        return n;
+    }
+    static constexpr int B1 = K >= 128 ? 1 : 4;             // V = 1 batch (K = 128: 32 KB weight images)
+    static constexpr int NSL = ONE ? deepest(B1) : (fits(2, 1) ? 2 : 1);
+    static constexpr int BATCH = ONE ? B1 : (fits(NSL, 4) ? 4 : (fits(NSL, 2) ? 2 : 1));
+    static constexpr int SLOTS = NISS * NSL;                // slot ring size (A in TMEM, weights in smem)
     static constexpr int SLOT_B = BATCH * B_BYTES;          // weight bytes of one slot
-    static constexpr int FIXED = 1024 + 2 * NSL * SLOT_B + 2 * kIdxBytes;
+    static constexpr int FIXED = 1024 + SLOTS * SLOT_B + 2 * kIdxBytes;
+    // slot and use count of batch ab
+    __device__ static constexpr uint32_t slot_of(uint32_t ab) {
+        return ONE ? ab % NSL : (ab & 1) * NSL + (ab >> 1) % NSL;
+    }
+    __device__ static constexpr uint32_t use_of(uint32_t ab) { return ONE ? ab / NSL : (ab >> 1) / NSL; }
     static constexpr int CAP = ((kSmemMax - 2048 - FIXED - ROWB) / (2 * (ROWB + 4))) & ~7;
     static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4) + ROWB;  // + one zero row
     static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, N, false, false);
@@ -111,13 +130,13 @@ struct HaloCfg {
     static_assert(27 + BATCH - 1 <= kImgExt, "weight batch wraps past the extended image array");
     // builder warps per (half, lane quarter), building alternate stages of a batch (K=128 builders hold
     // 64 data registers: one per slot keeps them within the register budget)
-    static constexpr int SUBS = (K >= 128 || BATCH < 2 || (K == 32 && V == 3)) ? 1 : 2;
+    static constexpr int SUBS = (K >= 128 || BATCH < 2) ? 1 : 2;
     static constexpr int BUILDERS = 4 * kHalves * SUBS;
     static constexpr int THREADS = (3 + BUILDERS + 4 + 1) * 32;
 };
 
-// warps: 0 halo loader, 1-2 MMA (half 0, 1), 3.. builders (4 quarters x 2 halves x SUBS), 4 epilogue,
-// 1 weight loader
+// warps: 0 halo loader, 1-2 MMA (V 0: half 0, 1; V 1: warp 1 only, warp 2 idles), 3.. builders (4 quarters x
+// 2 halves x SUBS), 4 epilogue, 1 weight loader
 
 // profiling trace (FVDB_DEBUG_HALO & 64): clock64 stamps of CTA 0, kTraceN events per channel
 constexpr int kTraceCh = 12, kTraceN = 2048;
@@ -140,14 +159,15 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
     extern __shared__ uint8_t dsmem[];
     __shared__ __align__(8) uint64_t bar_hfull[2], bar_hempty[2], bar_xfull[2];
     __shared__ __align__(8) uint64_t bar_ifull[2], bar_iempty[2];
-    __shared__ __align__(8) uint64_t bar_afull[2 * NSL], bar_adone[2 * NSL];   // per (half, slot)
-    __shared__ __align__(8) uint64_t bar_bfull[2 * NSL];  // per (half, slot); released via bar_adone
+    constexpr int SLOTS = C::SLOTS;
+    // afull[k]: the slot's A stages (builder arrivals) and weight images (loader arrival + TMA bytes) are in
+    __shared__ __align__(8) uint64_t bar_afull[SLOTS], bar_adone[SLOTS];   // per slot
     __shared__ __align__(8) uint64_t bar_tfull[NACC], bar_tempty[NACC];
     __shared__ uint32_t tmem_slot;
 
     const uint32_t sbase = smem_u32(dsmem);
-    const uint32_t bbase = (sbase + 1023u) & ~1023u;                  // weight slots [2 halves][NSL][SLOT_B]
-    const uint32_t ibase = bbase + 2 * NSL * C::SLOT_B;               // index blocks [2]
+    const uint32_t bbase = (sbase + 1023u) & ~1023u;                  // weight slots [SLOTS][SLOT_B]
+    const uint32_t ibase = bbase + SLOTS * C::SLOT_B;                 // index blocks [2]
     const uint32_t hbase = ibase + 2 * kIdxBytes;                     // halo rows [2][CAP][ROWB]
     const uint32_t xbase = hbase + 2 * C::CAP * C::ROWB;              // halo row ids [2][CAP]
     const uint32_t zrow = xbase + 2 * C::CAP * 4;                     // one zero row (missing neighbours)
@@ -165,13 +185,12 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
             mbar_init(smem_u32(&bar_ifull[b]), 1);
             mbar_init(smem_u32(&bar_iempty[b]), kBuilders);
         }
-        for (int b = 0; b < 2 * NSL; ++b) {
-            mbar_init(smem_u32(&bar_afull[b]), 4 * (kSubs < BATCH ? kSubs : BATCH));
+        for (int b = 0; b < SLOTS; ++b) {
+            mbar_init(smem_u32(&bar_afull[b]), 4 * (kSubs < BATCH ? kSubs : BATCH) + 1);
             mbar_init(smem_u32(&bar_adone[b]), 1);
-            mbar_init(smem_u32(&bar_bfull[b]), 1);
         }
         for (int b = 0; b < NACC; ++b) {
-            mbar_init(smem_u32(&bar_tfull[b]), 2);   // both MMA warps commit
+            mbar_init(smem_u32(&bar_tfull[b]), C::NISS);  // every MMA warp commits
             mbar_init(smem_u32(&bar_tempty[b]), 4);  // four epilogue warps
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -184,10 +203,8 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
     const uint32_t AFULL = smem_u32(bar_afull), ADONE = smem_u32(bar_adone);
-    const uint32_t BFULL = smem_u32(bar_bfull);
-    // TMEM columns: accumulator (half h, buffer b) at (h * NACC + b) * N; A slot (h, sl) at
-    // ACC + (h * NSL + sl) * BATCH * ACOLS.  Batch ab -> half ab & 1, half-local index hb = ab >> 1,
-    // slot hb % NSL, use count hb / NSL.
+    // TMEM columns: accumulator (set h, buffer b) at (h * NACC + b) * N; A slot k at ACC + k * BATCH * ACOLS.
+    // Batch ab -> slot C::slot_of(ab), use count C::use_of(ab); builder half ab & 1.
     if (warp >= W_EPI && warp < W_EPI + 4) {  // zero all accumulators (the MMAs always accumulate)
         const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         for (int c0 = 0; c0 < C::ACC; c0 += 32) tmem_st32_zero(lb + c0);
@@ -259,20 +276,20 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
             level = nlevel;
         }
     } else if (warp == W_BLOAD) {
-        // ---------------- weight loader: batch ab (BATCH consecutive offsets, one TMA) -> slot ab & 1 --------
+        // ---------------- weight loader: batch ab (BATCH consecutive offsets, one TMA) -> slot_of(ab) --------
         if (lane == 0) {
             const uint32_t nb = (nstages + BATCH - 1) / BATCH;
             for (uint32_t ab = 0; ab < nb; ++ab) {
-                const uint32_t hbi = ab >> 1, k = (ab & 1) * NSL + hbi % NSL, use = hbi / NSL;
+                const uint32_t k = C::slot_of(ab), use = C::use_of(ab);
                 mbar_wait_sleep(ADONE + 8 * k, (use & 1) ^ 1, 32);  // slot k's previous batch is done
                 trace(dbg, 6, ab);
-                if ((dbg & 16) && ab >= 2u * NSL) {  // profiling: reuse stale weight slots
-                    mbar_arrive(BFULL + 8 * k);
+                if ((dbg & 16) && ab >= (uint32_t)SLOTS) {  // profiling: reuse stale weight slots
+                    mbar_arrive(AFULL + 8 * k);
                     continue;
                 }
                 const uint32_t d0 = (ab * BATCH) % 27;  // offsets d0 .. d0+BATCH-1 (extended image array)
-                mbar_arrive_expect_tx(BFULL + 8 * k, C::SLOT_B);
-                bulk_g2s(bbase + k * C::SLOT_B, wimg + (size_t)d0 * C::B_BYTES, C::SLOT_B, BFULL + 8 * k);
+                mbar_arrive_expect_tx(AFULL + 8 * k, C::SLOT_B);
+                bulk_g2s(bbase + k * C::SLOT_B, wimg + (size_t)d0 * C::B_BYTES, C::SLOT_B, AFULL + 8 * k);
             }
         }
     } else if (warp >= W_BLD && warp < W_BLD + kBuilders) {
@@ -302,7 +319,7 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
                     const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
                     for (; ac < s1;) {
                         const uint32_t ab = ac / BATCH, within = ac % BATCH;
-                        const uint32_t hbi = ab >> 1, k = half * NSL + hbi % NSL, use = hbi / NSL;
+                        const uint32_t k = C::slot_of(ab), use = C::use_of(ab);
                         if (within == 0) {  // first stage of my batch: wait until my MMA warp released the slot
                             mbar_wait(ADONE + 8 * k, (use & 1) ^ 1);
                             if (lane == 0 && q == 0 && sub == 0) trace(dbg, 2, ab);
@@ -351,7 +368,7 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
                                 if (q == 0 && sub == 0) trace(dbg, 3, ab);
                                 mbar_arrive(AFULL + 8 * k);
                             }
-                            ac += BATCH;
+                            ac += BATCH;  // skip the other half's batch
                         }
                     }
                 }
@@ -362,7 +379,59 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
                 }
             }
         }
-    } else if (warp == W_MMA || warp == W_MMA + 1) {
+    } else if (C::ONE && warp == W_MMA) {
+        // ---------------- single MMA issuer: every batch in order, one accumulator set ----------------
+        // Everything here derives from kernel parameters, blockIdx and constants (the TMEM base is 0: the
+        // CTA is alone on its SM and owns all 512 columns), so the compiler keeps the loop state and MMA
+        // operands in uniform registers instead of re-broadcasting them before every MMA.
+        if (tmem != 0u) asm volatile("trap;");
+        const uint32_t TFULL = smem_u32(bar_tfull), TEMPTY = smem_u32(bar_tempty);
+        const uint64_t bdesc0 = smem_desc(bbase, 16, 8 * C::BROWB, C::BLAYOUT);
+        const uint32_t nb = (nstages + BATCH - 1) / BATCH;
+        uint32_t k = 0, upar = 0, tile_next = 0, cur = 0xffffffffu, ac0 = 0;
+        uint32_t acc = 1;  // 0 for the first K-stage of a tile: the MMA overwrites the accumulator
+        bool ready = false;
+        for (uint32_t ab = 0; ab < nb; ++ab, ac0 += BATCH) {
+            if (lane == 0) trace(dbg, 0, ab);
+            if (!ready) mbar_wait(AFULL + 8 * k, upar);
+            if (lane == 0) trace(dbg, 1, ab);
+            tc_fence_after();
+            const uint32_t kn = k + 1 == (uint32_t)NSL ? 0u : k + 1;
+            const uint32_t pn = k + 1 == (uint32_t)NSL ? upar ^ 1u : upar;
+            ready = mbar_test(AFULL + 8 * kn, pn);
+#pragma unroll
+            for (int w = 0; w < BATCH; ++w) {
+                const uint32_t ac = ac0 + w;
+                if (ac >= nstages) break;
+                if (ac >= tile_next) {
+                    if (cur != 0xffffffffu) mma_commit_elect(TFULL + 8 * (cur % NACC));
+                    ++cur;
+                    tile_next += 27;
+                    acc = 0;
+                    mbar_wait(TEMPTY + 8 * (cur % NACC), ((cur / NACC) & 1) ^ 1);
+                    tc_fence_after();
+                }
+                if (!(dbg & 1)) {
+                    const uint32_t dt = (cur % NACC) * N;
+                    const uint32_t at = C::ACC + (k * BATCH + w) * C::ACOLS;
+                    const uint64_t bd = bdesc0 + ((k * C::SLOT_B + w * C::B_BYTES) >> 4);
+                    if constexpr (K == 32) {
+                        mma_ts_x2_elect_acc<8, 2>(dt, at, bd, C::IDESC, acc);
+                    } else {
+                        mma_ts_x4_elect_acc<8, 16, 24, 2, 4, 6>(dt, at, bd, C::IDESC, acc);
+                        if constexpr (K == 128)
+                            mma_ts_x4_elect<8, 16, 24, 2, 4, 6>(dt, at + 32, bd + ((N * C::BROWB) >> 4), C::IDESC);
+                    }
+                }
+                acc = 1;
+            }
+            mma_commit_elect(ADONE + 8 * k);
+            k = kn;
+            upar = pn;
+        }
+        if (cur != 0xffffffffu) mma_commit_elect(TFULL + 8 * (cur % NACC));
+        __syncwarp();
+    } else if (!C::ONE && (warp == W_MMA || warp == W_MMA + 1)) {
         // ---------------- MMA issuers (one per half): A from TMEM, B from smem, D in TMEM ----------------
         // Iterates only this half's batches; barrier addresses and descriptors are loop-invariant bases
         // plus offsets (the issuing warp's instruction stream is the critical path at N <= 128).
@@ -370,36 +439,52 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
         const uint32_t TFULL = smem_u32(bar_tfull), TEMPTY = smem_u32(bar_tempty);
         const uint64_t bdesc0 = smem_desc(bbase, 16, 8 * C::BROWB, C::BLAYOUT);  // + (byte offset >> 4)
         const uint32_t nb = (nstages + BATCH - 1) / BATCH;
+        const uint32_t kbase = C::ONE ? 0u : (uint32_t)half * NSL;
+        // running counters instead of divisions: ring position j / use parity, tile index / next boundary
+        uint32_t j = 0, upar = 0, tile_next = 0;
         int cur = -1;  // local tile whose accumulator this warp is filling
-        for (uint32_t ab = half; ab < nb; ab += 2) {
-            const uint32_t hbi = ab >> 1, k = half * NSL + hbi % NSL, use = hbi / NSL;
-            mbar_wait(BFULL + 8 * k, use & 1);
-            mbar_wait(AFULL + 8 * k, use & 1);
+        bool ready = false;  // the current batch's afull phase was already seen complete (prefetched test)
+        for (uint32_t ab = half; ab < nb; ab += C::NISS) {
+            const uint32_t k = kbase + j;
+            if (lane == 0) trace(dbg, 0, ab);
+            if (!ready) mbar_wait(AFULL + 8 * k, upar);
+            if (lane == 0) trace(dbg, 1, ab);
             tc_fence_after();
+            {  // probe the next batch's slot now; the result is consumed one iteration later
+                const uint32_t jn = j + 1 == (uint32_t)NSL ? 0u : j + 1;
+                const uint32_t pn = j + 1 == (uint32_t)NSL ? upar ^ 1u : upar;
+                ready = mbar_test(AFULL + 8 * (kbase + jn), pn);
+            }
+            const uint32_t ac0 = ab * BATCH;
 #pragma unroll
             for (int w = 0; w < BATCH; ++w) {
-                const uint32_t ac = ab * BATCH + w;
+                const uint32_t ac = ac0 + w;
                 if (ac >= nstages) break;
-                const int lt = (int)(ac / 27u);
-                if (lt != cur) {  // tile boundary: publish the finished tile, claim the next accumulator
+                if (ac >= tile_next) {  // tile boundary (a half skips < 27 stages, never a whole tile)
                     if (cur >= 0) mma_commit_elect(TFULL + 8 * (cur % NACC));
-                    mbar_wait(TEMPTY + 8 * (lt % NACC), ((lt / NACC) & 1) ^ 1);
+                    ++cur;
+                    tile_next += 27;
+                    mbar_wait(TEMPTY + 8 * (cur % NACC), ((cur / NACC) & 1) ^ 1);
                     tc_fence_after();
-                    cur = lt;
                 }
                 if (!(dbg & 1)) {  // the whole warp runs this (uniform operands); one elected lane issues
-                    const uint32_t dt = tmem + (half * NACC + lt % NACC) * N;
+                    const uint32_t dt = tmem + (half * NACC + cur % NACC) * N;
                     const uint32_t at = tmem + C::ACC + (k * BATCH + w) * C::ACOLS;
-                    const uint32_t boff = k * C::SLOT_B + w * C::B_BYTES;
-#pragma unroll
-                    for (int ks = 0; ks < K / 16; ++ks) {
-                        const int kb = ks / (C::KB / 16), kk = ks % (C::KB / 16);
-                        mma_bf16_ts_elect(dt, at + ks * 8, bdesc0 + ((boff + kb * N * C::BROWB + kk * 32) >> 4),
-                                          C::IDESC, 1u);
+                    const uint64_t bd = bdesc0 + ((k * C::SLOT_B + w * C::B_BYTES) >> 4);
+                    if constexpr (K == 32) {
+                        mma_ts_x2_elect<8, 2>(dt, at, bd, C::IDESC);
+                    } else {
+                        mma_ts_x4_elect<8, 16, 24, 2, 4, 6>(dt, at, bd, C::IDESC);
+                        if constexpr (K == 128)  // second 64-wide K block of the image
+                            mma_ts_x4_elect<8, 16, 24, 2, 4, 6>(dt, at + 32, bd + ((N * C::BROWB) >> 4), C::IDESC);
                     }
                 }
             }
             mma_commit_elect(ADONE + 8 * k);  // frees A slot k and weight slot k
+            if (++j == (uint32_t)NSL) {
+                j = 0;
+                upar ^= 1u;
+            }
         }
         if (cur >= 0) mma_commit_elect(TFULL + 8 * (cur % NACC));
         __syncwarp();
@@ -415,16 +500,22 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
             tc_fence_after();
 #pragma unroll
             for (int c0 = 0; c0 < N; c0 += 32) {
-                uint32_t v[32], w[32];
+                uint32_t v[32];
                 const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + accb * N + c0;
-                const uint32_t tb = ta + NACC * N;  // half 1's accumulator
-                tmem_ld32(ta, v);
-                tmem_ld32(tb, w);
-                tmem_ld_wait();
-                tmem_st32_zero(ta);
-                tmem_st32_zero(tb);
+                if constexpr (C::ONE) {  // no zeroing: the next tile's first MMA overwrites the accumulator
+                    tmem_ld32(ta, v);
+                    tmem_ld_wait();
+                } else {
+                    uint32_t w[32];
+                    const uint32_t tb = ta + NACC * N;  // half 1's accumulator
+                    tmem_ld32(ta, v);
+                    tmem_ld32(tb, w);
+                    tmem_ld_wait();
+                    tmem_st32_zero(ta);
+                    tmem_st32_zero(tb);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+                }
                 if (row >= 0 && !(dbg & 4)) {
                     if constexpr (OUT_BF16) {
                         uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(out) + row * N + c0);
@@ -715,9 +806,21 @@ int sm_count_h() {
     return v;
 }
 
-int halo_variant() {
-    static const int v = getenv("FVDB_HALO_VARIANT") ? atoi(getenv("FVDB_HALO_VARIANT")) : 0;  // profiling
+// MMA-issue layout per (K, N) (HaloCfg V), from B200 measurements (tools/halo_bench.py, fwd ms V0 -> V1):
+// K >= 64 one issuer (cfg2 64x64 0.366 -> 0.358, dense 64x64 0.696 -> 0.660, cfg2 128x128 0.899 -> 0.873;
+// cfg2 training step 1.084 -> 1.060), K = 32 two half-pipelines (cfg5 4.07 vs 4.23, dense32 0.870 vs
+// 0.902: at 16 A columns per stage the second issuer hides more than the deeper ring gains).
+// FVDB_HALO_VARIANT=0/1 overrides (profiling).
+template <int K, int N>
+constexpr int kHaloDefaultV = K >= 64 ? 1 : 0;
+int halo_variant_env() {
+    static const int v = getenv("FVDB_HALO_VARIANT") ? atoi(getenv("FVDB_HALO_VARIANT")) : -1;
     return v;
+}
+template <int K, int N>
+int halo_variant() {
+    const int e = halo_variant_env();
+    return e == 0 || e == 1 ? e : kHaloDefaultV<K, N>;
 }
 
 template <int K, int N, bool OB, int V = 0>
@@ -738,13 +841,7 @@ int launch_halo_v(const void* in, const void* wimg, const fvdb_halo_plan& P, int
 
 template <int K, int N, bool OB>
 int launch_halo(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out, cudaStream_t st) {
-    if constexpr (K == 64 && N == 64) {
-        if (halo_variant() == 1) return launch_halo_v<K, N, OB, 1>(in, wimg, P, n_out, out, st);
-        if (halo_variant() == 2) return launch_halo_v<K, N, OB, 2>(in, wimg, P, n_out, out, st);
-    }
-    if constexpr (K == 32 && N == 32) {
-        if (halo_variant() == 3) return launch_halo_v<K, N, OB, 3>(in, wimg, P, n_out, out, st);
-    }
+    if (halo_variant<K, N>() == 1) return launch_halo_v<K, N, OB, 1>(in, wimg, P, n_out, out, st);
     return launch_halo_v<K, N, OB, 0>(in, wimg, P, n_out, out, st);
 }
 
@@ -775,11 +872,7 @@ extern "C" int fvdb_halo_cap(int K, int N) {
     int cap = 0;
     halo_dispatch(K, N, [&](auto k, auto n) {
         constexpr int KK = decltype(k)::value, NN = decltype(n)::value;
-        cap = HaloCfg<KK, NN>::CAP;
-        if constexpr (KK == 64 && NN == 64) {
-            if (halo_variant() == 1) cap = HaloCfg<KK, NN, 1>::CAP;
-            if (halo_variant() == 2) cap = HaloCfg<KK, NN, 2>::CAP;
-        }
+        cap = halo_variant<KK, NN>() == 1 ? HaloCfg<KK, NN, 1>::CAP : HaloCfg<KK, NN, 0>::CAP;
         return 0;
     });
     return cap;

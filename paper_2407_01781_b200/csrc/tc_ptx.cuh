@@ -47,6 +47,19 @@ __device__ __forceinline__ bool mbar_try_wait_sus(uint32_t bar, uint32_t parity)
         : "memory");
     return ok != 0;
 }
+// non-blocking probe of a phase (mbarrier.test_wait): issue it early, consume the result later, so the
+// ~300-cycle mbarrier round trip overlaps other work (a wait on an already-completed phase still costs it)
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 // bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t n = 0;
@@ -172,6 +185,65 @@ __device__ __forceinline__ void mma_bf16_elect(uint32_t d_tmem, uint64_t adesc, 
         "elect.sync _|e, 0xffffffff;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// One K-stage of TS MMAs from a convergent warp: a single elect.sync, then 2 or 4 MMAs whose A columns
+// and B descriptors advance by immediates (A + AI, B + BI), all accumulating into D.  One elect per stage
+// instead of one per MMA keeps the issuing warp's instruction stream short (the issue loop, not the
+// tensor pipe, bounds small-N kernels: a whole-warp issue reaches the 32-cycle M128/N64 hardware floor).
+template <int A1, int A2, int A3, int B1, int B2, int B3>
+__device__ __forceinline__ void mma_ts_x4_elect(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+        "setp.ne.b32 p, 1, 0;\n\t"
+        "add.u32 a1, %1, %4;\n\tadd.u32 a2, %1, %5;\n\tadd.u32 a3, %1, %6;\n\t"
+        "add.u64 b1, %2, %7;\n\tadd.u64 b2, %2, %8;\n\tadd.u64 b3, %2, %9;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, p;\n\t}"
+        ::"r"(d), "r"(a), "l"(b), "r"(idesc), "n"(A1), "n"(A2), "n"(A3), "n"(B1), "n"(B2), "n"(B3)
+        : "memory");
+}
+// same, the first MMA overwriting D when acc0 == 0 (first K-stage of a tile: no accumulator zeroing)
+template <int A1, int A2, int A3, int B1, int B2, int B3>
+__device__ __forceinline__ void mma_ts_x4_elect_acc(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, q;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+        "setp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t"
+        "add.u32 a1, %1, %4;\n\tadd.u32 a2, %1, %5;\n\tadd.u32 a3, %1, %6;\n\t"
+        "add.u64 b1, %2, %7;\n\tadd.u64 b2, %2, %8;\n\tadd.u64 b3, %2, %9;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, p;\n\t}"
+        ::"r"(d), "r"(a), "l"(b), "r"(idesc), "n"(A1), "n"(A2), "n"(A3), "n"(B1), "n"(B2), "n"(B3), "r"(acc0)
+        : "memory");
+}
+template <int A1, int B1>
+__device__ __forceinline__ void mma_ts_x2_elect_acc(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, q;\n\t.reg .b32 a1;\n\t.reg .b64 b1;\n\t"
+        "setp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %6, 0;\n\t"
+        "add.u32 a1, %1, %4;\n\tadd.u64 b1, %2, %5;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, p;\n\t}"
+        ::"r"(d), "r"(a), "l"(b), "r"(idesc), "n"(A1), "n"(B1), "r"(acc0)
+        : "memory");
+}
+template <int A1, int B1>
+__device__ __forceinline__ void mma_ts_x2_elect(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t.reg .b32 a1;\n\t.reg .b64 b1;\n\t"
+        "setp.ne.b32 p, 1, 0;\n\t"
+        "add.u32 a1, %1, %4;\n\tadd.u64 b1, %2, %5;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, p;\n\t}"
+        ::"r"(d), "r"(a), "l"(b), "r"(idesc), "n"(A1), "n"(B1)
         : "memory");
 }
 __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
