@@ -571,6 +571,8 @@ constexpr uint64_t kNoKey = ~0ull;
 
 
 struct PlanCounts {
+    uint32_t rmax;      // largest input row of the tile's pairs
+    int rb;             // key = (phase << rb) | row: rb = bits(rmax) + 1 (a spare bit keeps kNoKey last)
     int cnt[2][27];     // unique rows per (color, phase)
     int gfirst[2][27];  // exclusive unique-count prefix at each phase's first element
     int goff[27];       // phase slot offsets (multiples of 8)
@@ -580,30 +582,42 @@ struct PlanCounts {
 
 // Sort + dedupe the tile's (phase, row) keys for `level` phases.  Fills S.keys (sorted),
 // S.slot (slot of each unique key inside its phase), and the PlanCounts.  Block-wide.
+// The radix sort runs over the significant bits only (rb + 5 with phases, rb without): ~6-7 passes of
+// 4 bits for a 1M-row map instead of 16 over the full 64-bit key.
 __device__ void plan_tile(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out,
                           const uint8_t* __restrict__ color, int tile, int level, PlanSmem& S, PlanCounts& pc) {
     const int tid = threadIdx.x;
     const int gsz = 27 / level;
-    uint64_t key[kPlanItems];
+    int32_t row[kPlanItems];
+    uint32_t rmax = 0;
 #pragma unroll
     for (int k = 0; k < kPlanItems; ++k) {
         const int e = tid * kPlanItems + k;
-        key[k] = kNoKey;
+        row[k] = -1;
         if (e < 27 * kTileRows) {
             const int d = e / kTileRows, i = e % kTileRows;
             const int64_t o = (int64_t)tile * kTileRows + i;
-            if (o < n_out) {
-                const int32_t r = nbr[(int64_t)d * ld + o];
-                if (r >= 0) key[k] = ((uint64_t)(d / gsz) << 32) | (uint32_t)r;
-            }
+            if (o < n_out) row[k] = nbr[(int64_t)d * ld + o];
         }
+        if (row[k] > (int32_t)rmax) rmax = (uint32_t)row[k];
     }
+    if (tid == 0) pc.rmax = 0;
     if (tid < 27) {
         pc.cnt[0][tid] = pc.cnt[1][tid] = 0;
         pc.gfirst[0][tid] = pc.gfirst[1][tid] = 0;
     }
     __syncthreads();
-    PlanSort(S.tmp.sort).Sort(key);
+    atomicMax(&pc.rmax, rmax);
+    __syncthreads();
+    const int rb = 33 - __clz((int)pc.rmax | 1);  // bits(rmax) + 1
+    uint64_t key[kPlanItems];
+#pragma unroll
+    for (int k = 0; k < kPlanItems; ++k) {
+        const int d = (tid * kPlanItems + k) / kTileRows;
+        key[k] = row[k] >= 0 ? ((uint64_t)(d / gsz) << rb) | (uint32_t)row[k] : kNoKey;
+    }
+    if (tid == 0) pc.rb = rb;
+    PlanSort(S.tmp.sort).Sort(key, 0, rb + (level > 1 ? 5 : 0));
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kPlanItems; ++k) S.keys[tid * kPlanItems + k] = key[k];
@@ -615,10 +629,10 @@ __device__ void plan_tile(const int32_t* __restrict__ nbr, int64_t ld, int64_t n
         const int e = tid * kPlanItems + k;
         uc[k] = 0;
         if (key[k] != kNoKey && (e == 0 || S.keys[e - 1] != key[k])) {
-            const int c = color ? (color[(uint32_t)key[k]] & 1) : 0;
+            const int c = color ? (color[(uint32_t)(key[k] & ((1ull << rb) - 1))] & 1) : 0;
             uc[k] = (uint8_t)(1 + c);
             packed += c ? (1u << 16) : 1u;
-            atomicAdd(&pc.cnt[c][(int)(key[k] >> 32)], 1);
+            atomicAdd(&pc.cnt[c][(int)(key[k] >> rb)], 1);
         }
     }
     uint32_t excl;
@@ -628,8 +642,8 @@ __device__ void plan_tile(const int32_t* __restrict__ nbr, int64_t ld, int64_t n
     for (int k = 0; k < kPlanItems; ++k) {
         const int e = tid * kPlanItems + k;
         if (uc[k]) {
-            const int gr = (int)(key[k] >> 32);
-            if (e == 0 || (int)(S.keys[e - 1] >> 32) != gr) {  // first element of its phase
+            const int gr = (int)(key[k] >> rb);
+            if (e == 0 || (int)(S.keys[e - 1] >> rb) != gr) {  // first element of its phase
                 pc.gfirst[0][gr] = (int)(run & 0xFFFF);
                 pc.gfirst[1][gr] = (int)(run >> 16);
             }
@@ -643,7 +657,7 @@ __device__ void plan_tile(const int32_t* __restrict__ nbr, int64_t ld, int64_t n
         const int e = tid * kPlanItems + k;
         uint16_t sl = kNoSlot;
         if (uc[k]) {
-            const int gr = (int)(key[k] >> 32), c = uc[k] - 1;
+            const int gr = (int)(key[k] >> rb), c = uc[k] - 1;
             const int rank = (c ? (int)(run >> 16) : (int)(run & 0xFFFF)) - pc.gfirst[c][gr];
             sl = (uint16_t)(2 * rank + c);
             run += c ? (1u << 16) : 1u;
@@ -714,7 +728,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_fill(const int32_t* __res
         const uint16_t sl = S.slot[e];
         if (sl != kNoSlot) {
             const uint64_t k = S.keys[e];
-            P.halo_rows[base + pc.goff[(int)(k >> 32)] + sl] = (int32_t)(uint32_t)k;
+            P.halo_rows[base + pc.goff[(int)(k >> pc.rb)] + sl] = (int32_t)(k & ((1ull << pc.rb) - 1));
         }
     }
     // lane permutation: pair parity-0 rows with parity-1 rows (lanes 2p, 2p+1), leftovers after
@@ -757,7 +771,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_fill(const int32_t* __res
         const int32_t r = oo >= 0 ? nbr[(int64_t)d * ld + oo] : -1;
         uint16_t sl = kNoSlot;
         if (r >= 0) {
-            const uint64_t key = ((uint64_t)(d / gsz) << 32) | (uint32_t)r;
+            const uint64_t key = ((uint64_t)(d / gsz) << pc.rb) | (uint32_t)r;
             int lo = 0, hi = kPlanKeys;  // first key >= key (the unique element)
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
