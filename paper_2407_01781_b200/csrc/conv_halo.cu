@@ -558,14 +558,17 @@ constexpr int kPlanThreads = 256;
 constexpr int kPlanItems = 14;  // 256 × 14 = 3584 >= 27 × 128
 constexpr int kPlanKeys = kPlanThreads * kPlanItems;
 using PlanSort = cub::BlockRadixSort<uint64_t, kPlanThreads, kPlanItems>;
+using PlanSortV = cub::BlockRadixSort<uint64_t, kPlanThreads, kPlanItems, uint16_t>;  // + original index
 using PlanScan = cub::BlockScan<uint32_t, kPlanThreads>;
 struct PlanSmem {
     union {
         typename PlanSort::TempStorage sort;
+        typename PlanSortV::TempStorage sortv;
         typename PlanScan::TempStorage scan;
     } tmp;
     uint64_t keys[kPlanKeys];
     uint16_t slot[kPlanKeys];
+    uint16_t slot_e[kPlanKeys];  // fill pass: slot of element e = d * 128 + row (kNoSlot: no pair)
 };
 constexpr uint64_t kNoKey = ~0ull;
 
@@ -584,6 +587,9 @@ struct PlanCounts {
 // S.slot (slot of each unique key inside its phase), and the PlanCounts.  Block-wide.
 // The radix sort runs over the significant bits only (rb + 5 with phases, rb without): ~6-7 passes of
 // 4 bits for a 1M-row map instead of 16 over the full 64-bit key.
+// WITH_E (fill pass): the sort carries each key's element index, and S.slot_e gets every element's slot
+// (duplicates take their run's representative), so the tile record is a table lookup, not a search.
+template <bool WITH_E>
 __device__ void plan_tile(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out,
                           const uint8_t* __restrict__ color, int tile, int level, PlanSmem& S, PlanCounts& pc) {
     const int tid = threadIdx.x;
@@ -617,7 +623,14 @@ __device__ void plan_tile(const int32_t* __restrict__ nbr, int64_t ld, int64_t n
         key[k] = row[k] >= 0 ? ((uint64_t)(d / gsz) << rb) | (uint32_t)row[k] : kNoKey;
     }
     if (tid == 0) pc.rb = rb;
-    PlanSort(S.tmp.sort).Sort(key, 0, rb + (level > 1 ? 5 : 0));
+    uint16_t eidx[kPlanItems];
+    if constexpr (WITH_E) {
+#pragma unroll
+        for (int k = 0; k < kPlanItems; ++k) eidx[k] = (uint16_t)(tid * kPlanItems + k);
+        PlanSortV(S.tmp.sortv).Sort(key, eidx, 0, rb + (level > 1 ? 5 : 0));
+    } else {
+        PlanSort(S.tmp.sort).Sort(key, 0, rb + (level > 1 ? 5 : 0));
+    }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kPlanItems; ++k) S.keys[tid * kPlanItems + k] = key[k];
@@ -675,6 +688,20 @@ __device__ void plan_tile(const int32_t* __restrict__ nbr, int64_t ld, int64_t n
         pc.total = acc;
     }
     __syncthreads();
+    if constexpr (WITH_E) {
+        // run representative of each sorted position: inclusive max-scan of run-start positions
+        uint32_t start[kPlanItems];
+#pragma unroll
+        for (int k = 0; k < kPlanItems; ++k) {
+            const int e = tid * kPlanItems + k;
+            start[k] = (e == 0 || S.keys[e - 1] != key[k]) ? (uint32_t)e : 0u;
+        }
+        PlanScan(S.tmp.scan).InclusiveScan(start, start, cub::Max());
+#pragma unroll
+        for (int k = 0; k < kPlanItems; ++k)
+            S.slot_e[eidx[k]] = key[k] != kNoKey ? S.slot[start[k]] : kNoSlot;
+        __syncthreads();
+    }
 }
 
 __device__ __forceinline__ bool plan_fits(const PlanCounts& pc, int level, int cap) {
@@ -693,7 +720,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_count(const int32_t* __re
     const int tile = blockIdx.x;
     int level = 1;
     for (;; level *= 3) {
-        plan_tile(nbr, ld, n_out, color, tile, level, S, pc);
+        plan_tile<false>(nbr, ld, n_out, color, tile, level, S, pc);
         if (level == 27 || plan_fits(pc, level, P.halo_cap)) break;
         __syncthreads();
     }
@@ -718,9 +745,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_fill(const int32_t* __res
     __shared__ int perm[kTileRows];
     __shared__ int wcnt[2][4];
     const int tile = blockIdx.x, tid = threadIdx.x;
-    const int level = P.tile_level[tile], gsz = 27 / level;
+    const int level = P.tile_level[tile];
     const int base = P.tile_base[tile];
-    plan_tile(nbr, ld, n_out, color, tile, level, S, pc);
+    plan_tile<true>(nbr, ld, n_out, color, tile, level, S, pc);
     // halo rows: padding slots -1, then every unique key at its slot
     for (int s = tid; s < pc.total; s += kPlanThreads) P.halo_rows[base + s] = -1;
     __syncthreads();
@@ -768,17 +795,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_fill(const int32_t* __res
     for (int e = tid; e < 27 * kTileRows; e += kPlanThreads) {
         const int d = e / kTileRows, l = e % kTileRows;
         const int oo = perm[l];
-        const int32_t r = oo >= 0 ? nbr[(int64_t)d * ld + oo] : -1;
-        uint16_t sl = kNoSlot;
-        if (r >= 0) {
-            const uint64_t key = ((uint64_t)(d / gsz) << pc.rb) | (uint32_t)r;
-            int lo = 0, hi = kPlanKeys;  // first key >= key (the unique element)
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (S.keys[mid] < key) lo = mid + 1; else hi = mid;
-            }
-            sl = S.slot[lo];
-        }
+        const uint16_t sl = oo >= 0 ? S.slot_e[d * kTileRows + (oo - tile * kTileRows)] : kNoSlot;
         reinterpret_cast<uint16_t*>(rec)[d * kTileRows + l] = sl;
         const uint32_t none = __ballot_sync(0xffffffffu, sl == kNoSlot);
         if ((tid & 31) == 0) reinterpret_cast<uint32_t*>(rec + 6912)[d * 4 + (l >> 5)] = none;
