@@ -81,6 +81,10 @@ int fvdb_device_sm_count(int device);
 int fvdb_quantize_points(const double* points, int64_t n, const double* voxel_size3,
                          const double* origin3, int64_t* coords_out, int64_t* detail,
                          void* stream);
+/* Same without the synchronisation: coords_out holds 3n+1 int64, the last one the first non-finite row
+ * (all ones if none), for fvdb_build_plan2 to report with its first read-back. */
+int fvdb_quantize_points_async(const double* points, int64_t n, const double* voxel_size3,
+                               const double* origin3, int64_t* coords_out, void* stream);
 
 /* ---- a2-a4: build_from_coords (build.py:82-198), two-phase count -> fill ----
  * plan: validates ±2^30, sorts tile keys, ranks, sorts/dedupes voxel keys and counts
@@ -89,6 +93,10 @@ int fvdb_quantize_points(const double* points, int64_t n, const double* voxel_si
 size_t fvdb_build_workspace_bytes(int64_t n_coords);
 int fvdb_build_plan(const int64_t* coords, int64_t n, void* workspace, size_t workspace_bytes,
                     int64_t* counts, int64_t* detail, void* stream);
+/* plan with an optional pending non-finite slot (device, from fvdb_quantize_points_async), reported as
+ * FVDB_ERR_NONFINITE (detail = row) before the range check; two host read-backs in total. */
+int fvdb_build_plan2(const int64_t* coords, int64_t n, const int64_t* pending_nonfinite, void* workspace,
+                     size_t workspace_bytes, int64_t* counts, int64_t* detail, void* stream);
 int fvdb_build_fill(void* workspace, size_t workspace_bytes, int64_t n, const int64_t* counts,
                     const fvdb_grid_arrays* out, void* stream);
 /* a6: coarsen input — floor_divide(coords, factor) (build.py:325-339) */

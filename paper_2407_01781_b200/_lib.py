@@ -59,6 +59,8 @@ SIGNATURES = {
     "fvdb_quantize_points": (_i32, [_vp, _i64, _vp, _vp, _vp, C.POINTER(_i64), _vp]),
     "fvdb_build_workspace_bytes": (_sz, [_i64]),
     "fvdb_build_plan": (_i32, [_vp, _i64, _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "fvdb_build_plan2": (_i32, [_vp, _i64, _vp, _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "fvdb_quantize_points_async": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp]),
     "fvdb_build_fill": (_i32, [_vp, _sz, _i64, C.POINTER(_i64), C.POINTER(GridArrays), _vp]),
     "fvdb_floor_div_coords": (_i32, [_vp, _i64, _i64, _vp, _vp]),
     "fvdb_coord_to_index": (_i32, [C.POINTER(GridView), _vp, _i64, _vp, _vp]),

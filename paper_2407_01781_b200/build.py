@@ -47,8 +47,12 @@ def _alloc_arrays(counts, device):
     return {f: torch.empty(shapes[f], dtype=_TORCH_DTYPES[f], device=device) for f in ARRAY_FIELDS}
 
 
-def _build_device(c: torch.Tensor, transform, name, stats: BuildStats):
-    """Sort/RLE build of an int64 [N,3] CUDA coordinate tensor (N > 0)."""
+def _build_device(c: torch.Tensor, transform, name, stats: BuildStats, pending=None, points=None):
+    """Sort/RLE build of an int64 [N,3] CUDA coordinate tensor (N > 0).
+
+    ``pending``: the offending-row slot of an unsynchronised quantize (``points`` for its message); the
+    plan reports it with its first read-back, before the range check, as quantize_points would.
+    """
     L = _lib.lib()
     dev = c.device
     n = c.shape[0]
@@ -58,7 +62,10 @@ def _build_device(c: torch.Tensor, transform, name, stats: BuildStats):
     ws = _lib.workspace(ws_bytes, dev)
     counts = (C.c_int64 * 4)()
     detail = C.c_int64(0)
-    rc = L.fvdb_build_plan(c.data_ptr(), n, ws.data_ptr(), ws_bytes, counts, C.byref(detail), st)
+    rc = L.fvdb_build_plan2(c.data_ptr(), n, _lib.ptr(pending), ws.data_ptr(), ws_bytes, counts, C.byref(detail), st)
+    if rc == _lib.FVDB_ERR_NONFINITE:
+        row = int(detail.value)
+        raise ValueError(f"non-finite point at row {row}: {points[row].tolist()}")
     if rc == _lib.FVDB_ERR_COORD_RANGE:
         row = int(detail.value)
         raise ValueError(f"coordinate out of range at row {row}: {tuple(c[row].tolist())} "
@@ -115,13 +122,33 @@ def quantize_points(points, transform):
     return out[:3 * n].reshape(n, 3)
 
 
+def _points_f64(points):
+    dev = _device()
+    if isinstance(points, torch.Tensor):
+        p = points.to(device=dev, dtype=torch.float64)
+    else:
+        p = torch.from_numpy(np.ascontiguousarray(np.asarray(points, np.float64))).to(dev)
+    return p.reshape(-1, 3).contiguous()
+
+
 def build_from_points(points, transform, name=""):
-    """Quantize world points to voxel centres and build (build.py:219-230)."""
-    c = quantize_points(points, transform)
-    stats = BuildStats(input_count=int(c.shape[0]))
-    if c.shape[0] == 0:
+    """Quantize world points to voxel centres and build (build.py:219-230).
+
+    The finite check is not synchronised on its own: the build's first read-back reports it (same
+    error, same precedence as quantize_points followed by build_from_coords).
+    """
+    p = _points_f64(points)
+    n = p.shape[0]
+    stats = BuildStats(input_count=int(n))
+    if n == 0:
         return empty_grid(transform, name), stats
-    return _build_device(c, transform, name, stats), stats
+    out = torch.empty(3 * n + 1, dtype=torch.int64, device=p.device)  # +1: offending-row slot
+    vs = (C.c_double * 3)(*transform.voxel_size.tolist())
+    og = (C.c_double * 3)(*transform.origin.tolist())
+    _lib.check(_lib.lib().fvdb_quantize_points_async(p.data_ptr(), n, vs, og, out.data_ptr(), _lib.stream_ptr()),
+               "quantize_points")
+    c = out[:3 * n].reshape(n, 3)
+    return _build_device(c, transform, name, stats, pending=out[3 * n:], points=p), stats
 
 
 def coarsen(grid, factor):

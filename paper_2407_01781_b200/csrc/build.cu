@@ -132,9 +132,16 @@ __global__ void k_voxel_keys(const int64_t* __restrict__ coords, int64_t n,
 }
 
 // node head flags over the sorted unique voxel keys (build.py:150-152)
-__global__ void k_node_heads(const uint64_t* __restrict__ uvox, int n, int* __restrict__ leaf_h,
-                             int* __restrict__ lower_h, int* __restrict__ upper_h) {
+// head flags over n slots; slots at or past the device-side unique count *n_u are 0, so inclusive scans
+// over all n slots end at the node counts without the host knowing the unique count
+__global__ void k_node_heads(const uint64_t* __restrict__ uvox, int n, const int* __restrict__ n_u,
+                             int* __restrict__ leaf_h, int* __restrict__ lower_h, int* __restrict__ upper_h) {
+    const int nu = *n_u;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (i >= nu) {
+            leaf_h[i] = lower_h[i] = upper_h[i] = 0;
+            continue;
+        }
         uint64_t v = uvox[i];
         uint64_t p = i ? uvox[i - 1] : ~v;
         leaf_h[i] = (v >> 9) != (p >> 9);
@@ -251,6 +258,14 @@ extern "C" size_t fvdb_build_workspace_bytes(int64_t n) {
 
 extern "C" int fvdb_build_plan(const int64_t* coords, int64_t n, void* workspace, size_t ws_bytes,
                                int64_t* counts, int64_t* detail, void* stream_) {
+    return fvdb_build_plan2(coords, n, nullptr, workspace, ws_bytes, counts, detail, stream_);
+}
+
+// Two host read-backs (range/tile-key scalars, then the node counts; plus the tile count when the coords
+// span several root tiles).  `pending_nonfinite` (optional, device) is the offending-row slot of an
+// unsynchronised fvdb_quantize_points_async: it is read with the first scalars and reported first.
+extern "C" int fvdb_build_plan2(const int64_t* coords, int64_t n, const int64_t* pending_nonfinite, void* workspace,
+                                size_t ws_bytes, int64_t* counts, int64_t* detail, void* stream_) {
     cudaStream_t st = as_stream(stream_);
     if (n <= 0 || n >= (int64_t)INT32_MAX) return FVDB_ERR_INVALID;
     Carver c(workspace, ws_bytes);
@@ -263,8 +278,15 @@ extern "C" int fvdb_build_plan(const int64_t* coords, int64_t n, void* workspace
     k_tile_keys<<<g, kThreads, 0, st>>>(coords, n, w.tk, w.sc);
     FVDB_LAUNCH_CHECK();
     BuildScalars hs;
+    unsigned long long nonfinite = ~0ull;
     FVDB_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    if (pending_nonfinite)
+        FVDB_CUDA_TRY(cudaMemcpyAsync(&nonfinite, pending_nonfinite, sizeof(nonfinite), cudaMemcpyDeviceToHost, st));
     FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (nonfinite != ~0ull) {
+        *detail = (int64_t)nonfinite;
+        return FVDB_ERR_NONFINITE;
+    }
     if (hs.bad_row != ~0ull) {
         *detail = (int64_t)hs.bad_row;
         return FVDB_ERR_COORD_RANGE;
@@ -301,27 +323,19 @@ extern "C" int fvdb_build_plan(const int64_t* coords, int64_t n, void* workspace
     FVDB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, vb, (int)n, 0, end_bit, st));
     tb = w.cub_bytes;
     FVDB_CUDA_TRY(cub::DeviceSelect::Unique(w.cub_tmp, tb, vb.Current(), w.uvox, w.n_sel, (int)n, st));
-    int nu = 0;
-    FVDB_CUDA_TRY(cudaMemcpyAsync(&nu, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FVDB_CUDA_TRY(cudaStreamSynchronize(st));
-
-    // node ids = inclusive scans of head flags (build.py:148-150)
-    const int gu = grid_for(nu);
-    k_node_heads<<<gu, kThreads, 0, st>>>(w.uvox, nu, w.leaf_id, w.lower_id, w.upper_id);
+    // node ids = inclusive scans of head flags (build.py:148-150), over all n slots (flags past the
+    // unique count are 0), so the unique count and the node counts come back in one read-back
+    k_node_heads<<<g, kThreads, 0, st>>>(w.uvox, (int)n, w.n_sel, w.leaf_id, w.lower_id, w.upper_id);
     FVDB_LAUNCH_CHECK();
     int* ids[3] = {w.leaf_id, w.lower_id, w.upper_id};
     for (int t = 0; t < 3; ++t) {
         tb = w.cub_bytes;
-        FVDB_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, ids[t], ids[t], nu, st));
+        FVDB_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, ids[t], ids[t], (int)n, st));
     }
-    int last[3];
+    int last[3], nu = 0;
     for (int t = 0; t < 3; ++t)
-        FVDB_CUDA_TRY(cudaMemcpyAsync(&last[t], ids[t] + (nu - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
-    // store counts for fill()
-    BuildScalars fin = hs;
-    fin.n_tiles = n_tiles;
-    fin.n_unique = nu;
-    FVDB_CUDA_TRY(cudaMemcpyAsync(w.sc, &fin, sizeof(fin), cudaMemcpyHostToDevice, st));
+        FVDB_CUDA_TRY(cudaMemcpyAsync(&last[t], ids[t] + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&nu, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
     FVDB_CUDA_TRY(cudaStreamSynchronize(st));
     counts[0] = last[2];  // num_upper
     counts[1] = last[1];  // num_lower
@@ -359,6 +373,18 @@ extern "C" int fvdb_floor_div_coords(const int64_t* coords, int64_t n, int64_t f
     if (factor < 1) return FVDB_ERR_INVALID;
     if (n == 0) return FVDB_OK;
     k_floor_div<<<grid_for(3 * n), kThreads, 0, as_stream(stream_)>>>(coords, n, factor, out);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_quantize_points_async(const double* points, int64_t n, const double* vs, const double* og,
+                                          int64_t* coords_out, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n == 0) return FVDB_OK;
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(coords_out + 3 * n);
+    FVDB_CUDA_TRY(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), st));
+    k_quantize<<<grid_for(n), kThreads, 0, st>>>(points, n, vs[0], vs[1], vs[2], og[0], og[1], og[2],
+                                                 coords_out, bad);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
