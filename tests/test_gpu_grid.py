@@ -67,6 +67,29 @@ def test_build_errors_match_reference_text():
     assert g.coord_to_index_many([[0, 0, 0]]).tolist() == [0]
 
 
+def test_build_from_points_reports_nonfinite_before_range():
+    """The finite check is deferred into the build's first read-back: it must still win over the range
+    check (the reference quantizes, raising on non-finite points, before it builds)."""
+    pts = [[1e12, 0.0, 0.0], [0.0, 0.0, 0.0], [0.0, np.inf, 0.0]]
+    with pytest.raises(ValueError, match=r"non-finite point at row 2: \[0.0, inf, 0.0\]"):
+        P.build_from_points(pts, P.VoxelTransform.uniform(1.0))
+    with pytest.raises(ValueError, match=r"coordinate out of range at row 0"):
+        P.build_from_points(pts[:2], P.VoxelTransform.uniform(1.0))
+
+
+def test_build_from_points_with_many_duplicates():
+    """Node scans run over all input slots with the tail past the unique count masked: a cloud that
+    collapses ~7:1 onto voxels must give the oracle's grid exactly."""
+    rng = np.random.default_rng(11)
+    pts = rng.normal(size=(50_000, 3)) * 4.0
+    g, st = P.build_from_points(pts, P.VoxelTransform.uniform(1.0))
+    og = O.build_from_points(pts, (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    assert g.num_voxels < 10_000 and st.input_count == 50_000 and g.num_voxels == og.num_voxels
+    a = g.to_numpy()
+    for f in FIELDS:
+        assert np.array_equal(a[f], getattr(og, f)), f
+
+
 def test_coord_limit_edge_is_accepted():
     c = np.array([[1 << 30, -(1 << 30), 0], [-(1 << 30), 1 << 30, (1 << 30)]])
     g, _ = P.build_from_coords(c)
