@@ -112,7 +112,9 @@ struct HaloCfg {
         while (n > 1 && !fits(n, b)) --n;
         return n;
     }
-    static constexpr int B1 = K >= 128 ? 1 : 4;             // V = 1 batch (K = 128: 32 KB weight images)
+    // V = 1 batch: K = 128 one stage (32 KB weight images); K = 32 eight (2 MMAs per stage: the per-batch
+    // hand-off cost needs more stages to amortise over)
+    static constexpr int B1 = K >= 128 ? 1 : (K == 32 ? 8 : 4);
     static constexpr int NSL = ONE ? deepest(B1) : (fits(2, 1) ? 2 : 1);
     static constexpr int BATCH = ONE ? B1 : (fits(NSL, 4) ? 4 : (fits(NSL, 2) ? 2 : 1));
     static constexpr int SLOTS = NISS * NSL;                // slot ring size (A in TMEM, weights in smem)
@@ -838,12 +840,12 @@ int sm_count_h() {
 }
 
 // MMA-issue layout per (K, N) (HaloCfg V), from B200 measurements (tools/halo_bench.py, fwd ms V0 -> V1):
-// K >= 64 one issuer (cfg2 64x64 0.366 -> 0.358, dense 64x64 0.696 -> 0.660, cfg2 128x128 0.899 -> 0.873;
-// cfg2 training step 1.084 -> 1.060), K = 32 two half-pipelines (cfg5 4.07 vs 4.23, dense32 0.870 vs
-// 0.902: at 16 A columns per stage the second issuer hides more than the deeper ring gains).
+// one issuer everywhere: cfg2 64x64 0.366 -> 0.358, dense 64x64 0.696 -> 0.660, cfg2 128x128 0.899 -> 0.873,
+// cfg5 32x32 4.08 -> 3.97 and dense 32x32 0.871 -> 0.851 (K = 32 with 8-stage batches; with 4-stage
+// batches it lost to V0: 4.23 / 0.902); cfg2 training step 1.084 -> 1.054 ms.
 // FVDB_HALO_VARIANT=0/1 overrides (profiling).
 template <int K, int N>
-constexpr int kHaloDefaultV = K >= 64 ? 1 : 0;
+constexpr int kHaloDefaultV = 1;
 int halo_variant_env() {
     static const int v = getenv("FVDB_HALO_VARIANT") ? atoi(getenv("FVDB_HALO_VARIANT")) : -1;
     return v;
