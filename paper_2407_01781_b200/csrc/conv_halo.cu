@@ -13,8 +13,9 @@
 // shared memory, fp32 accumulators in TMEM.  L2 traffic drops ~9× and the A operand never
 // passes through shared memory as an MMA operand.
 //
-// Halo plan (k_halo_plan, once per kernel map; cached by the caller):
-//   * per tile, the 27×128 neighbour entries are block-radix-sorted and deduplicated;
+// Halo plan (k_halo_count + k_halo_fill, once per kernel map and direction; cached by the caller):
+//   * per tile, the 27×128 neighbour entries are block-radix-sorted (significant key bits only) and
+//     deduplicated;
 //   * unique rows get slots 2·rank + color (color = coordinate-sum parity, see
 //     fvdb_parity_colors), so a slot's parity is its color;
 //   * output rows are permuted into lanes so that lanes 2p, 2p+1 hold rows of opposite
@@ -22,7 +23,8 @@
 //     two rows a shared-memory phase (8 threads) reads fall into disjoint bank halves;
 //   * a tile whose halo exceeds the kernel's capacity is split into 3 / 9 / 27 offset phases.
 //
-// Warp roles (11 warps): 0 halo loader, 1 MMA, 2-5 A builders, 6-9 epilogue, 10 weight loader.
+// Warp roles: 0 halo loader, 1-2 MMA issuers (V 1: warp 1 only), 3.. A builders (two halves x 4 TMEM
+// lane quarters x SUBS), then 4 epilogue warps and 1 weight loader (HaloCfg::THREADS).
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
@@ -71,16 +73,16 @@ __host__ __device__ __forceinline__ int halo_phys(int K, int s, int c) {
     return K == 64 ? (c ^ (s & 1)) : (K == 128 ? (c ^ ((s & 1) << 2)) : c);
 }
 
-constexpr int kImgExt = 34;
-constexpr int kHalves = 2;  // builder/MMA half-pipelines  // weight images per layer: 27 offsets + 7 wrap-around copies (d = 0..6)
+constexpr int kImgExt = 34;  // weight images per layer: 27 offsets + 7 wrap-around copies (d = 0..6), so a
+                             // batch of consecutive offsets is one TMA
+constexpr int kHalves = 2;   // builder halves: the warps of half h build the batches ab with ab % 2 == h
 
-// Two half-pipelines (builder warps of half h -> MMA warp h -> accumulator set h) take alternate
-// batches of BATCH consecutive (tile, offset) stages.  Why two MMA issuers: at N <= 128 a single
-// issuing thread sustains only ~100 cycles per A-in-TMEM tcgen05.mma (M=128, K=16), several issuing
-// warps reach the ~32-36-cycle hardware rate (profiles/r01_halo_kernel.md).  Every hand-off is per
-// batch: an mbarrier wait costs ~150-190 cycles even when its phase has already completed.
-// V selects the TMEM/smem split (profiling experiments): 0 = double-buffered accumulators;
-// 1 = single-buffered accumulators, 2 slots x 3-stage batches; 2 = single-buffered, 3 slots x 2 stages
+// Pipeline: builders fill A slots (TMEM) batch by batch from the staged halo, the weight loader fills the
+// matching weight slot (smem), the MMA issuer consumes the slot and releases it with one tcgen05.commit.
+// Throughput is stages in flight / slot round trip: every hand-off costs fixed latency (an mbarrier
+// round trip ~300 cycles even on a completed phase, tcgen05.fence ~150, tcgen05.commit ~200; measured in
+// tools/mma_issue_probe.cu), and TMEM (accumulators + 32-column A stages at K = 64) caps the stages in
+// flight.  V picks the MMA-issue layout (profiles/r01_halo_kernel.md §v7).
 template <int K, int N, int V = 0>
 struct HaloCfg {
     static constexpr int ROWB = 2 * K;                      // halo row bytes
