@@ -171,3 +171,51 @@ def test_halo_empty_and_tiny():
     w = torch.ones(64, 64, 3, 3, 3, device="cuda") / 64
     y = gather_conv(x, km.fwd, w, out_dtype=torch.float32, impl="halo")
     assert torch.allclose(y, torch.ones_like(y))
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_halo_vs_torch_fp64():
+    """BASELINE cfg2 (1,018,216 voxels, 64->64): the halo kernels the bench times, forward and dgrad, against
+    a torch float64 per-offset reference of the same bf16-exact inputs (accumulation error only)."""
+    g, _ = P.build_from_coords(sphere_shell_coords(470, band=1.5))
+    km = P.build_kernel_map(g, g, 1)
+    n = g.num_voxels
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(n, 64, device="cuda", generator=gen).to(torch.bfloat16)
+    gy = torch.randn(n, 64, device="cuda", generator=gen).to(torch.bfloat16)
+    w = torch.randn(64, 64, 3, 3, 3, device="cuda", generator=gen) / (27 * 64) ** 0.5
+    y = gather_conv(x, km.fwd, w, out_dtype=torch.float32, impl="halo")
+    gi = gather_conv(gy, km.bwd, w, transpose=True, out_dtype=torch.float32, impl="halo")
+    wd = w.to(torch.bfloat16).double().reshape(64, 64, 27)
+    xd, gyd, nbr = x.double(), gy.double(), km.nbr.long()
+    ref_y = torch.zeros(n, 64, dtype=torch.float64, device="cuda")
+    ref_gi = torch.zeros_like(ref_y)
+    for d in range(27):
+        m = nbr[d] >= 0
+        o, i = torch.nonzero(m).squeeze(1), nbr[d][m]
+        ref_y[o] += xd[i] @ wd[:, :, d].T
+        ref_gi.index_add_(0, i, gyd[o] @ wd[:, :, d])
+    for got, ref in ((y, ref_y), (gi, ref_gi)):
+        assert float((got.double() - ref).abs().max() / ref.abs().max()) < 2e-5
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_halo_adjoint_and_determinism():
+    """BASELINE cfg5 (2048^3 shell, ~19.4M voxels, 32->32) at full size through size-independent
+    properties: <conv(x), y> = <x, conv^T(y)> (forward and dgrad kernels are each other's adjoint) and
+    bitwise run-to-run reproducibility."""
+    g, _ = P.build_from_coords(sphere_shell_coords(2048, band=1.5))
+    km = P.build_kernel_map(g, g, 1)
+    n = g.num_voxels
+    assert n > 19_000_000
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    x = torch.randn(n, 32, device="cuda", generator=gen).to(torch.bfloat16)
+    yv = torch.randn(n, 32, device="cuda", generator=gen).to(torch.bfloat16)
+    w = torch.randn(32, 32, 3, 3, 3, device="cuda", generator=gen) / (27 * 32) ** 0.5
+    cx = gather_conv(x, km.fwd, w, out_dtype=torch.float32, impl="halo")
+    cty = gather_conv(yv, km.bwd, w, transpose=True, out_dtype=torch.float32, impl="halo")
+    lhs = float((cx.double() * yv.double()).sum())
+    rhs = float((x.double() * cty.double()).sum())
+    scale = float((cx.double().abs() * yv.double().abs()).sum())
+    assert abs(lhs - rhs) / scale < 1e-6
+    assert torch.equal(cx, gather_conv(x, km.fwd, w, out_dtype=torch.float32, impl="halo"))
