@@ -219,3 +219,10 @@ def test_cfg5_full_size_halo_adjoint_and_determinism():
     scale = float((cx.double().abs() * yv.double().abs()).sum())
     assert abs(lhs - rhs) / scale < 1e-6
     assert torch.equal(cx, gather_conv(x, km.fwd, w, out_dtype=torch.float32, impl="halo"))
+    # wgrad is the adjoint of the weight -> output map: <wgrad(x, y), W> = <conv(x; W), y>
+    from paper_2407_01781_b200.conv import wgrad
+    gw = wgrad(x, yv, km.fwd)
+    wb = w.to(torch.bfloat16).double()
+    lhs_w = float((gw.double() * wb).sum())
+    scale_w = float((gw.double().abs() * wb.abs()).sum())
+    assert abs(lhs_w - lhs) / scale_w < 1e-5
