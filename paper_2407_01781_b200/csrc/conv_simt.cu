@@ -75,6 +75,100 @@ __global__ void __launch_bounds__(kThr) k_conv_gather(const T* __restrict__ in, 
     }
 }
 
+// Tiled form for K, N multiples of 8 and N <= 64 (the reference's common channel counts): 128 output rows per
+// CTA, each thread a 4-row x N/8-column register tile; the gathered rows and the offset's weights move
+// through two cp.async stages (zero-filled for missing neighbours and K/N padding).  The per-element
+// accumulation order is k_conv_gather's (offset-major, then K ascending), so results are identical.
+constexpr int kTR = 128, kTKC = 32;
+template <typename T, int NT>
+struct TileCfg {
+    static constexpr int EPV = 16 / (int)sizeof(T);          // elements per 16-byte copy
+    static constexpr int LDA = kTKC + EPV;                   // padded row stride of the A tile (16-B aligned)
+    static constexpr int CPT = NT / 8;                       // output columns per thread
+    static constexpr int A_ELEMS = kTR * LDA, W_ELEMS = kTKC * NT;
+    static constexpr int STAGE_BYTES = (A_ELEMS + W_ELEMS) * (int)sizeof(T);
+    static constexpr int SMEM = 2 * STAGE_BYTES;
+};
+
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(kThr) k_conv_gather_tiled(const T* __restrict__ in, int K, const T* __restrict__ wk,
+                                                            int N, const int32_t* __restrict__ nbr, int64_t ld,
+                                                            int64_t n_out, T* __restrict__ out) {
+    using C = TileCfg<T, NT>;
+    extern __shared__ __align__(16) uint8_t smraw[];
+    T* sm = reinterpret_cast<T*>(smraw);
+    const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+    const int64_t o0 = (int64_t)blockIdx.x * kTR;
+    const int kchunks = (K + kTKC - 1) / kTKC, steps = 27 * kchunks;
+    auto issue = [&](int step, int buf) {
+        const int d = step / kchunks, k0 = (step % kchunks) * kTKC;
+        T* sa = sm + buf * (C::A_ELEMS + C::W_ELEMS);
+        T* sw = sa + C::A_ELEMS;
+        constexpr int CPR = kTKC / C::EPV;                    // 16-B copies per A row
+        for (int c = tid; c < kTR * CPR; c += kThr) {
+            const int r = c / CPR, cc = c % CPR, k = k0 + cc * C::EPV;
+            const int64_t o = o0 + r;
+            const int32_t i = o < n_out ? nbr[(int64_t)d * ld + o] : -1;
+            const bool ok = i >= 0 && k < K;
+            cp_async16_zfill((uint32_t)__cvta_generic_to_shared(sa + r * C::LDA + cc * C::EPV),
+                             ok ? (const void*)(in + (int64_t)i * K + k) : (const void*)in, ok);
+        }
+        constexpr int CPW = NT / C::EPV;                      // 16-B copies per weight row
+        for (int c = tid; c < kTKC * CPW; c += kThr) {
+            const int kk = c / CPW, n = (c % CPW) * C::EPV;
+            const bool ok = k0 + kk < K && n < N;
+            cp_async16_zfill((uint32_t)__cvta_generic_to_shared(sw + kk * NT + n),
+                             ok ? (const void*)(wk + ((int64_t)d * K + k0 + kk) * N + n) : (const void*)wk, ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    T acc[4][C::CPT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < C::CPT; ++j) acc[i][j] = T(0);
+    issue(0, 0);
+    for (int step = 0; step < steps; ++step) {
+        const int buf = step & 1;
+        if (step + 1 < steps) {
+            issue(step + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const T* sa = sm + buf * (C::A_ELEMS + C::W_ELEMS);
+        const T* sw = sa + C::A_ELEMS;
+#pragma unroll 8
+        for (int kk = 0; kk < kTKC; ++kk) {
+            T a[4], b[C::CPT];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = sa[(ty + 32 * i) * C::LDA + kk];
+#pragma unroll
+            for (int j = 0; j < C::CPT; ++j) b[j] = sw[kk * NT + tx * C::CPT + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < C::CPT; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();  // the next issue overwrites this buffer
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t o = o0 + ty + 32 * i;
+        if (o >= n_out) continue;
+#pragma unroll
+        for (int j = 0; j < C::CPT; ++j) {
+            const int n = tx * C::CPT + j;
+            if (n < N) out[o * N + n] = acc[i][j];
+        }
+    }
+}
+
 // W[Cout][Cin][27] -> Wk[27][K][N]
 template <typename T>
 __global__ void k_pack_kn(const T* __restrict__ w, int cout, int cin, int transpose, T* __restrict__ wk) {
@@ -166,6 +260,20 @@ template <typename T>
 int run_gather(const void* in, int K, const void* wk, int N, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
                cudaStream_t st) {
     if (n_out == 0) return FVDB_OK;
+    if (K % 8 == 0 && N % 8 == 0 && N <= 64) {
+        const unsigned blocks = (unsigned)ceil_div(n_out, kTR);
+        if (N <= 32) {
+            auto kern = k_conv_gather_tiled<T, 32>;
+            FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TileCfg<T, 32>::SMEM));
+            kern<<<blocks, kThr, TileCfg<T, 32>::SMEM, st>>>((const T*)in, K, (const T*)wk, N, nbr, ld, n_out, (T*)out);
+        } else {
+            auto kern = k_conv_gather_tiled<T, 64>;
+            FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TileCfg<T, 64>::SMEM));
+            kern<<<blocks, kThr, TileCfg<T, 64>::SMEM, st>>>((const T*)in, K, (const T*)wk, N, nbr, ld, n_out, (T*)out);
+        }
+        FVDB_LAUNCH_CHECK();
+        return FVDB_OK;
+    }
     unsigned blocks = (unsigned)ceil_div(n_out, kRows);
     k_conv_gather<T><<<blocks, kThr, 0, st>>>((const T*)in, K, (const T*)wk, N, nbr, ld, n_out, (T*)out);
     FVDB_LAUNCH_CHECK();

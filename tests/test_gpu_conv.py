@@ -336,3 +336,21 @@ def test_cfg2_full_size_tc_vs_torch_fp64():
     assert r(y, ref_y) < 2e-5
     assert r(gi, ref_gi) < 2e-5
     assert r(gw.reshape(64, 64, 27), ref_gw) < 2e-5
+
+
+@pytest.mark.parametrize("cin,cout", [(64, 64), (40, 48), (8, 8), (32, 24)])
+def test_simt_tiled_shapes_match_oracle(shell, cin, cout):
+    """The tiled fp32/f64 kernel (K, N multiples of 8, N <= 64): several K chunks, a zero-padded last
+    chunk (K = 40), both column tiles (N <= 32, N <= 64); forward and dgrad against the oracle."""
+    g, _, ins, outs, km = shell
+    rng = np.random.default_rng(cin * 13 + cout)
+    n = g.num_voxels
+    x = rng.normal(size=(n, cin))
+    w = rng.normal(size=(cout, cin, 3, 3, 3)) / np.sqrt(27 * cin)
+    gy = rng.normal(size=(n, cout))
+    ref = O.conv_igemm(x, w, ins, outs, n)
+    gi_ref, _ = O.conv_backward(ins, outs, gy, x, w)
+    for dt, tol in ((torch.float64, 1e-10), (torch.float32, 1e-5)):
+        xt, wt, gyt = (torch.from_numpy(a).cuda().to(dt) for a in (x, w, gy))
+        assert rel(gather_conv(xt, km.fwd, wt), ref) < tol
+        assert rel(gather_conv(gyt, km.bwd, wt, transpose=True), gi_ref) < tol
