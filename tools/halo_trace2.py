@@ -12,10 +12,15 @@ from paper_2407_01781_b200 import _lib
 from paper_2407_01781_b200.conv import gather_conv, pack_weights_umma
 from paper_2407_01781_b200.workloads import sphere_shell_coords
 NSL = int(os.environ.get("NSL", "2"))  # per-half slots (two-issuer layout); R overrides the reuse distance
-g, _ = P.build_from_coords(sphere_shell_coords(470, 1.5))
+CH = int(os.environ.get("CH", "64"))  # channels (K = N); CFG=dense uses a 160^3 block instead of the cfg2 shell
+if os.environ.get("CFG") == "dense":
+    r = np.arange(160)
+    g, _ = P.build_from_coords(np.stack(np.meshgrid(r, r, r, indexing="ij"), -1).reshape(-1, 3))
+else:
+    g, _ = P.build_from_coords(sphere_shell_coords(470, 1.5))
 km = P.build_kernel_map(g, g, 1)
-x = torch.randn(g.num_voxels, 64, device="cuda").to(torch.bfloat16)
-w = torch.randn(64, 64, 3, 3, 3, device="cuda") / 40
+x = torch.randn(g.num_voxels, CH, device="cuda").to(torch.bfloat16)
+w = torch.randn(CH, CH, 3, 3, 3, device="cuda") / (27 * CH) ** 0.5
 img = pack_weights_umma(w, False, "halo")
 for _ in range(3):
     gather_conv(x, km.fwd, w, w_image=img, impl="halo")
