@@ -165,6 +165,15 @@ int fvdb_kmap_signature_order(const int32_t* nbr, int64_t ld, int64_t n_out, int
 int fvdb_conv_gather_tc_perm(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
                              const int32_t* nbr_perm, int64_t ld, int64_t n_out, const int32_t* row_perm,
                              void* out, int out_dtype, void* stream);
+/* Per-128-row-tile offset masks: masks[t] bit d set iff some row of tile t has a pair at offset d
+ * (masks holds ceil(n_out / 128) u32).  Given to fvdb_conv_gather_tc2, the kernel walks only the offsets
+ * present in each super-tile: absent offsets cost no index/weight copy and no pipeline stage. */
+int fvdb_kmap_tile_masks(const int32_t* nbr, int64_t ld, int64_t n_out, uint32_t* masks, void* stream);
+/* fvdb_conv_gather_tc with an optional row permutation (table column i -> output row_perm[i]) and optional
+ * tile masks (both nullable). */
+int fvdb_conv_gather_tc2(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
+                         const int32_t* nbr, int64_t ld, int64_t n_out, const int32_t* row_perm,
+                         const uint32_t* tile_masks, void* out, int out_dtype, void* stream);
 /* wgrad on tensor cores: gw fp32 [cout][cin][27]. */
 size_t fvdb_wgrad_tc_workspace_bytes(int64_t n_out, int cin, int cout);
 int fvdb_conv_wgrad_tc(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,

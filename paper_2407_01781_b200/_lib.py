@@ -79,6 +79,8 @@ SIGNATURES = {
     "fvdb_kmap_signature_workspace_bytes": (_sz, [_i64]),
     "fvdb_kmap_signature_order": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "fvdb_conv_gather_tc_perm": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _i32, _vp]),
+    "fvdb_conv_gather_tc2": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp]),
+    "fvdb_kmap_tile_masks": (_i32, [_vp, _i64, _i64, _vp, _vp]),
     "fvdb_wgrad_tc_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "fvdb_conv_wgrad_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "fvdb_f32_to_bf16": (_i32, [_vp, _i64, _vp, _vp]),

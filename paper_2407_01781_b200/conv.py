@@ -120,7 +120,8 @@ class NbrTable:
     uses to pair lanes; halo plans are built lazily per kernel capacity and cached.
     """
 
-    __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted")
+    __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
+                 "_masks", "sparse")
 
     def __init__(self, t, n, colors_fn=None, counts=None):
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
@@ -129,6 +130,8 @@ class NbrTable:
         self.counts = counts  # per-offset pair counts (device or host int64 [27]), when known
         self._density = None
         self._sorted = None
+        self._masks = None
+        self.sparse = False  # set for transposed stride-2 tables (<= 8 of 27 offsets per row)
 
     def density(self) -> float:
         """Mean pairs per output row (27 = every offset active); 27 when unknown."""
@@ -140,7 +143,7 @@ class NbrTable:
         return self._density
 
     def signature_sorted(self):
-        """(nbr_perm table, perm): rows stably sorted by their 27-bit offset signature, cached."""
+        """(nbr_perm table, perm, tile masks): rows stably sorted by their 27-bit offset signature, cached."""
         if self._sorted is None:
             L = _lib.lib()
             perm = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.t.device)
@@ -150,8 +153,14 @@ class NbrTable:
             _lib.check(L.fvdb_kmap_signature_order(self.t.data_ptr(), self.ld, self.n, perm.data_ptr(),
                                                    tp.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()),
                        "kmap_signature_order")
-            self._sorted = (tp, perm)
+            self._sorted = (tp, perm, _tile_masks(tp, self.ld, self.n))
         return self._sorted
+
+    def tile_masks(self):
+        """uint32 [ceil(n / 128)]: bit d of tile t = some row of the tile has a pair at offset d, cached."""
+        if self._masks is None:
+            self._masks = _tile_masks(self.t, self.ld, self.n)
+        return self._masks
 
     def has_plan(self, K: int, N: int) -> bool:
         cap = int(_lib.lib().fvdb_halo_cap(K, N))
@@ -174,6 +183,14 @@ class NbrTable:
         if p is None:
             p = self._plans[cap] = HaloPlan(self, cap)
         return p
+
+
+def _tile_masks(t: torch.Tensor, ld: int, n: int) -> torch.Tensor:
+    m = torch.empty(max(1, (n + 127) // 128), dtype=torch.int32, device=t.device)
+    if n:
+        _lib.check(_lib.lib().fvdb_kmap_tile_masks(t.data_ptr(), ld, n, m.data_ptr(), _lib.stream_ptr()),
+                   "kmap_tile_masks")
+    return m
 
 
 def parity_colors(coords: torch.Tensor, shift: int) -> torch.Tensor:
@@ -302,6 +319,7 @@ class KernelMap:
                                              t.data_ptr(), t.shape[1], _lib.stream_ptr()), "kmap_transpose")
             self._bwd = NbrTable(t, self.num_in, self._bwd_colors if self._grids is not None else None,
                                  counts=self._counts)
+            self._bwd.sparse = self.stride == 2  # fine voxel i pairs only offsets d with i - d even: <= 8 of 27
         return self._bwd
 
     def transposed_table(self):
@@ -393,17 +411,23 @@ def sig_sort_enabled(nbr: "NbrTable") -> bool:
     """Run the gather kernel over the signature-sorted table?
 
     Sorting output rows by which offsets they have (fvdb_kmap_signature_order) makes 128-row tiles
-    homogeneous, so the kernel skips the copies and MMAs of (tile, offset) stages with no pair.
-    Sparse maps gain (a transposed stride-2 map has ~3 of 27 offsets per row); dense ones
-    only pay the sort.  Opt-in: env FVDB_SIG_SORT=1 sorts tables below ``SORT_BELOW_DENSITY``,
-    "force" sorts every table.  Measured on B200 (tools/sigsort_bench.py), cfg4's transposed map
-    at 3.1 pairs/row runs 0.858 -> 0.645 ms per conv after a 0.21 ms one-off sort, while the halo
-    kernel runs the same map in 0.526 ms, so "auto" does not sort.
+    homogeneous. With the tile masks, the kernel then walks only the offsets present in each super-tile:
+    absent offsets cost no copy, MMA or pipeline stage. Measured on B200 (tools/sigsort_bench.py), cfg4's
+    transposed stride-2 map at 3.1 pairs/row runs 0.873 -> 0.178 ms per conv after a 0.22 ms sort. The
+    halo kernel runs that map in 0.528 ms.
+
+    Default: tables flagged ``sparse`` (the transposed table of a stride-2 map: at most 8 of 27 offsets per
+    row). Env FVDB_SIG_SORT: "0" never sorts, "1" sorts tables below ``SORT_BELOW_DENSITY`` mean pairs per
+    row, "force" sorts every table.
     """
-    v = os.environ.get("FVDB_SIG_SORT", "0")
+    v = os.environ.get("FVDB_SIG_SORT")
     if v == "force":
         return True
-    return v == "1" and nbr.density() < SORT_BELOW_DENSITY
+    if v == "0":
+        return False
+    if v == "1":
+        return nbr.density() < SORT_BELOW_DENSITY
+    return nbr.sparse
 
 
 def conv_impl() -> str:
@@ -411,7 +435,8 @@ def conv_impl() -> str:
 
     * "auto" (default): the gather-GEMM kernel (conv_tc.cu) for a neighbour table's first
       ``HALO_AFTER_USES`` bf16 uses, then the halo-staged kernel (conv_halo.cu); immediately if the
-      table already has a plan.  Building the plan costs ~3-6 gather convolutions (cfg2: 2.2 ms vs
+      table already has a plan.  Sparse tables (``sig_sort_enabled``) always take the gather kernel over
+      their signature-sorted, offset-masked form (3x faster than the halo kernel there).  Building the plan costs ~3-6 gather convolutions (cfg2: 2.2 ms vs
       0.67 ms per conv, saving ~0.3 ms per use), so it pays off for maps reused across layers and
       training iterations, not for maps used once or twice (cfg4 rebuilds its maps every step and uses
       each in one forward and one backward);
@@ -495,8 +520,9 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
         impl = _image_impl(w_image, K, N)  # the image decides
     else:
         impl = impl or conv_impl()
-        if impl == "auto":
-            impl = "halo" if nbr.uses >= HALO_AFTER_USES or nbr.has_plan(K, N) else "gather"
+        if impl == "auto":  # sparse tables stay on the signature-sorted, offset-masked gather kernel
+            reuse = nbr.uses >= HALO_AFTER_USES or nbr.has_plan(K, N)
+            impl = "halo" if reuse and not sig_sort_enabled(nbr) else "gather"
     nbr.uses += 1
     img = w_image if w_image is not None else pack_weights_umma(w, transpose, impl)
     out = torch.empty((n_out, N), dtype=out_dtype, device=x.device)
@@ -506,14 +532,16 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
         plan = nbr.halo_plan(K, N)
         _lib.check(L.fvdb_conv_halo_tc(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, C.byref(plan.c), n_out,
                                        out.data_ptr(), _dtype_code(out_dtype), st), "conv_halo_tc")
-    elif sig_sort_enabled(nbr):
-        tp, perm = nbr.signature_sorted()
-        _lib.check(L.fvdb_conv_gather_tc_perm(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, tp.data_ptr(), nbr.ld,
-                                              n_out, perm.data_ptr(), out.data_ptr(), _dtype_code(out_dtype), st),
-                   "conv_gather_tc_perm")
     else:
-        _lib.check(L.fvdb_conv_gather_tc(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, nbr.t.data_ptr(), nbr.ld,
-                                         n_out, out.data_ptr(), _dtype_code(out_dtype), st), "conv_gather_tc")
+        # the kernel walks only the offsets present in each super-tile (tile masks); sparse tables are
+        # signature-sorted first so that tiles are homogeneous and most offsets drop out
+        if sig_sort_enabled(nbr):
+            tab, perm, masks = nbr.signature_sorted()
+        else:
+            tab, perm, masks = nbr.t, None, nbr.tile_masks()
+        _lib.check(L.fvdb_conv_gather_tc2(x.data_ptr(), x.shape[0], K, img.data_ptr(), N, tab.data_ptr(), nbr.ld,
+                                          n_out, _lib.ptr(perm), masks.data_ptr(), out.data_ptr(),
+                                          _dtype_code(out_dtype), st), "conv_gather_tc")
     return out
 
 

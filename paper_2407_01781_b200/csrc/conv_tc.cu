@@ -82,7 +82,7 @@ template <int K, int N, bool OUT_BF16, int TPS = (N <= 64 ? 4 : 2), int NPW = 4>
 __global__ void __launch_bounds__(fwd_threads(NPW), 1)
     k_conv_fwd_tc(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, const int32_t* __restrict__ nbr,
                   int64_t ld, int64_t n_out, void* __restrict__ out, int num_super, int dbg,
-                  const int32_t* __restrict__ row_perm) {
+                  const int32_t* __restrict__ row_perm, const uint32_t* __restrict__ tile_mask) {
     using C = FwdCfg<K, N, TPS>;
     constexpr int W_LOAD = NPW, W_MMA = NPW + 1, W_EPI = NPW + 2;
     constexpr int RPW = kTile / NPW;  // rows per gather warp per tile
@@ -100,6 +100,18 @@ __global__ void __launch_bounds__(fwd_threads(NPW), 1)
     const uint32_t ibase = bbase + C::BSLOTS * C::B_BYTES;           // index blocks
     const int32_t* idx_smem = reinterpret_cast<const int32_t*>(dsmem + (ibase - sbase));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // offsets with at least one pair in super-tile st (tile_mask: per 128-row tile, 27 bits; null = all).
+    // Every warp walks the same list, so the stage / slot counters stay in step; absent offsets cost
+    // no index or weight copy and no barrier round trip.
+    const int n_tiles = (int)((n_out + kTile - 1) / kTile);
+    auto offsets_of = [&](int st) -> uint32_t {
+        if (!tile_mask) return 0x7FFFFFFu;
+        uint32_t m = 0;
+#pragma unroll
+        for (int t = 0; t < C::TPS; ++t)
+            if (st * C::TPS + t < n_tiles) m |= tile_mask[st * C::TPS + t];
+        return m;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -150,7 +162,7 @@ __global__ void __launch_bounds__(fwd_threads(NPW), 1)
         const bf16* in_c = in + cchunk * 8;
         uint32_t it = 0, ic = 0;
         for (int st = blockIdx.x; st < num_super; st += gridDim.x) {
-            for (int d = 0; d < 27; ++d, ++ic) {
+            for (uint32_t om = offsets_of(st); om; om &= om - 1, ++ic) {
                 const uint32_t islot = ic % C::ISLOTS;
                 mbar_wait(smem_u32(&bar_ifull[islot]), (ic / C::ISLOTS) & 1);
                 const int32_t* ib = idx_smem + islot * C::SUPER + warp * RPW;
@@ -185,7 +197,8 @@ __global__ void __launch_bounds__(fwd_threads(NPW), 1)
         if (lane == 0) {
             uint32_t ic = 0, bc = 0;
             for (int st = blockIdx.x; st < num_super; st += gridDim.x) {
-                for (int d = 0; d < 27; ++d, ++ic, ++bc) {
+                for (uint32_t om = offsets_of(st); om; om &= om - 1, ++ic, ++bc) {
+                    const int d = __ffs(om) - 1;
                     const uint32_t islot = ic % C::ISLOTS;
                     mbar_wait_sleep(smem_u32(&bar_iempty[islot]), ((ic / C::ISLOTS) & 1) ^ 1, 128);
                     mbar_arrive_expect_tx(smem_u32(&bar_ifull[islot]), C::IDX_BYTES);
@@ -210,7 +223,7 @@ __global__ void __launch_bounds__(fwd_threads(NPW), 1)
             const uint32_t buf = lt & 1;
             mbar_wait(smem_u32(&bar_tempty[buf]), ((lt >> 1) & 1) ^ 1);
             tc_fence_after();
-            for (int d = 0; d < 27; ++d, ++bc) {
+            for (uint32_t om = offsets_of(st); om; om &= om - 1, ++bc) {
                 const uint32_t bslot = bc % C::BSLOTS;
                 mbar_wait(smem_u32(&bar_bfull[bslot]), (bc / C::BSLOTS) & 1);
                 const uint32_t sB = bbase + bslot * C::B_BYTES;
@@ -543,9 +556,16 @@ int sm_count() {
     return v;
 }
 
+// optional inputs of the gather kernel: output-row permutation (signature-sorted tables) and per-128-row-tile
+// offset masks (fvdb_kmap_tile_masks)
+struct FwdOpt {
+    const int32_t* perm;
+    const uint32_t* mask;
+};
+
 template <int K, int N, bool OB, int TPS = (N <= 64 ? 4 : 2), int NPW = 4>
 int launch_fwd_t(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-                 cudaStream_t st, const int32_t* perm) {
+                 cudaStream_t st, FwdOpt opt) {
     using C = FwdCfg<K, N, TPS>;
     auto kern = k_conv_fwd_tc<K, N, OB, TPS, NPW>;
     FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -554,36 +574,36 @@ int launch_fwd_t(const void* in, const void* wimg, const int32_t* nbr, int64_t l
     if (grid > supers) grid = supers;
     static const int dbg = getenv("FVDB_DEBUG_FWD") ? atoi(getenv("FVDB_DEBUG_FWD")) : 0;  // profiling switches
     kern<<<grid, fwd_threads(NPW), C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, nbr, ld, n_out, out, supers,
-                                                  dbg, perm);
+                                                  dbg, opt.perm, opt.mask);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
 
 template <int K, int N, bool OB>
 int launch_fwd(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-               cudaStream_t st, const int32_t* perm) {
+               cudaStream_t st, FwdOpt opt) {
     if constexpr (K == 64 && N == 64) {
         static const int npw = getenv("FVDB_FWD_NPW") ? atoi(getenv("FVDB_FWD_NPW")) : 4;  // profiling switch
-        if (npw == 8) return launch_fwd_t<K, N, OB, 4, 8>(in, wimg, nbr, ld, n_out, out, st, perm);
+        if (npw == 8) return launch_fwd_t<K, N, OB, 4, 8>(in, wimg, nbr, ld, n_out, out, st, opt);
     }
-    return launch_fwd_t<K, N, OB>(in, wimg, nbr, ld, n_out, out, st, perm);
+    return launch_fwd_t<K, N, OB>(in, wimg, nbr, ld, n_out, out, st, opt);
 }
 
 template <int K, int N>
 int dispatch_out(const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-                 int out_dtype, cudaStream_t st, const int32_t* perm) {
-    if (out_dtype == FVDB_DTYPE_BF16) return launch_fwd<K, N, true>(in, wimg, nbr, ld, n_out, out, st, perm);
-    if (out_dtype == FVDB_DTYPE_F32) return launch_fwd<K, N, false>(in, wimg, nbr, ld, n_out, out, st, perm);
+                 int out_dtype, cudaStream_t st, FwdOpt opt) {
+    if (out_dtype == FVDB_DTYPE_BF16) return launch_fwd<K, N, true>(in, wimg, nbr, ld, n_out, out, st, opt);
+    if (out_dtype == FVDB_DTYPE_F32) return launch_fwd<K, N, false>(in, wimg, nbr, ld, n_out, out, st, opt);
     return FVDB_ERR_INVALID;
 }
 
 template <int K>
 int dispatch_n(int N, const void* in, const void* wimg, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-               int od, cudaStream_t st, const int32_t* perm) {
+               int od, cudaStream_t st, FwdOpt opt) {
     switch (N) {
-        case 32: return dispatch_out<K, 32>(in, wimg, nbr, ld, n_out, out, od, st, perm);
-        case 64: return dispatch_out<K, 64>(in, wimg, nbr, ld, n_out, out, od, st, perm);
-        case 128: return dispatch_out<K, 128>(in, wimg, nbr, ld, n_out, out, od, st, perm);
+        case 32: return dispatch_out<K, 32>(in, wimg, nbr, ld, n_out, out, od, st, opt);
+        case 64: return dispatch_out<K, 64>(in, wimg, nbr, ld, n_out, out, od, st, opt);
+        case 128: return dispatch_out<K, 128>(in, wimg, nbr, ld, n_out, out, od, st, opt);
         default: return FVDB_ERR_INVALID;
     }
 }
@@ -665,34 +685,60 @@ extern "C" int fvdb_pack_weights_umma(const float* w, int cout, int cin, int tra
     return FVDB_OK;
 }
 
-extern "C" int fvdb_conv_gather_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
-                                   const int32_t* nbr, int64_t ld, int64_t n_out, void* out, int out_dtype,
-                                   void* stream) {
+extern "C" int fvdb_conv_gather_tc2(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
+                                    const int32_t* nbr, int64_t ld, int64_t n_out, const int32_t* row_perm,
+                                    const uint32_t* tile_masks, void* out, int out_dtype, void* stream) {
     (void)n_in;
     if (n_out == 0) return FVDB_OK;
     if (ld % FVDB_NBR_ALIGN != 0 || ld < n_out) return FVDB_ERR_INVALID;
     cudaStream_t st = as_stream(stream);
+    const FwdOpt opt{row_perm, tile_masks};
     switch (K) {
-        case 32: return dispatch_n<32>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st, nullptr);
-        case 64: return dispatch_n<64>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st, nullptr);
-        case 128: return dispatch_n<128>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st, nullptr);
+        case 32: return dispatch_n<32>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st, opt);
+        case 64: return dispatch_n<64>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st, opt);
+        case 128: return dispatch_n<128>(N, in_bf16, w_image, nbr, ld, n_out, out, out_dtype, st, opt);
         default: return FVDB_ERR_INVALID;
     }
+}
+
+extern "C" int fvdb_conv_gather_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
+                                   const int32_t* nbr, int64_t ld, int64_t n_out, void* out, int out_dtype,
+                                   void* stream) {
+    return fvdb_conv_gather_tc2(in_bf16, n_in, K, w_image, N, nbr, ld, n_out, nullptr, nullptr, out, out_dtype,
+                                stream);
 }
 
 extern "C" int fvdb_conv_gather_tc_perm(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,
                                         const int32_t* nbr_perm, int64_t ld, int64_t n_out, const int32_t* row_perm,
                                         void* out, int out_dtype, void* stream) {
-    (void)n_in;
-    if (n_out == 0) return FVDB_OK;
-    if (ld % FVDB_NBR_ALIGN != 0 || ld < n_out || !row_perm) return FVDB_ERR_INVALID;
-    cudaStream_t st = as_stream(stream);
-    switch (K) {
-        case 32: return dispatch_n<32>(N, in_bf16, w_image, nbr_perm, ld, n_out, out, out_dtype, st, row_perm);
-        case 64: return dispatch_n<64>(N, in_bf16, w_image, nbr_perm, ld, n_out, out, out_dtype, st, row_perm);
-        case 128: return dispatch_n<128>(N, in_bf16, w_image, nbr_perm, ld, n_out, out, out_dtype, st, row_perm);
-        default: return FVDB_ERR_INVALID;
+    if (!row_perm) return FVDB_ERR_INVALID;
+    return fvdb_conv_gather_tc2(in_bf16, n_in, K, w_image, N, nbr_perm, ld, n_out, row_perm, nullptr, out,
+                                out_dtype, stream);
+}
+
+// masks[t] bit d: some row of 128-row tile t has a pair at offset d (one thread per row, warp OR-reduce)
+__global__ void k_tile_masks(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out, uint32_t* __restrict__ masks) {
+    __shared__ uint32_t wm[kTile / 32];
+    const int64_t o = (int64_t)blockIdx.x * kTile + threadIdx.x;
+    uint32_t sig = 0;
+    if (o < n_out)
+        for (int d = 0; d < 27; ++d) sig |= (nbr[(int64_t)d * ld + o] >= 0 ? 1u : 0u) << d;
+    sig = __reduce_or_sync(0xffffffffu, sig);
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = sig;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t m = 0;
+        for (int w = 0; w < kTile / 32; ++w) m |= wm[w];
+        masks[blockIdx.x] = m;
     }
+}
+
+extern "C" int fvdb_kmap_tile_masks(const int32_t* nbr, int64_t ld, int64_t n_out, uint32_t* masks, void* stream) {
+    if (n_out < 0 || ld < n_out) return FVDB_ERR_INVALID;
+    if (n_out == 0) return FVDB_OK;
+    k_tile_masks<<<(unsigned)ceil_div(n_out, kTile), kTile, 0, as_stream(stream)>>>(nbr, ld, n_out, masks);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
 }
 
 extern "C" size_t fvdb_kmap_signature_workspace_bytes(int64_t n_out) {

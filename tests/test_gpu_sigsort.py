@@ -11,7 +11,7 @@ import torch
 
 import oracle as O
 import paper_2407_01781_b200 as P
-from paper_2407_01781_b200.conv import gather_conv
+from paper_2407_01781_b200.conv import gather_conv, pack_weights_umma
 from paper_2407_01781_b200.workloads import sphere_shell_coords
 
 pytestmark = pytest.mark.gpu
@@ -51,7 +51,7 @@ def maps():
 def test_signature_order_is_stable_sort(maps, which):
     _, _, (km1, _, _), (km2, _, _) = maps
     tab = {"s1_fwd": km1.fwd, "s2_fwd": km2.fwd, "s2_bwd": km2.bwd}[which]
-    tp, perm = tab.signature_sorted()
+    tp, perm, masks = tab.signature_sorted()
     v = tab.view.cpu().numpy()
     sig = ((v >= 0).astype(np.int64) << np.arange(27)[:, None]).sum(0)
     expect = np.argsort(sig, kind="stable")
@@ -59,6 +59,17 @@ def test_signature_order_is_stable_sort(maps, which):
     tpn = tp.cpu().numpy()
     assert np.array_equal(tpn[:, :tab.n], v[:, expect])
     assert (tpn[:, tab.n:] == -1).all()
+    check_masks(masks, tpn, tab.n)
+    check_masks(tab.tile_masks(), v, tab.n)
+
+
+def check_masks(masks, table, n):
+    """masks[t] bit d == some row of 128-row tile t has a pair at offset d."""
+    has = table[:, :n] >= 0
+    pad = (-n) % 128
+    has = np.pad(has, ((0, 0), (0, pad))).reshape(27, -1, 128).any(-1)
+    expect = (has.astype(np.int64) << np.arange(27)[:, None]).sum(0)
+    assert np.array_equal(masks.cpu().numpy().astype(np.int64) & ((1 << 27) - 1), expect)
 
 
 @pytest.mark.parametrize("K,N", [(32, 32), (64, 64), (64, 128), (128, 64)])
@@ -88,7 +99,8 @@ def test_policy_sorts_sparse_tables_only(maps, monkeypatch):
     from paper_2407_01781_b200.conv import sig_sort_enabled
     _, _, (km1, _, _), (km2, _, _) = maps
     monkeypatch.delenv("FVDB_SIG_SORT", raising=False)
-    assert not sig_sort_enabled(km2.bwd)  # opt-in
+    assert sig_sort_enabled(km2.bwd) and km2.bwd.sparse  # transposed stride-2 table: sorted by default
+    assert not sig_sort_enabled(km2.fwd) and not sig_sort_enabled(km1.fwd)
     monkeypatch.setenv("FVDB_SIG_SORT", "1")
     assert km2.bwd.density() < 5 and sig_sort_enabled(km2.bwd)
     assert km1.fwd.density() > 15 and not sig_sort_enabled(km1.fwd)
@@ -106,3 +118,29 @@ def test_sorted_tiny_and_empty(sig_sort):
     kme = P.build_kernel_map(ge, ge, 1)
     ye = gather_conv(torch.zeros(0, 64, device="cuda", dtype=torch.bfloat16), kme.fwd, w, impl="gather")
     assert ye.shape == (0, 64)
+
+
+def test_masked_gather_equals_unmasked_and_oracle(maps, sig_sort):
+    """Tile masks only drop (super-tile, offset) stages without pairs: results are bitwise those of the
+    unmasked kernel (fvdb_conv_gather_tc), sorted or not, and match the oracle."""
+    from paper_2407_01781_b200 import _lib
+    g, gc, (km1, ins1, outs1), (km2, ins2, outs2) = maps
+    rng = np.random.default_rng(5)
+    for tab, K, N, tr, n_in, ref_fn in (
+            (km1.fwd, 64, 64, False, g.num_voxels,
+             lambda x, w: O.conv_igemm(bf16_round(x), bf16_round(w), ins1, outs1, g.num_voxels)),
+            (km2.bwd, 128, 64, True, gc.num_voxels,
+             lambda x, w: O.conv_backward(ins2, outs2, bf16_round(x), np.zeros((g.num_voxels, 64)),
+                                          bf16_round(w))[0])):
+        x = rng.normal(size=(n_in, K)).astype(np.float32)
+        w = (rng.normal(size=((K, N) if tr else (N, K)) + (3, 3, 3)) / np.sqrt(27 * K)).astype(np.float32)
+        xb, wt = torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(w).cuda()
+        img = pack_weights_umma(wt, tr, "gather")
+        plain = torch.empty((tab.n, N), dtype=torch.float32, device="cuda")
+        _lib.check(_lib.lib().fvdb_conv_gather_tc(xb.data_ptr(), n_in, K, img.data_ptr(), N, tab.t.data_ptr(), tab.ld,
+                                                  tab.n, plain.data_ptr(), _lib.DTYPE_F32, _lib.stream_ptr()), "plain")
+        for on in (False, True):
+            sig_sort(on)
+            y = gather_conv(xb, tab, wt, transpose=tr, out_dtype=torch.float32, w_image=img)
+            assert torch.equal(y, plain)
+        assert rel(plain, ref_fn(x, w)) < 2e-5
