@@ -121,7 +121,7 @@ class NbrTable:
     """
 
     __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
-                 "_masks", "sparse")
+                 "_masks", "sparse", "_steady")
 
     def __init__(self, t, n, colors_fn=None, counts=None):
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
@@ -132,6 +132,7 @@ class NbrTable:
         self._sorted = None
         self._masks = None
         self.sparse = False  # set for transposed stride-2 tables (<= 8 of 27 offsets per row)
+        self._steady = {}    # (K, N) -> steady_impl decision
 
     def density(self) -> float:
         """Mean pairs per output row (27 = every offset active); 27 when unknown."""
@@ -430,6 +431,30 @@ def sig_sort_enabled(nbr: "NbrTable") -> bool:
     return nbr.sparse
 
 
+HALO_MIN_DENSITY_WIDE = 18.0  # N >= 128: below this many mean pairs per row the sorted gather beats the halo
+
+
+def steady_impl(nbr: "NbrTable", K: int, N: int) -> tuple:
+    """(kernel, sorted) that ``auto`` runs for a reused table, decided once per (table, K, N).
+
+    Measured on B200 (tools/sigsort_bench.py GRID=1, ms per conv):
+    - the halo kernel wins everywhere at N <= 64, e.g. shell 64x64 0.34 vs 0.61 and LiDAR 64x64 0.068 vs
+      0.100, and on dense maps at N = 128: shell 64x128 0.48 vs 0.70;
+    - the signature-sorted, offset-masked gather wins at N = 128 on sparser maps, where the halo ring is
+      2 stages deep and most lanes are empty: LiDAR 128x128 at 9.2 pairs/row 0.131 vs 0.166, cfg4's
+      stride-2 64x128 at 16.6 pairs/row 0.164 vs 0.223.
+    Sparse tables (``sig_sort_enabled``) always take the sorted gather.
+    """
+    d = nbr._steady.get((K, N))
+    if d is None:
+        if sig_sort_enabled(nbr) or (N >= 128 and nbr.density() < HALO_MIN_DENSITY_WIDE):
+            d = ("gather", True)
+        else:
+            d = ("halo", False)
+        nbr._steady[(K, N)] = d
+    return d
+
+
 def conv_impl() -> str:
     """Tensor-core conv kernel policy, env FVDB_CONV_IMPL:
 
@@ -520,9 +545,9 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
         impl = _image_impl(w_image, K, N)  # the image decides
     else:
         impl = impl or conv_impl()
-        if impl == "auto":  # sparse tables stay on the signature-sorted, offset-masked gather kernel
+        if impl == "auto":  # first uses: gather; reused tables: steady_impl (halo or sorted gather)
             reuse = nbr.uses >= HALO_AFTER_USES or nbr.has_plan(K, N)
-            impl = "halo" if reuse and not sig_sort_enabled(nbr) else "gather"
+            impl = steady_impl(nbr, K, N)[0] if reuse else "gather"
     nbr.uses += 1
     img = w_image if w_image is not None else pack_weights_umma(w, transpose, impl)
     out = torch.empty((n_out, N), dtype=out_dtype, device=x.device)
@@ -535,7 +560,7 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
     else:
         # the kernel walks only the offsets present in each super-tile (tile masks); sparse tables are
         # signature-sorted first so that tiles are homogeneous and most offsets drop out
-        if sig_sort_enabled(nbr):
+        if sig_sort_enabled(nbr) or nbr._steady.get((K, N), (None, False))[1]:
             tab, perm, masks = nbr.signature_sorted()
         else:
             tab, perm, masks = nbr.t, None, nbr.tile_masks()

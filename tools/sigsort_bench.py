@@ -38,7 +38,17 @@ def main():
     gc = P.coarsen(g, 2)
     km2 = P.build_kernel_map(g, gc, 2)
     km1 = P.build_kernel_map(g, g, 1)
-    cases = [("cfg4_down_fwd", km2.fwd, 64, 128, False, g.num_voxels),
+    from paper_2407_01781_b200.workloads import lidar_scan_points
+    g3, _ = P.build_from_points(lidar_scan_points(0), P.VoxelTransform.uniform(0.05))
+    km3 = P.build_kernel_map(g3, g3, 1)
+    import os as _os
+    if _os.environ.get("GRID") == "1":  # density x channel-width grid for the conv-kernel policy
+        cases = [(f"shell_s1_{k}x{n}", km1.fwd, k, n, False, g.num_voxels) for k, n in ((128, 128), (64, 128), (128, 64), (32, 32), (32, 64))]
+        cases += [(f"lidar_s1_{k}x{n}", km3.fwd, k, n, False, g3.num_voxels) for k, n in ((64, 64), (32, 32), (64, 128))]
+    else:
+        cases = []
+    cases += [("cfg3_lidar_fwd", km3.fwd, 128, 128, False, g3.num_voxels),
+             ("cfg4_down_fwd", km2.fwd, 64, 128, False, g.num_voxels),
              ("cfg4_up_T", km2.bwd, 128, 64, True, gc.num_voxels),
              ("cfg2_s1", km1.fwd, 64, 64, False, g.num_voxels)]
     for name, tab, K, N, tr, n_in in cases:
