@@ -131,6 +131,11 @@ struct HaloCfg {
     static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4) + ROWB;  // + one zero row
     static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, N, false, false);
     static_assert(fits(NSL, BATCH) && CAP >= 256, "halo capacity must hold one offset phase (2 x 128 slots)");
+    // One issuer, one ring: the two builder halves take alternate batches.  With a single slot, a half would
+    // wait for the slot's use u+2 while use u may still be in flight, and an mbarrier parity wait cannot tell
+    // phase u+1 from phase u-1 (measured: wrong results).  With >= 2 slots every builder wait is at most one
+    // phase ahead (NSL = 2: each half owns a slot; NSL >= 3: chained through the previous slot's release).
+    static_assert(!ONE || NSL >= 2, "single-issuer ring needs >= 2 slots");
     static_assert(27 + BATCH - 1 <= kImgExt, "weight batch wraps past the extended image array");
     // builder warps per (half, lane quarter), building alternate stages of a batch (K=128 builders hold
     // 64 data registers: one per slot keeps them within the register budget)
