@@ -89,37 +89,39 @@ __global__ void k_neighbor_leaves(fvdb_grid_view gin, fvdb_grid_view gout, int s
     }
 }
 
-// CTA per output leaf: 27 probes per active voxel against staged neighbour-leaf masks
-__global__ void __launch_bounds__(kThreads) k_kernel_map(fvdb_grid_view gin, fvdb_grid_view gout, int stride,
-                                                         const int32_t* __restrict__ nleaf,
-                                                         int32_t* __restrict__ nbr, int64_t ld,
-                                                         unsigned long long* __restrict__ pair_counts) {
+// CTA per output leaf: 27 probes per active voxel against staged neighbour-leaf masks.  Nine warps own three
+// offsets each and their lanes walk the leaf's voxels (no per-item division; each offset row is written
+// coalesced); per-offset pair counts are warp reductions stored per leaf (partial[d][leaf]) and summed by
+// k_pair_counts, instead of shared + global atomics on 27 addresses.
+constexpr int kKmWarps = 9, kKmThreads = kKmWarps * 32;
+__global__ void __launch_bounds__(kKmThreads) k_kernel_map(fvdb_grid_view gin, fvdb_grid_view gout, int stride,
+                                                           const int32_t* __restrict__ nleaf,
+                                                           int32_t* __restrict__ nbr, int64_t ld,
+                                                           int32_t* __restrict__ partial) {
     __shared__ uint64_t s_mask[27][8];
     __shared__ uint64_t s_pre[27];
     __shared__ int64_t s_vo[27];
     __shared__ int32_t s_nl[27];
     __shared__ uint16_t s_pos[512];
-    __shared__ int s_cnt[27];
     __shared__ uint64_t s_own[8];
 
     const int64_t l = blockIdx.x;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid < 27) {
         int32_t nl = nleaf[l * 27 + tid];
         s_nl[tid] = nl;
-        s_cnt[tid] = 0;
         s_pre[tid] = nl >= 0 ? gin.leaf_prefix[nl] : 0;
         s_vo[tid] = nl >= 0 ? (int64_t)gin.leaf_value_offset[nl] - 1 : 0;
     }
     if (tid < 8) s_own[tid] = gout.leaf_masks[8 * l + tid];
-    for (int q = tid; q < 27 * 8; q += kThreads) {
+    for (int q = tid; q < 27 * 8; q += kKmThreads) {
         int e = q >> 3;
         int32_t nl = nleaf[l * 27 + e];
         s_mask[e][q & 7] = nl >= 0 ? gin.leaf_masks[8 * (int64_t)nl + (q & 7)] : 0ull;
     }
     __syncthreads();
     const uint64_t own_pre = gout.leaf_prefix[l];
-    for (uint32_t m = tid; m < 512; m += kThreads)
+    for (uint32_t m = tid; m < 512; m += kKmThreads)
         if ((s_own[m >> 6] >> (m & 63)) & 1ull) s_pos[leaf_rank(s_own, own_pre, m)] = (uint16_t)m;
     int nvox = 0;
 #pragma unroll
@@ -127,27 +129,48 @@ __global__ void __launch_bounds__(kThreads) k_kernel_map(fvdb_grid_view gin, fvd
     __syncthreads();
 
     const int64_t row0 = (int64_t)gout.leaf_value_offset[l] - 1;
-    const int items = 27 * nvox;
-    for (int f = tid; f < items; f += kThreads) {
-        int d = f / nvox;
-        int r = f - d * nvox;
-        uint32_t m = s_pos[r];
-        int qx = stride * (int)(m >> 6) + (d / 9 - 1);
-        int qy = stride * (int)((m >> 3) & 7) + ((d / 3) % 3 - 1);
-        int qz = stride * (int)(m & 7) + (d % 3 - 1);
-        int e = ((qx >> 3) + 1) * 9 + ((qy >> 3) + 1) * 3 + ((qz >> 3) + 1);
-        int32_t row = -1;
-        if (s_nl[e] >= 0) {
-            uint32_t b = (uint32_t)(((qx & 7) << 6) | ((qy & 7) << 3) | (qz & 7));
-            if ((s_mask[e][b >> 6] >> (b & 63)) & 1ull) {
-                row = (int32_t)(s_vo[e] + leaf_rank(s_mask[e], s_pre[e], b));
-                atomicAdd(&s_cnt[d], 1);
+    const int64_t n_leaf = gout.num_leaf;
+#pragma unroll
+    for (int j = 0; j < 27 / kKmWarps; ++j) {
+        const int d = warp + j * kKmWarps;
+        const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
+        int32_t* out = nbr + (int64_t)d * ld + row0;
+        int cnt = 0;
+        for (int r = lane; r < nvox; r += 32) {
+            const uint32_t m = s_pos[r];
+            const int qx = stride * (int)(m >> 6) + dx;
+            const int qy = stride * (int)((m >> 3) & 7) + dy;
+            const int qz = stride * (int)(m & 7) + dz;
+            const int e = ((qx >> 3) + 1) * 9 + ((qy >> 3) + 1) * 3 + ((qz >> 3) + 1);
+            int32_t row = -1;
+            if (s_nl[e] >= 0) {
+                const uint32_t b = (uint32_t)(((qx & 7) << 6) | ((qy & 7) << 3) | (qz & 7));
+                if ((s_mask[e][b >> 6] >> (b & 63)) & 1ull) {
+                    row = (int32_t)(s_vo[e] + leaf_rank(s_mask[e], s_pre[e], b));
+                    ++cnt;
+                }
             }
+            out[r] = row;
         }
-        nbr[(int64_t)d * ld + row0 + r] = row;
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) partial[(int64_t)d * n_leaf + l] = cnt;
     }
+}
+
+// pair_counts[d] = sum over output leaves of partial[d][leaf]   (one CTA per offset)
+__global__ void k_pair_counts(const int32_t* __restrict__ partial, int64_t n_leaf, int64_t* __restrict__ counts) {
+    __shared__ long long s_sum[8];
+    const int d = blockIdx.x;
+    long long acc = 0;
+    for (int64_t i = threadIdx.x; i < n_leaf; i += blockDim.x) acc += partial[(int64_t)d * n_leaf + i];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = acc;
     __syncthreads();
-    if (tid < 27 && s_cnt[tid]) atomicAdd(&pair_counts[tid], (unsigned long long)s_cnt[tid]);
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_sum[w];
+        counts[d] = t;
+    }
 }
 
 // padding columns [n_out, ld) of every offset row := -1
@@ -226,7 +249,8 @@ extern "C" int fvdb_active_coords(const fvdb_grid_view* g, int64_t* out, void* s
 }
 
 extern "C" size_t fvdb_kmap_workspace_bytes(int64_t num_leaf_out) {
-    return (size_t)(num_leaf_out > 0 ? num_leaf_out : 1) * 27 * sizeof(int32_t) + 256;
+    // neighbour leaves [leaf][27] + per-leaf pair counts [27][leaf]
+    return 2 * ((size_t)(num_leaf_out > 0 ? num_leaf_out : 1) * 27 * sizeof(int32_t) + 256);
 }
 
 extern "C" int fvdb_kernel_map(const fvdb_grid_view* gin, const fvdb_grid_view* gout, int stride, int32_t* nbr,
@@ -235,14 +259,18 @@ extern "C" int fvdb_kernel_map(const fvdb_grid_view* gin, const fvdb_grid_view* 
     if (stride != 1 && stride != 2) return FVDB_ERR_INVALID;
     if (ld < gout->num_voxels) return FVDB_ERR_INVALID;
     if (ws_bytes < fvdb_kmap_workspace_bytes(gout->num_leaf)) return FVDB_ERR_WORKSPACE;
-    FVDB_CUDA_TRY(cudaMemsetAsync(pair_counts, 0, 27 * sizeof(int64_t), st));
     if (ld > gout->num_voxels)
         k_pad<<<grid_for(27 * (ld - gout->num_voxels)), kThreads, 0, st>>>(nbr, ld, gout->num_voxels);
-    if (gout->num_leaf == 0) return FVDB_OK;
+    if (gout->num_leaf == 0) {
+        FVDB_CUDA_TRY(cudaMemsetAsync(pair_counts, 0, 27 * sizeof(int64_t), st));
+        return FVDB_OK;
+    }
     int32_t* nleaf = reinterpret_cast<int32_t*>(ws);
+    int32_t* partial = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(ws) +
+                                                  ((size_t)gout->num_leaf * 27 * sizeof(int32_t) + 255) / 256 * 256);
     k_neighbor_leaves<<<grid_for(gout->num_leaf * 27), kThreads, 0, st>>>(*gin, *gout, stride, nleaf);
-    k_kernel_map<<<(unsigned)gout->num_leaf, kThreads, 0, st>>>(
-        *gin, *gout, stride, nleaf, nbr, ld, reinterpret_cast<unsigned long long*>(pair_counts));
+    k_kernel_map<<<(unsigned)gout->num_leaf, kKmThreads, 0, st>>>(*gin, *gout, stride, nleaf, nbr, ld, partial);
+    k_pair_counts<<<27, 256, 0, st>>>(partial, gout->num_leaf, pair_counts);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
