@@ -314,14 +314,26 @@ class KernelMap:
     def bwd(self) -> NbrTable:
         """Transposed table nbrT[d][i] = o iff nbr[d][o] = i (dgrad / transposed conv), cached."""
         if self._bwd is None:
-            t = torch.empty((27, padded_len(self.num_in)), dtype=torch.int32, device=self.device)
-            L = _lib.lib()
-            _lib.check(L.fvdb_kmap_transpose(self.fwd.t.data_ptr(), self.fwd.ld, self.num_out, self.num_in,
-                                             t.data_ptr(), t.shape[1], _lib.stream_ptr()), "kmap_transpose")
+            if self._same_grids():
+                # stride 1 onto the same grid: nbr[d][o] = i  <=>  nbr[26 - d][i] = o (the mirrored offset),
+                # so the transposed table is the forward table with its offset rows reversed (a contiguous
+                # copy instead of the scatter; padding columns are -1 in every row)
+                t = torch.flip(self.fwd.t, dims=[0])
+            else:
+                t = torch.empty((27, padded_len(self.num_in)), dtype=torch.int32, device=self.device)
+                L = _lib.lib()
+                _lib.check(L.fvdb_kmap_transpose(self.fwd.t.data_ptr(), self.fwd.ld, self.num_out, self.num_in,
+                                                 t.data_ptr(), t.shape[1], _lib.stream_ptr()), "kmap_transpose")
             self._bwd = NbrTable(t, self.num_in, self._bwd_colors if self._grids is not None else None,
                                  counts=self._counts)
             self._bwd.sparse = self.stride == 2  # fine voxel i pairs only offsets d with i - d even: <= 8 of 27
         return self._bwd
+
+    def _same_grids(self):
+        if self.stride != 1 or self._grids is None or self.num_in != self.num_out:
+            return False
+        gi, go = self._grids
+        return len(gi) == len(go) and all(a is b for a, b in zip(gi, go))
 
     def transposed_table(self):
         return self.bwd.view

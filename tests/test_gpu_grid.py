@@ -193,3 +193,21 @@ def test_cfg3_lidar_counts(golden_sizes):
         g, _ = P.build_from_points(lidar_scan_points(ref["seed"]), P.VoxelTransform.uniform(0.05))
         assert list(g.counts) == ref["counts"]
         assert P.build_kernel_map(g, g, 1).total_pairs == ref["pairs"]
+
+
+@pytest.mark.parametrize("name", KMAP_CASES)
+def test_same_grid_transpose_by_row_reversal_is_exact(golden_grids, name):
+    """Stride-1 maps of a grid onto itself build the transposed table by reversing the offset rows
+    (nbr[d][o] = i <=> nbr[26-d][i] = o): bit-identical to the scatter transpose (fvdb_kmap_transpose)."""
+    from paper_2407_01781_b200 import _lib
+    from paper_2407_01781_b200.conv import padded_len
+    key = f"{name}/active_coords"
+    if key not in golden_grids:
+        pytest.skip("no coordinates in this golden case")
+    c = golden_grids[key]
+    g, _ = P.build_from_coords(c)
+    km = P.build_kernel_map(g, g, 1)
+    t = torch.empty((27, padded_len(g.num_voxels)), dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().fvdb_kmap_transpose(km.fwd.t.data_ptr(), km.fwd.ld, km.num_out, km.num_in, t.data_ptr(),
+                                              t.shape[1], _lib.stream_ptr()), "kmap_transpose")
+    assert km._same_grids() and torch.equal(km.bwd.t, t)
