@@ -31,6 +31,23 @@ import sys
 import threading
 import time
 
+# The reference arm (the oracle port: numpy + OpenBLAS) runs with every host thread the process may use.
+# torchrun exports OMP_NUM_THREADS=1 to each rank, which OpenBLAS reads when numpy loads, so override it
+# before the import.
+HOST_THREADS = len(os.sched_getaffinity(0))
+
+
+def _reference_arm(argv) -> bool:
+    for i, a in enumerate(argv):
+        if a == "--impl=reference" or (a == "--impl" and i + 1 < len(argv) and argv[i + 1] == "reference"):
+            return True
+    return False
+
+
+if _reference_arm(sys.argv):
+    for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[_v] = str(HOST_THREADS)
+
 import numpy as np
 
 ROOT = pathlib.Path(__file__).resolve().parent
@@ -536,7 +553,7 @@ def cpu_baseline(cfg, coords, points, args, frac=1 / 64, repeats=3):
         O.conv_igemm(f, w, si, so, lim)
         O.conv_backward(si, so, go, f, w)
         best = min(best, time.perf_counter() - t0)
-    return {"value": round(lim / best, 1), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+    return {"value": round(lim / best, 1), "unit": UNIT, "cores": HOST_THREADS, "kind": "port",
             "sample": f"first {lim} of {n} output voxels ({frac:.4f} of the grid, leaf-aligned index prefix), "
                       f"{sum(len(o) for o in so)} pairs, fp32 igemm fwd + conv_backward, best of {repeats}",
             "seconds_per_sample": round(best, 4)}
@@ -578,7 +595,7 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: {cfg['desc']}", "voxels": n, "cin": cin, "cout": cout},
-        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": HOST_THREADS, "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
