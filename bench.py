@@ -433,7 +433,7 @@ def run_e2e(args, P, torch, dist, grid, km, cin, cout, dev, use_dist):
     gb._kmaps[(id(gb), 1)] = km
     m = P.SparseConv3d(cin, cout).to(dev)
     rng = np.random.default_rng(7)
-    steps = args.e2e_steps or max(3, min(args.steps, 20))
+    steps = args.e2e_steps or max(3, min(args.steps, 50))  # long enough that pipeline fill / drain amortise
     x_h = [torch.from_numpy(rng.normal(size=(n, cin)).astype(np.float32)).pin_memory() for _ in range(2)]
     gy_h = [torch.from_numpy(rng.normal(size=(n, cout)).astype(np.float32)).pin_memory() for _ in range(2)]
     w_h = [m.weight.detach().cpu().pin_memory() for _ in range(2)]
