@@ -31,6 +31,7 @@ STENCIL = np.stack(np.meshgrid(_R, _R, _R, indexing="ij"), axis=-1).reshape(-1, 
 LGGS_BLOCK = 64
 LGGS_PAD = 16
 TC_CHANNELS = (32, 64, 128)  # channel counts the tcgen05 kernels are instantiated for
+SIMT_MAX_N = 256  # exact-precision gather kernel: output channels per launch (fvdb_conv_gather_simt)
 
 
 def _to_device_tensor(x, device, dtype=None):
@@ -532,6 +533,23 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
     K, N = (cout, cin) if transpose else (cin, cout)
     if x.shape[1] != K:
         raise ValueError(f"feature channels {x.shape[1]} != kernel K {K}")
+    # channel blocking beyond the kernels' widths (the reference takes any channel count): output channels
+    # in column blocks, bf16 input channels in K blocks summed in fp32
+    n_max = TC_CHANNELS[-1] if x.dtype == torch.bfloat16 else SIMT_MAX_N
+    if N > n_max:
+        parts = []
+        for n0 in range(0, N, n_max):
+            ws = w[:, n0:n0 + n_max] if transpose else w[n0:n0 + n_max]
+            parts.append(gather_conv(x, nbr, ws, transpose, out_dtype, impl=impl))
+        return torch.cat(parts, 1)
+    if x.dtype == torch.bfloat16 and K > TC_CHANNELS[-1]:
+        kb = TC_CHANNELS[-1]
+        acc = None
+        for k0 in range(0, K, kb):
+            ws = w[k0:k0 + kb] if transpose else w[:, k0:k0 + kb]
+            y = gather_conv(x[:, k0:k0 + kb], nbr, ws, transpose, torch.float32, impl=impl)
+            acc = y if acc is None else acc + y
+        return acc.to(out_dtype or torch.bfloat16)
     L = _lib.lib()
     st = _lib.stream_ptr()
     x = x.contiguous()
@@ -586,6 +604,13 @@ def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: NbrTable) -> torch.Tensor:
     """gw[co][ci][d] = Σ_o go[o,co]·x[nbr[d][o],ci]  → [Cout, Cin, 3, 3, 3] (fp32 for bf16 inputs)."""
     n_out = nbr.n
     cin, cout = int(x.shape[1]), int(go.shape[1])
+    if x.dtype == torch.bfloat16 and max(cin, cout) > TC_CHANNELS[-1]:  # channel blocks (independent)
+        b = TC_CHANNELS[-1]
+        gw = torch.empty((cout, cin, 3, 3, 3), dtype=torch.float32, device=x.device)
+        for c0 in range(0, cout, b):
+            for i0 in range(0, cin, b):
+                gw[c0:c0 + b, i0:i0 + b] = wgrad(x[:, i0:i0 + b], go[:, c0:c0 + b], nbr)
+        return gw
     L = _lib.lib()
     st = _lib.stream_ptr()
     x, go = x.contiguous(), go.contiguous()

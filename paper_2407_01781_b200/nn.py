@@ -59,10 +59,6 @@ class _SparseConvFn(torch.autograd.Function):
         return gx, gw, None, None, None
 
 
-def _tc_ok(w):
-    return int(w.shape[0]) in (32, 64, 128) and int(w.shape[1]) in (32, 64, 128)
-
-
 def coarsen_batch(batch: GridBatch, factor: int = 2) -> GridBatch:
     key = ("coarse", factor)
     cached = batch._kmaps.get(key)

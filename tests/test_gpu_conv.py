@@ -354,3 +354,30 @@ def test_simt_tiled_shapes_match_oracle(shell, cin, cout):
         xt, wt, gyt = (torch.from_numpy(a).cuda().to(dt) for a in (x, w, gy))
         assert rel(gather_conv(xt, km.fwd, wt), ref) < tol
         assert rel(gather_conv(gyt, km.bwd, wt, transpose=True), gi_ref) < tol
+
+
+def test_wide_channels_blocked(shell):
+    """Channel counts beyond the kernels' widths (the reference takes any): bf16 192 -> 256 through K / N
+    blocks (fwd, dgrad, wgrad) and fp32 / f64 with N = 300 through column blocks, against the oracle."""
+    g, _, ins, outs, km = shell
+    n = g.num_voxels
+    rng = np.random.default_rng(77)
+    cin, cout = 192, 256
+    x = rng.normal(size=(n, cin)).astype(np.float32)
+    w = (rng.normal(size=(cout, cin, 3, 3, 3)) / np.sqrt(27 * cin)).astype(np.float32)
+    gy = rng.normal(size=(n, cout)).astype(np.float32)
+    xb, gyb = (torch.from_numpy(a).cuda().to(torch.bfloat16) for a in (x, gy))
+    wt = torch.from_numpy(w).cuda()
+    y = gather_conv(xb, km.fwd, wt, out_dtype=torch.float32)
+    assert y.shape == (n, cout) and rel(y, O.conv_igemm(bf16_round(x), bf16_round(w), ins, outs, n)) < 2e-5
+    gi_r, gw_r = O.conv_backward(ins, outs, bf16_round(gy), bf16_round(x), bf16_round(w))
+    gi = gather_conv(gyb, km.bwd, wt, transpose=True, out_dtype=torch.float32)
+    assert gi.shape == (n, cin) and rel(gi, gi_r) < 2e-5
+    gw = wgrad(xb, gyb, km.fwd)
+    assert gw.shape == (cout, cin, 3, 3, 3) and rel(gw, gw_r) < 2e-5
+    x2 = rng.normal(size=(n, 20))
+    w2 = rng.normal(size=(300, 20, 3, 3, 3)) / np.sqrt(27 * 20)
+    ref2 = O.conv_igemm(x2, w2, ins, outs, n)
+    for dt, tol in ((torch.float64, 1e-10), (torch.float32, 1e-5)):
+        y2 = gather_conv(torch.from_numpy(x2).cuda().to(dt), km.fwd, torch.from_numpy(w2).cuda().to(dt))
+        assert y2.shape == (n, 300) and rel(y2, ref2) < tol
