@@ -33,20 +33,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-// try_wait with a suspend-time hint: the thread sleeps until the phase completes (or the hint
-// expires) instead of re-polling, so waiting warps do not steal issue slots from the warps they
-// share a sub-partition with
-__device__ __forceinline__ bool mbar_try_wait_sus(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity), "r"(1000000u)
-        : "memory");
-    return ok != 0;
-}
 // non-blocking probe of a phase (mbarrier.test_wait): issue it early, consume the result later, so the
 // ~300-cycle mbarrier round trip overlaps other work (a wait on an already-completed phase still costs it)
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
@@ -67,14 +53,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         if (++n == (1u << 24)) asm volatile("trap;");
     }
 }
-// same, suspending between polls (for warps that share sub-partitions with critical-path warps)
-__device__ __forceinline__ void mbar_wait_sus(uint32_t bar, uint32_t parity) {
-    uint32_t n = 0;
-    while (!mbar_try_wait_sus(bar, parity)) {
-        if (++n == (1u << 20)) asm volatile("trap;");
-    }
-}
-
 // wait for warps that are off the critical path (epilogue, loaders): back off with
 // nanosleep so idle waiters do not steal MIO issue slots from the gather warps
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns = 256) {
