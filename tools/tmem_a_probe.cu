@@ -239,18 +239,7 @@ extern "C" int probe_rate(int n, int iters, int mode, long long* cycles, float* 
     return (int)cudaGetLastError();
 }
 
-// ---- cost of waiting on an already-completed mbarrier phase: try_wait vs test_wait
-__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
+// ---- cost of waiting on an already-completed mbarrier phase: try_wait vs test_wait (mbar_test: tc_ptx.cuh)
 __global__ void k_wait_cost(int iters, long long* out) {
     __shared__ __align__(8) uint64_t bar;
     if (threadIdx.x == 0) {
