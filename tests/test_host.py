@@ -123,3 +123,33 @@ def test_choose_variant_thresholds_match_reference():
     assert P.choose_variant(G(0.1), 8, 16) == "igemm"
     assert P.choose_variant(G(0.3), 32, 32) == "leaf"
     assert P.choose_variant(G(0.3), 64, 64) == "igemm"
+
+
+def _table(n, pairs_per_row, sparse=False):
+    from paper_2407_01781_b200.conv import NbrTable
+    t = NbrTable(torch.full((27, 512), -1, dtype=torch.int32), n,
+                 counts=torch.full((27,), int(round(pairs_per_row * n / 27)), dtype=torch.int64))
+    t.sparse = sparse
+    return t
+
+
+def test_conv_kernel_policy_host_logic(monkeypatch):
+    """steady_impl / sig_sort_enabled (conv.py): the kernel a reused table settles on, from its density, the
+    layer width and the sparse flag (transposed stride-2 tables); FVDB_SIG_SORT overrides."""
+    from paper_2407_01781_b200.conv import HALO_MIN_DENSITY_WIDE, sig_sort_enabled, steady_impl
+    monkeypatch.delenv("FVDB_SIG_SORT", raising=False)
+    dense, lidar = _table(270, 20.85), _table(270, 9.23)
+    assert steady_impl(dense, 64, 64) == ("halo", False)
+    assert steady_impl(dense, 64, 128) == ("halo", False)         # dense wide layer: halo
+    assert steady_impl(lidar, 64, 64) == ("halo", False)          # sparse narrow layer: halo
+    assert steady_impl(lidar, 128, 128) == ("gather", True)       # sparse wide layer: sorted gather
+    assert steady_impl(_table(270, HALO_MIN_DENSITY_WIDE - 1), 64, 128) == ("gather", True)
+    sp = _table(270, 3.1, sparse=True)
+    assert sig_sort_enabled(sp) and steady_impl(sp, 128, 64) == ("gather", True)
+    assert not sig_sort_enabled(lidar)
+    monkeypatch.setenv("FVDB_SIG_SORT", "0")
+    assert not sig_sort_enabled(sp)
+    monkeypatch.setenv("FVDB_SIG_SORT", "1")
+    assert sig_sort_enabled(lidar) and not sig_sort_enabled(dense)
+    monkeypatch.setenv("FVDB_SIG_SORT", "force")
+    assert sig_sort_enabled(dense)
