@@ -210,8 +210,8 @@ typedef struct fvdb_halo_plan {
 int fvdb_parity_colors(const int64_t* coords, int64_t n, int shift, uint8_t* color, void* stream);
 /* halo capacity (slots per phase) of the conv kernel for K input / N output channels; 0 = unsupported.
  * It depends on the kernel's MMA-issue layout (one issuer by default; env FVDB_HALO_VARIANT=0 selects two
- * half-pipelines for profiling): a plan built for one layout's capacity is rejected (FVDB_ERR_INVALID) by
- * the other if the layout changes in between. */
+ * half-pipelines for profiling).  fvdb_conv_halo_tc rejects (FVDB_ERR_INVALID) a plan whose capacity exceeds
+ * the running layout's; a plan built for a smaller capacity runs unchanged. */
 int fvdb_halo_cap(int K, int N);
 /* count pass: writes tile_level, tile_base, phase; total slots -> *total (host). Synchronizes. */
 size_t fvdb_halo_plan_workspace_bytes(int64_t n_out);
