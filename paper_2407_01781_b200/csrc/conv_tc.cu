@@ -277,25 +277,24 @@ __global__ void __launch_bounds__(fwd_threads(NPW), 1)
                     tmem_ld32(ta, v);
                     tmem_ld_wait();
                     tmem_st32_zero(ta);  // reset for the next super-tile using this buffer
-                    if (row < n_out && !(dbg & 2)) {
+                    if (row < n_out && !(dbg & 2)) {  // full 32-byte sectors per thread (256-bit stores)
                         if constexpr (OUT_BF16) {
-                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(out) + row * N + c0);
+                            uint8_t* dst = reinterpret_cast<uint8_t*>(reinterpret_cast<bf16*>(out) + row * N + c0);
+                            uint32_t p[16];
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                uint32_t p[4];
-#pragma unroll
-                                for (int h = 0; h < 4; ++h) {
-                                    __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2 * h]),
-                                                                              __uint_as_float(v[8 * j + 2 * h + 1]));
-                                    p[h] = *reinterpret_cast<uint32_t*>(&b2);
-                                }
-                                dst[j] = make_uint4(p[0], p[1], p[2], p[3]);
+                            for (int h = 0; h < 16; ++h) {
+                                __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[2 * h]),
+                                                                          __uint_as_float(v[2 * h + 1]));
+                                p[h] = *reinterpret_cast<uint32_t*>(&b2);
                             }
+                            stg256(dst, p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7]);
+                            stg256(dst + 32, p[8], p[9], p[10], p[11], p[12], p[13], p[14], p[15]);
                         } else {
-                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<float*>(out) + row * N + c0);
+                            uint8_t* dst = reinterpret_cast<uint8_t*>(reinterpret_cast<float*>(out) + row * N + c0);
 #pragma unroll
-                            for (int j = 0; j < 8; ++j)
-                                dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                            for (int j = 0; j < 4; ++j)
+                                stg256(dst + 32 * j, v[8 * j], v[8 * j + 1], v[8 * j + 2], v[8 * j + 3], v[8 * j + 4],
+                                       v[8 * j + 5], v[8 * j + 6], v[8 * j + 7]);
                         }
                     }
                 }
