@@ -340,8 +340,8 @@ struct WgCfg {
     static constexpr int NACC = NACC0 < 8 ? NACC0 : 8;         // M-blocks (TMEM accumulators) per CTA
     static constexpr int OFFS = NACC * OPB;                    // offsets per CTA
     static constexpr int GROUPS = (27 + OFFS - 1) / OFFS;
-    // output rows (MMA K) per stage.  16 (twice the stages in flight) measured slower: the per-stage
-    // fixed cost in the MMA warps (wait, proxy fence, commit) dominates, not the stage round trip.
+    // output rows (MMA K) per stage.  16 (twice the stages in flight) measured slower, also after the
+    // prefetched barrier probe: wgrad 490 -> 457 TFLOP/s at cfg2, the per-stage fixed costs dominate.
     static constexpr int TK = 32;
     static constexpr int CHUNK = 128;                          // output rows per index block
     static constexpr int A_BLK = TK * 256;                     // one M-block: TK k-rows x 128 m (bf16)
@@ -479,21 +479,26 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const uint64_t adesc0 = smem_desc(base + C::B_BYTES, C::TK * 128, 1024, kSwizzle128B);
         const uint64_t bdesc0 = C::B_SW128 ? smem_desc(base, C::TK * 128, 1024, kSwizzle128B)
                                            : smem_desc(base, 64, 512, kSwizzle64B);
+
+        bool ready = false;  // this stage's full phase was already seen complete (prefetched test)
         for (int step = 0; step < n_steps; ++step) {
             const uint32_t s = step % C::STAGES, ph = (step / C::STAGES) & 1;
-            mbar_wait(smem_u32(&bar_full[s]), ph);
+            if (!ready) mbar_wait(smem_u32(&bar_full[s]), ph);
             fence_proxy_async_smem();
             tc_fence_after();
-            // whole warp runs the issue loop (warp-uniform operands); one elected lane issues
-            const uint32_t so = s * C::STAGE;
-            for (int a = a_lo; a < a_hi; ++a) {
-#pragma unroll
-                for (int ks = 0; ks < C::TK / 16; ++ks) {
-                    const uint64_t ad = adesc0 + ((so + a * C::A_BLK + ks * 2048) >> 4);
-                    const uint64_t bd = bdesc0 + ((so + (C::B_SW128 ? ks * 2048 : ks * 1024)) >> 4);
-                    if (!(dbg & 1)) mma_bf16_elect(tmem + a * COUT, ad, bd, C::IDESC, (step | ks) != 0);
-                }
+            {  // probe the next stage now (mbarrier round trip overlaps this stage's issue); the producer
+               // cannot refill it before both issuers committed its previous use, so the parity is unambiguous
+                const int sn = step + 1;
+                ready = sn < n_steps && mbar_test(smem_u32(&bar_full[sn % C::STAGES]), (sn / C::STAGES) & 1);
             }
+            // whole warp runs the issue loop (warp-uniform operands); one elected lane issues both K steps
+            const uint32_t so = s * C::STAGE;
+            const uint64_t bd = bdesc0 + (so >> 4);
+            static_assert(C::TK == 32, "the issue helper covers two K16 steps");
+            for (int a = a_lo; a < a_hi; ++a)
+                if (!(dbg & 1))
+                    mma_ss_x2_elect<C::B_SW128 ? 128 : 64>(tmem + a * COUT, adesc0 + ((so + a * C::A_BLK) >> 4), bd,
+                                                           C::IDESC, step != 0);
             mma_commit_elect(smem_u32(&bar_empty[s]));
         }
         mma_commit_elect(smem_u32(&bar_tfull));

@@ -224,6 +224,20 @@ __device__ __forceinline__ void mma_ts_x2_elect(uint32_t d, uint32_t a, uint64_t
         ::"r"(d), "r"(a), "l"(b), "r"(idesc), "n"(A1), "n"(B1)
         : "memory");
 }
+// Two SS MMAs (both K16 steps of a 32-deep stage) under one elect.sync: A advances 128 descriptor units
+// (2 KB), B advances BI; the first MMA accumulates iff acc0 != 0.
+template <int BI>
+__device__ __forceinline__ void mma_ss_x2_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a1, b1;\n\t"
+        "setp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+        "add.u64 a1, %1, 128;\n\tadd.u64 b1, %2, %5;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, p;\n\t}"
+        ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc0), "n"(BI)
+        : "memory");
+}
 __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
