@@ -521,10 +521,12 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = 0u;
                 }
-                if (u < n_off) {
-                    uint4* dst = reinterpret_cast<uint4*>(part + (((int64_t)split * 27 + d0 + u) * CIN + ci) * COUT + c0);
+                if (u < n_off) {  // 32-byte aligned: COUT multiple of 32 fp32, c0 multiple of 32
+                    uint8_t* dst = reinterpret_cast<uint8_t*>(part + (((int64_t)split * 27 + d0 + u) * CIN + ci) * COUT + c0);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    for (int j = 0; j < 4; ++j)
+                        stg256(dst + 32 * j, v[8 * j], v[8 * j + 1], v[8 * j + 2], v[8 * j + 3], v[8 * j + 4],
+                               v[8 * j + 5], v[8 * j + 6], v[8 * j + 7]);
                 }
             }
         }
