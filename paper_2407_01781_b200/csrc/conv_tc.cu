@@ -336,10 +336,12 @@ template <int CIN, int COUT>
 struct WgCfg {
     static constexpr int OPB = 128 / CIN;                      // offsets per M-block
     static constexpr int NMB = (27 + OPB - 1) / OPB;           // M-blocks for all offsets
-    static constexpr int NACC0 = (512 / COUT) < NMB ? (512 / COUT) : NMB;
-    static constexpr int NACC = NACC0 < 8 ? NACC0 : 8;         // M-blocks (TMEM accumulators) per CTA
+    static constexpr int NACC_MAX = (512 / COUT) < 8 ? (512 / COUT) : 8;  // TMEM columns, A stage size
+    static constexpr int GROUPS = (NMB + NACC_MAX - 1) / NACC_MAX;       // CTAs per row range
+    // M-blocks (TMEM accumulators) per CTA, balanced over the groups: the group with the most offsets is the
+    // critical path (all CTAs are co-resident), so 27 offsets at Cin 64 split 14 + 13, not 16 + 11
+    static constexpr int NACC = (NMB + GROUPS - 1) / GROUPS;
     static constexpr int OFFS = NACC * OPB;                    // offsets per CTA
-    static constexpr int GROUPS = (27 + OFFS - 1) / OFFS;
     // output rows (MMA K) per stage.  16 (twice the stages in flight) measured slower, also after the
     // prefetched barrier probe: wgrad 490 -> 457 TFLOP/s at cfg2, the per-stage fixed costs dominate.
     static constexpr int TK = 32;
@@ -470,6 +472,11 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 for (int u = 0; u < nc; ++u)
                     bulk_g2s(ibase + islot * C::IDX_BYTES + u * C::CHUNK * 4,
                              nbr + (int64_t)(d0 + u) * ld + o_begin + (int64_t)ch * C::CHUNK, C::CHUNK * 4, fb);
+                if (dbg & 8) {  // grad_out rows of the chunk after this one into L2 ahead of their cp.async
+                    const int64_t p0 = o_begin + (int64_t)(ch + 1) * C::CHUNK;
+                    const int64_t p1 = (p0 + C::CHUNK) < o_end ? (p0 + C::CHUNK) : o_end;
+                    if (p1 > p0) bulk_prefetch_l2(go + p0 * COUT, (uint32_t)((p1 - p0) * COUT * 2));
+                }
             }
         }
     } else if (warp == 5 || warp == 10) {
@@ -655,7 +662,7 @@ struct WgLaunch {
         rps = ceil_div(rps, C::CHUNK) * C::CHUNK;
         auto kern = k_wgrad_tc<CIN, COUT>;
         FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        // profiling switches (FVDB_DEBUG_WG): 1 no MMA, 2 no A gather, 4 one index row per chunk
+        // profiling switches (FVDB_DEBUG_WG): 1 no MMA, 2 no A gather, 4 one index row per chunk, 8 L2 prefetch
         static const int dbg = getenv("FVDB_DEBUG_WG") ? atoi(getenv("FVDB_DEBUG_WG")) : 0;
         kern<<<splits * C::GROUPS, kWgThreads, C::SMEM, st>>>((const bf16*)in, (const bf16*)go, nbr, ld, n_out, rps,
                                                               part, dbg);
