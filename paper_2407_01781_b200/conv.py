@@ -122,7 +122,7 @@ class NbrTable:
     """
 
     __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
-                 "_masks", "sparse", "_steady")
+                 "_masks", "sparse", "_steady", "_pairs")
 
     def __init__(self, t, n, colors_fn=None, counts=None):
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
@@ -134,6 +134,7 @@ class NbrTable:
         self._masks = None
         self.sparse = False  # set for transposed stride-2 tables (<= 8 of 27 offsets per row)
         self._steady = {}    # (K, N) -> steady_impl decision
+        self._pairs = None   # (pin, pout, seg, padded total): per-offset pair lists (wgrad)
 
     def density(self) -> float:
         """Mean pairs per output row (27 = every offset active); 27 when unknown."""
@@ -157,6 +158,28 @@ class NbrTable:
                        "kmap_signature_order")
             self._sorted = (tp, perm, _tile_masks(tp, self.ld, self.n))
         return self._sorted
+
+    def pair_lists(self):
+        """(pin, pout, seg, total): per-offset pair lists of the table, cached (fvdb_kmap_pair_lists).
+
+        Offset d's pairs (pin = t[d][o], pout = o, o ascending) fill [seg[d], seg[d+1]) of pin / pout, each
+        segment padded with -1 to a multiple of 128; seg is device int32 [28], total = seg[27]. Sizing the
+        lists reads seg[27] back to the host (one synchronisation per table)."""
+        if self._pairs is None:
+            L = _lib.lib()
+            dev, st = self.t.device, _lib.stream_ptr()
+            seg = torch.empty(28, dtype=torch.int32, device=dev)
+            wsb = L.fvdb_kmap_pair_lists_workspace_bytes(self.n)
+            ws = _lib.workspace(wsb, dev)
+            _lib.check(L.fvdb_kmap_pair_lists(self.t.data_ptr(), self.ld, self.n, seg.data_ptr(), None, None, 0,
+                                              ws.data_ptr(), wsb, st), "kmap_pair_lists")
+            total = int(seg[27].item())
+            pin = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+            pout = torch.empty_like(pin)
+            _lib.check(L.fvdb_kmap_pair_lists(self.t.data_ptr(), self.ld, self.n, seg.data_ptr(), pin.data_ptr(),
+                                              pout.data_ptr(), total, ws.data_ptr(), wsb, st), "kmap_pair_lists")
+            self._pairs = (pin, pout, seg, total)
+        return self._pairs
 
     def tile_masks(self):
         """uint32 [ceil(n / 128)]: bit d of tile t = some row of the tile has a pair at offset d, cached."""
@@ -600,6 +623,27 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
     return out
 
 
+def wgrad_pairs_enabled(nbr: "NbrTable", cin: int, cout: int) -> bool:
+    """Run the bf16 weight gradient over per-offset pair lists (fvdb_conv_wgrad_pairs_tc)? Opt-in.
+
+    The table kernel (fvdb_conv_wgrad_tc) processes 27 rows per output row whatever the density. Missing
+    neighbours cost it MMAs on zeros but no memory reads, and each grad_out row is shared by the CTA's
+    offsets. The pair-list kernel issues MMAs for the pairs only, but gathers both operand rows per pair.
+    Measured on B200 (tools/wgrad_pairs_bench.py, ms per wgrad, table vs pairs):
+    - LiDAR 128x128 (9.2 pairs/row): 0.140 vs 0.130;
+    - LiDAR 64x128: 0.095 vs 0.099-0.103;
+    - cfg4 stride-2 64x128 (16.6 pairs/row): 0.120 vs 0.240;
+    - shell 128x128 (20.9 pairs/row): 0.82 vs 1.94.
+    Building the lists costs 0.1-0.26 ms per table. The pair kernel runs at 5-6.5 TB/s of gathered rows, so
+    it is bound by that traffic, not by its tensor work. Stage depth (TK 32/64/128) makes no difference.
+    It needs a 128-channel side (Cin or Cout = 128, the other 32/64/128).
+    Env FVDB_WG_PAIRS: "force" runs it whenever the shape allows; otherwise the table kernel runs.
+    """
+    if not ((cin == 128 and cout in (32, 64, 128)) or (cout == 128 and cin in (32, 64, 128))):
+        return False
+    return os.environ.get("FVDB_WG_PAIRS") == "force"
+
+
 def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: NbrTable) -> torch.Tensor:
     """gw[co][ci][d] = Σ_o go[o,co]·x[nbr[d][o],ci]  → [Cout, Cin, 3, 3, 3] (fp32 for bf16 inputs)."""
     n_out = nbr.n
@@ -627,6 +671,14 @@ def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: NbrTable) -> torch.Tensor:
         gw = wgrad(_pad_cols(x, ci_p), _pad_cols(go, co_p), nbr)
         return gw[:cout, :cin].contiguous()
     gw = torch.empty((cout, cin, 3, 3, 3), dtype=torch.float32, device=x.device)
+    if wgrad_pairs_enabled(nbr, cin, cout):
+        pin, pout, seg, _ = nbr.pair_lists()
+        wsb = L.fvdb_wgrad_pairs_workspace_bytes(cin, cout)
+        ws = _lib.workspace(wsb, x.device)
+        _lib.check(L.fvdb_conv_wgrad_pairs_tc(x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, pin.data_ptr(),
+                                              pout.data_ptr(), seg.data_ptr(), gw.data_ptr(), ws.data_ptr(), wsb,
+                                              st), "conv_wgrad_pairs_tc")
+        return gw
     wsb = L.fvdb_wgrad_tc_workspace_bytes(n_out, cin, cout)
     ws = _lib.workspace(wsb, x.device)
     _lib.check(L.fvdb_conv_wgrad_tc(x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, nbr.t.data_ptr(), nbr.ld,

@@ -150,6 +150,14 @@ struct HaloCfg {
 // profiling trace (FVDB_DEBUG_HALO & 64): clock64 stamps of CTA 0, kTraceN events per channel
 constexpr int kTraceCh = 12, kTraceN = 2048;
 __device__ long long g_halo_trace[kTraceCh][kTraceN];
+// profiling (FVDB_DEBUG_HALO & 128): per-CTA globaltimer at start and end (load balance across CTAs)
+constexpr int kCtaTraceN = 1024;
+__device__ long long g_halo_cta[kCtaTraceN][2];
+__device__ __forceinline__ long long global_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void trace(int dbg, int ch, uint32_t i) {
     if ((dbg & 64) && blockIdx.x == 0 && i < (uint32_t)kTraceN) g_halo_trace[ch][i] = clock64();
 }
@@ -185,6 +193,7 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
     const int T = P.num_tiles;
     const int ntiles = blockIdx.x < T ? (T - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const uint32_t nstages = 27u * (uint32_t)ntiles;                  // this CTA's (tile, offset) stages
+    const long long t_start = (dbg & 128) ? global_ns() : 0;
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < 2; ++b) {
@@ -556,6 +565,10 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
     if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
+    }
+    if ((dbg & 128) && threadIdx.x == 0 && blockIdx.x < kCtaTraceN) {
+        g_halo_cta[blockIdx.x][0] = t_start;
+        g_halo_cta[blockIdx.x][1] = global_ns();
     }
 }
 
@@ -981,6 +994,13 @@ extern "C" int fvdb_pack_weights_halo(const float* w, int cout, int cin, int tra
 extern "C" int fvdb_halo_debug_trace(long long* host, int n) {
     const int cnt = n < kTraceCh * kTraceN ? n : kTraceCh * kTraceN;
     FVDB_CUDA_TRY(cudaMemcpyFromSymbol(host, g_halo_trace, cnt * sizeof(long long)));
+    return FVDB_OK;
+}
+
+// profiling hook (tools/): per-CTA [start, end] globaltimer ns of the last FVDB_DEBUG_HALO&128 launch
+extern "C" int fvdb_halo_debug_cta(long long* host, int n) {
+    const int cnt = n < kCtaTraceN * 2 ? n : kCtaTraceN * 2;
+    FVDB_CUDA_TRY(cudaMemcpyFromSymbol(host, g_halo_cta, cnt * sizeof(long long)));
     return FVDB_OK;
 }
 
