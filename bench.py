@@ -116,7 +116,7 @@ class ClockSampler:
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
 
-    def __init__(self, index, interval=0.005):
+    def __init__(self, index, interval=float(os.environ.get("FVDB_CLOCK_INTERVAL", "0.005"))):
         self.samples, self.reasons, self.max_mhz = [], 0, None
         self.interval = interval
         self._stop = threading.Event()
@@ -372,7 +372,7 @@ def run_special(args, rank, world, local_rank, cfg):
             fine = P.GridBatch([g])
             coarse, h = down(fine, fine.jagged(x))
             _, y = up(coarse, h, out_grid=fine)
-            y.jdata.float().sum().backward()
+            y.jdata.sum(dtype=torch.float32).backward()  # fp32 accumulation, no fp32 copy of y
             if use_dist:
                 P.dist.allreduce_gradients(list(down.parameters()) + list(up.parameters()))
             return y

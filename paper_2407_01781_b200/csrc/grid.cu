@@ -213,10 +213,21 @@ __global__ void k_transpose(const int32_t* __restrict__ nbr, int64_t ld, int64_t
     }
 }
 
-__global__ void k_f32_to_bf16(const float* __restrict__ s, int64_t n, __nv_bfloat16* __restrict__ d) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-         t += (int64_t)gridDim.x * blockDim.x)
-        d[t] = __float2bfloat16_rn(s[t]);
+// 8 elements per thread step (two 16-B loads, one 16-B store) when both pointers are 16-B aligned
+__global__ void k_f32_to_bf16(const float* __restrict__ s, int64_t n, __nv_bfloat16* __restrict__ d, int vec) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t done = 0;
+    if (vec) {
+        const int64_t n8 = n / 8;
+        for (int64_t t = t0; t < n8; t += stride) {
+            const float4 a = reinterpret_cast<const float4*>(s)[2 * t], b = reinterpret_cast<const float4*>(s)[2 * t + 1];
+            __nv_bfloat162 r[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
+                                   __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
+            reinterpret_cast<uint4*>(d)[t] = *reinterpret_cast<const uint4*>(r);
+        }
+        done = n8 * 8;
+    }
+    for (int64_t t = done + t0; t < n; t += stride) d[t] = __float2bfloat16_rn(s[t]);
 }
 
 }  // namespace
@@ -316,7 +327,9 @@ extern "C" int fvdb_kmap_transpose(const int32_t* nbr, int64_t ld, int64_t n_out
 
 extern "C" int fvdb_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream) {
     if (n == 0) return FVDB_OK;
-    k_f32_to_bf16<<<grid_for(n), kThreads, 0, as_stream(stream)>>>(src, n, (__nv_bfloat16*)dst);
+    const int vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    k_f32_to_bf16<<<grid_for(vec ? (n + 7) / 8 : n), kThreads, 0, as_stream(stream)>>>(src, n, (__nv_bfloat16*)dst,
+                                                                                     vec);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

@@ -19,15 +19,33 @@ import math
 import torch
 from torch import nn
 
+from . import _lib
 from .build import coarsen
 from .conv import batch_grid_kernel_map, gather_conv, wgrad
 from .jagged import GridBatch, JaggedTensor
 
 
+def _to_compute(t: torch.Tensor, cdt: torch.dtype) -> torch.Tensor:
+    """Contiguous ``t`` in the compute dtype; fp32 -> bf16 on the device by fvdb_f32_to_bf16."""
+    if t.dtype == torch.float32 and cdt == torch.bfloat16 and t.is_cuda:
+        t = t.contiguous()
+        out = torch.empty(t.shape, dtype=torch.bfloat16, device=t.device)
+        _lib.check(_lib.lib().fvdb_f32_to_bf16(t.data_ptr(), t.numel(), out.data_ptr(), _lib.stream_ptr()),
+                   "f32_to_bf16")
+        return out
+    return t.to(cdt).contiguous()
+
+
+def _grad_dtype(x_dtype: torch.dtype, cdt: torch.dtype) -> torch.dtype:
+    """The tensor-core conv kernels write fp32 or bf16 directly: the input gradient comes out in the
+    features' dtype (what autograd needs) with no separate cast pass."""
+    return x_dtype if cdt == torch.bfloat16 and x_dtype in (torch.float32, torch.bfloat16) else cdt
+
+
 class _SparseConvFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, kmap, transposed, cdt):
-        xc = x.to(cdt).contiguous()
+        xc = _to_compute(x, cdt)
         if transposed:
             y = gather_conv(xc, kmap.bwd, w, transpose=True, out_dtype=cdt)
         else:
@@ -40,16 +58,17 @@ class _SparseConvFn(torch.autograd.Function):
     def backward(ctx, gy):
         xc, w = ctx.saved_tensors
         km, cdt = ctx.kmap, ctx.cdt
-        gy = gy.to(cdt).contiguous()
+        gy = _to_compute(gy, cdt)
+        od = _grad_dtype(ctx.x_dtype, cdt)
         gx = gw = None
         if ctx.transposed:
             if ctx.needs_input_grad[0]:
-                gx = gather_conv(gy, km.fwd, w, transpose=False, out_dtype=cdt)
+                gx = gather_conv(gy, km.fwd, w, transpose=False, out_dtype=od)
             if ctx.needs_input_grad[1]:
                 gw = wgrad(gy, xc, km.fwd)
         else:
             if ctx.needs_input_grad[0]:
-                gx = gather_conv(gy, km.bwd, w, transpose=True, out_dtype=cdt)
+                gx = gather_conv(gy, km.bwd, w, transpose=True, out_dtype=od)
             if ctx.needs_input_grad[1]:
                 gw = wgrad(xc, gy, km.fwd)
         if gx is not None:

@@ -381,3 +381,28 @@ def test_wide_channels_blocked(shell):
     for dt, tol in ((torch.float64, 1e-10), (torch.float32, 1e-5)):
         y2 = gather_conv(torch.from_numpy(x2).cuda().to(dt), km.fwd, torch.from_numpy(w2).cuda().to(dt))
         assert y2.shape == (n, 300) and rel(y2, ref2) < tol
+
+
+@pytest.mark.parametrize("n,off", [(0, 0), (7, 0), (1 << 16, 0), ((1 << 16) + 5, 0), (1003, 1), (4096, 3)])
+def test_f32_to_bf16_matches_torch(n, off):
+    """fvdb_f32_to_bf16 (vectorised for 16-B aligned buffers, scalar otherwise) rounds to nearest even,
+    bit-identical to torch's cast, including the unaligned and tail paths."""
+    from paper_2407_01781_b200.nn import _to_compute
+    src = (torch.randn(n + off, device="cuda") * 1e3)[off:]
+    src[: min(n, 4)] = torch.tensor([float("inf"), float("-inf"), float("nan"), 3.0e38], device="cuda")[: min(n, 4)]
+    got = _to_compute(src, torch.bfloat16)
+    ref = src.to(torch.bfloat16)
+    assert got.dtype == torch.bfloat16 and got.shape == ref.shape
+    assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
+
+
+def test_module_input_grad_dtype():
+    """SparseConv3d (bf16 compute): y in bf16, the fp32 input's gradient written in fp32 by the kernel."""
+    g, _ = P.build_from_coords(sphere_shell_coords(24, band=1.5))
+    gb = P.GridBatch([g])
+    m = P.SparseConv3d(64, 64).cuda()
+    x = torch.randn(g.num_voxels, 64, device="cuda", requires_grad=True)
+    _, y = m(gb, gb.jagged(x))
+    assert y.jdata.dtype == torch.bfloat16
+    y.jdata.float().sum().backward()
+    assert x.grad.dtype == torch.float32 and torch.isfinite(x.grad).all()

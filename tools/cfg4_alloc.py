@@ -18,7 +18,7 @@ def step():
     fine = P.GridBatch([g])
     coarse, h = down(fine, fine.jagged(x))
     _, y = up(coarse, h, out_grid=fine)
-    y.jdata.float().sum().backward()
+    y.jdata.sum(dtype=torch.float32).backward()
 for loop in range(4):
     s0 = torch.cuda.memory_stats()
     torch.cuda.synchronize(); t0 = time.perf_counter()

@@ -23,7 +23,7 @@ def step(mark):
     _ = km.bwd; mark("transpose")
     coarse, h = down(fine, fine.jagged(x)); mark("down_fwd")
     _, y = up(coarse, h, out_grid=fine); mark("up_fwd")
-    y.jdata.float().sum().backward(); mark("backward")
+    y.jdata.sum(dtype=torch.float32).backward(); mark("backward")
 
 
 for _ in range(3):

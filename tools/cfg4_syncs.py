@@ -19,7 +19,7 @@ def step():
     fine = P.GridBatch([g])
     coarse, h = down(fine, fine.jagged(x))
     _, y = up(coarse, h, out_grid=fine)
-    y.jdata.float().sum().backward()
+    y.jdata.sum(dtype=torch.float32).backward()
 
 
 for _ in range(3):

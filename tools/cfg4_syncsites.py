@@ -1,11 +1,10 @@
-"""Per-kernel device time of one cfg4 step (torch.profiler / CUPTI), to attribute the step's phases."""
-import pathlib, sys
+"""Python call sites of torch-level host syncs (.item(), .cpu(), ...) in one cfg4 step, via
+torch.cuda.set_sync_debug_mode("warn"). Syncs inside libfvdb_b200 (the build's read-backs) are not seen."""
+import collections, pathlib, sys, traceback, warnings
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 import numpy as np, torch
-from torch.profiler import ProfilerActivity, profile
 import paper_2407_01781_b200 as P
 from paper_2407_01781_b200.workloads import sphere_shell_coords
-from paper_2407_01781_b200.nn import coarsen_batch
 
 coords = sphere_shell_coords(470, 1.5)
 pts = torch.from_numpy(coords.astype(np.float64)).cuda()
@@ -26,7 +25,19 @@ def step():
 for _ in range(3):
     step()
 torch.cuda.synchronize()
-with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-    step()
-    torch.cuda.synchronize()
-print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=60))
+sites = collections.Counter()
+
+
+def hook(message, category, filename, lineno, file=None, line=None):
+    st = [f"{pathlib.Path(f.filename).name}:{f.lineno}:{f.name}" for f in traceback.extract_stack()
+          if "paper_2407" in f.filename]
+    sites[" <- ".join(reversed(st[-3:]))] += 1
+
+
+warnings.simplefilter("always")
+warnings.showwarning = hook
+torch.cuda.set_sync_debug_mode("warn")
+step()
+torch.cuda.set_sync_debug_mode(0)
+for where, n in sites.most_common():
+    print(f"{n:3d}  {where}")
