@@ -134,6 +134,13 @@ int fvdb_kmap_transpose(const int32_t* nbr, int64_t ld, int64_t n_out, int64_t n
  *   wk: [27, K, N] in the feature dtype (see fvdb_pack_weights_kn). */
 int fvdb_conv_gather_simt(int dtype, const void* in, int64_t n_in, int K, const void* wk, int N,
                           const int32_t* nbr, int64_t ld, int64_t n_out, void* out, void* stream);
+/* fvdb_conv_gather_simt with optional per-128-row-tile offset masks (fvdb_kmap_tile_masks; offsets absent
+ * from a tile are skipped) and an optional row permutation (signature-sorted table, fvdb_kmap_signature_order:
+ * table column i is written to output row row_perm[i]).  row_perm needs K, N multiples of 8 and N <= 64
+ * (the tiled kernel); both nullable. */
+int fvdb_conv_gather_simt2(int dtype, const void* in, int64_t n_in, int K, const void* wk, int N,
+                           const int32_t* nbr, int64_t ld, int64_t n_out, const int32_t* row_perm,
+                           const uint32_t* tile_masks, void* out, void* stream);
 /* weight relayout [Cout,Cin,27] -> Wk[27][K][N]; transpose=0: K=Cin,N=Cout; 1: K=Cout,N=Cin */
 int fvdb_pack_weights_kn(int dtype, const void* w, int cout, int cin, int transpose, void* wk,
                          void* stream);

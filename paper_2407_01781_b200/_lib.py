@@ -71,6 +71,7 @@ SIGNATURES = {
     "fvdb_kmap_compact": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "fvdb_kmap_transpose": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp]),
     "fvdb_conv_gather_simt": (_i32, [_i32, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp]),
+    "fvdb_conv_gather_simt2": (_i32, [_i32, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "fvdb_pack_weights_kn": (_i32, [_i32, _vp, _i32, _i32, _i32, _vp, _vp]),
     "fvdb_wgrad_workspace_bytes": (_sz, [_i32, _i64, _i32, _i32]),
     "fvdb_conv_wgrad_simt": (_i32, [_i32, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),

@@ -122,7 +122,7 @@ class NbrTable:
     """
 
     __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
-                 "_masks", "sparse", "_steady", "_pairs")
+                 "_masks", "sparse", "_steady", "_pairs", "exact_uses")
 
     def __init__(self, t, n, colors_fn=None, counts=None):
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
@@ -135,6 +135,7 @@ class NbrTable:
         self.sparse = False  # set for transposed stride-2 tables (<= 8 of 27 offsets per row)
         self._steady = {}    # (K, N) -> steady_impl decision
         self._pairs = None   # (pin, pout, seg, padded total): per-offset pair lists (wgrad)
+        self.exact_uses = 0  # fp32 / f64 gather convolutions run over this table
 
     def density(self) -> float:
         """Mean pairs per output row (27 = every offset active); 27 when unknown."""
@@ -545,6 +546,30 @@ def _tc_width(c: int) -> int:
     raise ValueError(f"bf16 tensor-core path supports up to 128 channels per operand, got {c}")
 
 
+def exact_skip_mode(nbr: "NbrTable", K: int, N: int) -> str:
+    """How the exact-precision (fp32 / f64) gather kernel skips offsets without pairs.
+
+    - "sort": the signature-sorted table (fvdb_kmap_signature_order, cached on the table) with its tile
+      masks. Its 128-row tiles are homogeneous, so a tile walks only the offsets present in it.
+    - "masks": tile masks over the unsorted table.
+    - "none": all 27 offsets.
+    Skipping drops only zero-filled rows, so the results are bitwise those of "none".
+    Measured on B200 (tools/exact_skip_bench.py, fp32, ms per conv, none / masks / sort):
+    - cfg1 at 6.6 pairs/row: 0.229 / 0.242 / 0.172;
+    - cfg2 shell 64x64: 8.54 / 8.55 / 6.84.
+    Unsorted tiles hold every offset, so masks alone do not help.
+    Default: "sort" from a table's second exact use on (the sort is amortised over reuse), "none" before
+    that. It needs the tiled kernel (K, N multiples of 8, N <= 64). Env FVDB_EXACT_SKIP overrides.
+    """
+    tiled = K % 8 == 0 and N % 8 == 0 and N <= 64
+    v = os.environ.get("FVDB_EXACT_SKIP")
+    if v in ("none", "masks"):
+        return v
+    if v == "sort":
+        return "sort" if tiled else "masks"
+    return "sort" if tiled and (nbr._sorted is not None or nbr.exact_uses >= 1) else "none"
+
+
 def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool = False,
                 out_dtype=None, w_image=None, impl: str | None = None) -> torch.Tensor:
     """out[o] = Σ_d x[nbr[d][o]] @ Wk[d]; Wk from w [Cout,Cin,3,3,3] (transpose → dgrad form).
@@ -580,9 +605,16 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
         wk = pack_weights_kn(w, transpose, x.dtype)
         out = torch.empty((n_out, N), dtype=x.dtype, device=x.device)
         if n_out:
-            _lib.check(L.fvdb_conv_gather_simt(_dtype_code(x.dtype), x.data_ptr(), x.shape[0], K, wk.data_ptr(), N,
-                                               nbr.t.data_ptr(), nbr.ld, n_out, out.data_ptr(), st),
-                       "conv_gather_simt")
+            tab, perm, masks = nbr.t, None, None
+            mode = exact_skip_mode(nbr, K, N)
+            nbr.exact_uses += 1
+            if mode == "sort":
+                tab, perm, masks = nbr.signature_sorted()
+            elif mode == "masks":
+                masks = nbr.tile_masks()
+            _lib.check(L.fvdb_conv_gather_simt2(_dtype_code(x.dtype), x.data_ptr(), x.shape[0], K, wk.data_ptr(), N,
+                                                tab.data_ptr(), nbr.ld, n_out, _lib.ptr(perm), _lib.ptr(masks),
+                                                out.data_ptr(), st), "conv_gather_simt")
         return out
     if x.dtype != torch.bfloat16:
         raise TypeError(f"unsupported feature dtype {x.dtype}")

@@ -97,15 +97,20 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
 template <typename T, int NT>
 __global__ void __launch_bounds__(kThr) k_conv_gather_tiled(const T* __restrict__ in, int K, const T* __restrict__ wk,
                                                             int N, const int32_t* __restrict__ nbr, int64_t ld,
-                                                            int64_t n_out, T* __restrict__ out) {
+                                                            int64_t n_out, T* __restrict__ out,
+                                                            const uint32_t* __restrict__ tile_mask,
+                                                            const int32_t* __restrict__ row_perm) {
     using C = TileCfg<T, NT>;
     extern __shared__ __align__(16) uint8_t smraw[];
     T* sm = reinterpret_cast<T*>(smraw);
     const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
     const int64_t o0 = (int64_t)blockIdx.x * kTR;
-    const int kchunks = (K + kTKC - 1) / kTKC, steps = 27 * kchunks;
+    // offsets with a pair somewhere in this 128-row tile (all 27 without masks); absent offsets would only
+    // add zero-filled rows, so skipping them leaves every finite sum unchanged
+    const uint32_t m = tile_mask ? (tile_mask[blockIdx.x] & 0x7ffffffu) : 0x7ffffffu;
+    const int kchunks = (K + kTKC - 1) / kTKC, steps = __popc(m) * kchunks;
     auto issue = [&](int step, int buf) {
-        const int d = step / kchunks, k0 = (step % kchunks) * kTKC;
+        const int d = (int)__fns(m, 0, step / kchunks + 1), k0 = (step % kchunks) * kTKC;
         T* sa = sm + buf * (C::A_ELEMS + C::W_ELEMS);
         T* sw = sa + C::A_ELEMS;
         constexpr int CPR = kTKC / C::EPV;                    // 16-B copies per A row
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(kThr) k_conv_gather_tiled(const T* __restrict_
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < C::CPT; ++j) acc[i][j] = T(0);
-    issue(0, 0);
+    if (steps > 0) issue(0, 0);
     for (int step = 0; step < steps; ++step) {
         const int buf = step & 1;
         if (step + 1 < steps) {
@@ -161,10 +166,11 @@ __global__ void __launch_bounds__(kThr) k_conv_gather_tiled(const T* __restrict_
     for (int i = 0; i < 4; ++i) {
         const int64_t o = o0 + ty + 32 * i;
         if (o >= n_out) continue;
+        const int64_t orow = row_perm ? (int64_t)row_perm[o] : o;  // signature-sorted table: original row
 #pragma unroll
         for (int j = 0; j < C::CPT; ++j) {
             const int n = tx * C::CPT + j;
-            if (n < N) out[o * N + n] = acc[i][j];
+            if (n < N) out[orow * N + n] = acc[i][j];
         }
     }
 }
@@ -258,22 +264,25 @@ int wgrad_splits(int64_t n_out) {
 
 template <typename T>
 int run_gather(const void* in, int K, const void* wk, int N, const int32_t* nbr, int64_t ld, int64_t n_out, void* out,
-               cudaStream_t st) {
+               cudaStream_t st, const uint32_t* masks = nullptr, const int32_t* perm = nullptr) {
     if (n_out == 0) return FVDB_OK;
     if (K % 8 == 0 && N % 8 == 0 && N <= 64) {
         const unsigned blocks = (unsigned)ceil_div(n_out, kTR);
         if (N <= 32) {
             auto kern = k_conv_gather_tiled<T, 32>;
             FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TileCfg<T, 32>::SMEM));
-            kern<<<blocks, kThr, TileCfg<T, 32>::SMEM, st>>>((const T*)in, K, (const T*)wk, N, nbr, ld, n_out, (T*)out);
+            kern<<<blocks, kThr, TileCfg<T, 32>::SMEM, st>>>((const T*)in, K, (const T*)wk, N, nbr, ld, n_out, (T*)out,
+                                                             masks, perm);
         } else {
             auto kern = k_conv_gather_tiled<T, 64>;
             FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TileCfg<T, 64>::SMEM));
-            kern<<<blocks, kThr, TileCfg<T, 64>::SMEM, st>>>((const T*)in, K, (const T*)wk, N, nbr, ld, n_out, (T*)out);
+            kern<<<blocks, kThr, TileCfg<T, 64>::SMEM, st>>>((const T*)in, K, (const T*)wk, N, nbr, ld, n_out, (T*)out,
+                                                             masks, perm);
         }
         FVDB_LAUNCH_CHECK();
         return FVDB_OK;
     }
+    if (perm) return FVDB_ERR_INVALID;  // only the tiled kernel writes through a row permutation
     unsigned blocks = (unsigned)ceil_div(n_out, kRows);
     k_conv_gather<T><<<blocks, kThr, 0, st>>>((const T*)in, K, (const T*)wk, N, nbr, ld, n_out, (T*)out);
     FVDB_LAUNCH_CHECK();
@@ -309,6 +318,17 @@ extern "C" int fvdb_conv_gather_simt(int dtype, const void* in, int64_t n_in, in
     cudaStream_t st = as_stream(stream);
     if (dtype == FVDB_DTYPE_F32) return run_gather<float>(in, K, wk, N, nbr, ld, n_out, out, st);
     if (dtype == FVDB_DTYPE_F64) return run_gather<double>(in, K, wk, N, nbr, ld, n_out, out, st);
+    return FVDB_ERR_INVALID;
+}
+
+extern "C" int fvdb_conv_gather_simt2(int dtype, const void* in, int64_t n_in, int K, const void* wk, int N,
+                                      const int32_t* nbr, int64_t ld, int64_t n_out, const int32_t* row_perm,
+                                      const uint32_t* tile_masks, void* out, void* stream) {
+    (void)n_in;
+    if (K <= 0 || N <= 0 || N > 256 || ld < n_out) return FVDB_ERR_INVALID;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == FVDB_DTYPE_F32) return run_gather<float>(in, K, wk, N, nbr, ld, n_out, out, st, tile_masks, row_perm);
+    if (dtype == FVDB_DTYPE_F64) return run_gather<double>(in, K, wk, N, nbr, ld, n_out, out, st, tile_masks, row_perm);
     return FVDB_ERR_INVALID;
 }
 

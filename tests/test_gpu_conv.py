@@ -406,3 +406,37 @@ def test_module_input_grad_dtype():
     assert y.jdata.dtype == torch.bfloat16
     y.jdata.float().sum().backward()
     assert x.grad.dtype == torch.float32 and torch.isfinite(x.grad).all()
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.float32, 1e-5), (np.float64, 1e-10)])
+@pytest.mark.parametrize("which", ["s1", "s2T"])
+def test_exact_offset_skipping(monkeypatch, dtype, tol, which):
+    """The exact-precision gather kernel with tile masks / over the signature-sorted table skips only
+    zero-filled rows: bitwise equal to walking all 27 offsets, and within the exact-path tolerance of the
+    oracle (conv.py:180-191; transposed form conv.py:339-368)."""
+    c = sphere_shell_coords(30, band=1.5)
+    g, _ = P.build_from_coords(c)
+    og = O.build_from_coords(c)
+    if which == "s1":
+        km, (ins, outs), n_in, n_out = P.build_kernel_map(g, g, 1), O.kernel_map(og, og, 1), g.num_voxels, g.num_voxels
+    else:
+        gc, ogc = P.coarsen(g, 2), O.coarsen(og, 2)
+        km, (ins, outs) = P.build_kernel_map(g, gc, 2), O.kernel_map(og, ogc, 2)
+        n_in, n_out = gc.num_voxels, g.num_voxels
+    rng = np.random.default_rng(11)
+    x = rng.normal(size=(n_in, 32)).astype(dtype)
+    w = (rng.normal(size=(32, 32, 3, 3, 3)) / np.sqrt(27 * 32)).astype(dtype)
+    xt, wt = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    res = {}
+    for mode in ("none", "masks", "sort"):
+        monkeypatch.setenv("FVDB_EXACT_SKIP", mode)
+        if which == "s1":
+            res[mode] = gather_conv(xt, km.fwd, wt)
+        else:
+            res[mode] = gather_conv(xt, km.bwd, wt, transpose=True)
+    assert torch.equal(res["none"], res["masks"]) and torch.equal(res["none"], res["sort"])
+    if which == "s1":
+        ref = O.conv_igemm(x.astype(np.float64), w.astype(np.float64), ins, outs, n_out)
+    else:
+        ref = O.conv_transpose(ins, outs, x.astype(np.float64), w.astype(np.float64), n_out)
+    assert rel(res["sort"], ref) < tol

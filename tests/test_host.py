@@ -153,3 +153,17 @@ def test_conv_kernel_policy_host_logic(monkeypatch):
     assert sig_sort_enabled(lidar) and not sig_sort_enabled(dense)
     monkeypatch.setenv("FVDB_SIG_SORT", "force")
     assert sig_sort_enabled(dense)
+
+
+def test_exact_skip_policy(monkeypatch):
+    """fp32 / f64 gather: plain table on first use, signature-sorted from the second use (tiled shapes)."""
+    import torch
+    from paper_2407_01781_b200.conv import NbrTable, exact_skip_mode
+    monkeypatch.delenv("FVDB_EXACT_SKIP", raising=False)
+    t = NbrTable(torch.full((27, 128), -1, dtype=torch.int32), 10)
+    assert exact_skip_mode(t, 32, 32) == "none"
+    t.exact_uses = 1
+    assert exact_skip_mode(t, 32, 32) == "sort"
+    assert exact_skip_mode(t, 32, 128) == "none"  # N > 64: untiled kernel, no row permutation
+    monkeypatch.setenv("FVDB_EXACT_SKIP", "sort")
+    assert exact_skip_mode(t, 32, 128) == "masks"
