@@ -353,7 +353,10 @@ struct WgCfg {
     static constexpr int ISLOTS = 2;
     static constexpr int FIXED = ISLOTS * IDX_BYTES + 1024;
     static constexpr int STAGES0 = (222 * 1024 - FIXED) / STAGE;
-    static constexpr int STAGES = STAGES0 > 4 ? 4 : STAGES0;
+#ifndef FVDB_WG_MAX_STAGES
+#define FVDB_WG_MAX_STAGES 4
+#endif
+    static constexpr int STAGES = STAGES0 > FVDB_WG_MAX_STAGES ? FVDB_WG_MAX_STAGES : STAGES0;
     static constexpr int SMEM = FIXED + STAGES * STAGE;
     static constexpr int TMEM_COLS = pow2_cols(NACC * COUT);
     static constexpr bool B_SW128 = (COUT % 64) == 0;
