@@ -1,6 +1,6 @@
 """Gather-GEMM conv over signature-sorted vs unsorted tables (cfg4 stride-2 maps, cfg2 stride-1 map).
 
-python tools/sigsort_bench.py — one JSON line per (map, mode): median of 10 event-timed launches,
+python tools/sigsort_bench.py (GRID=1: more shapes; SKIP_HALO=1: gather only) — one JSON line per (map, mode): median of 10 event-timed launches,
 256 MB L2 flush before each; plus the one-off cost of fvdb_kmap_signature_order.
 """
 import json
@@ -68,9 +68,11 @@ def main():
         for on in ("0", "force"):
             os.environ["FVDB_SIG_SORT"] = on
             res[on] = timed(lambda: gather_conv(x, tab, w, transpose=tr, w_image=img))
-        imh = pack_weights_umma(w, tr, "halo")
-        tab.halo_plan(K, N)
-        halo = timed(lambda: gather_conv(x, tab, w, transpose=tr, w_image=imh))
+        halo = None
+        if not os.environ.get("SKIP_HALO"):
+            imh = pack_weights_umma(w, tr, "halo")
+            tab.halo_plan(K, N)
+            halo = timed(lambda: gather_conv(x, tab, w, transpose=tr, w_image=imh))
         print(json.dumps({"map": name, "rows": tab.n, "density": round(tab.density(), 2), "unsorted_ms": res["0"],
                           "sorted_ms": res["force"], "sort_ms": sort_ms, "halo_ms": halo}))
 
