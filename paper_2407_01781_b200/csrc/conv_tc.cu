@@ -65,11 +65,11 @@ struct FwdCfg {
     static constexpr int BSLOTS = B_BYTES <= 8192 ? 3 : 2;
     static constexpr int FIXED = BSLOTS * B_BYTES + ISLOTS * IDX_BYTES + 1024;
     static constexpr int STAGES0 = (222 * 1024 - FIXED) / A_BYTES;
-    // ~128 KB of A stages (4 at K = 128, 8 below): shared memory left over is L1, which serves the gather's
+    // ~96-128 KB of A stages (3 at K = 128, 8 below): shared memory left over is L1, which serves the gather's
     // row reuse. Measured optimum (profiles/r01_fwd_breakdown.md, ring depth): deeper rings lose L1 hits,
     // shallower ones lose latency hiding.
 #ifndef FVDB_FWD_MAX_STAGES
-#define FVDB_FWD_MAX_STAGES (K >= 128 ? 4 : 8)
+#define FVDB_FWD_MAX_STAGES (K >= 128 ? 3 : 8)
 #endif
     static constexpr int STAGES = STAGES0 > FVDB_FWD_MAX_STAGES ? FVDB_FWD_MAX_STAGES : STAGES0;
     static constexpr int SMEM = FIXED + STAGES * A_BYTES;
