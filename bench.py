@@ -165,7 +165,8 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_2407_01781_b200 as P
-    from paper_2407_01781_b200.conv import conv_impl, gather_conv, pack_weights_umma, steady_impl, wgrad
+    from paper_2407_01781_b200.conv import (conv_impl, gather_conv, pack_weights_umma, steady_impl, wgrad,
+                                            wgrad_pairs_enabled)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -317,7 +318,8 @@ def run_ours(args, rank, world, local_rank):
                        "l2": "flushed (256 MB write) before every timed step",
                        "kernel_map": "prebuilt outside the timed step (reference cli.py:353)",
                        "conv_kernel": {"fwd": impl_f + (" (signature-sorted)" if sorted_f else ""),
-                                       "dgrad": impl_b + (" (signature-sorted)" if sorted_b else "")}},
+                                       "dgrad": impl_b + (" (signature-sorted)" if sorted_b else ""),
+                                       "wgrad": "pair lists" if wgrad_pairs_enabled(nbr, cin, cout) else "table"}},
             "tflops_effective": round(step_tflops, 2),
             "frac_of_bf16_peak": round(step_tflops / pk["bf16_tflops"], 4),
             "phases_ms": {k: round(v, 4) for k, v in means.items()},

@@ -122,7 +122,7 @@ class NbrTable:
     """
 
     __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
-                 "_masks", "sparse", "_steady", "_pairs", "exact_uses")
+                 "_masks", "sparse", "_steady", "_pairs", "exact_uses", "wgrad_uses")
 
     def __init__(self, t, n, colors_fn=None, counts=None):
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
@@ -136,6 +136,7 @@ class NbrTable:
         self._steady = {}    # (K, N) -> steady_impl decision
         self._pairs = None   # (pin, pout, seg, padded total): per-offset pair lists (wgrad)
         self.exact_uses = 0  # fp32 / f64 gather convolutions run over this table
+        self.wgrad_uses = 0  # bf16 weight gradients run over this table
 
     def density(self) -> float:
         """Mean pairs per output row (27 = every offset active); 27 when unknown."""
@@ -655,25 +656,37 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
     return out
 
 
+WG_PAIRS_BELOW_DENSITY = 11.0  # mean pairs per output row under which the pair-list wgrad runs
+
+
 def wgrad_pairs_enabled(nbr: "NbrTable", cin: int, cout: int) -> bool:
-    """Run the bf16 weight gradient over per-offset pair lists (fvdb_conv_wgrad_pairs_tc)? Opt-in.
+    """Run the bf16 weight gradient over per-offset pair lists (fvdb_conv_wgrad_pairs_tc)?
 
     The table kernel (fvdb_conv_wgrad_tc) processes 27 rows per output row whatever the density. Missing
     neighbours cost it MMAs on zeros but no memory reads, and each grad_out row is shared by the CTA's
     offsets. The pair-list kernel issues MMAs for the pairs only, but gathers both operand rows per pair.
-    Measured on B200 (tools/wgrad_pairs_bench.py, ms per wgrad, table vs pairs):
-    - LiDAR 128x128 (9.2 pairs/row): 0.140 vs 0.130;
-    - LiDAR 64x128: 0.095 vs 0.099-0.103;
-    - cfg4 stride-2 64x128 (16.6 pairs/row): 0.120 vs 0.240;
-    - shell 128x128 (20.9 pairs/row): 0.82 vs 1.94.
-    Building the lists costs 0.1-0.26 ms per table. The pair kernel runs at 5-6.5 TB/s of gathered rows, so
-    it is bound by that traffic, not by its tensor work. Stage depth (TK 32/64/128) makes no difference.
-    It needs a 128-channel side (Cin or Cout = 128, the other 32/64/128).
-    Env FVDB_WG_PAIRS: "force" runs it whenever the shape allows; otherwise the table kernel runs.
+    Measured on B200 (tools/wgrad_pairs_bench.py, ms per wgrad, table vs pairs with a 6-stage ring):
+    - LiDAR 128x128 (9.2 pairs/row): 0.140 vs 0.108;
+    - LiDAR 64x128: 0.095 vs 0.093;
+    - LiDAR 128x64: 0.103 vs 0.093;
+    - cfg4 stride-2 64x128 (16.6 pairs/row): 0.120 vs 0.193;
+    - shell 128x128 (20.9 pairs/row): 0.83 vs 1.39.
+    Building the lists costs 0.1-0.26 ms per table (cached on it).
+    Default: tables below ``WG_PAIRS_BELOW_DENSITY`` mean pairs per row, from their third wgrad on, so
+    the list build and the density read-back are paid only by reused tables (a U-Net stage that rebuilds
+    its maps runs two wgrads per map). It needs a 128-channel side (Cin or Cout = 128, the other 32/64/128).
+    Env FVDB_WG_PAIRS: "0" never, "force" whenever the shape allows.
     """
     if not ((cin == 128 and cout in (32, 64, 128)) or (cout == 128 and cin in (32, 64, 128))):
         return False
-    return os.environ.get("FVDB_WG_PAIRS") == "force"
+    v = os.environ.get("FVDB_WG_PAIRS")
+    if v == "0":
+        return False
+    if v == "force":
+        return True
+    if nbr._pairs is None and nbr.wgrad_uses < 2:  # the density check reads counts back (one sync per table)
+        return False
+    return nbr.n > 0 and nbr.density() < WG_PAIRS_BELOW_DENSITY
 
 
 def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: NbrTable) -> torch.Tensor:
@@ -703,7 +716,9 @@ def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: NbrTable) -> torch.Tensor:
         gw = wgrad(_pad_cols(x, ci_p), _pad_cols(go, co_p), nbr)
         return gw[:cout, :cin].contiguous()
     gw = torch.empty((cout, cin, 3, 3, 3), dtype=torch.float32, device=x.device)
-    if wgrad_pairs_enabled(nbr, cin, cout):
+    use_pairs = wgrad_pairs_enabled(nbr, cin, cout)
+    nbr.wgrad_uses += 1
+    if use_pairs:
         pin, pout, seg, _ = nbr.pair_lists()
         wsb = L.fvdb_wgrad_pairs_workspace_bytes(cin, cout)
         ws = _lib.workspace(wsb, x.device)

@@ -199,7 +199,12 @@ struct WpCfg {
     static constexpr int IDX_BYTES = 2 * kPlChunk * 4;             // ia + ib of one chunk
     static constexpr int FIXED = ISLOTS * IDX_BYTES + 1024;
     static constexpr int STAGES0 = (222 * 1024 - FIXED) / STAGE;
-    static constexpr int STAGES = STAGES0 > 16 ? 16 : STAGES0;
+// 6 stages (~96 KB at N = 128): the rest of shared memory is L1 for row reuse across neighbouring pairs.
+// Measured (tools/wgrad_pairs_bench.py, LiDAR 128x128): 16 stages 0.134 ms, 10 0.107, 6 0.108, 4 0.112.
+#ifndef FVDB_WP_MAX_STAGES
+#define FVDB_WP_MAX_STAGES 6
+#endif
+    static constexpr int STAGES = STAGES0 > FVDB_WP_MAX_STAGES ? FVDB_WP_MAX_STAGES : STAGES0;
     static_assert(STAGES >= 2, "pair wgrad pipeline needs >= 2 stages");
     static constexpr int SMEM = FIXED + STAGES * STAGE;
     static constexpr int TMEM_COLS = 512;

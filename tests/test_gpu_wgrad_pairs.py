@@ -98,8 +98,16 @@ def test_wgrad_pairs_empty_offsets_and_tables(monkeypatch):
 
 
 def test_policy(maps, monkeypatch):
+    from paper_2407_01781_b200.conv import NbrTable
     monkeypatch.delenv("FVDB_WG_PAIRS", raising=False)
     _, _, km1, _ = maps["s1"]
-    assert not wgrad_pairs_enabled(km1.fwd, 64, 128)  # opt-in: the table kernel is faster or on par
+    assert km1.fwd.density() > 11 and not wgrad_pairs_enabled(km1.fwd, 64, 128)  # dense: table kernel
+    sparse = NbrTable(km1.fwd.t, km1.fwd.n, counts=km1.fwd.counts * 0 + 1)  # 27 pairs in n rows: sparse
+    sparse._pairs, sparse.wgrad_uses = None, 1
+    assert not wgrad_pairs_enabled(sparse, 128, 128)  # first two uses: no list build or density read-back
+    sparse.wgrad_uses = 2
+    assert wgrad_pairs_enabled(sparse, 128, 128) and not wgrad_pairs_enabled(sparse, 64, 64)
+    monkeypatch.setenv("FVDB_WG_PAIRS", "0")
+    assert not wgrad_pairs_enabled(sparse, 128, 128)
     monkeypatch.setenv("FVDB_WG_PAIRS", "force")
     assert not wgrad_pairs_enabled(km1.fwd, 64, 64) and wgrad_pairs_enabled(km1.fwd, 64, 128)
