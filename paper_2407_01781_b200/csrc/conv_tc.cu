@@ -342,7 +342,10 @@ template <int CIN, int COUT>
 struct WgCfg {
     static constexpr int OPB = 128 / CIN;                      // offsets per M-block
     static constexpr int NMB = (27 + OPB - 1) / OPB;           // M-blocks for all offsets
-    static constexpr int NACC_MAX = (512 / COUT) < 8 ? (512 / COUT) : 8;  // TMEM columns, A stage size
+#ifndef FVDB_WG_MAX_ACC
+#define FVDB_WG_MAX_ACC 8
+#endif
+    static constexpr int NACC_MAX = (512 / COUT) < FVDB_WG_MAX_ACC ? (512 / COUT) : FVDB_WG_MAX_ACC;  // TMEM, stage
     static constexpr int GROUPS = (NMB + NACC_MAX - 1) / NACC_MAX;       // CTAs per row range
     // M-blocks (TMEM accumulators) per CTA, balanced over the groups: the group with the most offsets is the
     // critical path (all CTAs are co-resident), so 27 offsets at Cin 64 split 14 + 13, not 16 + 11

@@ -1,4 +1,4 @@
-"""Time k_wgrad_tc on cfg2 under FVDB_DEBUG_WG switches (1 no MMA, 2 no A gather)."""
+"""Time k_wgrad_tc on cfg2 under FVDB_DEBUG_WG switches (1 no MMA, 2 no A gather); CH env = channels."""
 import json, os, subprocess, sys, pathlib
 if len(sys.argv) > 1 and sys.argv[1] == "run":
     sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
@@ -8,8 +8,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "run":
     from paper_2407_01781_b200.workloads import sphere_shell_coords
     g, _ = P.build_from_coords(sphere_shell_coords(470, 1.5))
     km = P.build_kernel_map(g, g, 1)
-    x = torch.randn(g.num_voxels, 64, device="cuda").to(torch.bfloat16)
-    gy = torch.randn(g.num_voxels, 64, device="cuda").to(torch.bfloat16)
+    ch = int(os.environ.get("CH", "64"))  # channels (Cin = Cout)
+    x = torch.randn(g.num_voxels, ch, device="cuda").to(torch.bfloat16)
+    gy = torch.randn(g.num_voxels, ch, device="cuda").to(torch.bfloat16)
     for _ in range(3):
         wgrad(x, gy, km.fwd)
     torch.cuda.synchronize()
