@@ -830,24 +830,36 @@ __global__ void k_parity_colors(const int64_t* __restrict__ c, int64_t n, int sh
 
 // fp32 W[Cout][Cin][27] -> per-offset bf16 B images [27][K/KB][N][KB] (swizzled), K permuted to the
 // halo kernel's TMEM A layout
-__global__ void k_pack_halo(const float* __restrict__ w, int cout, int cin, int transpose, uint8_t* __restrict__ img) {
+__global__ void __launch_bounds__(1024) k_pack_halo(const float* __restrict__ w, int cout, int cin, int transpose,
+                                                   uint8_t* __restrict__ img) {
+    // one block per image row n: the row's K x 27 weights are read coalesced into shared memory, then written
+    // as 16-byte swizzle chunks (8 consecutive MMA k of one offset; k -> channel through the K permutation)
+    __shared__ float s[128 * 27];
+    __shared__ int chan[128];
     const int K = transpose ? cout : cin, N = transpose ? cin : cout;
     const int KB = K >= 64 ? 64 : K, rowb = KB * 2;
-    const int64_t total = (int64_t)27 * cout * cin;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t co = t / ((int64_t)cin * 27);
-        const int64_t rem = t - co * cin * 27;
-        const int ci = (int)(rem / 27), d = (int)(rem - (int64_t)ci * 27);
-        const int n = transpose ? ci : (int)co, ch = transpose ? (int)co : ci;
-        const int k = halo_k_of_channel(K, ch);
-        const int kb = k / KB, e = k % KB;
-        const int x = rowb == 128 ? (n & 7) : ((n >> 1) & 3);
-        const size_t off = (size_t)kb * N * rowb + (size_t)n * rowb + (((e >> 3) ^ x) << 4) + (e & 7) * 2;
-        const bf16 v = __float2bfloat16_rn(w[t]);
-        const size_t img_bytes = (size_t)N * K * 2;
-        *reinterpret_cast<bf16*>(img + (size_t)d * img_bytes + off) = v;
-        if (d + 27 < kImgExt) *reinterpret_cast<bf16*>(img + (size_t)(d + 27) * img_bytes + off) = v;
+    const int n = blockIdx.x;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < K * 27; i += blockDim.x) {  // independent loads: keep several in flight  // i = ch * 27 + d
+        const int ch = i / 27, d = i - ch * 27;
+        const int co = transpose ? ch : n, ci = transpose ? n : ch;
+        s[i] = w[((int64_t)co * cin + ci) * 27 + d];
+    }
+    for (int ch = threadIdx.x; ch < K; ch += blockDim.x) chan[halo_k_of_channel(K, ch)] = ch;
+    __syncthreads();
+    const int KC = K / 8, x = rowb == 128 ? (n & 7) : ((n >> 1) & 3);
+    const size_t img_bytes = (size_t)N * K * 2;
+    for (int c = threadIdx.x; c < 27 * KC; c += blockDim.x) {
+        const int d = c / KC, k0 = (c - d * KC) * 8;
+        const int kb = k0 / KB, e = k0 % KB;
+        __nv_bfloat162 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            v[j] = __floats2bfloat162_rn(s[chan[k0 + 2 * j] * 27 + d], s[chan[k0 + 2 * j + 1] * 27 + d]);
+        const size_t off = (size_t)kb * N * rowb + (size_t)n * rowb + (((e >> 3) ^ x) << 4);
+        const uint4 q = *reinterpret_cast<const uint4*>(v);
+        *reinterpret_cast<uint4*>(img + (size_t)d * img_bytes + off) = q;
+        if (d + 27 < kImgExt) *reinterpret_cast<uint4*>(img + (size_t)(d + 27) * img_bytes + off) = q;
     }
 }
 
@@ -984,8 +996,7 @@ extern "C" int fvdb_halo_plan_fill(const int32_t* nbr, int64_t ld, int64_t n_out
 extern "C" int fvdb_pack_weights_halo(const float* w, int cout, int cin, int transpose, void* image, void* stream) {
     const int K = transpose ? cout : cin, N = transpose ? cin : cout;
     if ((K != 32 && K != 64 && K != 128) || (N != 32 && N != 64 && N != 128)) return FVDB_ERR_INVALID;
-    const int64_t total = (int64_t)27 * cout * cin;
-    k_pack_halo<<<(unsigned)ceil_div(total, 256), 256, 0, as_stream(stream)>>>(w, cout, cin, transpose, (uint8_t*)image);
+    k_pack_halo<<<transpose ? cin : cout, 1024, 0, as_stream(stream)>>>(w, cout, cin, transpose, (uint8_t*)image);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

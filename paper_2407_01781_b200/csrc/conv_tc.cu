@@ -318,20 +318,32 @@ __global__ void __launch_bounds__(fwd_threads(NPW), 1)
     }
 }
 
-// fp32 W[Cout][Cin][27] -> per-offset bf16 UMMA B images: [27][K/KB][N rows][KB] swizzled
-__global__ void k_pack_umma(const float* __restrict__ w, int cout, int cin, int transpose, uint8_t* __restrict__ img) {
+// fp32 W[Cout][Cin][27] -> per-offset bf16 UMMA B images: [27][K/KB][N rows][KB] swizzled.  One block per
+// image row n: the row's K x 27 weights are read coalesced into shared memory, then written as 16-byte
+// swizzle chunks (8 consecutive k of one offset d).
+__global__ void __launch_bounds__(1024) k_pack_umma(const float* __restrict__ w, int cout, int cin, int transpose,
+                                                   uint8_t* __restrict__ img) {
+    __shared__ float s[128 * 27];
     const int K = transpose ? cout : cin, N = transpose ? cin : cout;
     const int KB = K >= 64 ? 64 : K, rowb = KB * 2;
-    const int64_t total = (int64_t)27 * cout * cin;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t co = t / ((int64_t)cin * 27);
-        int64_t rem = t - co * cin * 27;
-        int ci = (int)(rem / 27), d = (int)(rem - (int64_t)ci * 27);
-        int n = transpose ? ci : (int)co, k = transpose ? (int)co : ci;
-        int kb = k / KB, e = k % KB;
-        size_t off = (size_t)d * N * K * 2 + (size_t)kb * N * rowb + swz_off(n, e >> 3, rowb) + (e & 7) * 2;
-        *reinterpret_cast<bf16*>(img + off) = __float2bfloat16_rn(w[t]);
+    const int n = blockIdx.x;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < K * 27; i += blockDim.x) {  // independent loads: keep several in flight  // i = k * 27 + d
+        const int k = i / 27, d = i - k * 27;
+        const int co = transpose ? k : n, ci = transpose ? n : k;
+        s[i] = w[((int64_t)co * cin + ci) * 27 + d];
+    }
+    __syncthreads();
+    const int KC = K / 8;
+    for (int c = threadIdx.x; c < 27 * KC; c += blockDim.x) {
+        const int d = c / KC, k0 = (c - d * KC) * 8;
+        const int kb = k0 / KB, e = k0 % KB;
+        __nv_bfloat162 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            v[j] = __floats2bfloat162_rn(s[(k0 + 2 * j) * 27 + d], s[(k0 + 2 * j + 1) * 27 + d]);
+        const size_t off = (size_t)d * N * K * 2 + (size_t)kb * N * rowb + swz_off(n, e >> 3, rowb);
+        *reinterpret_cast<uint4*>(img + off) = *reinterpret_cast<const uint4*>(v);
     }
 }
 
@@ -704,8 +716,7 @@ using namespace fvdb;
 extern "C" int fvdb_pack_weights_umma(const float* w, int cout, int cin, int transpose, void* image, void* stream) {
     const int K = transpose ? cout : cin, N = transpose ? cin : cout;
     if ((K != 32 && K != 64 && K != 128) || (N != 32 && N != 64 && N != 128)) return FVDB_ERR_INVALID;
-    int64_t total = (int64_t)27 * cout * cin;
-    k_pack_umma<<<(unsigned)ceil_div(total, 256), 256, 0, as_stream(stream)>>>(w, cout, cin, transpose, (uint8_t*)image);
+    k_pack_umma<<<N, 1024, 0, as_stream(stream)>>>(w, cout, cin, transpose, (uint8_t*)image);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
