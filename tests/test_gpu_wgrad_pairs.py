@@ -111,3 +111,15 @@ def test_policy(maps, monkeypatch):
     assert not wgrad_pairs_enabled(sparse, 128, 128)
     monkeypatch.setenv("FVDB_WG_PAIRS", "force")
     assert not wgrad_pairs_enabled(km1.fwd, 64, 64) and wgrad_pairs_enabled(km1.fwd, 64, 128)
+
+
+def test_wgrad_pairs_wide_channel_blocks(maps, monkeypatch):
+    """Cin = 256 is split into 128-channel blocks (conv.wgrad); each block runs the pair kernel."""
+    g, go_grid, km, (ins, outs) = maps["s2"]
+    rng = np.random.default_rng(3)
+    x = rng.normal(size=(g.num_voxels, 256)).astype(np.float32)
+    gy = rng.normal(size=(go_grid.num_voxels, 64)).astype(np.float32)
+    _, gw_r = O.conv_backward(ins, outs, bf16_round(gy), bf16_round(x), np.zeros((64, 256, 3, 3, 3)))
+    monkeypatch.setenv("FVDB_WG_PAIRS", "force")
+    gw = wgrad(torch.from_numpy(x).cuda().to(torch.bfloat16), torch.from_numpy(gy).cuda().to(torch.bfloat16), km.fwd)
+    assert tuple(gw.shape) == (64, 256, 3, 3, 3) and rel(gw, gw_r) < 2e-5
