@@ -656,13 +656,14 @@ __global__ void k_signature(const int32_t* __restrict__ nbr, int64_t ld, int64_t
     }
 }
 // nbrP[d][i] = nbr[d][perm[i]] for i < n_out, -1 in the padding
+// blockIdx.y = offset d (no 64-bit division per element); coalesced perm reads and table writes
 __global__ void k_permute_table(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out,
                                 const int32_t* __restrict__ perm, int32_t* __restrict__ nbrP) {
-    const int64_t total = 27 * ld;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t d = t / ld, i = t - d * ld;
-        nbrP[t] = i < n_out ? nbr[d * ld + perm[i]] : -1;
-    }
+    const int64_t d = blockIdx.y;
+    const int32_t* src = nbr + d * ld;
+    int32_t* dst = nbrP + d * ld;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ld; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = i < n_out ? src[perm[i]] : -1;
 }
 
 template <int CIN, int COUT>
@@ -807,9 +808,8 @@ extern "C" int fvdb_kmap_signature_order(const int32_t* nbr, int64_t ld, int64_t
         k_signature<<<g, 256, 0, st>>>(nbr, ld, n_out, key, val);
         FVDB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmpp, tmp, key, skey, val, perm, (int)n_out, 0, 27, st));
     }
-    const int64_t total = 27 * ld;
-    const unsigned g2 = (unsigned)(ceil_div(total, 256) < 8192 ? ceil_div(total, 256) : 8192);
-    k_permute_table<<<g2, 256, 0, st>>>(nbr, ld, n_out, perm, nbr_perm);
+    const unsigned g2 = (unsigned)(ceil_div(ld, 256) < 1024 ? ceil_div(ld, 256) : 1024);
+    k_permute_table<<<dim3(g2, 27), 256, 0, st>>>(nbr, ld, n_out, perm, nbr_perm);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

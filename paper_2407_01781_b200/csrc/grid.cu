@@ -203,13 +203,15 @@ __global__ void k_compact(const int32_t* __restrict__ nbr, int64_t ld, int64_t n
     }
 }
 
+// blockIdx.y = offset d: no 64-bit division per element
 __global__ void k_transpose(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out, int32_t* __restrict__ nbrT,
                             int64_t ldT) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 27 * n_out;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t d = t / n_out, o = t - d * n_out;
-        int32_t v = nbr[d * ld + o];
-        if (v >= 0) nbrT[d * ldT + v] = (int32_t)o;
+    const int64_t d = blockIdx.y;
+    const int32_t* src = nbr + d * ld;
+    int32_t* dst = nbrT + d * ldT;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n_out; o += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = src[o];
+        if (v >= 0) dst[v] = (int32_t)o;
     }
 }
 
@@ -320,7 +322,8 @@ extern "C" int fvdb_kmap_transpose(const int32_t* nbr, int64_t ld, int64_t n_out
     if (ldT < n_in || ld < n_out) return FVDB_ERR_INVALID;
     if (ldT > 0) FVDB_CUDA_TRY(cudaMemsetAsync(nbrT, 0xFF, (size_t)27 * ldT * sizeof(int32_t), st));
     if (n_out == 0 || n_in == 0) return FVDB_OK;
-    k_transpose<<<grid_for(27 * n_out), kThreads, 0, st>>>(nbr, ld, n_out, nbrT, ldT);
+    const unsigned gx = (unsigned)(ceil_div(n_out, kThreads) < 1024 ? ceil_div(n_out, kThreads) : 1024);
+    k_transpose<<<dim3(gx, 27), kThreads, 0, st>>>(nbr, ld, n_out, nbrT, ldT);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
