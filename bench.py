@@ -432,7 +432,8 @@ def run_e2e(args, P, torch, dist, grid, km, cin, cout, dev, use_dist):
     """
     n = grid.num_voxels
     gb = P.GridBatch([grid])
-    gb._kmaps[(id(gb), 1)] = km
+    from paper_2407_01781_b200.conv import cache_batch_kernel_map
+    cache_batch_kernel_map(gb, gb, 1, km)
     m = P.SparseConv3d(cin, cout).to(dev)
     rng = np.random.default_rng(7)
     steps = args.e2e_steps or max(3, min(args.steps, 50))  # long enough that pipeline fill / drain amortise

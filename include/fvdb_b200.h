@@ -32,6 +32,7 @@ extern "C" {
 #define FVDB_ERR_NONFINITE (-4)    /* non-finite point; detail = first bad row (build.py:226-229) */
 #define FVDB_ERR_CUDA (-5)         /* CUDA runtime error; see fvdb_last_error() */
 #define FVDB_ERR_WORKSPACE (-6)    /* workspace smaller than the *_workspace_bytes() query */
+#define FVDB_ERR_UNSUPPORTED (-7)  /* input this entry point does not handle; the caller has another path */
 
 /* Neighbour tables nbr[27][ld] are row-padded: ld is a multiple of FVDB_NBR_ALIGN and the
  * padding columns hold -1, so the tensor-core kernels can stream whole 512-row index blocks. */
@@ -99,6 +100,19 @@ int fvdb_build_plan2(const int64_t* coords, int64_t n, const int64_t* pending_no
                      size_t workspace_bytes, int64_t* counts, int64_t* detail, void* stream);
 int fvdb_build_fill(void* workspace, size_t workspace_bytes, int64_t n, const int64_t* counts,
                     const fvdb_grid_arrays* out, void* stream);
+/* Batched build: B grids from one jagged coordinate array (element b = rows [row_off[b], row_off[b+1]),
+ * row_off DEVICE int64 [B+1], every element non-empty) in one device pass.  Each element's grid is
+ * bit-identical to its standalone build.  counts (host) [B][4] = per-element {num_upper, num_lower,
+ * num_leaf, num_voxels}; fill writes batch-concatenated arrays: element b's nodes follow element b-1's,
+ * and upper/lower_child_starts hold U + B / Lo + B entries (element b's slice starts at its first node + b
+ * and ends with its own terminator).  Errors: as fvdb_build_plan2 (detail = batch-global row) and the root
+ * limit per element (detail = that element's tile count). */
+size_t fvdb_build_batch_workspace_bytes(int64_t n_coords, int64_t B);
+int fvdb_build_batch_plan(const int64_t* coords, int64_t n, const int64_t* row_off, int64_t B,
+                          const int64_t* pending_nonfinite, void* workspace, size_t workspace_bytes,
+                          int64_t* counts, int64_t* detail, void* stream);
+int fvdb_build_batch_fill(void* workspace, size_t workspace_bytes, int64_t n, int64_t B, const int64_t* counts,
+                          const fvdb_grid_arrays* out, void* stream);
 /* a6: coarsen input — floor_divide(coords, factor) (build.py:325-339) */
 int fvdb_floor_div_coords(const int64_t* coords, int64_t n, int64_t factor, int64_t* out,
                           void* stream);
@@ -116,6 +130,19 @@ size_t fvdb_kmap_workspace_bytes(int64_t num_leaf_out);
 int fvdb_kernel_map(const fvdb_grid_view* grid_in, const fvdb_grid_view* grid_out, int stride,
                     int32_t* nbr, int64_t ld, int64_t* pair_counts, void* workspace,
                     size_t workspace_bytes, void* stream);
+/* Batched kernel map (conv_batch, conv.py:371-383: one map per element, concatenated): B (input, output)
+ * grid pairs in one pass.  grid_in / grid_out / in_base / out_base are HOST arrays of B entries; element
+ * b's pairs are written as in_base[b] + local input row into columns out_base[b] + local output row
+ * (leaf_value_offset - 1) of one batch-global table; the caller keeps those column ranges disjoint and
+ * inside [0, sum of grid_out[b].num_voxels), which is where padding starts.  A grid_out view may cover a
+ * leaf range of a grid (leaf pointers advanced by l0, num_leaf / num_voxels of the range) with out_base =
+ * -(its first row): the kernel map of one output-row shard (dist.RowShard).  pair_counts[27] (device)
+ * sums over the batch.  Workspace: fvdb_kmap_workspace_bytes(total output leaves).  3 launches per 32
+ * elements. */
+int fvdb_kernel_map_batch(const fvdb_grid_view* grid_in, const fvdb_grid_view* grid_out, int64_t B,
+                          const int64_t* in_base, const int64_t* out_base, int stride, int32_t* nbr,
+                          int64_t ld, int64_t* pair_counts, void* workspace, size_t workspace_bytes,
+                          void* stream);
 /* per-offset (in_rows, out_rows) lists, concatenated in offset order, out ascending */
 size_t fvdb_kmap_compact_workspace_bytes(int64_t n_out);
 int fvdb_kmap_compact(const int32_t* nbr, int64_t ld, int64_t n_out, int64_t* in_rows,

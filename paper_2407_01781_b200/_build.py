@@ -51,8 +51,13 @@ def build(force: bool = False, verbose: bool = True) -> pathlib.Path:
     objdir.mkdir(exist_ok=True)
     cc = nvcc()
 
+    headers = list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "fvdb_b200.h"]
+    newest_header = max(h.stat().st_mtime for h in headers)
+
     def compile_one(src: pathlib.Path):
         obj = objdir / (src.stem + ".o")
+        if not force and obj.exists() and obj.stat().st_mtime > max(src.stat().st_mtime, newest_header):
+            return obj, ""
         cmd = [cc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -21,6 +21,7 @@ FVDB_ERR_ROOT_LIMIT = -3
 FVDB_ERR_NONFINITE = -4
 FVDB_ERR_CUDA = -5
 FVDB_ERR_WORKSPACE = -6
+FVDB_ERR_UNSUPPORTED = -7
 
 DTYPE_F32, DTYPE_F64, DTYPE_BF16 = 0, 1, 2
 NBR_ALIGN = 512  # FVDB_NBR_ALIGN
@@ -62,11 +63,16 @@ SIGNATURES = {
     "fvdb_build_plan2": (_i32, [_vp, _i64, _vp, _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
     "fvdb_quantize_points_async": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp]),
     "fvdb_build_fill": (_i32, [_vp, _sz, _i64, C.POINTER(_i64), C.POINTER(GridArrays), _vp]),
+    "fvdb_build_batch_workspace_bytes": (_sz, [_i64, _i64]),
+    "fvdb_build_batch_plan": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "fvdb_build_batch_fill": (_i32, [_vp, _sz, _i64, _i64, C.POINTER(_i64), C.POINTER(GridArrays), _vp]),
     "fvdb_floor_div_coords": (_i32, [_vp, _i64, _i64, _vp, _vp]),
     "fvdb_coord_to_index": (_i32, [C.POINTER(GridView), _vp, _i64, _vp, _vp]),
     "fvdb_active_coords": (_i32, [C.POINTER(GridView), _vp, _vp]),
     "fvdb_kmap_workspace_bytes": (_sz, [_i64]),
     "fvdb_kernel_map": (_i32, [C.POINTER(GridView), C.POINTER(GridView), _i32, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "fvdb_kernel_map_batch": (_i32, [C.POINTER(GridView), C.POINTER(GridView), _i64, C.POINTER(_i64),
+                                     C.POINTER(_i64), _i32, _vp, _i64, _vp, _vp, _sz, _vp]),
     "fvdb_kmap_compact_workspace_bytes": (_sz, [_i64]),
     "fvdb_kmap_compact": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "fvdb_kmap_transpose": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp]),

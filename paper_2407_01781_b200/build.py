@@ -38,10 +38,10 @@ class BuildStats:
         return sum(self.phase_seconds.values())
 
 
-def _alloc_arrays(counts, device):
+def _alloc_arrays(counts, device, extra_starts=1):
     nu, nlo, nl = counts[0], counts[1], counts[2]
-    shapes = {"tile_keys": (nu,), "upper_origins": (nu, 3), "upper_child_starts": (nu + 1,),
-              "lower_offset_in_upper": (nlo,), "lower_origins": (nlo, 3), "lower_child_starts": (nlo + 1,),
+    shapes = {"tile_keys": (nu,), "upper_origins": (nu, 3), "upper_child_starts": (nu + extra_starts,),
+              "lower_offset_in_upper": (nlo,), "lower_origins": (nlo, 3), "lower_child_starts": (nlo + extra_starts,),
               "leaf_offset_in_lower": (nl,), "leaf_keys": (nl,), "leaf_origins": (nl, 3),
               "leaf_masks": (nl, 8), "leaf_prefix": (nl,), "leaf_value_offset": (nl,)}
     return {f: torch.empty(shapes[f], dtype=_TORCH_DTYPES[f], device=device) for f in ARRAY_FIELDS}
@@ -63,15 +63,7 @@ def _build_device(c: torch.Tensor, transform, name, stats: BuildStats, pending=N
     counts = (C.c_int64 * 4)()
     detail = C.c_int64(0)
     rc = L.fvdb_build_plan2(c.data_ptr(), n, _lib.ptr(pending), ws.data_ptr(), ws_bytes, counts, C.byref(detail), st)
-    if rc == _lib.FVDB_ERR_NONFINITE:
-        row = int(detail.value)
-        raise ValueError(f"non-finite point at row {row}: {points[row].tolist()}")
-    if rc == _lib.FVDB_ERR_COORD_RANGE:
-        row = int(detail.value)
-        raise ValueError(f"coordinate out of range at row {row}: {tuple(c[row].tolist())} "
-                         f"(components must be within +-{COORD_LIMIT})")
-    if rc == _lib.FVDB_ERR_ROOT_LIMIT:
-        raise ValueError(f"root table limit exceeded: {int(detail.value)} tiles > {ROOT_TABLE_LIMIT}")
+    _raise_build_error(rc, detail.value, c, points)
     _lib.check(rc, "build_plan")
     t1 = time.perf_counter()
     cnt = [int(x) for x in counts]
@@ -85,11 +77,135 @@ def _build_device(c: torch.Tensor, transform, name, stats: BuildStats, pending=N
     return IndexGrid(num_voxels=cnt[3], transform=transform, name=name, **arrays)
 
 
+def _raise_build_error(rc, detail, c, points=None):
+    if rc == _lib.FVDB_ERR_NONFINITE:
+        row = int(detail)
+        raise ValueError(f"non-finite point at row {row}: {points[row].tolist()}")
+    if rc == _lib.FVDB_ERR_COORD_RANGE:
+        row = int(detail)
+        raise ValueError(f"coordinate out of range at row {row}: {tuple(c[row].tolist())} "
+                         f"(components must be within +-{COORD_LIMIT})")
+    if rc == _lib.FVDB_ERR_ROOT_LIMIT:
+        raise ValueError(f"root table limit exceeded: {int(detail)} tiles > {ROOT_TABLE_LIMIT}")
+
+
+def _batch_offsets(jt):
+    off = jt.joffsets.to("cpu")
+    return [int(v) for v in off[:, 0].tolist()] + [int(off[-1, 1])]
+
+
+def _build_batch_device(c: torch.Tensor, bounds, transform, names, stats, pending=None, points=None):
+    """One device pass building every element of a jagged coordinate array (fvdb_build_batch_plan/fill).
+
+    ``bounds``: host row offsets [B+1].  Empty elements become empty grids; each other element's arrays
+    are views into one batch-concatenated allocation and are bit-identical to its standalone build.
+    Falls back to per-element builds when the tile keys are too wide for the batched sort key."""
+    from .jagged import GridBatch
+    B = len(bounds) - 1
+    names = list(names) if names is not None else [""] * B
+    keep = [b for b in range(B) if bounds[b + 1] > bounds[b]]
+    grids = [None] * B
+    if keep:
+        L = _lib.lib()
+        dev = c.device
+        st = _lib.stream_ptr()
+        sel = [bounds[b] for b in keep] + [bounds[keep[-1] + 1]]
+        row_off = torch.tensor(sel, dtype=torch.int64).to(dev, non_blocking=False)
+        nb = len(keep)
+        n = int(c.shape[0])
+        t0 = time.perf_counter()
+        wsb = L.fvdb_build_batch_workspace_bytes(n, nb)
+        ws = _lib.workspace(wsb, dev)
+        counts = (C.c_int64 * (4 * nb))()
+        detail = C.c_int64(0)
+        rc = L.fvdb_build_batch_plan(c.data_ptr(), n, row_off.data_ptr(), nb, _lib.ptr(pending), ws.data_ptr(), wsb,
+                                     counts, C.byref(detail), st)
+        if rc == _lib.FVDB_ERR_UNSUPPORTED:
+            for b in keep:  # tile keys too wide for one batched sort key: element by element
+                cb = c[bounds[b]:bounds[b + 1]]
+                grids[b] = _build_device(cb, transform, names[b], BuildStats(input_count=int(cb.shape[0])))
+            stats.unique_count = sum(grids[b].num_voxels for b in keep)
+            stats.num_upper = sum(grids[b].num_upper_nodes for b in keep)
+            stats.num_lower = sum(grids[b].num_lower_nodes for b in keep)
+            stats.num_leaf = sum(grids[b].num_leaf_nodes for b in keep)
+            stats.phase_seconds["per_element"] = time.perf_counter() - t0
+        else:
+            _raise_build_error(rc, detail.value, c, points)
+            _lib.check(rc, "build_batch_plan")
+            t1 = time.perf_counter()
+            per = [[int(counts[4 * i + k]) for k in range(4)] for i in range(nb)]
+            tot = [sum(p[k] for p in per) for k in range(4)]
+            arrays = _alloc_arrays(tot, dev, extra_starts=nb)
+            ga = _lib.GridArrays(**{f: arrays[f].data_ptr() for f in ARRAY_FIELDS})
+            _lib.check(L.fvdb_build_batch_fill(ws.data_ptr(), wsb, n, nb, counts, C.byref(ga), st), "build_batch_fill")
+            stats.phase_seconds["plan"] = t1 - t0
+            stats.phase_seconds["fill"] = time.perf_counter() - t1
+            base = [0, 0, 0, 0]  # upper, lower, leaf, voxel
+            for i, b in enumerate(keep):
+                nu, nlo, nl, nv = per[i]
+                u0, lo0, l0, _ = base
+                sl = {"tile_keys": (u0, u0 + nu), "upper_origins": (u0, u0 + nu),
+                      "upper_child_starts": (u0 + i, u0 + i + nu + 1), "lower_offset_in_upper": (lo0, lo0 + nlo),
+                      "lower_origins": (lo0, lo0 + nlo), "lower_child_starts": (lo0 + i, lo0 + i + nlo + 1),
+                      "leaf_offset_in_lower": (l0, l0 + nl), "leaf_keys": (l0, l0 + nl),
+                      "leaf_origins": (l0, l0 + nl), "leaf_masks": (l0, l0 + nl), "leaf_prefix": (l0, l0 + nl),
+                      "leaf_value_offset": (l0, l0 + nl)}
+                grids[b] = IndexGrid(num_voxels=nv, transform=transform, name=names[b],
+                                     **{f: arrays[f][a:e] for f, (a, e) in sl.items()})
+                base = [base[0] + nu, base[1] + nlo, base[2] + nl, base[3] + nv]
+            stats.unique_count, stats.num_upper, stats.num_lower, stats.num_leaf = tot[3], tot[0], tot[1], tot[2]
+    for b in range(B):
+        if grids[b] is None:
+            grids[b] = empty_grid(transform, names[b])
+    return GridBatch(grids)
+
+
+def _jagged_coords(jt):
+    from .jagged import JaggedTensor
+    return isinstance(jt, JaggedTensor)
+
+
+def build_batch_from_coords(coords, transform=None, names=None):
+    """GridBatch of the elements of a jagged ijk array, built in one device pass.
+
+    ``coords``: a JaggedTensor with [ΣN_b, 3] integer jdata.  Element b's grid is bit-identical to
+    ``build_from_coords(coords.element(b), transform)`` (build.py:82-142); the reference assembles the same
+    GridBatch from per-element builds (jagged.py:112-123).  Returns ``(GridBatch, BuildStats)`` (batch
+    totals); errors name the batch-global row."""
+    transform = transform or VoxelTransform.uniform(1.0)
+    bounds = _batch_offsets(coords)
+    c = as_coords(coords.jdata, _device())
+    stats = BuildStats(input_count=int(c.shape[0]))
+    return _build_batch_device(c, bounds, transform, names, stats), stats
+
+
+def build_batch_from_points(points, transform, names=None):
+    """GridBatch from a jagged [ΣN_b, 3] world-point array (build.py:219-230 per element), one device pass:
+    one quantize launch over the batch, then the batched build."""
+    bounds = _batch_offsets(points)
+    p = _points_f64(points.jdata)
+    n = p.shape[0]
+    stats = BuildStats(input_count=int(n))
+    if n == 0:
+        return _build_batch_device(p.new_empty((0, 3), dtype=torch.int64), bounds, transform, names, stats), stats
+    out = torch.empty(3 * n + 1, dtype=torch.int64, device=p.device)  # +1: offending-row slot
+    vs = (C.c_double * 3)(*transform.voxel_size.tolist())
+    og = (C.c_double * 3)(*transform.origin.tolist())
+    _lib.check(_lib.lib().fvdb_quantize_points_async(p.data_ptr(), n, vs, og, out.data_ptr(), _lib.stream_ptr()),
+               "quantize_points")
+    c = out[:3 * n].reshape(n, 3)
+    return _build_batch_device(c, bounds, transform, names, stats, pending=out[3 * n:], points=p), stats
+
+
 def build_from_coords(coords, transform=None, name=""):
     """Grid whose active set is the distinct input coords (build.py:82-142).
 
-    Returns ``(grid, BuildStats)``; coordinates outside ±2^30 raise ValueError naming the row.
+    Returns ``(grid, BuildStats)``; coordinates outside ±2^30 raise ValueError naming the row.  A
+    JaggedTensor of coordinates builds its elements in one device pass and returns a GridBatch
+    (``build_batch_from_coords``).
     """
+    if _jagged_coords(coords):
+        return build_batch_from_coords(coords, transform)
     transform = transform or VoxelTransform.uniform(1.0)
     c = as_coords(coords, _device())
     stats = BuildStats(input_count=int(c.shape[0]))
@@ -137,6 +253,8 @@ def build_from_points(points, transform, name=""):
     The finite check is not synchronised on its own: the build's first read-back reports it (same
     error, same precedence as quantize_points followed by build_from_coords).
     """
+    if _jagged_coords(points):
+        return build_batch_from_points(points, transform)
     p = _points_f64(points)
     n = p.shape[0]
     stats = BuildStats(input_count=int(n))
@@ -170,6 +288,31 @@ def coarsen(grid, factor):
         return empty_grid(tc, grid.name)
     g, _ = build_from_coords(coords, tc, grid.name)
     return g
+
+
+def coarsen_batch(batch, factor):
+    """GridBatch of every element coarsened by ``factor`` (build.py:325-339 per element), one batched build."""
+    from .jagged import GridBatch
+    factor = int(factor)
+    if factor < 1:
+        raise ValueError("coarsening factor must be >= 1")
+    if factor == 1:
+        return GridBatch(list(batch.grids))
+    grids = list(batch.grids)
+    t = grids[0].transform
+    if any(not (np.array_equal(g.transform.voxel_size, t.voxel_size) and np.array_equal(g.transform.origin, t.origin))
+           for g in grids):
+        return GridBatch([coarsen(g, factor) for g in grids])
+    coords = torch.cat([g.active_coords() for g in grids], 0)
+    if coords.shape[0]:
+        out = torch.empty_like(coords)
+        _lib.check(_lib.lib().fvdb_floor_div_coords(coords.data_ptr(), coords.shape[0], factor, out.data_ptr(),
+                                                    _lib.stream_ptr()), "floor_div")
+        coords = out
+    tc = VoxelTransform(t.voxel_size * factor, t.origin + t.voxel_size * (factor - 1) / 2.0)
+    bounds = [0] + np.cumsum([g.num_voxels for g in grids]).tolist()
+    stats = BuildStats(input_count=int(coords.shape[0]))
+    return _build_batch_device(coords, bounds, tc, [g.name for g in grids], stats)
 
 
 def _expand(coords: torch.Tensor, scale: int, lo: int, width: int) -> torch.Tensor:

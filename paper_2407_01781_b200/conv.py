@@ -242,6 +242,15 @@ def _empty_table(n, device):
     return torch.full((27, padded_len(n)), -1, dtype=torch.int32, device=device)
 
 
+def _check_rows(rows, n, what):
+    """Row bounds of a list-constructed map, one device min/max reduction (the kernels trust the table)."""
+    cat = torch.cat([r.reshape(-1) for r in rows]) if rows else torch.zeros(0, dtype=torch.int64)
+    if cat.numel():
+        lo, hi = (int(v) for v in torch.stack([cat.min(), cat.max()]).tolist())
+        if lo < 0 or hi >= n:
+            raise IndexError(f"{what} out of range: values span [{lo}, {hi}] for {n} rows")
+
+
 class KernelMap:
     """Per-offset (input_row, output_row) pairs (conv.py:80-102), device-resident.
 
@@ -265,6 +274,13 @@ class KernelMap:
             t = _empty_table(self.num_out, dev)
             ins = [_to_device_tensor(r, dev, torch.int64) for r in in_rows]
             outs = [_to_device_tensor(r, dev, torch.int64) for r in out_rows]
+            if len(ins) != 27 or len(outs) != 27:
+                raise ValueError(f"a kernel map has 27 offsets, got {len(ins)} in_rows / {len(outs)} out_rows lists")
+            _check_rows(ins, self.num_in, "in_rows")
+            _check_rows(outs, self.num_out, "out_rows")
+            for d in range(27):
+                if ins[d].shape != outs[d].shape:
+                    raise ValueError(f"offset {d}: in_rows and out_rows differ in length")
             for d in range(27):
                 if outs[d].numel():
                     t[d, outs[d]] = ins[d].to(torch.int32)
@@ -385,6 +401,37 @@ def build_kernel_map(grid_in, grid_out, stride=1):
                "kernel_map")
     return KernelMap(num_in=grid_in.num_voxels, num_out=n_out, stride=stride, table=NbrTable(t, n_out),
                      pair_counts=counts, grids=([grid_in], [grid_out]))
+
+
+def build_batch_kernel_map(batch_in, batch_out, stride=1):
+    """Batch-global kernel map of two aligned GridBatches in one device pass (fvdb_kernel_map_batch).
+
+    Element b's map is build_kernel_map(batch_in.grids[b], batch_out.grids[b], stride) with its rows shifted
+    by the batches' voxel offsets: the concatenation conv_batch's per-element loop implies
+    (conv.py:371-383), written straight into one table without per-element maps or a concatenation pass.
+    """
+    stride = int(stride)
+    if stride not in (1, 2):
+        raise ValueError(f"stride must be 1 or 2, got {stride}")
+    gi, go = list(batch_in.grids), list(batch_out.grids)
+    if len(gi) != len(go):
+        raise ValueError(f"grid batches differ in size: {len(gi)} vs {len(go)}")
+    B = len(go)
+    dev = go[0].device
+    n_in, n_out = batch_in.total_voxels, batch_out.total_voxels
+    t = torch.empty((27, padded_len(n_out)), dtype=torch.int32, device=dev)
+    counts = torch.zeros(27, dtype=torch.int64, device=dev)
+    L = _lib.lib()
+    views_in = (_lib.GridView * B)(*[g.view() for g in gi])
+    views_out = (_lib.GridView * B)(*[g.view() for g in go])
+    in_base = (C.c_int64 * B)(*[int(v) for v in batch_in.voxel_joffsets[:, 0].tolist()])
+    out_base = (C.c_int64 * B)(*[int(v) for v in batch_out.voxel_joffsets[:, 0].tolist()])
+    wsb = L.fvdb_kmap_workspace_bytes(sum(g.num_leaf_nodes for g in go))
+    ws = _lib.workspace(wsb, dev)
+    _lib.check(L.fvdb_kernel_map_batch(views_in, views_out, B, in_base, out_base, stride, t.data_ptr(), t.shape[1],
+                                       counts.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()), "kernel_map_batch")
+    return KernelMap(num_in=n_in, num_out=n_out, stride=stride, table=NbrTable(t, n_out), pair_counts=counts,
+                     grids=(gi, go))
 
 
 def batch_kernel_map(kmaps, in_offsets, out_offsets):
@@ -634,6 +681,8 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
         if impl == "auto":  # first uses: gather; reused tables: steady_impl (halo or sorted gather)
             reuse = nbr.uses >= HALO_AFTER_USES or nbr.has_plan(K, N)
             impl = steady_impl(nbr, K, N)[0] if reuse else "gather"
+            if impl == "halo" and n_out >= INT32_ROWS_LIMIT:
+                impl = "gather"
     nbr.uses += 1
     img = w_image if w_image is not None else pack_weights_umma(w, transpose, impl)
     out = torch.empty((n_out, N), dtype=out_dtype, device=x.device)
@@ -659,6 +708,10 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
 WG_PAIRS_BELOW_DENSITY = 11.0  # mean pairs per output row under which the pair-list wgrad runs
 
 
+# int32 positions inside the pair lists, kmap_compact and the halo plan's tile bases (27 * rows + padding)
+INT32_ROWS_LIMIT = (2 ** 31 - 27 * 128) // 27
+
+
 def wgrad_pairs_enabled(nbr: "NbrTable", cin: int, cout: int) -> bool:
     """Run the bf16 weight gradient over per-offset pair lists (fvdb_conv_wgrad_pairs_tc)?
 
@@ -678,6 +731,8 @@ def wgrad_pairs_enabled(nbr: "NbrTable", cin: int, cout: int) -> bool:
     Env FVDB_WG_PAIRS: "0" never, "force" whenever the shape allows.
     """
     if not ((cin == 128 and cout in (32, 64, 128)) or (cout == 128 and cin in (32, 64, 128))):
+        return False
+    if nbr.n >= INT32_ROWS_LIMIT:
         return False
     v = os.environ.get("FVDB_WG_PAIRS")
     if v == "0":
@@ -846,17 +901,39 @@ def conv_batch(batch, features, kernel, variant="igemm"):
     return batch.jagged(gather_conv(feats, km.fwd, w))
 
 
+def cache_batch_kernel_map(batch_in, batch_out, stride, km):
+    """Store ``km`` as the (batch_in -> batch_out, stride) map in ``batch_out``'s cache.
+
+    The entry is keyed by ``id(batch_in)`` but holds a weak reference to ``batch_in`` that every lookup
+    checks, so a new batch that reuses a collected batch's id never gets the old map; entries of
+    collected batches are dropped on the next store."""
+    import weakref
+    cache = batch_out._kmaps
+    for k in [k for k, v in cache.items() if isinstance(v, tuple) and v[0]() is None]:
+        del cache[k]
+    cache[("kmap", id(batch_in), int(stride))] = (weakref.ref(batch_in), km)
+    return km
+
+
+def cached_batch_kernel_map(batch_in, batch_out, stride):
+    v = batch_out._kmaps.get(("kmap", id(batch_in), int(stride)))
+    if v is not None and v[0]() is batch_in:
+        return v[1]
+    return None
+
+
 def batch_grid_kernel_map(batch_in, batch_out, stride):
     """Batch-global kernel map of two aligned GridBatches (cached on ``batch_out``)."""
-    key = (id(batch_in), stride)
-    cached = batch_out._kmaps.get(key)
-    if cached is not None:
-        return cached
-    kms = [build_kernel_map(gi, go, stride) for gi, go in zip(batch_in.grids, batch_out.grids)]
-    km = kms[0] if len(kms) == 1 else batch_kernel_map(kms, batch_in.voxel_joffsets[:, 0].tolist(),
-                                                       batch_out.voxel_joffsets[:, 0].tolist())
-    batch_out._kmaps[key] = km
-    return km
+    km = cached_batch_kernel_map(batch_in, batch_out, stride)
+    if km is not None:
+        return km
+    if len(batch_in.grids) != len(batch_out.grids):
+        raise ValueError(f"grid batches differ in size: {len(batch_in.grids)} vs {len(batch_out.grids)}")
+    if len(batch_in.grids) == 1:
+        km = build_kernel_map(batch_in.grids[0], batch_out.grids[0], stride)
+    else:
+        km = build_batch_kernel_map(batch_in, batch_out, stride)
+    return cache_batch_kernel_map(batch_in, batch_out, stride, km)
 
 
 # ---------------------------------------------------------------------------

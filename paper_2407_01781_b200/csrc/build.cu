@@ -237,6 +237,165 @@ __global__ void k_quantize(const double* __restrict__ p, int64_t n, double vx, d
     }
 }
 
+// ---- batched build (B grids from one jagged coordinate array, one device pass) ----
+// Element b's rows are [row_off[b], row_off[b+1]).  Every element builds exactly the grid its standalone
+// build gives: tile keys are sorted per element through a composite key (element id above the varying tile
+// key bits), voxel keys carry the batch-global tile rank (monotone in (element, local rank)), so one sort
+// orders voxels by element and then by the standalone key; node ids are global and every grid's arrays are
+// the slices between its bases (first unique voxel / leaf / lower / upper of the element).
+
+__device__ __forceinline__ int batch_of_row(const int64_t* __restrict__ off, int B, int64_t r) {
+    int lo = 0, hi = B - 1;  // last b with off[b] <= r
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (__ldg(off + mid) <= r) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void k_tile_keys_batch(const int64_t* __restrict__ coords, int64_t n, const int64_t* __restrict__ off,
+                                  int B, uint64_t* __restrict__ tk, int* __restrict__ row_b, BuildScalars* sc) {
+    uint64_t k_or = 0, k_and = ~0ull;
+    const int64_t lim = (int64_t)1 << 30;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
+        bool bad = (i > lim) | (i < -lim) | (j > lim) | (j < -lim) | (k > lim) | (k < -lim);
+        if (bad) atomicMin(&sc->bad_row, (unsigned long long)r);
+        uint64_t key = tile_key(i, j, k);
+        tk[r] = key;
+        row_b[r] = batch_of_row(off, B, r);
+        k_or |= key;
+        k_and &= key;
+    }
+    typedef cub::BlockReduce<uint64_t, kThreads> BR;
+    __shared__ typename BR::TempStorage t1;
+    uint64_t bo = BR(t1).Reduce(k_or, [](uint64_t a, uint64_t b) { return a | b; });
+    __syncthreads();
+    uint64_t ba = BR(t1).Reduce(k_and, [](uint64_t a, uint64_t b) { return a & b; });
+    if (threadIdx.x == 0) {
+        atomicOr(&sc->key_or, (unsigned long long)bo);
+        atomicAnd(&sc->key_and, (unsigned long long)ba);
+    }
+}
+
+// per-row (element, tile) composite: element id above the rank of the row's tile among the batch's distinct
+// tile keys (gtiles, sorted unsigned); ordering composites orders by element, then by tile key
+__global__ void k_row_composite(const int64_t* __restrict__ coords, int64_t n, const int* __restrict__ row_b,
+                                const uint64_t* __restrict__ gtiles, int64_t ng, int gbits,
+                                uint64_t* __restrict__ rowck) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t gt = (uint64_t)lower_bound_u64(gtiles, ng, tile_key(coords[3 * r], coords[3 * r + 1],
+                                                                             coords[3 * r + 2]));
+        rowck[r] = ((uint64_t)row_b[r] << gbits) | gt;
+    }
+}
+
+// decoded tile keys and owning element of every batch-global root tile; gbits < 0: one tile per element
+__global__ void k_decode_tiles(const uint64_t* __restrict__ ctiles, int64_t n_tiles, const uint64_t* __restrict__ gtiles,
+                               uint64_t key_or, int gbits, uint64_t* __restrict__ tiles, int* __restrict__ tile_grid) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tiles;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        if (gbits < 0) {
+            tiles[t] = key_or;
+            tile_grid[t] = (int)t;
+        } else {
+            const uint64_t c = ctiles[t];
+            tiles[t] = gtiles[c & ((1ull << gbits) - 1ull)];
+            tile_grid[t] = (int)(c >> gbits);
+        }
+    }
+}
+
+// voxel keys with the batch-global tile rank (rank of the row's composite among the distinct composites)
+__global__ void k_voxel_keys_batch(const int64_t* __restrict__ coords, int64_t n, const int* __restrict__ row_b,
+                                   const uint64_t* __restrict__ rowck, const uint64_t* __restrict__ ctiles,
+                                   int64_t n_tiles, int gbits, uint64_t* __restrict__ vk) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
+        uint64_t rank = gbits < 0 ? (uint64_t)row_b[r] : (uint64_t)lower_bound_u64(ctiles, n_tiles, rowck[r]);
+        vk[r] = (rank << 36) | ((uint64_t)upper_off(i, j, k) << 21) |
+                ((uint64_t)lower_off(i, j, k) << 9) | leaf_off(i, j, k);
+    }
+}
+
+// bases[g] = {first unique voxel, leaf, lower, upper} of element g; bases[B] = totals
+__global__ void k_grid_bases(const uint64_t* __restrict__ uvox, int n, const int* __restrict__ n_u,
+                             const int* __restrict__ tile_grid, const int* __restrict__ leaf_id,
+                             const int* __restrict__ lower_id, const int* __restrict__ upper_id, int B,
+                             int64_t* __restrict__ bases) {
+    const int nu = *n_u;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nu; i += gridDim.x * blockDim.x) {
+        const int g = tile_grid[uvox[i] >> 36];
+        if (i == 0 || tile_grid[uvox[i - 1] >> 36] != g) {
+            bases[4 * g + 0] = i;
+            bases[4 * g + 1] = leaf_id[i] - 1;
+            bases[4 * g + 2] = lower_id[i] - 1;
+            bases[4 * g + 3] = upper_id[i] - 1;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        bases[4 * B + 0] = nu;
+        bases[4 * B + 1] = leaf_id[n - 1];
+        bases[4 * B + 2] = lower_id[n - 1];
+        bases[4 * B + 3] = upper_id[n - 1];
+    }
+}
+
+// k_register with grid-local ranks, value offsets and child starts; child-start arrays hold U + B / Lo + B
+// entries (element g's slice starts at its first node + g and ends with its terminator)
+__global__ void k_register_batch(const uint64_t* __restrict__ uvox, int n, const uint64_t* __restrict__ tiles,
+                                 const int* __restrict__ tile_grid, const int* __restrict__ leaf_id,
+                                 const int* __restrict__ lower_id, const int* __restrict__ upper_id,
+                                 const int64_t* __restrict__ bases, fvdb_grid_arrays o) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint64_t v = uvox[i];
+        int leaf = leaf_id[i] - 1;
+        atomicOr((unsigned long long*)&o.leaf_masks[(int64_t)leaf * 8 + ((v >> 6) & 7)], 1ull << (v & 63));
+        uint64_t p = i ? uvox[i - 1] : ~v;
+        if ((v >> 9) == (p >> 9)) continue;  // not a leaf head
+        const uint64_t t = v >> 36;
+        const int g = tile_grid[t];
+        const int64_t* gb = bases + 4 * g;
+        const uint64_t local_rank = t - (uint64_t)gb[3];
+        uint64_t tkey = tiles[t];
+        int64_t ox = tile_field_origin(tkey, 42), oy = tile_field_origin(tkey, 21), oz = tile_field_origin(tkey, 0);
+        uint32_t up = (uint32_t)((v >> 21) & 0x7FFF), lo = (uint32_t)((v >> 9) & 0xFFF);
+        int64_t lx = ox + ((int64_t)((up >> 10) & 31) << 7), ly = oy + ((int64_t)((up >> 5) & 31) << 7),
+                lz = oz + ((int64_t)(up & 31) << 7);
+        o.leaf_keys[leaf] = (local_rank << 27) | ((v >> 9) & 0x7FFFFFFull);
+        o.leaf_offset_in_lower[leaf] = (uint16_t)lo;
+        o.leaf_value_offset[leaf] = (uint64_t)(i - gb[0]) + 1;
+        o.leaf_origins[3 * (int64_t)leaf + 0] = lx + ((int64_t)((lo >> 8) & 15) << 3);
+        o.leaf_origins[3 * (int64_t)leaf + 1] = ly + ((int64_t)((lo >> 4) & 15) << 3);
+        o.leaf_origins[3 * (int64_t)leaf + 2] = lz + ((int64_t)(lo & 15) << 3);
+        if ((v >> 21) == (p >> 21)) continue;  // not a lower head
+        int lower = lower_id[i] - 1;
+        o.lower_child_starts[lower + g] = leaf - gb[1];
+        o.lower_offset_in_upper[lower] = (uint16_t)up;
+        o.lower_origins[3 * (int64_t)lower + 0] = lx;
+        o.lower_origins[3 * (int64_t)lower + 1] = ly;
+        o.lower_origins[3 * (int64_t)lower + 2] = lz;
+        if ((v >> 36) == (p >> 36)) continue;  // not an upper head
+        int upper = upper_id[i] - 1;
+        o.upper_child_starts[upper + g] = lower - gb[2];
+        o.tile_keys[upper] = tkey;
+        o.upper_origins[3 * (int64_t)upper + 0] = ox;
+        o.upper_origins[3 * (int64_t)upper + 1] = oy;
+        o.upper_origins[3 * (int64_t)upper + 2] = oz;
+    }
+}
+
+__global__ void k_child_terminators(const int64_t* __restrict__ bases, int B, fvdb_grid_arrays o) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < B; g += gridDim.x * blockDim.x) {
+        const int64_t* a = bases + 4 * g;
+        const int64_t* e = bases + 4 * (g + 1);
+        o.lower_child_starts[e[2] + g] = e[1] - a[1];
+        o.upper_child_starts[e[3] + g] = e[2] - a[2];
+    }
+}
+
 int grid_for(int64_t n) {
     int64_t b = ceil_div(n > 0 ? n : 1, kThreads);
     return (int)(b < 148 * 16 ? b : 148 * 16);
@@ -363,6 +522,177 @@ extern "C" int fvdb_build_fill(void* workspace, size_t ws_bytes, int64_t n, cons
     const int gu = grid_for(nu);
     k_register<<<gu, kThreads, 0, st>>>(w.uvox, nu, w.tiles, w.leaf_id, w.lower_id, w.upper_id, *out,
                                         n_leaf, n_lower, n_upper);
+    k_leaf_prefix<<<grid_for(n_leaf), kThreads, 0, st>>>(out->leaf_masks, n_leaf, out->leaf_prefix);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+
+// ---- batched build entry points ----
+struct BatchWs {
+    BuildWs w;
+    uint64_t *ctiles, *gtiles, *rowck;
+    int *row_b, *tile_grid;
+    int64_t* bases;
+};
+
+template <class C>
+void carve_batch(C& c, int64_t n, int64_t B, size_t cub_bytes, BatchWs* bw) {
+    carve(c, n, cub_bytes, &bw->w);
+    size_t m = (size_t)(n > 0 ? n : 1);
+    if constexpr (std::is_same_v<C, Carver>) {
+        bw->ctiles = c.template take<uint64_t>(m);
+        bw->gtiles = c.template take<uint64_t>(m);
+        bw->rowck = c.template take<uint64_t>(m);
+        bw->row_b = c.template take<int>(m);
+        bw->tile_grid = c.template take<int>(m);
+        bw->bases = c.template take<int64_t>(4 * (size_t)(B + 1));
+    } else {
+        for (int i = 0; i < 3; ++i) c.template take<uint64_t>(m);
+        c.template take<int>(m);
+        c.template take<int>(m);
+        c.template take<int64_t>(4 * (size_t)(B + 1));
+    }
+}
+
+extern "C" size_t fvdb_build_batch_workspace_bytes(int64_t n, int64_t B) {
+    Sizer s;
+    BatchWs w;
+    carve_batch(s, n, B, cub_temp_bytes((int)(n > 0 ? n : 1)), &w);
+    return s.used + 256;
+}
+
+// counts (host) [B][4] = {num_upper, num_lower, num_leaf, num_voxels} per element.  Every element must be
+// non-empty (row_off strictly ascending).  Three host read-backs (four when the coordinates span several root
+// tiles).
+extern "C" int fvdb_build_batch_plan(const int64_t* coords, int64_t n, const int64_t* row_off, int64_t B,
+                                     const int64_t* pending_nonfinite, void* workspace, size_t ws_bytes,
+                                     int64_t* counts, int64_t* detail, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n <= 0 || n >= (int64_t)INT32_MAX || B < 1 || B > n) return FVDB_ERR_INVALID;
+    Carver c(workspace, ws_bytes);
+    BatchWs bw;
+    carve_batch(c, n, B, cub_temp_bytes((int)n), &bw);
+    if (!c.ok()) return FVDB_ERR_WORKSPACE;
+    BuildWs& w = bw.w;
+    const int g = grid_for(n);
+
+    k_init_scalars<<<1, 1, 0, st>>>(w.sc);
+    k_tile_keys_batch<<<g, kThreads, 0, st>>>(coords, n, row_off, (int)B, w.tk, bw.row_b, w.sc);
+    FVDB_LAUNCH_CHECK();
+    BuildScalars hs;
+    unsigned long long nonfinite = ~0ull;
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    if (pending_nonfinite)
+        FVDB_CUDA_TRY(cudaMemcpyAsync(&nonfinite, pending_nonfinite, sizeof(nonfinite), cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (nonfinite != ~0ull) {
+        *detail = (int64_t)nonfinite;
+        return FVDB_ERR_NONFINITE;
+    }
+    if (hs.bad_row != ~0ull) {
+        *detail = (int64_t)hs.bad_row;
+        return FVDB_ERR_COORD_RANGE;
+    }
+
+    // batch-global root tiles, sorted by (element, tile key): the batch's distinct tile keys (sorted over the
+    // varying bits), then the distinct (element, tile rank) composites
+    int64_t n_tiles = B;
+    int gbits = -1;
+    const uint64_t diff = hs.key_or ^ hs.key_and;
+    if (diff != 0) {
+        const int lo_bit = __builtin_ctzll(diff), hi_bit = bit_length(diff);
+        cub::DoubleBuffer<uint64_t> db(w.tk, w.tk_alt);
+        size_t tb = w.cub_bytes;
+        FVDB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, db, (int)n, lo_bit, hi_bit, st));
+        tb = w.cub_bytes;
+        FVDB_CUDA_TRY(cub::DeviceSelect::Unique(w.cub_tmp, tb, db.Current(), bw.gtiles, w.n_sel, (int)n, st));
+        int ng = 0;
+        FVDB_CUDA_TRY(cudaMemcpyAsync(&ng, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
+        FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+        gbits = bit_length((uint64_t)(ng - 1));
+        const int bb = bit_length((uint64_t)(B - 1));
+        k_row_composite<<<g, kThreads, 0, st>>>(coords, n, bw.row_b, bw.gtiles, ng, gbits, bw.rowck);
+        FVDB_CUDA_TRY(cudaMemcpyAsync(w.tk, bw.rowck, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+        cub::DoubleBuffer<uint64_t> cb(w.tk, w.tk_alt);
+        tb = w.cub_bytes;
+        if (gbits + bb > 0)
+            FVDB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, cb, (int)n, 0, gbits + bb, st));
+        tb = w.cub_bytes;
+        FVDB_CUDA_TRY(cub::DeviceSelect::Unique(w.cub_tmp, tb, cb.Current(), bw.ctiles, w.n_sel, (int)n, st));
+        int nt = 0;
+        FVDB_CUDA_TRY(cudaMemcpyAsync(&nt, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
+        FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+        n_tiles = nt;
+    }
+    k_decode_tiles<<<grid_for(n_tiles), kThreads, 0, st>>>(bw.ctiles, n_tiles, bw.gtiles, hs.key_or, gbits, w.tiles,
+                                                           bw.tile_grid);
+    k_voxel_keys_batch<<<g, kThreads, 0, st>>>(coords, n, bw.row_b, bw.rowck, bw.ctiles, n_tiles, gbits, w.vk);
+    FVDB_LAUNCH_CHECK();
+    int end_bit = 36 + bit_length((uint64_t)(n_tiles - 1));
+    cub::DoubleBuffer<uint64_t> vb(w.vk, w.vk_alt);
+    size_t tb = w.cub_bytes;
+    FVDB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, vb, (int)n, 0, end_bit, st));
+    tb = w.cub_bytes;
+    FVDB_CUDA_TRY(cub::DeviceSelect::Unique(w.cub_tmp, tb, vb.Current(), w.uvox, w.n_sel, (int)n, st));
+    k_node_heads<<<g, kThreads, 0, st>>>(w.uvox, (int)n, w.n_sel, w.leaf_id, w.lower_id, w.upper_id);
+    FVDB_LAUNCH_CHECK();
+    int* ids[3] = {w.leaf_id, w.lower_id, w.upper_id};
+    for (int t = 0; t < 3; ++t) {
+        tb = w.cub_bytes;
+        FVDB_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, ids[t], ids[t], (int)n, st));
+    }
+    k_grid_bases<<<g, kThreads, 0, st>>>(w.uvox, (int)n, w.n_sel, bw.tile_grid, w.leaf_id, w.lower_id, w.upper_id,
+                                         (int)B, bw.bases);
+    FVDB_LAUNCH_CHECK();
+    int64_t* hb = new int64_t[4 * (B + 1)];
+    cudaError_t e = cudaMemcpyAsync(hb, bw.bases, sizeof(int64_t) * 4 * (B + 1), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        delete[] hb;
+        set_error("build_batch_plan read-back", e);
+        return FVDB_ERR_CUDA;
+    }
+    int rc = FVDB_OK;
+    for (int64_t b = 0; b < B; ++b) {
+        const int64_t* a = hb + 4 * b;
+        const int64_t* z = hb + 4 * (b + 1);
+        counts[4 * b + 0] = z[3] - a[3];
+        counts[4 * b + 1] = z[2] - a[2];
+        counts[4 * b + 2] = z[1] - a[1];
+        counts[4 * b + 3] = z[0] - a[0];
+        if (counts[4 * b + 0] > ((int64_t)1 << 28) && rc == FVDB_OK) {
+            *detail = counts[4 * b + 0];
+            rc = FVDB_ERR_ROOT_LIMIT;
+        }
+    }
+    if (rc == FVDB_OK && hb[4 * B + 3] != n_tiles) {
+        set_error_msg("internal: batched tile count mismatch");
+        rc = FVDB_ERR_INVALID;
+    }
+    delete[] hb;
+    return rc;
+}
+
+// out: batch-concatenated arrays (sum of the per-element counts; child-start arrays + B entries)
+extern "C" int fvdb_build_batch_fill(void* workspace, size_t ws_bytes, int64_t n, int64_t B, const int64_t* counts,
+                                     const fvdb_grid_arrays* out, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n <= 0 || n >= (int64_t)INT32_MAX || B < 1) return FVDB_ERR_INVALID;
+    Carver c(workspace, ws_bytes);
+    BatchWs bw;
+    carve_batch(c, n, B, cub_temp_bytes((int)n), &bw);
+    if (!c.ok()) return FVDB_ERR_WORKSPACE;
+    BuildWs& w = bw.w;
+    int64_t n_leaf = 0, nu = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        n_leaf += counts[4 * b + 2];
+        nu += counts[4 * b + 3];
+    }
+    FVDB_CUDA_TRY(cudaMemsetAsync(out->leaf_masks, 0, (size_t)n_leaf * 8 * sizeof(uint64_t), st));
+    k_register_batch<<<grid_for(nu), kThreads, 0, st>>>(w.uvox, (int)nu, w.tiles, bw.tile_grid, w.leaf_id,
+                                                        w.lower_id, w.upper_id, bw.bases, *out);
+    k_child_terminators<<<grid_for(B), kThreads, 0, st>>>(bw.bases, (int)B, *out);
     k_leaf_prefix<<<grid_for(n_leaf), kThreads, 0, st>>>(out->leaf_masks, n_leaf, out->leaf_prefix);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;

@@ -74,18 +74,38 @@ __global__ void k_active_coords(fvdb_grid_view g, int64_t* __restrict__ out) {
     }
 }
 
-// tree walk once per (output leaf, neighbour leaf): nleaf[l][e], e over {-1,0,1}^3
-__global__ void k_neighbor_leaves(fvdb_grid_view gin, fvdb_grid_view gout, int stride,
-                                  int32_t* __restrict__ nleaf) {
-    const int64_t total = gout.num_leaf * 27;
+// Grids of one kernel-map launch: B (input, output) grid pairs whose rows are concatenated in a batch-global
+// index space (row = base + grid-local row).  A single grid is B = 1 with zero bases.  Output leaves are
+// numbered globally: leaf_start[b] = output leaves of grids < b.  Passed as a __grid_constant__ parameter,
+// so the per-leaf grid lookup indexes parameter memory (no copy, no device allocation).
+constexpr int kMaxBatch = 32;
+struct KmapBatch {
+    fvdb_grid_view gin[kMaxBatch], gout[kMaxBatch];
+    int64_t in_base[kMaxBatch], out_base[kMaxBatch];
+    int64_t leaf_start[kMaxBatch + 1];
+    int B;
+};
+
+__device__ __forceinline__ int batch_of_leaf(const KmapBatch& kb, int64_t l) {
+    int b = 0;
+    while (b + 1 < kb.B && l >= kb.leaf_start[b + 1]) ++b;
+    return b;
+}
+
+// tree walk once per (output leaf, neighbour leaf): nleaf[l][e] (grid-local leaf of the element's input grid)
+__global__ void k_neighbor_leaves(const __grid_constant__ KmapBatch kb, int stride, int32_t* __restrict__ nleaf) {
+    const int64_t total = kb.leaf_start[kb.B] * 27;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t l = t / 27;
-        int e = (int)(t - l * 27);
+        const int64_t lg = t / 27;
+        const int e = (int)(t - lg * 27);
+        const int b = batch_of_leaf(kb, lg);
+        const fvdb_grid_view& gout = kb.gout[b];
+        const int64_t l = lg - kb.leaf_start[b];
         int64_t bx = stride * gout.leaf_origins[3 * l] + 8 * (e / 9 - 1);
         int64_t by = stride * gout.leaf_origins[3 * l + 1] + 8 * ((e / 3) % 3 - 1);
         int64_t bz = stride * gout.leaf_origins[3 * l + 2] + 8 * (e % 3 - 1);
-        nleaf[t] = (int32_t)find_leaf(gin, bx, by, bz);
+        nleaf[t] = (int32_t)find_leaf(kb.gin[b], bx, by, bz);
     }
 }
 
@@ -94,10 +114,10 @@ __global__ void k_neighbor_leaves(fvdb_grid_view gin, fvdb_grid_view gout, int s
 // coalesced); per-offset pair counts are warp reductions stored per leaf (partial[d][leaf]) and summed by
 // k_pair_counts, instead of shared + global atomics on 27 addresses.
 constexpr int kKmWarps = 9, kKmThreads = kKmWarps * 32;
-__global__ void __launch_bounds__(kKmThreads) k_kernel_map(fvdb_grid_view gin, fvdb_grid_view gout, int stride,
+__global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant__ KmapBatch kb, int stride,
                                                            const int32_t* __restrict__ nleaf,
                                                            int32_t* __restrict__ nbr, int64_t ld,
-                                                           int32_t* __restrict__ partial) {
+                                                           int32_t* __restrict__ partial, int64_t n_leaf_all) {
     __shared__ uint64_t s_mask[27][8];
     __shared__ uint64_t s_pre[27];
     __shared__ int64_t s_vo[27];
@@ -105,18 +125,22 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(fvdb_grid_view gin, f
     __shared__ uint16_t s_pos[512];
     __shared__ uint64_t s_own[8];
 
-    const int64_t l = blockIdx.x;
+    const int64_t lg = blockIdx.x;
+    const int b = batch_of_leaf(kb, lg);
+    const fvdb_grid_view& gin = kb.gin[b];
+    const fvdb_grid_view& gout = kb.gout[b];
+    const int64_t l = lg - kb.leaf_start[b];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid < 27) {
-        int32_t nl = nleaf[l * 27 + tid];
+        int32_t nl = nleaf[lg * 27 + tid];
         s_nl[tid] = nl;
         s_pre[tid] = nl >= 0 ? gin.leaf_prefix[nl] : 0;
-        s_vo[tid] = nl >= 0 ? (int64_t)gin.leaf_value_offset[nl] - 1 : 0;
+        s_vo[tid] = nl >= 0 ? kb.in_base[b] + (int64_t)gin.leaf_value_offset[nl] - 1 : 0;
     }
     if (tid < 8) s_own[tid] = gout.leaf_masks[8 * l + tid];
     for (int q = tid; q < 27 * 8; q += kKmThreads) {
         int e = q >> 3;
-        int32_t nl = nleaf[l * 27 + e];
+        int32_t nl = nleaf[lg * 27 + e];
         s_mask[e][q & 7] = nl >= 0 ? gin.leaf_masks[8 * (int64_t)nl + (q & 7)] : 0ull;
     }
     __syncthreads();
@@ -128,8 +152,7 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(fvdb_grid_view gin, f
     for (int w = 0; w < 8; ++w) nvox += __popcll(s_own[w]);
     __syncthreads();
 
-    const int64_t row0 = (int64_t)gout.leaf_value_offset[l] - 1;
-    const int64_t n_leaf = gout.num_leaf;
+    const int64_t row0 = kb.out_base[b] + (int64_t)gout.leaf_value_offset[l] - 1;
 #pragma unroll
     for (int j = 0; j < 27 / kKmWarps; ++j) {
         const int d = warp + j * kKmWarps;
@@ -144,16 +167,16 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(fvdb_grid_view gin, f
             const int e = ((qx >> 3) + 1) * 9 + ((qy >> 3) + 1) * 3 + ((qz >> 3) + 1);
             int32_t row = -1;
             if (s_nl[e] >= 0) {
-                const uint32_t b = (uint32_t)(((qx & 7) << 6) | ((qy & 7) << 3) | (qz & 7));
-                if ((s_mask[e][b >> 6] >> (b & 63)) & 1ull) {
-                    row = (int32_t)(s_vo[e] + leaf_rank(s_mask[e], s_pre[e], b));
+                const uint32_t bb = (uint32_t)(((qx & 7) << 6) | ((qy & 7) << 3) | (qz & 7));
+                if ((s_mask[e][bb >> 6] >> (bb & 63)) & 1ull) {
+                    row = (int32_t)(s_vo[e] + leaf_rank(s_mask[e], s_pre[e], bb));
                     ++cnt;
                 }
             }
             out[r] = row;
         }
         cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0) partial[(int64_t)d * n_leaf + l] = cnt;
+        if (lane == 0) partial[(int64_t)d * n_leaf_all + lg] = cnt;
     }
 }
 
@@ -268,22 +291,55 @@ extern "C" size_t fvdb_kmap_workspace_bytes(int64_t num_leaf_out) {
 
 extern "C" int fvdb_kernel_map(const fvdb_grid_view* gin, const fvdb_grid_view* gout, int stride, int32_t* nbr,
                                int64_t ld, int64_t* pair_counts, void* ws, size_t ws_bytes, void* stream_) {
+    const int64_t zero = 0;
+    return fvdb_kernel_map_batch(gin, gout, 1, &zero, &zero, stride, nbr, ld, pair_counts, ws, ws_bytes, stream_);
+}
+
+// B grid pairs in one pass (launches per 32 grids): rows of element b are in_base[b] + local input row and
+// out_base[b] + local output row of one batch-global table.
+extern "C" int fvdb_kernel_map_batch(const fvdb_grid_view* gin, const fvdb_grid_view* gout, int64_t B,
+                                     const int64_t* in_base, const int64_t* out_base, int stride, int32_t* nbr,
+                                     int64_t ld, int64_t* pair_counts, void* ws, size_t ws_bytes, void* stream_) {
     cudaStream_t st = as_stream(stream_);
     if (stride != 1 && stride != 2) return FVDB_ERR_INVALID;
-    if (ld < gout->num_voxels) return FVDB_ERR_INVALID;
-    if (ws_bytes < fvdb_kmap_workspace_bytes(gout->num_leaf)) return FVDB_ERR_WORKSPACE;
-    if (ld > gout->num_voxels)
-        k_pad<<<grid_for(27 * (ld - gout->num_voxels)), kThreads, 0, st>>>(nbr, ld, gout->num_voxels);
-    if (gout->num_leaf == 0) {
+    if (B < 1) return FVDB_ERR_INVALID;
+    int64_t n_out = 0, n_leaf = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        if (in_base[b] < 0 || gout[b].num_leaf < 0 || gout[b].num_voxels < 0) return FVDB_ERR_INVALID;
+        n_out += gout[b].num_voxels;
+        n_leaf += gout[b].num_leaf;
+    }
+    if (ld < n_out) return FVDB_ERR_INVALID;
+    if (ws_bytes < fvdb_kmap_workspace_bytes(n_leaf)) return FVDB_ERR_WORKSPACE;
+    if (ld > n_out) k_pad<<<grid_for(27 * (ld - n_out)), kThreads, 0, st>>>(nbr, ld, n_out);
+    if (n_leaf == 0) {
         FVDB_CUDA_TRY(cudaMemsetAsync(pair_counts, 0, 27 * sizeof(int64_t), st));
         return FVDB_OK;
     }
     int32_t* nleaf = reinterpret_cast<int32_t*>(ws);
     int32_t* partial = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(ws) +
-                                                  ((size_t)gout->num_leaf * 27 * sizeof(int32_t) + 255) / 256 * 256);
-    k_neighbor_leaves<<<grid_for(gout->num_leaf * 27), kThreads, 0, st>>>(*gin, *gout, stride, nleaf);
-    k_kernel_map<<<(unsigned)gout->num_leaf, kKmThreads, 0, st>>>(*gin, *gout, stride, nleaf, nbr, ld, partial);
-    k_pair_counts<<<27, 256, 0, st>>>(partial, gout->num_leaf, pair_counts);
+                                                  ((size_t)n_leaf * 27 * sizeof(int32_t) + 255) / 256 * 256);
+    // leaves of every chunk are numbered after the previous chunks', so partial[d][leaf] is one array
+    int64_t leaf0 = 0;
+    for (int64_t c0 = 0; c0 < B; c0 += kMaxBatch) {
+        KmapBatch kb;
+        kb.B = (int)(B - c0 < kMaxBatch ? B - c0 : kMaxBatch);
+        kb.leaf_start[0] = 0;
+        for (int b = 0; b < kb.B; ++b) {
+            kb.gin[b] = gin[c0 + b];
+            kb.gout[b] = gout[c0 + b];
+            kb.in_base[b] = in_base[c0 + b];
+            kb.out_base[b] = out_base[c0 + b];
+            kb.leaf_start[b + 1] = kb.leaf_start[b] + gout[c0 + b].num_leaf;
+        }
+        const int64_t nl = kb.leaf_start[kb.B];
+        if (nl == 0) continue;
+        k_neighbor_leaves<<<grid_for(nl * 27), kThreads, 0, st>>>(kb, stride, nleaf + leaf0 * 27);
+        k_kernel_map<<<(unsigned)nl, kKmThreads, 0, st>>>(kb, stride, nleaf + leaf0 * 27, nbr, ld, partial + leaf0,
+                                                          n_leaf);
+        leaf0 += nl;
+    }
+    k_pair_counts<<<27, 256, 0, st>>>(partial, n_leaf, pair_counts);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

@@ -21,8 +21,9 @@ from torch import nn
 
 from . import _lib
 from .build import coarsen
+from .build import coarsen_batch as _coarsen_batch
 from .conv import batch_grid_kernel_map, gather_conv, wgrad
-from .jagged import GridBatch, JaggedTensor
+from .jagged import GridBatch, JaggedTensor, as_grid_batch
 
 
 def _to_compute(t: torch.Tensor, cdt: torch.dtype) -> torch.Tensor:
@@ -44,14 +45,14 @@ def _grad_dtype(x_dtype: torch.dtype, cdt: torch.dtype) -> torch.dtype:
 
 class _SparseConvFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w, kmap, transposed, cdt):
+    def forward(ctx, x, w, kmap, transposed, cdt, reducer=None):
         xc = _to_compute(x, cdt)
         if transposed:
             y = gather_conv(xc, kmap.bwd, w, transpose=True, out_dtype=cdt)
         else:
             y = gather_conv(xc, kmap.fwd, w, transpose=False, out_dtype=cdt)
         ctx.save_for_backward(xc, w)
-        ctx.kmap, ctx.transposed, ctx.cdt, ctx.x_dtype = kmap, transposed, cdt, x.dtype
+        ctx.kmap, ctx.transposed, ctx.cdt, ctx.x_dtype, ctx.reducer = kmap, transposed, cdt, x.dtype, reducer
         return y
 
     @staticmethod
@@ -61,28 +62,28 @@ class _SparseConvFn(torch.autograd.Function):
         gy = _to_compute(gy, cdt)
         od = _grad_dtype(ctx.x_dtype, cdt)
         gx = gw = None
-        if ctx.transposed:
-            if ctx.needs_input_grad[0]:
-                gx = gather_conv(gy, km.fwd, w, transpose=False, out_dtype=od)
-            if ctx.needs_input_grad[1]:
-                gw = wgrad(gy, xc, km.fwd)
-        else:
-            if ctx.needs_input_grad[0]:
-                gx = gather_conv(gy, km.bwd, w, transpose=True, out_dtype=od)
-            if ctx.needs_input_grad[1]:
-                gw = wgrad(xc, gy, km.fwd)
-        if gx is not None:
-            gx = gx.to(ctx.x_dtype)
-        if gw is not None:
+        # weight gradient first: its data-parallel all-reduce (if any) overlaps the input-gradient kernel
+        if ctx.needs_input_grad[1]:
+            gw = wgrad(gy, xc, km.fwd) if ctx.transposed else wgrad(xc, gy, km.fwd)
             gw = gw.to(w.dtype)
-        return gx, gw, None, None, None
+        handle = ctx.reducer.start(gw) if (ctx.reducer is not None and gw is not None) else None
+        if ctx.needs_input_grad[0]:
+            if ctx.transposed:
+                gx = gather_conv(gy, km.fwd, w, transpose=False, out_dtype=od)
+            else:
+                gx = gather_conv(gy, km.bwd, w, transpose=True, out_dtype=od)
+            gx = gx.to(ctx.x_dtype)
+        if handle is not None:
+            ctx.reducer.wait(handle)
+        return gx, gw, None, None, None, None
 
 
 def coarsen_batch(batch: GridBatch, factor: int = 2) -> GridBatch:
+    """coarsen() of every element (one batched build), cached on the batch."""
     key = ("coarse", factor)
     cached = batch._kmaps.get(key)
     if cached is None:
-        cached = GridBatch([coarsen(g, factor) for g in batch.grids])
+        cached = _coarsen_batch(batch, factor) if batch.num_grids > 1 else GridBatch([coarsen(batch.grids[0], factor)])
         batch._kmaps[key] = cached
     return cached
 
@@ -102,6 +103,7 @@ class SparseConv3d(nn.Module):
         shape = (in_channels, out_channels, 3, 3, 3) if transposed else (out_channels, in_channels, 3, 3, 3)
         self.weight = nn.Parameter(torch.empty(shape, device=device))
         self.bias = nn.Parameter(torch.zeros(out_channels, device=device)) if bias else None
+        self.grad_reducer = None  # dist.attach_grad_reducer: weight-gradient all-reduce inside backward
         self.reset_parameters()
 
     def reset_parameters(self):
@@ -109,8 +111,9 @@ class SparseConv3d(nn.Module):
             self.weight.normal_(0.0, 1.0 / math.sqrt(27 * self.in_channels))
 
     def forward(self, grid: GridBatch, x, out_grid: GridBatch | None = None):
-        if not isinstance(grid, GridBatch):
-            grid = GridBatch([grid])
+        grid = as_grid_batch(grid)
+        if out_grid is not None:
+            out_grid = as_grid_batch(out_grid)
         feats = grid.check_features(x)
         if self.transposed:
             if out_grid is None:
@@ -122,7 +125,7 @@ class SparseConv3d(nn.Module):
         else:
             out_grid = out_grid or grid
             kmap = batch_grid_kernel_map(grid, out_grid, 1)
-        y = _SparseConvFn.apply(feats, self.weight, kmap, self.transposed, self.compute_dtype)
+        y = _SparseConvFn.apply(feats, self.weight, kmap, self.transposed, self.compute_dtype, self.grad_reducer)
         if self.bias is not None:
             y = y + self.bias.to(y.dtype)
         return out_grid, out_grid.jagged(y)

@@ -90,7 +90,7 @@ def _device():
 class IndexGrid:
     """Immutable sparse topology on one CUDA device (topology.py:140-305)."""
 
-    __slots__ = ARRAY_FIELDS + ("num_voxels", "transform", "name", "_view")
+    __slots__ = ARRAY_FIELDS + ("num_voxels", "transform", "name", "_view", "_batch", "__weakref__")
 
     def __init__(self, *, num_voxels, transform, name="", **arrays):
         for f in ARRAY_FIELDS:
@@ -99,6 +99,7 @@ class IndexGrid:
         self.transform = transform
         self.name = name
         self._view = None
+        self._batch = None  # single-grid GridBatch wrapper (SparseConv3d on a bare grid), cached
 
     # -- counts (topology.py:179-201) ---------------------------------------
     @property
