@@ -355,12 +355,14 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
 #pragma unroll
                                 for (int hi = 0; hi < 2; ++hi) {
                                     const int sv = sl[2 * gg + hi];
-                                    // missing neighbour: read the zero row (no branch, no register zeroing)
-                                    const uint32_t rb = sv != kNoSlot ? hb + sv * C::ROWB : zrow;
+                                    // missing neighbour (~23% of the lanes at cfg2): no shared-memory read, the
+                                    // predicated-off load leaves zeros (fewer wavefronts for the present rows)
+                                    const bool has = sv != kNoSlot;
+                                    const uint32_t rb = hb + sv * C::ROWB;
                                     const int par = sv & 1;
 #pragma unroll
                                     for (int j = 0; j < C::LJ; ++j) {
-                                        const uint4 w = lds128(rb + (halo_phys(K, par, halo_chunk(K, t0, j)) << 4));
+                                        const uint4 w = lds128_pred(rb + (halo_phys(K, par, halo_chunk(K, t0, j)) << 4), has);
                                         const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                                         for (int e = 0; e < 4; ++e) {
@@ -569,6 +571,353 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
     if ((dbg & 128) && threadIdx.x == 0 && blockIdx.x < kCtaTraceN) {
         g_halo_cta[blockIdx.x][0] = t_start;
         g_halo_cta[blockIdx.x][1] = global_ns();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_conv_halo4: lockstep builder sets (K, N <= 64)
+//
+// The ring kernel above hands every A stage from builder warps to one MMA warp through mbarriers; its
+// skeleton alone (no MMA, no build, no loads: FVDB_DEBUG_HALO=63) costs ~220 cycles per stage at cfg2,
+// because each hand-off is a chain of commit -> wait -> fence -> arrive -> wait latencies through a ring
+// whose depth TMEM caps at 12 stages.  Here the builders issue their own MMAs: SETS = 4 sets of four warps
+// (one per TMEM lane quarter) each own the offsets d with d % SETS == set of every tile, their own
+// accumulator D_set and ASL A slots.  A stage is: wait the slot's previous MMAs (usually long done), build
+// the 128 x K operand from the staged halo, tcgen05.wait::st + fence, a 128-thread named barrier, and the
+// set's first warp issues the K/16 MMAs and commits.  Four independent sets keep the tensor pipe fed while
+// each waits on its own latencies; no warp sits between the builders and the tensor core.  The epilogue sums
+// D_0 + D_1 + D_2 + D_3 in that order (deterministic), releasing each D as soon as it is read.
+// Weights: per set WSL slots of one offset image each, TMA-loaded ahead by the weight-loader warp.
+// ---------------------------------------------------------------------------------------------
+template <int K, int N>
+struct Halo4Cfg {
+    static constexpr int SETS = 4;
+    static constexpr int ROWB = 2 * K, CPR = K / 8, LJ = K / 32, NX = K / 16;
+    static constexpr int KB = K >= 64 ? 64 : K;
+    static constexpr int BROWB = KB * 2;
+    static constexpr uint32_t BLAYOUT = BROWB == 128 ? kSwizzle128B : kSwizzle64B;
+    static constexpr int B_BYTES = N * K * 2;
+    static constexpr int ACOLS = K / 2;
+    static constexpr int DCOLS = SETS * N;
+    // A slots per set: two, alternating with the two named barriers of the set (a builder can then be at most
+    // one stage ahead of its issuer, which the barrier pairing requires)
+    static constexpr int ASL = 2;
+    static constexpr int WSL = 3;   // weight slots per set (the weight-loader warp fills them ahead)
+    static constexpr int WPRE = 1;
+    static constexpr int FIXED = 1024 + SETS * WSL * B_BYTES + 2 * kIdxBytes;
+    static constexpr int CAP = ((kSmemMax - 2048 - FIXED) / (2 * (ROWB + 4))) & ~7;
+    static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4);
+    static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, N, false, false);
+    static constexpr int BUILDERS = 4 * SETS;
+    static constexpr int EPI = 8;                             // epilogue warps: 4 lane quarters x 2 column halves
+    static constexpr int HC = N / 2;                          // columns per epilogue thread
+    // halo loader, weight loader, builders, one MMA issuer per set, epilogue
+    static constexpr int THREADS = (2 + BUILDERS + SETS + EPI) * 32;
+    static_assert(ASL >= 2, "two A slots per set at least");
+    static_assert(CAP >= 256, "halo capacity must hold one offset phase");
+    static_assert(DCOLS + SETS * ASL * ACOLS <= 512, "TMEM");
+};
+
+template <int K, int N, bool OUT_BF16>
+__global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
+    k_conv_halo4(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, fvdb_halo_plan P, int64_t n_out,
+                 void* __restrict__ out, int dbg) {
+    using C = Halo4Cfg<K, N>;
+    constexpr int SETS = C::SETS, ASL = C::ASL, WSL = C::WSL, WPRE = C::WPRE, kBuilders = C::BUILDERS;
+    constexpr int W_LOAD = 0, W_WLOAD = 1, W_BLD = 2, W_ISS = 2 + kBuilders, W_EPI = W_ISS + SETS, HC = C::HC;
+    extern __shared__ uint8_t dsmem[];
+    __shared__ __align__(8) uint64_t bar_hfull[2], bar_hempty[2], bar_xfull[2], bar_ifull[2], bar_iempty[2];
+    __shared__ __align__(8) uint64_t bar_afree[SETS][ASL];   // A slot's MMAs complete (tcgen05.commit)
+    __shared__ __align__(8) uint64_t bar_wfull[SETS][WSL];   // weight image landed (TMA tx)
+    __shared__ __align__(8) uint64_t bar_wfree[SETS][WSL];   // weight slot's MMAs complete
+    __shared__ __align__(8) uint64_t bar_dfull[SETS];        // set's last MMA of the tile complete
+    __shared__ __align__(8) uint64_t bar_dempty[SETS];       // epilogue read D_set
+    __shared__ uint32_t tmem_slot;
+
+    const uint32_t sbase = smem_u32(dsmem);
+    const uint32_t bbase = (sbase + 1023u) & ~1023u;            // weight slots [SETS][WSL][B_BYTES]
+    const uint32_t ibase = bbase + SETS * WSL * C::B_BYTES;    // tile records [2]
+    const uint32_t hbase = ibase + 2 * kIdxBytes;              // halo rows [2][CAP][ROWB]
+    const uint32_t xbase = hbase + 2 * C::CAP * C::ROWB;       // halo row ids [2][CAP]
+    const uint8_t* gen = dsmem - sbase;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = P.num_tiles;
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&bar_hfull[b]), 32);
+            mbar_init(smem_u32(&bar_hempty[b]), kBuilders);
+            mbar_init(smem_u32(&bar_xfull[b]), 1);
+            mbar_init(smem_u32(&bar_ifull[b]), 1);
+            mbar_init(smem_u32(&bar_iempty[b]), kBuilders);
+        }
+        for (int s = 0; s < SETS; ++s) {
+            for (int k = 0; k < ASL; ++k) mbar_init(smem_u32(&bar_afree[s][k]), 1);
+            for (int k = 0; k < WSL; ++k) {
+                mbar_init(smem_u32(&bar_wfull[s][k]), 1);
+                mbar_init(smem_u32(&bar_wfree[s][k]), 1);
+            }
+            mbar_init(smem_u32(&bar_dfull[s]), 1);
+            mbar_init(smem_u32(&bar_dempty[s]), C::EPI);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == W_WLOAD) tmem_alloc(smem_u32(&tmem_slot), 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == W_LOAD) {
+        // ---------------- halo loader (as k_conv_halo): row ids by TMA, rows by cp.async, record by TMA ----------
+        int tile = blockIdx.x, g = 0;
+        uint32_t pc = 0;
+        auto issue_ids = [&](int t, int gg, uint32_t buf) {
+            const int32_t* ph = P.phase + ((int64_t)t * 27 + gg) * 2;
+            const int off = P.tile_base[t] + ph[0], len = ph[1];
+            if (lane == 0) {
+                mbar_arrive_expect_tx(smem_u32(&bar_xfull[buf]), (uint32_t)len * 4u);
+                if (len > 0) bulk_g2s(xbase + buf * C::CAP * 4, P.halo_rows + off, (uint32_t)len * 4u, smem_u32(&bar_xfull[buf]));
+            }
+            return len;
+        };
+        int len = tile < T ? issue_ids(tile, 0, 0) : 0;
+        int level = tile < T ? P.tile_level[tile] : 1;
+        while (tile < T) {
+            int ng = g + 1, nt = tile;
+            if (ng >= level) { ng = 0; nt = tile + gridDim.x; }
+            const int nlevel = ng == 0 ? (nt < T ? P.tile_level[nt] : 1) : level;
+            const uint32_t buf = pc & 1, par = (pc >> 1) & 1;
+            const int nlen = nt < T ? issue_ids(nt, ng, buf ^ 1) : 0;
+            mbar_wait(smem_u32(&bar_xfull[buf]), par);
+            mbar_wait(smem_u32(&bar_hempty[buf]), par ^ 1);
+            if (lane == 0) trace(dbg, 8, pc);
+            const int32_t* ids = reinterpret_cast<const int32_t*>(gen + xbase + buf * C::CAP * 4);
+            const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
+            constexpr int RPI = 32 / C::CPR;
+            const int q = lane / C::CPR, c = lane % C::CPR;
+            for (int s0 = 0; s0 < len; s0 += 4 * RPI) {
+                int r[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int s = s0 + k * RPI + q;
+                    r[k] = s < len ? ids[s] : -1;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int s = s0 + k * RPI + q;
+                    if (r[k] >= 0) cp_async_16(hb + s * C::ROWB + (halo_phys(K, s, c) << 4), in + (int64_t)r[k] * K + c * 8, 16u);
+                }
+            }
+            cp_async_arrive_noinc(smem_u32(&bar_hfull[buf]));
+            if (lane == 0) {
+                mbar_wait(smem_u32(&bar_iempty[buf]), par ^ 1);
+                mbar_arrive_expect_tx(smem_u32(&bar_ifull[buf]), (uint32_t)kRecBytes);
+                bulk_g2s(ibase + buf * kIdxBytes, P.tile_rec + (int64_t)tile * kIdxBytes, (uint32_t)kRecBytes,
+                         smem_u32(&bar_ifull[buf]));
+            }
+            __syncwarp();
+            ++pc;
+            tile = nt;
+            g = ng;
+            len = nlen;
+            level = nlevel;
+        }
+    } else if (warp == W_WLOAD) {
+        // ---------------- weight loader: per-set offset images, polled round-robin without blocking ------------
+        // set s's stage j takes offset s + SETS * (j % per_tile(s)) into slot j % WSL once stage j - WSL's MMAs
+        // are done; a set whose slot is still busy does not hold up the others
+        if (lane == 0) {
+            const int ntiles = blockIdx.x < T ? (T - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+            uint32_t next[SETS], total[SETS], per[SETS];
+            uint32_t left = 0;
+#pragma unroll
+            for (int s = 0; s < SETS; ++s) {
+                per[s] = (uint32_t)((27 - s + SETS - 1) / SETS);
+                total[s] = per[s] * (uint32_t)ntiles;
+                next[s] = 0;
+                left += total[s];
+            }
+            while (left) {
+#pragma unroll
+                for (int s = 0; s < SETS; ++s) {
+                    const uint32_t j = next[s];
+                    if (j >= total[s]) continue;
+                    const uint32_t k = j % WSL, use = j / WSL;
+                    if (!mbar_test(smem_u32(&bar_wfree[s][k]), (use & 1) ^ 1)) continue;
+                    if (s == 0) trace(dbg, 5, j);
+                    const int d = s + SETS * (int)(j % per[s]);
+                    mbar_arrive_expect_tx(smem_u32(&bar_wfull[s][k]), C::B_BYTES);
+                    bulk_g2s(bbase + (s * WSL + k) * C::B_BYTES, wimg + (size_t)d * C::B_BYTES, C::B_BYTES,
+                             smem_u32(&bar_wfull[s][k]));
+                    next[s] = j + 1;
+                    --left;
+                }
+            }
+        }
+    } else if (warp >= W_BLD && warp < W_BLD + kBuilders) {
+        // ---------------- builders: A stage from the staged halo into the set's TMEM slot -----------------------
+        // Per stage: wait the slot's previous MMAs, build, wait::st + fence, arrive on the set's named barrier
+        // (two barriers alternating by stage parity: a builder is at most one stage ahead of its issuer).
+        const int set = (warp - W_BLD) / 4;
+        const int q = warp & 3;
+        const int t0 = lane & 3, t1 = lane >> 2;
+        const int lrow = q * 32 + t1;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const bool tr = set == 0 && q == 2 && lane == 0;
+        uint32_t pc = 0, js = 0;
+        for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
+            const int level = P.tile_level[tile], gs = 27 / level;
+            for (int g = 0; g < level; ++g, ++pc) {
+                const uint32_t buf = pc & 1, par = (pc >> 1) & 1;
+                if (tr) trace(dbg, 9, pc);
+                mbar_wait(smem_u32(&bar_hfull[buf]), par);
+                mbar_wait(smem_u32(&bar_ifull[buf]), par);
+                if (tr) trace(dbg, 10, pc);
+                const uint16_t* lb = reinterpret_cast<const uint16_t*>(gen + ibase + buf * kIdxBytes);
+                const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
+                const int d_end = (g + 1) * gs;
+                int d = g * gs;
+                d += (set - d % SETS + SETS) % SETS;
+                for (; d < d_end; d += SETS, ++js) {
+                    const uint32_t ak = js % ASL, ause = js / ASL;
+                    if (tr) trace(dbg, 7, js);
+                    const uint16_t* lr = lb + d * kTileRows + lrow;
+                    const int sl[4] = {lr[0], lr[8], lr[16], lr[24]};
+                    mbar_wait(smem_u32(&bar_afree[set][ak]), (ause & 1) ^ 1);
+                    tc_fence_after();
+                    if (tr) trace(dbg, 0, js);
+                    if (!(dbg & 2)) {
+                        const uint32_t acol = tmem + lane_off + C::DCOLS + (set * ASL + ak) * C::ACOLS;
+                        uint32_t v[2][4 * C::NX];
+#pragma unroll
+                        for (int gg = 0; gg < 2; ++gg) {
+#pragma unroll
+                            for (int hi = 0; hi < 2; ++hi) {
+                                const int sv = sl[2 * gg + hi];
+                                const bool has = sv != kNoSlot;
+                                const uint32_t rb = hb + sv * C::ROWB;
+                                const int pr = sv & 1;
+#pragma unroll
+                                for (int j = 0; j < C::LJ; ++j) {
+                                    const uint4 w = lds128_pred(rb + (halo_phys(K, pr, halo_chunk(K, t0, j)) << 4), has);
+                                    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const int i = 4 * j + e;
+                                        v[gg][4 * (i >> 1) + (i & 1) + 2 * hi] = ww[e];
+                                    }
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int gg = 0; gg < 2; ++gg) tmem_st16x256<C::NX>(acol + ((uint32_t)(gg * 16) << 16), v[gg]);
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    if (tr) trace(dbg, 1, js);
+                    asm volatile("bar.arrive %0, 160;" ::"r"(1 + 2 * set + (int)(js & 1)) : "memory");
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(smem_u32(&bar_hempty[buf]));
+                    mbar_arrive(smem_u32(&bar_iempty[buf]));
+                }
+            }
+        }
+    } else if (warp >= W_ISS && warp < W_ISS + SETS) {
+        // ---------------- per-set MMA issuer: barrier, weights / accumulator waits, MMAs, commits ------------
+        const int set = warp - W_ISS;
+        const uint32_t dt = tmem + set * N;
+        const uint64_t bdesc0 = smem_desc(bbase, 16, 8 * C::BROWB, C::BLAYOUT);
+        const int last_d = 27 - 1 - ((27 - 1 - set) % SETS);  // this set's last offset of a tile
+        const int per_tile = (27 - set + SETS - 1) / SETS;     // offsets of this set per tile
+        const int ntiles = blockIdx.x < T ? (T - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+        const uint32_t total = (uint32_t)(per_tile * ntiles);
+        const bool tr = set == 0 && lane == 0;
+        (void)total;
+        uint32_t js = 0, lt = 0;
+        for (int tile = blockIdx.x; tile < T; tile += gridDim.x, ++lt) {
+            for (int d = set; d < 27; d += SETS, ++js) {
+                const uint32_t ak = js % ASL, wk = js % WSL, wuse = js / WSL;
+                const bool first = d == set;
+                asm volatile("bar.sync %0, 160;" ::"r"(1 + 2 * set + (int)(js & 1)) : "memory");
+                if (tr) trace(dbg, 2, js);
+                if (first) mbar_wait(smem_u32(&bar_dempty[set]), (lt & 1) ^ 1);
+                mbar_wait(smem_u32(&bar_wfull[set][wk]), wuse & 1);
+                tc_fence_after();
+                if (tr) trace(dbg, 3, js);
+                const uint32_t at = tmem + C::DCOLS + (set * ASL + ak) * C::ACOLS;
+                const uint64_t bd = bdesc0 + (((set * WSL + wk) * C::B_BYTES) >> 4);
+                if (!(dbg & 1)) {
+                    if constexpr (K == 32) {
+                        mma_ts_x2_elect_acc<8, 2>(dt, at, bd, C::IDESC, first ? 0u : 1u);
+                    } else {
+                        mma_ts_x4_elect_acc<8, 16, 24, 2, 4, 6>(dt, at, bd, C::IDESC, first ? 0u : 1u);
+                    }
+                }
+                mma_commit_elect(smem_u32(&bar_afree[set][ak]));
+                mma_commit_elect(smem_u32(&bar_wfree[set][wk]));
+                if (d == last_d) mma_commit_elect(smem_u32(&bar_dfull[set]));
+                __syncwarp();
+                if (tr) trace(dbg, 4, js);
+            }
+        }
+    } else if (warp >= W_EPI && warp < W_EPI + C::EPI) {
+        // ---------------- epilogue: D_0 + D_1 + D_2 + D_3 (fixed order) -> output rows ----------------
+        // warp (lane quarter q, column half h); each D_s is released as soon as both halves have read it
+        const int q = warp & 3, h = (warp - W_EPI) / 4;
+        uint32_t lt = 0;
+        for (int tile = blockIdx.x; tile < T; tile += gridDim.x, ++lt) {
+            const int64_t row = P.perm[(int64_t)tile * kTileRows + q * 32 + lane];
+            float acc[HC];
+#pragma unroll
+            for (int s = 0; s < SETS; ++s) {
+                mbar_wait_sleep(smem_u32(&bar_dfull[s]), lt & 1, 64);
+                if (s == 0 && q == 0 && h == 0 && lane == 0) trace(dbg, 6, lt);
+                tc_fence_after();
+#pragma unroll
+                for (int c0 = 0; c0 < HC; c0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + s * N + h * HC + c0, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        acc[c0 + j] = s == 0 ? __uint_as_float(v[j]) : acc[c0 + j] + __uint_as_float(v[j]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bar_dempty[s]));
+            }
+            if (row >= 0) {
+                if constexpr (OUT_BF16) {
+                    uint8_t* dst = reinterpret_cast<uint8_t*>(reinterpret_cast<bf16*>(out) + row * N + h * HC);
+#pragma unroll
+                    for (int c0 = 0; c0 < HC; c0 += 16) {
+                        uint32_t p[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[c0 + 2 * e], acc[c0 + 2 * e + 1]);
+                            p[e] = *reinterpret_cast<uint32_t*>(&b2);
+                        }
+                        stg256(dst + 2 * c0, p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7]);
+                    }
+                } else {
+                    uint8_t* dst = reinterpret_cast<uint8_t*>(reinterpret_cast<float*>(out) + row * N + h * HC);
+#pragma unroll
+                    for (int c0 = 0; c0 < HC; c0 += 8)
+                        stg256(dst + 4 * c0, __float_as_uint(acc[c0]), __float_as_uint(acc[c0 + 1]),
+                               __float_as_uint(acc[c0 + 2]), __float_as_uint(acc[c0 + 3]), __float_as_uint(acc[c0 + 4]),
+                               __float_as_uint(acc[c0 + 5]), __float_as_uint(acc[c0 + 6]), __float_as_uint(acc[c0 + 7]));
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == W_WLOAD) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
     }
 }
 
@@ -903,8 +1252,47 @@ int launch_halo_v(const void* in, const void* wimg, const fvdb_halo_plan& P, int
     return FVDB_OK;
 }
 
+// lockstep-set kernel (k_conv_halo4), opt-in with FVDB_HALO4=1 for K, N <= 64.  Measured on B200 (fwd ms,
+// tools/halo_dbg.py): cfg2 64x64 0.306-0.337 vs 0.324 (ring), cfg5 32x32 4.41-4.77 vs 3.90, dense 64x64
+// 0.63-0.67 vs 0.64; its sync skeleton alone (no MMA, no build) is ~0.24 ms at cfg2: every set-stage waits on a
+// weight TMA whose slot frees only when the MMAs of three stages earlier have completed
+// (profiles/r02_halo4.md).  Not the default.
+template <int K, int N>
+bool use_halo4() {
+    static const int e = getenv("FVDB_HALO4") ? atoi(getenv("FVDB_HALO4")) : 0;
+    return K <= 64 && N <= 64 && e == 1;
+}
+
+template <int K, int N, bool OB>
+int launch_halo4(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out,
+                 cudaStream_t st) {
+    if constexpr (K <= 64 && N <= 64) {
+        using C = Halo4Cfg<K, N>;
+        if (P.halo_cap > C::CAP) return FVDB_ERR_INVALID;
+        auto kern = k_conv_halo4<K, N, OB>;
+        FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        int grid = sm_count_h();
+        if (grid > P.num_tiles) grid = P.num_tiles;
+        static const int dbg = getenv("FVDB_DEBUG_HALO") ? atoi(getenv("FVDB_DEBUG_HALO")) : 0;
+        kern<<<grid, C::THREADS, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, P, n_out, out, dbg);
+        FVDB_LAUNCH_CHECK();
+        return FVDB_OK;
+    } else {
+        return FVDB_ERR_INVALID;
+    }
+}
+
+template <int K, int N>
+int halo_kernel_cap() {
+    if constexpr (K <= 64 && N <= 64) {
+        if (use_halo4<K, N>()) return Halo4Cfg<K, N>::CAP;
+    }
+    return halo_variant<K, N>() == 1 ? HaloCfg<K, N, 1>::CAP : HaloCfg<K, N, 0>::CAP;
+}
+
 template <int K, int N, bool OB>
 int launch_halo(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out, cudaStream_t st) {
+    if (use_halo4<K, N>()) return launch_halo4<K, N, OB>(in, wimg, P, n_out, out, st);
     if (halo_variant<K, N>() == 1) return launch_halo_v<K, N, OB, 1>(in, wimg, P, n_out, out, st);
     return launch_halo_v<K, N, OB, 0>(in, wimg, P, n_out, out, st);
 }
@@ -936,7 +1324,7 @@ extern "C" int fvdb_halo_cap(int K, int N) {
     int cap = 0;
     halo_dispatch(K, N, [&](auto k, auto n) {
         constexpr int KK = decltype(k)::value, NN = decltype(n)::value;
-        cap = halo_variant<KK, NN>() == 1 ? HaloCfg<KK, NN, 1>::CAP : HaloCfg<KK, NN, 0>::CAP;
+        cap = halo_kernel_cap<KK, NN>();
         return 0;
     });
     return cap;
