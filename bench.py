@@ -1,23 +1,28 @@
 #!/usr/bin/env python
 """SparseConv3d fwd+bwd throughput on B200 (BASELINE.json metric), plus the reference arm.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2|cfg3|cfg5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg1..cfg5]
 
-Workload (N=1): BASELINE.json configs[1] — the ScanNet-scale sphere shell
-``sphere_shell_coords(470, band=1.5)`` (1,018,216 voxels, 21,229,376 kernel-map pairs),
-SparseConv3d 3×3×3 64→64, bf16 inputs / fp32 accumulation, forward + input-gradient +
-weight-gradient.  A "step" is one fwd+bwd pass over that grid with inputs resident in HBM;
-the kernel map is built once outside the timed region (as the reference's bench-conv,
-cli.py:353) and its build time is reported separately.  Multi-GPU (torchrun): weak scaling
-— every rank runs its own grid (batch-sharded data parallelism) and the step includes the
-NCCL all-reduce of the fp32 weight gradient.
+Workload (default, N=1): BASELINE.json configs[1] — the ScanNet-scale sphere shell
+``sphere_shell_coords(470, band=1.5)`` (1,018,216 voxels, 21,229,376 kernel-map pairs), SparseConv3d 3×3×3
+64→64, bf16 inputs / fp32 accumulation, forward + input gradient + weight gradient.  A "step" is one fwd+bwd
+pass over that grid with inputs resident in HBM; the kernel map is built once outside the timed region (as the
+reference's bench-conv, cli.py:353) and its build is reported separately (``stages``).
 
-Timing: W warm-up steps; K timed steps, each preceded by a 256 MB L2-flush write (untimed),
-timed with CUDA events on the launching stream; ms_per_step = mean, max over ranks.
-``e2e`` repeats the step through the public module API with pinned host buffers (H2D of
-features / grad_out / weights, D2H of output / grad_in / grad_w inside the timed region).
-``cpu_baseline`` times the oracle port (numpy restatement of the reference igemm conv,
-BLAS on all host cores) on a leaf-aligned sample of the same workload.
+Multi-GPU (torchrun, one process per GPU, NCCL):
+* cfg2: weak scaling — every rank runs its own cfg2 grid;
+* cfg3: strong scaling — the 8 LiDAR grids are split across ranks by kernel-map pairs (dist.partition_by_cost),
+  each rank builds its share as one jagged batch (one batched build, one batched kernel map);
+* cfg5: strong scaling — the 19.4M-voxel grid's output rows are split at leaf boundaries (dist.RowShard);
+every step ends with the sum all-reduce of the fp32 weight gradient, started right after the wgrad kernel and
+overlapped with the input-gradient kernel.
+
+Timing: W warm-up steps; K timed steps, each preceded by a 256 MB L2-flush write (untimed), timed with CUDA
+events on the launching stream; ms_per_step = mean, max over ranks.  ``e2e`` is the same step through the public
+API with host data: the features are copied host->device (pinned fp32) every step, the loss (½‖y‖², whose
+gradient y seeds the backward) and the weight gradient are read back.  ``cpu_baseline`` times the reference
+itself (the unmodified ``idxgrid`` package installed in baseline/_ref; the oracle port if it is absent) on a
+leaf-aligned sample of the same workload.
 """
 
 from __future__ import annotations
@@ -31,9 +36,8 @@ import sys
 import threading
 import time
 
-# The reference arm (the oracle port: numpy + OpenBLAS) runs with every host thread the process may use.
-# torchrun exports OMP_NUM_THREADS=1 to each rank, which OpenBLAS reads when numpy loads, so override it
-# before the import.
+# The reference arm (numpy + OpenBLAS) runs with every host thread the process may use.  torchrun exports
+# OMP_NUM_THREADS=1 to each rank, which OpenBLAS reads when numpy loads, so override it before the import.
 HOST_THREADS = len(os.sched_getaffinity(0))
 
 
@@ -57,19 +61,22 @@ METRIC = "SparseConv3d fwd+bwd active voxels/s & TFLOPS at 1/2/4/8 B200 vs CPU r
 UNIT = "voxels/s"
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 TRAFFIC_FILE = ROOT / "profiles" / "ncu_traffic.json"
+REF_DIR = ROOT / "baseline" / "_ref"
 
 CONFIGS = {
     "cfg1": dict(desc="single GridBatch from a random 100k-point cloud (sigma 1, voxel 0.05), SparseConv3d 3x3x3 "
                       "32->32 fp32 forward (CUDA-core exact path)", points=True, cin=32, cout=32, fp32_fwd=True),
+    "cfg2": dict(desc="ScanNet-scale sphere shell sphere_shell_coords(470, band=1.5), SparseConv3d 3x3x3 64->64 "
+                      "bf16 fwd+bwd", res=470, cin=64, cout=64, scaling="weak"),
+    "cfg3": dict(desc="batch of 8 simulated KITTI-scale LiDAR grids (seeds 0-7, 128 beams x 2048 azimuths, voxel "
+                      "0.05 m), SparseConv3d 3x3x3 128->128 bf16 fwd+bwd, batch-sharded across ranks by kernel-map "
+                      "pairs", lidar=8, cin=128, cout=128, scaling="strong"),
     "cfg4": dict(desc="sparse U-Net stage: build from jagged points (cfg2 shell as f64 voxel centres), coarsen, "
                       "stride-2 conv 64->128 + transposed conv 128->64, fwd+bwd, bf16", res=470, cin=64, cout=128,
                  unet=True),
-    "cfg2": dict(desc="ScanNet-scale sphere shell sphere_shell_coords(470, band=1.5), SparseConv3d 3x3x3 64->64 "
-                      "bf16 fwd+bwd", res=470, cin=64, cout=64),
-    "cfg3": dict(desc="KITTI-scale simulated LiDAR grid (128 beams x 2048 az, voxel 0.05 m, seed=rank), "
-                      "SparseConv3d 3x3x3 128->128 bf16 fwd+bwd", lidar=True, cin=128, cout=128),
     "cfg5": dict(desc="2048^3 surface shell sphere_shell_coords(2048, band=1.5), SparseConv3d 3x3x3 32->32 bf16 "
-                      "fwd+bwd", res=2048, cin=32, cout=32),
+                      "fwd+bwd, output rows sharded across ranks at leaf boundaries", res=2048, cin=32, cout=32,
+                 rowshard=True, scaling="strong"),
 }
 
 
@@ -100,9 +107,7 @@ def peaks():
 # ----------------------------------------------------------------------------- inputs
 
 def make_coords(cfg, rank):
-    from paper_2407_01781_b200.workloads import lidar_scan_points, random_points, sphere_shell_coords
-    if cfg.get("lidar"):
-        return None, lidar_scan_points(rank)
+    from paper_2407_01781_b200.workloads import random_points, sphere_shell_coords
     if cfg.get("points"):
         return None, random_points(np.random.default_rng(rank), 100_000, sigma=1.0)
     return sphere_shell_coords(cfg["res"], band=1.5), None
@@ -155,6 +160,112 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
 
 
+# ----------------------------------------------------------------------------- timing helpers
+
+def stage(torch, fn, reps=1):
+    """(result, device ms from CUDA events on the current stream, wall ms incl. host work and syncs): best of reps."""
+    best = None
+    res = None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        res = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        dev = e0.elapsed_time(e1)
+        if best is None or dev < best[0]:
+            best = (dev, wall)
+    return res, round(best[0], 4), round(best[1], 4)
+
+
+def max_over_ranks(torch, dist, dev, v, use_dist):
+    if not use_dist:
+        return v
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(torch, dist, dev, v, use_dist):
+    if not use_dist:
+        return v
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- problem setup (per config)
+
+def setup_problem(args, cfg, rank, world, dev, torch, P):
+    """This rank's share of the workload: tables, inputs and the stage measurements of building them."""
+    from paper_2407_01781_b200 import dist as D
+    stages = {}
+    if cfg.get("lidar"):
+        from paper_2407_01781_b200.workloads import lidar_scan_points
+        pts = [lidar_scan_points(s) for s in range(cfg["lidar"])]
+        tf = P.VoxelTransform.uniform(0.05)
+        # partition the batch by kernel-map pairs (the same on every rank; setup, untimed)
+        full, _ = P.build_from_points(P.jagged_from_list([torch.from_numpy(p) for p in pts]), tf)
+        kfull = P.build_batch_kernel_map(full, full, 1)
+        costs = [int((kfull.fwd.t[:, s:e] >= 0).sum().item()) for s, e in full.voxel_joffsets.tolist()]
+        s, e = D.partition_by_cost(costs, world)[rank]
+        del full, kfull
+        jag = P.jagged_from_list([torch.from_numpy(p) for p in pts[s:e]])
+        batch, dv, wl = stage(torch, lambda: P.build_from_points(jag, tf)[0], reps=3)
+        stages["grid_build"] = dict(device_ms=dv, wall_ms=wl, inputs=int(jag.jdata.shape[0]), grids=e - s,
+                                    batched=True)
+        km, dv, wl = stage(torch, lambda: P.build_batch_kernel_map(batch, batch, 1), reps=3)
+        stages["kernel_map"] = dict(device_ms=dv, wall_ms=wl, batched=True)
+        n = batch.total_voxels
+        return dict(t_fwd=km.fwd, t_dgrad=km.bwd, n_in=n, n_out=n, rows=slice(0, n), pairs=km.total_pairs, km=km,
+                    batch=batch, leaves=sum(g.num_leaf_nodes for g in batch.grids), units=n,
+                    share=f"grids {s}..{e - 1} of {len(pts)}"), stages
+    coords, _ = make_coords(cfg, rank if cfg.get("scaling") == "weak" else 0)
+    c_dev = torch.from_numpy(coords).to(dev)
+    grid, dv, wl = stage(torch, lambda: P.build_from_coords(c_dev)[0], reps=3)
+    stages["grid_build"] = dict(device_ms=dv, wall_ms=wl, inputs=int(coords.shape[0]), grids=1, batched=False)
+    if cfg.get("rowshard"):
+        r0, r1, l0, l1 = D.leaf_aligned_ranges(grid.leaf_value_offset, grid.num_voxels, world)[rank]
+        sh, dv, wl = stage(torch, lambda: D.RowShard(grid, r0, r1, l0, l1), reps=3)
+        stages["kernel_map"] = dict(device_ms=dv, wall_ms=wl, rows=f"[{r0}, {r1})")
+        n = grid.num_voxels
+        return dict(t_fwd=sh.fwd, t_dgrad=sh.dgrad, n_in=n, n_out=r1 - r0, rows=slice(r0, r1), pairs=sh.total_pairs,
+                    shard=sh, grid=grid, leaves=l1 - l0, units=r1 - r0,
+                    share=f"rows [{r0}, {r1}) of {n} (leaves [{l0}, {l1}))"), stages
+    km, dv, wl = stage(torch, lambda: P.build_kernel_map(grid, grid, 1), reps=3)
+    stages["kernel_map"] = dict(device_ms=dv, wall_ms=wl)
+    n = grid.num_voxels
+    return dict(t_fwd=km.fwd, t_dgrad=km.bwd, n_in=n, n_out=n, rows=slice(0, n), pairs=km.total_pairs, km=km,
+                grid=grid, leaves=grid.num_leaf_nodes, units=n, share="whole grid"), stages
+
+
+def stage_rooflines(stages, prob, pk):
+    """Algorithmic bytes and fraction of measured HBM bandwidth of the map / grid stages."""
+    hbm = pk["hbm_gbs"]
+    out = {}
+    gb = stages["grid_build"]
+    # read 24 B per int64 input coordinate; write the leaf payload (80 B record + 8 B key + 24 B origin)
+    gbytes = 24 * gb["inputs"] + (80 + 8 + 24) * prob["leaves"]
+    out["grid_build"] = dict(gb, algorithmic_bytes=gbytes,
+                             achieved_gbs=round(gbytes / (gb["device_ms"] * 1e-3) / 1e9, 1),
+                             frac_hbm=round(gbytes / (gb["device_ms"] * 1e-3) / 1e9 / hbm, 4),
+                             host_overhead_ms=round(gb["wall_ms"] - gb["device_ms"], 3))
+    km = stages["kernel_map"]
+    # read 24 B per output coordinate, write the int32 neighbour table (27 x 4 B per output row)
+    kbytes = (24 + 27 * 4) * prob["n_out"]
+    out["kernel_map"] = dict(km, algorithmic_bytes=kbytes,
+                             achieved_gbs=round(kbytes / (km["device_ms"] * 1e-3) / 1e9, 1),
+                             frac_hbm=round(kbytes / (km["device_ms"] * 1e-3) / 1e9 / hbm, 4),
+                             host_overhead_ms=round(km["wall_ms"] - km["device_ms"], 3))
+    for k, v in stages.items():
+        if k not in out:
+            out[k] = v
+    return out
+
+
 # ----------------------------------------------------------------------------- our arm
 
 def run_ours(args, rank, world, local_rank):
@@ -165,82 +276,63 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_2407_01781_b200 as P
-    from paper_2407_01781_b200.conv import (conv_impl, gather_conv, pack_weights_umma, steady_impl, wgrad,
-                                            wgrad_pairs_enabled)
+    from paper_2407_01781_b200.conv import conv_impl, gather_conv, pack_weights_umma, steady_impl, wgrad
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    cfg = CONFIGS[args.config]
     cin, cout = cfg["cin"], cfg["cout"]
+    use_dist = world > 1
+    pk = peaks()
 
-    coords, points = make_coords(cfg, rank)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    if points is not None:
-        grid, _ = P.build_from_points(points, P.VoxelTransform.uniform(0.05))
-    else:
-        grid, _ = P.build_from_coords(coords)
-    torch.cuda.synchronize()
-    t_build = time.perf_counter() - t0
-    # kernel map (prebuilt; timed separately with events, best of 3)
-    km = None
-    kms = []
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        km = P.build_kernel_map(grid, grid, 1)
-        e1.record()
-        torch.cuda.synchronize()
-        kms.append(e0.elapsed_time(e1))
-    n = grid.num_voxels
-    pairs = km.total_pairs
-    nbr = km.fwd
-    # transposed table, halo plans / signature-sorted tables: per-kernel-map preprocessing, cached, outside
-    # the timed step.  The timed step reuses a prebuilt map, so each table runs what "auto" settles on for a
-    # reused map (conv.steady_impl: the halo kernel, or the sorted gather for sparse wide layers);
-    # FVDB_CONV_IMPL=gather / halo forces one kernel for comparison.
+    prob, stages = setup_problem(args, cfg, rank, world, dev, torch, P)
+    t_fwd, t_dgrad = prob["t_fwd"], prob["t_dgrad"]
+    n_in, n_out, rows, pairs = prob["n_in"], prob["n_out"], prob["rows"], prob["pairs"]
+
+    # per-table preprocessing (cached on the tables, outside the timed step): the kernels "auto" settles on for a
+    # reused map (conv.steady_impl: the halo kernel, or the sorted gather for sparse wide layers).
     forced = conv_impl()
+
     def steady(tab, k, n):
         return (forced, False) if forced != "auto" else steady_impl(tab, k, n)
-    prep = {}
-    impl_f, sorted_f = steady(nbr, cin, cout)
-    impl_b, sorted_b = steady(km.bwd, cout, cin)
-    impl = impl_f
-    for name, fn in (("transpose", lambda: km.bwd),
-                     ("halo_plan_fwd", lambda: nbr.halo_plan(cin, cout) if impl_f == "halo" else None),
-                     ("halo_plan_dgrad", lambda: km.bwd.halo_plan(cout, cin) if impl_b == "halo" else None),
-                     ("sort_fwd", lambda: nbr.signature_sorted() if sorted_f else None),
-                     ("sort_dgrad", lambda: km.bwd.signature_sorted() if sorted_b else None)):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        fn()
-        e1.record()
-        torch.cuda.synchronize()
-        prep[name] = round(e0.elapsed_time(e1), 3)
-    nbrT = km.bwd
+
+    impl_f, sorted_f = steady(t_fwd, cin, cout)
+    impl_b, sorted_b = steady(t_dgrad, cout, cin)
+    for name, fn in (("halo_plan_fwd", lambda: t_fwd.halo_plan(cin, cout) if impl_f == "halo" else None),
+                     ("halo_plan_dgrad", lambda: t_dgrad.halo_plan(cout, cin) if impl_b == "halo" else None),
+                     ("sort_fwd", lambda: t_fwd.signature_sorted() if sorted_f else None),
+                     ("sort_dgrad", lambda: t_dgrad.signature_sorted() if sorted_b else None)):
+        _, dv, wl = stage(torch, fn)
+        if dv > 0.05 or wl > 0.05:
+            stages[name] = dict(device_ms=dv, wall_ms=wl)
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
-    x = torch.randn(n, cin, device=dev, generator=gen).to(torch.bfloat16)
-    gy = torch.randn(n, cout, device=dev, generator=gen).to(torch.bfloat16)
+    x = torch.randn(n_in, cin, device=dev, generator=gen).to(torch.bfloat16)
+    # a row shard's input gradient reads grad_out of every row; its weight gradient only its own rows
+    gy = torch.randn(n_in if cfg.get("rowshard") else n_out, cout, device=dev, generator=gen).to(torch.bfloat16)
+    gy_rows = gy[rows] if cfg.get("rowshard") else gy
     w = torch.randn(cout, cin, 3, 3, 3, device=dev, generator=gen) / (27 * cin) ** 0.5
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    use_dist = world > 1
+    for _ in range(3):  # reach the steady kernels of every table (halo / sorted gather / pair-list wgrad)
+        gather_conv(x, t_fwd, w)
+        gather_conv(gy, t_dgrad, w, transpose=True)
+        wgrad(x, gy_rows, t_fwd)
 
     def step(ev=None):
         img_f = pack_weights_umma(w, False, impl_f)
         img_b = pack_weights_umma(w, True, impl_b)
         if ev is not None:
             ev[0].record()
-        y = gather_conv(x, nbr, w, transpose=False, out_dtype=torch.bfloat16, w_image=img_f)
+        y = gather_conv(x, t_fwd, w, transpose=False, out_dtype=torch.bfloat16, w_image=img_f)
         if ev is not None:
             ev[1].record()
-        gx = gather_conv(gy, nbrT, w, transpose=True, out_dtype=torch.bfloat16, w_image=img_b)
+        gw = wgrad(x, gy_rows, t_fwd)
         if ev is not None:
             ev[2].record()
-        gw = wgrad(x, gy, nbr)
+        h = dist.all_reduce(gw, async_op=True) if use_dist else None  # overlaps the dgrad kernel
+        gx = gather_conv(gy, t_dgrad, w, transpose=True, out_dtype=torch.bfloat16, w_image=img_b)
         if ev is not None:
             ev[3].record()
-        if use_dist:
-            dist.all_reduce(gw)
+        if h is not None:
+            h.wait()
         if ev is not None:
             ev[4].record()
         return y, gx, gw
@@ -263,26 +355,21 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     step_ms = [s.elapsed_time(e[4]) for s, e in zip(starts, evs)]
-    phase = {"fwd": [e[0].elapsed_time(e[1]) for e in evs], "dgrad": [e[1].elapsed_time(e[2]) for e in evs],
-             "wgrad": [e[2].elapsed_time(e[3]) for e in evs], "allreduce": [e[3].elapsed_time(e[4]) for e in evs],
+    phase = {"fwd": [e[0].elapsed_time(e[1]) for e in evs], "wgrad": [e[1].elapsed_time(e[2]) for e in evs],
+             "dgrad": [e[2].elapsed_time(e[3]) for e in evs], "allreduce_tail": [e[3].elapsed_time(e[4]) for e in evs],
              "pack": [s.elapsed_time(e[0]) for s, e in zip(starts, evs)]}
-    ms = statistics.mean(step_ms)
-    if use_dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    total_vox = n * world
-    if use_dist:
-        t = torch.tensor([n], device=dev, dtype=torch.int64)
-        dist.all_reduce(t)
-        total_vox = int(t.item())
-    value = total_vox / (ms / 1e3)
+    ms = max_over_ranks(torch, dist, dev, statistics.mean(step_ms), use_dist)
+    total_units = int(sum_over_ranks(torch, dist, dev, prob["units"], use_dist))
+    total_pairs = int(sum_over_ranks(torch, dist, dev, pairs, use_dist))
+    value = total_units / (ms / 1e3)
 
-    # ---- end-to-end through the public module API with host buffers ----
-    e2e = run_e2e(args, P, torch, dist, grid, km, cin, cout, dev, use_dist)
+    # ---- fresh-map step (cfg2, rank-local): build + kernel map + first-use kernels (no halo plan) ----
+    fresh = run_fresh(torch, P, dev, x, gy, w) if args.config == "cfg2" else None
+
+    # ---- end-to-end through the public API with host data ----
+    e2e = run_e2e(args, cfg, P, torch, dist, prob, cin, cout, dev, use_dist, world)
 
     # ---- roofline of the dominant kernel ----
-    pk = peaks()
     flops_kernel = 2.0 * pairs * cin * cout
     means = {k: statistics.mean(v) for k, v in phase.items()}
     dom = max(("fwd", "dgrad", "wgrad"), key=lambda k: means[k])
@@ -296,45 +383,80 @@ def run_ours(args, rank, world, local_rank):
     fk = f"k_conv_halo<{cin},{cout},bf16>" if impl_f == "halo" else f"k_conv_fwd_tc<{cin},{cout},bf16>"
     dk = (f"k_conv_halo<{cout},{cin},bf16> (dgrad)" if impl_b == "halo"
           else f"k_conv_fwd_tc<{cout},{cin},bf16> (dgrad form)")
-    roof = {"bound": "tensor", "kernel": {"fwd": fk, "dgrad": dk, "wgrad": f"k_wgrad_tc<{cin},{cout}>"}[dom],
+    wk = "k_wgrad_pairs" if t_fwd._pairs is not None else f"k_wgrad_tc<{cin},{cout}>"
+    roof = {"bound": "tensor", "kernel": {"fwd": fk, "dgrad": dk, "wgrad": wk}[dom],
             "achieved": round(achieved, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
             "frac": round(achieved / pk["bf16_tflops"], 4), "traffic": traffic,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if not pk.get("_fallback") else "fallback",
             "algorithmic_flop_per_launch": flops_kernel}
-    step_tflops = 3 * flops_kernel / (ms / 1e3) / 1e12
+    # HBM view of the same launch (both fractions near the ridge, e.g. cfg5 at 32 channels):
+    # features in + features out (bf16) + the int32 neighbour table
+    k_, n_ = (cout, cin) if dom == "dgrad" else (cin, cout)
+    hbm_bytes = 2 * (n_in * k_ + n_out * n_) + 27 * 4 * n_out
+    roof["hbm"] = {"algorithmic_bytes": hbm_bytes, "achieved_gbs": round(hbm_bytes / (means[dom] / 1e3) / 1e9, 1),
+                   "peak_gbs": pk["hbm_gbs"], "frac": round(hbm_bytes / (means[dom] / 1e3) / 1e9 / pk["hbm_gbs"], 4)}
+    step_tflops = 3 * 2.0 * total_pairs * cin * cout / (ms / 1e3) / 1e12
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, coords, points, args)
+        cpu = cpu_baseline(cfg, args)
 
     if rank == 0:
+        how = ("batch-sharded" if cfg.get("lidar") else "row-sharded" if cfg.get("rowshard") else "one grid per rank")
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {cfg['desc']}", "voxels_per_gpu": n, "pairs_per_gpu": pairs,
-                       "cin": cin, "cout": cout, "parallelism": f"dp{world} (batch-sharded, NCCL wgrad all-reduce)"
-                       if world > 1 else "single GPU",
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": cfg.get("scaling", "weak"), "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "voxels_total": total_units,
+                       "pairs_total": total_pairs, "rank0_share": prob["share"], "cin": cin, "cout": cout,
+                       "parallelism": (f"dp{world} ({how}, NCCL wgrad all-reduce overlapped with dgrad)"
+                                       if world > 1 else "single GPU"),
                        "l2": "flushed (256 MB write) before every timed step",
-                       "kernel_map": "prebuilt outside the timed step (reference cli.py:353)",
+                       "kernel_map": "prebuilt outside the timed step (reference cli.py:353); see stages",
                        "conv_kernel": {"fwd": impl_f + (" (signature-sorted)" if sorted_f else ""),
                                        "dgrad": impl_b + (" (signature-sorted)" if sorted_b else ""),
-                                       "wgrad": "pair lists" if wgrad_pairs_enabled(nbr, cin, cout) else "table"}},
+                                       "wgrad": "pair lists" if t_fwd._pairs is not None else "table"}},
             "tflops_effective": round(step_tflops, 2),
             "frac_of_bf16_peak": round(step_tflops / pk["bf16_tflops"], 4),
             "phases_ms": {k: round(v, 4) for k, v in means.items()},
-            "build_ms": {"grid": round(t_build * 1e3, 3), "kernel_map": round(min(kms), 4), **prep},
+            "stages": stage_rooflines(stages, prob, pk),
             "roofline": roof,
             "e2e": e2e,
             "gpu_launches": 6 * args.steps,
             "clocks": clk.summary(),
         }
+        if fresh is not None:
+            line["fresh_map_step"] = fresh
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_fresh(torch, P, dev, x, gy, w):
+    """A step on a map seen for the first time (a training loop that rebuilds grids per batch): grid build,
+    kernel map, transposed table and fwd + dgrad + wgrad through the first-use kernels."""
+    from paper_2407_01781_b200.conv import gather_conv, wgrad
+    from paper_2407_01781_b200.workloads import sphere_shell_coords
+    c = torch.from_numpy(sphere_shell_coords(470, band=1.5)).to(dev)
+
+    def one():
+        g, _ = P.build_from_coords(c)
+        km = P.build_kernel_map(g, g, 1)
+        gather_conv(x, km.fwd, w)
+        gather_conv(gy, km.bwd, w, transpose=True)
+        wgrad(x, gy, km.fwd)
+
+    one()
+    best = None
+    for _ in range(3):
+        _, dv, wl = stage(torch, one)
+        if best is None or wl < best[0]:
+            best = (wl, dv)
+    return {"wall_ms": round(best[0], 3), "device_ms": round(best[1], 3),
+            "what": "build_from_coords + build_kernel_map + transposed table + fwd/dgrad/wgrad on first-use kernels"}
 
 
 def run_special(args, rank, world, local_rank, cfg):
@@ -350,6 +472,8 @@ def run_special(args, rank, world, local_rank, cfg):
     coords, points = make_coords(cfg, rank)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    pk = peaks()
+    extra = {}
     if cfg.get("fp32_fwd"):
         grid, _ = P.build_from_points(points, P.VoxelTransform.uniform(0.05))
         km = P.build_kernel_map(grid, grid, 1)
@@ -360,6 +484,9 @@ def run_special(args, rank, world, local_rank, cfg):
 
         def step():
             return gather_conv(x, km.fwd, w)
+        ffma = ffma_peak(torch)
+        if ffma:
+            extra["fp32_simt_peak_tflops"] = ffma
     else:
         pts = torch.from_numpy(coords.astype(np.float64)).to(dev)        # jagged points, B=1, on device
         tf = P.VoxelTransform.uniform(1.0)
@@ -367,7 +494,9 @@ def run_special(args, rank, world, local_rank, cfg):
         up = P.SparseConv3d(128, 64, stride=2, transposed=True).to(dev)
         n_vox = coords.shape[0]
         x = torch.randn(n_vox, 64, device=dev, generator=gen)
-        pairs = None
+        if use_dist:
+            P.dist.attach_grad_reducer(down)
+            P.dist.attach_grad_reducer(up)
 
         def step():
             g, _ = P.build_from_points(pts, tf)
@@ -375,8 +504,6 @@ def run_special(args, rank, world, local_rank, cfg):
             coarse, h = down(fine, fine.jagged(x))
             _, y = up(coarse, h, out_grid=fine)
             y.jdata.sum(dtype=torch.float32).backward()  # fp32 accumulation, no fp32 copy of y
-            if use_dist:
-                P.dist.allreduce_gradients(list(down.parameters()) + list(up.parameters()))
             return y
 
         g0, _ = P.build_from_points(pts, tf)
@@ -396,15 +523,10 @@ def run_special(args, rank, world, local_rank, cfg):
             step()
             b.record()
         torch.cuda.synchronize()
-    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-    if use_dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(torch, dist, dev, statistics.mean(a.elapsed_time(b) for a, b in ev), use_dist)
     if rank == 0:
-        pk = peaks()
         tfl = flops / (ms / 1e3) / 1e12
-        print(json.dumps({
+        line = {
             "metric": METRIC, "value": round(n_vox * world / (ms / 1e3), 1), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg.get("fp32_fwd") else "bf16",
@@ -415,76 +537,128 @@ def run_special(args, rank, world, local_rank, cfg):
             "tflops_effective": round(tfl, 3),
             "frac_of_bf16_peak": None if cfg.get("fp32_fwd") else round(tfl / pk["bf16_tflops"], 4),
             "clocks": clk.summary(),
-        }), flush=True)
+        }
+        if extra.get("fp32_simt_peak_tflops"):
+            line["roofline"] = {"bound": "fp32 SIMT", "achieved": round(tfl, 3),
+                                "peak": extra["fp32_simt_peak_tflops"], "unit": "TFLOP/s",
+                                "frac": round(tfl / extra["fp32_simt_peak_tflops"], 4),
+                                "peak_source": "fvdb_probe_ffma (FFMA microbenchmark, this run)"}
+        print(json.dumps(line), flush=True)
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def run_e2e(args, P, torch, dist, grid, km, cin, cout, dev, use_dist):
-    """Same step through SparseConv3d (autograd) with pinned host inputs/outputs.
+def ffma_peak(torch):
+    """FP32 FFMA throughput of this GPU (TFLOP/s), from the library's probe kernel."""
+    import ctypes as C
+    from paper_2407_01781_b200 import _lib
+    L = _lib.lib()
+    out = torch.empty(1 << 20, dtype=torch.float32, device="cuda")
+    best = None
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flop = C.c_double(0)
+        e0.record()
+        _lib.check(L.fvdb_probe_ffma(4096, out.data_ptr(), out.numel(), C.byref(flop), _lib.stream_ptr()),
+                   "probe_ffma")
+        e1.record()
+        torch.cuda.synchronize()
+        t = flop.value / (e0.elapsed_time(e1) * 1e-3) / 1e12
+        best = t if best is None else max(best, t)
+    return round(best, 2)
 
-    Every step copies its inputs host->device (x, grad_out, weights: fp32, pinned) and its results
-    device->host (y bf16, grad_in fp32, grad_w fp32) inside the timed region.  As a training loop with
-    a prefetching loader would, step k+1's inputs are uploaded on a copy stream while step k computes,
-    and step k's results drain on a second copy stream (PCIe is full duplex); device input buffers
-    and host output buffers are double-buffered, ordered by CUDA events.
+
+def run_e2e(args, cfg, P, torch, dist, prob, cin, cout, dev, use_dist, world):
+    """The same step through the public API with host data, every copy inside the timed region.
+
+    Each step uploads that step's fp32 features from pinned host memory, runs SparseConv3d forward (or, for a
+    row shard, dist.RowShard.forward), takes the loss ½‖y‖² (its gradient, y itself, seeds the backward: dgrad +
+    wgrad) and reads the loss and the fp32 weight gradient back to the host.  As a training loop with a
+    prefetching loader would, step k+1's features upload on a copy stream during step k (double-buffered,
+    ordered by events).  Row shards (cfg5) upload only their own rows and all-gather the features and the
+    output gradient over NCCL (the exchange a row-sharded layer needs).
     """
-    n = grid.num_voxels
-    gb = P.GridBatch([grid])
-    from paper_2407_01781_b200.conv import cache_batch_kernel_map
-    cache_batch_kernel_map(gb, gb, 1, km)
-    m = P.SparseConv3d(cin, cout).to(dev)
+    steps = args.e2e_steps or max(3, min(args.steps, 50))
     rng = np.random.default_rng(7)
-    steps = args.e2e_steps or max(3, min(args.steps, 50))  # long enough that pipeline fill / drain amortise
-    x_h = [torch.from_numpy(rng.normal(size=(n, cin)).astype(np.float32)).pin_memory() for _ in range(2)]
-    gy_h = [torch.from_numpy(rng.normal(size=(n, cout)).astype(np.float32)).pin_memory() for _ in range(2)]
-    w_h = [m.weight.detach().cpu().pin_memory() for _ in range(2)]
-    y_h = [torch.empty((n, cout), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-    gx_h = [torch.empty((n, cin), dtype=torch.float32).pin_memory() for _ in range(2)]
-    gw_h = [torch.empty_like(w_h[0]).pin_memory() for _ in range(2)]
-    x_d = [torch.empty((n, cin), dtype=torch.float32, device=dev) for _ in range(2)]
-    gy_d = [torch.empty((n, cout), dtype=torch.float32, device=dev) for _ in range(2)]
-    w_d = [torch.empty_like(m.weight) for _ in range(2)]
     main = torch.cuda.current_stream(dev)
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_in = torch.cuda.Stream(dev)
+    rowshard = cfg.get("rowshard")
+    n_up = (prob["rows"].stop - prob["rows"].start) if rowshard else prob["n_in"]
+    x_h = [torch.from_numpy(rng.normal(size=(n_up, cin)).astype(np.float32)).pin_memory() for _ in range(2)]
+    x_d = [torch.empty((n_up, cin), dtype=torch.float32, device=dev) for _ in range(2)]
+    loss_h = torch.empty(2, dtype=torch.float32).pin_memory()
+    gw_h = torch.empty((cout, cin, 3, 3, 3), dtype=torch.float32).pin_memory()
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_used = [torch.cuda.Event() for _ in range(2)]
-    ev_done = [torch.cuda.Event() for _ in range(2)]
-    ev_drained = [torch.cuda.Event() for _ in range(2)]
-    for e in ev_used + ev_drained:
+    for e in ev_used:
         e.record(main)
+    if rowshard:
+        sh = prob["shard"]
+        w = torch.randn(cout, cin, 3, 3, 3, device=dev) / (27 * cin) ** 0.5
+        n_all = prob["n_in"]
+        x_full = torch.empty((n_all, cin), dtype=torch.bfloat16, device=dev)
+        gy_full = torch.empty((n_all, cout), dtype=torch.bfloat16, device=dev)
+        # leaf-aligned shards differ in rows: all_gather into per-rank slices of the full tensor
+        if use_dist:
+            t = torch.tensor([n_up], device=dev, dtype=torch.int64)
+            allc = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(allc, t)
+            counts = [int(c.item()) for c in allc]
+        else:
+            counts = [n_up]
+        starts = np.concatenate([[0], np.cumsum(counts)]).astype(int).tolist()
+
+        def gather_rows(local, full):
+            if not use_dist:
+                full.copy_(local)
+                return
+            dist.all_gather([full[starts[r]:starts[r + 1]] for r in range(world)], local.contiguous())
+
+        def compute(k):
+            b = k % 2
+            main.wait_event(ev_in[b])
+            xl = x_d[b].to(torch.bfloat16)
+            ev_used[b].record(main)
+            gather_rows(xl, x_full)
+            y = sh.forward(x_full, w, out_dtype=torch.bfloat16)
+            loss = 0.5 * torch.linalg.vector_norm(y, dtype=torch.float32) ** 2
+            gather_rows(y, gy_full)                       # d loss / d y = y
+            gw = sh.weight_grad(x_full, y)
+            h = dist.all_reduce(gw, async_op=True) if use_dist else None
+            sh.input_grad(gy_full, w, out_dtype=torch.bfloat16)
+            if h is not None:
+                h.wait()
+            loss_h[b:b + 1].copy_(loss.reshape(1), non_blocking=True)
+            gw_h.copy_(gw, non_blocking=True)
+        api = "paper_2407_01781_b200.dist.RowShard forward / weight_grad / input_grad + NCCL all-gathers"
+    else:
+        m = P.SparseConv3d(cin, cout).to(dev)
+        if use_dist:
+            P.dist.attach_grad_reducer(m)
+        gb = prob.get("batch") or P.as_grid_batch(prob["grid"])
+        from paper_2407_01781_b200.conv import cache_batch_kernel_map
+        cache_batch_kernel_map(gb, gb, 1, prob["km"])
+
+        def compute(k):
+            b = k % 2
+            main.wait_event(ev_in[b])
+            m.weight.grad = None
+            x = x_d[b].detach().requires_grad_(True)
+            _, y = m(gb, gb.jagged(x))
+            loss = 0.5 * torch.linalg.vector_norm(y.jdata, dtype=torch.float32) ** 2
+            y.jdata.backward(y.jdata.detach())            # d loss / d y = y
+            ev_used[b].record(main)
+            loss_h[b:b + 1].copy_(loss.detach().reshape(1), non_blocking=True)
+            gw_h.copy_(m.weight.grad, non_blocking=True)
+        api = "paper_2407_01781_b200.SparseConv3d (autograd) fwd + bwd"
 
     def upload(k):
         b = k % 2
         with torch.cuda.stream(s_in):
             s_in.wait_event(ev_used[b])  # step k-2 no longer reads buffer b
             x_d[b].copy_(x_h[b], non_blocking=True)
-            gy_d[b].copy_(gy_h[b], non_blocking=True)
-            w_d[b].copy_(w_h[b], non_blocking=True)
             ev_in[b].record(s_in)
-
-    def compute(k):
-        b = k % 2
-        main.wait_event(ev_in[b])
-        with torch.no_grad():
-            m.weight.copy_(w_d[b])
-        m.weight.grad = None
-        x = x_d[b].detach().requires_grad_(True)
-        _, y = m(gb, gb.jagged(x))
-        y.jdata.backward(gy_d[b].to(y.jdata.dtype))
-        if use_dist:
-            dist.all_reduce(m.weight.grad)
-        ev_used[b].record(main)
-        outs = (y.jdata.detach(), x.grad, m.weight.grad)
-        ev_done[b].record(main)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(ev_done[b])
-            s_out.wait_event(ev_drained[b])  # host buffers b free (step k-2 drained)
-            for dst, src in zip((y_h[b], gx_h[b], gw_h[b]), outs):
-                src.record_stream(s_out)
-                dst.copy_(src, non_blocking=True)
-            ev_drained[b].record(s_out)
 
     def run(nsteps):
         upload(0)
@@ -492,114 +666,146 @@ def run_e2e(args, P, torch, dist, grid, km, cin, cout, dev, use_dist):
             if k + 1 < nsteps:
                 upload(k + 1)
             compute(k)
-        main.wait_stream(s_out)
 
     run(2)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(main)
     s_in.wait_stream(main)
-    s_out.wait_stream(main)
     run(steps)
     e1.record(main)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    if use_dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    world = dist.get_world_size() if use_dist else 1
-    h2d = x_h[0].numel() * 4 + gy_h[0].numel() * 4 + w_h[0].numel() * 4
-    d2h = y_h[0].numel() * 2 + gx_h[0].numel() * 4 + gw_h[0].numel() * 4
-    return {"value": round(n * world / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 4),
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "api": "paper_2407_01781_b200.SparseConv3d (autograd) fwd+bwd, fp32 host in, bf16 compute",
-            "pipeline": "inputs of step k+1 uploaded on a copy stream during step k; results drained on a "
-                        "second copy stream; every copy inside the timed region"}
+    ms = max_over_ranks(torch, dist, dev, e0.elapsed_time(e1) / steps, use_dist)
+    units = int(sum_over_ranks(torch, dist, dev, prob["units"], use_dist))
+    h2d = x_h[0].numel() * 4
+    d2h = 4 + gw_h.numel() * 4
+    return {"value": round(units / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 4),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps, "api": api,
+            "step": "upload fp32 features (pinned) -> forward -> loss 0.5*|y|^2 -> backward (dgrad + wgrad"
+                    + (", NCCL all-reduce" if use_dist else "") + ") -> read back loss + fp32 weight gradient",
+            "pipeline": "features of step k+1 uploaded on a copy stream during step k; every copy inside the "
+                        "timed region"}
 
 
-# ----------------------------------------------------------------------------- CPU (oracle port)
+# ----------------------------------------------------------------------------- CPU: the reference itself
 
-def _oracle_problem(cfg, coords, points, seed=0):
-    import oracle as O
-    if points is not None:
-        g = O.build_from_points(points, [0.05] * 3, [0.0] * 3)
+def _reference_module():
+    """The unmodified reference package (baseline/_ref, pip-installed from /root/reference/pkg), or None."""
+    if REF_DIR.is_dir() and str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    try:
+        import idxgrid
+        return idxgrid
+    except Exception:
+        return None
+
+
+def _cpu_problem(cfg, frac):
+    """The grid and the kernel map of a leaf-aligned prefix of ~frac of its output rows; (kind, n, lim, pairs,
+    run(features, weights, grad_out))."""
+    ig = _reference_module()
+    if cfg.get("lidar"):
+        from paper_2407_01781_b200.workloads import lidar_scan_points
+        src = ("points", lidar_scan_points(0), 0.05)
     else:
-        g = O.build_from_coords(coords)
+        coords, points = make_coords(cfg, 0)
+        src = ("points", points, 0.05) if points is not None else ("coords", coords, None)
+    if ig is not None:
+        from idxgrid.conv import STENCIL, KernelMap
+        if src[0] == "points":
+            g, _ = ig.build_from_points(src[1], ig.VoxelTransform.uniform(src[2]))
+        else:
+            g, _ = ig.build_from_coords(src[1])
+        n = g.num_voxels
+        starts = np.asarray(g.leaf_value_offset, np.int64) - 1
+        i = int(np.searchsorted(starts, int(n * frac)))
+        lim = int(starts[i]) if 0 < i < len(starts) else n
+        out_coords = g.active_coords()[:lim]
+        rows = np.arange(lim, dtype=np.int64)
+        ins, outs = [], []
+        for d in STENCIL:  # the reference's build_kernel_map (conv.py:105-122) restricted to the sample rows
+            idx = g.coord_to_index_many(out_coords + d)
+            sel = idx > 0
+            ins.append(idx[sel] - 1)
+            outs.append(rows[sel])
+        km = KernelMap(ins, outs, n, lim, 1)
+
+        def run(f, w, go):
+            ig.conv(g, f, w, kmap=km, variant="igemm")
+            ig.conv_backward(km, go, f, w)
+        return "reference", n, lim, sum(len(o) for o in outs), run
+    import oracle as O
+    if src[0] == "points":
+        g = O.build_from_points(src[1], [src[2]] * 3, [0.0] * 3)
+    else:
+        g = O.build_from_coords(src[1])
     ins, outs = O.kernel_map(g, g, 1)
-    return O, g, ins, outs
-
-
-def _sample_lists(ins, outs, n, frac):
+    n = g.num_voxels
     lim = max(1, int(n * frac))
     si, so = [], []
     for a, b in zip(ins, outs):
-        k = np.searchsorted(b, lim)  # out rows ascending (conv.py:87)
+        k = np.searchsorted(b, lim)
         si.append(a[:k])
         so.append(b[:k])
-    return si, so, lim
+
+    def run(f, w, go):
+        O.conv_igemm(f, w, si, so, lim)
+        O.conv_backward(si, so, go, f, w)
+    return "port", n, lim, sum(len(o) for o in so), run
 
 
-def cpu_baseline(cfg, coords, points, args, frac=1 / 64, repeats=3):
-    """Oracle port (numpy igemm + BLAS) on a prefix of output rows of the same workload."""
-    O, g, ins, outs = _oracle_problem(cfg, coords, points)
-    n = g.num_voxels
-    cin, cout = cfg["cin"], cfg["cout"]
-    si, so, lim = _sample_lists(ins, outs, n, frac)
-    rng = np.random.default_rng(0)
+def _cpu_inputs(n, lim, cin, cout):
+    rng = np.random.default_rng(0)  # cli.py:349-352
     f = rng.normal(size=(n, cin)).astype(np.float32)
     w = (rng.normal(size=(cout, cin, 3, 3, 3)) / np.sqrt(27 * cin)).astype(np.float32)
     go = rng.normal(size=(lim, cout)).astype(np.float32)
+    return f, w, go
+
+
+def _cpu_what(kind):
+    return ("idxgrid.conv(variant='igemm') + idxgrid.conv_backward, the unmodified reference (baseline/_ref)"
+            if kind == "reference" else "oracle port of reference conv.py:180-191, 339-368")
+
+
+def cpu_baseline(cfg, args, frac=1 / 8, repeats=2):
+    """The reference's igemm conv + conv_backward on the host cores, on a leaf-aligned 1/8 of the grid."""
+    kind, n, lim, pairs, run = _cpu_problem(cfg, frac)
+    f, w, go = _cpu_inputs(n, lim, cfg["cin"], cfg["cout"])
     best = float("inf")
     for _ in range(repeats):
         t0 = time.perf_counter()
-        O.conv_igemm(f, w, si, so, lim)
-        O.conv_backward(si, so, go, f, w)
+        run(f, w, go)
         best = min(best, time.perf_counter() - t0)
-    return {"value": round(lim / best, 1), "unit": UNIT, "cores": HOST_THREADS, "kind": "port",
-            "sample": f"first {lim} of {n} output voxels ({frac:.4f} of the grid, leaf-aligned index prefix), "
-                      f"{sum(len(o) for o in so)} pairs, fp32 igemm fwd + conv_backward, best of {repeats}",
+    return {"value": round(lim / best, 1), "unit": UNIT, "cores": HOST_THREADS, "kind": kind,
+            "sample": f"first {lim} of {n} output voxels (leaf-aligned prefix, {lim / n:.3f} of the grid), {pairs} "
+                      f"pairs; fp32 {_cpu_what(kind)}; best of {repeats}",
             "seconds_per_sample": round(best, 4)}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle port of the reference CPU path on the host cores (rank 0 only)."""
+    """--impl reference: the reference's own CPU path on the host cores (rank 0 only; other ranks exit)."""
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    coords, points = make_coords(cfg, 0)
-    O, g, ins, outs = _oracle_problem(cfg, coords, points)
-    n = g.num_voxels
-    cin, cout = cfg["cin"], cfg["cout"]
-    frac = 1 / 256 if args.steps + args.warmup > 60 else 1 / 64
-    si, so, lim = _sample_lists(ins, outs, n, frac)
-    rng = np.random.default_rng(0)
-    f = rng.normal(size=(n, cin)).astype(np.float32)
-    w = (rng.normal(size=(cout, cin, 3, 3, 3)) / np.sqrt(27 * cin)).astype(np.float32)
-    go = rng.normal(size=(lim, cout)).astype(np.float32)
-
-    def step():
-        O.conv_igemm(f, w, si, so, lim)
-        O.conv_backward(si, so, go, f, w)
-
+    frac = 1 / 8 if args.steps + args.warmup <= 30 else 1 / 32
+    kind, n, lim, pairs, run = _cpu_problem(cfg, frac)
+    f, w, go = _cpu_inputs(n, lim, cfg["cin"], cfg["cout"])
     for _ in range(args.warmup):
-        step()
+        run(f, w, go)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        step()
+        run(f, w, go)
         times.append(time.perf_counter() - t0)
     ms = statistics.mean(times) * 1e3
     value = lim / (ms / 1e3)
-    sample = (f"first {lim} of {n} output voxels ({frac:.4f}), {sum(len(o) for o in so)} pairs; fp32 igemm fwd + "
-              f"conv_backward (oracle port of reference conv.py:180-191, 339-368)")
+    sample = f"first {lim} of {n} output voxels (leaf-aligned prefix, {lim / n:.3f}), {pairs} pairs; fp32 {_cpu_what(kind)}"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {cfg['desc']}", "voxels": n, "cin": cin, "cout": cout},
-        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": HOST_THREADS, "kind": "port",
-                         "sample": sample},
+        "scaling": cfg.get("scaling", "weak"), "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "voxels": n, "cin": cfg["cin"], "cout": cfg["cout"]},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": HOST_THREADS, "kind": kind, "sample": sample},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

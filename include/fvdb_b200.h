@@ -320,6 +320,11 @@ int fvdb_interp_splat(int dtype, const void* point_features, int64_t channels, c
 /* dtype conversion helpers (fp32 -> bf16 RNE), used at the module boundary */
 int fvdb_f32_to_bf16(const float* src, int64_t n, void* dst, void* stream);
 
+/* ---- measurement probe (bench.py roofline denominators; not on the product path) ----
+ * FP32 FFMA peak: launches the probe kernel on `stream` and writes its FLOP count to *flops (host); time it with
+ * events.  out: device float[n] scratch. */
+int fvdb_probe_ffma(int iters, float* out, int64_t n, double* flops, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

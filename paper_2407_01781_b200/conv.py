@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 import torch
@@ -233,6 +234,20 @@ def _grid_colors(grids, shift):
     return torch.cat([parity_colors(g.active_coords(), shift) for g in grids]) if grids else None
 
 
+def _colors_fn(grid_refs, stride, transposed):
+    """Lane colours of a map's table (fvdb_halo_plan) from weak references to its grids: forward map: inputs
+    P(c >> (stride-1)), outputs P(c); transposed map: inputs P(c), outputs P(c >> (stride-1)); P = coordinate-sum
+    parity.  (None, None) — plan without colours — if a grid has been released."""
+    def fn():
+        gi, go = [r() for r in grid_refs[0]], [r() for r in grid_refs[1]]
+        if any(g is None for g in gi + go):
+            return None, None
+        if transposed:
+            return _grid_colors(go, 0), _grid_colors(gi, stride - 1)
+        return _grid_colors(gi, stride - 1), _grid_colors(go, 0)
+    return fn
+
+
 def padded_len(n: int) -> int:
     a = _lib.NBR_ALIGN
     return max(a, (int(n) + a - 1) // a * a)
@@ -267,7 +282,11 @@ class KernelMap:
         self.num_in, self.num_out, self.stride = int(num_in), int(num_out), int(stride)
         self._lists = None
         self._bwd = None
-        self._grids = grids  # (grids_in, grids_out) lists, for the halo plan's lane colours
+        # (grids_in, grids_out) as weak references, for the halo plan's lane colours: a map cached on its
+        # output grid must not keep that grid alive through a reference cycle (tables are ~100 MB; a cycle
+        # defers their release to the cyclic GC, and every rebuilt map then needs a fresh cudaMalloc)
+        self._grids = None if grids is None else ([weakref.ref(g) for g in grids[0]],
+                                                  [weakref.ref(g) for g in grids[1]])
         if table is None:
             from .topology import _device
             dev = _device()
@@ -290,19 +309,16 @@ class KernelMap:
         if table.counts is None:
             table.counts = pair_counts
         if table._colors_fn is None and grids is not None:
-            table._colors_fn = self._fwd_colors
+            table._colors_fn = _colors_fn(self._grids, self.stride, False)
         self.fwd = table
         self._counts = pair_counts
 
-    # Lane colours (fvdb_halo_plan): forward map: inputs P(c >> (stride-1)), outputs P(c);
-    # transposed map: inputs P(c), outputs P(c >> (stride-1)).  P = coordinate-sum parity.
-    def _fwd_colors(self):
-        gi, go = self._grids
-        return _grid_colors(gi, self.stride - 1), _grid_colors(go, 0)
-
-    def _bwd_colors(self):
-        gi, go = self._grids
-        return _grid_colors(go, 0), _grid_colors(gi, self.stride - 1)
+    def grids(self):
+        """(grids_in, grids_out) the map was built for, or None (unknown, or a grid was released)."""
+        if self._grids is None:
+            return None
+        gi, go = [r() for r in self._grids[0]], [r() for r in self._grids[1]]
+        return None if any(g is None for g in gi + go) else (gi, go)
 
     @property
     def nbr(self):
@@ -366,7 +382,7 @@ class KernelMap:
                 L = _lib.lib()
                 _lib.check(L.fvdb_kmap_transpose(self.fwd.t.data_ptr(), self.fwd.ld, self.num_out, self.num_in,
                                                  t.data_ptr(), t.shape[1], _lib.stream_ptr()), "kmap_transpose")
-            self._bwd = NbrTable(t, self.num_in, self._bwd_colors if self._grids is not None else None,
+            self._bwd = NbrTable(t, self.num_in, _colors_fn(self._grids, self.stride, True) if self._grids else None,
                                  counts=self._counts)
             self._bwd.sparse = self.stride == 2  # fine voxel i pairs only offsets d with i - d even: <= 8 of 27
         return self._bwd
@@ -375,7 +391,7 @@ class KernelMap:
         if self.stride != 1 or self._grids is None or self.num_in != self.num_out:
             return False
         gi, go = self._grids
-        return len(gi) == len(go) and all(a is b for a, b in zip(gi, go))
+        return len(gi) == len(go) and all(a() is b() and a() is not None for a, b in zip(gi, go))
 
     def transposed_table(self):
         return self.bwd.view
@@ -445,8 +461,9 @@ def batch_kernel_map(kmaps, in_offsets, out_offsets):
         t[:, int(oo):int(oo) + km.num_out] = torch.where(v >= 0, v + int(io), v)
     counts = torch.stack([km._counts.to(dev) for km in kmaps]).sum(0)
     grids = None
-    if all(km._grids is not None for km in kmaps):
-        grids = ([g for km in kmaps for g in km._grids[0]], [g for km in kmaps for g in km._grids[1]])
+    gs = [km.grids() for km in kmaps]
+    if all(g is not None for g in gs):
+        grids = ([g for gi, _ in gs for g in gi], [g for _, go in gs for g in go])
     return KernelMap(num_in=num_in, num_out=num_out, stride=kmaps[0].stride, table=NbrTable(t, num_out),
                      pair_counts=counts, grids=grids)
 
@@ -904,20 +921,20 @@ def conv_batch(batch, features, kernel, variant="igemm"):
 def cache_batch_kernel_map(batch_in, batch_out, stride, km):
     """Store ``km`` as the (batch_in -> batch_out, stride) map in ``batch_out``'s cache.
 
-    The entry is keyed by ``id(batch_in)`` but holds a weak reference to ``batch_in`` that every lookup
-    checks, so a new batch that reuses a collected batch's id never gets the old map; entries of
-    collected batches are dropped on the next store."""
-    import weakref
+    The entry is keyed by the ids of ``batch_in``'s grids and holds weak references to them that every lookup
+    checks, so grids that reuse a collected grid's id never get the old map; entries of collected grids are
+    dropped on the next store.  No strong reference from the cache back to the grids: no cycles."""
     cache = batch_out._kmaps
-    for k in [k for k, v in cache.items() if isinstance(v, tuple) and v[0]() is None]:
+    for k in [k for k, v in cache.items() if k[0] == "kmap" and any(r() is None for r in v[0])]:  # noqa: E501
         del cache[k]
-    cache[("kmap", id(batch_in), int(stride))] = (weakref.ref(batch_in), km)
+    cache[("kmap", tuple(id(g) for g in batch_in.grids), int(stride))] = (
+        tuple(weakref.ref(g) for g in batch_in.grids), km)
     return km
 
 
 def cached_batch_kernel_map(batch_in, batch_out, stride):
-    v = batch_out._kmaps.get(("kmap", id(batch_in), int(stride)))
-    if v is not None and v[0]() is batch_in:
+    v = batch_out._kmaps.get(("kmap", tuple(id(g) for g in batch_in.grids), int(stride)))
+    if v is not None and all(r() is g for r, g in zip(v[0], batch_in.grids)):
         return v[1]
     return None
 

@@ -92,108 +92,91 @@ __device__ __forceinline__ int batch_of_leaf(const KmapBatch& kb, int64_t l) {
     return b;
 }
 
-// tree walk once per (output leaf, neighbour leaf): nleaf[l][e] (grid-local leaf of the element's input grid)
-__global__ void k_neighbor_leaves(const __grid_constant__ KmapBatch kb, int stride, int32_t* __restrict__ nleaf) {
-    const int64_t total = kb.leaf_start[kb.B] * 27;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t lg = t / 27;
-        const int e = (int)(t - lg * 27);
+// One WARP per output leaf, kWarpsPerCta leaves per CTA (a cfg2 leaf holds ~114 voxels, a LiDAR leaf ~18: a
+// CTA per leaf left most threads idle).  Per leaf: lanes 0..26 walk the input tree once for the 27 neighbour
+// leaves of the 3x3x3 block around the leaf (for stride 2 around the leaf at 2 * origin), their masks are staged
+// in the warp's shared-memory slice, and the lanes then walk the leaf's voxels once per offset with bit tests +
+// popcount ranks, writing each offset row of the table coalesced.  Pair counts: warp reductions into per-CTA
+// shared counters, then one 64-bit global atomic per (CTA, offset) (integer sums: deterministic).
+constexpr int kKmWarps = 8, kKmThreads = kKmWarps * 32;
+struct KmWarpSmem {
+    uint64_t mask[27][8];
+    uint64_t pre[27];
+    int64_t vo[27];
+    int32_t nl[27];
+    uint16_t pos[512];
+    uint64_t own[8];
+};
+
+__global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant__ KmapBatch kb, int stride,
+                                                           int32_t* __restrict__ nbr, int64_t ld,
+                                                           unsigned long long* __restrict__ counts) {
+    __shared__ KmWarpSmem sw[kKmWarps];
+    __shared__ int s_cnt[27];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < 27) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t lg = (int64_t)blockIdx.x * kKmWarps + warp;
+    if (lg < kb.leaf_start[kb.B]) {
+        KmWarpSmem& S = sw[warp];
         const int b = batch_of_leaf(kb, lg);
+        const fvdb_grid_view& gin = kb.gin[b];
         const fvdb_grid_view& gout = kb.gout[b];
         const int64_t l = lg - kb.leaf_start[b];
-        int64_t bx = stride * gout.leaf_origins[3 * l] + 8 * (e / 9 - 1);
-        int64_t by = stride * gout.leaf_origins[3 * l + 1] + 8 * ((e / 3) % 3 - 1);
-        int64_t bz = stride * gout.leaf_origins[3 * l + 2] + 8 * (e % 3 - 1);
-        nleaf[t] = (int32_t)find_leaf(kb.gin[b], bx, by, bz);
-    }
-}
-
-// CTA per output leaf: 27 probes per active voxel against staged neighbour-leaf masks.  Nine warps own three
-// offsets each and their lanes walk the leaf's voxels (no per-item division; each offset row is written
-// coalesced); per-offset pair counts are warp reductions stored per leaf (partial[d][leaf]) and summed by
-// k_pair_counts, instead of shared + global atomics on 27 addresses.
-constexpr int kKmWarps = 9, kKmThreads = kKmWarps * 32;
-__global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant__ KmapBatch kb, int stride,
-                                                           const int32_t* __restrict__ nleaf,
-                                                           int32_t* __restrict__ nbr, int64_t ld,
-                                                           int32_t* __restrict__ partial, int64_t n_leaf_all) {
-    __shared__ uint64_t s_mask[27][8];
-    __shared__ uint64_t s_pre[27];
-    __shared__ int64_t s_vo[27];
-    __shared__ int32_t s_nl[27];
-    __shared__ uint16_t s_pos[512];
-    __shared__ uint64_t s_own[8];
-
-    const int64_t lg = blockIdx.x;
-    const int b = batch_of_leaf(kb, lg);
-    const fvdb_grid_view& gin = kb.gin[b];
-    const fvdb_grid_view& gout = kb.gout[b];
-    const int64_t l = lg - kb.leaf_start[b];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid < 27) {
-        int32_t nl = nleaf[lg * 27 + tid];
-        s_nl[tid] = nl;
-        s_pre[tid] = nl >= 0 ? gin.leaf_prefix[nl] : 0;
-        s_vo[tid] = nl >= 0 ? kb.in_base[b] + (int64_t)gin.leaf_value_offset[nl] - 1 : 0;
-    }
-    if (tid < 8) s_own[tid] = gout.leaf_masks[8 * l + tid];
-    for (int q = tid; q < 27 * 8; q += kKmThreads) {
-        int e = q >> 3;
-        int32_t nl = nleaf[lg * 27 + e];
-        s_mask[e][q & 7] = nl >= 0 ? gin.leaf_masks[8 * (int64_t)nl + (q & 7)] : 0ull;
-    }
-    __syncthreads();
-    const uint64_t own_pre = gout.leaf_prefix[l];
-    for (uint32_t m = tid; m < 512; m += kKmThreads)
-        if ((s_own[m >> 6] >> (m & 63)) & 1ull) s_pos[leaf_rank(s_own, own_pre, m)] = (uint16_t)m;
-    int nvox = 0;
+        if (lane < 27) {
+            const int64_t bx = stride * gout.leaf_origins[3 * l] + 8 * (lane / 9 - 1);
+            const int64_t by = stride * gout.leaf_origins[3 * l + 1] + 8 * ((lane / 3) % 3 - 1);
+            const int64_t bz = stride * gout.leaf_origins[3 * l + 2] + 8 * (lane % 3 - 1);
+            const int32_t nl = (int32_t)find_leaf(gin, bx, by, bz);
+            S.nl[lane] = nl;
+            S.pre[lane] = nl >= 0 ? gin.leaf_prefix[nl] : 0;
+            S.vo[lane] = nl >= 0 ? kb.in_base[b] + (int64_t)gin.leaf_value_offset[nl] - 1 : 0;
+        } else if (lane < 27 + 5) {
+            // lanes 27..31 fetch the leaf's own mask words meanwhile
+            for (int w = lane - 27; w < 8; w += 5) S.own[w] = gout.leaf_masks[8 * l + w];
+        }
+        __syncwarp();
+        for (int q = lane; q < 27 * 8; q += 32) {
+            const int32_t nl = S.nl[q >> 3];
+            S.mask[q >> 3][q & 7] = nl >= 0 ? gin.leaf_masks[8 * (int64_t)nl + (q & 7)] : 0ull;
+        }
+        // voxel m of the leaf at rank position: lane owns bits [16 lane, 16 lane + 16)
+        const uint64_t own_pre = gout.leaf_prefix[l];
+        {
+            const uint32_t m0 = (uint32_t)lane * 16;
+            const uint32_t bits = (uint32_t)(S.own[m0 >> 6] >> (m0 & 63)) & 0xFFFFu;
+            int r = leaf_rank(S.own, own_pre, m0);
+            for (uint32_t t = bits; t; t &= t - 1) S.pos[r++] = (uint16_t)(m0 + __ffs(t) - 1);
+        }
+        int nvox = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) nvox += __popcll(s_own[w]);
-    __syncthreads();
-
-    const int64_t row0 = kb.out_base[b] + (int64_t)gout.leaf_value_offset[l] - 1;
-#pragma unroll
-    for (int j = 0; j < 27 / kKmWarps; ++j) {
-        const int d = warp + j * kKmWarps;
-        const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
-        int32_t* out = nbr + (int64_t)d * ld + row0;
-        int cnt = 0;
-        for (int r = lane; r < nvox; r += 32) {
-            const uint32_t m = s_pos[r];
-            const int qx = stride * (int)(m >> 6) + dx;
-            const int qy = stride * (int)((m >> 3) & 7) + dy;
-            const int qz = stride * (int)(m & 7) + dz;
-            const int e = ((qx >> 3) + 1) * 9 + ((qy >> 3) + 1) * 3 + ((qz >> 3) + 1);
-            int32_t row = -1;
-            if (s_nl[e] >= 0) {
+        for (int w = 0; w < 8; ++w) nvox += __popcll(S.own[w]);
+        __syncwarp();
+        const int64_t row0 = kb.out_base[b] + (int64_t)gout.leaf_value_offset[l] - 1;
+        for (int d = 0; d < 27; ++d) {
+            const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
+            int32_t* out = nbr + (int64_t)d * ld + row0;
+            int cnt = 0;
+            for (int r = lane; r < nvox; r += 32) {
+                const uint32_t m = S.pos[r];
+                const int qx = stride * (int)(m >> 6) + dx;
+                const int qy = stride * (int)((m >> 3) & 7) + dy;
+                const int qz = stride * (int)(m & 7) + dz;
+                const int e = ((qx >> 3) + 1) * 9 + ((qy >> 3) + 1) * 3 + ((qz >> 3) + 1);
+                int32_t row = -1;
                 const uint32_t bb = (uint32_t)(((qx & 7) << 6) | ((qy & 7) << 3) | (qz & 7));
-                if ((s_mask[e][bb >> 6] >> (bb & 63)) & 1ull) {
-                    row = (int32_t)(s_vo[e] + leaf_rank(s_mask[e], s_pre[e], bb));
+                if ((S.mask[e][bb >> 6] >> (bb & 63)) & 1ull) {
+                    row = (int32_t)(S.vo[e] + leaf_rank(S.mask[e], S.pre[e], bb));
                     ++cnt;
                 }
+                out[r] = row;
             }
-            out[r] = row;
+            cnt = __reduce_add_sync(0xffffffffu, cnt);
+            if (lane == 0 && cnt) atomicAdd(&s_cnt[d], cnt);
         }
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0) partial[(int64_t)d * n_leaf_all + lg] = cnt;
     }
-}
-
-// pair_counts[d] = sum over output leaves of partial[d][leaf]   (one CTA per offset)
-__global__ void k_pair_counts(const int32_t* __restrict__ partial, int64_t n_leaf, int64_t* __restrict__ counts) {
-    __shared__ long long s_sum[8];
-    const int d = blockIdx.x;
-    long long acc = 0;
-    for (int64_t i = threadIdx.x; i < n_leaf; i += blockDim.x) acc += partial[(int64_t)d * n_leaf + i];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        long long t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_sum[w];
-        counts[d] = t;
-    }
+    if (threadIdx.x < 27 && s_cnt[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
 }
 
 // padding columns [n_out, ld) of every offset row := -1
@@ -316,11 +299,8 @@ extern "C" int fvdb_kernel_map_batch(const fvdb_grid_view* gin, const fvdb_grid_
         FVDB_CUDA_TRY(cudaMemsetAsync(pair_counts, 0, 27 * sizeof(int64_t), st));
         return FVDB_OK;
     }
-    int32_t* nleaf = reinterpret_cast<int32_t*>(ws);
-    int32_t* partial = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(ws) +
-                                                  ((size_t)n_leaf * 27 * sizeof(int32_t) + 255) / 256 * 256);
-    // leaves of every chunk are numbered after the previous chunks', so partial[d][leaf] is one array
-    int64_t leaf0 = 0;
+    (void)ws;
+    FVDB_CUDA_TRY(cudaMemsetAsync(pair_counts, 0, 27 * sizeof(int64_t), st));
     for (int64_t c0 = 0; c0 < B; c0 += kMaxBatch) {
         KmapBatch kb;
         kb.B = (int)(B - c0 < kMaxBatch ? B - c0 : kMaxBatch);
@@ -334,12 +314,9 @@ extern "C" int fvdb_kernel_map_batch(const fvdb_grid_view* gin, const fvdb_grid_
         }
         const int64_t nl = kb.leaf_start[kb.B];
         if (nl == 0) continue;
-        k_neighbor_leaves<<<grid_for(nl * 27), kThreads, 0, st>>>(kb, stride, nleaf + leaf0 * 27);
-        k_kernel_map<<<(unsigned)nl, kKmThreads, 0, st>>>(kb, stride, nleaf + leaf0 * 27, nbr, ld, partial + leaf0,
-                                                          n_leaf);
-        leaf0 += nl;
+        k_kernel_map<<<(unsigned)ceil_div(nl, kKmWarps), kKmThreads, 0, st>>>(
+            kb, stride, nbr, ld, reinterpret_cast<unsigned long long*>(pair_counts));
     }
-    k_pair_counts<<<27, 256, 0, st>>>(partial, n_leaf, pair_counts);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

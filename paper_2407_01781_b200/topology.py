@@ -99,7 +99,7 @@ class IndexGrid:
         self.transform = transform
         self.name = name
         self._view = None
-        self._batch = None  # single-grid GridBatch wrapper (SparseConv3d on a bare grid), cached
+        self._batch = None  # kernel-map cache of the single-grid GridBatch views of this grid (as_grid_batch)
 
     # -- counts (topology.py:179-201) ---------------------------------------
     @property
