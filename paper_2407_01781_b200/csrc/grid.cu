@@ -101,8 +101,8 @@ __device__ __forceinline__ int batch_of_leaf(const KmapBatch& kb, int64_t l) {
 constexpr int kKmWarps = 8, kKmThreads = kKmWarps * 32;
 struct KmWarpSmem {
     uint64_t mask[27][8];
-    uint64_t pre[27];
-    int64_t vo[27];
+    int32_t base[27][8];   // row of the first voxel of mask word w of neighbour leaf e (input_base + value offset
+                           // - 1 + popcount of words < w): a probe's row is base + popcount below its bit
     int32_t nl[27];
     uint16_t pos[512];
     uint64_t own[8];
@@ -123,15 +123,15 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant
         const fvdb_grid_view& gin = kb.gin[b];
         const fvdb_grid_view& gout = kb.gout[b];
         const int64_t l = lg - kb.leaf_start[b];
+        int64_t vo = 0;
         if (lane < 27) {
             const int64_t bx = stride * gout.leaf_origins[3 * l] + 8 * (lane / 9 - 1);
             const int64_t by = stride * gout.leaf_origins[3 * l + 1] + 8 * ((lane / 3) % 3 - 1);
             const int64_t bz = stride * gout.leaf_origins[3 * l + 2] + 8 * (lane % 3 - 1);
             const int32_t nl = (int32_t)find_leaf(gin, bx, by, bz);
             S.nl[lane] = nl;
-            S.pre[lane] = nl >= 0 ? gin.leaf_prefix[nl] : 0;
-            S.vo[lane] = nl >= 0 ? kb.in_base[b] + (int64_t)gin.leaf_value_offset[nl] - 1 : 0;
-        } else if (lane < 27 + 5) {
+            vo = nl >= 0 ? kb.in_base[b] + (int64_t)gin.leaf_value_offset[nl] - 1 : 0;
+        } else {
             // lanes 27..31 fetch the leaf's own mask words meanwhile
             for (int w = lane - 27; w < 8; w += 5) S.own[w] = gout.leaf_masks[8 * l + w];
         }
@@ -140,39 +140,61 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant
             const int32_t nl = S.nl[q >> 3];
             S.mask[q >> 3][q & 7] = nl >= 0 ? gin.leaf_masks[8 * (int64_t)nl + (q & 7)] : 0ull;
         }
-        // voxel m of the leaf at rank position: lane owns bits [16 lane, 16 lane + 16)
-        const uint64_t own_pre = gout.leaf_prefix[l];
+        __syncwarp();
+        if (lane < 27) {  // per-word row bases of neighbour leaf `lane`
+            int32_t acc = (int32_t)vo;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                S.base[lane][w] = acc;
+                acc += __popcll(S.mask[lane][w]);
+            }
+        }
+        // voxel positions in rank order: lane owns bits [16 lane, 16 lane + 16) of the leaf's mask
         {
             const uint32_t m0 = (uint32_t)lane * 16;
             const uint32_t bits = (uint32_t)(S.own[m0 >> 6] >> (m0 & 63)) & 0xFFFFu;
-            int r = leaf_rank(S.own, own_pre, m0);
+            int r = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w)
+                if (w < (int)(m0 >> 6)) r += __popcll(S.own[w]);
+            r += __popcll(S.own[m0 >> 6] & ((1ull << (m0 & 63)) - 1ull));
             for (uint32_t t = bits; t; t &= t - 1) S.pos[r++] = (uint16_t)(m0 + __ffs(t) - 1);
         }
         int nvox = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) nvox += __popcll(S.own[w]);
         __syncwarp();
-        const int64_t row0 = kb.out_base[b] + (int64_t)gout.leaf_value_offset[l] - 1;
-        for (int d = 0; d < 27; ++d) {
-            const int dx = d / 9 - 1, dy = (d / 3) % 3 - 1, dz = d % 3 - 1;
-            int32_t* out = nbr + (int64_t)d * ld + row0;
-            int cnt = 0;
-            for (int r = lane; r < nvox; r += 32) {
-                const uint32_t m = S.pos[r];
-                const int qx = stride * (int)(m >> 6) + dx;
-                const int qy = stride * (int)((m >> 3) & 7) + dy;
-                const int qz = stride * (int)(m & 7) + dz;
-                const int e = ((qx >> 3) + 1) * 9 + ((qy >> 3) + 1) * 3 + ((qz >> 3) + 1);
-                int32_t row = -1;
-                const uint32_t bb = (uint32_t)(((qx & 7) << 6) | ((qy & 7) << 3) | (qz & 7));
-                if ((S.mask[e][bb >> 6] >> (bb & 63)) & 1ull) {
-                    row = (int32_t)(S.vo[e] + leaf_rank(S.mask[e], S.pre[e], bb));
-                    ++cnt;
-                }
-                out[r] = row;
+        // voxel-outer, offset-inner: a lane's 27 probes share the per-axis neighbour-leaf / bit terms; each offset's
+        // stores stay coalesced across the lanes (consecutive rows)
+        int32_t* out = nbr + kb.out_base[b] + (int64_t)gout.leaf_value_offset[l] - 1;
+        for (int r = lane; r < nvox; r += 32) {
+            const uint32_t act = __activemask();
+            const bool leader = lane == __ffs(act) - 1;
+            const int m = S.pos[r];
+            const int x = m >> 6, y = (m >> 3) & 7, z = m & 7;
+            int ex[3], ey[3], ez[3], bx[3], by[3], bz[3];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const int qx = stride * x + t - 1, qy = stride * y + t - 1, qz = stride * z + t - 1;
+                ex[t] = ((qx >> 3) + 1) * 9;
+                ey[t] = ((qy >> 3) + 1) * 3;
+                ez[t] = (qz >> 3) + 1;
+                bx[t] = (qx & 7) << 6;
+                by[t] = (qy & 7) << 3;
+                bz[t] = qz & 7;
             }
-            cnt = __reduce_add_sync(0xffffffffu, cnt);
-            if (lane == 0 && cnt) atomicAdd(&s_cnt[d], cnt);
+#pragma unroll
+            for (int d = 0; d < 27; ++d) {
+                const int i = d / 9, j = (d / 3) % 3, k = d % 3;
+                const int e = ex[i] + ey[j] + ez[k];
+                const int bb = bx[i] | by[j] | bz[k];
+                const uint64_t word = S.mask[e][bb >> 6];
+                const uint64_t below = word & ((1ull << (bb & 63)) - 1ull);
+                const bool hit = (word >> (bb & 63)) & 1ull;
+                out[(int64_t)d * ld + r] = hit ? S.base[e][bb >> 6] + __popcll(below) : -1;
+                const int c = __popc(__ballot_sync(act, hit));
+                if (leader && c) atomicAdd(&s_cnt[d], c);
+            }
         }
     }
     __syncthreads();
