@@ -74,6 +74,13 @@ CONFIGS = {
     "cfg4": dict(desc="sparse U-Net stage: build from jagged points (cfg2 shell as f64 voxel centres), coarsen, "
                       "stride-2 conv 64->128 + transposed conv 128->64, fwd+bwd, bf16", res=470, cin=64, cout=128,
                  unet=True),
+    # the reference's dense-window regime (leaf / brick schedules): fully occupied blocks
+    "dense32": dict(desc="dense 160^3 block (4.1M voxels, 100% leaf occupancy), SparseConv3d 3x3x3 32->32 bf16 fwd+bwd",
+                    dense=160, cin=32, cout=32, scaling="weak"),
+    "dense64": dict(desc="dense 128^3 block (2.1M voxels, 100% leaf occupancy), SparseConv3d 3x3x3 64->64 bf16 fwd+bwd",
+                    dense=128, cin=64, cout=64, scaling="weak"),
+    "dense128": dict(desc="dense 96^3 block (0.88M voxels, 100% leaf occupancy), SparseConv3d 3x3x3 128->128 bf16 "
+                          "fwd+bwd", dense=96, cin=128, cout=128, scaling="weak"),
     "cfg5": dict(desc="2048^3 surface shell sphere_shell_coords(2048, band=1.5), SparseConv3d 3x3x3 32->32 bf16 "
                       "fwd+bwd, output rows sharded across ranks at leaf boundaries", res=2048, cin=32, cout=32,
                  rowshard=True, scaling="strong"),
@@ -110,6 +117,9 @@ def make_coords(cfg, rank):
     from paper_2407_01781_b200.workloads import random_points, sphere_shell_coords
     if cfg.get("points"):
         return None, random_points(np.random.default_rng(rank), 100_000, sigma=1.0)
+    if cfg.get("dense"):
+        r = np.arange(cfg["dense"])
+        return np.stack(np.meshgrid(r, r, r, indexing="ij"), -1).reshape(-1, 3), None
     return sphere_shell_coords(cfg["res"], band=1.5), None
 
 
@@ -365,6 +375,8 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- fresh-map step (cfg2, rank-local): build + kernel map + first-use kernels (no halo plan) ----
     fresh = run_fresh(torch, P, dev, x, gy, w) if args.config == "cfg2" else None
+    # ---- schedules side by side (the reference's igemm vs its dense-window leaf / brick regime) ----
+    schedules = compare_schedules(torch, flush, x, t_fwd, w) if cfg.get("dense") or args.config == "cfg2" else None
 
     # ---- end-to-end through the public API with host data ----
     e2e = run_e2e(args, cfg, P, torch, dist, prob, cin, cout, dev, use_dist, world)
@@ -427,12 +439,37 @@ def run_ours(args, rank, world, local_rank):
         }
         if fresh is not None:
             line["fresh_map_step"] = fresh
+        if schedules is not None:
+            line["schedules_fwd_ms"] = schedules
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def compare_schedules(torch, flush, x, table, w, reps=10):
+    """Forward time of the gather kernel (igemm schedule: every pair's row gathered from L2) and of the halo
+    kernel (dense-window schedule: each tile's neighbourhood staged once), median of reps with L2 flushes."""
+    from paper_2407_01781_b200.conv import gather_conv, pack_weights_umma
+    out = {}
+    for impl in ("gather", "halo"):
+        img = pack_weights_umma(w, False, impl)
+        gather_conv(x, table, w, w_image=img, impl=impl)
+        ts = []
+        for _ in range(reps):
+            flush.fill_(3)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            gather_conv(x, table, w, w_image=img, impl=impl)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        out[{"gather": "igemm (gather kernel)", "halo": "leaf/brick (halo kernel)"}[impl]] = round(sorted(ts)[reps // 2], 4)
+    v = list(out.values())
+    out["speedup"] = round(v[0] / v[1], 3)
+    return out
 
 
 def run_fresh(torch, P, dev, x, gy, w):
@@ -819,8 +856,16 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # FVDB_DIST_BACKEND=gloo runs the multi-rank code paths on fewer GPUs than ranks (functional check only:
+        # NCCL needs one GPU per rank); ranks then share devices round-robin
+        backend = os.environ.get("FVDB_DIST_BACKEND", "nccl")
+        if backend != "nccl":
+            local_rank = local_rank % torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     elif args.gpus > 1:
         print(json.dumps({"error": "--gpus > 1 needs torchrun (one process per GPU)"}), file=sys.stderr)
     run_ours(args, rank, world, local_rank)

@@ -226,3 +226,24 @@ def test_cfg5_full_size_halo_adjoint_and_determinism():
     lhs_w = float((gw.double() * wb).sum())
     scale_w = float((gw.double().abs() * wb.abs()).sum())
     assert abs(lhs_w - lhs) / scale_w < 1e-5
+
+
+def test_variant_selects_dense_window_schedule():
+    """variant="leaf"/"brick" (the reference's dense-window schedules, conv.py:200-261) run the halo kernel from
+    the first call; "igemm" keeps the gather kernel for a fresh map; all compute the same operator."""
+    r = np.arange(24)
+    coords = np.stack(np.meshgrid(r, r, r, indexing="ij"), -1).reshape(-1, 3)
+    g, _ = P.build_from_coords(coords)
+    rng = np.random.default_rng(4)
+    x = torch.from_numpy(rng.normal(size=(g.num_voxels, 64)).astype(np.float32)).cuda().to(torch.bfloat16)
+    w = torch.from_numpy((rng.normal(size=(64, 64, 3, 3, 3)) / np.sqrt(27 * 64)).astype(np.float32))
+    km = P.build_kernel_map(g, g, 1)
+    y_igemm = P.conv(g, x, w, variant="igemm", kmap=km)
+    assert not km.fwd.has_plan(64, 64)
+    for v in ("leaf", "brick"):
+        y = P.conv(g, x, w, variant=v, kmap=km)
+        assert km.fwd.has_plan(64, 64)
+        assert float((y.float() - y_igemm.float()).abs().max()) <= 2e-2 * float(y_igemm.float().abs().max())
+    assert P.choose_variant(g, 64, 64) == "brick"  # 100% leaf occupancy
+    y_auto = P.conv(g, x, w, variant="auto", kmap=km)
+    assert torch.equal(y_auto, P.conv(g, x, w, variant="brick", kmap=km))
