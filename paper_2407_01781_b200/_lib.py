@@ -7,12 +7,15 @@ The product path has no CPU fallback: every operator calls into this library and
 from __future__ import annotations
 
 import ctypes as C
+import os
 import pathlib
 
 import torch
 
 _PKG = pathlib.Path(__file__).resolve().parent
 LIB_PATH = _PKG / "_lib" / "libfvdb_b200.so"
+if os.environ.get("FVDB_LIB_VARIANT"):  # profiling: an alternative build in _lib/variants/ (tools/)
+    LIB_PATH = _PKG / "_lib" / "variants" / f"libfvdb_b200_{os.environ['FVDB_LIB_VARIANT']}.so"
 
 FVDB_OK = 0
 FVDB_ERR_INVALID = -1

@@ -589,6 +589,14 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
 // D_0 + D_1 + D_2 + D_3 in that order (deterministic), releasing each D as soon as it is read.
 // Weights: per set WSL slots of one offset image each, TMA-loaded ahead by the weight-loader warp.
 // ---------------------------------------------------------------------------------------------
+// A slots per set / accumulator buffers per set (compile-time; measured at K = 32, fwd ms cfg5 / cfg2_32:
+// 2 / 1: 3.22 / 0.183, 2 / 2: 3.26 / 0.185, 3 / 1: 3.29 / 0.187, 3 / 2: 3.34 / 0.189)
+#ifndef FVDB_H4_ASL
+#define FVDB_H4_ASL 2
+#endif
+#ifndef FVDB_H4_DB
+#define FVDB_H4_DB 1
+#endif
 template <int K, int N>
 struct Halo4Cfg {
     static constexpr int SETS = 4;
@@ -598,13 +606,20 @@ struct Halo4Cfg {
     static constexpr uint32_t BLAYOUT = BROWB == 128 ? kSwizzle128B : kSwizzle64B;
     static constexpr int B_BYTES = N * K * 2;
     static constexpr int ACOLS = K / 2;
-    static constexpr int DCOLS = SETS * N;
-    // A slots per set: two, alternating with the two named barriers of the set (a builder can then be at most
-    // one stage ahead of its issuer, which the barrier pairing requires)
-    static constexpr int ASL = 2;
+    // accumulators: double-buffered per set when TMEM allows (the set starts its next tile while the epilogue
+    // drains the last one), single otherwise
+    static constexpr int DB = FVDB_H4_DB == 2 && 2 * SETS * N + SETS * 2 * ACOLS <= 512 ? 2 : 1;
+    static constexpr int DCOLS = DB * SETS * N;
+    // A slots per set, one named barrier per slot (a builder is then at most ASL - 1 stages ahead of its issuer,
+    // which the barrier ring requires); SETS * ASL <= 15 hardware barriers besides barrier 0
+    static constexpr int ASL = cmin(FVDB_H4_ASL, (512 - DCOLS) / (SETS * ACOLS));
     static constexpr int WSL = 3;   // weight slots per set (the weight-loader warp fills them ahead)
     static constexpr int WPRE = 1;
-    static constexpr int FIXED = 1024 + SETS * WSL * B_BYTES + 2 * kIdxBytes;
+    // all 27 offset images resident in shared memory (loaded once per CTA) when they fit beside the halo:
+    // no weight hand-off at all (K = 32 or N = 32: 54-108 KB)
+    static constexpr bool RESIDENT = 27 * B_BYTES <= 110 * 1024;
+    static constexpr int WBYTES = RESIDENT ? 27 * B_BYTES : SETS * WSL * B_BYTES;
+    static constexpr int FIXED = 1024 + WBYTES + 2 * kIdxBytes;
     static constexpr int CAP = ((kSmemMax - 2048 - FIXED) / (2 * (ROWB + 4))) & ~7;
     static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4);
     static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, N, false, false);
@@ -613,7 +628,7 @@ struct Halo4Cfg {
     static constexpr int HC = N / 2;                          // columns per epilogue thread
     // halo loader, weight loader, builders, one MMA issuer per set, epilogue
     static constexpr int THREADS = (2 + BUILDERS + SETS + EPI) * 32;
-    static_assert(ASL >= 2, "two A slots per set at least");
+    static_assert(ASL >= 2 && SETS * ASL <= 15, "two A slots per set at least; named barriers");
     static_assert(CAP >= 256, "halo capacity must hold one offset phase");
     static_assert(DCOLS + SETS * ASL * ACOLS <= 512, "TMEM");
 };
@@ -623,20 +638,20 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
     k_conv_halo4(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, fvdb_halo_plan P, int64_t n_out,
                  void* __restrict__ out, int dbg) {
     using C = Halo4Cfg<K, N>;
-    constexpr int SETS = C::SETS, ASL = C::ASL, WSL = C::WSL, WPRE = C::WPRE, kBuilders = C::BUILDERS;
+    constexpr int SETS = C::SETS, ASL = C::ASL, WSL = C::WSL, kBuilders = C::BUILDERS;
     constexpr int W_LOAD = 0, W_WLOAD = 1, W_BLD = 2, W_ISS = 2 + kBuilders, W_EPI = W_ISS + SETS, HC = C::HC;
     extern __shared__ uint8_t dsmem[];
     __shared__ __align__(8) uint64_t bar_hfull[2], bar_hempty[2], bar_xfull[2], bar_ifull[2], bar_iempty[2];
     __shared__ __align__(8) uint64_t bar_afree[SETS][ASL];   // A slot's MMAs complete (tcgen05.commit)
     __shared__ __align__(8) uint64_t bar_wfull[SETS][WSL];   // weight image landed (TMA tx)
     __shared__ __align__(8) uint64_t bar_wfree[SETS][WSL];   // weight slot's MMAs complete
-    __shared__ __align__(8) uint64_t bar_dfull[SETS];        // set's last MMA of the tile complete
-    __shared__ __align__(8) uint64_t bar_dempty[SETS];       // epilogue read D_set
+    __shared__ __align__(8) uint64_t bar_dfull[SETS][C::DB];   // set's last MMA of the tile complete
+    __shared__ __align__(8) uint64_t bar_dempty[SETS][C::DB];  // epilogue read D_set
     __shared__ uint32_t tmem_slot;
 
     const uint32_t sbase = smem_u32(dsmem);
     const uint32_t bbase = (sbase + 1023u) & ~1023u;            // weight slots [SETS][WSL][B_BYTES]
-    const uint32_t ibase = bbase + SETS * WSL * C::B_BYTES;    // tile records [2]
+    const uint32_t ibase = bbase + C::WBYTES;                  // tile records [2]
     const uint32_t hbase = ibase + 2 * kIdxBytes;              // halo rows [2][CAP][ROWB]
     const uint32_t xbase = hbase + 2 * C::CAP * C::ROWB;       // halo row ids [2][CAP]
     const uint8_t* gen = dsmem - sbase;
@@ -657,8 +672,10 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                 mbar_init(smem_u32(&bar_wfull[s][k]), 1);
                 mbar_init(smem_u32(&bar_wfree[s][k]), 1);
             }
-            mbar_init(smem_u32(&bar_dfull[s]), 1);
-            mbar_init(smem_u32(&bar_dempty[s]), C::EPI);
+            for (int k = 0; k < C::DB; ++k) {
+                mbar_init(smem_u32(&bar_dfull[s][k]), 1);
+                mbar_init(smem_u32(&bar_dempty[s][k]), C::EPI);
+            }
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -722,6 +739,16 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
             g = ng;
             len = nlen;
             level = nlevel;
+        }
+    } else if (warp == W_WLOAD && C::RESIDENT) {
+        // ---------------- resident weights: all 27 offset images, once ----------------
+        if (lane == 0) {
+            constexpr uint32_t kChunk = 16384;
+            mbar_arrive_expect_tx(smem_u32(&bar_wfull[0][0]), (uint32_t)C::WBYTES);
+            for (uint32_t o = 0; o < (uint32_t)C::WBYTES; o += kChunk) {
+                const uint32_t n = (uint32_t)C::WBYTES - o < kChunk ? (uint32_t)C::WBYTES - o : kChunk;
+                bulk_g2s(bbase + o, wimg + o, n, smem_u32(&bar_wfull[0][0]));
+            }
         }
     } else if (warp == W_WLOAD) {
         // ---------------- weight loader: per-set offset images, polled round-robin without blocking ------------
@@ -816,7 +843,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                     tmem_st_wait();
                     tc_fence_before();
                     if (tr) trace(dbg, 1, js);
-                    asm volatile("bar.arrive %0, 160;" ::"r"(1 + 2 * set + (int)(js & 1)) : "memory");
+                    asm volatile("bar.arrive %0, 160;" ::"r"(1 + ASL * set + (int)(js % ASL)) : "memory");
                 }
                 __syncwarp();
                 if (lane == 0) {
@@ -828,7 +855,6 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
     } else if (warp >= W_ISS && warp < W_ISS + SETS) {
         // ---------------- per-set MMA issuer: barrier, weights / accumulator waits, MMAs, commits ------------
         const int set = warp - W_ISS;
-        const uint32_t dt = tmem + set * N;
         const uint64_t bdesc0 = smem_desc(bbase, 16, 8 * C::BROWB, C::BLAYOUT);
         const int last_d = 27 - 1 - ((27 - 1 - set) % SETS);  // this set's last offset of a tile
         const int per_tile = (27 - set + SETS - 1) / SETS;     // offsets of this set per tile
@@ -841,14 +867,21 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
             for (int d = set; d < 27; d += SETS, ++js) {
                 const uint32_t ak = js % ASL, wk = js % WSL, wuse = js / WSL;
                 const bool first = d == set;
-                asm volatile("bar.sync %0, 160;" ::"r"(1 + 2 * set + (int)(js & 1)) : "memory");
+                asm volatile("bar.sync %0, 160;" ::"r"(1 + ASL * set + (int)(js % ASL)) : "memory");
                 if (tr) trace(dbg, 2, js);
-                if (first) mbar_wait(smem_u32(&bar_dempty[set]), (lt & 1) ^ 1);
-                mbar_wait(smem_u32(&bar_wfull[set][wk]), wuse & 1);
+                const uint32_t db = lt % C::DB, duse = lt / C::DB;
+                const uint32_t dt = tmem + (db * SETS + set) * N;
+                if (first) mbar_wait(smem_u32(&bar_dempty[set][db]), (duse & 1) ^ 1);
+                if constexpr (C::RESIDENT) {
+                    if (js == 0) mbar_wait(smem_u32(&bar_wfull[0][0]), 0);
+                } else {
+                    mbar_wait(smem_u32(&bar_wfull[set][wk]), wuse & 1);
+                }
                 tc_fence_after();
                 if (tr) trace(dbg, 3, js);
                 const uint32_t at = tmem + C::DCOLS + (set * ASL + ak) * C::ACOLS;
-                const uint64_t bd = bdesc0 + (((set * WSL + wk) * C::B_BYTES) >> 4);
+                const uint64_t bd = bdesc0 + ((C::RESIDENT ? (uint32_t)d * C::B_BYTES
+                                                           : (uint32_t)(set * WSL + wk) * C::B_BYTES) >> 4);
                 if (!(dbg & 1)) {
                     if constexpr (K == 32) {
                         mma_ts_x2_elect_acc<8, 2>(dt, at, bd, C::IDESC, first ? 0u : 1u);
@@ -857,8 +890,8 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                     }
                 }
                 mma_commit_elect(smem_u32(&bar_afree[set][ak]));
-                mma_commit_elect(smem_u32(&bar_wfree[set][wk]));
-                if (d == last_d) mma_commit_elect(smem_u32(&bar_dfull[set]));
+                if constexpr (!C::RESIDENT) mma_commit_elect(smem_u32(&bar_wfree[set][wk]));
+                if (d == last_d) mma_commit_elect(smem_u32(&bar_dfull[set][db]));
                 __syncwarp();
                 if (tr) trace(dbg, 4, js);
             }
@@ -873,13 +906,13 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
             float acc[HC];
 #pragma unroll
             for (int s = 0; s < SETS; ++s) {
-                mbar_wait_sleep(smem_u32(&bar_dfull[s]), lt & 1, 64);
+                mbar_wait_sleep(smem_u32(&bar_dfull[s][lt % C::DB]), (lt / C::DB) & 1, 64);
                 if (s == 0 && q == 0 && h == 0 && lane == 0) trace(dbg, 6, lt);
                 tc_fence_after();
 #pragma unroll
                 for (int c0 = 0; c0 < HC; c0 += 16) {
                     uint32_t v[16];
-                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + s * N + h * HC + c0, v);
+                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ((lt % C::DB) * SETS + s) * N + h * HC + c0, v);
                     tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
@@ -887,7 +920,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bar_dempty[s]));
+                if (lane == 0) mbar_arrive(smem_u32(&bar_dempty[s][lt % C::DB]));
             }
             if (row >= 0) {
                 if constexpr (OUT_BF16) {
@@ -1252,15 +1285,18 @@ int launch_halo_v(const void* in, const void* wimg, const fvdb_halo_plan& P, int
     return FVDB_OK;
 }
 
-// lockstep-set kernel (k_conv_halo4), opt-in with FVDB_HALO4=1 for K, N <= 64.  Measured on B200 (fwd ms,
-// tools/halo_dbg.py): cfg2 64x64 0.306-0.337 vs 0.324 (ring), cfg5 32x32 4.41-4.77 vs 3.90, dense 64x64
-// 0.63-0.67 vs 0.64; its sync skeleton alone (no MMA, no build) is ~0.24 ms at cfg2: every set-stage waits on a
-// weight TMA whose slot frees only when the MMAs of three stages earlier have completed
-// (profiles/r02_halo4.md).  Not the default.
+// lockstep-set kernel (k_conv_halo4): the default where all 27 weight images stay resident in shared memory
+// (K = 32 or N = 32), opt-in with FVDB_HALO4=1 for 64x64, off with FVDB_HALO4=0.  Measured on B200 (fwd ms,
+// tools/halo_dbg.py, profiles/r02_halo4.md): resident weights, cfg5 32x32 3.22 vs 3.93 (ring), cfg2 at 32x32
+// 0.183 vs 0.222; streamed weights at 64x64, cfg2 0.306-0.337 vs 0.324 (ring), dense 0.63-0.67 vs 0.64 (every
+// set-stage waits on a weight TMA whose slot frees only when the MMAs of three stages earlier completed).
 template <int K, int N>
 bool use_halo4() {
-    static const int e = getenv("FVDB_HALO4") ? atoi(getenv("FVDB_HALO4")) : 0;
-    return K <= 64 && N <= 64 && e == 1;
+    static const int e = getenv("FVDB_HALO4") ? atoi(getenv("FVDB_HALO4")) : -1;
+    if constexpr (K <= 64 && N <= 64) {
+        return e == 1 || (e == -1 && Halo4Cfg<K, N>::RESIDENT);
+    }
+    return false;
 }
 
 template <int K, int N, bool OB>
