@@ -955,6 +955,349 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
+// k_conv_halo2: CTA pairs (cta_group::2) with resident weights, K = N = 64
+//
+// At 64x64 the 27 weight images (216 KB) do not fit beside the halo, and streaming them is what bounds
+// k_conv_halo4 (profiles/r02_halo4.md).  A cluster of two CTAs issues M = 256 MMAs (tcgen05 cta_group::2): each
+// CTA holds its own 128-row tile's A stages in its TMEM and HALF of every weight image (output channels
+// 32r..32r+31, 4 KB per offset) in its shared memory, so all 27 offsets stay resident (108 KB per CTA) and are
+// loaded once.  The pair works on tiles 2p (rank 0) and 2p+1 (rank 1) in lockstep over offsets: SETS sets of four
+// builder warps per CTA as in k_conv_halo4; rank 0's per-set issuer waits for its own builders (named barrier)
+// and the peer's (remote mbarrier arrivals), issues the pair MMAs and commits to both CTAs' barriers
+// (multicast).  Each CTA's epilogue drains its own rows of D_set.
+// ---------------------------------------------------------------------------------------------
+#ifndef FVDB_H2_SETS
+#define FVDB_H2_SETS 2
+#endif
+#ifndef FVDB_H2_GROUPS
+#define FVDB_H2_GROUPS 2
+#endif
+struct Halo2Cfg {
+    // SETS accumulators, each fed by GROUPS builder groups (four warps, one per TMEM lane quarter) taking the
+    // set's stages in turn, through ASL A slots (one named barrier each)
+    static constexpr int K = 64, N = 64, SETS = FVDB_H2_SETS, GROUPS = FVDB_H2_GROUPS;
+    static constexpr int ASL = cmin(15 / SETS, (512 - SETS * N) / (SETS * (K / 2))) / GROUPS * GROUPS;
+    static constexpr int ROWB = 2 * K, CPR = K / 8, LJ = K / 32, NX = K / 16;
+    static constexpr int BROWB = 128;
+    static constexpr int HALF_B = (N / 2) * K * 2;          // this CTA's half of one offset image: 4 KB
+    static constexpr int ACOLS = K / 2;
+    static constexpr int DCOLS = SETS * N;
+    static constexpr int WBYTES = 27 * HALF_B;              // 108 KB resident
+    static constexpr int FIXED = 1024 + WBYTES + 2 * kIdxBytes;
+    static constexpr int CAP = ((kSmemMax - 2048 - FIXED) / (2 * (ROWB + 4))) & ~7;
+    static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4);
+    static constexpr uint32_t IDESC = idesc_bf16_f32(2 * kTileRows, N, false, false);  // M = 256 over the pair
+    static constexpr int BUILDERS = 4 * SETS * GROUPS, EPI = 8, HC = N / 2;
+    static constexpr int THREADS = (2 + BUILDERS + SETS + EPI) * 32;
+    static_assert(DCOLS + SETS * ASL * ACOLS <= 512, "TMEM");
+    static_assert(ASL >= 2 && ASL % GROUPS == 0 && SETS * ASL <= 15, "slots / named barriers");
+    static_assert(CAP >= 256, "halo capacity must hold one offset phase");
+};
+
+template <bool OUT_BF16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Halo2Cfg::THREADS, 1)
+    k_conv_halo2(const bf16* __restrict__ in, const uint8_t* __restrict__ wimg, fvdb_halo_plan P, int64_t n_out,
+                 void* __restrict__ out, int dbg) {
+    using C = Halo2Cfg;
+    constexpr int K = C::K, N = C::N, SETS = C::SETS, ASL = C::ASL, kBuilders = C::BUILDERS, HC = C::HC;
+    constexpr int W_LOAD = 0, W_W = 1, W_BLD = 2, W_ISS = 2 + kBuilders, W_EPI = W_ISS + SETS;
+    extern __shared__ uint8_t dsmem[];
+    __shared__ __align__(8) uint64_t bar_hfull[2], bar_hempty[2], bar_xfull[2], bar_ifull[2], bar_iempty[2];
+    __shared__ __align__(8) uint64_t bar_afree[SETS][ASL];  // pair MMAs of the slot complete (multicast commit)
+    __shared__ __align__(8) uint64_t bar_pfull[SETS][ASL];  // rank 0: the peer's builders finished the slot
+    __shared__ __align__(8) uint64_t bar_dfull[SETS];       // the set's last MMA of the tile pair complete
+    __shared__ __align__(8) uint64_t bar_dempty[SETS];      // rank 0: both CTAs' epilogues read D_set
+    __shared__ __align__(8) uint64_t bar_wres, bar_wpeer;   // own weight halves landed / (rank 0) the peer's
+    __shared__ uint32_t tmem_slot;
+
+    const uint32_t rank = cluster_ctarank();
+    const uint32_t sbase = smem_u32(dsmem);
+    const uint32_t bbase = (sbase + 1023u) & ~1023u;           // resident weight halves [27][HALF_B]
+    const uint32_t ibase = bbase + C::WBYTES;
+    const uint32_t hbase = ibase + 2 * kIdxBytes;
+    const uint32_t xbase = hbase + 2 * C::CAP * C::ROWB;
+    const uint8_t* gen = dsmem - sbase;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = P.num_tiles;
+    const int npairs = (T + 1) / 2;
+    const int cid = (int)(blockIdx.x >> 1), ncl = (int)(gridDim.x >> 1);
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&bar_hfull[b]), 32);
+            mbar_init(smem_u32(&bar_hempty[b]), kBuilders);
+            mbar_init(smem_u32(&bar_xfull[b]), 1);
+            mbar_init(smem_u32(&bar_ifull[b]), 1);
+            mbar_init(smem_u32(&bar_iempty[b]), kBuilders);
+        }
+        for (int s = 0; s < SETS; ++s) {
+            for (int k = 0; k < ASL; ++k) {
+                mbar_init(smem_u32(&bar_afree[s][k]), 1);
+                mbar_init(smem_u32(&bar_pfull[s][k]), 4);
+            }
+            mbar_init(smem_u32(&bar_dfull[s]), 1);
+            mbar_init(smem_u32(&bar_dempty[s]), 2 * C::EPI);
+        }
+        mbar_init(smem_u32(&bar_wres), 1);
+        mbar_init(smem_u32(&bar_wpeer), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == W_W) tmem_alloc2(smem_u32(&tmem_slot), 512);
+    tc_fence_before();
+    cluster_sync_all();  // barriers of both CTAs initialised before any remote arrival; TMEM allocated
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == W_LOAD) {
+        // ---------------- halo loader: this CTA's tile of every pair ----------------
+        int pi = cid, g = 0;
+        uint32_t pc = 0;
+        auto tile_of = [&](int q) { return 2 * q + (int)rank; };
+        auto issue_ids = [&](int t, int gg, uint32_t buf) {
+            int len = 0;
+            if (t < T) {
+                const int32_t* ph = P.phase + ((int64_t)t * 27 + gg) * 2;
+                len = ph[1];
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(smem_u32(&bar_xfull[buf]), (uint32_t)len * 4u);
+                    if (len > 0)
+                        bulk_g2s(xbase + buf * C::CAP * 4, P.halo_rows + P.tile_base[t] + ph[0], (uint32_t)len * 4u,
+                                 smem_u32(&bar_xfull[buf]));
+                }
+            } else if (lane == 0) {
+                mbar_arrive(smem_u32(&bar_xfull[buf]));
+            }
+            return len;
+        };
+        int len = pi < npairs ? issue_ids(tile_of(pi), 0, 0) : 0;
+        int level = pi < npairs && tile_of(pi) < T ? P.tile_level[tile_of(pi)] : 1;
+        while (pi < npairs) {
+            const int tile = tile_of(pi);
+            int ng = g + 1, np = pi;
+            if (ng >= level) { ng = 0; np = pi + ncl; }
+            const int nt = tile_of(np);
+            const int nlevel = ng == 0 ? (np < npairs && nt < T ? P.tile_level[nt] : 1) : level;
+            const uint32_t buf = pc & 1, par = (pc >> 1) & 1;
+            const int nlen = np < npairs ? issue_ids(nt, ng, buf ^ 1) : 0;
+            mbar_wait(smem_u32(&bar_xfull[buf]), par);
+            mbar_wait(smem_u32(&bar_hempty[buf]), par ^ 1);
+            const int32_t* ids = reinterpret_cast<const int32_t*>(gen + xbase + buf * C::CAP * 4);
+            const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
+            constexpr int RPI = 32 / C::CPR;
+            const int q = lane / C::CPR, c = lane % C::CPR;
+            for (int s0 = 0; s0 < len; s0 += 4 * RPI) {
+                int r[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int sl = s0 + k * RPI + q;
+                    r[k] = sl < len ? ids[sl] : -1;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int sl = s0 + k * RPI + q;
+                    if (r[k] >= 0) cp_async_16(hb + sl * C::ROWB + (halo_phys(K, sl, c) << 4), in + (int64_t)r[k] * K + c * 8, 16u);
+                }
+            }
+            cp_async_arrive_noinc(smem_u32(&bar_hfull[buf]));
+            if (lane == 0) {
+                mbar_wait(smem_u32(&bar_iempty[buf]), par ^ 1);
+                if (tile < T) {
+                    mbar_arrive_expect_tx(smem_u32(&bar_ifull[buf]), (uint32_t)kRecBytes);
+                    bulk_g2s(ibase + buf * kIdxBytes, P.tile_rec + (int64_t)tile * kIdxBytes, (uint32_t)kRecBytes,
+                             smem_u32(&bar_ifull[buf]));
+                } else {
+                    mbar_arrive(smem_u32(&bar_ifull[buf]));
+                }
+            }
+            __syncwarp();
+            ++pc;
+            pi = np;
+            g = ng;
+            len = nlen;
+            level = nlevel;
+        }
+    } else if (warp == W_W) {
+        // ---------------- resident weights: this CTA's half of all 27 offset images, once ----------------
+        if (lane == 0) {
+            mbar_arrive_expect_tx(smem_u32(&bar_wres), (uint32_t)C::WBYTES);
+            for (int d = 0; d < 27; ++d)
+                bulk_g2s(bbase + d * C::HALF_B, wimg + (size_t)d * (2 * C::HALF_B) + rank * C::HALF_B, C::HALF_B,
+                         smem_u32(&bar_wres));
+            if (rank == 1) {  // tell the issuing CTA
+                mbar_wait(smem_u32(&bar_wres), 0);
+                mbar_arrive_remote(mapa_shared(smem_u32(&bar_wpeer), 0));
+            }
+        }
+    } else if (warp >= W_BLD && warp < W_BLD + kBuilders) {
+        // ---------------- builders (both CTAs) ----------------
+        const int set = (warp - W_BLD) / (4 * C::GROUPS);
+        const int grp = ((warp - W_BLD) / 4) % C::GROUPS;  // builds the set's stages js with js % GROUPS == grp
+        const int q = warp & 3;
+        const int t0 = lane & 3, t1 = lane >> 2;
+        const int lrow = q * 32 + t1;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        uint32_t pc = 0, js = 0;
+        for (int pi = cid; pi < npairs; pi += ncl) {
+            const int tile = 2 * pi + (int)rank;
+            const bool valid = tile < T;
+            const int level = valid ? P.tile_level[tile] : 1, gs = 27 / level;
+            for (int g = 0; g < level; ++g, ++pc) {
+                const uint32_t buf = pc & 1, par = (pc >> 1) & 1;
+                mbar_wait(smem_u32(&bar_hfull[buf]), par);
+                mbar_wait(smem_u32(&bar_ifull[buf]), par);
+                const uint16_t* lb = reinterpret_cast<const uint16_t*>(gen + ibase + buf * kIdxBytes);
+                const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
+                const int d_end = (g + 1) * gs;
+                int d = g * gs;
+                d += (set - d % SETS + SETS) % SETS;
+                for (; d < d_end; d += SETS, ++js) {
+                    if ((int)(js % C::GROUPS) != grp) continue;
+                    const uint32_t ak = js % ASL, ause = js / ASL;
+                    const bool tr = (dbg & 64) && blockIdx.x < 2 && set == 0 && q == 2 && lane == 0 && js < (uint32_t)kTraceN;
+                    if (tr && rank == 0) g_halo_trace[7][js] = clock64();
+                    mbar_wait_cluster(smem_u32(&bar_afree[set][ak]), (ause & 1) ^ 1);
+                    if (tr && rank == 0) g_halo_trace[0][js] = clock64();
+                    tc_fence_after();
+                    if (valid && !(dbg & 2)) {
+                        const uint16_t* lr = lb + d * kTileRows + lrow;
+                        const int sl[4] = {lr[0], lr[8], lr[16], lr[24]};
+                        const uint32_t acol = tmem + lane_off + C::DCOLS + (set * ASL + ak) * C::ACOLS;
+                        uint32_t v[2][4 * C::NX];
+#pragma unroll
+                        for (int gg = 0; gg < 2; ++gg) {
+#pragma unroll
+                            for (int hi = 0; hi < 2; ++hi) {
+                                const int sv = sl[2 * gg + hi];
+                                const bool has = sv != kNoSlot;
+                                const uint32_t rb = hb + sv * C::ROWB;
+                                const int pr = sv & 1;
+#pragma unroll
+                                for (int j = 0; j < C::LJ; ++j) {
+                                    const uint4 w = lds128_pred(rb + (halo_phys(K, pr, halo_chunk(K, t0, j)) << 4), has);
+                                    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const int i = 4 * j + e;
+                                        v[gg][4 * (i >> 1) + (i & 1) + 2 * hi] = ww[e];
+                                    }
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int gg = 0; gg < 2; ++gg) tmem_st16x256<C::NX>(acol + ((uint32_t)(gg * 16) << 16), v[gg]);
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    if (tr) g_halo_trace[rank == 0 ? 1 : 5][js] = clock64();
+                    if (rank == 0) {
+                        asm volatile("bar.arrive %0, 160;" ::"r"(1 + ASL * set + (int)ak) : "memory");
+                    } else {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&bar_pfull[set][ak]), 0));
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(smem_u32(&bar_hempty[buf]));
+                    mbar_arrive(smem_u32(&bar_iempty[buf]));
+                }
+            }
+        }
+    } else if (warp >= W_ISS && warp < W_ISS + SETS) {
+        // ---------------- rank 0: per-set pair-MMA issuer ----------------
+        if (rank == 0) {
+            const int set = warp - W_ISS;
+            const uint32_t dt = tmem + set * N;
+            const uint64_t bdesc0 = smem_desc(bbase, 16, 8 * C::BROWB, kSwizzle128B);
+            const int last_d = 27 - 1 - ((27 - 1 - set) % SETS);
+            uint32_t js = 0, lt = 0;
+            for (int pi = cid; pi < npairs; pi += ncl, ++lt) {
+                for (int d = set; d < 27; d += SETS, ++js) {
+                    const uint32_t ak = js % ASL, ause = js / ASL;
+                    const bool first = d == set;
+                    const bool tr = (dbg & 64) && blockIdx.x == 0 && set == 0 && lane == 0 && js < (uint32_t)kTraceN;
+                    asm volatile("bar.sync %0, 160;" ::"r"(1 + ASL * set + (int)ak) : "memory");
+                    if (tr) g_halo_trace[2][js] = clock64();
+                    mbar_wait_cluster(smem_u32(&bar_pfull[set][ak]), ause & 1);
+                    if (tr) g_halo_trace[3][js] = clock64();
+                    if (js == 0) {
+                        mbar_wait(smem_u32(&bar_wres), 0);
+                        mbar_wait_cluster(smem_u32(&bar_wpeer), 0);
+                    }
+                    if (first) mbar_wait_cluster(smem_u32(&bar_dempty[set]), (lt & 1) ^ 1);
+                    if (tr) g_halo_trace[6][js] = clock64();
+                    tc_fence_after();
+                    const uint32_t at = tmem + C::DCOLS + (set * ASL + ak) * C::ACOLS;
+                    const uint64_t bd = bdesc0 + (((uint32_t)d * C::HALF_B) >> 4);
+                    if (!(dbg & 1)) mma2_ts_x4_elect_acc<8, 16, 24, 2, 4, 6>(dt, at, bd, C::IDESC, first ? 0u : 1u);
+                    mma2_commit_mc_elect(smem_u32(&bar_afree[set][ak]), (uint16_t)3);
+                    if (d == last_d) mma2_commit_mc_elect(smem_u32(&bar_dfull[set]), (uint16_t)3);
+                    __syncwarp();
+                    if (tr) g_halo_trace[4][js] = clock64();
+                }
+            }
+        }
+    } else if (warp >= W_EPI && warp < W_EPI + C::EPI) {
+        // ---------------- epilogue (both CTAs): this CTA's 128 rows of D_0 + ... + D_3 ----------------
+        const int q = warp & 3, h = (warp - W_EPI) / 4;
+        uint32_t lt = 0;
+        for (int pi = cid; pi < npairs; pi += ncl, ++lt) {
+            const int tile = 2 * pi + (int)rank;
+            const int64_t row = tile < T ? P.perm[(int64_t)tile * kTileRows + q * 32 + lane] : -1;
+            float acc[HC];
+#pragma unroll
+            for (int s = 0; s < SETS; ++s) {
+                mbar_wait_cluster_sleep(smem_u32(&bar_dfull[s]), lt & 1, 64);
+                tc_fence_after();
+#pragma unroll
+                for (int c0 = 0; c0 < HC; c0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + s * N + h * HC + c0, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        acc[c0 + j] = s == 0 ? __uint_as_float(v[j]) : acc[c0 + j] + __uint_as_float(v[j]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (rank == 0) mbar_arrive(smem_u32(&bar_dempty[s]));
+                    else mbar_arrive_remote(mapa_shared(smem_u32(&bar_dempty[s]), 0));
+                }
+            }
+            if (row >= 0) {
+                if constexpr (OUT_BF16) {
+                    uint8_t* dst = reinterpret_cast<uint8_t*>(reinterpret_cast<bf16*>(out) + row * N + h * HC);
+#pragma unroll
+                    for (int c0 = 0; c0 < HC; c0 += 16) {
+                        uint32_t pk[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[c0 + 2 * e], acc[c0 + 2 * e + 1]);
+                            pk[e] = *reinterpret_cast<uint32_t*>(&b2);
+                        }
+                        stg256(dst + 2 * c0, pk[0], pk[1], pk[2], pk[3], pk[4], pk[5], pk[6], pk[7]);
+                    }
+                } else {
+                    uint8_t* dst = reinterpret_cast<uint8_t*>(reinterpret_cast<float*>(out) + row * N + h * HC);
+#pragma unroll
+                    for (int c0 = 0; c0 < HC; c0 += 8)
+                        stg256(dst + 4 * c0, __float_as_uint(acc[c0]), __float_as_uint(acc[c0 + 1]),
+                               __float_as_uint(acc[c0 + 2]), __float_as_uint(acc[c0 + 3]), __float_as_uint(acc[c0 + 4]),
+                               __float_as_uint(acc[c0 + 5]), __float_as_uint(acc[c0 + 6]), __float_as_uint(acc[c0 + 7]));
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // both CTAs done with TMEM (all pair MMAs committed, all epilogues drained)
+    if (warp == W_W) {
+        tc_fence_after();
+        tmem_dealloc2(tmem, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // halo plan
 // ---------------------------------------------------------------------------------------------
 constexpr int kPlanThreads = 256;
@@ -1318,8 +1661,36 @@ int launch_halo4(const void* in, const void* wimg, const fvdb_halo_plan& P, int6
     }
 }
 
+// CTA-pair kernel (k_conv_halo2) for 64x64, opt-in with FVDB_HALO2=1.  Correct, but slower than the ring kernel
+// on B200 (cfg2 fwd ms, tools/halo_dbg.py): 4 sets x 2 slots 0.480, 2 sets x 2 groups x 6 slots 0.463 (ring
+// 0.324); its sync skeleton alone (no MMA, no build) takes 0.367: every stage costs the issuing warp a named
+// barrier, a cluster-scope wait for the peer's remote arrivals and two multicast commits (~900 cycles serial).
+// profiles/r02_halo4.md.
+template <int K, int N>
+bool use_halo2() {
+    static const int e = getenv("FVDB_HALO2") ? atoi(getenv("FVDB_HALO2")) : 0;
+    return K == 64 && N == 64 && e == 1;
+}
+
+template <bool OB>
+int launch_halo2(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out,
+                 cudaStream_t st) {
+    using C = Halo2Cfg;
+    if (P.halo_cap > C::CAP) return FVDB_ERR_INVALID;
+    auto kern = k_conv_halo2<OB>;
+    FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    int grid = sm_count_h() & ~1;
+    const int pairs = (P.num_tiles + 1) / 2;
+    if (grid > 2 * pairs) grid = 2 * pairs;
+    static const int dbg = getenv("FVDB_DEBUG_HALO") ? atoi(getenv("FVDB_DEBUG_HALO")) : 0;
+    kern<<<grid, C::THREADS, C::SMEM, st>>>((const bf16*)in, (const uint8_t*)wimg, P, n_out, out, dbg);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
 template <int K, int N>
 int halo_kernel_cap() {
+    if (use_halo2<K, N>()) return Halo2Cfg::CAP;
     if constexpr (K <= 64 && N <= 64) {
         if (use_halo4<K, N>()) return Halo4Cfg<K, N>::CAP;
     }
@@ -1328,6 +1699,7 @@ int halo_kernel_cap() {
 
 template <int K, int N, bool OB>
 int launch_halo(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out, cudaStream_t st) {
+    if (use_halo2<K, N>()) return launch_halo2<OB>(in, wimg, P, n_out, out, st);
     if (use_halo4<K, N>()) return launch_halo4<K, N, OB>(in, wimg, P, n_out, out, st);
     if (halo_variant<K, N>() == 1) return launch_halo_v<K, N, OB, 1>(in, wimg, P, n_out, out, st);
     return launch_halo_v<K, N, OB, 0>(in, wimg, P, n_out, out, st);

@@ -339,6 +339,81 @@ __device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// ---- CTA pairs (cluster of 2, tcgen05 cta_group::2) ----
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `saddr` (a shared::cta address) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t n = 0;
+    while (!mbar_try_wait_cluster(bar, parity)) {
+        if (++n == (1u << 24)) asm volatile("trap;");
+    }
+}
+__device__ __forceinline__ void mbar_wait_cluster_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
+    uint32_t n = 0;
+    while (!mbar_try_wait_cluster(bar, parity)) {
+        __nanosleep(ns);
+        if (++n == (1u << 22)) asm volatile("trap;");
+    }
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t slot_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot_smem), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// four M256 x N x K16 MMAs of a CTA pair (A in both CTAs' TMEM, B halves in both CTAs' smem), one elected lane
+template <int A1, int A2, int A3, int B1, int B2, int B3>
+__device__ __forceinline__ void mma2_ts_x4_elect_acc(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, q;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+        "setp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t"
+        "add.u32 a1, %1, %4;\n\tadd.u32 a2, %1, %5;\n\tadd.u32 a3, %1, %6;\n\t"
+        "add.u64 b1, %2, %7;\n\tadd.u64 b2, %2, %8;\n\tadd.u64 b3, %2, %9;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], b3, %3, p;\n\t}"
+        ::"r"(d), "r"(a), "l"(b), "r"(idesc), "n"(A1), "n"(A2), "n"(A3), "n"(B1), "n"(B2), "n"(B3), "r"(acc0)
+        : "memory");
+}
+// arrive on `bar` (same shared offset) in every CTA of `mask` when this thread's prior pair MMAs complete
+__device__ __forceinline__ void mma2_commit_mc_elect(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+        ::"r"(bar), "h"(mask)
+        : "memory");
+}
+
 // ---- descriptors ----
 enum : uint32_t { kSwizzleNone = 0, kSwizzle128B = 2, kSwizzle64B = 4, kSwizzle32B = 6 };
 
