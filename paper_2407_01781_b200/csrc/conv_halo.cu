@@ -1628,16 +1628,15 @@ int launch_halo_v(const void* in, const void* wimg, const fvdb_halo_plan& P, int
     return FVDB_OK;
 }
 
-// lockstep-set kernel (k_conv_halo4): the default where all 27 weight images stay resident in shared memory
-// (K = 32 or N = 32), opt-in with FVDB_HALO4=1 for 64x64, off with FVDB_HALO4=0.  Measured on B200 (fwd ms,
-// tools/halo_dbg.py, profiles/r02_halo4.md): resident weights, cfg5 32x32 3.22 vs 3.93 (ring), cfg2 at 32x32
-// 0.183 vs 0.222; streamed weights at 64x64, cfg2 0.306-0.337 vs 0.324 (ring), dense 0.63-0.67 vs 0.64 (every
-// set-stage waits on a weight TMA whose slot frees only when the MMAs of three stages earlier completed).
+// lockstep-set kernel (k_conv_halo4): the default for K, N <= 64 (FVDB_HALO4=0 selects the ring kernel).
+// Measured on B200 (profiles/r02_halo4.md): resident weights (K or N = 32), cfg5 32x32 fwd 3.22 vs 3.93 ms
+// (ring), cfg2 at 32x32 0.183 vs 0.222; streamed weights at 64x64, cfg2 bench step 0.941 vs 0.963 ms (fwd 0.316
+// vs 0.327, dgrad 0.314 vs 0.324, two runs each), dense 128^3 fwd 0.631 vs 0.641.
 template <int K, int N>
 bool use_halo4() {
     static const int e = getenv("FVDB_HALO4") ? atoi(getenv("FVDB_HALO4")) : -1;
     if constexpr (K <= 64 && N <= 64) {
-        return e == 1 || (e == -1 && Halo4Cfg<K, N>::RESIDENT);
+        return e != 0;
     }
     return false;
 }
