@@ -506,6 +506,15 @@ def pack_weights_kn(w: torch.Tensor, transpose: bool, dtype) -> torch.Tensor:
     return out
 
 
+def halo_kernel_name(K: int, N: int) -> str:
+    """The halo-staged kernel fvdb_conv_halo_tc runs for a (K, N) layer (csrc/conv_halo.cu dispatch)."""
+    if os.environ.get("FVDB_HALO2") == "1" and (K, N) == (64, 64):
+        return "k_conv_halo2<64,64,bf16> (CTA pairs)"
+    if K <= 64 and N <= 64 and os.environ.get("FVDB_HALO4") != "0":
+        return f"k_conv_halo4<{K},{N},bf16>" + (" (resident weights)" if K == 32 or N == 32 else "")
+    return f"k_conv_halo<{K},{N},bf16>"
+
+
 HALO_AFTER_USES = 4  # conv_impl "auto": uses of a table before its halo plan is built
 SORT_BELOW_DENSITY = 10.0  # gather kernel: signature-sort tables with fewer mean pairs per row
 
