@@ -597,9 +597,12 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
 #ifndef FVDB_H4_DB
 #define FVDB_H4_DB 1
 #endif
+#ifndef FVDB_H4_SETS
+#define FVDB_H4_SETS 4
+#endif
 template <int K, int N>
 struct Halo4Cfg {
-    static constexpr int SETS = 4;
+    static constexpr int SETS = FVDB_H4_SETS;
     static constexpr int ROWB = 2 * K, CPR = K / 8, LJ = K / 32, NX = K / 16;
     static constexpr int KB = K >= 64 ? 64 : K;
     static constexpr int BROWB = KB * 2;
@@ -613,7 +616,7 @@ struct Halo4Cfg {
     // A slots per set, one named barrier per slot (a builder is then at most ASL - 1 stages ahead of its issuer,
     // which the barrier ring requires); SETS * ASL <= 15 hardware barriers besides barrier 0
     static constexpr int ASL = cmin(FVDB_H4_ASL, (512 - DCOLS) / (SETS * ACOLS));
-    static constexpr int WSL = 3;   // weight slots per set (the weight-loader warp fills them ahead)
+    static constexpr int WSL = ASL + 1;  // weight slots per set (stage j + 1 loads while stage j builds)
     static constexpr int WPRE = 1;
     // all 27 offset images resident in shared memory (loaded once per CTA) when they fit beside the halo:
     // no weight hand-off at all (K = 32 or N = 32: 54-108 KB)
@@ -629,6 +632,7 @@ struct Halo4Cfg {
     // halo loader, weight loader, builders, one MMA issuer per set, epilogue
     static constexpr int THREADS = (2 + BUILDERS + SETS + EPI) * 32;
     static_assert(ASL >= 2 && SETS * ASL <= 15, "two A slots per set at least; named barriers");
+    static_assert(RESIDENT || WSL == ASL + 1, "streamed weights: stage j's A-slot wait frees stage j + 1's image slot");
     static_assert(CAP >= 256, "halo capacity must hold one offset phase");
     static_assert(DCOLS + SETS * ASL * ACOLS <= 512, "TMEM");
 };
@@ -750,38 +754,6 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                 bulk_g2s(bbase + o, wimg + o, n, smem_u32(&bar_wfull[0][0]));
             }
         }
-    } else if (warp == W_WLOAD) {
-        // ---------------- weight loader: per-set offset images, polled round-robin without blocking ------------
-        // set s's stage j takes offset s + SETS * (j % per_tile(s)) into slot j % WSL once stage j - WSL's MMAs
-        // are done; a set whose slot is still busy does not hold up the others
-        if (lane == 0) {
-            const int ntiles = blockIdx.x < T ? (T - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-            uint32_t next[SETS], total[SETS], per[SETS];
-            uint32_t left = 0;
-#pragma unroll
-            for (int s = 0; s < SETS; ++s) {
-                per[s] = (uint32_t)((27 - s + SETS - 1) / SETS);
-                total[s] = per[s] * (uint32_t)ntiles;
-                next[s] = 0;
-                left += total[s];
-            }
-            while (left) {
-#pragma unroll
-                for (int s = 0; s < SETS; ++s) {
-                    const uint32_t j = next[s];
-                    if (j >= total[s]) continue;
-                    const uint32_t k = j % WSL, use = j / WSL;
-                    if (!mbar_test(smem_u32(&bar_wfree[s][k]), (use & 1) ^ 1)) continue;
-                    if (s == 0) trace(dbg, 5, j);
-                    const int d = s + SETS * (int)(j % per[s]);
-                    mbar_arrive_expect_tx(smem_u32(&bar_wfull[s][k]), C::B_BYTES);
-                    bulk_g2s(bbase + (s * WSL + k) * C::B_BYTES, wimg + (size_t)d * C::B_BYTES, C::B_BYTES,
-                             smem_u32(&bar_wfull[s][k]));
-                    next[s] = j + 1;
-                    --left;
-                }
-            }
-        }
     } else if (warp >= W_BLD && warp < W_BLD + kBuilders) {
         // ---------------- builders: A stage from the staged halo into the set's TMEM slot -----------------------
         // Per stage: wait the slot's previous MMAs, build, wait::st + fence, arrive on the set's named barrier
@@ -792,6 +764,22 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
         const int lrow = q * 32 + t1;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const bool tr = set == 0 && q == 2 && lane == 0;
+        // streamed weights: the set's first builder warp loads stage j + 1's image into slot (j + 1) % WSL right
+        // after its A-slot wait for stage j, which proved stage j - 2's MMAs (that slot's previous user) complete
+        const bool wl = !C::RESIDENT && ((warp - W_BLD) & 3) == 0 && lane == 0;
+        const int per_tile = (27 - set + SETS - 1) / SETS;
+        const int ntiles_b = blockIdx.x < T ? (T - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+        const uint32_t total = (uint32_t)(per_tile * ntiles_b);
+        auto load_w = [&](uint32_t j) {
+            if (j < total) {
+                const uint32_t k = j % WSL;
+                const int dd = set + SETS * (int)(j % (uint32_t)per_tile);
+                mbar_arrive_expect_tx(smem_u32(&bar_wfull[set][k]), C::B_BYTES);
+                bulk_g2s(bbase + (set * WSL + k) * C::B_BYTES, wimg + (size_t)dd * C::B_BYTES, C::B_BYTES,
+                         smem_u32(&bar_wfull[set][k]));
+            }
+        };
+        if (wl) load_w(0);
         uint32_t pc = 0, js = 0;
         for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
             const int level = P.tile_level[tile], gs = 27 / level;
@@ -812,6 +800,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                     const uint16_t* lr = lb + d * kTileRows + lrow;
                     const int sl[4] = {lr[0], lr[8], lr[16], lr[24]};
                     mbar_wait(smem_u32(&bar_afree[set][ak]), (ause & 1) ^ 1);
+                    if (wl) load_w(js + 1);
                     tc_fence_after();
                     if (tr) trace(dbg, 0, js);
                     if (!(dbg & 2)) {
@@ -890,7 +879,6 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                     }
                 }
                 mma_commit_elect(smem_u32(&bar_afree[set][ak]));
-                if constexpr (!C::RESIDENT) mma_commit_elect(smem_u32(&bar_wfree[set][wk]));
                 if (d == last_d) mma_commit_elect(smem_u32(&bar_dfull[set][db]));
                 __syncwarp();
                 if (tr) trace(dbg, 4, js);

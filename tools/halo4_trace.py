@@ -39,6 +39,11 @@ out["issuer_waits"] = d(3, 2)
 out["issuer_issue_commit"] = d(4, 3)
 out["issuer_period"] = float(np.median(np.diff(t[2, lo:hi])))
 out["wload_issue_minus_stage_start"] = d(5, 7)
+out["tma_issue_to_issuer_past_waits"] = d(3, 5)
+out["loader_poll_start_to_issue"] = d(5, 11)
+out["commit_j-3_to_poll_start_j"] = float(np.median(t[11, lo + 3:hi + 3] - t[4, lo:hi]))
+out["commit_j_to_builder_afree_j+2"] = float(np.median(t[0, lo + 2:hi + 2] - t[4, lo:hi]))
+out["commit_j-3_to_tma_issue_j"] = float(np.median(t[5, lo + 3:hi + 3] - t[4, lo:hi]))
 ph = t[9, 5:60]
 out["phase_wait"] = float(np.median(t[10, 5:60] - t[9, 5:60]))
 out["epi_tile_period"] = float(np.median(np.diff(t[6, 5:60])))
