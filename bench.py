@@ -226,7 +226,7 @@ def setup_problem(args, cfg, rank, world, dev, torch, P):
         costs = [int((kfull.fwd.t[:, s:e] >= 0).sum().item()) for s, e in full.voxel_joffsets.tolist()]
         s, e = D.partition_by_cost(costs, world)[rank]
         del full, kfull
-        jag = P.jagged_from_list([torch.from_numpy(p) for p in pts[s:e]])
+        jag = P.jagged_from_list([torch.from_numpy(p).to(dev) for p in pts[s:e]])  # points resident, as cfg2's coords
         batch, dv, wl = stage(torch, lambda: P.build_from_points(jag, tf)[0], reps=3)
         stages["grid_build"] = dict(device_ms=dv, wall_ms=wl, inputs=int(jag.jdata.shape[0]), grids=e - s,
                                     batched=True)

@@ -140,10 +140,16 @@ def load_library(require_cuda: bool = True):
     return h
 
 
+_CUDA_OK = False
+
+
 def lib():
     """The library handle for a compute call: requires a CUDA device (no CPU fallback)."""
-    if not torch.cuda.is_available():
-        raise FvdbError("paper_2407_01781_b200 needs a CUDA (sm_100a) device; there is no CPU fallback")
+    global _CUDA_OK
+    if not _CUDA_OK:  # checked until it first succeeds (a device does not disappear from a process)
+        if not torch.cuda.is_available():
+            raise FvdbError("paper_2407_01781_b200 needs a CUDA (sm_100a) device; there is no CPU fallback")
+        _CUDA_OK = True
     return load_library()
 
 

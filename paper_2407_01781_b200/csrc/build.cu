@@ -35,7 +35,86 @@ struct BuildScalars {
     long long n_tiles;
     int n_unique;
     int pad;
+    // per axis, the 21-bit tile fields of non-negative (lo: < 2^20) and negative (hi) coordinates: min / max,
+    // for an order-preserving compression of the tile keys before sorting (TileCompress)
+    unsigned int lo_min[3], lo_max[3], hi_min[3], hi_max[3];
 };
+
+// Order-preserving compression of 63-bit tile keys (three 21-bit fields, compared unsigned as the reference's
+// uint64 sort does, build.py:111-124): per axis, fields of non-negative coordinates map to [0, ra) and fields of
+// negative ones (>= 2^20 unsigned) to [ra, ra + rb).  A scene that straddles an axis (LiDAR around its sensor)
+// has tile keys differing in ~60 bits but compresses to a few bits: one or two radix passes instead of eight.
+struct TileCompress {
+    unsigned int lo_min[3], hi_min[3], ra[3], w[3];
+    int total;
+    __host__ __device__ uint64_t field(uint64_t key, int a) const { return (key >> (42 - 21 * a)) & 0x1FFFFF; }
+    __host__ __device__ uint64_t enc(uint64_t key) const {
+        uint64_t c = 0;
+        for (int a = 0; a < 3; ++a) {
+            const uint64_t f = field(key, a);
+            const uint64_t v = f < (1u << 20) ? f - lo_min[a] : ra[a] + (f - hi_min[a]);
+            c = (c << w[a]) | v;
+        }
+        return c;
+    }
+    __host__ __device__ uint64_t dec(uint64_t c) const {
+        uint64_t key = 0;
+        int sh = 0;
+        for (int a = 2; a >= 0; --a) {
+            const uint64_t v = w[a] ? (c >> sh) & ((1ull << w[a]) - 1ull) : 0;
+            sh += w[a];
+            const uint64_t f = v < ra[a] ? lo_min[a] + v : hi_min[a] + (v - ra[a]);
+            key |= f << (42 - 21 * a);
+        }
+        return key;
+    }
+};
+
+inline int bits_for(uint64_t n) { return n <= 1 ? 0 : 64 - __builtin_clzll(n - 1); }
+
+// host: compression parameters from the first read-back's field ranges; false when they need > 63 bits
+inline bool make_compress(const BuildScalars& hs, TileCompress* tc) {
+    int total = 0;
+    for (int a = 0; a < 3; ++a) {
+        const bool has_lo = hs.lo_min[a] <= hs.lo_max[a], has_hi = hs.hi_min[a] <= hs.hi_max[a];
+        tc->lo_min[a] = has_lo ? hs.lo_min[a] : 0;
+        tc->hi_min[a] = has_hi ? hs.hi_min[a] : 0;
+        tc->ra[a] = has_lo ? hs.lo_max[a] - hs.lo_min[a] + 1 : 0;
+        const uint64_t rb = has_hi ? hs.hi_max[a] - hs.hi_min[a] + 1 : 0;
+        tc->w[a] = (unsigned)bits_for((uint64_t)tc->ra[a] + rb);
+        total += (int)tc->w[a];
+    }
+    tc->total = total;
+    return total <= 63;
+}
+
+__global__ void k_compress_keys(const uint64_t* __restrict__ tk, int64_t n, TileCompress tc, uint64_t* __restrict__ ck) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        ck[r] = tc.enc(tk[r]);
+}
+
+__global__ void k_decompress_keys(uint64_t* __restrict__ keys, const int* __restrict__ n_sel, TileCompress tc) {
+    const int n = *n_sel;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) keys[r] = tc.dec(keys[r]);
+}
+
+// per-warp min / max of the lo / hi tile fields of one axis, folded into the scalars
+__device__ __forceinline__ void fold_fields(BuildScalars* sc, const uint32_t (&f)[3], bool valid) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const bool lo = valid && f[a] < (1u << 20), hi = valid && f[a] >= (1u << 20);
+        const uint32_t lmin = __reduce_min_sync(0xffffffffu, lo ? f[a] : 0xFFFFFFFFu);
+        const uint32_t lmax = __reduce_max_sync(0xffffffffu, lo ? f[a] : 0u);
+        const uint32_t hmin = __reduce_min_sync(0xffffffffu, hi ? f[a] : 0xFFFFFFFFu);
+        const uint32_t hmax = __reduce_max_sync(0xffffffffu, hi ? f[a] : 0u);
+        if ((threadIdx.x & 31) == 0) {
+            if (lmin != 0xFFFFFFFFu) atomicMin(&sc->lo_min[a], lmin);
+            if (lmax) atomicMax(&sc->lo_max[a], lmax);
+            if (hmin != 0xFFFFFFFFu) atomicMin(&sc->hi_min[a], hmin);
+            if (hmax) atomicMax(&sc->hi_max[a], hmax);
+        }
+    }
+}
 
 struct BuildWs {
     uint64_t *tk, *tk_alt, *vk, *vk_alt, *tiles, *uvox;
@@ -89,6 +168,10 @@ __global__ void k_init_scalars(BuildScalars* s) {
     s->key_and = ~0ull;
     s->n_tiles = 0;
     s->n_unique = 0;
+    for (int a = 0; a < 3; ++a) {
+        s->lo_min[a] = s->hi_min[a] = 0xFFFFFFFFu;
+        s->lo_max[a] = s->hi_max[a] = 0u;
+    }
 }
 
 // tile keys + range check + OR/AND reduction (build.py:96-101, topology.py:83-88)
@@ -96,15 +179,23 @@ __global__ void k_tile_keys(const int64_t* __restrict__ coords, int64_t n, uint6
                             BuildScalars* sc) {
     uint64_t k_or = 0, k_and = ~0ull;
     const int64_t lim = (int64_t)1 << 30;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
-        bool bad = (i > lim) | (i < -lim) | (j > lim) | (j < -lim) | (k > lim) | (k < -lim);
-        if (bad) atomicMin(&sc->bad_row, (unsigned long long)r);
-        uint64_t key = tile_key(i, j, k);
-        tk[r] = key;
-        k_or |= key;
-        k_and &= key;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x; r0 < n; r0 += stride) {  // warp-uniform trip count
+        const int64_t r = r0 + threadIdx.x;
+        uint32_t f[3] = {0u, 0u, 0u};
+        if (r < n) {
+            int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
+            bool bad = (i > lim) | (i < -lim) | (j > lim) | (j < -lim) | (k > lim) | (k < -lim);
+            if (bad) atomicMin(&sc->bad_row, (unsigned long long)r);
+            uint64_t key = tile_key(i, j, k);
+            tk[r] = key;
+            k_or |= key;
+            k_and &= key;
+            f[0] = (uint32_t)((key >> 42) & 0x1FFFFF);
+            f[1] = (uint32_t)((key >> 21) & 0x1FFFFF);
+            f[2] = (uint32_t)(key & 0x1FFFFF);
+        }
+        fold_fields(sc, f, r < n);
     }
     typedef cub::BlockReduce<uint64_t, kThreads> BR;
     __shared__ typename BR::TempStorage t1;
@@ -257,16 +348,24 @@ __global__ void k_tile_keys_batch(const int64_t* __restrict__ coords, int64_t n,
                                   int B, uint64_t* __restrict__ tk, int* __restrict__ row_b, BuildScalars* sc) {
     uint64_t k_or = 0, k_and = ~0ull;
     const int64_t lim = (int64_t)1 << 30;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
-        bool bad = (i > lim) | (i < -lim) | (j > lim) | (j < -lim) | (k > lim) | (k < -lim);
-        if (bad) atomicMin(&sc->bad_row, (unsigned long long)r);
-        uint64_t key = tile_key(i, j, k);
-        tk[r] = key;
-        row_b[r] = batch_of_row(off, B, r);
-        k_or |= key;
-        k_and &= key;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x; r0 < n; r0 += stride) {  // warp-uniform trip count
+        const int64_t r = r0 + threadIdx.x;
+        uint32_t f[3] = {0u, 0u, 0u};
+        if (r < n) {
+            int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
+            bool bad = (i > lim) | (i < -lim) | (j > lim) | (j < -lim) | (k > lim) | (k < -lim);
+            if (bad) atomicMin(&sc->bad_row, (unsigned long long)r);
+            uint64_t key = tile_key(i, j, k);
+            tk[r] = key;
+            row_b[r] = batch_of_row(off, B, r);
+            k_or |= key;
+            k_and &= key;
+            f[0] = (uint32_t)((key >> 42) & 0x1FFFFF);
+            f[1] = (uint32_t)((key >> 21) & 0x1FFFFF);
+            f[2] = (uint32_t)(key & 0x1FFFFF);
+        }
+        fold_fields(sc, f, r < n);
     }
     typedef cub::BlockReduce<uint64_t, kThreads> BR;
     __shared__ typename BR::TempStorage t1;
@@ -403,6 +502,76 @@ int grid_for(int64_t n) {
 
 int bit_length(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
+// tiles[0] := the common tile key (device side: no read-back needed to start the voxel sort)
+__global__ void k_single_tile(uint64_t* __restrict__ tiles, const BuildScalars* __restrict__ sc) {
+    tiles[0] = sc->key_or;
+}
+
+}  // namespace
+
+// Voxel keys for coordinates that all share one root tile (rank 0), sorted, deduped, node ids scanned; then one
+// read-back of the range / tile scalars, the pending non-finite slot and the node counts.  Returns 1 when the
+// coordinates do span several root tiles (the caller redoes the general path), 0 when `counts` are final.
+static int single_tile_pass(const int64_t* coords, int64_t n, const int64_t* pending_nonfinite, BuildWs& w,
+                            int64_t* counts, int64_t* detail, int* rc, cudaStream_t st) {
+    const int g = grid_for(n);
+    k_single_tile<<<1, 1, 0, st>>>(w.tiles, w.sc);
+    k_voxel_keys<<<g, kThreads, 0, st>>>(coords, n, w.tiles, 1, w.vk);
+    cub::DoubleBuffer<uint64_t> vb(w.vk, w.vk_alt);
+    size_t tb = w.cub_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, vb, (int)n, 0, 36, st);
+    tb = w.cub_bytes;
+    if (e == cudaSuccess) e = cub::DeviceSelect::Unique(w.cub_tmp, tb, vb.Current(), w.uvox, w.n_sel, (int)n, st);
+    if (e == cudaSuccess) {
+        k_node_heads<<<g, kThreads, 0, st>>>(w.uvox, (int)n, w.n_sel, w.leaf_id, w.lower_id, w.upper_id);
+        int* ids[3] = {w.leaf_id, w.lower_id, w.upper_id};
+        for (int t = 0; t < 3 && e == cudaSuccess; ++t) {
+            tb = w.cub_bytes;
+            e = cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, ids[t], ids[t], (int)n, st);
+        }
+    }
+    struct {
+        BuildScalars hs;
+        int last[3];
+        int nu;
+        unsigned long long nonfinite;
+    } h;
+    h.nonfinite = ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h.hs, w.sc, sizeof(h.hs), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && pending_nonfinite)
+        e = cudaMemcpyAsync(&h.nonfinite, pending_nonfinite, sizeof(h.nonfinite), cudaMemcpyDeviceToHost, st);
+    int* ids[3] = {w.leaf_id, w.lower_id, w.upper_id};
+    for (int t = 0; t < 3 && e == cudaSuccess; ++t)
+        e = cudaMemcpyAsync(&h.last[t], ids[t] + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h.nu, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("build (single-tile pass)", e);
+        *rc = FVDB_ERR_CUDA;
+        return 1;
+    }
+    if (h.nonfinite != ~0ull) {
+        *detail = (int64_t)h.nonfinite;
+        *rc = FVDB_ERR_NONFINITE;
+        return 0;
+    }
+    if (h.hs.bad_row != ~0ull) {
+        *detail = (int64_t)h.hs.bad_row;
+        *rc = FVDB_ERR_COORD_RANGE;
+        return 0;
+    }
+    if ((h.hs.key_or ^ h.hs.key_and) != 0) return 1;  // several root tiles: the general path
+    counts[0] = h.last[2];
+    counts[1] = h.last[1];
+    counts[2] = h.last[0];
+    counts[3] = h.nu;
+    *rc = counts[0] == 1 ? FVDB_OK : FVDB_ERR_INVALID;
+    if (*rc != FVDB_OK) set_error_msg("internal: single-tile pass tile count");
+    return 0;
+}
+
+namespace {
 }  // namespace
 }  // namespace fvdb
 
@@ -436,6 +605,12 @@ extern "C" int fvdb_build_plan2(const int64_t* coords, int64_t n, const int64_t*
     k_init_scalars<<<1, 1, 0, st>>>(w.sc);
     k_tile_keys<<<g, kThreads, 0, st>>>(coords, n, w.tk, w.sc);
     FVDB_LAUNCH_CHECK();
+    {
+        // optimistic single-root-tile pass (every BASELINE shell and point cloud): one host read-back instead of two
+        int rc = FVDB_OK;
+        if (single_tile_pass(coords, n, pending_nonfinite, w, counts, detail, &rc, st) == 0) return rc;
+        if (rc != FVDB_OK) return rc;
+    }
     BuildScalars hs;
     unsigned long long nonfinite = ~0ull;
     FVDB_CUDA_TRY(cudaMemcpyAsync(&hs, w.sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -457,12 +632,20 @@ extern "C" int fvdb_build_plan2(const int64_t* coords, int64_t n, const int64_t*
     if (diff == 0) {
         FVDB_CUDA_TRY(cudaMemcpyAsync(w.tiles, &hs.key_or, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     } else {
+        TileCompress tcm;
+        const bool comp = make_compress(hs, &tcm);
         int lo_bit = __builtin_ctzll(diff), hi_bit = bit_length(diff);
+        if (comp) {  // sort the order-preserving compressed keys (few bits), decode the distinct ones
+            k_compress_keys<<<g, kThreads, 0, st>>>(w.tk, n, tcm, w.tk);
+            lo_bit = 0;
+            hi_bit = tcm.total > 0 ? tcm.total : 1;
+        }
         cub::DoubleBuffer<uint64_t> db(w.tk, w.tk_alt);
         size_t tb = w.cub_bytes;
         FVDB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, db, (int)n, lo_bit, hi_bit, st));
         tb = w.cub_bytes;
         FVDB_CUDA_TRY(cub::DeviceSelect::Unique(w.cub_tmp, tb, db.Current(), w.tiles, w.n_sel, (int)n, st));
+        if (comp) k_decompress_keys<<<grid_for(n), kThreads, 0, st>>>(w.tiles, w.n_sel, tcm);
         int nt = 0;
         FVDB_CUDA_TRY(cudaMemcpyAsync(&nt, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
         FVDB_CUDA_TRY(cudaStreamSynchronize(st));
@@ -601,12 +784,20 @@ extern "C" int fvdb_build_batch_plan(const int64_t* coords, int64_t n, const int
     int gbits = -1;
     const uint64_t diff = hs.key_or ^ hs.key_and;
     if (diff != 0) {
-        const int lo_bit = __builtin_ctzll(diff), hi_bit = bit_length(diff);
+        TileCompress tcm;
+        const bool comp = make_compress(hs, &tcm);
+        int lo_bit = __builtin_ctzll(diff), hi_bit = bit_length(diff);
+        if (comp) {
+            k_compress_keys<<<g, kThreads, 0, st>>>(w.tk, n, tcm, w.tk);
+            lo_bit = 0;
+            hi_bit = tcm.total > 0 ? tcm.total : 1;
+        }
         cub::DoubleBuffer<uint64_t> db(w.tk, w.tk_alt);
         size_t tb = w.cub_bytes;
         FVDB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(w.cub_tmp, tb, db, (int)n, lo_bit, hi_bit, st));
         tb = w.cub_bytes;
         FVDB_CUDA_TRY(cub::DeviceSelect::Unique(w.cub_tmp, tb, db.Current(), bw.gtiles, w.n_sel, (int)n, st));
+        if (comp) k_decompress_keys<<<grid_for(n), kThreads, 0, st>>>(bw.gtiles, w.n_sel, tcm);
         int ng = 0;
         FVDB_CUDA_TRY(cudaMemcpyAsync(&ng, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
         FVDB_CUDA_TRY(cudaStreamSynchronize(st));
