@@ -12,8 +12,11 @@
  *     the offending row / count for the data errors so the caller can raise the
  *     reference's exact message;
  *   - the library never allocates device memory outside the caller-provided
- *     workspace, never frees caller memory, and keeps no global mutable state
- *     (the last CUDA error string is thread-local).
+ *     workspace and never frees caller memory.  Mutable state it does keep, none of
+ *     it on a result's data path: the last CUDA error string (thread-local); the
+ *     FVDB_* environment switches, read once per process into function-local
+ *     statics; device-global trace buffers written only when a profiling switch
+ *     (FVDB_DEBUG_HALO & 64 / 128) is set.  Entry points are reentrant per stream.
  */
 #ifndef FVDB_B200_H
 #define FVDB_B200_H
