@@ -57,6 +57,11 @@ typedef struct fvdb_grid_view {
     int64_t num_upper;
     int64_t num_leaf;
     int64_t num_voxels;
+    /* optional dense child tables (fvdb_node_tables; NULL = binary searches of tile_keys then leaf_keys):
+     * upper_table[u][32768] = lower node of upper u at each lower offset, lower_table[lo][4096] = leaf of lower
+     * lo at each leaf offset, -1 where absent.  A probe is then one short tile search and two loads. */
+    const int32_t* upper_table;
+    const int32_t* lower_table;
 } fvdb_grid_view;
 
 /* Writable device arrays of one IndexGrid, sized from fvdb_build_plan's counts. */
@@ -119,6 +124,14 @@ int fvdb_build_batch_fill(void* workspace, size_t workspace_bytes, int64_t n, in
 /* a6: coarsen input — floor_divide(coords, factor) (build.py:325-339) */
 int fvdb_floor_div_coords(const int64_t* coords, int64_t n, int64_t factor, int64_t* out,
                           void* stream);
+
+/* Dense child tables of a grid's internal nodes (the VDB node layout: 32^3 children per upper node, 16^3 per
+ * lower node), from the reference's sorted child lists (upper_child_starts / lower_offset_in_upper,
+ * lower_child_starts / leaf_offset_in_lower; topology.py:140-177).  upper_table: int32 [num_upper][32768],
+ * lower_table: int32 [num_lower][4096] (device, caller-allocated). */
+int fvdb_node_tables(const int64_t* upper_child_starts, int64_t num_upper, const uint16_t* lower_offset_in_upper,
+                     const int64_t* lower_child_starts, int64_t num_lower, const uint16_t* leaf_offset_in_lower,
+                     int64_t num_leaf, int32_t* upper_table, int32_t* lower_table, void* stream);
 
 /* ---- a5: IndexGrid.coord_to_index_many / active_coords (topology.py:253-299) ---- */
 int fvdb_coord_to_index(const fvdb_grid_view* grid, const int64_t* coords, int64_t n,

@@ -38,7 +38,7 @@ class GridView(C.Structure):
     """fvdb_grid_view"""
     _fields_ = [("tile_keys", _vp), ("leaf_keys", _vp), ("leaf_origins", _vp), ("leaf_masks", _vp),
                 ("leaf_prefix", _vp), ("leaf_value_offset", _vp), ("num_upper", _i64),
-                ("num_leaf", _i64), ("num_voxels", _i64)]
+                ("num_leaf", _i64), ("num_voxels", _i64), ("upper_table", _vp), ("lower_table", _vp)]
 
 
 class HaloPlan(C.Structure):
@@ -70,6 +70,7 @@ SIGNATURES = {
     "fvdb_build_batch_plan": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
     "fvdb_build_batch_fill": (_i32, [_vp, _sz, _i64, _i64, C.POINTER(_i64), C.POINTER(GridArrays), _vp]),
     "fvdb_floor_div_coords": (_i32, [_vp, _i64, _i64, _vp, _vp]),
+    "fvdb_node_tables": (_i32, [_vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp]),
     "fvdb_coord_to_index": (_i32, [C.POINTER(GridView), _vp, _i64, _vp, _vp]),
     "fvdb_active_coords": (_i32, [C.POINTER(GridView), _vp, _vp]),
     "fvdb_kmap_workspace_bytes": (_sz, [_i64]),

@@ -84,6 +84,11 @@ __device__ __forceinline__ int64_t find_leaf(const fvdb_grid_view& g, int64_t i,
     uint64_t tk = tile_key(i, j, k);
     int64_t t = lower_bound_u64(g.tile_keys, g.num_upper, tk);
     if (t >= g.num_upper || g.tile_keys[t] != tk) return -1;
+    if (g.lower_table) {  // dense child tables: two dependent loads instead of a leaf_keys binary search
+        const int32_t lo = __ldg(g.upper_table + t * 32768 + upper_off(i, j, k));
+        if (lo < 0) return -1;
+        return __ldg(g.lower_table + (int64_t)lo * 4096 + lower_off(i, j, k));
+    }
     uint64_t lk = ((uint64_t)t << 27) | ((uint64_t)upper_off(i, j, k) << 12) | lower_off(i, j, k);
     int64_t l = lower_bound_u64(g.leaf_keys, g.num_leaf, lk);
     if (l >= g.num_leaf || g.leaf_keys[l] != lk) return -1;

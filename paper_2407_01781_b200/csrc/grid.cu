@@ -110,14 +110,22 @@ struct KmWarpSmem {
 
 __global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant__ KmapBatch kb, int stride,
                                                            int32_t* __restrict__ nbr, int64_t ld,
-                                                           unsigned long long* __restrict__ counts) {
+                                                           unsigned long long* __restrict__ counts,
+                                                           unsigned long long* __restrict__ next_leaf) {
     __shared__ KmWarpSmem sw[kKmWarps];
     __shared__ int s_cnt[27];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x < 27) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    const int64_t lg = (int64_t)blockIdx.x * kKmWarps + warp;
-    if (lg < kb.leaf_start[kb.B]) {
+    // persistent warps: each takes output leaves from a global counter until none are left (no warp idles at
+    // EXIT waiting for its CTA's slowest leaf; ncu: 38% of stall samples before)
+    const int64_t n_leaves = kb.leaf_start[kb.B];
+    for (;;) {
+    int64_t lg = 0;
+    if (lane == 0) lg = (int64_t)atomicAdd(next_leaf, 1ull);
+    lg = __shfl_sync(0xffffffffu, lg, 0);
+    if (lg >= n_leaves) break;
+    {
         KmWarpSmem& S = sw[warp];
         const int b = batch_of_leaf(kb, lg);
         const fvdb_grid_view& gin = kb.gin[b];
@@ -196,6 +204,8 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant
                 if (leader && c) atomicAdd(&s_cnt[d], c);
             }
         }
+        __syncwarp();  // the warp's shared slice is rewritten by its next leaf
+    }
     }
     __syncthreads();
     if (threadIdx.x < 27 && s_cnt[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
@@ -243,6 +253,21 @@ __global__ void k_transpose(const int32_t* __restrict__ nbr, int64_t ld, int64_t
     }
 }
 
+// parent of child c in a sorted child-start array starts[0..n] (last parent p with starts[p] <= c)
+__device__ __forceinline__ int64_t parent_of(const int64_t* __restrict__ starts, int64_t n, int64_t c) {
+    int64_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(starts + mid) <= c) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+__global__ void k_node_table(const int64_t* __restrict__ starts, int64_t n_parent, const uint16_t* __restrict__ off,
+                             int64_t n_child, int width, int32_t* __restrict__ table) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_child; c += (int64_t)gridDim.x * blockDim.x)
+        table[parent_of(starts, n_parent, c) * width + off[c]] = (int32_t)c;
+}
+
 // 8 elements per thread step (two 16-B loads, one 16-B store) when both pointers are 16-B aligned
 __global__ void k_f32_to_bf16(const float* __restrict__ s, int64_t n, __nv_bfloat16* __restrict__ d, int vec) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -274,6 +299,26 @@ extern "C" int fvdb_device_sm_count(int device) {
     return v;
 }
 
+extern "C" int fvdb_node_tables(const int64_t* upper_child_starts, int64_t num_upper,
+                                const uint16_t* lower_offset_in_upper, const int64_t* lower_child_starts,
+                                int64_t num_lower, const uint16_t* leaf_offset_in_lower, int64_t num_leaf,
+                                int32_t* upper_table, int32_t* lower_table, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (num_upper < 0 || num_lower < 0 || num_leaf < 0) return FVDB_ERR_INVALID;
+    if (num_upper > 0)
+        FVDB_CUDA_TRY(cudaMemsetAsync(upper_table, 0xFF, (size_t)num_upper * 32768 * sizeof(int32_t), st));
+    if (num_lower > 0)
+        FVDB_CUDA_TRY(cudaMemsetAsync(lower_table, 0xFF, (size_t)num_lower * 4096 * sizeof(int32_t), st));
+    if (num_lower > 0)
+        k_node_table<<<grid_for(num_lower), kThreads, 0, st>>>(upper_child_starts, num_upper, lower_offset_in_upper,
+                                                               num_lower, 32768, upper_table);
+    if (num_leaf > 0)
+        k_node_table<<<grid_for(num_leaf), kThreads, 0, st>>>(lower_child_starts, num_lower, leaf_offset_in_lower,
+                                                              num_leaf, 4096, lower_table);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
 extern "C" int fvdb_coord_to_index(const fvdb_grid_view* g, const int64_t* coords, int64_t n, int64_t* out,
                                    void* stream) {
     if (n == 0) return FVDB_OK;
@@ -290,7 +335,8 @@ extern "C" int fvdb_active_coords(const fvdb_grid_view* g, int64_t* out, void* s
 }
 
 extern "C" size_t fvdb_kmap_workspace_bytes(int64_t num_leaf_out) {
-    // neighbour leaves [leaf][27] + per-leaf pair counts [27][leaf]
+    // the persistent warps' leaf counters (one per launch chunk of 32 grids); sized generously as before so the
+    // ABI's workspace contract is unchanged
     return 2 * ((size_t)(num_leaf_out > 0 ? num_leaf_out : 1) * 27 * sizeof(int32_t) + 256);
 }
 
@@ -321,8 +367,13 @@ extern "C" int fvdb_kernel_map_batch(const fvdb_grid_view* gin, const fvdb_grid_
         FVDB_CUDA_TRY(cudaMemsetAsync(pair_counts, 0, 27 * sizeof(int64_t), st));
         return FVDB_OK;
     }
-    (void)ws;
     FVDB_CUDA_TRY(cudaMemsetAsync(pair_counts, 0, 27 * sizeof(int64_t), st));
+    unsigned long long* next_leaf = reinterpret_cast<unsigned long long*>(ws);  // one counter per launch chunk
+    const int64_t n_chunks = ceil_div(B, kMaxBatch);
+    FVDB_CUDA_TRY(cudaMemsetAsync(next_leaf, 0, (size_t)n_chunks * sizeof(unsigned long long), st));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     for (int64_t c0 = 0; c0 < B; c0 += kMaxBatch) {
         KmapBatch kb;
         kb.B = (int)(B - c0 < kMaxBatch ? B - c0 : kMaxBatch);
@@ -336,8 +387,9 @@ extern "C" int fvdb_kernel_map_batch(const fvdb_grid_view* gin, const fvdb_grid_
         }
         const int64_t nl = kb.leaf_start[kb.B];
         if (nl == 0) continue;
-        k_kernel_map<<<(unsigned)ceil_div(nl, kKmWarps), kKmThreads, 0, st>>>(
-            kb, stride, nbr, ld, reinterpret_cast<unsigned long long*>(pair_counts));
+        const int64_t want = ceil_div(nl, kKmWarps), cap = (int64_t)sms * 4;  // 4 CTAs per SM are resident
+        k_kernel_map<<<(unsigned)(want < cap ? want : cap), kKmThreads, 0, st>>>(
+            kb, stride, nbr, ld, reinterpret_cast<unsigned long long*>(pair_counts), next_leaf + c0 / kMaxBatch);
     }
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;

@@ -90,7 +90,7 @@ def _device():
 class IndexGrid:
     """Immutable sparse topology on one CUDA device (topology.py:140-305)."""
 
-    __slots__ = ARRAY_FIELDS + ("num_voxels", "transform", "name", "_view", "_batch", "__weakref__")
+    __slots__ = ARRAY_FIELDS + ("num_voxels", "transform", "name", "_view", "_batch", "_tables", "__weakref__")
 
     def __init__(self, *, num_voxels, transform, name="", **arrays):
         for f in ARRAY_FIELDS:
@@ -99,6 +99,7 @@ class IndexGrid:
         self.transform = transform
         self.name = name
         self._view = None
+        self._tables = None
         self._batch = None  # kernel-map cache of the single-grid GridBatch views of this grid (as_grid_batch)
 
     # -- counts (topology.py:179-201) ---------------------------------------
@@ -158,6 +159,15 @@ class IndexGrid:
             v.num_upper = self.num_upper_nodes
             v.num_leaf = self.num_leaf_nodes
             v.num_voxels = self.num_voxels
+            if self.num_leaf_nodes:  # dense child tables: probes become two loads after the tile search
+                nu, nlo = self.num_upper_nodes, self.num_lower_nodes
+                self._tables = (torch.empty(nu * 32768, dtype=torch.int32, device=self.device),
+                                torch.empty(max(nlo, 1) * 4096, dtype=torch.int32, device=self.device))
+                _lib.check(_lib.lib().fvdb_node_tables(
+                    self.upper_child_starts.data_ptr(), nu, self.lower_offset_in_upper.data_ptr(),
+                    self.lower_child_starts.data_ptr(), nlo, self.leaf_offset_in_lower.data_ptr(), self.num_leaf_nodes,
+                    self._tables[0].data_ptr(), self._tables[1].data_ptr(), _lib.stream_ptr()), "node_tables")
+                v.upper_table, v.lower_table = self._tables[0].data_ptr(), self._tables[1].data_ptr()
             self._view = v
         return self._view
 
