@@ -211,3 +211,24 @@ def test_same_grid_transpose_by_row_reversal_is_exact(golden_grids, name):
     _lib.check(_lib.lib().fvdb_kmap_transpose(km.fwd.t.data_ptr(), km.fwd.ld, km.num_out, km.num_in, t.data_ptr(),
                                               t.shape[1], _lib.stream_ptr()), "kmap_transpose")
     assert km._same_grids() and torch.equal(km.bwd.t, t)
+
+
+@pytest.mark.parametrize("name", ["multi_tile", "neg_boundary", "scattered", "wide"])
+def test_probe_with_and_without_node_tables(golden_grids, name):
+    """coord_to_index through the dense child tables (default views) equals the binary-search path (a view without
+    tables) and the reference's probe results."""
+    import ctypes as C
+    from paper_2407_01781_b200 import _lib
+    g, _ = P.build_from_coords(golden_grids[f"{name}/coords"])
+    q = torch.from_numpy(np.ascontiguousarray(golden_grids[f"{name}/probe"])).cuda()
+    with_t = g.coord_to_index_many(q)
+    v = g.view()
+    assert v.lower_table
+    bare = _lib.GridView(tile_keys=v.tile_keys, leaf_keys=v.leaf_keys, leaf_origins=v.leaf_origins,
+                         leaf_masks=v.leaf_masks, leaf_prefix=v.leaf_prefix, leaf_value_offset=v.leaf_value_offset,
+                         num_upper=v.num_upper, num_leaf=v.num_leaf, num_voxels=v.num_voxels)
+    out = torch.empty(q.shape[0], dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().fvdb_coord_to_index(C.byref(bare), q.data_ptr(), q.shape[0], out.data_ptr(),
+                                              _lib.stream_ptr()), "coord_to_index")
+    assert torch.equal(with_t, out)
+    assert np.array_equal(with_t.cpu().numpy(), golden_grids[f"{name}/probe_index"])
