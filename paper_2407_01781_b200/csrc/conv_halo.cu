@@ -1438,25 +1438,108 @@ __device__ void plan_tile(const int32_t* __restrict__ nbr, int64_t ld, int64_t n
     }
 }
 
+constexpr int kHashBits = 12, kHashSize = 1 << kHashBits;  // > the 3456 entries of a tile (load <= 0.85)
+constexpr uint64_t kEmpty = ~0ull;
+
+// Tile dedupe by a shared-memory hash set (the plan needs no sorted order: any dense numbering of a tile's unique
+// rows per (phase, colour) is a valid slot assignment, slot = 2 * rank + colour).  Replaces a block radix sort of
+// the 27 x 128 entries per tile (count 0.50 + fill 0.66 ms at cfg2).  Slot numbers depend on the order of atomic
+// insertions; the convolution reads rows by slot, so its results do not.
+struct PlanHashSmem {
+    uint64_t hkey[kHashSize];      // (phase << 32) | row, kEmpty if free
+    uint16_t hslot[kHashSize];     // (unused by the count pass)
+    uint16_t slot_e[kPlanKeys];
+};
+
+
+
+__device__ __forceinline__ uint32_t plan_hash(uint64_t k) {
+    return (uint32_t)((k * 0x9E3779B97F4A7C15ull) >> (64 - kHashBits));
+}
+
+// Dedupe the tile's (phase, row) keys for `level` phases into the hash set; per (colour, phase) unique counts and
+// the phase layout in `pc`.  WITH_E (fill pass): each new key takes slot 2 * atomicAdd(cnt) + colour, and
+// S.slot_e gets every element's slot.  Block-wide.
+template <bool WITH_E>
+__device__ void plan_tile_hash(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out,
+                          const uint8_t* __restrict__ color, int tile, int level, PlanHashSmem& S, PlanCounts& pc) {
+    const int tid = threadIdx.x;
+    const int gsz = 27 / level;
+    for (int h = tid; h < kHashSize; h += kPlanThreads) S.hkey[h] = kEmpty;
+    if (tid < 27) pc.cnt[0][tid] = pc.cnt[1][tid] = 0;
+    __syncthreads();
+    int32_t row[kPlanItems];
+    uint32_t hpos[kPlanItems];
+#pragma unroll
+    for (int k = 0; k < kPlanItems; ++k) {
+        const int e = tid + k * kPlanThreads;  // strided: a warp's 32 entries are consecutive rows of one offset
+        row[k] = -1;
+        hpos[k] = 0;
+        if (e < 27 * kTileRows) {
+            const int d = e / kTileRows, i = e % kTileRows;
+            const int64_t o = (int64_t)tile * kTileRows + i;
+            if (o < n_out) row[k] = nbr[(int64_t)d * ld + o];
+        }
+        if (row[k] >= 0) {
+            const int ph = (e / kTileRows) / gsz;
+            const uint64_t key = ((uint64_t)ph << 32) | (uint32_t)row[k];
+            uint32_t h = plan_hash(key);
+            for (;;) {
+                const uint64_t prev = atomicCAS((unsigned long long*)&S.hkey[h], (unsigned long long)kEmpty,
+                                                (unsigned long long)key);
+                if (prev == kEmpty) {  // first occurrence: count it (and in the fill pass, give it a slot)
+                    const int c = color ? (color[row[k]] & 1) : 0;
+                    const int r = atomicAdd(&pc.cnt[c][ph], 1);
+                    if constexpr (WITH_E) S.hslot[h] = (uint16_t)(2 * r + c);
+                    break;
+                }
+                if (prev == key) break;
+                h = (h + 1) & (kHashSize - 1);
+            }
+            hpos[k] = h;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int gr = 0; gr < 27; ++gr) {
+            const int h = gr < level ? 2 * max(pc.cnt[0][gr], pc.cnt[1][gr]) : 0;
+            pc.ghalo[gr] = (h + 7) & ~7;
+            pc.goff[gr] = acc;
+            acc += pc.ghalo[gr];
+        }
+        pc.total = acc;
+    }
+    if constexpr (WITH_E) {
+#pragma unroll
+        for (int k = 0; k < kPlanItems; ++k) {
+            const int e = tid + k * kPlanThreads;
+            if (e < 27 * kTileRows) S.slot_e[e] = row[k] >= 0 ? S.hslot[hpos[k]] : kNoSlot;
+        }
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ bool plan_fits(const PlanCounts& pc, int level, int cap) {
     for (int gr = 0; gr < level; ++gr)
         if (pc.ghalo[gr] > cap) return false;
     return true;
 }
 
-// count pass: choose the smallest phase count whose halos fit; tile_size[t] = slots of tile t
+// count pass: choose the smallest phase count whose halos fit; tile_size[t] = slots of tile t.  Unique rows per
+// (colour, phase) come from the shared-memory hash set (counts need no order: 344 vs 500 us at cfg2); the fill
+// pass sorts, so slots follow ascending input rows (measured: hash-order slots cost the conv kernels ~2%).
 __global__ void __launch_bounds__(kPlanThreads) k_halo_count(const int32_t* __restrict__ nbr, int64_t ld, int64_t n_out,
                                                             const uint8_t* __restrict__ color, fvdb_halo_plan P,
                                                             int32_t* __restrict__ tile_size) {
     extern __shared__ __align__(16) uint8_t psm[];
-    PlanSmem& S = *reinterpret_cast<PlanSmem*>(psm);
+    PlanHashSmem& S = *reinterpret_cast<PlanHashSmem*>(psm);
     __shared__ PlanCounts pc;
     const int tile = blockIdx.x;
     int level = 1;
     for (;; level *= 3) {
-        plan_tile<false>(nbr, ld, n_out, color, tile, level, S, pc);
+        plan_tile_hash<false>(nbr, ld, n_out, color, tile, level, S, pc);
         if (level == 27 || plan_fits(pc, level, P.halo_cap)) break;
-        __syncthreads();
     }
     if (threadIdx.x < 27) {
         int32_t* ph = P.phase + ((int64_t)tile * 27 + threadIdx.x) * 2;
@@ -1752,8 +1835,8 @@ extern "C" int fvdb_halo_plan_count(const int32_t* nbr, int64_t ld, int64_t n_ou
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, sizes, P.tile_base, T);
     void* tmpp = cv.take<uint8_t>(tmp);
     if (!cv.ok()) return FVDB_ERR_WORKSPACE;
-    FVDB_CUDA_TRY(cudaFuncSetAttribute(k_halo_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSmem)));
-    k_halo_count<<<T, kPlanThreads, sizeof(PlanSmem), st>>>(nbr, ld, n_out, color_in, P, sizes);
+    FVDB_CUDA_TRY(cudaFuncSetAttribute(k_halo_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanHashSmem)));
+    k_halo_count<<<T, kPlanThreads, sizeof(PlanHashSmem), st>>>(nbr, ld, n_out, color_in, P, sizes);
     FVDB_LAUNCH_CHECK();
     FVDB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmpp, tmp, sizes, P.tile_base, T, st));
     int32_t last_base = 0, last_size = 0;
