@@ -96,6 +96,8 @@ def parse():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--e2e-dtype", default="bf16", choices=["bf16", "fp32"],
+                    help="host dtype of the features the e2e step uploads (bf16: the config's compute dtype)")
     return ap.parse_args()
 
 
@@ -620,7 +622,9 @@ def ffma_peak(torch):
 def run_e2e(args, cfg, P, torch, dist, prob, cin, cout, dev, use_dist, world):
     """The same step through the public API with host data, every copy inside the timed region.
 
-    Each step uploads that step's fp32 features from pinned host memory, runs SparseConv3d forward (or, for a
+    Each step uploads that step's features from pinned host memory (bf16, the configs' compute dtype, as a
+    training pipeline would keep them; ``--e2e-dtype fp32`` uploads fp32 and casts on the device), runs
+    SparseConv3d forward (or, for a
     row shard, dist.RowShard.forward), takes the loss ½‖y‖² (its gradient, y itself, seeds the backward: dgrad +
     wgrad) and reads the loss and the fp32 weight gradient back to the host.  As a training loop with a
     prefetching loader would, step k+1's features upload on a copy stream during step k (double-buffered,
@@ -633,8 +637,9 @@ def run_e2e(args, cfg, P, torch, dist, prob, cin, cout, dev, use_dist, world):
     s_in = torch.cuda.Stream(dev)
     rowshard = cfg.get("rowshard")
     n_up = (prob["rows"].stop - prob["rows"].start) if rowshard else prob["n_in"]
-    x_h = [torch.from_numpy(rng.normal(size=(n_up, cin)).astype(np.float32)).pin_memory() for _ in range(2)]
-    x_d = [torch.empty((n_up, cin), dtype=torch.float32, device=dev) for _ in range(2)]
+    hdt = torch.bfloat16 if args.e2e_dtype == "bf16" else torch.float32
+    x_h = [torch.from_numpy(rng.normal(size=(n_up, cin)).astype(np.float32)).to(hdt).pin_memory() for _ in range(2)]
+    x_d = [torch.empty((n_up, cin), dtype=hdt, device=dev) for _ in range(2)]
     loss_h = torch.empty(2, dtype=torch.float32).pin_memory()
     gw_h = torch.empty((cout, cin, 3, 3, 3), dtype=torch.float32).pin_memory()
     ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -725,11 +730,11 @@ def run_e2e(args, cfg, P, torch, dist, prob, cin, cout, dev, use_dist, world):
     torch.cuda.synchronize()
     ms = max_over_ranks(torch, dist, dev, e0.elapsed_time(e1) / steps, use_dist)
     units = int(sum_over_ranks(torch, dist, dev, prob["units"], use_dist))
-    h2d = x_h[0].numel() * 4
+    h2d = x_h[0].numel() * x_h[0].element_size()
     d2h = 4 + gw_h.numel() * 4
     return {"value": round(units / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps, "api": api,
-            "step": "upload fp32 features (pinned) -> forward -> loss 0.5*|y|^2 -> backward (dgrad + wgrad"
+            "step": f"upload {args.e2e_dtype} features (pinned) -> forward -> loss 0.5*|y|^2 -> backward (dgrad + wgrad"
                     + (", NCCL all-reduce" if use_dist else "") + ") -> read back loss + fp32 weight gradient",
             "pipeline": "features of step k+1 uploaded on a copy stream during step k; every copy inside the "
                         "timed region"}
