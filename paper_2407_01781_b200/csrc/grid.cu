@@ -175,9 +175,12 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant
         // voxel-outer, offset-inner: a lane's 27 probes share the per-axis neighbour-leaf / bit terms; each offset's
         // stores stay coalesced across the lanes (consecutive rows)
         int32_t* out = nbr + kb.out_base[b] + (int64_t)gout.leaf_value_offset[l] - 1;
+        // per-lane pair counts of the leaf, two offsets per register (16-bit halves: <= 16 voxels per lane per
+        // leaf, <= 512 summed over the warp): no per-probe ballot / atomic / reconvergence
+        uint32_t pc[14];
+#pragma unroll
+        for (int k = 0; k < 14; ++k) pc[k] = 0u;
         for (int r = lane; r < nvox; r += 32) {
-            const uint32_t act = __activemask();
-            const bool leader = lane == __ffs(act) - 1;
             const int m = S.pos[r];
             const int x = m >> 6, y = (m >> 3) & 7, z = m & 7;
             int ex[3], ey[3], ez[3], bx[3], by[3], bz[3];
@@ -200,8 +203,15 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant
                 const uint64_t below = word & ((1ull << (bb & 63)) - 1ull);
                 const bool hit = (word >> (bb & 63)) & 1ull;
                 out[(int64_t)d * ld + r] = hit ? S.base[e][bb >> 6] + __popcll(below) : -1;
-                const int c = __popc(__ballot_sync(act, hit));
-                if (leader && c) atomicAdd(&s_cnt[d], c);
+                pc[d >> 1] += (uint32_t)hit << (16 * (d & 1));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 14; ++k) {
+            const uint32_t v = __reduce_add_sync(0xffffffffu, pc[k]);
+            if (lane == 0) {
+                if (v & 0xFFFFu) atomicAdd(&s_cnt[2 * k], (int)(v & 0xFFFFu));
+                if (2 * k + 1 < 27 && (v >> 16)) atomicAdd(&s_cnt[2 * k + 1], (int)(v >> 16));
             }
         }
         __syncwarp();  // the warp's shared slice is rewritten by its next leaf
@@ -387,7 +397,7 @@ extern "C" int fvdb_kernel_map_batch(const fvdb_grid_view* gin, const fvdb_grid_
         }
         const int64_t nl = kb.leaf_start[kb.B];
         if (nl == 0) continue;
-        const int64_t want = ceil_div(nl, kKmWarps), cap = (int64_t)sms * 4;  // 4 CTAs per SM are resident
+        const int64_t want = ceil_div(nl, kKmWarps), cap = (int64_t)sms * 3;  // 3 CTAs per SM are resident (80 regs)
         k_kernel_map<<<(unsigned)(want < cap ? want : cap), kKmThreads, 0, st>>>(
             kb, stride, nbr, ld, reinterpret_cast<unsigned long long*>(pair_counts), next_leaf + c0 / kMaxBatch);
     }
