@@ -1619,6 +1619,67 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_fill(const int32_t* __res
     }
 }
 
+// fill pass over the hash set (opt-in, FVDB_PLAN_HASH_FILL=1): slots in hash-insertion order instead of ascending
+// rows; same record format.
+__global__ void __launch_bounds__(kPlanThreads) k_halo_fill_hash(const int32_t* __restrict__ nbr, int64_t ld,
+                                                                int64_t n_out, const uint8_t* __restrict__ color,
+                                                                const uint8_t* __restrict__ q_out, fvdb_halo_plan P) {
+    extern __shared__ __align__(16) uint8_t psm[];
+    PlanHashSmem& S = *reinterpret_cast<PlanHashSmem*>(psm);
+    __shared__ PlanCounts pc;
+    __shared__ int perm[kTileRows];
+    __shared__ int wcnt[2][4];
+    const int tile = blockIdx.x, tid = threadIdx.x;
+    const int level = P.tile_level[tile];
+    const int base = P.tile_base[tile];
+    plan_tile_hash<true>(nbr, ld, n_out, color, tile, level, S, pc);
+    for (int s = tid; s < pc.total; s += kPlanThreads) P.halo_rows[base + s] = -1;
+    __syncthreads();
+    for (int h = tid; h < kHashSize; h += kPlanThreads) {
+        const uint64_t k = S.hkey[h];
+        if (k != kEmpty) P.halo_rows[base + pc.goff[(int)(k >> 32)] + S.hslot[h]] = (int32_t)(uint32_t)k;
+    }
+    int f = -1, o = -1;
+    if (tid < kTileRows) {
+        perm[tid] = -1;
+        const int64_t oo = (int64_t)tile * kTileRows + tid;
+        if (oo < n_out) {
+            o = (int)oo;
+            f = q_out ? (q_out[oo] & 1) : 0;
+        }
+    }
+    const int w = tid >> 5, ln = tid & 31;
+    const uint32_t b0 = __ballot_sync(0xffffffffu, f == 0), b1 = __ballot_sync(0xffffffffu, f == 1);
+    if (w < 4 && ln == 0) {
+        wcnt[0][w] = __popc(b0);
+        wcnt[1][w] = __popc(b1);
+    }
+    __syncthreads();
+    if (f >= 0) {
+        const uint32_t bm = f ? b1 : b0;
+        int pos = __popc(bm & ((1u << ln) - 1u));
+        for (int ww = 0; ww < w; ++ww) pos += wcnt[f][ww];
+        int n0 = 0, n1 = 0;
+        for (int ww = 0; ww < 4; ++ww) {
+            n0 += wcnt[0][ww];
+            n1 += wcnt[1][ww];
+        }
+        const int m = min(n0, n1);
+        perm[pos < m ? 2 * pos + f : 2 * m + (pos - m)] = o;
+    }
+    __syncthreads();
+    if (tid < kTileRows) P.perm[(int64_t)tile * kTileRows + tid] = perm[tid];
+    uint8_t* rec = P.tile_rec + (int64_t)tile * kIdxBytes;
+    for (int e = tid; e < 27 * kTileRows; e += kPlanThreads) {
+        const int d = e / kTileRows, l = e % kTileRows;
+        const int oo = perm[l];
+        const uint16_t sl = oo >= 0 ? S.slot_e[d * kTileRows + (oo - tile * kTileRows)] : kNoSlot;
+        reinterpret_cast<uint16_t*>(rec)[d * kTileRows + l] = sl;
+        const uint32_t none = __ballot_sync(0xffffffffu, sl == kNoSlot);
+        if ((tid & 31) == 0) reinterpret_cast<uint32_t*>(rec + 6912)[d * 4 + (l >> 5)] = none;
+    }
+}
+
 __global__ void k_parity_colors(const int64_t* __restrict__ c, int64_t n, int shift, uint8_t* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = (uint8_t)(((c[3 * i] >> shift) + (c[3 * i + 1] >> shift) + (c[3 * i + 2] >> shift)) & 1);
@@ -1853,6 +1914,15 @@ extern "C" int fvdb_halo_plan_fill(const int32_t* nbr, int64_t ld, int64_t n_out
     if (n_out <= 0) return FVDB_OK;
     const fvdb_halo_plan& P = *plan;
     if (P.num_tiles != (int)ceil_div(n_out, kTileRows)) return FVDB_ERR_INVALID;
+    static const bool hash_fill = getenv("FVDB_PLAN_HASH_FILL") && atoi(getenv("FVDB_PLAN_HASH_FILL")) == 1;
+    if (hash_fill) {
+        FVDB_CUDA_TRY(cudaFuncSetAttribute(k_halo_fill_hash, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sizeof(PlanHashSmem)));
+        k_halo_fill_hash<<<P.num_tiles, kPlanThreads, sizeof(PlanHashSmem), as_stream(stream)>>>(nbr, ld, n_out,
+                                                                                                 color_in, q_out, P);
+        FVDB_LAUNCH_CHECK();
+        return FVDB_OK;
+    }
     FVDB_CUDA_TRY(cudaFuncSetAttribute(k_halo_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSmem)));
     k_halo_fill<<<P.num_tiles, kPlanThreads, sizeof(PlanSmem), as_stream(stream)>>>(nbr, ld, n_out, color_in, q_out, P);
     FVDB_LAUNCH_CHECK();
