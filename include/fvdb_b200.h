@@ -12,7 +12,8 @@
  *     the offending row / count for the data errors so the caller can raise the
  *     reference's exact message;
  *   - the library never allocates device memory outside the caller-provided
- *     workspace and never frees caller memory.  Mutable state it does keep, none of
+ *     workspace (16-byte aligned; cudaMalloc and torch allocations are) and never
+ *     frees caller memory.  Mutable state it does keep, none of
  *     it on a result's data path: the last CUDA error string (thread-local); the
  *     FVDB_* environment switches, read once per process into function-local
  *     statics; device-global trace buffers written only when a profiling switch

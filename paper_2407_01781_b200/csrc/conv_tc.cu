@@ -573,16 +573,33 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 // gw[co][ci][d] = Σ_s part[s][d][ci][co]   (fixed split order: deterministic).  Threads walk the
 // partials' own layout (co fastest) so the split-strided reads are coalesced; the scattered writes are
 // only 27·Cin·Cout elements.
+// Sum of the per-split partials, in split order (deterministic).  Each thread owns 4 consecutive Cout entries
+// (float4 loads, Cout % 4 == 0 for every instantiated shape) and keeps 8 split loads in flight: the pass is a
+// pure HBM read of splits x 27 x Cin x Cout fp32, which one dependent load per iteration left latency-bound.
 __global__ void k_wgrad_tc_reduce(const float* __restrict__ part, int splits, int cin, int cout, float* __restrict__ gw) {
-    const int64_t total = (int64_t)27 * cout * cin, stride = total;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+    const int64_t total = (int64_t)27 * cout * cin, stride4 = total / 4;
+    const float4* __restrict__ p4 = reinterpret_cast<const float4*>(part);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < stride4;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t d = t / ((int64_t)cin * cout);
-        const int64_t rem = t - d * cin * cout;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        int s = 0;
+        for (; s + 8 <= splits; s += 8) {
+            float4 r[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __ldcs(p4 + (int64_t)(s + j) * stride4 + t);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { v.x += r[j].x; v.y += r[j].y; v.z += r[j].z; v.w += r[j].w; }
+        }
+        for (; s < splits; ++s) {
+            const float4 r = __ldcs(p4 + (int64_t)s * stride4 + t);
+            v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
+        }
+        const int64_t e = 4 * t, d = e / ((int64_t)cin * cout);
+        const int64_t rem = e - d * cin * cout;
         const int64_t ci = rem / cout, co = rem - ci * cout;
-        float v = 0.f;
-        for (int s = 0; s < splits; ++s) v += part[s * stride + t];
-        gw[(co * cin + ci) * 27 + d] = v;
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) gw[((co + j) * cin + ci) * 27 + d] = vv[j];
     }
 }
 
@@ -681,7 +698,7 @@ struct WgLaunch {
         const int splits = splits_for(n_out);
         const size_t need = (size_t)splits * 27 * CIN * COUT * sizeof(float);
         if (ws_bytes < need) return FVDB_ERR_WORKSPACE;
-        if (ld % FVDB_NBR_ALIGN != 0 || ld < n_out) return FVDB_ERR_INVALID;
+        if (ld % FVDB_NBR_ALIGN != 0 || ld < n_out || ((uintptr_t)ws & 15)) return FVDB_ERR_INVALID;
         float* part = (float*)ws;
         int64_t rps = ceil_div(n_out > 0 ? n_out : 1, splits);
         rps = ceil_div(rps, C::CHUNK) * C::CHUNK;
@@ -691,7 +708,8 @@ struct WgLaunch {
         static const int dbg = getenv("FVDB_DEBUG_WG") ? atoi(getenv("FVDB_DEBUG_WG")) : 0;
         kern<<<splits * C::GROUPS, kWgThreads, C::SMEM, st>>>((const bf16*)in, (const bf16*)go, nbr, ld, n_out, rps,
                                                               part, dbg);
-        k_wgrad_tc_reduce<<<(unsigned)ceil_div((int64_t)27 * CIN * COUT, 256), 256, 0, st>>>(part, splits, CIN, COUT, gw);
+        static_assert(COUT % 4 == 0, "reduce loads float4 rows");
+        k_wgrad_tc_reduce<<<(unsigned)ceil_div((int64_t)27 * CIN * COUT / 4, 128), 128, 0, st>>>(part, splits, CIN, COUT, gw);
         FVDB_LAUNCH_CHECK();
         return FVDB_OK;
     }
