@@ -290,7 +290,10 @@ int fvdb_halo_plan_fill(const int32_t* nbr, int64_t ld, int64_t n_out, const uin
 /* B images for the halo kernel: as fvdb_pack_weights_umma with the K index permuted to the
  * TMEM A layout the kernel's tcgen05.st produces, followed by copies of offsets 0..6 so that any
  * run of up to 8 consecutive offsets (mod 27) is one contiguous TMA copy.
- * Image bytes: FVDB_HALO_IMAGES*K*N*2. */
+ * K = 32 with N <= 64 under the default lockstep kernel (env FVDB_HALO4 unset or != 0): 14
+ * offset-pair images [N][64] instead, image v holding offsets 2v and 2v + 1 (zero past 26) as one
+ * 64-deep K (the kernel multiplies two offsets per stage).
+ * Image bytes: FVDB_HALO_IMAGES*K*N*2 (both layouts fit). */
 #define FVDB_HALO_IMAGES 34
 int fvdb_pack_weights_halo(const float* w, int cout, int cin, int transpose, void* image, void* stream);
 int fvdb_conv_halo_tc(const void* in_bf16, int64_t n_in, int K, const void* w_image, int N,

@@ -73,6 +73,51 @@ __host__ __device__ __forceinline__ int halo_phys(int K, int s, int c) {
     return K == 64 ? (c ^ (s & 1)) : (K == 128 ? (c ^ ((s & 1) << 2)) : c);
 }
 
+// K = 32 offset pairs (k_conv_halo4): one stage multiplies the offsets 2v and 2v + 1 at once, its A row being
+// [halo row at 2v | halo row at 2v + 1] (64 MMA K indices, 4 MMAs per stage instead of 2).  Builder threads
+// t0 < 2 read the first offset's 64-byte row, t0 >= 2 the second's, 2 chunks each.  Consecutive offsets have
+// opposite coordinate-sum parity, so of the 4 slots a shared-memory phase (8 threads, two rows of opposite
+// output parity) reads, two lie in each bank half of the 64-byte rows; the chunk order below gives those
+// two rows' threads complementary chunks in each half: 8 distinct 16-byte bank groups, conflict-free.
+__host__ __device__ __forceinline__ int pair_chunk(int t0, int j) {
+    return t0 < 2 ? 2 * j + t0 : 2 * (1 - j) + (t0 - 2);
+}
+// virtual channel (0..31: offset 2v's channels, 32..63: offset 2v + 1's) -> MMA K index
+__host__ __device__ __forceinline__ int pair_k_of_channel(int vch) {
+    const int vc = vch >> 3, e = (vch >> 1) & 3, h = vch & 1;
+    int t0, j;
+    if (vc < 4) {
+        t0 = vc & 1;
+        j = vc >> 1;
+    } else {
+        const int c = vc - 4;
+        t0 = 2 + (c & 1);
+        j = 1 - (c >> 1);
+    }
+    const int i = 4 * j + e;
+    const int col = 8 * (i >> 1) + 2 * t0 + (i & 1);
+    return 2 * col + h;
+}
+constexpr int kPairImages = 14;  // offset pairs (0,1) .. (24,25), (26, zero)
+
+// Stages of builder set `set` (of `sets`) in one tile of `level` offset phases: the offsets (or, with pairs,
+// the offset pairs) v of each phase with v % sets == set.  A pair split by a phase boundary runs in both
+// phases, each time with the other phase's half masked off.
+__device__ __forceinline__ int h4_stage_count(bool pair, int level, int set, int sets) {
+    const int gs = 27 / level;
+    int n = 0;
+    for (int g = 0; g < level; ++g) {
+        int a = g * gs, b = (g + 1) * gs - 1;
+        if (pair) {
+            a >>= 1;
+            b >>= 1;
+        }
+        const int f = a + (set - a % sets + sets) % sets;
+        if (f <= b) n += (b - f) / sets + 1;
+    }
+    return n;
+}
+
 constexpr int kImgExt = 34;  // weight images per layer: 27 offsets + 7 wrap-around copies (d = 0..6), so a
                              // batch of consecutive offsets is one TMA
 constexpr int kHalves = 2;   // builder halves: the warps of half h build the batches ab with ab % 2 == h
@@ -597,18 +642,26 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
 #ifndef FVDB_H4_DB
 #define FVDB_H4_DB 1
 #endif
+#ifndef FVDB_H4_NB
+#define FVDB_H4_NB 0
+#endif
 #ifndef FVDB_H4_SETS
-#define FVDB_H4_SETS 4
+#define FVDB_H4_SETS 0
 #endif
 template <int K, int N>
 struct Halo4Cfg {
-    static constexpr int SETS = FVDB_H4_SETS;
-    static constexpr int ROWB = 2 * K, CPR = K / 8, LJ = K / 32, NX = K / 16;
-    static constexpr int KB = K >= 64 ? 64 : K;
+    // K = 32: offset-pair stages (pair_chunk): a stage is 64 MMA K indices, two offsets' rows.  Sets: 4, or 3
+    // over the 14 pair stages of a tile (5 + 5 + 4 instead of 4 + 4 + 3 + 3; cfg5 fwd 3.03 -> 2.93 ms)
+    static constexpr bool PAIR = K == 32;
+    static constexpr int SETS = FVDB_H4_SETS > 0 ? FVDB_H4_SETS : (PAIR ? 3 : 4);
+    static constexpr int KV = PAIR ? 64 : K;    // MMA K per stage
+    static constexpr int NIMG = PAIR ? kPairImages : 27;
+    static constexpr int ROWB = 2 * K, CPR = K / 8, LJ = KV / 32, NX = KV / 16;
+    static constexpr int KB = KV >= 64 ? 64 : KV;
     static constexpr int BROWB = KB * 2;
     static constexpr uint32_t BLAYOUT = BROWB == 128 ? kSwizzle128B : kSwizzle64B;
-    static constexpr int B_BYTES = N * K * 2;
-    static constexpr int ACOLS = K / 2;
+    static constexpr int B_BYTES = N * KV * 2;
+    static constexpr int ACOLS = KV / 2;
     // accumulators: double-buffered per set when TMEM allows (the set starts its next tile while the epilogue
     // drains the last one), single otherwise
     static constexpr int DB = FVDB_H4_DB == 2 && 2 * SETS * N + SETS * 2 * ACOLS <= 512 ? 2 : 1;
@@ -618,13 +671,16 @@ struct Halo4Cfg {
     static constexpr int ASL = cmin(FVDB_H4_ASL, (512 - DCOLS) / (SETS * ACOLS));
     static constexpr int WSL = ASL + 1;  // weight slots per set (stage j + 1 loads while stage j builds)
     static constexpr int WPRE = 1;
-    // all 27 offset images resident in shared memory (loaded once per CTA) when they fit beside the halo:
-    // no weight hand-off at all (K = 32 or N = 32: 54-108 KB)
-    static constexpr bool RESIDENT = 27 * B_BYTES <= 110 * 1024;
-    static constexpr int WBYTES = RESIDENT ? 27 * B_BYTES : SETS * WSL * B_BYTES;
-    static constexpr int FIXED = 1024 + WBYTES + 2 * kIdxBytes;
-    static constexpr int CAP = ((kSmemMax - 2048 - FIXED) / (2 * (ROWB + 4))) & ~7;
-    static constexpr int SMEM = FIXED + 2 * CAP * (ROWB + 4);
+    // all offset images resident in shared memory (loaded once per CTA) when they fit beside the halo:
+    // no weight hand-off at all (K = 32 or N = 32: 54-112 KB)
+    static constexpr bool RESIDENT = NIMG * B_BYTES <= 116 * 1024;
+    static constexpr int WBYTES = RESIDENT ? NIMG * B_BYTES : SETS * WSL * B_BYTES;
+    // halo buffers (row ids, rows, tile record): the loader runs NB - 1 tile phases ahead of the builders.
+    // Measured at K = 32 with pairs (cfg5 fwd): NB 2 / 4 3.04 / 3.03 ms; the default keeps the larger capacity.
+    static constexpr int NB = FVDB_H4_NB > 0 ? FVDB_H4_NB : 2;
+    static constexpr int FIXED = 1024 + WBYTES + NB * kIdxBytes;
+    static constexpr int CAP = ((kSmemMax - 2048 - FIXED) / (NB * (ROWB + 4))) & ~7;
+    static constexpr int SMEM = FIXED + NB * CAP * (ROWB + 4);
     static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, N, false, false);
     static constexpr int BUILDERS = 4 * SETS;
     static constexpr int EPI = 8;                             // epilogue warps: 4 lane quarters x 2 column halves
@@ -633,6 +689,7 @@ struct Halo4Cfg {
     static constexpr int THREADS = (2 + BUILDERS + SETS + EPI) * 32;
     static_assert(ASL >= 2 && SETS * ASL <= 15, "two A slots per set at least; named barriers");
     static_assert(RESIDENT || WSL == ASL + 1, "streamed weights: stage j's A-slot wait frees stage j + 1's image slot");
+    static_assert(!PAIR || RESIDENT, "offset pairs assume resident images (the streamed loader walks offsets)");
     static_assert(CAP >= 256, "halo capacity must hold one offset phase");
     static_assert(DCOLS + SETS * ASL * ACOLS <= 512, "TMEM");
 };
@@ -645,7 +702,8 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
     constexpr int SETS = C::SETS, ASL = C::ASL, WSL = C::WSL, kBuilders = C::BUILDERS;
     constexpr int W_LOAD = 0, W_WLOAD = 1, W_BLD = 2, W_ISS = 2 + kBuilders, W_EPI = W_ISS + SETS, HC = C::HC;
     extern __shared__ uint8_t dsmem[];
-    __shared__ __align__(8) uint64_t bar_hfull[2], bar_hempty[2], bar_xfull[2], bar_ifull[2], bar_iempty[2];
+    constexpr int NB = C::NB;
+    __shared__ __align__(8) uint64_t bar_hfull[NB], bar_hempty[NB], bar_xfull[NB], bar_ifull[NB], bar_iempty[NB];
     __shared__ __align__(8) uint64_t bar_afree[SETS][ASL];   // A slot's MMAs complete (tcgen05.commit)
     __shared__ __align__(8) uint64_t bar_wfull[SETS][WSL];   // weight image landed (TMA tx)
     __shared__ __align__(8) uint64_t bar_wfree[SETS][WSL];   // weight slot's MMAs complete
@@ -655,15 +713,15 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
 
     const uint32_t sbase = smem_u32(dsmem);
     const uint32_t bbase = (sbase + 1023u) & ~1023u;            // weight slots [SETS][WSL][B_BYTES]
-    const uint32_t ibase = bbase + C::WBYTES;                  // tile records [2]
-    const uint32_t hbase = ibase + 2 * kIdxBytes;              // halo rows [2][CAP][ROWB]
-    const uint32_t xbase = hbase + 2 * C::CAP * C::ROWB;       // halo row ids [2][CAP]
+    const uint32_t ibase = bbase + C::WBYTES;                  // tile records [NB]
+    const uint32_t hbase = ibase + NB * kIdxBytes;             // halo rows [NB][CAP][ROWB]
+    const uint32_t xbase = hbase + NB * C::CAP * C::ROWB;      // halo row ids [NB][CAP]
     const uint8_t* gen = dsmem - sbase;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int T = P.num_tiles;
 
     if (threadIdx.x == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NB; ++b) {
             mbar_init(smem_u32(&bar_hfull[b]), 32);
             mbar_init(smem_u32(&bar_hempty[b]), kBuilders);
             mbar_init(smem_u32(&bar_xfull[b]), 1);
@@ -708,8 +766,9 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
             int ng = g + 1, nt = tile;
             if (ng >= level) { ng = 0; nt = tile + gridDim.x; }
             const int nlevel = ng == 0 ? (nt < T ? P.tile_level[nt] : 1) : level;
-            const uint32_t buf = pc & 1, par = (pc >> 1) & 1;
-            const int nlen = nt < T ? issue_ids(nt, ng, buf ^ 1) : 0;
+            const uint32_t buf = pc % NB, par = (pc / NB) & 1;
+            if (lane == 0) trace(dbg, 5, pc);
+            const int nlen = nt < T ? issue_ids(nt, ng, (pc + 1) % NB) : 0;
             mbar_wait(smem_u32(&bar_xfull[buf]), par);
             mbar_wait(smem_u32(&bar_hempty[buf]), par ^ 1);
             if (lane == 0) trace(dbg, 8, pc);
@@ -727,9 +786,10 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int s = s0 + k * RPI + q;
-                    if (r[k] >= 0) cp_async_16(hb + s * C::ROWB + (halo_phys(K, s, c) << 4), in + (int64_t)r[k] * K + c * 8, 16u);
+                    if (r[k] >= 0 && !(dbg & 8)) cp_async_16(hb + s * C::ROWB + (halo_phys(K, s, c) << 4), in + (int64_t)r[k] * K + c * 8, 16u);
                 }
             }
+            if (lane == 0) trace(dbg, 11, pc);
             cp_async_arrive_noinc(smem_u32(&bar_hfull[buf]));
             if (lane == 0) {
                 mbar_wait(smem_u32(&bar_iempty[buf]), par ^ 1);
@@ -784,21 +844,29 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
         for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
             const int level = P.tile_level[tile], gs = 27 / level;
             for (int g = 0; g < level; ++g, ++pc) {
-                const uint32_t buf = pc & 1, par = (pc >> 1) & 1;
+                const uint32_t buf = pc % NB, par = (pc / NB) & 1;
                 if (tr) trace(dbg, 9, pc);
                 mbar_wait(smem_u32(&bar_hfull[buf]), par);
                 mbar_wait(smem_u32(&bar_ifull[buf]), par);
                 if (tr) trace(dbg, 10, pc);
                 const uint16_t* lb = reinterpret_cast<const uint16_t*>(gen + ibase + buf * kIdxBytes);
                 const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
-                const int d_end = (g + 1) * gs;
-                int d = g * gs;
-                d += (set - d % SETS + SETS) % SETS;
-                for (; d < d_end; d += SETS, ++js) {
+                // stage v: offset v, or with pairs offsets 2v (threads t0 < 2) and 2v + 1 (t0 >= 2), each masked
+                // off outside this phase
+                const int d0 = g * gs, d_end = (g + 1) * gs;
+                const int v0 = C::PAIR ? d0 >> 1 : d0, v_end = C::PAIR ? ((d_end - 1) >> 1) + 1 : d_end;
+                for (int vi = v0 + (set - v0 % SETS + SETS) % SETS; vi < v_end; vi += SETS, ++js) {
                     const uint32_t ak = js % ASL, ause = js / ASL;
                     if (tr) trace(dbg, 7, js);
-                    const uint16_t* lr = lb + d * kTileRows + lrow;
-                    const int sl[4] = {lr[0], lr[8], lr[16], lr[24]};
+                    int dd = vi;
+                    bool ok = true;
+                    if constexpr (C::PAIR) {
+                        dd = 2 * vi + (t0 >> 1);
+                        ok = dd >= d0 && dd < d_end;
+                    }
+                    const uint16_t* lr = lb + dd * kTileRows + lrow;
+                    const int sl[4] = {ok ? lr[0] : kNoSlot, ok ? lr[8] : kNoSlot, ok ? lr[16] : kNoSlot,
+                                       ok ? lr[24] : kNoSlot};
                     mbar_wait(smem_u32(&bar_afree[set][ak]), (ause & 1) ^ 1);
                     if (wl) load_w(js + 1);
                     tc_fence_after();
@@ -816,7 +884,8 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                                 const int pr = sv & 1;
 #pragma unroll
                                 for (int j = 0; j < C::LJ; ++j) {
-                                    const uint4 w = lds128_pred(rb + (halo_phys(K, pr, halo_chunk(K, t0, j)) << 4), has);
+                                    const int ch = C::PAIR ? pair_chunk(t0, j) : halo_phys(K, pr, halo_chunk(K, t0, j));
+                                    const uint4 w = lds128_pred(rb + (ch << 4), has);
                                     const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                                     for (int e = 0; e < 4; ++e) {
@@ -845,7 +914,6 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
         // ---------------- per-set MMA issuer: barrier, weights / accumulator waits, MMAs, commits ------------
         const int set = warp - W_ISS;
         const uint64_t bdesc0 = smem_desc(bbase, 16, 8 * C::BROWB, C::BLAYOUT);
-        const int last_d = 27 - 1 - ((27 - 1 - set) % SETS);  // this set's last offset of a tile
         const int per_tile = (27 - set + SETS - 1) / SETS;     // offsets of this set per tile
         const int ntiles = blockIdx.x < T ? (T - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
         const uint32_t total = (uint32_t)(per_tile * ntiles);
@@ -853,9 +921,15 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
         (void)total;
         uint32_t js = 0, lt = 0;
         for (int tile = blockIdx.x; tile < T; tile += gridDim.x, ++lt) {
-            for (int d = set; d < 27; d += SETS, ++js) {
+          // the builders' stage sequence: offsets (pairs) v of each phase g in order
+          const int level = C::PAIR ? P.tile_level[tile] : 1, gs = 27 / level;
+          const int nst = C::PAIR ? h4_stage_count(true, level, set, SETS) : per_tile;
+          int k = 0;
+          for (int g = 0; g < level; ++g) {
+            const int v0 = C::PAIR ? (g * gs) >> 1 : 0, v_end = C::PAIR ? (((g + 1) * gs - 1) >> 1) + 1 : 27;
+            for (int d = v0 + (set - v0 % SETS + SETS) % SETS; d < v_end; d += SETS, ++js, ++k) {
                 const uint32_t ak = js % ASL, wk = js % WSL, wuse = js / WSL;
-                const bool first = d == set;
+                const bool first = k == 0, last = k == nst - 1;
                 asm volatile("bar.sync %0, 160;" ::"r"(1 + ASL * set + (int)(js % ASL)) : "memory");
                 if (tr) trace(dbg, 2, js);
                 const uint32_t db = lt % C::DB, duse = lt / C::DB;
@@ -872,17 +946,18 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                 const uint64_t bd = bdesc0 + ((C::RESIDENT ? (uint32_t)d * C::B_BYTES
                                                            : (uint32_t)(set * WSL + wk) * C::B_BYTES) >> 4);
                 if (!(dbg & 1)) {
-                    if constexpr (K == 32) {
+                    if constexpr (C::KV == 32) {
                         mma_ts_x2_elect_acc<8, 2>(dt, at, bd, C::IDESC, first ? 0u : 1u);
                     } else {
                         mma_ts_x4_elect_acc<8, 16, 24, 2, 4, 6>(dt, at, bd, C::IDESC, first ? 0u : 1u);
                     }
                 }
                 mma_commit_elect(smem_u32(&bar_afree[set][ak]));
-                if (d == last_d) mma_commit_elect(smem_u32(&bar_dfull[set][db]));
+                if (last) mma_commit_elect(smem_u32(&bar_dfull[set][db]));
                 __syncwarp();
                 if (tr) trace(dbg, 4, js);
             }
+          }
         }
     } else if (warp >= W_EPI && warp < W_EPI + C::EPI) {
         // ---------------- epilogue: D_0 + D_1 + D_2 + D_3 (fixed order) -> output rows ----------------
@@ -1688,7 +1763,7 @@ __global__ void k_parity_colors(const int64_t* __restrict__ c, int64_t n, int sh
 // fp32 W[Cout][Cin][27] -> per-offset bf16 B images [27][K/KB][N][KB] (swizzled), K permuted to the
 // halo kernel's TMEM A layout
 __global__ void __launch_bounds__(1024) k_pack_halo(const float* __restrict__ w, int cout, int cin, int transpose,
-                                                   uint8_t* __restrict__ img) {
+                                                   int pair, uint8_t* __restrict__ img) {
     // one block per image row n: the row's K x 27 weights are read coalesced into shared memory, then written
     // as 16-byte swizzle chunks (8 consecutive MMA k of one offset; k -> channel through the K permutation)
     __shared__ float s[128 * 27];
@@ -1701,6 +1776,28 @@ __global__ void __launch_bounds__(1024) k_pack_halo(const float* __restrict__ w,
         const int ch = i / 27, d = i - ch * 27;
         const int co = transpose ? ch : n, ci = transpose ? n : ch;
         s[i] = w[((int64_t)co * cin + ci) * 27 + d];
+    }
+    if (pair) {
+        // K = 32 offset pairs (k_conv_halo4): image v = [N][64] over virtual channels (offset 2v's 32, then
+        // 2v + 1's, zero past offset 26), 128-byte swizzled rows
+        for (int ch = threadIdx.x; ch < 64; ch += blockDim.x) chan[pair_k_of_channel(ch)] = ch;
+        __syncthreads();
+        const int x = n & 7;
+        for (int c = threadIdx.x; c < kPairImages * 8; c += blockDim.x) {
+            const int v = c >> 3, k0 = (c & 7) * 8;
+            float f[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int vch = chan[k0 + j], d = 2 * v + (vch >> 5);
+                f[j] = d < 27 ? s[(vch & 31) * 27 + d] : 0.f;
+            }
+            __nv_bfloat162 b[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+            *reinterpret_cast<uint4*>(img + (size_t)v * N * 128 + (size_t)n * 128 + (((k0 >> 3) ^ x) << 4)) =
+                *reinterpret_cast<const uint4*>(b);
+        }
+        return;
     }
     for (int ch = threadIdx.x; ch < K; ch += blockDim.x) chan[halo_k_of_channel(K, ch)] = ch;
     __syncthreads();
@@ -1764,11 +1861,14 @@ int launch_halo_v(const void* in, const void* wimg, const fvdb_halo_plan& P, int
 // Measured on B200 (profiles/r02_halo4.md): resident weights (K or N = 32), cfg5 32x32 fwd 3.22 vs 3.93 ms
 // (ring), cfg2 at 32x32 0.183 vs 0.222; streamed weights at 64x64, cfg2 bench step 0.941 vs 0.963 ms (fwd 0.316
 // vs 0.327, dgrad 0.314 vs 0.324, two runs each), dense 128^3 fwd 0.631 vs 0.641.
+int halo4_env() {
+    static const int e = getenv("FVDB_HALO4") ? atoi(getenv("FVDB_HALO4")) : -1;
+    return e;
+}
 template <int K, int N>
 bool use_halo4() {
-    static const int e = getenv("FVDB_HALO4") ? atoi(getenv("FVDB_HALO4")) : -1;
     if constexpr (K <= 64 && N <= 64) {
-        return e != 0;
+        return halo4_env() != 0;
     }
     return false;
 }
@@ -1932,7 +2032,9 @@ extern "C" int fvdb_halo_plan_fill(const int32_t* nbr, int64_t ld, int64_t n_out
 extern "C" int fvdb_pack_weights_halo(const float* w, int cout, int cin, int transpose, void* image, void* stream) {
     const int K = transpose ? cout : cin, N = transpose ? cin : cout;
     if ((K != 32 && K != 64 && K != 128) || (N != 32 && N != 64 && N != 128)) return FVDB_ERR_INVALID;
-    k_pack_halo<<<transpose ? cin : cout, 1024, 0, as_stream(stream)>>>(w, cout, cin, transpose, (uint8_t*)image);
+    // K = 32 under the lockstep kernel: offset-pair images (same byte budget: 14 x N x 64 <= 34 x N x 32)
+    const int pair = K == 32 && N <= 64 && halo4_env() != 0;
+    k_pack_halo<<<transpose ? cin : cout, 1024, 0, as_stream(stream)>>>(w, cout, cin, transpose, pair, (uint8_t*)image);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

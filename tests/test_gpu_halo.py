@@ -151,6 +151,38 @@ def test_halo_conv_phases_and_stride2():
         pass
 
 
+@pytest.mark.parametrize("cap", [256, 320])
+@pytest.mark.parametrize("K,N", [(32, 32), (32, 64)])
+def test_halo_offset_pairs_across_phases(K, N, cap):
+    """K = 32 runs offset-pair stages (offsets 2v, 2v+1 as one 64-deep MMA K); a pair split by a phase
+    boundary runs in both phases with the other half masked.  Plans at small capacities force 3-, 9- and
+    27-phase tiles on a dense cube; fwd and dgrad must match the oracle."""
+    from paper_2407_01781_b200.conv import HaloPlan
+    c = dense_cube(20)
+    g, _ = P.build_from_coords(c)
+    og = O.build_from_coords(c)
+    km = P.build_kernel_map(g, g, 1)
+    ins, outs = O.kernel_map(og, og, 1)
+    kcap = int(P._lib.lib().fvdb_halo_cap(K, N))
+    for tab in (km.fwd, km.bwd):
+        tab._plans[kcap] = HaloPlan(tab, cap)
+    assert (km.fwd._plans[kcap].tensors["tile_level"] > 1).any()
+    rng = np.random.default_rng(K + N + cap)
+    n = g.num_voxels
+    x = rng.normal(size=(n, K)).astype(np.float32)
+    w = (rng.normal(size=(N, K, 3, 3, 3)) / np.sqrt(27 * K)).astype(np.float32)
+    y = gather_conv(torch.from_numpy(x).cuda().to(torch.bfloat16), km.fwd, torch.from_numpy(w).cuda(),
+                    out_dtype=torch.float32, impl="halo")
+    assert rel(y, O.conv_igemm(bf16_round(x), bf16_round(w), ins, outs, n)) < 2e-5
+    # dgrad: K input channels of the transposed conv = N
+    w2 = (rng.normal(size=(K, N, 3, 3, 3)) / np.sqrt(27 * K)).astype(np.float32)
+    gy = rng.normal(size=(n, K)).astype(np.float32)
+    gi = gather_conv(torch.from_numpy(gy).cuda().to(torch.bfloat16), km.bwd, torch.from_numpy(w2).cuda(),
+                     transpose=True, out_dtype=torch.float32, impl="halo")
+    gi_r, _ = O.conv_backward(ins, outs, bf16_round(gy), bf16_round(np.zeros((n, N), np.float32)), bf16_round(w2))
+    assert rel(gi, gi_r) < 2e-5
+
+
 def test_halo_conv_without_colours_and_deterministic(shell):
     """A KernelMap built from reference lists has no grids (no lane colours): same results."""
     g, ins, outs, km = shell

@@ -49,3 +49,8 @@ out["phase_wait"] = float(np.median(t[10, 5:60] - t[9, 5:60]))
 out["epi_tile_period"] = float(np.median(np.diff(t[6, 5:60])))
 out["loader_phase_period"] = float(np.median(np.diff(t[8, 5:60])))
 print(json.dumps(out))
+# loader: 5 phase top, 8 after the id / buffer waits, 11 after the cp.async loop
+ld = {"loader_top_to_after_waits": float(np.median(t[8, 5:60] - t[5, 5:60])),
+      "loader_cp_async_loop": float(np.median(t[11, 5:60] - t[8, 5:60])),
+      "loader_after_loop_to_next_top": float(np.median(t[5, 6:61] - t[11, 5:60]))}
+print(json.dumps(ld))
