@@ -109,6 +109,16 @@ int fvdb_build_plan2(const int64_t* coords, int64_t n, const int64_t* pending_no
                      size_t workspace_bytes, int64_t* counts, int64_t* detail, void* stream);
 int fvdb_build_fill(void* workspace, size_t workspace_bytes, int64_t n, const int64_t* counts,
                     const fvdb_grid_arrays* out, void* stream);
+/* Coarsen by 2 from the fine grid's leaves (build.py:325-339): one sort key per fine LEAF instead of one per
+ * voxel.  The result is bit-identical to fvdb_build_* over unique(ijk // 2).  leaf_origins int64 [n_leaf,3],
+ * leaf_masks [n_leaf,8] (device, the fine grid's arrays).  plan synchronizes once and writes counts[5] =
+ * {num_upper (1), num_lower, num_leaf, num_voxels, coarse tile key}; FVDB_ERR_UNSUPPORTED when the coarse
+ * voxels span several root tiles (use the coordinate build).  fill writes the arrays (same workspace). */
+size_t fvdb_coarsen2_workspace_bytes(int64_t n_leaf);
+int fvdb_coarsen2_plan(const int64_t* leaf_origins, const uint64_t* leaf_masks, int64_t n_leaf, void* workspace,
+                       size_t workspace_bytes, int64_t* counts, void* stream);
+int fvdb_coarsen2_fill(void* workspace, size_t workspace_bytes, int64_t n_leaf, const int64_t* counts,
+                       const fvdb_grid_arrays* out, void* stream);
 /* Batched build: B grids from one jagged coordinate array (element b = rows [row_off[b], row_off[b+1]),
  * row_off DEVICE int64 [B+1], every element non-empty) in one device pass.  Each element's grid is
  * bit-identical to its standalone build.  counts (host) [B][4] = per-element {num_upper, num_lower,

@@ -269,11 +269,38 @@ def build_from_points(points, transform, name=""):
     return _build_device(c, transform, name, stats, pending=out[3 * n:], points=p), stats
 
 
+def _coarsen2_leaves(grid, tc):
+    """coarsen(grid, 2) from the fine leaves (fvdb_coarsen2_*): one sort key per fine leaf.  None when the coarse
+    grid spans several root tiles (the coordinate build handles those)."""
+    L = _lib.lib()
+    nl = grid.num_leaf_nodes
+    dev = grid.leaf_origins.device
+    st = _lib.stream_ptr()
+    wsb = L.fvdb_coarsen2_workspace_bytes(nl)
+    ws = _lib.workspace(wsb, dev)
+    counts = (C.c_int64 * 5)()
+    rc = L.fvdb_coarsen2_plan(grid.leaf_origins.data_ptr(), grid.leaf_masks.data_ptr(), nl, ws.data_ptr(), wsb,
+                              counts, st)
+    if rc == _lib.FVDB_ERR_UNSUPPORTED:
+        return None
+    _lib.check(rc, "coarsen2_plan")
+    cnt = [int(counts[k]) for k in range(4)]
+    arrays = _alloc_arrays(cnt, dev)
+    ga = _lib.GridArrays(**{f: arrays[f].data_ptr() for f in ARRAY_FIELDS})
+    _lib.check(L.fvdb_coarsen2_fill(ws.data_ptr(), wsb, nl, counts, C.byref(ga), st), "coarsen2_fill")
+    return IndexGrid(num_voxels=cnt[3], transform=tc, name=grid.name, **arrays)
+
+
 def coarsen(grid, factor):
     """Coarse voxel active iff any fine child is active (build.py:325-339)."""
     factor = int(factor)
     if factor < 1:
         raise ValueError("coarsening factor must be >= 1")
+    if factor == 2 and grid.num_voxels > 0:
+        t = grid.transform
+        g = _coarsen2_leaves(grid, VoxelTransform(t.voxel_size * 2, t.origin + t.voxel_size / 2.0))
+        if g is not None:
+            return g
     coords = grid.active_coords()
     if factor > 1 and coords.shape[0]:
         out = torch.empty_like(coords)

@@ -98,21 +98,57 @@ __global__ void k_decompress_keys(uint64_t* __restrict__ keys, const int* __rest
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) keys[r] = tc.dec(keys[r]);
 }
 
-// per-warp min / max of the lo / hi tile fields of one axis, folded into the scalars
-__device__ __forceinline__ void fold_fields(BuildScalars* sc, const uint32_t (&f)[3], bool valid) {
+// min / max of the lo / hi tile fields of each axis: per-thread running values (fields_acc), reduced per warp,
+// then per block in shared memory, then one global atomic per block and value (fold_fields_block).  Per-warp
+// global atomics on the 12 scalars every 32 rows serialised k_tile_keys (66 us for 1M rows).
+struct FieldAcc {
+    uint32_t lmin[3], lmax[3], hmin[3], hmax[3];
+    __device__ void init() {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lmin[a] = hmin[a] = 0xFFFFFFFFu;
+            lmax[a] = hmax[a] = 0u;
+        }
+    }
+    __device__ void add(const uint32_t (&f)[3]) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (f[a] < (1u << 20)) {
+                lmin[a] = min(lmin[a], f[a]);
+                lmax[a] = max(lmax[a], f[a]);
+            } else {
+                hmin[a] = min(hmin[a], f[a]);
+                hmax[a] = max(hmax[a], f[a]);
+            }
+        }
+    }
+};
+// block-level fold into the scalars; every thread of the block must call it (contains __syncthreads)
+__device__ __forceinline__ void fold_fields_block(BuildScalars* sc, const FieldAcc& acc) {
+    __shared__ uint32_t s[12];
+    if (threadIdx.x < 12) s[threadIdx.x] = (threadIdx.x % 4 == 0 || threadIdx.x % 4 == 2) ? 0xFFFFFFFFu : 0u;
+    __syncthreads();
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const bool lo = valid && f[a] < (1u << 20), hi = valid && f[a] >= (1u << 20);
-        const uint32_t lmin = __reduce_min_sync(0xffffffffu, lo ? f[a] : 0xFFFFFFFFu);
-        const uint32_t lmax = __reduce_max_sync(0xffffffffu, lo ? f[a] : 0u);
-        const uint32_t hmin = __reduce_min_sync(0xffffffffu, hi ? f[a] : 0xFFFFFFFFu);
-        const uint32_t hmax = __reduce_max_sync(0xffffffffu, hi ? f[a] : 0u);
+        const uint32_t lmin = __reduce_min_sync(0xffffffffu, acc.lmin[a]);
+        const uint32_t lmax = __reduce_max_sync(0xffffffffu, acc.lmax[a]);
+        const uint32_t hmin = __reduce_min_sync(0xffffffffu, acc.hmin[a]);
+        const uint32_t hmax = __reduce_max_sync(0xffffffffu, acc.hmax[a]);
         if ((threadIdx.x & 31) == 0) {
-            if (lmin != 0xFFFFFFFFu) atomicMin(&sc->lo_min[a], lmin);
-            if (lmax) atomicMax(&sc->lo_max[a], lmax);
-            if (hmin != 0xFFFFFFFFu) atomicMin(&sc->hi_min[a], hmin);
-            if (hmax) atomicMax(&sc->hi_max[a], hmax);
+            atomicMin(&s[4 * a + 0], lmin);
+            atomicMax(&s[4 * a + 1], lmax);
+            atomicMin(&s[4 * a + 2], hmin);
+            atomicMax(&s[4 * a + 3], hmax);
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < 12) {
+        const int a = threadIdx.x / 4, k = threadIdx.x % 4;
+        const uint32_t v = s[threadIdx.x];
+        if (k == 0 && v != 0xFFFFFFFFu) atomicMin(&sc->lo_min[a], v);
+        if (k == 1 && v) atomicMax(&sc->lo_max[a], v);
+        if (k == 2 && v != 0xFFFFFFFFu) atomicMin(&sc->hi_min[a], v);
+        if (k == 3 && v) atomicMax(&sc->hi_max[a], v);
     }
 }
 
@@ -180,6 +216,8 @@ __global__ void k_tile_keys(const int64_t* __restrict__ coords, int64_t n, uint6
     uint64_t k_or = 0, k_and = ~0ull;
     const int64_t lim = (int64_t)1 << 30;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    FieldAcc acc;
+    acc.init();
     for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x; r0 < n; r0 += stride) {  // warp-uniform trip count
         const int64_t r = r0 + threadIdx.x;
         uint32_t f[3] = {0u, 0u, 0u};
@@ -194,9 +232,10 @@ __global__ void k_tile_keys(const int64_t* __restrict__ coords, int64_t n, uint6
             f[0] = (uint32_t)((key >> 42) & 0x1FFFFF);
             f[1] = (uint32_t)((key >> 21) & 0x1FFFFF);
             f[2] = (uint32_t)(key & 0x1FFFFF);
+            acc.add(f);
         }
-        fold_fields(sc, f, r < n);
     }
+    fold_fields_block(sc, acc);
     typedef cub::BlockReduce<uint64_t, kThreads> BR;
     __shared__ typename BR::TempStorage t1;
     uint64_t bo = BR(t1).Reduce(k_or, [](uint64_t a, uint64_t b) { return a | b; });
@@ -349,6 +388,8 @@ __global__ void k_tile_keys_batch(const int64_t* __restrict__ coords, int64_t n,
     uint64_t k_or = 0, k_and = ~0ull;
     const int64_t lim = (int64_t)1 << 30;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    FieldAcc acc;
+    acc.init();
     for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x; r0 < n; r0 += stride) {  // warp-uniform trip count
         const int64_t r = r0 + threadIdx.x;
         uint32_t f[3] = {0u, 0u, 0u};
@@ -364,9 +405,10 @@ __global__ void k_tile_keys_batch(const int64_t* __restrict__ coords, int64_t n,
             f[0] = (uint32_t)((key >> 42) & 0x1FFFFF);
             f[1] = (uint32_t)((key >> 21) & 0x1FFFFF);
             f[2] = (uint32_t)(key & 0x1FFFFF);
+            acc.add(f);
         }
-        fold_fields(sc, f, r < n);
     }
+    fold_fields_block(sc, acc);
     typedef cub::BlockReduce<uint64_t, kThreads> BR;
     __shared__ typename BR::TempStorage t1;
     uint64_t bo = BR(t1).Reduce(k_or, [](uint64_t a, uint64_t b) { return a | b; });
@@ -927,5 +969,273 @@ extern "C" int fvdb_quantize_points(const double* points, int64_t n, const doubl
         *detail = (int64_t)hb;
         return FVDB_ERR_NONFINITE;
     }
+    return FVDB_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// coarsen by 2 from the fine LEAVES (build.py:325-339: coarse voxel active iff any fine child is)
+//
+// A fine leaf (8^3 at origin o) maps onto the 4^3 sub-block at (o >> 1) of the coarse leaf at (o >> 1) & ~7.
+// The fine leaves are sorted by that coarse leaf's key (one key per fine LEAF, ~100x fewer than the voxel
+// keys build_from_coords(unique(ijk // 2)) sorts), their downsampled sub-block masks are OR-ed into the
+// coarse leaves (OR commutes: deterministic) and the coarse arrays are registered leaf-parallel.  The voxel
+// order is the build's (leaf key, then in-leaf offset), so the grid is bit-identical to the coordinate build.
+// Coarse grids spanning several root tiles return FVDB_ERR_UNSUPPORTED (the caller takes the coordinate build).
+// ---------------------------------------------------------------------------------------------
+namespace fvdb {
+namespace {
+
+struct CoarsenWs {
+    uint64_t *key, *key_alt;
+    int *idx, *idx_alt;
+    int *leaf_id, *lower_id;
+    uint64_t* masks;          // [nl][8] coarse leaf masks by coarse leaf id (first n_leaf used)
+    int64_t *pop, *incl;      // [nl] popcounts by coarse leaf id (0 past n_leaf) and their inclusive scan
+    unsigned long long* tk;   // [2] OR / AND of the coarse tile keys
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+
+size_t coarsen_cub_bytes(int n) {
+    size_t a = 0, b = 0, c = 0;
+    cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
+    cub::DoubleBuffer<int> vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, n, 0, 27);
+    cub::DeviceScan::InclusiveSum(nullptr, b, (int*)nullptr, (int*)nullptr, n);
+    cub::DeviceScan::InclusiveSum(nullptr, c, (int64_t*)nullptr, (int64_t*)nullptr, n);
+    size_t m = a > b ? a : b;
+    return m > c ? m : c;
+}
+
+template <class C>
+void carve_coarsen(C& c, int64_t n, CoarsenWs* w) {
+    const size_t m = (size_t)(n > 0 ? n : 1);
+    const size_t cb = coarsen_cub_bytes((int)m);
+    if constexpr (std::is_same_v<C, Carver>) {
+        w->key = c.template take<uint64_t>(m);
+        w->key_alt = c.template take<uint64_t>(m);
+        w->idx = c.template take<int>(m);
+        w->idx_alt = c.template take<int>(m);
+        w->leaf_id = c.template take<int>(m);
+        w->lower_id = c.template take<int>(m);
+        w->masks = c.template take<uint64_t>(8 * m);
+        w->pop = c.template take<int64_t>(m);
+        w->incl = c.template take<int64_t>(m);
+        w->tk = c.template take<unsigned long long>(2);
+        w->cub_tmp = c.template take<char>(cb);
+        w->cub_bytes = cb;
+    } else {
+        c.template take<uint64_t>(m);
+        c.template take<uint64_t>(m);
+        for (int i = 0; i < 4; ++i) c.template take<int>(m);
+        c.template take<uint64_t>(8 * m);
+        c.template take<int64_t>(m);
+        c.template take<int64_t>(m);
+        c.template take<unsigned long long>(2);
+        c.template take<char>(cb);
+    }
+}
+
+__global__ void k_coarsen_init(unsigned long long* tk) {
+    tk[0] = 0ull;
+    tk[1] = ~0ull;
+}
+
+// per fine leaf: coarse leaf key (rank 0: upper << 12 | lower), payload = fine leaf id, coarse tile key OR / AND
+__global__ void k_coarsen_keys(const int64_t* __restrict__ origins, int n, uint64_t* __restrict__ key,
+                               int* __restrict__ idx, unsigned long long* __restrict__ tk) {
+    uint64_t k_or = 0, k_and = ~0ull;
+    for (int l0 = blockIdx.x * blockDim.x; l0 < n; l0 += gridDim.x * blockDim.x) {  // warp-uniform trips
+        const int l = l0 + threadIdx.x;
+        if (l < n) {
+            const int64_t ci = (origins[3 * l] >> 1) & ~(int64_t)7, cj = (origins[3 * l + 1] >> 1) & ~(int64_t)7,
+                          ck = (origins[3 * l + 2] >> 1) & ~(int64_t)7;
+            key[l] = ((uint64_t)upper_off(ci, cj, ck) << 12) | lower_off(ci, cj, ck);
+            idx[l] = l;
+            const uint64_t t = tile_key(ci, cj, ck);
+            k_or |= t;
+            k_and &= t;
+        }
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+        k_or |= __shfl_xor_sync(0xffffffffu, k_or, s);
+        k_and &= __shfl_xor_sync(0xffffffffu, k_and, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(&tk[0], (unsigned long long)k_or);
+        atomicAnd(&tk[1], (unsigned long long)k_and);
+    }
+}
+
+// head flags over the sorted coarse keys: leaf (key changes) and lower (key >> 12 changes)
+__global__ void k_coarsen_heads(const uint64_t* __restrict__ key, int n, int* __restrict__ leaf_h,
+                                int* __restrict__ lower_h) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t v = key[i], p = i ? key[i - 1] : ~v;
+        leaf_h[i] = v != p;
+        lower_h[i] = (v >> 12) != (p >> 12);
+    }
+}
+
+// the 4^3 downsample of fine words 2a, 2a+1 (bits y << 3 | z), placed at (sy + b) << 3 | (sz + c)
+__device__ __forceinline__ uint64_t coarsen_word(uint64_t w0, uint64_t w1, int sy, int sz) {
+    uint64_t m = w0 | w1;
+    m |= m >> 1;  // bit (y, 2c) |= (y, 2c + 1)
+    m |= m >> 8;  // bit (2b, z) |= (2b + 1, z)
+    uint64_t out = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            out |= ((m >> (16 * b + 2 * c)) & 1ull) << (((sy + b) << 3) | (sz + c));
+    return out;
+}
+
+// OR every fine leaf's downsampled sub-block into its coarse leaf (masks zeroed beforehand)
+__global__ void k_coarsen_or(const int* __restrict__ idx, int n, const int* __restrict__ leaf_id,
+                             const int64_t* __restrict__ origins, const uint64_t* __restrict__ fmasks,
+                             uint64_t* __restrict__ masks) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int f = idx[i], cl = leaf_id[i] - 1;
+        const int sx = (int)((origins[3 * f] >> 1) & 7), sy = (int)((origins[3 * f + 1] >> 1) & 7),
+                  sz = (int)((origins[3 * f + 2] >> 1) & 7);
+        const uint64_t* fm = fmasks + 8 * (int64_t)f;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const uint64_t w = coarsen_word(fm[2 * a], fm[2 * a + 1], sy, sz);
+            if (w) atomicOr((unsigned long long*)&masks[8 * (int64_t)cl + sx + a], (unsigned long long)w);
+        }
+    }
+}
+
+__global__ void k_coarsen_pop(const uint64_t* __restrict__ masks, int n, const int* __restrict__ n_leaf,
+                              int64_t* __restrict__ pop) {
+    const int nl = *n_leaf;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        int64_t p = 0;
+        if (j < nl)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) p += __popcll(masks[8 * (int64_t)j + t]);
+        pop[j] = p;
+    }
+}
+
+// coarse arrays from the sorted entries that head a coarse leaf (k_register's formulas at leaf granularity)
+__global__ void k_coarsen_register(const uint64_t* __restrict__ key, int n, const int* __restrict__ leaf_id,
+                                   const int* __restrict__ lower_id, const uint64_t* __restrict__ masks,
+                                   const int64_t* __restrict__ pop, const int64_t* __restrict__ incl, uint64_t tkey,
+                                   fvdb_grid_arrays o, int64_t n_leaf, int64_t n_lower) {
+    const int64_t ox = tile_field_origin(tkey, 42), oy = tile_field_origin(tkey, 21), oz = tile_field_origin(tkey, 0);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t v = key[i], p = i ? key[i - 1] : ~v;
+        if (v == p) continue;  // not a coarse leaf head
+        const int leaf = leaf_id[i] - 1;
+        const uint32_t up = (uint32_t)((v >> 12) & 0x7FFF), lo = (uint32_t)(v & 0xFFF);
+        const int64_t lx = ox + ((int64_t)((up >> 10) & 31) << 7), ly = oy + ((int64_t)((up >> 5) & 31) << 7),
+                      lz = oz + ((int64_t)(up & 31) << 7);
+        o.leaf_keys[leaf] = v;
+        o.leaf_offset_in_lower[leaf] = (uint16_t)lo;
+        o.leaf_value_offset[leaf] = (uint64_t)(incl[leaf] - pop[leaf]) + 1;
+        o.leaf_origins[3 * (int64_t)leaf + 0] = lx + ((int64_t)((lo >> 8) & 15) << 3);
+        o.leaf_origins[3 * (int64_t)leaf + 1] = ly + ((int64_t)((lo >> 4) & 15) << 3);
+        o.leaf_origins[3 * (int64_t)leaf + 2] = lz + ((int64_t)(lo & 15) << 3);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) o.leaf_masks[8 * (int64_t)leaf + t] = masks[8 * (int64_t)leaf + t];
+        if ((v >> 12) == (p >> 12)) continue;  // not a lower head
+        const int lower = lower_id[i] - 1;
+        o.lower_child_starts[lower] = leaf;
+        o.lower_offset_in_upper[lower] = (uint16_t)up;
+        o.lower_origins[3 * (int64_t)lower + 0] = lx;
+        o.lower_origins[3 * (int64_t)lower + 1] = ly;
+        o.lower_origins[3 * (int64_t)lower + 2] = lz;
+        if (i != 0) continue;  // the single upper node
+        o.upper_child_starts[0] = 0;
+        o.tile_keys[0] = tkey;
+        o.upper_origins[0] = ox;
+        o.upper_origins[1] = oy;
+        o.upper_origins[2] = oz;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        o.lower_child_starts[n_lower] = n_leaf;
+        o.upper_child_starts[1] = n_lower;
+    }
+}
+
+}  // namespace
+}  // namespace fvdb
+
+extern "C" size_t fvdb_coarsen2_workspace_bytes(int64_t n_leaf) {
+    Sizer s;
+    CoarsenWs w;
+    carve_coarsen(s, n_leaf, &w);
+    return s.used + 256;
+}
+
+extern "C" int fvdb_coarsen2_plan(const int64_t* leaf_origins, const uint64_t* leaf_masks, int64_t n_leaf,
+                                  void* workspace, size_t ws_bytes, int64_t* counts, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n_leaf <= 0 || n_leaf >= (int64_t)INT32_MAX / 8) return FVDB_ERR_INVALID;
+    Carver c(workspace, ws_bytes);
+    CoarsenWs w;
+    carve_coarsen(c, n_leaf, &w);
+    if (!c.ok()) return FVDB_ERR_WORKSPACE;
+    const int n = (int)n_leaf, g = grid_for(n);
+    k_coarsen_init<<<1, 1, 0, st>>>(w.tk);
+    k_coarsen_keys<<<g, kThreads, 0, st>>>(leaf_origins, n, w.key, w.idx, w.tk);
+    FVDB_LAUNCH_CHECK();
+    cub::DoubleBuffer<uint64_t> kb(w.key, w.key_alt);
+    cub::DoubleBuffer<int> vb(w.idx, w.idx_alt);
+    size_t tb = w.cub_bytes;
+    FVDB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, kb, vb, n, 0, 27, st));
+    // the sorted arrays stay where the sort left them: copy them to the primary buffers for the fill
+    if (kb.Current() != w.key) FVDB_CUDA_TRY(cudaMemcpyAsync(w.key, kb.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    if (vb.Current() != w.idx) FVDB_CUDA_TRY(cudaMemcpyAsync(w.idx, vb.Current(), n * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    k_coarsen_heads<<<g, kThreads, 0, st>>>(w.key, n, w.leaf_id, w.lower_id);
+    FVDB_LAUNCH_CHECK();
+    int* ids[2] = {w.leaf_id, w.lower_id};
+    for (int t = 0; t < 2; ++t) {
+        tb = w.cub_bytes;
+        FVDB_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, ids[t], ids[t], n, st));
+    }
+    FVDB_CUDA_TRY(cudaMemsetAsync(w.masks, 0, (size_t)n * 64, st));
+    k_coarsen_or<<<g, kThreads, 0, st>>>(w.idx, n, w.leaf_id, leaf_origins, leaf_masks, w.masks);
+    FVDB_LAUNCH_CHECK();
+    k_coarsen_pop<<<g, kThreads, 0, st>>>(w.masks, n, w.leaf_id + (n - 1), w.pop);
+    FVDB_LAUNCH_CHECK();
+    tb = w.cub_bytes;
+    FVDB_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, w.pop, w.incl, n, st));
+    struct {
+        unsigned long long tk[2];
+        int last[2];
+        int64_t nv;
+    } h;
+    FVDB_CUDA_TRY(cudaMemcpyAsync(h.tk, w.tk, sizeof(h.tk), cudaMemcpyDeviceToHost, st));
+    for (int t = 0; t < 2; ++t)
+        FVDB_CUDA_TRY(cudaMemcpyAsync(&h.last[t], ids[t] + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&h.nv, w.incl + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h.tk[0] != h.tk[1]) return FVDB_ERR_UNSUPPORTED;  // several coarse root tiles
+    counts[0] = 1;
+    counts[1] = h.last[1];
+    counts[2] = h.last[0];
+    counts[3] = h.nv;
+    counts[4] = (int64_t)h.tk[0];
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_coarsen2_fill(void* workspace, size_t ws_bytes, int64_t n_leaf, const int64_t* counts,
+                                  const fvdb_grid_arrays* out, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n_leaf <= 0 || n_leaf >= (int64_t)INT32_MAX / 8) return FVDB_ERR_INVALID;
+    Carver c(workspace, ws_bytes);
+    CoarsenWs w;
+    carve_coarsen(c, n_leaf, &w);
+    if (!c.ok()) return FVDB_ERR_WORKSPACE;
+    const int n = (int)n_leaf, g = grid_for(n);
+    k_coarsen_register<<<g, kThreads, 0, st>>>(w.key, n, w.leaf_id, w.lower_id, w.masks, w.pop, w.incl,
+                                               (uint64_t)counts[4], *out, counts[2], counts[1]);
+    FVDB_LAUNCH_CHECK();
+    k_leaf_prefix<<<grid_for(counts[2]), kThreads, 0, st>>>(out->leaf_masks, counts[2], out->leaf_prefix);
+    FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

@@ -232,3 +232,25 @@ def test_probe_with_and_without_node_tables(golden_grids, name):
                                               _lib.stream_ptr()), "coord_to_index")
     assert torch.equal(with_t, out)
     assert np.array_equal(with_t.cpu().numpy(), golden_grids[f"{name}/probe_index"])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_coarsen2_from_leaves_matches_coordinate_build(seed):
+    """coarsen(g, 2) runs from the fine leaves (fvdb_coarsen2_*); it must equal the coordinate build of
+    unique(ijk // 2) in every array, including negative coordinates (arithmetic floor) and sparse / dense mixes."""
+    from paper_2407_01781_b200.build import _coarsen2_leaves
+    rng = np.random.default_rng(seed)
+    c = np.concatenate([rng.integers(-300, 300, size=(20000, 3)),
+                        sphere_shell_coords(60, band=1.5) - 40,
+                        rng.integers(-9, 9, size=(3000, 3))])
+    # one root tile (negative coordinates: tile -1) for the leaf path; the multi-tile input falls back
+    multi, _ = P.build_from_coords(c)
+    assert _coarsen2_leaves(multi, multi.transform) is None
+    g, _ = P.build_from_coords(c - 2000)
+    fast = _coarsen2_leaves(g, g.transform)
+    assert fast is not None
+    ref, _ = P.build_from_coords(np.floor_divide(g.active_coords().cpu().numpy(), 2))
+    a, b = fast.to_numpy(), ref.to_numpy()
+    for f in FIELDS:
+        assert a[f].dtype == b[f].dtype and np.array_equal(a[f], b[f]), f
+    assert fast.num_voxels == ref.num_voxels
