@@ -297,6 +297,16 @@ int fvdb_halo_plan_count(const int32_t* nbr, int64_t ld, int64_t n_out, const ui
 /* fill pass: writes halo_rows, perm, tile_rec */
 int fvdb_halo_plan_fill(const int32_t* nbr, int64_t ld, int64_t n_out, const uint8_t* color_in,
                         const uint8_t* q_out, const fvdb_halo_plan* plan, void* stream);
+/* Single-pass plan (the default; no count pass, no host read-back): per tile, dedupe + phase choice + slot
+ * ranking by ascending row, then one atomicAdd on *counter (device int32, zeroed here) takes the tile's slot
+ * range, so tile_base is in allocation order.  halo_rows must hold halo_rows_capacity >=
+ * num_tiles * FVDB_HALO_TILE_SLOTS_MAX slots (the per-tile worst case); the used prefix is *counter.
+ * Table rows must be < n_in < 2^27 and num_tiles * FVDB_HALO_TILE_SLOTS_MAX < 2^31 (else FVDB_ERR_UNSUPPORTED:
+ * use the count / fill passes). */
+#define FVDB_HALO_TILE_SLOTS_MAX (2 * 27 * 128 + 27 * 8)
+int fvdb_halo_plan_build(const int32_t* nbr, int64_t ld, int64_t n_out, int64_t n_in, const uint8_t* color_in,
+                         const uint8_t* q_out, const fvdb_halo_plan* plan, int64_t halo_rows_capacity,
+                         int32_t* counter, void* stream);
 /* B images for the halo kernel: as fvdb_pack_weights_umma with the K index permuted to the
  * TMEM A layout the kernel's tcgen05.st produces, followed by copies of offsets 0..6 so that any
  * run of up to 8 consecutive offsets (mod 27) is one contiguous TMA copy.

@@ -29,6 +29,7 @@ FVDB_ERR_UNSUPPORTED = -7
 DTYPE_F32, DTYPE_F64, DTYPE_BF16 = 0, 1, 2
 NBR_ALIGN = 512  # FVDB_NBR_ALIGN
 HALO_IMAGES = 34  # FVDB_HALO_IMAGES
+HALO_TILE_SLOTS_MAX = 2 * 27 * 128 + 27 * 8  # FVDB_HALO_TILE_SLOTS_MAX
 HALO_REC_BYTES = 7424  # FVDB_HALO_REC_BYTES
 
 _vp, _i64, _i32, _sz = C.c_void_p, C.c_int64, C.c_int, C.c_size_t
@@ -108,6 +109,7 @@ SIGNATURES = {
     "fvdb_halo_plan_workspace_bytes": (_sz, [_i64]),
     "fvdb_halo_plan_count": (_i32, [_vp, _i64, _i64, _vp, C.POINTER(HaloPlan), C.POINTER(_i64), _vp, _sz, _vp]),
     "fvdb_halo_plan_fill": (_i32, [_vp, _i64, _i64, _vp, _vp, C.POINTER(HaloPlan), _vp]),
+    "fvdb_halo_plan_build": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, C.POINTER(HaloPlan), _i64, _vp, _vp]),
     "fvdb_pack_weights_halo": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp]),
     "fvdb_conv_halo_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, C.POINTER(HaloPlan), _i64, _vp, _i32, _vp]),
     "fvdb_expand_coords": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),

@@ -81,6 +81,9 @@ def _kernel_weights(kernel):
     return kernel.weights if isinstance(kernel, ConvKernel) else kernel
 
 
+_TWO_PASS_PLAN = os.environ.get("FVDB_PLAN_TWO_PASS", "0") == "1"
+
+
 class HaloPlan:
     """Device halo plan of one neighbour table for one kernel capacity (include/fvdb_b200.h)."""
 
@@ -97,22 +100,34 @@ class HaloPlan:
              "tile_rec": z(T, _lib.HALO_REC_BYTES, dt=torch.uint8)}
         c = _lib.HaloPlan(T, cap, *(t[k].data_ptr() for k in ("tile_level", "tile_base", "phase")), None,
                           t["perm"].data_ptr(), t["tile_rec"].data_ptr())
-        wsb = L.fvdb_halo_plan_workspace_bytes(n)
-        ws = _lib.workspace(wsb, dev)
-        total = C.c_int64(0)
         st = _lib.stream_ptr()
         cp = _lib.ptr(ci)
-        _lib.check(L.fvdb_halo_plan_count(table.t.data_ptr(), table.ld, n, cp, C.byref(c), C.byref(total),
-                                          ws.data_ptr(), wsb, st), "halo_plan_count")
-        t["halo_rows"] = z(max(int(total.value), 8))
-        c.halo_rows = t["halo_rows"].data_ptr()
-        _lib.check(L.fvdb_halo_plan_fill(table.t.data_ptr(), table.ld, n, cp, _lib.ptr(qo), C.byref(c), st),
-                   "halo_plan_fill")
+        one_pass = (not _TWO_PASS_PLAN and table.rows_bound is not None and table.rows_bound < (1 << 27)
+                    and T * _lib.HALO_TILE_SLOTS_MAX < (1 << 31))
+        if not one_pass:  # count pass + host read-back of the exact total + fill pass
+            wsb = L.fvdb_halo_plan_workspace_bytes(n)
+            ws = _lib.workspace(wsb, dev)
+            total = C.c_int64(0)
+            _lib.check(L.fvdb_halo_plan_count(table.t.data_ptr(), table.ld, n, cp, C.byref(c), C.byref(total),
+                                              ws.data_ptr(), wsb, st), "halo_plan_count")
+            t["halo_rows"] = z(max(int(total.value), 8))
+            c.halo_rows = t["halo_rows"].data_ptr()
+            _lib.check(L.fvdb_halo_plan_fill(table.t.data_ptr(), table.ld, n, cp, _lib.ptr(qo), C.byref(c), st),
+                       "halo_plan_fill")
+        else:  # one pass, no read-back: worst-case row capacity, tiles allocate by a device counter
+            cap_rows = T * _lib.HALO_TILE_SLOTS_MAX
+            t["halo_rows"] = z(cap_rows)
+            t["used"] = z(1)
+            c.halo_rows = t["halo_rows"].data_ptr()
+            _lib.check(L.fvdb_halo_plan_build(table.t.data_ptr(), table.ld, n, table.rows_bound, cp, _lib.ptr(qo),
+                                              C.byref(c), cap_rows, t["used"].data_ptr(), st), "halo_plan_build")
         self.cap, self.tensors, self.c = cap, t, c
 
     @property
     def total_slots(self):
-        return int(self.tensors["halo_rows"].numel())
+        """Slots the tiles use (synchronises)."""
+        u = self.tensors.get("used")
+        return int(u.item()) if u is not None else int(self.tensors["halo_rows"].numel())
 
 
 class NbrTable:
@@ -123,9 +138,10 @@ class NbrTable:
     """
 
     __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
-                 "_masks", "sparse", "_steady", "_pairs", "exact_uses", "wgrad_uses")
+                 "_masks", "sparse", "_steady", "_pairs", "exact_uses", "wgrad_uses", "rows_bound")
 
     def __init__(self, t, n, colors_fn=None, counts=None):
+        self.rows_bound = None  # exclusive bound of the input rows in t (known: single-pass halo plans)
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
         self._colors_fn, self._colors, self._plans = colors_fn, None, {}
         self.uses = 0  # bf16 tensor-core convolutions run over this table (conv_impl "auto")
@@ -308,6 +324,8 @@ class KernelMap:
             table = NbrTable(t, self.num_out)
         if table.counts is None:
             table.counts = pair_counts
+        if table.rows_bound is None:
+            table.rows_bound = int(num_in)
         if table._colors_fn is None and grids is not None:
             table._colors_fn = _colors_fn(self._grids, self.stride, False)
         self.fwd = table
@@ -385,6 +403,7 @@ class KernelMap:
             self._bwd = NbrTable(t, self.num_in, _colors_fn(self._grids, self.stride, True) if self._grids else None,
                                  counts=self._counts)
             self._bwd.sparse = self.stride == 2  # fine voxel i pairs only offsets d with i - d even: <= 8 of 27
+            self._bwd.rows_bound = int(self.num_out)
         return self._bwd
 
     def _same_grids(self):
@@ -515,7 +534,7 @@ def halo_kernel_name(K: int, N: int) -> str:
     return f"k_conv_halo<{K},{N},bf16>"
 
 
-HALO_AFTER_USES = 4  # conv_impl "auto": uses of a table before its halo plan is built
+HALO_AFTER_USES = 3  # conv_impl "auto": uses of a table before its halo plan is built (plan ~ 1.2 gather convs)
 SORT_BELOW_DENSITY = 10.0  # gather kernel: signature-sort tables with fewer mean pairs per row
 
 
@@ -572,10 +591,11 @@ def conv_impl() -> str:
     * "auto" (default): the gather-GEMM kernel (conv_tc.cu) for a neighbour table's first
       ``HALO_AFTER_USES`` bf16 uses, then the halo-staged kernel (conv_halo.cu); immediately if the
       table already has a plan.  Sparse tables (``sig_sort_enabled``) always take the gather kernel over
-      their signature-sorted, offset-masked form (3x faster than the halo kernel there).  Building the plan costs ~3-6 gather convolutions (cfg2: 2.2 ms vs
-      0.67 ms per conv, saving ~0.3 ms per use), so it pays off for maps reused across layers and
-      training iterations, not for maps used once or twice (cfg4 rebuilds its maps every step and uses
-      each in one forward and one backward);
+      their signature-sorted, offset-masked form (3x faster than the halo kernel there).  Building the
+      plan (one pass, no host read-back) costs about what one use saves (cfg2: 0.40 ms; 0.66 ms gather vs
+      0.32 ms halo per conv), so it pays off for maps reused across layers and training iterations, not
+      for maps used once or twice (cfg4 rebuilds its maps every step and uses each in one forward and one
+      backward);
     * "halo" / "gather": always that kernel.
     """
     v = os.environ.get("FVDB_CONV_IMPL", "auto")

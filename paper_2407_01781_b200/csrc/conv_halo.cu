@@ -1755,6 +1755,235 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_fill_hash(const int32_t* 
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// single-pass plan (fvdb_halo_plan_build): no count pass, no host read-back.  Each tile dedupes its (phase, row)
+// keys in a shared-memory hash set (raising the phase count until every phase fits the capacity), sorts its
+// unique keys (only those: typically ~150-400, not the 27 x 128 entries) so slots follow ascending input rows,
+// takes its slot range with one atomicAdd on a global counter (tile_base: allocation order is arbitrary, the
+// kernel reads every tile's base) and writes rows, lane permutation and record.  halo_rows must hold
+// T * FVDB_HALO_TILE_SLOTS_MAX slots (the worst case of 2 x 27 x 128 + padding per tile).
+// ---------------------------------------------------------------------------------------------
+constexpr int kTileSlotsMax = 2 * 27 * kTileRows + 27 * 8;
+constexpr int kSortSmall = 4;  // 256 x 4 = 1024 unique keys sorted; more (dense 128-channel tiles) keep hash order
+constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
+using PlanSortSmall = cub::BlockRadixSort<uint32_t, kPlanThreads, kSortSmall, uint16_t>;
+// 32-bit keys (row << 5 | phase): input rows < 2^27 (fvdb_halo_plan_build rejects larger tables)
+struct PlanOneSmem {
+    uint32_t hkey[kHashSize];
+    uint16_t hslot[kHashSize];
+    uint8_t hcol[kHashSize];   // colour of the entry's row
+    uint16_t hpos[kPlanKeys];  // hash entry of element e = d * 128 + lane row (0xFFFF: no pair)
+    union {
+        typename PlanSortSmall::TempStorage sort;
+        typename PlanScan::TempStorage scan;
+    } tmp;
+    uint32_t ukey[kPlanThreads * kSortSmall];
+    uint16_t uh[kPlanThreads * kSortSmall];
+};
+
+__device__ __forceinline__ uint32_t plan_hash32(uint32_t k) { return (k * 0x9E3779B1u) >> (32 - kHashBits); }
+
+__global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* __restrict__ nbr, int64_t ld,
+                                                               int64_t n_out, const uint8_t* __restrict__ color,
+                                                               const uint8_t* __restrict__ q_out, fvdb_halo_plan P,
+                                                               int32_t* __restrict__ counter) {
+    extern __shared__ __align__(16) uint8_t psm[];
+    PlanOneSmem& S = *reinterpret_cast<PlanOneSmem*>(psm);
+    __shared__ PlanCounts pc;
+    __shared__ int perm[kTileRows];
+    __shared__ int wcnt[2][4];
+    __shared__ int nu, base_s;
+    __shared__ uint32_t rmax_s;
+    const int tile = blockIdx.x, tid = threadIdx.x;
+    int32_t row[kPlanItems];
+    uint8_t col[kPlanItems];
+    uint32_t rmax = 1;
+#pragma unroll
+    for (int k = 0; k < kPlanItems; ++k) {
+        const int e = tid + k * kPlanThreads;  // a warp's 32 entries: consecutive rows of one offset
+        row[k] = -1;
+        if (e < 27 * kTileRows) {
+            const int64_t o = (int64_t)tile * kTileRows + (e % kTileRows);
+            if (o < n_out) row[k] = __ldg(nbr + (int64_t)(e / kTileRows) * ld + o);
+        }
+        if (row[k] > (int32_t)rmax) rmax = (uint32_t)row[k];
+    }
+    // colours loaded up front (independent loads in flight together, not one dependent load per new key)
+#pragma unroll
+    for (int k = 0; k < kPlanItems; ++k) col[k] = (color && row[k] >= 0) ? (__ldg(color + row[k]) & 1) : 0;
+    if (tid == 0) rmax_s = 1;
+    // dedupe per (phase, row); raise the phase count until every phase's halo fits the capacity
+    int level = 1;
+    for (;; level *= 3) {
+        const int gsz = 27 / level;
+        for (int h = tid; h < kHashSize; h += kPlanThreads) S.hkey[h] = kEmpty32;
+        if (tid < 27) pc.cnt[0][tid] = pc.cnt[1][tid] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPlanItems; ++k) {
+            const int e = tid + k * kPlanThreads;
+            if (row[k] >= 0) {
+                const uint32_t key = ((uint32_t)row[k] << 5) | (uint32_t)((e / kTileRows) / gsz);
+                uint32_t h = plan_hash32(key);
+                for (;;) {
+                    const uint32_t prev = atomicCAS(&S.hkey[h], kEmpty32, key);
+                    if (prev == kEmpty32) {
+                        const int c = col[k];
+                        const int r = atomicAdd(&pc.cnt[c][key & 31], 1);
+                        S.hslot[h] = (uint16_t)(2 * r + c);  // hash order (kept when too many keys to sort)
+                        S.hcol[h] = (uint8_t)c;
+                        break;
+                    }
+                    if (prev == key) break;
+                    h = (h + 1) & (kHashSize - 1);
+                }
+                S.hpos[e] = (uint16_t)h;
+            } else if (e < 27 * kTileRows) {
+                S.hpos[e] = 0xFFFF;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0;
+            bool fits = true;
+            for (int gr = 0; gr < 27; ++gr) {
+                const int hh = gr < level ? 2 * max(pc.cnt[0][gr], pc.cnt[1][gr]) : 0;
+                pc.ghalo[gr] = (hh + 7) & ~7;
+                pc.goff[gr] = acc;
+                acc += pc.ghalo[gr];
+                fits = fits && pc.ghalo[gr] <= P.halo_cap;
+            }
+            pc.total = acc;
+            pc.rb = fits ? 1 : 0;  // (flag)
+            nu = 0;
+        }
+        __syncthreads();
+        if (level == 27 || pc.rb) break;
+        __syncthreads();
+    }
+    atomicMax(&rmax_s, rmax);
+    // unique keys -> (phase << rb) | row, sorted over rb + 5 bits: slots follow ascending rows per (phase, colour)
+    for (int h = tid; h < kHashSize; h += kPlanThreads) {
+        const uint32_t k = S.hkey[h];
+        if (k != kEmpty32) {
+            const int i = atomicAdd(&nu, 1);
+            if (i < kPlanThreads * kSortSmall) S.uh[i] = (uint16_t)h;
+        }
+    }
+    __syncthreads();
+    const int n_u = nu;
+    if (n_u <= kPlanThreads * kSortSmall) {
+        const int rb = 32 - __clz((int)rmax_s);
+        uint32_t key[kSortSmall];
+        uint16_t hv[kSortSmall];
+#pragma unroll
+        for (int k = 0; k < kSortSmall; ++k) {
+            const int i = tid * kSortSmall + k;
+            hv[k] = i < n_u ? S.uh[i] : (uint16_t)0;
+            const uint32_t u = i < n_u ? S.hkey[hv[k]] : kEmpty32;
+            key[k] = i < n_u ? ((u & 31) << rb) | (u >> 5) : kEmpty32;
+        }
+        __syncthreads();
+        PlanSortSmall(S.tmp.sort).Sort(key, hv, 0, rb + 5);
+        __syncthreads();
+        uint32_t packed = 0;
+        uint8_t c1[kSortSmall];
+#pragma unroll
+        for (int k = 0; k < kSortSmall; ++k) {
+            c1[k] = 0;
+            if (key[k] != kEmpty32) {
+                const int c = S.hcol[hv[k]];
+                c1[k] = (uint8_t)(1 + c);
+                packed += c ? (1u << 16) : 1u;
+            }
+        }
+        uint32_t excl;
+        PlanScan(S.tmp.scan).ExclusiveSum(packed, excl);
+#pragma unroll
+        for (int k = 0; k < kSortSmall; ++k) S.ukey[tid * kSortSmall + k] = key[k];
+        __syncthreads();
+        uint32_t run = excl;
+#pragma unroll
+        for (int k = 0; k < kSortSmall; ++k) {
+            const int e = tid * kSortSmall + k;
+            if (c1[k]) {
+                const int gr = (int)(key[k] >> rb);
+                if (e == 0 || (int)(S.ukey[e - 1] >> rb) != gr) {
+                    pc.gfirst[0][gr] = (int)(run & 0xFFFF);
+                    pc.gfirst[1][gr] = (int)(run >> 16);
+                }
+                run += (c1[k] == 2) ? (1u << 16) : 1u;
+            }
+        }
+        __syncthreads();
+        run = excl;
+#pragma unroll
+        for (int k = 0; k < kSortSmall; ++k) {
+            if (c1[k]) {
+                const int gr = (int)(key[k] >> rb), c = c1[k] - 1;
+                const int rank = (c ? (int)(run >> 16) : (int)(run & 0xFFFF)) - pc.gfirst[c][gr];
+                S.hslot[hv[k]] = (uint16_t)(2 * rank + c);
+                run += c ? (1u << 16) : 1u;
+            }
+        }
+    }
+    if (tid == 0) base_s = atomicAdd(counter, pc.total);
+    if (tid < 27) {
+        int32_t* ph = P.phase + ((int64_t)tile * 27 + tid) * 2;
+        ph[0] = pc.goff[tid];
+        ph[1] = pc.ghalo[tid];
+    }
+    __syncthreads();
+    const int base = base_s;
+    if (tid == 0) {
+        P.tile_level[tile] = level;
+        P.tile_base[tile] = base;
+    }
+    for (int s = tid; s < pc.total; s += kPlanThreads) P.halo_rows[base + s] = -1;
+    __syncthreads();
+    for (int h = tid; h < kHashSize; h += kPlanThreads) {
+        const uint32_t k = S.hkey[h];
+        if (k != kEmpty32) P.halo_rows[base + pc.goff[k & 31] + S.hslot[h]] = (int32_t)(k >> 5);
+    }
+    int f = -1, o = -1;
+    if (tid < kTileRows) {
+        perm[tid] = -1;
+        const int64_t oo = (int64_t)tile * kTileRows + tid;
+        if (oo < n_out) {
+            o = (int)oo;
+            f = q_out ? (q_out[oo] & 1) : 0;
+        }
+    }
+    const int w = tid >> 5, ln = tid & 31;
+    const uint32_t b0 = __ballot_sync(0xffffffffu, f == 0), b1 = __ballot_sync(0xffffffffu, f == 1);
+    if (w < 4 && ln == 0) {
+        wcnt[0][w] = __popc(b0);
+        wcnt[1][w] = __popc(b1);
+    }
+    __syncthreads();
+    if (f >= 0) {
+        const uint32_t bm = f ? b1 : b0;
+        int pos = __popc(bm & ((1u << ln) - 1u));
+        for (int ww = 0; ww < w; ++ww) pos += wcnt[f][ww];
+        const int n0 = wcnt[0][0] + wcnt[0][1] + wcnt[0][2] + wcnt[0][3];
+        const int n1 = wcnt[1][0] + wcnt[1][1] + wcnt[1][2] + wcnt[1][3];
+        const int m = min(n0, n1);
+        perm[pos < m ? 2 * pos + f : 2 * m + (pos - m)] = o;
+    }
+    __syncthreads();
+    if (tid < kTileRows) P.perm[(int64_t)tile * kTileRows + tid] = perm[tid];
+    uint8_t* rec = P.tile_rec + (int64_t)tile * kIdxBytes;
+    for (int e = tid; e < 27 * kTileRows; e += kPlanThreads) {
+        const int d = e / kTileRows, l = e % kTileRows;
+        const int oo = perm[l];
+        const uint16_t hp = oo >= 0 ? S.hpos[d * kTileRows + (oo - tile * kTileRows)] : (uint16_t)0xFFFF;
+        const uint16_t sl = hp != 0xFFFF ? S.hslot[hp] : kNoSlot;
+        reinterpret_cast<uint16_t*>(rec)[d * kTileRows + l] = sl;
+        const uint32_t none = __ballot_sync(0xffffffffu, sl == kNoSlot);
+        if ((tid & 31) == 0) reinterpret_cast<uint32_t*>(rec + 6912)[d * 4 + (l >> 5)] = none;
+    }
+}
+
 __global__ void k_parity_colors(const int64_t* __restrict__ c, int64_t n, int shift, uint8_t* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = (uint8_t)(((c[3 * i] >> shift) + (c[3 * i + 1] >> shift) + (c[3 * i + 2] >> shift)) & 1);
@@ -2025,6 +2254,25 @@ extern "C" int fvdb_halo_plan_fill(const int32_t* nbr, int64_t ld, int64_t n_out
     }
     FVDB_CUDA_TRY(cudaFuncSetAttribute(k_halo_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PlanSmem)));
     k_halo_fill<<<P.num_tiles, kPlanThreads, sizeof(PlanSmem), as_stream(stream)>>>(nbr, ld, n_out, color_in, q_out, P);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_halo_plan_build(const int32_t* nbr, int64_t ld, int64_t n_out, int64_t n_in, const uint8_t* color_in,
+                                    const uint8_t* q_out, const fvdb_halo_plan* plan, int64_t halo_rows_capacity,
+                                    int32_t* counter, void* stream) {
+    if (n_out <= 0) return FVDB_OK;
+    const fvdb_halo_plan& P = *plan;
+    const int T = (int)ceil_div(n_out, kTileRows);
+    if (P.num_tiles != T || P.halo_cap < 256 || P.halo_cap > 32768 || ld < n_out) return FVDB_ERR_INVALID;
+    if (halo_rows_capacity < (int64_t)T * kTileSlotsMax) return FVDB_ERR_WORKSPACE;
+    // 32-bit (row << 5 | phase) keys and int32 tile bases
+    if (n_in >= ((int64_t)1 << 27) || (int64_t)T * kTileSlotsMax >= ((int64_t)1 << 31)) return FVDB_ERR_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    FVDB_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int32_t), st));
+    FVDB_CUDA_TRY(cudaFuncSetAttribute(k_halo_plan_one, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(PlanOneSmem)));
+    k_halo_plan_one<<<T, kPlanThreads, sizeof(PlanOneSmem), st>>>(nbr, ld, n_out, color_in, q_out, P, counter);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }

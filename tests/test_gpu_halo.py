@@ -44,6 +44,12 @@ def check_plan(table, K, N):
     phase = t["phase"]
     hr = t["halo_rows"]
     masks = rec[:, 6912:6912 + 432].copy().view(np.uint32).reshape(T, 27, 4)
+    # tiles' slot ranges are disjoint (single-pass plans allocate them by a device counter, in any order)
+    ends = t["tile_base"] + np.array([max(int(phase[i, g, 0] + phase[i, g, 1]) for g in range(level[i]))
+                                      for i in range(T)])
+    order = np.argsort(t["tile_base"], kind="stable")
+    assert np.all(t["tile_base"][order][1:] >= ends[order][:-1]), "tile slot ranges overlap"
+    assert ends.max() <= hr.shape[0]
     for tile in range(T):
         gs = 27 // level[tile]
         for d in range(27):
