@@ -645,6 +645,9 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
 #ifndef FVDB_H4_NB
 #define FVDB_H4_NB 0
 #endif
+#ifndef FVDB_H4_WPRE
+#define FVDB_H4_WPRE 1
+#endif
 #ifndef FVDB_H4_SETS
 #define FVDB_H4_SETS 0
 #endif
@@ -669,8 +672,10 @@ struct Halo4Cfg {
     // A slots per set, one named barrier per slot (a builder is then at most ASL - 1 stages ahead of its issuer,
     // which the barrier ring requires); SETS * ASL <= 15 hardware barriers besides barrier 0
     static constexpr int ASL = cmin(FVDB_H4_ASL, (512 - DCOLS) / (SETS * ACOLS));
-    static constexpr int WSL = ASL + 1;  // weight slots per set (stage j + 1 loads while stage j builds)
-    static constexpr int WPRE = 1;
+    // streamed weights: stage j + WPRE's image loads right after stage j's A-slot wait, into one of WSL = ASL + WPRE
+    // slots per set (that wait proves stage j - ASL's MMAs, the slot's previous user, complete)
+    static constexpr int WPRE = FVDB_H4_WPRE;
+    static constexpr int WSL = ASL + WPRE;
     // all offset images resident in shared memory (loaded once per CTA) when they fit beside the halo:
     // no weight hand-off at all (K = 32 or N = 32: 54-112 KB)
     static constexpr bool RESIDENT = NIMG * B_BYTES <= 116 * 1024;
@@ -688,7 +693,7 @@ struct Halo4Cfg {
     // halo loader, weight loader, builders, one MMA issuer per set, epilogue
     static constexpr int THREADS = (2 + BUILDERS + SETS + EPI) * 32;
     static_assert(ASL >= 2 && SETS * ASL <= 15, "two A slots per set at least; named barriers");
-    static_assert(RESIDENT || WSL == ASL + 1, "streamed weights: stage j's A-slot wait frees stage j + 1's image slot");
+    static_assert(RESIDENT || WSL == ASL + WPRE, "streamed weights: stage j's A-slot wait frees stage j + WPRE's slot");
     static_assert(!PAIR || RESIDENT, "offset pairs assume resident images (the streamed loader walks offsets)");
     static_assert(CAP >= 256, "halo capacity must hold one offset phase");
     static_assert(DCOLS + SETS * ASL * ACOLS <= 512, "TMEM");
@@ -839,7 +844,8 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                          smem_u32(&bar_wfull[set][k]));
             }
         };
-        if (wl) load_w(0);
+        if (wl)
+            for (int j = 0; j < C::WPRE; ++j) load_w(j);
         uint32_t pc = 0, js = 0;
         for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
             const int level = P.tile_level[tile], gs = 27 / level;
@@ -868,7 +874,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                     const int sl[4] = {ok ? lr[0] : kNoSlot, ok ? lr[8] : kNoSlot, ok ? lr[16] : kNoSlot,
                                        ok ? lr[24] : kNoSlot};
                     mbar_wait(smem_u32(&bar_afree[set][ak]), (ause & 1) ^ 1);
-                    if (wl) load_w(js + 1);
+                    if (wl) load_w(js + C::WPRE);
                     tc_fence_after();
                     if (tr) trace(dbg, 0, js);
                     if (!(dbg & 2)) {

@@ -100,9 +100,9 @@ __device__ __forceinline__ int batch_of_leaf(const KmapBatch& kb, int64_t l) {
 // shared counters, then one 64-bit global atomic per (CTA, offset) (integer sums: deterministic).
 constexpr int kKmWarps = 8, kKmThreads = kKmWarps * 32;
 struct KmWarpSmem {
-    uint64_t mask[27][8];
-    int32_t base[27][8];   // row of the first voxel of mask word w of neighbour leaf e (input_base + value offset
-                           // - 1 + popcount of words < w): a probe's row is base + popcount below its bit
+    uint64_t mask[27][8];  // read as 32-bit words in the probe loop (32-bit shifts / popcounts: fewer instructions)
+    int32_t base[27][16];  // row of the first voxel of 32-bit mask word w of neighbour leaf e (input_base + value
+                           // offset - 1 + popcount of words < w): a probe's row is base + popcount below its bit
     int32_t nl[27];
     uint16_t pos[512];
     uint64_t own[8];
@@ -149,12 +149,15 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant
             S.mask[q >> 3][q & 7] = nl >= 0 ? gin.leaf_masks[8 * (int64_t)nl + (q & 7)] : 0ull;
         }
         __syncwarp();
-        if (lane < 27) {  // per-word row bases of neighbour leaf `lane`
+        if (lane < 27) {  // per-32-bit-word row bases of neighbour leaf `lane`
             int32_t acc = (int32_t)vo;
 #pragma unroll
             for (int w = 0; w < 8; ++w) {
-                S.base[lane][w] = acc;
-                acc += __popcll(S.mask[lane][w]);
+                const uint64_t m = S.mask[lane][w];
+                S.base[lane][2 * w] = acc;
+                acc += __popc((uint32_t)m);
+                S.base[lane][2 * w + 1] = acc;
+                acc += __popc((uint32_t)(m >> 32));
             }
         }
         // voxel positions in rank order: lane owns bits [16 lane, 16 lane + 16) of the leaf's mask
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant
 #pragma unroll
         for (int k = 0; k < 14; ++k) pc[k] = 0u;
         for (int r = lane; r < nvox; r += 32) {
+            int32_t* orow = out + r;
             const int m = S.pos[r];
             const int x = m >> 6, y = (m >> 3) & 7, z = m & 7;
             int ex[3], ey[3], ez[3], bx[3], by[3], bz[3];
@@ -199,10 +203,11 @@ __global__ void __launch_bounds__(kKmThreads) k_kernel_map(const __grid_constant
                 const int i = d / 9, j = (d / 3) % 3, k = d % 3;
                 const int e = ex[i] + ey[j] + ez[k];
                 const int bb = bx[i] | by[j] | bz[k];
-                const uint64_t word = S.mask[e][bb >> 6];
-                const uint64_t below = word & ((1ull << (bb & 63)) - 1ull);
-                const bool hit = (word >> (bb & 63)) & 1ull;
-                out[(int64_t)d * ld + r] = hit ? S.base[e][bb >> 6] + __popcll(below) : -1;
+                const uint32_t word = reinterpret_cast<const uint32_t*>(S.mask[e])[bb >> 5];
+                const uint32_t sh = word << (31 - (bb & 31));  // bit bb at the top, the bits below it beneath
+                const bool hit = (int32_t)sh < 0;
+                *orow = hit ? S.base[e][bb >> 5] + __popc(sh) - 1 : -1;
+                orow += ld;  // next offset's row: one 64-bit add, not a 64-bit multiply-add per probe
                 pc[d >> 1] += (uint32_t)hit << (16 * (d & 1));
             }
         }
@@ -397,7 +402,7 @@ extern "C" int fvdb_kernel_map_batch(const fvdb_grid_view* gin, const fvdb_grid_
         }
         const int64_t nl = kb.leaf_start[kb.B];
         if (nl == 0) continue;
-        const int64_t want = ceil_div(nl, kKmWarps), cap = (int64_t)sms * 3;  // 3 CTAs per SM are resident (80 regs)
+        const int64_t want = ceil_div(nl, kKmWarps), cap = (int64_t)sms * 3;  // 3 CTAs per SM are resident (80 regs; forcing 4 at 64 regs: same time)
         k_kernel_map<<<(unsigned)(want < cap ? want : cap), kKmThreads, 0, st>>>(
             kb, stride, nbr, ld, reinterpret_cast<unsigned long long*>(pair_counts), next_leaf + c0 / kMaxBatch);
     }
