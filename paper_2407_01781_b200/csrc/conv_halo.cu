@@ -120,6 +120,7 @@ __device__ __forceinline__ int h4_stage_count(bool pair, int level, int set, int
 
 constexpr int kImgExt = 34;  // weight images per layer: 27 offsets + 7 wrap-around copies (d = 0..6), so a
                              // batch of consecutive offsets is one TMA
+constexpr int kEpiBar = 15;  // k_conv_halo4: named barrier of the epilogue warps
 constexpr int kHalves = 2;   // builder halves: the warps of half h build the batches ab with ab % 2 == h
 
 // Pipeline: builders fill A slots (TMEM) batch by batch from the staged halo, the weight loader fills the
@@ -203,8 +204,13 @@ __device__ __forceinline__ long long global_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// compiled in only with -DFVDB_HALO_TRACE=1 (tools/build_variant.py): the runtime checks at every trace site were
+// ~7% of the lockstep kernel's issued instructions (ncu, profiles/r02_ncu_pair.md)
+#ifndef FVDB_HALO_TRACE
+#define FVDB_HALO_TRACE 0
+#endif
 __device__ __forceinline__ void trace(int dbg, int ch, uint32_t i) {
-    if ((dbg & 64) && blockIdx.x == 0 && i < (uint32_t)kTraceN) g_halo_trace[ch][i] = clock64();
+    if (FVDB_HALO_TRACE && (dbg & 64) && blockIdx.x == 0 && i < (uint32_t)kTraceN) g_halo_trace[ch][i] = clock64();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -692,7 +698,7 @@ struct Halo4Cfg {
     static constexpr int HC = N / 2;                          // columns per epilogue thread
     // halo loader, weight loader, builders, one MMA issuer per set, epilogue
     static constexpr int THREADS = (2 + BUILDERS + SETS + EPI) * 32;
-    static_assert(ASL >= 2 && SETS * ASL <= 15, "two A slots per set at least; named barriers");
+    static_assert(ASL >= 2 && SETS * ASL <= 14, "two A slots per set at least; named barriers 1..14 (15: epilogue)");
     static_assert(RESIDENT || WSL == ASL + WPRE, "streamed weights: stage j's A-slot wait frees stage j + WPRE's slot");
     static_assert(!PAIR || RESIDENT, "offset pairs assume resident images (the streamed loader walks offsets)");
     static_assert(CAP >= 256, "halo capacity must hold one offset phase");
@@ -975,7 +981,10 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
             float acc[HC];
 #pragma unroll
             for (int s = 0; s < SETS; ++s) {
-                mbar_wait_sleep(smem_u32(&bar_dfull[s][lt % C::DB]), (lt / C::DB) & 1, 64);
+                // one thread polls D_s's barrier, the other epilogue warps wait on a named barrier (suspended in
+                // hardware): eight polling warps were ~30% of the kernel's issued instructions (ncu)
+                if (warp == W_EPI && lane == 0) mbar_wait(smem_u32(&bar_dfull[s][lt % C::DB]), (lt / C::DB) & 1);
+                asm volatile("bar.sync %0, %1;" ::"r"(kEpiBar), "r"(C::EPI * 32) : "memory");
                 if (s == 0 && q == 0 && h == 0 && lane == 0) trace(dbg, 6, lt);
                 tc_fence_after();
 #pragma unroll

@@ -46,11 +46,33 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint: the waiting warp stays suspended (no issue slots) until the phase completes
+// or the hint expires, instead of re-polling at the hardware's default time limit
+#ifndef FVDB_MBAR_HINT_NS
+#define FVDB_MBAR_HINT_NS 1000
+#endif
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"((uint32_t)FVDB_MBAR_HINT_NS)
+        : "memory");
+    return ok != 0;
+}
 // bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t n = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if (++n == (1u << 24)) asm volatile("trap;");
+    if (FVDB_MBAR_HINT_NS > 0) {
+        while (!mbar_try_wait_hint(bar, parity)) {
+            if (++n == (1u << 22)) asm volatile("trap;");
+        }
+    } else {
+        while (!mbar_try_wait(bar, parity)) {
+            if (++n == (1u << 24)) asm volatile("trap;");
+        }
     }
 }
 // wait for warps that are off the critical path (epilogue, loaders): back off with
