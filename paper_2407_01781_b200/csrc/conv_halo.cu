@@ -100,18 +100,34 @@ __host__ __device__ __forceinline__ int pair_k_of_channel(int vch) {
 }
 constexpr int kPairImages = 14;  // offset pairs (0,1) .. (24,25), (26, zero)
 
-// Stages of builder set `set` (of `sets`) in one tile of `level` offset phases: the offsets (or, with pairs,
-// the offset pairs) v of each phase with v % sets == set.  A pair split by a phase boundary runs in both
-// phases, each time with the other phase's half masked off.
-__device__ __forceinline__ int h4_stage_count(bool pair, int level, int set, int sets) {
+// K = 32 offset quads (FVDB_H4_G32 = 4, opt-in: cfg5 fwd 3.35 vs 2.85 ms with pairs, the kernel's fixed per-tile
+// sync skeleton (FVDB_DEBUG_HALO=11: 2.0 ms either way) does not shrink with the stage count, while the
+// builders' register pressure grows (spills)): a stage multiplies offsets 4v .. 4v + 3, its A row
+// the four offsets' 64-byte halo rows (128 MMA K indices, 8 MMAs).  Builder thread t0 reads the row of offset
+// 4v + t0, chunk (j + t0) & 3 at load j: of the 8 threads of a shared-memory phase (two lanes of opposite output
+// parity x four offsets of alternating parity) each bank half then receives its 4 chunks exactly once.
+__host__ __device__ __forceinline__ int quad_chunk(int t0, int j) { return (j + t0) & 3; }
+// virtual channel (offset 4v + (vch >> 5), channel vch & 31) -> MMA K index
+__host__ __device__ __forceinline__ int quad_k_of_channel(int vch) {
+    const int t0 = vch >> 5, ch = vch & 31;
+    const int c = ch >> 3, e = (ch >> 1) & 3, h = ch & 1;
+    const int j = (c - t0) & 3;
+    const int i = 4 * j + e;
+    const int col = 8 * (i >> 1) + 2 * t0 + (i & 1);
+    return 2 * col + h;
+}
+constexpr int kQuadImages = 7;  // offset quads (0..3) .. (24..26, zero)
+
+// Stages of builder set `set` (of `sets`) in one tile of `level` offset phases: the offsets (or, with grp > 1, the
+// offset groups 4v.. / 2v..) v of each phase with v % sets == set.  A group split by a phase boundary runs in every
+// phase it touches, each time with the other phases' offsets masked off.
+__device__ __forceinline__ int h4_stage_count(int grp, int level, int set, int sets) {
     const int gs = 27 / level;
     int n = 0;
     for (int g = 0; g < level; ++g) {
         int a = g * gs, b = (g + 1) * gs - 1;
-        if (pair) {
-            a >>= 1;
-            b >>= 1;
-        }
+        a /= grp;
+        b /= grp;
         const int f = a + (set - a % sets + sets) % sets;
         if (f <= b) n += (b - f) / sets + 1;
     }
@@ -651,6 +667,9 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
 #ifndef FVDB_H4_NB
 #define FVDB_H4_NB 0
 #endif
+#ifndef FVDB_H4_G32
+#define FVDB_H4_G32 2  // offsets per stage at K = 32, N = 32: 2 (pairs) or 4 (quads: correct, measured slower)
+#endif
 #ifndef FVDB_H4_WPRE
 #define FVDB_H4_WPRE 1
 #endif
@@ -661,10 +680,13 @@ template <int K, int N>
 struct Halo4Cfg {
     // K = 32: offset-pair stages (pair_chunk): a stage is 64 MMA K indices, two offsets' rows.  Sets: 4, or 3
     // over the 14 pair stages of a tile (5 + 5 + 4 instead of 4 + 4 + 3 + 3; cfg5 fwd 3.03 -> 2.93 ms)
-    static constexpr bool PAIR = K == 32;
+    // G offsets per stage: 4 (quads) or 2 (pairs, FVDB_H4_G32=2) at K = 32, 1 otherwise
+    // (quads at N = 64 would leave one A slot per set in TMEM: pairs there)
+    static constexpr int G = K == 32 ? (N <= 32 ? FVDB_H4_G32 : 2) : 1;
+    static constexpr bool PAIR = G > 1;
     static constexpr int SETS = FVDB_H4_SETS > 0 ? FVDB_H4_SETS : (PAIR ? 3 : 4);
-    static constexpr int KV = PAIR ? 64 : K;    // MMA K per stage
-    static constexpr int NIMG = PAIR ? kPairImages : 27;
+    static constexpr int KV = K * G;    // MMA K per stage
+    static constexpr int NIMG = G == 4 ? kQuadImages : (G == 2 ? kPairImages : 27);
     static constexpr int ROWB = 2 * K, CPR = K / 8, LJ = KV / 32, NX = KV / 16;
     static constexpr int KB = KV >= 64 ? 64 : KV;
     static constexpr int BROWB = KB * 2;
@@ -686,6 +708,7 @@ struct Halo4Cfg {
     // no weight hand-off at all (K = 32 or N = 32: 54-112 KB)
     static constexpr bool RESIDENT = NIMG * B_BYTES <= 116 * 1024;
     static constexpr int WBYTES = RESIDENT ? NIMG * B_BYTES : SETS * WSL * B_BYTES;
+    static constexpr int NLD = 2;  // halo loader warps: warp 0 and the weight-loader warp (after the resident weights)
     // halo buffers (row ids, rows, tile record): the loader runs NB - 1 tile phases ahead of the builders.
     // Measured at K = 32 with pairs (cfg5 fwd): NB 2 / 4 3.04 / 3.03 ms; the default keeps the larger capacity.
     static constexpr int NB = FVDB_H4_NB > 0 ? FVDB_H4_NB : 2;
@@ -733,7 +756,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < NB; ++b) {
-            mbar_init(smem_u32(&bar_hfull[b]), 32);
+            mbar_init(smem_u32(&bar_hfull[b]), 32 * C::NLD);
             mbar_init(smem_u32(&bar_hempty[b]), kBuilders);
             mbar_init(smem_u32(&bar_xfull[b]), 1);
             mbar_init(smem_u32(&bar_ifull[b]), 1);
@@ -758,71 +781,108 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
 
-    if (warp == W_LOAD) {
-        // ---------------- halo loader (as k_conv_halo): row ids by TMA, rows by cp.async, record by TMA ----------
-        int tile = blockIdx.x, g = 0;
-        uint32_t pc = 0;
-        auto issue_ids = [&](int t, int gg, uint32_t buf) {
-            const int32_t* ph = P.phase + ((int64_t)t * 27 + gg) * 2;
-            const int off = P.tile_base[t] + ph[0], len = ph[1];
-            if (lane == 0) {
-                mbar_arrive_expect_tx(smem_u32(&bar_xfull[buf]), (uint32_t)len * 4u);
-                if (len > 0) bulk_g2s(xbase + buf * C::CAP * 4, P.halo_rows + off, (uint32_t)len * 4u, smem_u32(&bar_xfull[buf]));
-            }
-            return len;
-        };
-        int len = tile < T ? issue_ids(tile, 0, 0) : 0;
-        int level = tile < T ? P.tile_level[tile] : 1;
-        while (tile < T) {
-            int ng = g + 1, nt = tile;
-            if (ng >= level) { ng = 0; nt = tile + gridDim.x; }
-            const int nlevel = ng == 0 ? (nt < T ? P.tile_level[nt] : 1) : level;
-            const uint32_t buf = pc % NB, par = (pc / NB) & 1;
-            if (lane == 0) trace(dbg, 5, pc);
-            const int nlen = nt < T ? issue_ids(nt, ng, (pc + 1) % NB) : 0;
-            mbar_wait(smem_u32(&bar_xfull[buf]), par);
-            mbar_wait(smem_u32(&bar_hempty[buf]), par ^ 1);
-            if (lane == 0) trace(dbg, 8, pc);
-            const int32_t* ids = reinterpret_cast<const int32_t*>(gen + xbase + buf * C::CAP * 4);
-            const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
-            constexpr int RPI = 32 / C::CPR;
-            const int q = lane / C::CPR, c = lane % C::CPR;
-            for (int s0 = 0; s0 < len; s0 += 4 * RPI) {
-                int r[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int s = s0 + k * RPI + q;
-                    r[k] = s < len ? ids[s] : -1;
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int s = s0 + k * RPI + q;
-                    if (r[k] >= 0 && !(dbg & 8)) cp_async_16(hb + s * C::ROWB + (halo_phys(K, s, c) << 4), in + (int64_t)r[k] * K + c * 8, 16u);
-                }
-            }
-            if (lane == 0) trace(dbg, 11, pc);
-            cp_async_arrive_noinc(smem_u32(&bar_hfull[buf]));
-            if (lane == 0) {
-                mbar_wait(smem_u32(&bar_iempty[buf]), par ^ 1);
-                mbar_arrive_expect_tx(smem_u32(&bar_ifull[buf]), (uint32_t)kRecBytes);
-                bulk_g2s(ibase + buf * kIdxBytes, P.tile_rec + (int64_t)tile * kIdxBytes, (uint32_t)kRecBytes,
-                         smem_u32(&bar_ifull[buf]));
-            }
-            __syncwarp();
-            ++pc;
-            tile = nt;
-            g = ng;
-            len = nlen;
-            level = nlevel;
-        }
-    } else if (warp == W_WLOAD && C::RESIDENT) {
-        // ---------------- resident weights: all 27 offset images, once ----------------
-        if (lane == 0) {
+    if (warp == W_LOAD || (C::NLD == 2 && warp == W_WLOAD)) {
+        // ---------------- halo loaders: row ids by TMA, record by TMA, rows by cp.async ----------------
+        // With resident weights the weight-loader warp loads them once and then joins as a second halo loader
+        // (NLD = 2: each issues half of the rows' cp.async; one warp's loop was ~3000 of a ~5000-cycle tile
+        // period at K = 32).  Tile metadata (level, base, phase 0) is prefetched 32 tiles at a time, one tile
+        // per lane, instead of two dependent global loads per tile on the loader's critical path.
+        const int lw = warp == W_LOAD ? 0 : 1;
+        if (C::RESIDENT && lw == 1 && lane == 0) {
             constexpr uint32_t kChunk = 16384;
             mbar_arrive_expect_tx(smem_u32(&bar_wfull[0][0]), (uint32_t)C::WBYTES);
             for (uint32_t o = 0; o < (uint32_t)C::WBYTES; o += kChunk) {
                 const uint32_t n = (uint32_t)C::WBYTES - o < kChunk ? (uint32_t)C::WBYTES - o : kChunk;
                 bulk_g2s(bbase + o, wimg + o, n, smem_u32(&bar_wfull[0][0]));
+            }
+        }
+        int mk0 = -1, m_level = 1, m_base = 0, m_off = 0, m_len = 0;
+        // metadata of this CTA's k-th tile (level, base, phase-0 offset and length); warp-uniform k
+        auto meta = [&](int k, int& lvl, int& base, int& off0, int& len0) {
+            if ((k & ~31) != mk0) {
+                mk0 = k & ~31;
+                const int t = blockIdx.x + (mk0 + lane) * (int)gridDim.x;
+                if (t < T) {
+                    m_level = P.tile_level[t];
+                    m_base = P.tile_base[t];
+                    m_off = P.phase[(int64_t)t * 54];
+                    m_len = P.phase[(int64_t)t * 54 + 1];
+                }
+            }
+            lvl = __shfl_sync(0xffffffffu, m_level, k & 31);
+            base = __shfl_sync(0xffffffffu, m_base, k & 31);
+            off0 = __shfl_sync(0xffffffffu, m_off, k & 31);
+            len0 = __shfl_sync(0xffffffffu, m_len, k & 31);
+        };
+        auto issue_ids = [&](int off, int len, uint32_t buf) {
+            if (lw == 0 && lane == 0) {
+                mbar_arrive_expect_tx(smem_u32(&bar_xfull[buf]), (uint32_t)len * 4u);
+                if (len > 0) bulk_g2s(xbase + buf * C::CAP * 4, P.halo_rows + off, (uint32_t)len * 4u, smem_u32(&bar_xfull[buf]));
+            }
+        };
+        int tile = blockIdx.x, g = 0, k = 0;
+        uint32_t pc = 0;
+        int level = 1, base = 0, off = 0, len = 0;
+        if (tile < T) {
+            meta(0, level, base, off, len);
+            issue_ids(base + off, len, 0);
+        }
+        while (tile < T) {
+            int ng = g + 1, nt = tile, nk = k;
+            int nlevel = level, nbase = base, noff = 0, nlen = 0;
+            if (ng >= level) {
+                ng = 0;
+                nt = tile + gridDim.x;
+                nk = k + 1;
+                if (nt < T) meta(nk, nlevel, nbase, noff, nlen);
+            } else {  // next offset phase of a multi-phase tile (rare): its slice of the phase table
+                const int32_t* ph = P.phase + ((int64_t)tile * 27 + ng) * 2;
+                noff = ph[0];
+                nlen = ph[1];
+            }
+            const uint32_t buf = pc % NB, par = (pc / NB) & 1;
+            if (lane == 0 && lw == 0) trace(dbg, 5, pc);
+            if (nt < T) issue_ids(nbase + noff, nlen, (pc + 1) % NB);
+            mbar_wait(smem_u32(&bar_xfull[buf]), par);
+            mbar_wait(smem_u32(&bar_hempty[buf]), par ^ 1);
+            if (lane == 0 && lw == 0) {
+                trace(dbg, 8, pc);
+                // the record right away (builders release a buffer's record together with its rows)
+                mbar_wait(smem_u32(&bar_iempty[buf]), par ^ 1);
+                mbar_arrive_expect_tx(smem_u32(&bar_ifull[buf]), (uint32_t)kRecBytes);
+                bulk_g2s(ibase + buf * kIdxBytes, P.tile_rec + (int64_t)tile * kIdxBytes, (uint32_t)kRecBytes,
+                         smem_u32(&bar_ifull[buf]));
+            }
+            const int32_t* ids = reinterpret_cast<const int32_t*>(gen + xbase + buf * C::CAP * 4);
+            const uint32_t hb = hbase + buf * C::CAP * C::ROWB;
+            constexpr int RPI = 32 / C::CPR;
+            const int q = lane / C::CPR, c = lane % C::CPR;
+            for (int s0 = lw * 4 * RPI; s0 < len; s0 += C::NLD * 4 * RPI) {
+                int r[4];
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const int sl = s0 + kk * RPI + q;
+                    r[kk] = sl < len ? ids[sl] : -1;
+                }
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const int sl = s0 + kk * RPI + q;
+                    if (r[kk] >= 0 && !(dbg & 8))
+                        cp_async_16(hb + sl * C::ROWB + (halo_phys(K, sl, c) << 4), in + (int64_t)r[kk] * K + c * 8, 16u);
+                }
+            }
+            if (lane == 0 && lw == 0) trace(dbg, 11, pc);
+            cp_async_arrive_noinc(smem_u32(&bar_hfull[buf]));
+            __syncwarp();
+            ++pc;
+            tile = nt;
+            g = ng;
+            k = nk;
+            len = nlen;
+            off = noff;
+            if (ng == 0) {
+                level = nlevel;
+                base = nbase;
             }
         }
     } else if (warp >= W_BLD && warp < W_BLD + kBuilders) {
@@ -866,14 +926,14 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                 // stage v: offset v, or with pairs offsets 2v (threads t0 < 2) and 2v + 1 (t0 >= 2), each masked
                 // off outside this phase
                 const int d0 = g * gs, d_end = (g + 1) * gs;
-                const int v0 = C::PAIR ? d0 >> 1 : d0, v_end = C::PAIR ? ((d_end - 1) >> 1) + 1 : d_end;
+                const int v0 = d0 / C::G, v_end = (d_end - 1) / C::G + 1;
                 for (int vi = v0 + (set - v0 % SETS + SETS) % SETS; vi < v_end; vi += SETS, ++js) {
                     const uint32_t ak = js % ASL, ause = js / ASL;
                     if (tr) trace(dbg, 7, js);
                     int dd = vi;
                     bool ok = true;
                     if constexpr (C::PAIR) {
-                        dd = 2 * vi + (t0 >> 1);
+                        dd = C::G * vi + (C::G == 4 ? t0 : (t0 >> 1));
                         ok = dd >= d0 && dd < d_end;
                     }
                     const uint16_t* lr = lb + dd * kTileRows + lrow;
@@ -896,7 +956,8 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                                 const int pr = sv & 1;
 #pragma unroll
                                 for (int j = 0; j < C::LJ; ++j) {
-                                    const int ch = C::PAIR ? pair_chunk(t0, j) : halo_phys(K, pr, halo_chunk(K, t0, j));
+                                    const int ch = C::G == 4 ? quad_chunk(t0, j)
+                                                   : (C::G == 2 ? pair_chunk(t0, j) : halo_phys(K, pr, halo_chunk(K, t0, j)));
                                     const uint4 w = lds128_pred(rb + (ch << 4), has);
                                     const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -935,10 +996,10 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
         for (int tile = blockIdx.x; tile < T; tile += gridDim.x, ++lt) {
           // the builders' stage sequence: offsets (pairs) v of each phase g in order
           const int level = C::PAIR ? P.tile_level[tile] : 1, gs = 27 / level;
-          const int nst = C::PAIR ? h4_stage_count(true, level, set, SETS) : per_tile;
+          const int nst = C::PAIR ? h4_stage_count(C::G, level, set, SETS) : per_tile;
           int k = 0;
           for (int g = 0; g < level; ++g) {
-            const int v0 = C::PAIR ? (g * gs) >> 1 : 0, v_end = C::PAIR ? (((g + 1) * gs - 1) >> 1) + 1 : 27;
+            const int v0 = C::PAIR ? (g * gs) / C::G : 0, v_end = C::PAIR ? ((g + 1) * gs - 1) / C::G + 1 : 27;
             for (int d = v0 + (set - v0 % SETS + SETS) % SETS; d < v_end; d += SETS, ++js, ++k) {
                 const uint32_t ak = js % ASL, wk = js % WSL, wuse = js / WSL;
                 const bool first = k == 0, last = k == nst - 1;
@@ -962,6 +1023,8 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                         mma_ts_x2_elect_acc<8, 2>(dt, at, bd, C::IDESC, first ? 0u : 1u);
                     } else {
                         mma_ts_x4_elect_acc<8, 16, 24, 2, 4, 6>(dt, at, bd, C::IDESC, first ? 0u : 1u);
+                        if constexpr (C::KV == 128)  // second 64-wide K block of the image
+                            mma_ts_x4_elect<8, 16, 24, 2, 4, 6>(dt, at + 32, bd + ((N * C::BROWB) >> 4), C::IDESC);
                     }
                 }
                 mma_commit_elect(smem_u32(&bar_afree[set][ak]));
@@ -1000,7 +1063,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_dempty[s][lt % C::DB]));
             }
-            if (row >= 0) {
+            if (row >= 0 && !(dbg & 4)) {
                 if constexpr (OUT_BF16) {
                     uint8_t* dst = reinterpret_cast<uint8_t*>(reinterpret_cast<bf16*>(out) + row * N + h * HC);
 #pragma unroll
@@ -2021,6 +2084,29 @@ __global__ void __launch_bounds__(1024) k_pack_halo(const float* __restrict__ w,
         const int co = transpose ? ch : n, ci = transpose ? n : ch;
         s[i] = w[((int64_t)co * cin + ci) * 27 + d];
     }
+    if (pair == 4) {
+        // K = 32 offset quads (k_conv_halo4): image v = [2][N][64] over virtual channels (offsets 4v .. 4v + 3, 32
+        // each, zero past offset 26), two 64-wide K blocks of 128-byte swizzled rows
+        for (int ch = threadIdx.x; ch < 128; ch += blockDim.x) chan[quad_k_of_channel(ch)] = ch;
+        __syncthreads();
+        const int x = n & 7;
+        for (int c = threadIdx.x; c < kQuadImages * 16; c += blockDim.x) {
+            const int v = c >> 4, k0 = (c & 15) * 8;
+            float f[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int vch = chan[k0 + j], d = 4 * v + (vch >> 5);
+                f[j] = d < 27 ? s[(vch & 31) * 27 + d] : 0.f;
+            }
+            __nv_bfloat162 b[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+            const int kb = k0 >> 6, e = k0 & 63;
+            *reinterpret_cast<uint4*>(img + (size_t)v * N * 256 + (size_t)kb * N * 128 + (size_t)n * 128 +
+                                      (((e >> 3) ^ x) << 4)) = *reinterpret_cast<const uint4*>(b);
+        }
+        return;
+    }
     if (pair) {
         // K = 32 offset pairs (k_conv_halo4): image v = [N][64] over virtual channels (offset 2v's 32, then
         // 2v + 1's, zero past offset 26), 128-byte swizzled rows
@@ -2296,7 +2382,7 @@ extern "C" int fvdb_pack_weights_halo(const float* w, int cout, int cin, int tra
     const int K = transpose ? cout : cin, N = transpose ? cin : cout;
     if ((K != 32 && K != 64 && K != 128) || (N != 32 && N != 64 && N != 128)) return FVDB_ERR_INVALID;
     // K = 32 under the lockstep kernel: offset-pair images (same byte budget: 14 x N x 64 <= 34 x N x 32)
-    const int pair = K == 32 && N <= 64 && halo4_env() != 0;
+    const int pair = K == 32 && N <= 64 && halo4_env() != 0 ? (N <= 32 ? FVDB_H4_G32 : 2) : 0;
     k_pack_halo<<<transpose ? cin : cout, 1024, 0, as_stream(stream)>>>(w, cout, cin, transpose, pair, (uint8_t*)image);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
