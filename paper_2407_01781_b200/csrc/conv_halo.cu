@@ -678,13 +678,14 @@ __global__ void __launch_bounds__(HaloCfg<K, N, V>::THREADS, 1)
 #endif
 template <int K, int N>
 struct Halo4Cfg {
-    // K = 32: offset-pair stages (pair_chunk): a stage is 64 MMA K indices, two offsets' rows.  Sets: 4, or 3
-    // over the 14 pair stages of a tile (5 + 5 + 4 instead of 4 + 4 + 3 + 3; cfg5 fwd 3.03 -> 2.93 ms)
+    // K = 32: offset-pair stages (pair_chunk): a stage is 64 MMA K indices, two offsets' rows.  Sets: 4 (with
+    // the two-warp loader, cfg5 fwd 2.46 ms vs 2.54 with 3 sets; 3 sets were faster while one loader warp bound
+    // the tile period: 2.93 vs 3.03)
     // G offsets per stage: 4 (quads) or 2 (pairs, FVDB_H4_G32=2) at K = 32, 1 otherwise
     // (quads at N = 64 would leave one A slot per set in TMEM: pairs there)
     static constexpr int G = K == 32 ? (N <= 32 ? FVDB_H4_G32 : 2) : 1;
     static constexpr bool PAIR = G > 1;
-    static constexpr int SETS = FVDB_H4_SETS > 0 ? FVDB_H4_SETS : (PAIR ? 3 : 4);
+    static constexpr int SETS = FVDB_H4_SETS > 0 ? FVDB_H4_SETS : 4;
     static constexpr int KV = K * G;    // MMA K per stage
     static constexpr int NIMG = G == 4 ? kQuadImages : (G == 2 ? kPairImages : 27);
     static constexpr int ROWB = 2 * K, CPR = K / 8, LJ = KV / 32, NX = KV / 16;
