@@ -152,10 +152,18 @@ __device__ __forceinline__ void fold_fields_block(BuildScalars* sc, const FieldA
     }
 }
 
+struct SinglePassHost {
+    BuildScalars hs;
+    unsigned long long nonfinite;
+    int last[3];
+    int nu;
+};
+
 struct BuildWs {
     uint64_t *tk, *tk_alt, *vk, *vk_alt, *tiles, *uvox;
     int *leaf_id, *lower_id, *upper_id, *n_sel;
     BuildScalars* sc;
+    SinglePassHost* pack;
     void* cub_tmp;
     size_t cub_bytes;
 };
@@ -187,6 +195,7 @@ void carve(C& c, int64_t n, size_t cub_bytes, BuildWs* w) {
         w->upper_id = c.template take<int>(m);
         w->n_sel = c.template take<int>(4);
         w->sc = c.template take<BuildScalars>(1);
+        w->pack = c.template take<SinglePassHost>(1);
         w->cub_tmp = c.template take<char>(cub_bytes);
         w->cub_bytes = cub_bytes;
     } else {
@@ -194,6 +203,7 @@ void carve(C& c, int64_t n, size_t cub_bytes, BuildWs* w) {
         for (int i = 0; i < 3; ++i) c.template take<int>(m);
         c.template take<int>(4);
         c.template take<BuildScalars>(1);
+        c.template take<SinglePassHost>(1);
         c.template take<char>(cub_bytes);
     }
 }
@@ -544,6 +554,20 @@ int grid_for(int64_t n) {
 
 int bit_length(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
+__global__ void k_pack_single(const BuildScalars* __restrict__ sc, const int64_t* __restrict__ pending,
+                              const int* __restrict__ leaf_last, const int* __restrict__ lower_last,
+                              const int* __restrict__ upper_last, const int* __restrict__ n_sel,
+                              SinglePassHost* __restrict__ out) {
+    if (threadIdx.x == 0) {
+        out->hs = *sc;
+        out->nonfinite = pending ? (unsigned long long)*pending : ~0ull;
+        out->last[0] = *leaf_last;
+        out->last[1] = *lower_last;
+        out->last[2] = *upper_last;
+        out->nu = *n_sel;
+    }
+}
+
 // tiles[0] := the common tile key (device side: no read-back needed to start the voxel sort)
 __global__ void k_single_tile(uint64_t* __restrict__ tiles, const BuildScalars* __restrict__ sc) {
     tiles[0] = sc->key_or;
@@ -572,20 +596,14 @@ static int single_tile_pass(const int64_t* coords, int64_t n, const int64_t* pen
             e = cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, ids[t], ids[t], (int)n, st);
         }
     }
-    struct {
-        BuildScalars hs;
-        int last[3];
-        int nu;
-        unsigned long long nonfinite;
-    } h;
-    h.nonfinite = ~0ull;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&h.hs, w.sc, sizeof(h.hs), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && pending_nonfinite)
-        e = cudaMemcpyAsync(&h.nonfinite, pending_nonfinite, sizeof(h.nonfinite), cudaMemcpyDeviceToHost, st);
-    int* ids[3] = {w.leaf_id, w.lower_id, w.upper_id};
-    for (int t = 0; t < 3 && e == cudaSuccess; ++t)
-        e = cudaMemcpyAsync(&h.last[t], ids[t] + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&h.nu, w.n_sel, sizeof(int), cudaMemcpyDeviceToHost, st);
+    // one read-back: the scalars, the pending non-finite slot, the node counts and the unique count are packed
+    // into one device record first (six pageable copies were ~3 us of device time and a host call each)
+    SinglePassHost h;
+    if (e == cudaSuccess) {
+        k_pack_single<<<1, 32, 0, st>>>(w.sc, pending_nonfinite, w.leaf_id + (n - 1), w.lower_id + (n - 1),
+                                        w.upper_id + (n - 1), w.n_sel, w.pack);
+        e = cudaMemcpyAsync(&h, w.pack, sizeof(h), cudaMemcpyDeviceToHost, st);
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -985,6 +1003,24 @@ extern "C" int fvdb_quantize_points(const double* points, int64_t n, const doubl
 namespace fvdb {
 namespace {
 
+struct CoarsenHost {
+    unsigned long long tk[2];
+    int64_t nv;
+    int last[2];
+};
+
+__global__ void k_coarsen_pack(const unsigned long long* __restrict__ tk, const int* __restrict__ leaf_last,
+                               const int* __restrict__ lower_last, const int64_t* __restrict__ nv,
+                               CoarsenHost* __restrict__ out) {
+    if (threadIdx.x == 0) {
+        out->tk[0] = tk[0];
+        out->tk[1] = tk[1];
+        out->nv = *nv;
+        out->last[0] = *leaf_last;
+        out->last[1] = *lower_last;
+    }
+}
+
 struct CoarsenWs {
     uint64_t *key, *key_alt;
     int *idx, *idx_alt;
@@ -992,6 +1028,7 @@ struct CoarsenWs {
     uint64_t* masks;          // [nl][8] coarse leaf masks by coarse leaf id (first n_leaf used)
     int64_t *pop, *incl;      // [nl] popcounts by coarse leaf id (0 past n_leaf) and their inclusive scan
     unsigned long long* tk;   // [2] OR / AND of the coarse tile keys
+    CoarsenHost* pack;        // the plan's one read-back
     void* cub_tmp;
     size_t cub_bytes;
 };
@@ -1022,6 +1059,7 @@ void carve_coarsen(C& c, int64_t n, CoarsenWs* w) {
         w->pop = c.template take<int64_t>(m);
         w->incl = c.template take<int64_t>(m);
         w->tk = c.template take<unsigned long long>(2);
+        w->pack = c.template take<CoarsenHost>(1);
         w->cub_tmp = c.template take<char>(cb);
         w->cub_bytes = cb;
     } else {
@@ -1032,6 +1070,7 @@ void carve_coarsen(C& c, int64_t n, CoarsenWs* w) {
         c.template take<int64_t>(m);
         c.template take<int64_t>(m);
         c.template take<unsigned long long>(2);
+        c.template take<CoarsenHost>(1);
         c.template take<char>(cb);
     }
 }
@@ -1204,15 +1243,10 @@ extern "C" int fvdb_coarsen2_plan(const int64_t* leaf_origins, const uint64_t* l
     FVDB_LAUNCH_CHECK();
     tb = w.cub_bytes;
     FVDB_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, w.pop, w.incl, n, st));
-    struct {
-        unsigned long long tk[2];
-        int last[2];
-        int64_t nv;
-    } h;
-    FVDB_CUDA_TRY(cudaMemcpyAsync(h.tk, w.tk, sizeof(h.tk), cudaMemcpyDeviceToHost, st));
-    for (int t = 0; t < 2; ++t)
-        FVDB_CUDA_TRY(cudaMemcpyAsync(&h.last[t], ids[t] + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
-    FVDB_CUDA_TRY(cudaMemcpyAsync(&h.nv, w.incl + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CoarsenHost h;
+    k_coarsen_pack<<<1, 32, 0, st>>>(w.tk, w.leaf_id + (n - 1), w.lower_id + (n - 1), w.incl + (n - 1), w.pack);
+    FVDB_LAUNCH_CHECK();
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&h, w.pack, sizeof(h), cudaMemcpyDeviceToHost, st));  // one read-back
     FVDB_CUDA_TRY(cudaStreamSynchronize(st));
     if (h.tk[0] != h.tk[1]) return FVDB_ERR_UNSUPPORTED;  // several coarse root tiles
     counts[0] = 1;
