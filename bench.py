@@ -19,7 +19,7 @@ overlapped with the input-gradient kernel.
 
 Timing: W warm-up steps; K timed steps, each preceded by a 256 MB L2-flush write (untimed), timed with CUDA
 events on the launching stream; ms_per_step = mean, max over ranks.  ``e2e`` is the same step through the public
-API with host data: the features are copied host->device (pinned fp32) every step, the loss (½‖y‖², whose
+API with host data: the features are copied host->device (pinned bf16; --e2e-dtype fp32) every step, the loss (½‖y‖², whose
 gradient y seeds the backward) and the weight gradient are read back.  ``cpu_baseline`` times the reference
 itself (the unmodified ``idxgrid`` package installed in baseline/_ref; the oracle port if it is absent) on a
 leaf-aligned sample of the same workload.
@@ -543,7 +543,7 @@ def run_special(args, rank, world, local_rank, cfg):
         down = P.SparseConv3d(64, 128, stride=2).to(dev)
         up = P.SparseConv3d(128, 64, stride=2, transposed=True).to(dev)
         n_vox = coords.shape[0]
-        x = torch.randn(n_vox, 64, device=dev, generator=gen)
+        x = torch.randn(n_vox, 64, device=dev, generator=gen).to(torch.bfloat16)  # bf16 features (compute dtype)
         if use_dist:
             P.dist.attach_grad_reducer(down)
             P.dist.attach_grad_reducer(up)
