@@ -911,7 +911,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                          smem_u32(&bar_wfull[set][k]));
             }
         };
-        if (wl)
+        if (wl && !(dbg & 16))  // dbg 16 (profiling): no streamed weights at all (results wrong)
             for (int j = 0; j < C::WPRE; ++j) load_w(j);
         uint32_t pc = 0, js = 0;
         for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
@@ -941,7 +941,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                     const int sl[4] = {ok ? lr[0] : kNoSlot, ok ? lr[8] : kNoSlot, ok ? lr[16] : kNoSlot,
                                        ok ? lr[24] : kNoSlot};
                     mbar_wait(smem_u32(&bar_afree[set][ak]), (ause & 1) ^ 1);
-                    if (wl) load_w(js + C::WPRE);
+                    if (wl && !(dbg & 16)) load_w(js + C::WPRE);
                     tc_fence_after();
                     if (tr) trace(dbg, 0, js);
                     if (!(dbg & 2)) {
@@ -1012,7 +1012,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                 if constexpr (C::RESIDENT) {
                     if (js == 0) mbar_wait(smem_u32(&bar_wfull[0][0]), 0);
                 } else {
-                    mbar_wait(smem_u32(&bar_wfull[set][wk]), wuse & 1);
+                    if (!(dbg & 16)) mbar_wait(smem_u32(&bar_wfull[set][wk]), wuse & 1);
                 }
                 tc_fence_after();
                 if (tr) trace(dbg, 3, js);
