@@ -109,6 +109,17 @@ int fvdb_build_plan2(const int64_t* coords, int64_t n, const int64_t* pending_no
                      size_t workspace_bytes, int64_t* counts, int64_t* detail, void* stream);
 int fvdb_build_fill(void* workspace, size_t workspace_bytes, int64_t n, const int64_t* counts,
                     const fvdb_grid_arrays* out, void* stream);
+/* Leaf-hash build (the default for coordinates in one root tile; build.py:82-142 for the same result): every
+ * voxel ORs its bit into its leaf's mask in a hash table keyed by the leaf key, the occupied entries are sorted
+ * and registered leaf-parallel -- no per-voxel sort.  Bit-identical to fvdb_build_plan2/fill.  plan synchronizes
+ * once (error precedence as fvdb_build_plan2: non-finite pending slot, then the range check) and writes counts[5]
+ * = {num_upper (1), num_lower, num_leaf, num_voxels, tile key}; FVDB_ERR_UNSUPPORTED when the coordinates span
+ * several root tiles or more leaves than half the table (n / 4 entries): use fvdb_build_plan2. */
+size_t fvdb_build_leaf_workspace_bytes(int64_t n);
+int fvdb_build_leaf_plan(const int64_t* coords, int64_t n, const int64_t* pending_nonfinite, void* workspace,
+                         size_t workspace_bytes, int64_t* counts, int64_t* detail, void* stream);
+int fvdb_build_leaf_fill(void* workspace, size_t workspace_bytes, int64_t n, const int64_t* counts,
+                         const fvdb_grid_arrays* out, void* stream);
 /* Coarsen by 2 from the fine grid's leaves (build.py:325-339): one sort key per fine LEAF instead of one per
  * voxel.  The result is bit-identical to fvdb_build_* over unique(ijk // 2).  leaf_origins int64 [n_leaf,3],
  * leaf_masks [n_leaf,8] (device, the fine grid's arrays).  plan synchronizes once and writes counts[5] =

@@ -67,6 +67,9 @@ SIGNATURES = {
     "fvdb_build_plan2": (_i32, [_vp, _i64, _vp, _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
     "fvdb_quantize_points_async": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp]),
     "fvdb_build_fill": (_i32, [_vp, _sz, _i64, C.POINTER(_i64), C.POINTER(GridArrays), _vp]),
+    "fvdb_build_leaf_workspace_bytes": (_sz, [_i64]),
+    "fvdb_build_leaf_plan": (_i32, [_vp, _i64, _vp, _vp, _sz, C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "fvdb_build_leaf_fill": (_i32, [_vp, _sz, _i64, C.POINTER(_i64), C.POINTER(GridArrays), _vp]),
     "fvdb_coarsen2_workspace_bytes": (_sz, [_i64]),
     "fvdb_coarsen2_plan": (_i32, [_vp, _vp, _i64, _vp, _sz, C.POINTER(_i64), _vp]),
     "fvdb_coarsen2_fill": (_i32, [_vp, _sz, _i64, C.POINTER(_i64), C.POINTER(GridArrays), _vp]),

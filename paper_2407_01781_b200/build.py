@@ -8,6 +8,7 @@ the work runs in ``csrc/build.cu`` through the C ABI (two-phase plan → fill).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -59,6 +60,11 @@ def _build_device(c: torch.Tensor, transform, name, stats: BuildStats, pending=N
     n = c.shape[0]
     st = _lib.stream_ptr()
     t0 = time.perf_counter()
+    if _LEAF_BUILD:  # one root tile: leaf-hash build (no per-voxel sort); else the coordinate build below
+        g = _build_leaf(c, transform, name, stats, pending, points)
+        if g is not None:
+            stats.phase_seconds["plan+fill (leaf hash)"] = time.perf_counter() - t0
+            return g
     ws_bytes = L.fvdb_build_workspace_bytes(n)
     ws = _lib.workspace(ws_bytes, dev)
     counts = (C.c_int64 * 4)()
@@ -73,6 +79,34 @@ def _build_device(c: torch.Tensor, transform, name, stats: BuildStats, pending=N
     _lib.check(L.fvdb_build_fill(ws.data_ptr(), ws_bytes, n, counts, C.byref(ga), st), "build_fill")
     stats.phase_seconds["plan"] = t1 - t0
     stats.phase_seconds["fill"] = time.perf_counter() - t1
+    stats.unique_count = cnt[3]
+    stats.num_upper, stats.num_lower, stats.num_leaf = cnt[0], cnt[1], cnt[2]
+    return IndexGrid(num_voxels=cnt[3], transform=transform, name=name, **arrays)
+
+
+_LEAF_BUILD = os.environ.get("FVDB_BUILD_LEAF", "1") != "0"
+
+
+def _build_leaf(c, transform, name, stats, pending=None, points=None):
+    """Leaf-hash build (fvdb_build_leaf_*): voxels OR their bits into per-leaf masks in a hash table, the leaves
+    are sorted and registered leaf-parallel; bit-identical to the coordinate build.  None when the coordinates
+    span several root tiles (or crowd the table): the caller runs the coordinate build."""
+    L = _lib.lib()
+    n = c.shape[0]
+    st = _lib.stream_ptr()
+    wsb = L.fvdb_build_leaf_workspace_bytes(n)
+    ws = _lib.workspace(wsb, c.device)
+    counts = (C.c_int64 * 5)()
+    detail = C.c_int64(0)
+    rc = L.fvdb_build_leaf_plan(c.data_ptr(), n, _lib.ptr(pending), ws.data_ptr(), wsb, counts, C.byref(detail), st)
+    if rc == _lib.FVDB_ERR_UNSUPPORTED:
+        return None
+    _raise_build_error(rc, detail.value, c, points)
+    _lib.check(rc, "build_leaf_plan")
+    cnt = [int(counts[k]) for k in range(4)]
+    arrays = _alloc_arrays(cnt, c.device)
+    ga = _lib.GridArrays(**{f: arrays[f].data_ptr() for f in ARRAY_FIELDS})
+    _lib.check(L.fvdb_build_leaf_fill(ws.data_ptr(), wsb, n, counts, C.byref(ga), st), "build_leaf_fill")
     stats.unique_count = cnt[3]
     stats.num_upper, stats.num_lower, stats.num_leaf = cnt[0], cnt[1], cnt[2]
     return IndexGrid(num_voxels=cnt[3], transform=transform, name=name, **arrays)

@@ -1273,3 +1273,314 @@ extern "C" int fvdb_coarsen2_fill(void* workspace, size_t ws_bytes, int64_t n_le
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
 }
+
+// ---------------------------------------------------------------------------------------------
+// Grid build by leaf hashing (single root tile; build.py:82-142 for the same result).  Instead of radix-sorting
+// one 36-bit key per voxel (the coordinate build's dominant cost), every voxel ORs its bit into its LEAF's mask in
+// a hash table keyed by the leaf's 27-bit key (upper << 12 | lower; warp-aggregated: lanes of one leaf elect one
+// probe, lanes of one mask word one atomicOr), then the occupied entries (~1 per 100 voxels) are sorted by key and
+// registered leaf-parallel exactly as coarsen2 does.  Voxel order = (leaf key, in-leaf offset) = the build's, so
+// every array is bit-identical to the coordinate build (tests/test_gpu_grid.py goldens).  Coordinates spanning
+// several root tiles, or more leaves than the table takes, return FVDB_ERR_UNSUPPORTED (use fvdb_build_plan2).
+// ---------------------------------------------------------------------------------------------
+namespace fvdb {
+namespace {
+
+constexpr uint32_t kLhEmpty = 0xFFFFFFFFu;
+constexpr int kLhMaxProbe = 64;
+
+struct LeafHashScalars {
+    unsigned long long bad_row, key_or, key_and;
+    int n_leaves, overflow;
+};
+struct LeafHashHost {
+    LeafHashScalars sc;
+    unsigned long long nonfinite;
+    int64_t nv;
+    int lower_last;
+    int pad;
+};
+
+struct LeafHashWs {
+    uint32_t* tkey;   // [cap] leaf key per table entry, kLhEmpty = free
+    uint64_t* tmask;  // [cap][8]
+    uint32_t *key, *key_alt;
+    int *val, *val_alt;
+    int* lower_id;
+    int64_t *pop, *incl;
+    LeafHashScalars* sc;
+    LeafHashHost* pack;
+    void* cub_tmp;
+    size_t cub_bytes;
+    int64_t cap;
+};
+
+int64_t leafhash_cap(int64_t n) {
+    int64_t c = 1024;
+    while (c < n / 4 && c < ((int64_t)1 << 24)) c <<= 1;
+    return c;
+}
+
+template <class C>
+void carve_leafhash(C& c, int64_t n, LeafHashWs* w) {
+    const int64_t cap = leafhash_cap(n);
+    size_t a = 0, b = 0, d = 0;
+    cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr);
+    cub::DoubleBuffer<int> vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int)cap, 0, 28);
+    cub::DeviceScan::InclusiveSum(nullptr, b, (int*)nullptr, (int*)nullptr, (int)cap);
+    cub::DeviceScan::InclusiveSum(nullptr, d, (int64_t*)nullptr, (int64_t*)nullptr, (int)cap);
+    size_t cb = a > b ? a : b;
+    cb = cb > d ? cb : d;
+    if constexpr (std::is_same_v<C, Carver>) {
+        w->cap = cap;
+        w->tkey = c.template take<uint32_t>(cap);
+        w->tmask = c.template take<uint64_t>(8 * cap);
+        w->key = c.template take<uint32_t>(cap);
+        w->key_alt = c.template take<uint32_t>(cap);
+        w->val = c.template take<int>(cap);
+        w->val_alt = c.template take<int>(cap);
+        w->lower_id = c.template take<int>(cap);
+        w->pop = c.template take<int64_t>(cap);
+        w->incl = c.template take<int64_t>(cap);
+        w->sc = c.template take<LeafHashScalars>(1);
+        w->pack = c.template take<LeafHashHost>(1);
+        w->cub_tmp = c.template take<char>(cb);
+        w->cub_bytes = cb;
+    } else {
+        for (int i = 0; i < 3; ++i) c.template take<uint32_t>(cap);
+        c.template take<uint64_t>(8 * cap);
+        for (int i = 0; i < 3; ++i) c.template take<int>(cap);
+        c.template take<int64_t>(cap);
+        c.template take<int64_t>(cap);
+        c.template take<LeafHashScalars>(1);
+        c.template take<LeafHashHost>(1);
+        c.template take<char>(cb);
+    }
+}
+
+__global__ void k_lh_init(LeafHashScalars* sc) {
+    sc->bad_row = ~0ull;
+    sc->key_or = 0ull;
+    sc->key_and = ~0ull;
+    sc->n_leaves = 0;
+    sc->overflow = 0;
+}
+
+__device__ __forceinline__ uint32_t lh_hash(uint32_t k) { return k * 0x9E3779B1u; }
+
+__global__ void __launch_bounds__(kThreads) k_lh_insert(const int64_t* __restrict__ coords, int64_t n, int64_t cap,
+                                                       int cap_bits, uint32_t* __restrict__ tkey,
+                                                       uint64_t* __restrict__ tmask, LeafHashScalars* sc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t lim = (int64_t)1 << 30;
+    uint64_t k_or = 0, k_and = ~0ull;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x; r0 < n; r0 += stride) {  // warp-uniform trip count
+        const int64_t r = r0 + threadIdx.x;
+        const bool valid = r < n;
+        uint32_t L = 0, bit = 0;
+        if (valid) {
+            const int64_t i = coords[3 * r], j = coords[3 * r + 1], k = coords[3 * r + 2];
+            if ((i > lim) | (i < -lim) | (j > lim) | (j < -lim) | (k > lim) | (k < -lim))
+                atomicMin(&sc->bad_row, (unsigned long long)r);
+            const uint64_t t = tile_key(i, j, k);
+            k_or |= t;
+            k_and &= t;
+            L = (upper_off(i, j, k) << 12) | lower_off(i, j, k);
+            bit = leaf_off(i, j, k);
+        }
+        const unsigned act = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            const unsigned grp = __match_any_sync(act, L);
+            const int leader = __ffs(grp) - 1;
+            uint32_t slot = 0;
+            if (lane == leader) {
+                uint32_t h = lh_hash(L) >> (32 - cap_bits);  // high product bits: all key bits mix in
+                int p = 0;
+                for (; p < kLhMaxProbe; ++p) {
+                    const uint32_t prev = atomicCAS(&tkey[h], kLhEmpty, L);
+                    if (prev == kLhEmpty) {
+                        atomicAdd(&sc->n_leaves, 1);
+                        break;
+                    }
+                    if (prev == L) break;
+                    h = (h + 1) & (uint32_t)(cap - 1);
+                }
+                if (p == kLhMaxProbe) sc->overflow = 1;
+                slot = h;
+            }
+            slot = __shfl_sync(grp, slot, leader);
+            const uint32_t word = bit >> 6;
+            const unsigned wg = __match_any_sync(grp, word);
+            const uint64_t m = 1ull << (bit & 63);
+            const uint32_t lo = __reduce_or_sync(wg, (uint32_t)m), hi = __reduce_or_sync(wg, (uint32_t)(m >> 32));
+            if (lane == __ffs(wg) - 1)
+                atomicOr((unsigned long long*)&tmask[8 * (int64_t)slot + word], ((unsigned long long)hi << 32) | lo);
+        }
+    }
+    typedef cub::BlockReduce<uint64_t, kThreads> BR;
+    __shared__ typename BR::TempStorage t1;
+    const uint64_t bo = BR(t1).Reduce(k_or, [](uint64_t a, uint64_t b) { return a | b; });
+    __syncthreads();
+    const uint64_t ba = BR(t1).Reduce(k_and, [](uint64_t a, uint64_t b) { return a & b; });
+    if (threadIdx.x == 0) {
+        atomicOr(&sc->key_or, (unsigned long long)bo);
+        atomicAnd(&sc->key_and, (unsigned long long)ba);
+    }
+}
+
+// sort input: occupied entries keep their key (< 2^27), free ones sort last (2^27)
+__global__ void k_lh_prep(const uint32_t* __restrict__ tkey, int64_t cap, uint32_t* __restrict__ key,
+                          int* __restrict__ val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = tkey[i];
+        key[i] = k == kLhEmpty ? (1u << 27) : k;
+        val[i] = (int)i;
+    }
+}
+
+// lower-node heads and leaf popcounts over the sorted entries (entries past the leaf count: 0)
+__global__ void k_lh_heads_pop(const uint32_t* __restrict__ key, const int* __restrict__ val, int64_t cap,
+                               const uint64_t* __restrict__ tmask, int* __restrict__ lower_h,
+                               int64_t* __restrict__ pop) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = key[i];
+        const bool ok = v < (1u << 27);
+        const uint32_t p = i ? key[i - 1] : ~v;
+        lower_h[i] = ok && ((v >> 12) != (p >> 12));
+        int64_t c = 0;
+        if (ok) {
+            const uint64_t* m = tmask + 8 * (int64_t)val[i];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) c += __popcll(m[t]);
+        }
+        pop[i] = c;
+    }
+}
+
+__global__ void k_lh_pack(const LeafHashScalars* __restrict__ sc, const int64_t* __restrict__ pending,
+                          const int* __restrict__ lower_last, const int64_t* __restrict__ nv,
+                          LeafHashHost* __restrict__ out) {
+    if (threadIdx.x == 0) {
+        out->sc = *sc;
+        out->nonfinite = pending ? (unsigned long long)*pending : ~0ull;
+        out->lower_last = *lower_last;
+        out->nv = *nv;
+    }
+}
+
+__global__ void k_lh_register(const uint32_t* __restrict__ key, const int* __restrict__ val, int64_t n_leaf,
+                              const int* __restrict__ lower_id, const uint64_t* __restrict__ tmask,
+                              const int64_t* __restrict__ pop, const int64_t* __restrict__ incl, uint64_t tkey,
+                              fvdb_grid_arrays o, int64_t n_lower) {
+    const int64_t ox = tile_field_origin(tkey, 42), oy = tile_field_origin(tkey, 21), oz = tile_field_origin(tkey, 0);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_leaf; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = key[i], p = i ? key[i - 1] : ~v;
+        const uint32_t up = (v >> 12) & 0x7FFF, lo = v & 0xFFF;
+        const int64_t lx = ox + ((int64_t)((up >> 10) & 31) << 7), ly = oy + ((int64_t)((up >> 5) & 31) << 7),
+                      lz = oz + ((int64_t)(up & 31) << 7);
+        o.leaf_keys[i] = v;
+        o.leaf_offset_in_lower[i] = (uint16_t)lo;
+        o.leaf_value_offset[i] = (uint64_t)(incl[i] - pop[i]) + 1;
+        o.leaf_origins[3 * i + 0] = lx + ((int64_t)((lo >> 8) & 15) << 3);
+        o.leaf_origins[3 * i + 1] = ly + ((int64_t)((lo >> 4) & 15) << 3);
+        o.leaf_origins[3 * i + 2] = lz + ((int64_t)(lo & 15) << 3);
+        const uint64_t* m = tmask + 8 * (int64_t)val[i];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) o.leaf_masks[8 * i + t] = m[t];
+        if ((v >> 12) == (p >> 12)) continue;  // not a lower head
+        const int lower = lower_id[i] - 1;
+        o.lower_child_starts[lower] = i;
+        o.lower_offset_in_upper[lower] = (uint16_t)up;
+        o.lower_origins[3 * (int64_t)lower + 0] = lx;
+        o.lower_origins[3 * (int64_t)lower + 1] = ly;
+        o.lower_origins[3 * (int64_t)lower + 2] = lz;
+        if (i != 0) continue;
+        o.upper_child_starts[0] = 0;
+        o.tile_keys[0] = tkey;
+        o.upper_origins[0] = ox;
+        o.upper_origins[1] = oy;
+        o.upper_origins[2] = oz;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        o.lower_child_starts[n_lower] = n_leaf;
+        o.upper_child_starts[1] = n_lower;
+    }
+}
+
+}  // namespace
+}  // namespace fvdb
+
+extern "C" size_t fvdb_build_leaf_workspace_bytes(int64_t n) {
+    Sizer s;
+    LeafHashWs w;
+    carve_leafhash(s, n, &w);
+    return s.used + 256;
+}
+
+extern "C" int fvdb_build_leaf_plan(const int64_t* coords, int64_t n, const int64_t* pending_nonfinite, void* workspace,
+                                    size_t ws_bytes, int64_t* counts, int64_t* detail, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n <= 0 || n >= (int64_t)INT32_MAX) return FVDB_ERR_INVALID;
+    Carver c(workspace, ws_bytes);
+    LeafHashWs w;
+    carve_leafhash(c, n, &w);
+    if (!c.ok()) return FVDB_ERR_WORKSPACE;
+    const int64_t cap = w.cap;
+    k_lh_init<<<1, 1, 0, st>>>(w.sc);
+    FVDB_CUDA_TRY(cudaMemsetAsync(w.tkey, 0xFF, (size_t)cap * sizeof(uint32_t), st));
+    FVDB_CUDA_TRY(cudaMemsetAsync(w.tmask, 0, (size_t)cap * 64, st));
+    k_lh_insert<<<grid_for(n), kThreads, 0, st>>>(coords, n, cap, bit_length((uint64_t)cap) - 1, w.tkey, w.tmask, w.sc);
+    k_lh_prep<<<grid_for(cap), kThreads, 0, st>>>(w.tkey, cap, w.key, w.val);
+    FVDB_LAUNCH_CHECK();
+    cub::DoubleBuffer<uint32_t> kb(w.key, w.key_alt);
+    cub::DoubleBuffer<int> vb(w.val, w.val_alt);
+    size_t tb = w.cub_bytes;
+    FVDB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, kb, vb, (int)cap, 0, 28, st));
+    if (kb.Current() != w.key) FVDB_CUDA_TRY(cudaMemcpyAsync(w.key, kb.Current(), cap * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    if (vb.Current() != w.val) FVDB_CUDA_TRY(cudaMemcpyAsync(w.val, vb.Current(), cap * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    k_lh_heads_pop<<<grid_for(cap), kThreads, 0, st>>>(w.key, w.val, cap, w.tmask, w.lower_id, w.pop);
+    FVDB_LAUNCH_CHECK();
+    tb = w.cub_bytes;
+    FVDB_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, w.lower_id, w.lower_id, (int)cap, st));
+    tb = w.cub_bytes;
+    FVDB_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub_tmp, tb, w.pop, w.incl, (int)cap, st));
+    k_lh_pack<<<1, 32, 0, st>>>(w.sc, pending_nonfinite, w.lower_id + (cap - 1), w.incl + (cap - 1), w.pack);
+    FVDB_LAUNCH_CHECK();
+    LeafHashHost h;
+    FVDB_CUDA_TRY(cudaMemcpyAsync(&h, w.pack, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FVDB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h.nonfinite != ~0ull) {
+        *detail = (int64_t)h.nonfinite;
+        return FVDB_ERR_NONFINITE;
+    }
+    if (h.sc.bad_row != ~0ull) {
+        *detail = (int64_t)h.sc.bad_row;
+        return FVDB_ERR_COORD_RANGE;
+    }
+    if (h.sc.key_or != h.sc.key_and || h.sc.overflow || (int64_t)h.sc.n_leaves * 2 > cap)
+        return FVDB_ERR_UNSUPPORTED;  // several root tiles, or a crowded table: the coordinate build
+    counts[0] = 1;
+    counts[1] = h.lower_last;
+    counts[2] = h.sc.n_leaves;
+    counts[3] = h.nv;
+    counts[4] = (int64_t)h.sc.key_or;
+    return FVDB_OK;
+}
+
+extern "C" int fvdb_build_leaf_fill(void* workspace, size_t ws_bytes, int64_t n, const int64_t* counts,
+                                    const fvdb_grid_arrays* out, void* stream_) {
+    cudaStream_t st = as_stream(stream_);
+    if (n <= 0 || n >= (int64_t)INT32_MAX) return FVDB_ERR_INVALID;
+    Carver c(workspace, ws_bytes);
+    LeafHashWs w;
+    carve_leafhash(c, n, &w);
+    if (!c.ok()) return FVDB_ERR_WORKSPACE;
+    const int64_t n_leaf = counts[2];
+    k_lh_register<<<grid_for(n_leaf), kThreads, 0, st>>>(w.key, w.val, n_leaf, w.lower_id, w.tmask, w.pop, w.incl,
+                                                         (uint64_t)counts[4], *out, counts[1]);
+    k_leaf_prefix<<<grid_for(n_leaf), kThreads, 0, st>>>(out->leaf_masks, n_leaf, out->leaf_prefix);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}

@@ -254,3 +254,33 @@ def test_coarsen2_from_leaves_matches_coordinate_build(seed):
     for f in FIELDS:
         assert a[f].dtype == b[f].dtype and np.array_equal(a[f], b[f]), f
     assert fast.num_voxels == ref.num_voxels
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_leaf_hash_build_matches_coordinate_build(seed):
+    """The leaf-hash build (default for one root tile) against the coordinate build (FVDB_BUILD_LEAF=0 path):
+    duplicates, negative coordinates, dense and scattered parts; and its fallback on a multi-tile input."""
+    from paper_2407_01781_b200 import build as B
+    rng = np.random.default_rng(seed)
+    # ~3.6K leaves for ~38K voxels: under half of the n / 4 table entries (a crowded table falls back, below)
+    c = np.concatenate([rng.integers(-2400, -1700, size=(2000, 3)), sphere_shell_coords(80, band=1.5) - 2000,
+                        rng.integers(-2100, -2090, size=(5000, 3))])
+    c = np.concatenate([c, c[:777]])  # duplicates
+    cc = torch.from_numpy(c).cuda()
+    fast = B._build_leaf(cc, P.VoxelTransform.uniform(1.0), "", B.BuildStats())
+    assert fast is not None
+    try:
+        B._LEAF_BUILD = False
+        ref, _ = P.build_from_coords(c)
+    finally:
+        B._LEAF_BUILD = True
+    a, b = fast.to_numpy(), ref.to_numpy()
+    for f in FIELDS:
+        assert a[f].dtype == b[f].dtype and np.array_equal(a[f], b[f]), f
+    assert fast.num_voxels == ref.num_voxels
+    multi = torch.from_numpy(rng.integers(-5000, 5000, size=(1000, 3))).cuda()  # several root tiles
+    assert B._build_leaf(multi, P.VoxelTransform.uniform(1.0), "", B.BuildStats()) is None
+    crowded = torch.from_numpy(rng.integers(0, 4000, size=(20000, 3))).cuda()  # ~1 voxel per leaf
+    assert B._build_leaf(crowded, P.VoxelTransform.uniform(1.0), "", B.BuildStats()) is None
+    g, _ = P.build_from_coords(crowded)  # falls back to the coordinate build
+    assert g.num_voxels == len(np.unique(crowded.cpu().numpy(), axis=0))
