@@ -290,6 +290,10 @@ typedef struct fvdb_halo_plan {
     int32_t* halo_rows;  /* [total] input row per slot, -1 = padding */
     int32_t* perm;       /* [T*128] */
     uint8_t* tile_rec;   /* [T][FVDB_HALO_REC_BYTES] */
+    int32_t offsets_reversed; /* 1: a plan built for this table with its 27 offset rows reversed (the forward
+                                 plan of a same-grid stride-1 map, whose transposed table is exactly that) is
+                                 run on it: phases in reverse order, record offset d read at 26 - d.  The plan
+                                 builders ignore it; only the lockstep kernel (K, N <= 64) accepts 1. */
 } fvdb_halo_plan;
 
 /* color[i] = ((c.x >> shift) + (c.y >> shift) + (c.z >> shift)) & 1, coords int64 [n,3] */
@@ -299,6 +303,8 @@ int fvdb_parity_colors(const int64_t* coords, int64_t n, int shift, uint8_t* col
  * half-pipelines for profiling).  fvdb_conv_halo_tc rejects (FVDB_ERR_INVALID) a plan whose capacity exceeds
  * the running layout's; a plan built for a smaller capacity runs unchanged. */
 int fvdb_halo_cap(int K, int N);
+/* 1 when fvdb_conv_halo_tc for (K, N) accepts plans with offsets_reversed = 1 (the lockstep kernel) */
+int fvdb_halo_reversed_ok(int K, int N);
 /* count pass: writes tile_level, tile_base, phase; total slots -> *total (host). Synchronizes. */
 size_t fvdb_halo_plan_workspace_bytes(int64_t n_out);
 int fvdb_halo_plan_count(const int32_t* nbr, int64_t ld, int64_t n_out, const uint8_t* color_in,

@@ -45,7 +45,7 @@ class GridView(C.Structure):
 class HaloPlan(C.Structure):
     """fvdb_halo_plan"""
     _fields_ = [("num_tiles", C.c_int32), ("halo_cap", C.c_int32)] + [(n, _vp) for n in (
-        "tile_level", "tile_base", "phase", "halo_rows", "perm", "tile_rec")]
+        "tile_level", "tile_base", "phase", "halo_rows", "perm", "tile_rec")] + [("offsets_reversed", C.c_int32)]
 
 
 class GridArrays(C.Structure):
@@ -109,6 +109,7 @@ SIGNATURES = {
     "fvdb_probe_ffma": (_i32, [_i32, _vp, _i64, C.POINTER(C.c_double), _vp]),
     "fvdb_parity_colors": (_i32, [_vp, _i64, _i32, _vp, _vp]),
     "fvdb_halo_cap": (_i32, [_i32, _i32]),
+    "fvdb_halo_reversed_ok": (_i32, [_i32, _i32]),
     "fvdb_halo_plan_workspace_bytes": (_sz, [_i64]),
     "fvdb_halo_plan_count": (_i32, [_vp, _i64, _i64, _vp, C.POINTER(HaloPlan), C.POINTER(_i64), _vp, _sz, _vp]),
     "fvdb_halo_plan_fill": (_i32, [_vp, _i64, _i64, _vp, _vp, C.POINTER(HaloPlan), _vp]),

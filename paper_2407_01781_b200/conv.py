@@ -82,6 +82,7 @@ def _kernel_weights(kernel):
 
 
 _TWO_PASS_PLAN = os.environ.get("FVDB_PLAN_TWO_PASS", "0") == "1"
+_PLAN_SHARE = os.environ.get("FVDB_PLAN_SHARE", "1") != "0"  # transposed same-grid tables run the forward plan reversed
 
 
 class HaloPlan:
@@ -123,6 +124,15 @@ class HaloPlan:
                                               C.byref(c), cap_rows, t["used"].data_ptr(), st), "halo_plan_build")
         self.cap, self.tensors, self.c = cap, t, c
 
+    def reversed(self) -> "HaloPlan":
+        """The same device plan run on the offset-reversed table (fvdb_halo_plan.offsets_reversed = 1)."""
+        r = HaloPlan.__new__(HaloPlan)
+        c = _lib.HaloPlan()
+        C.pointer(c)[0] = self.c
+        c.offsets_reversed = 1 - self.c.offsets_reversed
+        r.cap, r.tensors, r.c = self.cap, self.tensors, c
+        return r
+
     @property
     def total_slots(self):
         """Slots the tiles use (synchronises)."""
@@ -138,10 +148,11 @@ class NbrTable:
     """
 
     __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
-                 "_masks", "sparse", "_steady", "_pairs", "exact_uses", "wgrad_uses", "rows_bound")
+                 "_masks", "sparse", "_steady", "_pairs", "exact_uses", "wgrad_uses", "rows_bound", "rev_src")
 
     def __init__(self, t, n, colors_fn=None, counts=None):
         self.rows_bound = None  # exclusive bound of the input rows in t (known: single-pass halo plans)
+        self.rev_src = None  # NbrTable whose offset rows reversed are this table (halo plans are shared)
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
         self._colors_fn, self._colors, self._plans = colors_fn, None, {}
         self.uses = 0  # bf16 tensor-core convolutions run over this table (conv_impl "auto")
@@ -208,7 +219,10 @@ class NbrTable:
 
     def has_plan(self, K: int, N: int) -> bool:
         cap = int(_lib.lib().fvdb_halo_cap(K, N))
-        return cap in self._plans
+        if cap in self._plans:
+            return True
+        src = self.rev_src if _PLAN_SHARE else None
+        return src is not None and cap in src._plans and bool(_lib.lib().fvdb_halo_reversed_ok(K, N))
 
     @property
     def view(self):
@@ -223,6 +237,15 @@ class NbrTable:
         cap = int(_lib.lib().fvdb_halo_cap(K, N))
         if cap <= 0:
             raise ValueError(f"halo conv does not support K={K}, N={N}")
+        src = self.rev_src if _PLAN_SHARE else None
+        if src is not None and cap not in self._plans and _lib.lib().fvdb_halo_reversed_ok(K, N):
+            # this table is `src` with its offset rows reversed (transposed table of a same-grid stride-1 map):
+            # run src's plan reversed instead of building a second one
+            p = src._plans.get(cap)
+            if p is None:
+                p = src._plans[cap] = HaloPlan(src, cap)
+            self._plans[cap] = p.reversed()
+            return self._plans[cap]
         p = self._plans.get(cap)
         if p is None:
             p = self._plans[cap] = HaloPlan(self, cap)
@@ -390,7 +413,8 @@ class KernelMap:
     def bwd(self) -> NbrTable:
         """Transposed table nbrT[d][i] = o iff nbr[d][o] = i (dgrad / transposed conv), cached."""
         if self._bwd is None:
-            if self._same_grids():
+            flipped = self._same_grids()
+            if flipped:
                 # stride 1 onto the same grid: nbr[d][o] = i  <=>  nbr[26 - d][i] = o (the mirrored offset),
                 # so the transposed table is the forward table with its offset rows reversed (a contiguous
                 # copy instead of the scatter; padding columns are -1 in every row)
@@ -404,6 +428,8 @@ class KernelMap:
                                  counts=self._counts)
             self._bwd.sparse = self.stride == 2  # fine voxel i pairs only offsets d with i - d even: <= 8 of 27
             self._bwd.rows_bound = int(self.num_out)
+            if flipped:
+                self._bwd.rev_src = self.fwd
         return self._bwd
 
     def _same_grids(self):

@@ -754,6 +754,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
     const uint8_t* gen = dsmem - sbase;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int T = P.num_tiles;
+    const bool rev = P.offsets_reversed != 0;
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < NB; ++b) {
@@ -826,6 +827,11 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
         int level = 1, base = 0, off = 0, len = 0;
         if (tile < T) {
             meta(0, level, base, off, len);
+            if (rev && level > 1) {
+                const int32_t* ph = P.phase + ((int64_t)tile * 27 + level - 1) * 2;
+                off = ph[0];
+                len = ph[1];
+            }
             issue_ids(base + off, len, 0);
         }
         while (tile < T) {
@@ -836,8 +842,13 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                 nt = tile + gridDim.x;
                 nk = k + 1;
                 if (nt < T) meta(nk, nlevel, nbase, noff, nlen);
+                if (rev && nt < T && nlevel > 1) {  // reversed plan: the last physical phase comes first
+                    const int32_t* ph = P.phase + ((int64_t)nt * 27 + nlevel - 1) * 2;
+                    noff = ph[0];
+                    nlen = ph[1];
+                }
             } else {  // next offset phase of a multi-phase tile (rare): its slice of the phase table
-                const int32_t* ph = P.phase + ((int64_t)tile * 27 + ng) * 2;
+                const int32_t* ph = P.phase + ((int64_t)tile * 27 + (rev ? level - 1 - ng : ng)) * 2;
                 noff = ph[0];
                 nlen = ph[1];
             }
@@ -937,7 +948,9 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                         dd = C::G * vi + (C::G == 4 ? t0 : (t0 >> 1));
                         ok = dd >= d0 && dd < d_end;
                     }
-                    const uint16_t* lr = lb + dd * kTileRows + lrow;
+                    // reversed plan: processing phase g holds physical phase level-1-g, whose forward offsets
+                    // 26 - d are this table's offsets d in [g*gs, (g+1)*gs)
+                    const uint16_t* lr = lb + (rev ? 26 - dd : dd) * kTileRows + lrow;
                     const int sl[4] = {ok ? lr[0] : kNoSlot, ok ? lr[8] : kNoSlot, ok ? lr[16] : kNoSlot,
                                        ok ? lr[24] : kNoSlot};
                     mbar_wait(smem_u32(&bar_afree[set][ak]), (ause & 1) ^ 1);
@@ -2261,6 +2274,7 @@ int halo_kernel_cap() {
 
 template <int K, int N, bool OB>
 int launch_halo(const void* in, const void* wimg, const fvdb_halo_plan& P, int64_t n_out, void* out, cudaStream_t st) {
+    if (P.offsets_reversed && !(use_halo4<K, N>() && !use_halo2<K, N>())) return FVDB_ERR_UNSUPPORTED;
     if (use_halo2<K, N>()) return launch_halo2<OB>(in, wimg, P, n_out, out, st);
     if (use_halo4<K, N>()) return launch_halo4<K, N, OB>(in, wimg, P, n_out, out, st);
     if (halo_variant<K, N>() == 1) return launch_halo_v<K, N, OB, 1>(in, wimg, P, n_out, out, st);
@@ -2288,6 +2302,17 @@ extern "C" int fvdb_parity_colors(const int64_t* coords, int64_t n, int shift, u
     k_parity_colors<<<(unsigned)cmin((int)ceil_div(n, 256), 4096), 256, 0, as_stream(stream)>>>(coords, n, shift, color);
     FVDB_LAUNCH_CHECK();
     return FVDB_OK;
+}
+
+// 1 when the kernel fvdb_conv_halo_tc runs for (K, N) accepts plans with offsets_reversed = 1
+extern "C" int fvdb_halo_reversed_ok(int K, int N) {
+    int ok = 0;
+    halo_dispatch(K, N, [&](auto k, auto n) {
+        constexpr int KK = decltype(k)::value, NN = decltype(n)::value;
+        ok = use_halo4<KK, NN>() && !use_halo2<KK, NN>();
+        return 0;
+    });
+    return ok;
 }
 
 extern "C" int fvdb_halo_cap(int K, int N) {

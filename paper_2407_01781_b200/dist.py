@@ -124,6 +124,7 @@ class RowShard:
         self.fwd = NbrTable(t, n, colors, counts=counts)
         self.dgrad = NbrTable(torch.flip(t, dims=[0]), n, colors, counts=counts)
         self.fwd.rows_bound = self.dgrad.rows_bound = int(grid.num_voxels)
+        self.dgrad.rev_src = self.fwd  # stride 1, one grid: the dgrad table is the forward table reversed
         self.counts = counts
 
     @property

@@ -50,16 +50,18 @@ def check_plan(table, K, N):
     order = np.argsort(t["tile_base"], kind="stable")
     assert np.all(t["tile_base"][order][1:] >= ends[order][:-1]), "tile slot ranges overlap"
     assert ends.max() <= hr.shape[0]
+    rev = bool(plan.c.offsets_reversed)  # the forward plan run on the reversed (transposed) table
     for tile in range(T):
         gs = 27 // level[tile]
         for d in range(27):
-            g = d // gs
+            rd = 26 - d if rev else d
+            g = rd // gs
             off, cnt = phase[tile, g]
             assert cnt <= plan.cap and cnt % 8 == 0
             lanes = np.arange(128)
             o = perm[tile]
             want = np.where(o >= 0, nbr[d][np.maximum(o, 0)], -1)
-            s = lnbr[d, tile]
+            s = lnbr[rd, tile]
             has = s != 0xFFFF
             assert np.array_equal(has, want >= 0), (tile, d)
             assert np.all(s[has] < cnt)
@@ -67,7 +69,7 @@ def check_plan(table, K, N):
             assert np.array_equal(got, want[has]), (tile, d)
             bits = np.zeros(128, bool)
             for wd in range(4):
-                bits[32 * wd:32 * wd + 32] = (masks[tile, d, wd] >> np.arange(32, dtype=np.uint32)) & 1
+                bits[32 * wd:32 * wd + 32] = (masks[tile, rd, wd] >> np.arange(32, dtype=np.uint32)) & 1
             assert np.array_equal(bits, ~has), (tile, d)
             del lanes
     return plan
@@ -186,6 +188,33 @@ def test_halo_offset_pairs_across_phases(K, N, cap):
     gi = gather_conv(torch.from_numpy(gy).cuda().to(torch.bfloat16), km.bwd, torch.from_numpy(w2).cuda(),
                      transpose=True, out_dtype=torch.float32, impl="halo")
     gi_r, _ = O.conv_backward(ins, outs, bf16_round(gy), bf16_round(np.zeros((n, N), np.float32)), bf16_round(w2))
+    assert rel(gi, gi_r) < 2e-5
+
+
+@pytest.mark.parametrize("K,N", [(64, 64), (32, 32), (32, 64), (64, 32)])
+def test_dgrad_runs_the_forward_plan_reversed(K, N):
+    """A same-grid stride-1 map's transposed table is its forward table with the offset rows reversed; the dgrad
+    runs the forward plan with offsets_reversed = 1 (phases in reverse order, record offset 26 - d).  Small-capacity
+    plans force multi-phase tiles."""
+    from paper_2407_01781_b200.conv import HaloPlan
+    c = dense_cube(20)
+    g, _ = P.build_from_coords(c)
+    og = O.build_from_coords(c)
+    km = P.build_kernel_map(g, g, 1)
+    ins, outs = O.kernel_map(og, og, 1)
+    kcap = int(P._lib.lib().fvdb_halo_cap(N, K))
+    km.fwd._plans[kcap] = HaloPlan(km.fwd, 256)
+    assert (km.fwd._plans[kcap].tensors["tile_level"] > 1).any()
+    plan = km.bwd.halo_plan(N, K)
+    assert plan.c.offsets_reversed == 1 and plan.tensors is km.fwd._plans[kcap].tensors
+    check_plan(km.bwd, N, K)
+    rng = np.random.default_rng(K * 3 + N)
+    n = g.num_voxels
+    w = (rng.normal(size=(N, K, 3, 3, 3)) / np.sqrt(27 * K)).astype(np.float32)
+    gy = rng.normal(size=(n, N)).astype(np.float32)
+    gi = gather_conv(torch.from_numpy(gy).cuda().to(torch.bfloat16), km.bwd, torch.from_numpy(w).cuda(),
+                     transpose=True, out_dtype=torch.float32, impl="halo")
+    gi_r, _ = O.conv_backward(ins, outs, bf16_round(gy), bf16_round(np.zeros((n, K), np.float32)), bf16_round(w))
     assert rel(gi, gi_r) < 2e-5
 
 
