@@ -316,6 +316,10 @@ def run_ours(args, rank, world, local_rank):
     from paper_2407_01781_b200.conv import HaloPlan
     for name, tab, k, n, on in (("halo_plan_fwd", t_fwd, cin, cout, impl_f == "halo"),
                                 ("halo_plan_dgrad", t_dgrad, cout, cin, impl_b == "halo")):
+        if on and getattr(tab, "rev_src", None) is not None and _L.lib().fvdb_halo_reversed_ok(k, n) and \
+                os.environ.get("FVDB_PLAN_SHARE", "1") != "0":
+            stages[name] = dict(device_ms=0.0, wall_ms=0.0, shared="the forward plan, run with offsets reversed")
+            continue
         if on:  # steady state (warm allocator: a loop that rebuilds its maps), then cache the table's own plan
             cap = int(_L.lib().fvdb_halo_cap(k, n))
             _, dv, wl = stage(torch, lambda: HaloPlan(tab, cap), reps=3)

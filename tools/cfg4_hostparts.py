@@ -21,7 +21,8 @@ def wrap(name, fn):
 
 
 for n in ("fvdb_build_plan2", "fvdb_build_fill", "fvdb_quantize_points_async", "fvdb_coarsen2_plan",
-          "fvdb_coarsen2_fill", "fvdb_build_workspace_bytes", "fvdb_coarsen2_workspace_bytes"):
+          "fvdb_coarsen2_fill", "fvdb_build_workspace_bytes", "fvdb_coarsen2_workspace_bytes",
+          "fvdb_build_leaf_plan", "fvdb_build_leaf_fill", "fvdb_build_leaf_workspace_bytes"):
     setattr(L, n, wrap(n, getattr(L, n)))
 B._alloc_arrays = wrap("_alloc_arrays", B._alloc_arrays)
 _lib.workspace = wrap("workspace", _lib.workspace)
