@@ -435,7 +435,11 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         // loaded before its copies are issued (a runtime-trip loop serialised one LDS latency per copy)
         constexpr int RPP = 128 / ACH, NPASS = C::TK / RPP;
         static_assert(RPP * NPASS == C::TK, "gather mapping");
-        const int c = pt % ACH, r0 = pt / ACH;
+        // thread -> (chunk c, row r0).  With 4 chunks per row (Cin 32) the 8 threads of a shared-memory phase write
+        // two rows; rows r and r ^ 1 map their chunks onto the same 4 banks of the 128B swizzle (41% of the
+        // kernel's shared wavefronts were bank conflicts at cfg5), rows r and r ^ 4 onto complementary ones
+        const int c = pt % ACH, j = pt / ACH;
+        const int r0 = ACH == 4 ? ((((j >> 1) >> 2) << 3) | ((j & 1) << 2) | ((j >> 1) & 3)) : j;
         uint32_t roff[NPASS][C::OPB];                                 // swizzled offset inside an M-block
 #pragma unroll
         for (int p = 0; p < NPASS; ++p)
