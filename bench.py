@@ -491,7 +491,7 @@ def compare_schedules(torch, flush, x, table, w, reps=10):
 
 def run_fresh(torch, P, dev, x, gy, w):
     """A step on a map seen for the first time (a training loop that rebuilds grids per batch): grid build,
-    kernel map, transposed table and fwd + dgrad + wgrad through the first-use kernels."""
+    kernel map, transposed table and fwd + dgrad + wgrad with the kernels `auto` picks for a new map."""
     from paper_2407_01781_b200.conv import gather_conv, wgrad
     from paper_2407_01781_b200.workloads import sphere_shell_coords
     c = torch.from_numpy(sphere_shell_coords(470, band=1.5)).to(dev)
@@ -510,7 +510,8 @@ def run_fresh(torch, P, dev, x, gy, w):
         if best is None or wl < best[0]:
             best = (wl, dv)
     return {"wall_ms": round(best[0], 3), "device_ms": round(best[1], 3),
-            "what": "build_from_coords + build_kernel_map + transposed table + fwd/dgrad/wgrad on first-use kernels"}
+            "what": "build_from_coords + build_kernel_map + transposed table + fwd/dgrad/wgrad as the auto policy runs a "
+                    "map's first step (same-grid map: the halo kernel with one plan shared by fwd and dgrad)"}
 
 
 def run_special(args, rank, world, local_rank, cfg):

@@ -148,11 +148,13 @@ class NbrTable:
     """
 
     __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
-                 "_masks", "sparse", "_steady", "_pairs", "exact_uses", "wgrad_uses", "rows_bound", "rev_src")
+                 "_masks", "sparse", "_steady", "_pairs", "exact_uses", "wgrad_uses", "rows_bound", "rev_src",
+                 "plan_shared")
 
     def __init__(self, t, n, colors_fn=None, counts=None):
         self.rows_bound = None  # exclusive bound of the input rows in t (known: single-pass halo plans)
         self.rev_src = None  # NbrTable whose offset rows reversed are this table (halo plans are shared)
+        self.plan_shared = False  # one halo plan serves this table and its reversed partner (fwd + dgrad)
         self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
         self._colors_fn, self._colors, self._plans = colors_fn, None, {}
         self.uses = 0  # bf16 tensor-core convolutions run over this table (conv_impl "auto")
@@ -353,6 +355,8 @@ class KernelMap:
             table._colors_fn = _colors_fn(self._grids, self.stride, False)
         self.fwd = table
         self._counts = pair_counts
+        if self._same_grids():  # its transposed table will run this table's halo plan reversed
+            table.plan_shared = True
 
     def grids(self):
         """(grids_in, grids_out) the map was built for, or None (unknown, or a grid was released)."""
@@ -430,6 +434,7 @@ class KernelMap:
             self._bwd.rows_bound = int(self.num_out)
             if flipped:
                 self._bwd.rev_src = self.fwd
+                self._bwd.plan_shared = True
         return self._bwd
 
     def _same_grids(self):
@@ -561,6 +566,12 @@ def halo_kernel_name(K: int, N: int) -> str:
 
 
 HALO_AFTER_USES = 3  # conv_impl "auto": uses of a table before its halo plan is built (plan ~ 1.2 gather convs)
+
+
+def halo_shares_plan(K: int, N: int) -> bool:
+    """Both directions of a (K, N) layer run the lockstep halo kernel, which takes reversed plans."""
+    L = _lib.lib()
+    return bool(L.fvdb_halo_reversed_ok(K, N)) and bool(L.fvdb_halo_reversed_ok(N, K))
 SORT_BELOW_DENSITY = 10.0  # gather kernel: signature-sort tables with fewer mean pairs per row
 
 
@@ -621,7 +632,9 @@ def conv_impl() -> str:
       plan (one pass, no host read-back) costs about what one use saves (cfg2: 0.40 ms; 0.66 ms gather vs
       0.32 ms halo per conv), so it pays off for maps reused across layers and training iterations, not
       for maps used once or twice (cfg4 rebuilds its maps every step and uses each in one forward and one
-      backward);
+      backward).  A same-grid stride-1 map's forward and transposed tables share one plan (run reversed),
+      so with K, N <= 64 those take the halo kernel from their first use (the plan pays within one
+      forward + input-gradient pair);
     * "halo" / "gather": always that kernel.
     """
     v = os.environ.get("FVDB_CONV_IMPL", "auto")
@@ -750,8 +763,12 @@ def gather_conv(x: torch.Tensor, nbr: NbrTable, w: torch.Tensor, transpose: bool
         impl = _image_impl(w_image, K, N)  # the image decides
     else:
         impl = impl or conv_impl()
-        if impl == "auto":  # first uses: gather; reused tables: steady_impl (halo or sorted gather)
-            reuse = nbr.uses >= HALO_AFTER_USES or nbr.has_plan(K, N)
+        if impl in ("auto", "auto-reuse"):  # first uses: gather; reused tables: steady_impl (halo or sorted gather)
+            # a plan shared by a same-grid map's forward and transposed tables pays within one training step
+            # (forward + input gradient: 0.40 ms plan vs 2 x 0.34 ms saved at cfg2), so under "auto" those go halo
+            # at once ("auto-reuse": the reference variants igemm / lggs keep the gather kernel for a new map)
+            reuse = (nbr.uses >= HALO_AFTER_USES or nbr.has_plan(K, N)
+                     or (impl == "auto" and nbr.plan_shared and _PLAN_SHARE and halo_shares_plan(K, N)))
             impl = steady_impl(nbr, K, N)[0] if reuse else "gather"
             if impl == "halo" and n_out >= INT32_ROWS_LIMIT:
                 impl = "gather"
@@ -887,11 +904,11 @@ def variant_impl(variant, dtype):
     exact neighbourhood in shared memory once (a window fitted to the data instead of a fixed box) and builds
     every offset's operand from it: ``leaf`` / ``brick`` run it from the first call (building the tile plan).
     ``igemm`` / ``lggs`` (gather-GEMM-scatter) keep the reuse policy (``conv_impl``): the gather kernel for a
-    map's first uses, then the steady kernel.  Measured on B200 (bench.py --config dense*, fwd ms): dense 128^3
+    map's first uses, then the steady kernel (``auto-reuse``: without ``auto``'s first-use halo for shared plans).  Measured on B200 (bench.py --config dense*, fwd ms): dense 128^3
     at 64 ch, gather 1.30 vs halo 0.64."""
     if dtype == torch.bfloat16 and variant in ("leaf", "brick"):
         return "halo"
-    return None
+    return "auto-reuse" if conv_impl() == "auto" else None
 
 
 def conv(grid_in, features, kernel, grid_out=None, variant="igemm", stride=1, kmap=None, stats=None):

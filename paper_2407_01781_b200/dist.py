@@ -125,6 +125,7 @@ class RowShard:
         self.dgrad = NbrTable(torch.flip(t, dims=[0]), n, colors, counts=counts)
         self.fwd.rows_bound = self.dgrad.rows_bound = int(grid.num_voxels)
         self.dgrad.rev_src = self.fwd  # stride 1, one grid: the dgrad table is the forward table reversed
+        self.fwd.plan_shared = self.dgrad.plan_shared = True
         self.counts = counts
 
     @property
