@@ -462,7 +462,7 @@ def build_kernel_map(grid_in, grid_out, stride=1):
     L = _lib.lib()
     wsb = L.fvdb_kmap_workspace_bytes(grid_out.num_leaf_nodes)
     ws = _lib.workspace(wsb, dev)
-    _lib.check(L.fvdb_kernel_map(C.byref(grid_in.view()), C.byref(grid_out.view()), stride, t.data_ptr(),
+    _lib.check(L.fvdb_kernel_map(C.byref(grid_in.view()), C.byref(grid_out.leaf_view()), stride, t.data_ptr(),
                                  t.shape[1], counts.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()),
                "kernel_map")
     return KernelMap(num_in=grid_in.num_voxels, num_out=n_out, stride=stride, table=NbrTable(t, n_out),
@@ -489,7 +489,7 @@ def build_batch_kernel_map(batch_in, batch_out, stride=1):
     counts = torch.zeros(27, dtype=torch.int64, device=dev)
     L = _lib.lib()
     views_in = (_lib.GridView * B)(*[g.view() for g in gi])
-    views_out = (_lib.GridView * B)(*[g.view() for g in go])
+    views_out = (_lib.GridView * B)(*[g.leaf_view() for g in go])  # output grids are never probed
     in_base = (C.c_int64 * B)(*[int(v) for v in batch_in.voxel_joffsets[:, 0].tolist()])
     out_base = (C.c_int64 * B)(*[int(v) for v in batch_out.voxel_joffsets[:, 0].tolist()])
     wsb = L.fvdb_kmap_workspace_bytes(sum(g.num_leaf_nodes for g in go))

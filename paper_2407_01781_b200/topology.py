@@ -147,6 +147,23 @@ class IndexGrid:
         return self.leaf_origins.min(dim=0).values, self.leaf_origins.max(dim=0).values + (LEAF_SPAN - 1)
 
     # -- C-ABI view ----------------------------------------------------------
+    def leaf_view(self) -> _lib.GridView:
+        """GridView for kernels that read only the leaf arrays (a kernel map's OUTPUT grid): no node tables, so
+        no table build (memsets + two kernels) for a grid that is never probed."""
+        if self._view is not None:
+            return self._view
+        v = _lib.GridView()
+        v.tile_keys = self.tile_keys.data_ptr()
+        v.leaf_keys = self.leaf_keys.data_ptr()
+        v.leaf_origins = self.leaf_origins.data_ptr()
+        v.leaf_masks = self.leaf_masks.data_ptr()
+        v.leaf_prefix = self.leaf_prefix.data_ptr()
+        v.leaf_value_offset = self.leaf_value_offset.data_ptr()
+        v.num_upper = self.num_upper_nodes
+        v.num_leaf = self.num_leaf_nodes
+        v.num_voxels = self.num_voxels
+        return v
+
     def view(self) -> _lib.GridView:
         if self._view is None:
             v = _lib.GridView()
