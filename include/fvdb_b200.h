@@ -324,6 +324,16 @@ int fvdb_halo_plan_fill(const int32_t* nbr, int64_t ld, int64_t n_out, const uin
 int fvdb_halo_plan_build(const int32_t* nbr, int64_t ld, int64_t n_out, int64_t n_in, const uint8_t* color_in,
                          const uint8_t* q_out, const fvdb_halo_plan* plan, int64_t halo_rows_capacity,
                          int32_t* counter, void* stream);
+/* Weight gradient on a halo plan (Cin = Cout = 32; conv.py:367): each tile's staged halo feeds A = x^T into TMEM
+ * (ldmatrix.trans -> tcgen05.st), B = the tile's grad_out rows; per-CTA partials summed in CTA order
+ * (deterministic).  gw fp32 [Cout][Cin][27] as fvdb_conv_wgrad_tc.  plan: the table's own (not reversed) plan
+ * with halo_cap <= the kernel's capacity.  FVDB_ERR_UNSUPPORTED for other channel counts. */
+size_t fvdb_wgrad_halo_workspace_bytes(int64_t n_out);
+int fvdb_conv_wgrad_halo(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,
+                         const fvdb_halo_plan* plan, int64_t n_out, float* gw, void* workspace,
+                         size_t workspace_bytes, void* stream);
+/* gw[co][ci][d] = sum over s < splits of part[s][d][ci][co], in split order */
+int fvdb_wgrad_reduce_parts(const float* part, int splits, int cin, int cout, float* gw, void* stream);
 /* B images for the halo kernel: as fvdb_pack_weights_umma with the K index permuted to the
  * TMEM A layout the kernel's tcgen05.st produces, followed by copies of offsets 0..6 so that any
  * run of up to 8 consecutive offsets (mod 27) is one contiguous TMA copy.

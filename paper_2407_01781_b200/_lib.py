@@ -110,6 +110,9 @@ SIGNATURES = {
     "fvdb_parity_colors": (_i32, [_vp, _i64, _i32, _vp, _vp]),
     "fvdb_halo_cap": (_i32, [_i32, _i32]),
     "fvdb_halo_reversed_ok": (_i32, [_i32, _i32]),
+    "fvdb_wgrad_halo_workspace_bytes": (_sz, [_i64]),
+    "fvdb_conv_wgrad_halo": (_i32, [_vp, _i64, _i32, _vp, _i32, C.POINTER(HaloPlan), _i64, _vp, _vp, _sz, _vp]),
+    "fvdb_wgrad_reduce_parts": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp]),
     "fvdb_halo_plan_workspace_bytes": (_sz, [_i64]),
     "fvdb_halo_plan_count": (_i32, [_vp, _i64, _i64, _vp, C.POINTER(HaloPlan), C.POINTER(_i64), _vp, _sz, _vp]),
     "fvdb_halo_plan_fill": (_i32, [_vp, _i64, _i64, _vp, _vp, C.POINTER(HaloPlan), _vp]),

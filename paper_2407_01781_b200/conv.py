@@ -833,6 +833,20 @@ def wgrad_pairs_enabled(nbr: "NbrTable", cin: int, cout: int) -> bool:
     return nbr.n > 0 and nbr.density() < WG_PAIRS_BELOW_DENSITY
 
 
+def wgrad_halo_enabled(nbr: "NbrTable", cin: int, cout: int) -> bool:
+    """Run the bf16 weight gradient on the table's halo plan (fvdb_conv_wgrad_halo, Cin = Cout = 32)?
+
+    The table kernel is bound by shared memory at 32x32 (per 16-cycle MMA it writes the gathered 4 KB A block
+    and reads it back with B); the halo form builds A = xᵀ in TMEM from the staged halo, so an MMA reads only B
+    from shared memory.  Measured on B200 (cfg5, bench.py): 3.59 ms vs 2.83 for the table kernel -- its
+    hand-off skeleton alone (FVDB_DEBUG_WGH=15: no MMA, no A build, no loads) takes 2.0 ms, so it is opt-in.
+    Env FVDB_WG_HALO: "force" whenever the shape allows (the table's own plan is built if missing), else never.
+    """
+    if cin != 32 or cout != 32 or nbr.n >= INT32_ROWS_LIMIT:
+        return False
+    return os.environ.get("FVDB_WG_HALO") == "force"
+
+
 def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: NbrTable) -> torch.Tensor:
     """gw[co][ci][d] = Σ_o go[o,co]·x[nbr[d][o],ci]  → [Cout, Cin, 3, 3, 3] (fp32 for bf16 inputs)."""
     n_out = nbr.n
@@ -860,6 +874,14 @@ def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: NbrTable) -> torch.Tensor:
         gw = wgrad(_pad_cols(x, ci_p), _pad_cols(go, co_p), nbr)
         return gw[:cout, :cin].contiguous()
     gw = torch.empty((cout, cin, 3, 3, 3), dtype=torch.float32, device=x.device)
+    if wgrad_halo_enabled(nbr, cin, cout):  # xᵀ in TMEM from the table's halo plan (csrc/conv_halo.cu)
+        nbr.wgrad_uses += 1
+        plan = nbr.halo_plan(cin, cout)
+        wsb = L.fvdb_wgrad_halo_workspace_bytes(n_out)
+        ws = _lib.workspace(wsb, x.device)
+        _lib.check(L.fvdb_conv_wgrad_halo(x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, C.byref(plan.c), n_out,
+                                          gw.data_ptr(), ws.data_ptr(), wsb, st), "conv_wgrad_halo")
+        return gw
     use_pairs = wgrad_pairs_enabled(nbr, cin, cout)
     nbr.wgrad_uses += 1
     if use_pairs:

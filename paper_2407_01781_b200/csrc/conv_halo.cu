@@ -1453,6 +1453,302 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Halo2Cfg::THREADS, 1
 }
 
 // ---------------------------------------------------------------------------------------------
+// k_wgrad_halo32: weight gradient at Cin = Cout = 32 on the forward table's halo plan, A = xᵀ in TMEM
+//
+// dW[d][ci][co] = Σ_o x[nbr[d][o]][ci] · g[o][co]  (conv.py:367).  The table kernel (conv_tc.cu) gathers every
+// pair's input row into shared memory by cp.async and multiplies SS: per 16-cycle M128·N32·K16 MMA it writes 4 KB
+// and reads 4 + 1 KB of shared memory (72 cycles at 128 B/clk, ~22% of the tensor peak at best).  Here each tile's
+// halo (its unique input rows, staged once by the forward plan's loader) feeds A = xᵀ straight into TMEM:
+// ldmatrix.trans turns 8 halo rows (any slots: per-row addresses) x 8 channels into the tcgen05.st.16x256b
+// fragment (lane = channel, column = a pair of tile lanes), so an MMA reads only its 1 KB of B from shared memory.
+//   M-block mb = offsets 4mb .. 4mb + 3 (TMEM lane quarter q = offset 4mb + q, lane = input channel); K = the
+//   tile's 128 lanes in the order pi below; N = 32 output channels.  All 7 M-blocks' accumulators stay in TMEM
+//   (7 x 32 columns) for the CTA's whole run; two builder sets take alternate M-blocks, each with two 64-column
+//   A slots, as in k_conv_halo4.  B = the tile's grad_out rows gathered in the same K order (64B-swizzled,
+//   MN-major).  Partials [cta][27][32][32] are summed in CTA order by k_wgrad_tc_reduce (deterministic).
+// K order: 16x256b register 4c + 2e + (lane half) at column 8c + 2t0 + e holds ldmatrix matrix 2(lane half) + e,
+// whose thread t0 pair is tile lanes 16c + 8e + 2t0 + {0,1}: MMA K index 16c + 4t0 + 2e + h <-> tile lane
+// 16c + 8e + 2t0 + h.
+// Halo rows (64 B) keep chunk c of slot s at c ^ ((s >> 1) & 3): an ldmatrix matrix reads 8 tile lanes, which
+// alternate colour (the plan pairs lanes 2p, 2p + 1 by output parity) and step each colour's slot by 2 in the
+// typical run, so the 8 rows fill the 8 bank groups.
+// ---------------------------------------------------------------------------------------------
+// stage = (M-block, half of the tile's 128 lanes): 4 MMAs; M-block mb belongs to set mb % 4 (one issuer per
+// accumulator: a fixed accumulation order)
+constexpr int kWhMB = 7, kWhSets = 4, kWhAsl = 2, kWhAcols = 32, kWhDcols = kWhMB * 32;
+constexpr int kWhRowb = 64, kWhNB = 2;
+constexpr int kWhB = kTileRows * kWhRowb;  // one tile's grad_out rows
+struct WhCfg {
+    static constexpr int FIXED = 1024 + kWhNB * kWhB + kWhNB * kIdxBytes + kWhRowb;  // + zero row
+    static constexpr int CAP = ((kSmemMax - 2048 - FIXED) / (kWhNB * (kWhRowb + 4))) & ~7;
+    static constexpr int SMEM = FIXED + kWhNB * CAP * (kWhRowb + 4);
+    static constexpr int THREADS = (2 + 4 * kWhSets + kWhSets + 4) * 32;
+    static constexpr uint32_t IDESC = idesc_bf16_f32(kTileRows, 32, false, true);
+    static_assert(kWhDcols + kWhSets * kWhAsl * kWhAcols <= 512, "TMEM");
+};
+__device__ __forceinline__ int wh_lane_of_k(int kk) {  // MMA K index -> tile lane (pi)
+    const int c = kk >> 4, t0 = (kk >> 2) & 3, e = (kk >> 1) & 1, h = kk & 1;
+    return 16 * c + 8 * e + 2 * t0 + h;
+}
+// slot = 2 * rank + colour (the plan): consecutive same-colour neighbours step the slot by 2, so bits 1-2 rotate
+__device__ __forceinline__ uint32_t wh_chunk(uint32_t s, int c) { return (uint32_t)(c ^ ((s >> 1) & 3)); }
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(WhCfg::THREADS, 1)
+    k_wgrad_halo32(const bf16* __restrict__ in, const bf16* __restrict__ go, fvdb_halo_plan P, int64_t n_out,
+                   float* __restrict__ part, int dbg) {  // dbg (profiling): 1 no MMA, 2 no A build, 4 no B, 8 no halo
+    using C = WhCfg;
+    constexpr int NB = kWhNB, SETS = kWhSets, ASL = kWhAsl;
+    constexpr int W_LOAD = 0, W_BLOAD = 1, W_BLD = 2, W_ISS = 2 + 4 * SETS, W_EPI = W_ISS + SETS;
+    extern __shared__ uint8_t dsmem[];
+    __shared__ __align__(8) uint64_t bar_hfull[NB], bar_hempty[NB], bar_xfull[NB], bar_ifull[NB], bar_iempty[NB];
+    __shared__ __align__(8) uint64_t bar_bfull[NB], bar_bempty[NB], bar_afree[SETS][ASL], bar_dfull;
+    __shared__ uint32_t tmem_slot;
+    const uint32_t sbase = smem_u32(dsmem);
+    const uint32_t gbase = (sbase + 1023u) & ~1023u;          // grad_out tiles [NB][128][64]
+    const uint32_t ibase = gbase + NB * kWhB;                  // tile records [NB]
+    const uint32_t zrow = ibase + NB * kIdxBytes;              // one zero row
+    const uint32_t hbase = zrow + kWhRowb;                     // halo rows [NB][CAP][64]
+    const uint32_t xbase = hbase + NB * C::CAP * kWhRowb;      // halo row ids [NB][CAP]
+    const uint8_t* gen = dsmem - sbase;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int T = P.num_tiles;
+    const bool rev = P.offsets_reversed != 0;
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NB; ++b) {
+            mbar_init(smem_u32(&bar_hfull[b]), 32);
+            mbar_init(smem_u32(&bar_hempty[b]), 4 * SETS);
+            mbar_init(smem_u32(&bar_xfull[b]), 1);
+            mbar_init(smem_u32(&bar_ifull[b]), 1);
+            mbar_init(smem_u32(&bar_iempty[b]), 4 * SETS);
+            mbar_init(smem_u32(&bar_bfull[b]), 32);
+            mbar_init(smem_u32(&bar_bempty[b]), SETS);
+        }
+        for (int s = 0; s < SETS; ++s)
+            for (int k = 0; k < ASL; ++k) mbar_init(smem_u32(&bar_afree[s][k]), 1);
+        mbar_init(smem_u32(&bar_dfull), SETS);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < kWhRowb / 4) reinterpret_cast<uint32_t*>(dsmem + (zrow - sbase))[threadIdx.x] = 0u;
+    if (warp == W_BLOAD) tmem_alloc(smem_u32(&tmem_slot), 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == W_LOAD) {
+        // ---------------- halo loader: row ids (TMA), rows (cp.async, swizzled chunks), record (TMA) ----------------
+        int tile = blockIdx.x, g = 0;
+        uint32_t pc = 0;
+        auto phase_of = [&](int t, int gg, int lvl) {
+            const int32_t* ph = P.phase + ((int64_t)t * 27 + (rev ? lvl - 1 - gg : gg)) * 2;
+            return make_int2(P.tile_base[t] + ph[0], ph[1]);
+        };
+        auto issue_ids = [&](int2 ol, uint32_t buf) {
+            if (lane == 0) {
+                mbar_arrive_expect_tx(smem_u32(&bar_xfull[buf]), (uint32_t)ol.y * 4u);
+                if (ol.y > 0) bulk_g2s(xbase + buf * C::CAP * 4, P.halo_rows + ol.x, (uint32_t)ol.y * 4u, smem_u32(&bar_xfull[buf]));
+            }
+        };
+        int level = tile < T ? P.tile_level[tile] : 1;
+        int len = 0;
+        if (tile < T) {
+            const int2 ol = phase_of(tile, 0, level);
+            len = ol.y;
+            issue_ids(ol, 0);
+        }
+        while (tile < T) {
+            int ng = g + 1, nt = tile;
+            if (ng >= level) { ng = 0; nt = tile + gridDim.x; }
+            const int nlevel = ng == 0 ? (nt < T ? P.tile_level[nt] : 1) : level;
+            const uint32_t buf = pc % NB, par = (pc / NB) & 1;
+            int nlen = 0;
+            if (nt < T) {
+                const int2 ol = phase_of(nt, ng, nlevel);
+                nlen = ol.y;
+                issue_ids(ol, (pc + 1) % NB);
+            }
+            mbar_wait(smem_u32(&bar_xfull[buf]), par);
+            mbar_wait(smem_u32(&bar_hempty[buf]), par ^ 1);
+            if (lane == 0) {
+                mbar_wait(smem_u32(&bar_iempty[buf]), par ^ 1);
+                mbar_arrive_expect_tx(smem_u32(&bar_ifull[buf]), (uint32_t)kRecBytes);
+                bulk_g2s(ibase + buf * kIdxBytes, P.tile_rec + (int64_t)tile * kIdxBytes, (uint32_t)kRecBytes,
+                         smem_u32(&bar_ifull[buf]));
+            }
+            const int32_t* ids = reinterpret_cast<const int32_t*>(gen + xbase + buf * C::CAP * 4);
+            const uint32_t hb = hbase + buf * C::CAP * kWhRowb;
+            const int q = lane >> 2, c = lane & 3;  // 8 rows x 4 chunks per instruction
+            for (int s0 = 0; s0 < len; s0 += 32) {
+                int r[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int s = s0 + 8 * k + q;
+                    r[k] = s < len ? ids[s] : -1;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int s = s0 + 8 * k + q;
+                    if (r[k] >= 0 && !(dbg & 8)) cp_async_16(hb + s * kWhRowb + (wh_chunk((uint32_t)s, c) << 4), in + (int64_t)r[k] * 32 + c * 8, 16u);
+                }
+            }
+            cp_async_arrive_noinc(smem_u32(&bar_hfull[buf]));
+            __syncwarp();
+            ++pc;
+            tile = nt;
+            g = ng;
+            len = nlen;
+            level = nlevel;
+        }
+    } else if (warp == W_BLOAD) {
+        // ---------------- grad_out rows of each tile in the MMA's K order (64B swizzle, MN-major B) ----------------
+        uint32_t lt = 0;
+        for (int tile = blockIdx.x; tile < T; tile += gridDim.x, ++lt) {
+            const uint32_t buf = lt % NB, par = (lt / NB) & 1;
+            mbar_wait(smem_u32(&bar_bempty[buf]), par ^ 1);
+            const uint32_t gb = gbase + buf * kWhB;
+#pragma unroll 4
+            for (int i = lane; i < kTileRows * 4 && !(dbg & 4); i += 32) {
+                const int kk = i >> 2, c = i & 3;
+                const int o = P.perm[(int64_t)tile * kTileRows + wh_lane_of_k(kk)];
+                const uint32_t dst = gb + kk * 64 + ((c ^ ((kk >> 1) & 3)) << 4);
+                cp_async_16(dst, go + (int64_t)(o < 0 ? 0 : o) * 32 + c * 8, o < 0 ? 0u : 16u);
+            }
+            cp_async_arrive_noinc(smem_u32(&bar_bfull[buf]));
+        }
+    } else if (warp >= W_BLD && warp < W_BLD + 4 * SETS) {
+        // ---------------- builders: xᵀ of offset 4mb + q into TMEM lanes 32q.. (ldmatrix.trans -> 16x256b) ----------
+        const int set = (warp - W_BLD) / 4, q = warp & 3;
+        const int m = lane >> 3, rr = lane & 7, kb = (m & 1) * 8;
+        uint32_t pc = 0, js = 0;
+        for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
+            const int level = P.tile_level[tile], gs = 27 / level;
+            for (int g = 0; g < level; ++g, ++pc) {
+                const uint32_t buf = pc % NB, par = (pc / NB) & 1;
+                mbar_wait(smem_u32(&bar_hfull[buf]), par);
+                mbar_wait(smem_u32(&bar_ifull[buf]), par);
+                const uint16_t* lb = reinterpret_cast<const uint16_t*>(gen + ibase + buf * kIdxBytes);
+                const uint32_t hb = hbase + buf * C::CAP * kWhRowb;
+                const int d0 = g * gs, d_end = (g + 1) * gs;
+                for (int mb = d0 / 4 + ((set - (d0 / 4) % SETS + SETS) % SETS); mb <= (d_end - 1) / 4; mb += SETS)
+                for (int kh = 0; kh < 2; ++kh, ++js) {
+                    const uint32_t ak = js % ASL, ause = js / ASL;
+                    const int d = 4 * mb + q;
+                    const bool ok = d >= d0 && d < d_end;
+                    // slots of this thread's ldmatrix rows: tile lanes 64 kh + 16c + kb + rr, c < 4
+                    uint32_t sl[4];
+                    const uint16_t* lr = lb + (rev ? 26 - d : d) * kTileRows + 64 * kh + kb + rr;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) sl[c] = ok ? lr[16 * c] : kNoSlot;
+                    mbar_wait(smem_u32(&bar_afree[set][ak]), (ause & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t acol = tmem + ((uint32_t)(q * 32) << 16) + kWhDcols + (set * ASL + ak) * kWhAcols;
+#pragma unroll
+                    for (int gg = 0; gg < 2 && !(dbg & 2); ++gg) {
+                        const int ch = 2 * gg + (m >> 1);
+                        uint32_t v[16];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint32_t s = sl[c];
+                            const uint32_t addr = s == kNoSlot ? zrow : hb + s * kWhRowb + (wh_chunk(s, ch) << 4);
+                            ldsm_x4_trans(addr, v[4 * c + 0], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        }
+                        tmem_st16x256<4>(acol + ((uint32_t)(gg * 16) << 16), v);
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    asm volatile("bar.arrive %0, 160;" ::"r"(1 + ASL * set + (int)ak) : "memory");
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(smem_u32(&bar_hempty[buf]));
+                    mbar_arrive(smem_u32(&bar_iempty[buf]));
+                }
+            }
+        }
+    } else if (warp >= W_ISS && warp < W_ISS + SETS) {
+        // ---------------- per-set issuer: 8 TS MMAs per stage into the M-block's accumulator ----------------
+        const int set = warp - W_ISS;
+        uint32_t js = 0, lt = 0, inited = 0;
+        for (int tile = blockIdx.x; tile < T; tile += gridDim.x, ++lt) {
+            const int level = P.tile_level[tile], gs = 27 / level;
+            const uint32_t bbuf = lt % NB;
+            // the set's last stage of this tile releases the grad_out buffer
+            int last_g = -1, last_mb = -1;
+            for (int g = 0; g < level; ++g) {
+                const int d0 = g * gs, d_end = (g + 1) * gs;
+                for (int mb = d0 / 4 + ((set - (d0 / 4) % SETS + SETS) % SETS); mb <= (d_end - 1) / 4; mb += SETS) {
+                    last_g = g;
+                    last_mb = mb;
+                }
+            }
+            // (the last stage is (last_g, last_mb, kh = 1))
+            mbar_wait(smem_u32(&bar_bfull[bbuf]), (lt / NB) & 1);
+            const uint64_t bdesc = smem_desc(gbase + bbuf * kWhB, 64, 512, kSwizzle64B);
+            for (int g = 0; g < level; ++g) {
+                const int d0 = g * gs, d_end = (g + 1) * gs;
+                for (int mb = d0 / 4 + ((set - (d0 / 4) % SETS + SETS) % SETS); mb <= (d_end - 1) / 4; mb += SETS)
+                for (int kh = 0; kh < 2; ++kh, ++js) {
+                    const uint32_t ak = js % ASL;
+                    asm volatile("bar.sync %0, 160;" ::"r"(1 + ASL * set + (int)ak) : "memory");
+                    tc_fence_after();
+                    const uint32_t at = tmem + kWhDcols + (set * ASL + ak) * kWhAcols;
+                    const uint32_t dt = tmem + mb * 32;
+                    const uint32_t acc = (inited >> mb) & 1u;
+                    inited |= 1u << mb;
+                    if (!(dbg & 1)) mma_ts_x4_elect_acc<8, 16, 24, 64, 128, 192>(dt, at, bdesc + 256 * kh, C::IDESC, acc);
+                    mma_commit_elect(smem_u32(&bar_afree[set][ak]));
+                    if (g == last_g && mb == last_mb && kh == 1) mma_commit_elect(smem_u32(&bar_bempty[bbuf]));
+                    __syncwarp();
+                }
+            }
+            if (last_mb < 0) mma_commit_elect(smem_u32(&bar_bempty[bbuf]));  // (no stage: release anyway)
+        }
+        // every CTA has >= 1 tile (grid <= tiles) and every tile touches all 7 M-blocks: all accumulators written
+        mma_commit_elect(smem_u32(&bar_dfull));
+        __syncwarp();
+    } else if (warp >= W_EPI && warp < W_EPI + 4) {
+        // ---------------- epilogue: the CTA's partial dW of every M-block -> part[cta][d][ci][co] ----------------
+        const int q = warp & 3;
+        const bool any = (int)blockIdx.x < T;
+        if (any) {
+            mbar_wait_sleep(smem_u32(&bar_dfull), 0, 1024);
+            tc_fence_after();
+        }
+        for (int mb = 0; mb < kWhMB; ++mb) {
+            const int d = 4 * mb + q;
+            uint32_t v[32];
+            if (any) {
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + mb * 32, v);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = 0u;
+            }
+            if (d < 27) {
+                uint8_t* dst = reinterpret_cast<uint8_t*>(part + (((int64_t)blockIdx.x * 27 + d) * 32 + lane) * 32);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    stg256(dst + 32 * j, v[8 * j], v[8 * j + 1], v[8 * j + 2], v[8 * j + 3], v[8 * j + 4], v[8 * j + 5],
+                           v[8 * j + 6], v[8 * j + 7]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == W_BLOAD) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // halo plan
 // ---------------------------------------------------------------------------------------------
 constexpr int kPlanThreads = 256;
@@ -2441,4 +2737,35 @@ extern "C" int fvdb_conv_halo_tc(const void* in_bf16, int64_t n_in, int K, const
         return out_dtype == FVDB_DTYPE_BF16 ? launch_halo<KK, NN, true>(in_bf16, w_image, P, n_out, out, st)
                                             : launch_halo<KK, NN, false>(in_bf16, w_image, P, n_out, out, st);
     });
+}
+
+extern "C" int fvdb_wgrad_reduce_parts(const float* part, int splits, int cin, int cout, float* gw, void* stream);
+
+extern "C" size_t fvdb_wgrad_halo_workspace_bytes(int64_t n_out) {
+    const int64_t T = ceil_div(n_out > 0 ? n_out : 1, kTileRows);
+    const int64_t g = T < 1024 ? T : 1024;
+    return (size_t)g * 27 * 32 * 32 * sizeof(float) + 256;
+}
+
+extern "C" int fvdb_conv_wgrad_halo(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,
+                                    const fvdb_halo_plan* plan, int64_t n_out, float* gw, void* ws, size_t ws_bytes,
+                                    void* stream) {
+    (void)n_in;
+    if (cin != 32 || cout != 32) return FVDB_ERR_UNSUPPORTED;
+    cudaStream_t st = as_stream(stream);
+    if (n_out <= 0) {
+        FVDB_CUDA_TRY(cudaMemsetAsync(gw, 0, (size_t)27 * 32 * 32 * sizeof(float), st));
+        return FVDB_OK;
+    }
+    const fvdb_halo_plan& P = *plan;
+    if (P.num_tiles != (int)ceil_div(n_out, kTileRows) || P.halo_cap > WhCfg::CAP) return FVDB_ERR_INVALID;
+    int grid = sm_count_h();
+    if (grid > P.num_tiles) grid = P.num_tiles;
+    if (ws_bytes < (size_t)grid * 27 * 32 * 32 * sizeof(float)) return FVDB_ERR_WORKSPACE;
+    float* part = reinterpret_cast<float*>(ws);
+    FVDB_CUDA_TRY(cudaFuncSetAttribute(k_wgrad_halo32, cudaFuncAttributeMaxDynamicSharedMemorySize, WhCfg::SMEM));
+    static const int dbg = getenv("FVDB_DEBUG_WGH") ? atoi(getenv("FVDB_DEBUG_WGH")) : 0;  // profiling switches
+    k_wgrad_halo32<<<grid, WhCfg::THREADS, WhCfg::SMEM, st>>>((const bf16*)in_bf16, (const bf16*)go_bf16, P, n_out, part, dbg);
+    FVDB_LAUNCH_CHECK();
+    return fvdb_wgrad_reduce_parts(part, grid, 32, 32, gw, stream);
 }

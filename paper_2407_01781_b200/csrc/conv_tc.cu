@@ -854,3 +854,12 @@ extern "C" int fvdb_conv_wgrad_tc(const void* in_bf16, int64_t n_in, int cin, co
         return decltype(L)::run(in_bf16, go_bf16, nbr, ld, n_out, gw, ws, ws_bytes, st);
     });
 }
+
+// gw[co][ci][d] = sum over splits of part[s][d][ci][co], in split order (shared with fvdb_conv_wgrad_halo)
+extern "C" int fvdb_wgrad_reduce_parts(const float* part, int splits, int cin, int cout, float* gw, void* stream) {
+    if (splits <= 0 || cout % 4 != 0) return FVDB_ERR_INVALID;
+    const int64_t total4 = (int64_t)27 * cin * cout / 4;
+    k_wgrad_tc_reduce<<<(unsigned)ceil_div(total4, 256), 256, 0, as_stream(stream)>>>(part, splits, cin, cout, gw);
+    FVDB_LAUNCH_CHECK();
+    return FVDB_OK;
+}

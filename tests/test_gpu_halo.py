@@ -314,3 +314,45 @@ def test_variant_selects_dense_window_schedule():
     assert P.choose_variant(g, 64, 64) == "brick"  # 100% leaf occupancy
     y_auto = P.conv(g, x, w, variant="auto", kmap=km)
     assert torch.equal(y_auto, P.conv(g, x, w, variant="brick", kmap=km))
+
+
+@pytest.mark.parametrize("case", ["shell", "cube_phases"])
+def test_wgrad_on_halo_plan_matches_oracle(case, shell):
+    """fvdb_conv_wgrad_halo (Cin = Cout = 32: xᵀ built in TMEM from the halo by ldmatrix.trans) against the oracle
+    on bf16-rounded inputs and against the table kernel; multi-phase plans forced on a dense cube."""
+    from paper_2407_01781_b200 import _lib
+    from paper_2407_01781_b200.conv import C, HaloPlan
+    if case == "shell":
+        g, ins, outs, km = shell
+    else:
+        c = dense_cube(20)
+        g, _ = P.build_from_coords(c)
+        og = O.build_from_coords(c)
+        km = P.build_kernel_map(g, g, 1)
+        ins, outs = O.kernel_map(og, og, 1)
+    rng = np.random.default_rng(17)
+    n = g.num_voxels
+    x = rng.normal(size=(n, 32)).astype(np.float32)
+    gy = rng.normal(size=(n, 32)).astype(np.float32)
+    kcap = int(_lib.lib().fvdb_halo_cap(32, 32))
+    plan = HaloPlan(km.fwd, kcap if case == "shell" else 256)
+    if case != "shell":
+        assert (plan.tensors["tile_level"] > 1).any()
+    xb = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    gyb = torch.from_numpy(gy).cuda().to(torch.bfloat16)
+    L = _lib.lib()
+    gw = torch.empty((32, 32, 3, 3, 3), dtype=torch.float32, device="cuda")
+    wsb = L.fvdb_wgrad_halo_workspace_bytes(n)
+    ws = _lib.workspace(wsb, "cuda")
+    _lib.check(L.fvdb_conv_wgrad_halo(xb.data_ptr(), n, 32, gyb.data_ptr(), 32, C.byref(plan.c), n, gw.data_ptr(),
+                                      ws.data_ptr(), wsb, _lib.stream_ptr()), "wgrad_halo")
+    _, gw_r = O.conv_backward(ins, outs, bf16_round(gy), bf16_round(x), np.zeros((32, 32, 3, 3, 3)))
+    assert rel(gw, gw_r) < 2e-5
+    from paper_2407_01781_b200.conv import wgrad
+    import os
+    os.environ["FVDB_WG_HALO"] = "0"
+    try:
+        gw_t = wgrad(xb, gyb, km.fwd)  # the table kernel
+    finally:
+        del os.environ["FVDB_WG_HALO"]
+    assert rel(gw, gw_t.cpu().numpy()) < 2e-5
