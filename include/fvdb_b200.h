@@ -16,8 +16,9 @@
  *     frees caller memory.  Mutable state it does keep, none of
  *     it on a result's data path: the last CUDA error string (thread-local); the
  *     FVDB_* environment switches, read once per process into function-local
- *     statics; device-global trace buffers written only when a profiling switch
- *     (FVDB_DEBUG_HALO & 64 / 128) is set.  Entry points are reentrant per stream.
+ *     statics; each device's SM count, queried once; device-global trace buffers
+ *     written only when a profiling switch (FVDB_DEBUG_HALO & 64 / 128, trace builds)
+ *     is set.  Entry points are reentrant per stream.
  */
 #ifndef FVDB_B200_H
 #define FVDB_B200_H

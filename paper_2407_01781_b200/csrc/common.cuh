@@ -17,6 +17,21 @@ void set_error_msg(const std::string& msg);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// SM count of the current device, queried once per device (cudaDeviceGetAttribute per launch was measurable
+// host time on launch-bound steps); a benign race writes the same value
+inline int device_sm_count() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cache[dev] == 0) {
+        int v = 148;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
 #define FVDB_CUDA_TRY(expr)                                   \
     do {                                                      \
         cudaError_t _e = (expr);                              \

@@ -2458,10 +2458,7 @@ __global__ void __launch_bounds__(1024) k_pack_halo(const float* __restrict__ w,
 }
 
 int sm_count_h() {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
+    return device_sm_count();
 }
 
 // MMA-issue layout per (K, N) (HaloCfg V), from B200 measurements (tools/halo_bench.py, fwd ms V0 -> V1):

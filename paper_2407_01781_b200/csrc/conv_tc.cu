@@ -608,10 +608,7 @@ __global__ void k_wgrad_tc_reduce(const float* __restrict__ part, int splits, in
 }
 
 int sm_count() {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
+    return device_sm_count();
 }
 
 // optional inputs of the gather kernel: output-row permutation (signature-sorted tables) and per-128-row-tile

@@ -386,9 +386,7 @@ extern "C" int fvdb_kernel_map_batch(const fvdb_grid_view* gin, const fvdb_grid_
     unsigned long long* next_leaf = reinterpret_cast<unsigned long long*>(ws);  // one counter per launch chunk
     const int64_t n_chunks = ceil_div(B, kMaxBatch);
     FVDB_CUDA_TRY(cudaMemsetAsync(next_leaf, 0, (size_t)n_chunks * sizeof(unsigned long long), st));
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sm_count();
     for (int64_t c0 = 0; c0 < B; c0 += kMaxBatch) {
         KmapBatch kb;
         kb.B = (int)(B - c0 < kMaxBatch ? B - c0 : kMaxBatch);

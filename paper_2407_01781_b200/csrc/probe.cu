@@ -33,9 +33,7 @@ __global__ void __launch_bounds__(256) k_probe_ffma(int iters, float* __restrict
 using namespace fvdb;
 
 extern "C" int fvdb_probe_ffma(int iters, float* out, int64_t n, double* flops, void* stream) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sm_count();
     const int blocks = sms * 8, threads = 256;
     k_probe_ffma<<<blocks, threads, 0, as_stream(stream)>>>(iters, out, n);
     FVDB_LAUNCH_CHECK();

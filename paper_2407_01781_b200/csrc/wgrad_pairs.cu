@@ -388,10 +388,7 @@ __global__ void k_wgrad_pairs_reduce(const float* __restrict__ part, PlSched s, 
 }
 
 int pl_sm_count() {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
+    return device_sm_count();
 }
 
 int pl_nacc(int nc) { return nc == 32 ? WpCfg<32, 32>::NACC : nc == 64 ? WpCfg<64, 32>::NACC : WpCfg<128, 32>::NACC; }
