@@ -435,11 +435,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         // loaded before its copies are issued (a runtime-trip loop serialised one LDS latency per copy)
         constexpr int RPP = 128 / ACH, NPASS = C::TK / RPP;
         static_assert(RPP * NPASS == C::TK, "gather mapping");
-        // thread -> (chunk c, row r0).  With 4 chunks per row (Cin 32) the 8 threads of a shared-memory phase write
-        // two rows; rows r and r ^ 1 map their chunks onto the same 4 banks of the 128B swizzle (41% of the
-        // kernel's shared wavefronts were bank conflicts at cfg5), rows r and r ^ 4 onto complementary ones
-        const int c = pt % ACH, j = pt / ACH;
-        const int r0 = ACH == 4 ? ((((j >> 1) >> 2) << 3) | ((j & 1) << 2) | ((j >> 1) & 3)) : j;
+        // thread -> (chunk c, row r0)
+        const int c = pt % ACH, r0 = pt / ACH;
         uint32_t roff[NPASS][C::OPB];                                 // swizzled offset inside an M-block
 #pragma unroll
         for (int p = 0; p < NPASS; ++p)
@@ -449,6 +446,20 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 roff[p][v] = (m >> 6) * (C::TK * 128) + swz_off(r, (m & 63) >> 3, 128);
             }
         const bf16* in_c = in + c * 8;
+        // Cin 32: a 128-byte A line holds the 64-byte rows of two offsets (u, u + 1 of an M-block half).  Thread c8
+        // of each 8-thread phase copies chunk c8 & 3 of offset 2w + (c8 >> 2), so a phase writes one whole line (one
+        // wavefront); the row-per-thread mapping above wrote two half lines per phase (bank conflicts: 41% of the
+        // kernel's shared wavefronts at cfg5)
+        constexpr int RP2 = 16, NP2 = C::TK / RP2;
+        const int c8 = pt & 7, rr0 = pt >> 3, hs = c8 >> 2;
+        uint32_t roff2[NP2][2];
+#pragma unroll
+        for (int p = 0; p < NP2; ++p)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) roff2[p][h] = h * (C::TK * 128) + swz_off(rr0 + p * RP2, c8, 128);
+        const bf16* in_c8 = in + (c8 & 3) * 8;
+        (void)roff2;
+        (void)in_c8;
         uint32_t it = 0;
         for (int ch = 0; ch < n_chunks; ++ch) {
             const uint32_t islot = ch % C::ISLOTS;
@@ -457,23 +468,45 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             for (int sub = 0; sub < SPC; ++sub, ++it) {
                 const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
                 const int64_t o0 = o_begin + (int64_t)ch * C::CHUNK + sub * C::TK;
-                int32_t idx[C::OFFS][NPASS];
-#pragma unroll
-                for (int u = 0; u < C::OFFS; ++u)
-#pragma unroll
-                    for (int p = 0; p < NPASS; ++p)
-                        idx[u][p] = u < n_off ? ib[u * C::CHUNK + sub * C::TK + r0 + p * RPP] : -1;
-                mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
                 const uint32_t sB = base + s * C::STAGE, sA = sB + C::B_BYTES;
+                if constexpr (ACH == 4) {
+                    static_assert(C::OPB == 4 && C::OFFS % 2 == 0, "Cin 32 pairs offsets within M-block halves");
+                    int32_t idx[C::OFFS / 2][NP2];
 #pragma unroll
-                for (int u = 0; u < C::OFFS; ++u)
+                    for (int w = 0; w < C::OFFS / 2; ++w)
 #pragma unroll
-                    for (int p = 0; p < NPASS; ++p) {
-                        const int32_t x = idx[u][p];  // missing neighbour: zero-fill (src-size 0, no read)
-                        if (u < n_off && !(dbg & 2))
-                            cp_async_16(sA + (u / C::OPB) * C::A_BLK + roff[p][u % C::OPB],
-                                        in_c + (int64_t)(x < 0 ? 0 : x) * CIN, x < 0 ? 0u : 16u);
-                    }
+                        for (int p = 0; p < NP2; ++p) {
+                            const int u = 2 * w + hs;
+                            idx[w][p] = u < n_off ? ib[u * C::CHUNK + sub * C::TK + rr0 + p * RP2] : -1;
+                        }
+                    mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+#pragma unroll
+                    for (int w = 0; w < C::OFFS / 2; ++w)
+#pragma unroll
+                        for (int p = 0; p < NP2; ++p) {
+                            const int32_t x = idx[w][p];  // missing neighbour: zero-fill (src-size 0, no read)
+                            if (2 * w + hs < n_off && !(dbg & 2))
+                                cp_async_16(sA + (w >> 1) * C::A_BLK + roff2[p][w & 1],
+                                            in_c8 + (int64_t)(x < 0 ? 0 : x) * CIN, x < 0 ? 0u : 16u);
+                        }
+                } else {
+                    int32_t idx[C::OFFS][NPASS];
+#pragma unroll
+                    for (int u = 0; u < C::OFFS; ++u)
+#pragma unroll
+                        for (int p = 0; p < NPASS; ++p)
+                            idx[u][p] = u < n_off ? ib[u * C::CHUNK + sub * C::TK + r0 + p * RPP] : -1;
+                    mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+#pragma unroll
+                    for (int u = 0; u < C::OFFS; ++u)
+#pragma unroll
+                        for (int p = 0; p < NPASS; ++p) {
+                            const int32_t x = idx[u][p];  // missing neighbour: zero-fill (src-size 0, no read)
+                            if (u < n_off && !(dbg & 2))
+                                cp_async_16(sA + (u / C::OPB) * C::A_BLK + roff[p][u % C::OPB],
+                                            in_c + (int64_t)(x < 0 ? 0 : x) * CIN, x < 0 ? 0u : 16u);
+                        }
+                }
                 for (int i = pt; i < C::TK * BCH; i += 128) {
                     const int r = i / BCH, c = i % BCH;
                     const int64_t o = o0 + r;
