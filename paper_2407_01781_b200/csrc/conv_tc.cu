@@ -370,7 +370,10 @@ struct WgCfg {
     static constexpr int A_BLK = TK * 256;                     // one M-block: TK k-rows x 128 m (bf16)
     static constexpr int B_BYTES = TK * COUT * 2;
     static constexpr int STAGE = B_BYTES + NACC * A_BLK;
-    static constexpr int IDX_BYTES = OFFS * CHUNK * 4;
+    // one index row per offset, rows 136 entries apart (not 128): two offsets' rows read by one instruction fall
+    // in different banks (544 B stride; 512 B put them on the same banks)
+    static constexpr int IDX_STRIDE = CHUNK + 8;
+    static constexpr int IDX_BYTES = OFFS * IDX_STRIDE * 4;
     static constexpr int ISLOTS = 2;
     static constexpr int FIXED = ISLOTS * IDX_BYTES + 1024;
     static constexpr int STAGES0 = (222 * 1024 - FIXED) / STAGE;
@@ -464,7 +467,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         for (int ch = 0; ch < n_chunks; ++ch) {
             const uint32_t islot = ch % C::ISLOTS;
             mbar_wait(smem_u32(&bar_ifull[islot]), (ch / C::ISLOTS) & 1);
-            const int32_t* ib = idx_smem + islot * (C::OFFS * C::CHUNK);
+            const int32_t* ib = idx_smem + islot * (C::OFFS * C::IDX_STRIDE);
             for (int sub = 0; sub < SPC; ++sub, ++it) {
                 const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
                 const int64_t o0 = o_begin + (int64_t)ch * C::CHUNK + sub * C::TK;
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
                         for (int p = 0; p < NP2; ++p) {
                             const int u = 2 * w + hs;
-                            idx[w][p] = u < n_off ? ib[u * C::CHUNK + sub * C::TK + rr0 + p * RP2] : -1;
+                            idx[w][p] = u < n_off ? ib[u * C::IDX_STRIDE + sub * C::TK + rr0 + p * RP2] : -1;
                         }
                     mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
 #pragma unroll
@@ -495,7 +498,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     for (int u = 0; u < C::OFFS; ++u)
 #pragma unroll
                         for (int p = 0; p < NPASS; ++p)
-                            idx[u][p] = u < n_off ? ib[u * C::CHUNK + sub * C::TK + r0 + p * RPP] : -1;
+                            idx[u][p] = u < n_off ? ib[u * C::IDX_STRIDE + sub * C::TK + r0 + p * RPP] : -1;
                     mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
 #pragma unroll
                     for (int u = 0; u < C::OFFS; ++u)
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const int nc = (dbg & 4) ? 1 : n_off;  // profiling: one index row per chunk
                 mbar_arrive_expect_tx(fb, nc * C::CHUNK * 4);
                 for (int u = 0; u < nc; ++u)
-                    bulk_g2s(ibase + islot * C::IDX_BYTES + u * C::CHUNK * 4,
+                    bulk_g2s(ibase + islot * C::IDX_BYTES + u * C::IDX_STRIDE * 4,
                              nbr + (int64_t)(d0 + u) * ld + o_begin + (int64_t)ch * C::CHUNK, C::CHUNK * 4, fb);
                 if (dbg & 8) {  // grad_out rows of the chunk after this one into L2 ahead of their cp.async
                     const int64_t p0 = o_begin + (int64_t)(ch + 1) * C::CHUNK;
