@@ -255,17 +255,25 @@ int fvdb_conv_wgrad_tc(const void* in_bf16, int64_t n_in, int cin, const void* g
 /* Per-offset pair lists of a neighbour table (for fvdb_conv_wgrad_pairs_tc).  Offset d's pairs
  * (pin = nbr[d][o], pout = o, o ascending) fill [seg[d], seg[d+1]) of pin / pout, each segment padded
  * with -1 to a multiple of 128; seg is a device int32[28] (seg[27] = padded total).  Call once with
- * pin = pout = NULL to fill seg, read seg[27], then again with pin / pout of cap >= seg[27] entries. */
+ * pin = pout = NULL to fill seg, read seg[27], then again with pin / pout of cap >= seg[27] entries.
+ * tile_pos (optional, device int32 [27][ceil(n_out / 128) + 1]): offset d's pairs of 128-row output tile t
+ * are [tile_pos[d][t], tile_pos[d][t + 1]); written when non-NULL. */
 size_t fvdb_kmap_pair_lists_workspace_bytes(int64_t n_out);
 int fvdb_kmap_pair_lists(const int32_t* nbr, int64_t ld, int64_t n_out, int32_t* seg, int32_t* pin,
-                         int32_t* pout, int64_t cap, void* workspace, size_t workspace_bytes, void* stream);
+                         int32_t* pout, int32_t* tile_pos, int64_t cap, void* workspace, size_t workspace_bytes,
+                         void* stream);
 /* wgrad over pair lists (same result as fvdb_conv_wgrad_tc up to fp32 summation order; deterministic):
  * work scales with the pairs, not 27 x n_out, for sparse tables.  cin or cout must be 128, the other 32,
- * 64 or 128.  gw fp32 [cout][cin][27]. */
-size_t fvdb_wgrad_pairs_workspace_bytes(int cin, int cout);
+ * 64 or 128.  gw fp32 [cout][cin][27].  With tile_pos (from fvdb_kmap_pair_lists; n_out = the table's
+ * rows) a CTA owns a group of 3 (N = 128) or 6 consecutive offsets and a range of output tiles and takes
+ * the group's pairs tile by tile, so operand rows are re-read from L2 rather than DRAM (half the DRAM reads
+ * at cfg3, but slower: 0.91 vs 0.70 ms); with tile_pos = NULL each CTA takes a linear share of the
+ * offset-major lists (the faster schedule, conv.py's default). */
+size_t fvdb_wgrad_pairs_workspace_bytes(int cin, int cout, int64_t n_out);
 int fvdb_conv_wgrad_pairs_tc(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,
-                             const int32_t* pin, const int32_t* pout, const int32_t* seg, float* gw,
-                             void* workspace, size_t workspace_bytes, void* stream);
+                             const int32_t* pin, const int32_t* pout, const int32_t* seg,
+                             const int32_t* tile_pos, int64_t n_out, float* gw, void* workspace,
+                             size_t workspace_bytes, void* stream);
 
 /* ---- Halo-staged tensor-core conv (same operator as fvdb_conv_gather_tc, conv.py:180-191) ----
  * The output rows are cut into 128-row tiles.  For each tile a "halo plan" (built once per kernel

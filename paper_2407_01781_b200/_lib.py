@@ -102,9 +102,9 @@ SIGNATURES = {
     "fvdb_wgrad_tc_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "fvdb_conv_wgrad_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "fvdb_kmap_pair_lists_workspace_bytes": (_sz, [_i64]),
-    "fvdb_kmap_pair_lists": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp, _sz, _vp]),
-    "fvdb_wgrad_pairs_workspace_bytes": (_sz, [_i32, _i32]),
-    "fvdb_conv_wgrad_pairs_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fvdb_kmap_pair_lists": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _sz, _vp]),
+    "fvdb_wgrad_pairs_workspace_bytes": (_sz, [_i32, _i32, _i64]),
+    "fvdb_conv_wgrad_pairs_tc": (_i32, [_vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "fvdb_f32_to_bf16": (_i32, [_vp, _i64, _vp, _vp]),
     "fvdb_probe_ffma": (_i32, [_i32, _vp, _i64, C.POINTER(C.c_double), _vp]),
     "fvdb_parity_colors": (_i32, [_vp, _i64, _i32, _vp, _vp]),

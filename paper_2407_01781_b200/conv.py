@@ -83,6 +83,9 @@ def _kernel_weights(kernel):
 
 _TWO_PASS_PLAN = os.environ.get("FVDB_PLAN_TWO_PASS", "0") == "1"
 _PLAN_SHARE = os.environ.get("FVDB_PLAN_SHARE", "1") != "0"  # transposed same-grid tables run the forward plan reversed
+# pair-list wgrad schedule: "linear" (linear shares of the offset-major lists, default) or "tiles" (offset groups x
+# tile ranges: half the DRAM reads at cfg3 but 0.91 vs 0.70 ms, latency-bound; profiles/r02_wgrad_pairs_sched.md)
+_WG_PAIRS_SCHED = os.environ.get("FVDB_WG_PAIRS_SCHED", "linear")
 
 
 class HaloPlan:
@@ -148,8 +151,8 @@ class NbrTable:
     """
 
     __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
-                 "_masks", "sparse", "_steady", "_pairs", "exact_uses", "wgrad_uses", "rows_bound", "rev_src",
-                 "plan_shared")
+                 "_masks", "sparse", "_steady", "_pairs", "_pair_tp", "exact_uses", "wgrad_uses", "rows_bound",
+                 "rev_src", "plan_shared")
 
     def __init__(self, t, n, colors_fn=None, counts=None):
         self.rows_bound = None  # exclusive bound of the input rows in t (known: single-pass halo plans)
@@ -165,6 +168,7 @@ class NbrTable:
         self.sparse = False  # set for transposed stride-2 tables (<= 8 of 27 offsets per row)
         self._steady = {}    # (K, N) -> steady_impl decision
         self._pairs = None   # (pin, pout, seg, padded total): per-offset pair lists (wgrad)
+        self._pair_tp = None  # per-(offset, tile) positions in the pair lists
         self.exact_uses = 0  # fp32 / f64 gather convolutions run over this table
         self.wgrad_uses = 0  # bf16 weight gradients run over this table
 
@@ -196,22 +200,32 @@ class NbrTable:
 
         Offset d's pairs (pin = t[d][o], pout = o, o ascending) fill [seg[d], seg[d+1]) of pin / pout, each
         segment padded with -1 to a multiple of 128; seg is device int32 [28], total = seg[27]. Sizing the
-        lists reads seg[27] back to the host (one synchronisation per table)."""
+        lists reads seg[27] back to the host (one synchronisation per table).  The per-tile positions
+        (``pair_tile_pos``) are filled in the same call."""
         if self._pairs is None:
             L = _lib.lib()
             dev, st = self.t.device, _lib.stream_ptr()
             seg = torch.empty(28, dtype=torch.int32, device=dev)
             wsb = L.fvdb_kmap_pair_lists_workspace_bytes(self.n)
             ws = _lib.workspace(wsb, dev)
-            _lib.check(L.fvdb_kmap_pair_lists(self.t.data_ptr(), self.ld, self.n, seg.data_ptr(), None, None, 0,
+            _lib.check(L.fvdb_kmap_pair_lists(self.t.data_ptr(), self.ld, self.n, seg.data_ptr(), None, None, None, 0,
                                               ws.data_ptr(), wsb, st), "kmap_pair_lists")
             total = int(seg[27].item())
             pin = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
             pout = torch.empty_like(pin)
+            tp = torch.empty(27 * ((self.n + 127) // 128 + 1), dtype=torch.int32, device=dev)
             _lib.check(L.fvdb_kmap_pair_lists(self.t.data_ptr(), self.ld, self.n, seg.data_ptr(), pin.data_ptr(),
-                                              pout.data_ptr(), total, ws.data_ptr(), wsb, st), "kmap_pair_lists")
+                                              pout.data_ptr(), tp.data_ptr(), total, ws.data_ptr(), wsb, st),
+                       "kmap_pair_lists")
             self._pairs = (pin, pout, seg, total)
+            self._pair_tp = tp
         return self._pairs
+
+    def pair_tile_pos(self):
+        """int32 [27][ceil(n / 128) + 1]: offset d's pairs of output tile t are [tp[d][t], tp[d][t+1]) of the
+        pair lists (fvdb_kmap_pair_lists' tile_pos), cached with them."""
+        self.pair_lists()
+        return self._pair_tp
 
     def tile_masks(self):
         """uint32 [ceil(n / 128)]: bit d of tile t = some row of the tile has a pair at offset d, cached."""
@@ -886,11 +900,12 @@ def wgrad(x: torch.Tensor, go: torch.Tensor, nbr: NbrTable) -> torch.Tensor:
     nbr.wgrad_uses += 1
     if use_pairs:
         pin, pout, seg, _ = nbr.pair_lists()
-        wsb = L.fvdb_wgrad_pairs_workspace_bytes(cin, cout)
+        tp = nbr.pair_tile_pos() if _WG_PAIRS_SCHED == "tiles" else None
+        wsb = L.fvdb_wgrad_pairs_workspace_bytes(cin, cout, n_out)
         ws = _lib.workspace(wsb, x.device)
         _lib.check(L.fvdb_conv_wgrad_pairs_tc(x.data_ptr(), x.shape[0], cin, go.data_ptr(), cout, pin.data_ptr(),
-                                              pout.data_ptr(), seg.data_ptr(), gw.data_ptr(), ws.data_ptr(), wsb,
-                                              st), "conv_wgrad_pairs_tc")
+                                              pout.data_ptr(), seg.data_ptr(), None if tp is None else tp.data_ptr(),
+                                              n_out, gw.data_ptr(), ws.data_ptr(), wsb, st), "conv_wgrad_pairs_tc")
         return gw
     wsb = L.fvdb_wgrad_tc_workspace_bytes(n_out, cin, cout)
     ws = _lib.workspace(wsb, x.device)

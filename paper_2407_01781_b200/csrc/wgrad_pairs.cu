@@ -102,6 +102,17 @@ __global__ void k_pl_scatter(const int32_t* __restrict__ nbr, int64_t ld, int64_
     }
 }
 
+// tile_pos[d][t] = list position of offset d's first pair in 128-row tile t (t <= tiles: [d][tiles] = the
+// segment's unpadded end), so offset d's pairs of tile t are [tile_pos[d][t], tile_pos[d][t + 1]).
+__global__ void k_pl_tile_pos(const int32_t* __restrict__ cnt, const int32_t* __restrict__ sc,
+                              const int32_t* __restrict__ shift, int tiles, int32_t* __restrict__ tp) {
+    const int d = blockIdx.y;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= tiles; t += gridDim.x * blockDim.x) {
+        const int64_t i = (int64_t)d * tiles + (t < tiles ? t : tiles - 1);
+        tp[(int64_t)d * (tiles + 1) + t] = sc[i] + shift[d] + (t < tiles ? 0 : cnt[i]);
+    }
+}
+
 // ---------------------------------------------------------------------------------------------------------
 // schedule: CTA chunk ranges (each covering <= nacc offsets) and, per offset, the CTAs that cover it
 // ---------------------------------------------------------------------------------------------------------
@@ -184,6 +195,120 @@ __global__ void __launch_bounds__(kSchedThreads) k_pl_schedule(const int32_t* __
 }
 
 // ---------------------------------------------------------------------------------------------------------
+// tile-ordered schedule: offset groups x tile ranges
+//
+// The linear schedule above puts the CTAs of different offsets at different row positions (offset densities
+// differ), so each operand row is fetched from DRAM once per offset: 4.38 GB per launch for 644 MB of rows at
+// cfg3.  Here the 27 offsets form groups of GS consecutive offsets (GS = 3 at N = 128: one (dx, dy) line,
+// dz = -1..1), a CTA owns one group and a range of 128-row tiles, and walks its tiles in order taking the
+// group's pairs of each tile back to back: the tile's grad-out rows serve all GS offsets and the input rows of
+// a z-line overlap, so the re-reads hit L2.  Ranges are cut at equal 32-pair stage counts within a group, and
+// each group gets CTAs in proportion to its stages.
+// Measured at cfg3 (tools/wgrad_pairs_sched.py, profiles/r02_wgrad_pairs_sched.md): DRAM reads drop from 4.29 to
+// 2.44 GB, but the kernel takes 0.91 ms against the linear schedule's 0.70: 597 vs 491 SM cycles per 32-pair
+// stage (the stage ring waits on re-reads of rows still in flight) and a 14% per-SM spread.  Opt-in
+// (FVDB_WG_PAIRS_SCHED=tiles in conv.py).
+// ---------------------------------------------------------------------------------------------------------
+constexpr int kPtStage = 32;  // pairs per stage of the tile-ordered kernel
+
+// work[g][t] = 32-pair stages of group g in tile t (work[ng * tiles] = 0: the scan's total slot)
+__global__ void k_pt_work(const int32_t* __restrict__ tp, int tiles, int gs, int32_t* __restrict__ work) {
+    const int ng = (27 + gs - 1) / gs;
+    const int64_t n = (int64_t)ng * tiles;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i == n) {
+            work[i] = 0;
+            continue;
+        }
+        const int g = (int)(i / tiles), t = (int)(i - (int64_t)g * tiles);
+        int w = 0;
+        for (int d = g * gs; d < g * gs + gs && d < 27; ++d) {
+            const int64_t r = (int64_t)d * (tiles + 1) + t;
+            w += (tp[r + 1] - tp[r] + kPtStage - 1) / kPtStage;
+        }
+        work[i] = w;
+    }
+}
+
+// One block.  Group g gets G_g ~ G * W_g / W CTA slots (largest remainder, >= 1; sum <= G + 9 <= slots) from S_g; slot
+// S_g + k takes tiles [t(k), t(k + 1)) with t(k) = first tile whose stage prefix reaches k * W_g / G_g.
+// Slots past the groups are idle (c0 = c1 = 0, d0 = -1).  lo / hi[d] = the slots of d's group.
+__global__ void __launch_bounds__(kSchedThreads) k_pt_schedule(const int32_t* __restrict__ ex, int tiles, int gs,
+                                                               int G, int slots, PlSched s) {
+    __shared__ int32_t gcnt[10], gstart[10];
+    __shared__ int64_t gw[10];
+    const int ng = (27 + gs - 1) / gs;
+    if (threadIdx.x == 0) {
+        int64_t W = 0;
+        for (int g = 0; g < ng; ++g) {
+            gw[g] = (int64_t)ex[(int64_t)(g + 1) * tiles] - ex[(int64_t)g * tiles];
+            W += gw[g];
+        }
+        // largest remainder: sum G_g = G when every group has work (each group >= 1 CTA)
+        int64_t rem[10];
+        int used = 0;
+        for (int g = 0; g < ng; ++g) {
+            const int64_t q = W > 0 ? (int64_t)G * gw[g] : 0;
+            int c = W > 0 ? (int)(q / W) : 0;
+            rem[g] = W > 0 ? q % W : 0;
+            if (c < 1) {
+                c = 1;
+                rem[g] = -1;
+            }
+            gcnt[g] = c;
+            used += c;
+        }
+        while (used < G && W > 0) {
+            int best = -1;
+            for (int g = 0; g < ng; ++g)
+                if (rem[g] >= 0 && (best < 0 || rem[g] > rem[best])) best = g;
+            if (best < 0) break;
+            ++gcnt[best];
+            rem[best] = -1;
+            ++used;
+        }
+        int st = 0;
+        for (int g = 0; g < ng; ++g) {
+            gstart[g] = st;
+            st += gcnt[g];
+        }
+        gstart[ng] = st;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < slots; r += blockDim.x) {
+        int g = 0;
+        while (g < ng && r >= gstart[g + 1]) ++g;
+        if (g >= ng) {
+            s.c0[r] = s.c1[r] = 0;
+            s.d0[r] = -1;
+            continue;
+        }
+        const int k = r - gstart[g], c = gcnt[g];
+        const int32_t* e = ex + (int64_t)g * tiles;
+        auto cut = [&](int kk) -> int {  // first t with e[t] - e[0] >= kk * W_g / c
+            if (kk <= 0) return 0;
+            if (kk >= c) return tiles;
+            const int64_t target = (int64_t)e[0] + gw[g] * kk / c;
+            int lo = 0, hi = tiles;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if ((int64_t)e[mid] >= target) hi = mid;
+                else lo = mid + 1;
+            }
+            return lo;
+        };
+        s.c0[r] = cut(k);
+        s.c1[r] = cut(k + 1);
+        s.d0[r] = g * gs;
+    }
+    if (threadIdx.x < 27) {
+        const int g = threadIdx.x / gs;
+        s.lo[threadIdx.x] = gstart[g];
+        s.hi[threadIdx.x] = gstart[g] + gcnt[g] - 1;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------------------
 // kernel
 // ---------------------------------------------------------------------------------------------------------
 template <int NC, int TK_>
@@ -213,6 +338,14 @@ struct WpCfg {
 };
 
 constexpr int kWpThreads = 320;  // warps 0-3 gather, 4 index loader, 5 MMA, 6-9 epilogue
+// Each CTA allocates all 512 TMEM columns: a second CTA on the same SM would sit blocked in tcgen05.alloc
+// while other SMs idle (ncu: max 12.4 warps active on an SM, min 0.02).  Launches request at least this much
+// shared memory so only one CTA fits per SM.
+#ifndef FVDB_WP_MIN_SMEM_KB
+#define FVDB_WP_MIN_SMEM_KB 118
+#endif
+constexpr int kWpMinSmem = FVDB_WP_MIN_SMEM_KB * 1024;
+__host__ __device__ constexpr int wp_launch_smem(int smem) { return smem > kWpMinSmem ? smem : kWpMinSmem; }
 
 template <int NC, int TK>
 __global__ void __launch_bounds__(kWpThreads, 1)
@@ -372,6 +505,214 @@ __global__ void __launch_bounds__(kWpThreads, 1)
     }
 }
 
+// Tile-ordered form (k_pt_schedule): CTA = (offset group, tile range).  The range is walked in windows of
+// kPtWin tiles; a "piece" is one offset's pairs of one window ([tile_pos[d][w0], tile_pos[d][w1]), contiguous
+// in the list), cut into <= 128-pair index chunks and 32-pair stages (the last zero-padded).  Every warp
+// enumerates the same pieces: a warp-wide load fetches the group's positions at 32 window boundaries, lanes
+// shuffle them out.  Warp 4 copies each chunk's indices into one of kPtIslots shared slots with 4-byte
+// cp.async (many chunks in flight); warps 0-3 gather the stage rows; warp 5 issues; warps 6-9 write the
+// partials (zeros for an offset the range never touched).
+constexpr int kPtIslots = 8;
+#ifndef FVDB_PT_WIN
+#define FVDB_PT_WIN 16
+#endif
+constexpr int kPtWin = FVDB_PT_WIN;  // tiles per window (cfg3 measured: 1 / 2 / 4 / 8 / 16 -> 1.41 / 1.18 / 0.98 / 0.92 / 0.91 ms)
+
+// Calls f(j, pos, n) for every non-empty index chunk (n <= 128) of tiles [t0, t1), group offsets
+// d0 .. d0 + GS - 1, window by window.  Whole-warp call (shuffles).
+template <int GS, class F>
+__device__ __forceinline__ void for_each_piece(const int32_t* tp, int tiles, int d0, int t0, int t1, F&& f) {
+    const int lane = threadIdx.x & 31;
+    for (int wb = t0; wb < t1; wb += 31 * kPtWin) {
+        const int bt = wb + lane * kPtWin < t1 ? wb + lane * kPtWin : t1;  // this lane's boundary tile
+        int32_t pb[GS];
+#pragma unroll
+        for (int j = 0; j < GS; ++j)
+            pb[j] = d0 + j < 27 ? __ldg(tp + (int64_t)(d0 + j) * (tiles + 1) + bt) : 0;
+        const int nw0 = (t1 - wb + kPtWin - 1) / kPtWin, nw = nw0 < 31 ? nw0 : 31;
+        for (int u = 0; u < nw; ++u)
+#pragma unroll 1
+            for (int j = 0; j < GS; ++j) {
+                int32_t v = 0;
+#pragma unroll
+                for (int i = 0; i < GS; ++i)
+                    if (i == j) v = pb[i];
+                const int p0 = __shfl_sync(0xffffffffu, v, u), p1 = __shfl_sync(0xffffffffu, v, u + 1);
+                for (int p = p0; p < p1; p += kPlChunk) f(j, p, p1 - p < kPlChunk ? p1 - p : kPlChunk);
+            }
+    }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(kWpThreads, 1)
+    k_wgrad_pairs_tiles(const bf16* __restrict__ am, const int32_t* __restrict__ ia, const bf16* __restrict__ bn,
+                        const int32_t* __restrict__ ib, const int32_t* __restrict__ tp, int tiles, PlSched sch,
+                        float* __restrict__ part) {
+    using C = WpCfg<NC, kPtStage>;
+    constexpr int GS = C::NACC / 3 * 3;
+    const int cta = blockIdx.x;
+    const int t0 = sch.c0[cta], t1 = sch.c1[cta], d0 = sch.d0[cta];
+    if (d0 < 0) return;  // slot past the groups: never reduced
+    if (t0 >= t1) {      // empty range of a group: zero partials
+        float4* p = reinterpret_cast<float4*>(part + (int64_t)cta * C::NACC * 128 * NC);
+        for (int i = threadIdx.x; i < GS * 128 * NC / 4; i += blockDim.x) p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    extern __shared__ uint8_t dsmem[];
+    __shared__ __align__(8) uint64_t bar_full[C::STAGES], bar_empty[C::STAGES], bar_ifull[kPtIslots],
+        bar_iempty[kPtIslots], bar_tfull;
+    __shared__ uint32_t tmem_slot;
+    __shared__ int32_t idx_s[kPtIslots][2][kPlChunk];
+    const uint32_t sbase = smem_u32(dsmem);
+    const uint32_t base = (sbase + 1023u) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(smem_u32(&bar_full[s]), 128);
+            mbar_init(smem_u32(&bar_empty[s]), 1);
+        }
+        for (int s = 0; s < kPtIslots; ++s) {
+            mbar_init(smem_u32(&bar_ifull[s]), 32);
+            mbar_init(smem_u32(&bar_iempty[s]), 128);
+        }
+        mbar_init(smem_u32(&bar_tfull), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 5) tmem_alloc(smem_u32(&tmem_slot), C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp < 4) {
+        const int pt = threadIdx.x;
+        constexpr int BCH = NC / 8;
+        constexpr int BPT = kPtStage * BCH / 128;
+        constexpr int APT = kPtStage / 8;
+        const int ca = pt % 16, ra = pt / 16;
+        uint32_t aoff[APT];
+#pragma unroll
+        for (int p = 0; p < APT; ++p) aoff[p] = (ca >> 3) * (kPtStage * 128) + pl_swz(ra + 8 * p, ca & 7, 128);
+        uint32_t boff[BPT];
+        int brow[BPT], bcol[BPT];
+#pragma unroll
+        for (int p = 0; p < BPT; ++p) {
+            const int i = pt + 128 * p, r = i / BCH, c = i % BCH;
+            brow[p] = r;
+            bcol[p] = c;
+            boff[p] = C::B_SW128 ? (c >> 3) * (kPtStage * 128) + pl_swz(r, c & 7, 128) : pl_swz(r, c, 64);
+        }
+        const bf16* am_c = am + ca * 8;
+        uint32_t it = 0, pc = 0;
+        for_each_piece<GS>(tp, tiles, d0, t0, t1, [&](int, int, int n) {
+            const uint32_t islot = pc % kPtIslots;
+            mbar_wait(smem_u32(&bar_ifull[islot]), (pc / kPtIslots) & 1);
+            const int32_t* ias = idx_s[islot][0];
+            const int32_t* ibs = idx_s[islot][1];
+            for (int q0 = 0; q0 < n; q0 += kPtStage, ++it) {
+                const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
+                int32_t xa[APT], xb[BPT];
+#pragma unroll
+                for (int p = 0; p < APT; ++p) {
+                    const int q = q0 + ra + 8 * p;
+                    xa[p] = q < n ? ias[q] : -1;
+                }
+#pragma unroll
+                for (int p = 0; p < BPT; ++p) {
+                    const int q = q0 + brow[p];
+                    xb[p] = q < n ? ibs[q] : -1;
+                }
+                mbar_wait(smem_u32(&bar_empty[s]), ph ^ 1);
+                const uint32_t sB = base + s * C::STAGE, sA = sB + C::B_BYTES;
+#pragma unroll
+                for (int p = 0; p < APT; ++p)
+                    cp_async_16(sA + aoff[p], am_c + (int64_t)(xa[p] < 0 ? 0 : xa[p]) * 128, xa[p] < 0 ? 0u : 16u);
+#pragma unroll
+                for (int p = 0; p < BPT; ++p)
+                    cp_async_16(sB + boff[p], bn + (int64_t)(xb[p] < 0 ? 0 : xb[p]) * NC + bcol[p] * 8,
+                                xb[p] < 0 ? 0u : 16u);
+                cp_async_arrive_noinc(smem_u32(&bar_full[s]));
+            }
+            mbar_arrive(smem_u32(&bar_iempty[islot]));
+            ++pc;
+        });
+    } else if (warp == 4) {
+        uint32_t pc = 0;
+        for_each_piece<GS>(tp, tiles, d0, t0, t1, [&](int, int p0, int n) {
+            const uint32_t islot = pc % kPtIslots;
+            mbar_wait(smem_u32(&bar_iempty[islot]), ((pc / kPtIslots) & 1) ^ 1);
+            const uint32_t sa = smem_u32(&idx_s[islot][0][0]), sb = smem_u32(&idx_s[islot][1][0]);
+#pragma unroll
+            for (int k = 0; k < kPlChunk / 32; ++k) {
+                const int q = lane + 32 * k;
+                if (q < n) {
+                    cp_async_4(sa + 4 * q, ia + p0 + q);
+                    cp_async_4(sb + 4 * q, ib + p0 + q);
+                }
+            }
+            cp_async_arrive_noinc(smem_u32(&bar_ifull[islot]));  // lands when this lane's copies have
+            ++pc;
+        });
+    } else if (warp == 5) {
+        const uint64_t adesc0 = smem_desc(base + C::B_BYTES, kPtStage * 128, 1024, kSwizzle128B);
+        const uint64_t bdesc0 = C::B_SW128 ? smem_desc(base, kPtStage * 128, 1024, kSwizzle128B)
+                                           : smem_desc(base, 64, 512, kSwizzle64B);
+        constexpr uint32_t BI = C::B_SW128 ? 128 : 64;
+        uint32_t it = 0, started = 0;
+        for_each_piece<GS>(tp, tiles, d0, t0, t1, [&](int j, int, int n) {
+            for (int q0 = 0; q0 < n; q0 += kPtStage, ++it) {
+                const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
+                mbar_wait(smem_u32(&bar_full[s]), ph);
+                fence_proxy_async_smem();
+                tc_fence_after();
+                const uint32_t so = s * C::STAGE;
+                mma_ss_x2_elect<BI>(tmem + j * NC, adesc0 + (so >> 4), bdesc0 + (so >> 4), C::IDESC,
+                                    (started >> j) & 1u);
+                started |= 1u << j;
+                mma_commit_elect(smem_u32(&bar_empty[s]));
+            }
+        });
+        mma_commit_elect(smem_u32(&bar_tfull));
+        __syncwarp();
+    } else {
+        const int q = warp & 3, m = q * 32 + lane;
+        uint32_t started = 0;  // offsets with pairs in [t0, t1): the others' accumulators were never written
+        for (int t = t0 + lane; t < t1; t += 32)
+            for (int j = 0; j < GS; ++j)
+                if (d0 + j < 27) {
+                    const int64_t r = (int64_t)(d0 + j) * (tiles + 1) + t;
+                    if (__ldg(tp + r + 1) > __ldg(tp + r)) started |= 1u << j;
+                }
+        started = __reduce_or_sync(0xffffffffu, started);
+        mbar_wait_sleep(smem_u32(&bar_tfull), 0, 1024);
+        tc_fence_after();
+        for (int j = 0; j < GS; ++j) {
+            for (int cc = 0; cc < NC; cc += 32) {
+                uint32_t v[32];
+                if ((started >> j) & 1u) {
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + j * NC + cc, v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) v[k] = 0u;
+                }
+                uint8_t* dst = reinterpret_cast<uint8_t*>(part + (((int64_t)cta * C::NACC + j) * 128 + m) * NC + cc);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    stg256(dst + 32 * k, v[8 * k], v[8 * k + 1], v[8 * k + 2], v[8 * k + 3], v[8 * k + 4],
+                           v[8 * k + 5], v[8 * k + 6], v[8 * k + 7]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+}
+
 // gw[co][ci][d] = Σ_{cta = lo[d]..hi[d]} part[cta][d - d0[cta]][m][n]  (CTA order: deterministic)
 __global__ void k_wgrad_pairs_reduce(const float* __restrict__ part, PlSched s, int nacc, int nc, int swapped,
                                      int cin, int cout, float* __restrict__ gw) {
@@ -393,11 +734,26 @@ int pl_sm_count() {
 
 int pl_nacc(int nc) { return nc == 32 ? WpCfg<32, 32>::NACC : nc == 64 ? WpCfg<64, 32>::NACC : WpCfg<128, 32>::NACC; }
 
-size_t pl_ws_bytes(int nc, int G) {
+int pl_groups(int nc) { return (27 + pl_nacc(nc) / 3 * 3 - 1) / (pl_nacc(nc) / 3 * 3); }
+
+// tiles > 0: the tile-ordered schedule's stage counts and their scan follow the partials
+size_t pl_scan_bytes(int n) {
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, (const int32_t*)nullptr, (int32_t*)nullptr, n);
+    return tmp;
+}
+
+size_t pl_ws_bytes(int nc, int G, int tiles) {
     const int slots = G + 27;
     Sizer sz;
     sz.take<int32_t>(3 * (size_t)slots + 54);
     sz.take<float>((size_t)slots * pl_nacc(nc) * 128 * nc);
+    if (tiles > 0) {
+        const int n = pl_groups(nc) * tiles + 1;
+        sz.take<int32_t>(n);
+        sz.take<int32_t>(n);
+        sz.take<uint8_t>(pl_scan_bytes(n));
+    }
     return sz.used + 256;
 }
 
@@ -420,8 +776,8 @@ extern "C" size_t fvdb_kmap_pair_lists_workspace_bytes(int64_t n_out) {
 }
 
 extern "C" int fvdb_kmap_pair_lists(const int32_t* nbr, int64_t ld, int64_t n_out, int32_t* seg, int32_t* pin,
-                                    int32_t* pout, int64_t cap, void* workspace, size_t workspace_bytes,
-                                    void* stream) {
+                                    int32_t* pout, int32_t* tile_pos, int64_t cap, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
     if (n_out < 0 || ld < n_out || !seg) return FVDB_ERR_INVALID;
     if (27 * n_out + 27 * (int64_t)kPlChunk > 0x7fffffffLL) return FVDB_ERR_INVALID;  // int32 pair positions
     if ((pin == nullptr) != (pout == nullptr)) return FVDB_ERR_INVALID;
@@ -450,57 +806,94 @@ extern "C" int fvdb_kmap_pair_lists(const int32_t* nbr, int64_t ld, int64_t n_ou
         if (tiles > 0) k_pl_scatter<<<tiles, 128, 0, st>>>(nbr, ld, n_out, tiles, sc, shift, pin, pout);
         FVDB_LAUNCH_CHECK();
     }
+    if (tile_pos && tiles > 0) {
+        k_pl_tile_pos<<<dim3((unsigned)ceil_div(tiles + 1, 256), 27), 256, 0, st>>>(cnt, sc, shift, tiles, tile_pos);
+        FVDB_LAUNCH_CHECK();
+    }
     return FVDB_OK;
 }
 
-extern "C" size_t fvdb_wgrad_pairs_workspace_bytes(int cin, int cout) {
+extern "C" size_t fvdb_wgrad_pairs_workspace_bytes(int cin, int cout, int64_t n_out) {
     const int nc = cin == 128 ? cout : cin;
-    if ((cin != 128 && cout != 128) || (nc != 32 && nc != 64 && nc != 128)) return 0;
-    return pl_ws_bytes(nc, pl_sm_count());
+    if ((cin != 128 && cout != 128) || (nc != 32 && nc != 64 && nc != 128) || n_out < 0) return 0;
+    return pl_ws_bytes(nc, pl_sm_count(), (int)ceil_div(n_out, 128));
 }
 
 extern "C" int fvdb_conv_wgrad_pairs_tc(const void* in_bf16, int64_t n_in, int cin, const void* go_bf16, int cout,
-                                        const int32_t* pin, const int32_t* pout, const int32_t* seg, float* gw,
-                                        void* workspace, size_t workspace_bytes, void* stream) {
+                                        const int32_t* pin, const int32_t* pout, const int32_t* seg,
+                                        const int32_t* tile_pos, int64_t n_out, float* gw, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
     (void)n_in;
     const bool swapped = cin != 128;  // M side = grad_out (Cout = 128)
     const int nc = swapped ? cin : cout;
-    if ((cin != 128 && cout != 128) || (nc != 32 && nc != 64 && nc != 128)) return FVDB_ERR_INVALID;
+    if ((cin != 128 && cout != 128) || (nc != 32 && nc != 64 && nc != 128) || n_out < 0) return FVDB_ERR_INVALID;
     cudaStream_t st = as_stream(stream);
     int G = pl_sm_count();
     if (G > kSchedThreads) G = kSchedThreads;
     const int nacc = pl_nacc(nc), slots = G + 27;
+    const int tiles = (int)ceil_div(n_out, 128);
+    const bool by_tiles = tile_pos != nullptr && tiles > 0;
     Carver cv(workspace, workspace_bytes);
     int32_t* sb = cv.take<int32_t>(3 * (size_t)slots + 54);
     float* part = cv.take<float>((size_t)slots * nacc * 128 * nc);
+    int32_t *work = nullptr, *ex = nullptr;
+    void* tmpp = nullptr;
+    size_t tmp = 0;
+    if (by_tiles) {
+        const int n = pl_groups(nc) * tiles + 1;
+        work = cv.take<int32_t>(n);
+        ex = cv.take<int32_t>(n);
+        tmp = pl_scan_bytes(n);
+        tmpp = cv.take<uint8_t>(tmp);
+    }
     if (!cv.ok()) return FVDB_ERR_WORKSPACE;
     const PlSched s{sb, sb + slots, sb + 2 * slots, sb + 3 * slots, sb + 3 * slots + 27};
-    k_pl_schedule<<<1, kSchedThreads, 0, st>>>(seg, G, nacc, slots, s);
     const bf16* am = (const bf16*)(swapped ? go_bf16 : in_bf16);
     const bf16* bn = (const bf16*)(swapped ? in_bf16 : go_bf16);
     const int32_t* ia = swapped ? pout : pin;
     const int32_t* ib = swapped ? pin : pout;
-    auto go = [&](auto kern, int smem) -> int {
-        FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        // ranges beyond G exist only when a linear share spans more than nacc offsets (tiny offsets)
-        kern<<<slots, kWpThreads, smem, st>>>(am, ia, bn, ib, seg, s, part);
+    int rc = FVDB_OK;
+    if (by_tiles) {
+        const int gs = nacc / 3 * 3, n = pl_groups(nc) * tiles + 1;
+        k_pt_work<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(tile_pos, tiles, gs, work);
         FVDB_LAUNCH_CHECK();
-        return FVDB_OK;
-    };
-    static const int tk = getenv("FVDB_WG_PAIRS_TK") ? atoi(getenv("FVDB_WG_PAIRS_TK")) : 32;  // profiling
-    int rc;
-    if (tk == 128)
-        rc = nc == 32 ? go(k_wgrad_pairs<32, 128>, WpCfg<32, 128>::SMEM)
-           : nc == 64 ? go(k_wgrad_pairs<64, 128>, WpCfg<64, 128>::SMEM)
-                      : go(k_wgrad_pairs<128, 128>, WpCfg<128, 128>::SMEM);
-    else if (tk == 64)
-        rc = nc == 32 ? go(k_wgrad_pairs<32, 64>, WpCfg<32, 64>::SMEM)
-           : nc == 64 ? go(k_wgrad_pairs<64, 64>, WpCfg<64, 64>::SMEM)
-                      : go(k_wgrad_pairs<128, 64>, WpCfg<128, 64>::SMEM);
-    else
-        rc = nc == 32 ? go(k_wgrad_pairs<32, 32>, WpCfg<32, 32>::SMEM)
-           : nc == 64 ? go(k_wgrad_pairs<64, 32>, WpCfg<64, 32>::SMEM)
-                      : go(k_wgrad_pairs<128, 32>, WpCfg<128, 32>::SMEM);
+        FVDB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmpp, tmp, work, ex, n, st));
+        k_pt_schedule<<<1, kSchedThreads, 0, st>>>(ex, tiles, gs, G, slots, s);
+        FVDB_LAUNCH_CHECK();
+        auto go = [&](auto kern, int smem) -> int {
+            smem = wp_launch_smem(smem);
+            FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            kern<<<slots, kWpThreads, smem, st>>>(am, ia, bn, ib, tile_pos, tiles, s, part);
+            FVDB_LAUNCH_CHECK();
+            return FVDB_OK;
+        };
+        rc = nc == 32 ? go(k_wgrad_pairs_tiles<32>, WpCfg<32, kPtStage>::SMEM)
+           : nc == 64 ? go(k_wgrad_pairs_tiles<64>, WpCfg<64, kPtStage>::SMEM)
+                      : go(k_wgrad_pairs_tiles<128>, WpCfg<128, kPtStage>::SMEM);
+    } else {
+        k_pl_schedule<<<1, kSchedThreads, 0, st>>>(seg, G, nacc, slots, s);
+        auto go = [&](auto kern, int smem) -> int {
+            smem = wp_launch_smem(smem);
+            FVDB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            // ranges beyond G exist only when a linear share spans more than nacc offsets (tiny offsets)
+            kern<<<slots, kWpThreads, smem, st>>>(am, ia, bn, ib, seg, s, part);
+            FVDB_LAUNCH_CHECK();
+            return FVDB_OK;
+        };
+        static const int tk = getenv("FVDB_WG_PAIRS_TK") ? atoi(getenv("FVDB_WG_PAIRS_TK")) : 32;  // profiling
+        if (tk == 128)
+            rc = nc == 32 ? go(k_wgrad_pairs<32, 128>, WpCfg<32, 128>::SMEM)
+               : nc == 64 ? go(k_wgrad_pairs<64, 128>, WpCfg<64, 128>::SMEM)
+                          : go(k_wgrad_pairs<128, 128>, WpCfg<128, 128>::SMEM);
+        else if (tk == 64)
+            rc = nc == 32 ? go(k_wgrad_pairs<32, 64>, WpCfg<32, 64>::SMEM)
+               : nc == 64 ? go(k_wgrad_pairs<64, 64>, WpCfg<64, 64>::SMEM)
+                          : go(k_wgrad_pairs<128, 64>, WpCfg<128, 64>::SMEM);
+        else
+            rc = nc == 32 ? go(k_wgrad_pairs<32, 32>, WpCfg<32, 32>::SMEM)
+               : nc == 64 ? go(k_wgrad_pairs<64, 32>, WpCfg<64, 32>::SMEM)
+                          : go(k_wgrad_pairs<128, 32>, WpCfg<128, 32>::SMEM);
+    }
     if (rc != FVDB_OK) return rc;
     k_wgrad_pairs_reduce<<<(unsigned)ceil_div((int64_t)27 * 128 * nc, 256), 256, 0, st>>>(part, s, nacc, nc, swapped,
                                                                                           cin, cout, gw);

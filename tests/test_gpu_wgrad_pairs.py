@@ -2,6 +2,8 @@
 csrc/wgrad_pairs.cu) against the oracle's per-offset form gw[:,:,d] = go[outs[d]]ᵀ · x[ins[d]]
 (conv.py:358-366), on bf16-rounded inputs with fp32 accumulation (rel <= 2e-5).
 """
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -50,14 +52,24 @@ def test_pair_lists_exact(maps, which):
         assert b - a == (len(o) + 127) // 128 * 128
         assert np.array_equal(pout[a:a + len(o)], o) and np.array_equal(pin[a:a + len(o)], v[d, o])
         assert (pout[a + len(o):b] == -1).all() and (pin[a + len(o):b] == -1).all()
+    tp = tab.pair_tile_pos().cpu().numpy().reshape(27, -1)
+    tiles = (tab.n + 127) // 128
+    assert tp.shape == (27, tiles + 1)
+    for d in range(27):
+        o = np.nonzero(v[d] >= 0)[0]
+        want = seg[d] + np.searchsorted(o, np.arange(tiles + 1) * 128)
+        assert np.array_equal(tp[d], want)
 
 
 SHAPES = [(128, 128), (64, 128), (128, 64), (32, 128), (128, 32)]
 
 
+@pytest.mark.parametrize("sched", ["tiles", "linear"])
 @pytest.mark.parametrize("which", ["s1", "s2"])
 @pytest.mark.parametrize("cin,cout", SHAPES)
-def test_wgrad_pairs_vs_oracle(maps, monkeypatch, which, cin, cout):
+def test_wgrad_pairs_vs_oracle(maps, monkeypatch, which, cin, cout, sched):
+    """Both schedules: linear shares of the offset-major lists (default) and offset groups x tile ranges."""
+    monkeypatch.setattr(sys.modules["paper_2407_01781_b200.conv"], "_WG_PAIRS_SCHED", sched)
     g, go_grid, km, (ins, outs) = maps[which]
     rng = np.random.default_rng(cin + 7 * cout + (which == "s2"))
     x = rng.normal(size=(g.num_voxels, cin)).astype(np.float32)
@@ -76,8 +88,11 @@ def test_wgrad_pairs_vs_oracle(maps, monkeypatch, which, cin, cout):
     assert rel(wgrad(xb, gyb, km.fwd), gw_r) < 2e-5
 
 
-def test_wgrad_pairs_empty_offsets_and_tables(monkeypatch):
-    """Offsets without pairs get zero gradient; an empty table gives all zeros."""
+@pytest.mark.parametrize("sched", ["tiles", "linear"])
+def test_wgrad_pairs_empty_offsets_and_tables(monkeypatch, sched):
+    """Offsets without pairs get zero gradient; an empty table gives all zeros.  With one tile the
+    tile-ordered schedule leaves most CTAs of the dense group with empty tile ranges (zero partials)."""
+    monkeypatch.setattr(sys.modules["paper_2407_01781_b200.conv"], "_WG_PAIRS_SCHED", sched)
     monkeypatch.setenv("FVDB_WG_PAIRS", "force")
     g, _ = P.build_from_coords(np.array([[0, 0, 0], [0, 0, 1], [9, 9, 9]]))
     km = P.build_kernel_map(g, g, 1)
