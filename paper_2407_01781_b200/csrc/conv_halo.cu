@@ -739,6 +739,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
     extern __shared__ uint8_t dsmem[];
     constexpr int NB = C::NB;
     __shared__ __align__(8) uint64_t bar_hfull[NB], bar_hempty[NB], bar_xfull[NB], bar_ifull[NB], bar_iempty[NB];
+    __shared__ __align__(8) uint64_t bar_xempty[NB];          // second loader warp done reading a row-id buffer
     __shared__ __align__(8) uint64_t bar_afree[SETS][ASL];   // A slot's MMAs complete (tcgen05.commit)
     __shared__ __align__(8) uint64_t bar_wfull[SETS][WSL];   // weight image landed (TMA tx)
     __shared__ __align__(8) uint64_t bar_wfree[SETS][WSL];   // weight slot's MMAs complete
@@ -763,6 +764,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
             mbar_init(smem_u32(&bar_xfull[b]), 1);
             mbar_init(smem_u32(&bar_ifull[b]), 1);
             mbar_init(smem_u32(&bar_iempty[b]), kBuilders);
+            mbar_init(smem_u32(&bar_xempty[b]), 32);
         }
         for (int s = 0; s < SETS; ++s) {
             for (int k = 0; k < ASL; ++k) mbar_init(smem_u32(&bar_afree[s][k]), 1);
@@ -816,8 +818,14 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
             off0 = __shfl_sync(0xffffffffu, m_off, k & 31);
             len0 = __shfl_sync(0xffffffffu, m_len, k & 31);
         };
-        auto issue_ids = [&](int off, int len, uint32_t buf) {
+        // Row ids of phase p go to buffer p % NB, issued by warp 0 while the other loader warp may still read
+        // that buffer for phase p - NB (warp 0 runs up to one phase ahead): wait for its xempty arrival first.
+        // (Without it a CTA's first phases, before builder back-pressure, could stage another phase's rows:
+        // rare wrong output rows, first seen on a multi-phase first tile.)
+        auto issue_ids = [&](int off, int len, uint32_t p) {
+            const uint32_t buf = p % NB;
             if (lw == 0 && lane == 0) {
+                if (C::NLD == 2) mbar_wait(smem_u32(&bar_xempty[buf]), ((p / NB) & 1) ^ 1);
                 mbar_arrive_expect_tx(smem_u32(&bar_xfull[buf]), (uint32_t)len * 4u);
                 if (len > 0) bulk_g2s(xbase + buf * C::CAP * 4, P.halo_rows + off, (uint32_t)len * 4u, smem_u32(&bar_xfull[buf]));
             }
@@ -854,7 +862,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
             }
             const uint32_t buf = pc % NB, par = (pc / NB) & 1;
             if (lane == 0 && lw == 0) trace(dbg, 5, pc);
-            if (nt < T) issue_ids(nbase + noff, nlen, (pc + 1) % NB);
+            if (nt < T) issue_ids(nbase + noff, nlen, pc + 1);
             mbar_wait(smem_u32(&bar_xfull[buf]), par);
             mbar_wait(smem_u32(&bar_hempty[buf]), par ^ 1);
             if (lane == 0 && lw == 0) {
@@ -884,6 +892,7 @@ __global__ void __launch_bounds__(Halo4Cfg<K, N>::THREADS, 1)
                 }
             }
             if (lane == 0 && lw == 0) trace(dbg, 11, pc);
+            if (lw == 1) mbar_arrive(smem_u32(&bar_xempty[buf]));  // this lane's ids reads are done
             cp_async_arrive_noinc(smem_u32(&bar_hfull[buf]));
             __syncwarp();
             ++pc;

@@ -356,3 +356,24 @@ def test_wgrad_on_halo_plan_matches_oracle(case, shell):
     finally:
         del os.environ["FVDB_WG_HALO"]
     assert rel(gw, gw_t.cpu().numpy()) < 2e-5
+
+
+def test_halo_conv_repeated_runs_identical():
+    """Stress for races between the halo kernel's warps: 200 forwards on the cfg2 shell (64x64: two halo loader
+    warps, multi-phase tiles such as tile 2, the plan's first, which is also CTA 2's first tile), each compared
+    bitwise with the first and within 2e-5 with the gather kernel.  The second loader warp once read a row-id
+    buffer the first had already refilled: 2 of 300 runs wrong (tools/halo_stress.py)."""
+    g, _ = P.build_from_coords(sphere_shell_coords(470, band=1.5))
+    km = P.build_kernel_map(g, g, 1)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(g.num_voxels, 64, device="cuda", generator=gen).to(torch.bfloat16)
+    w = torch.randn(64, 64, 3, 3, 3, device="cuda", generator=gen) / (27 * 64) ** 0.5
+    ref = gather_conv(x, km.fwd, w, out_dtype=torch.float32, impl="gather")
+    first = gather_conv(x, km.fwd, w, out_dtype=torch.float32, impl="halo")
+    assert int(km.fwd.halo_plan(64, 64).tensors["tile_level"][2]) > 1  # the case that exposed the race
+    assert rel(first, ref.cpu().numpy()) < 2e-5
+    bad = 0
+    for _ in range(200):
+        y = gather_conv(x, km.fwd, w, out_dtype=torch.float32, impl="halo")
+        bad += int(not torch.equal(y, first))
+    assert bad == 0
