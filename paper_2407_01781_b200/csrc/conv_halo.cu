@@ -2190,11 +2190,11 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
     __shared__ int perm[kTileRows];
     __shared__ int wcnt[2][4];
     __shared__ int nu, base_s;
-    __shared__ uint32_t rmax_s;
+    __shared__ uint32_t rmax_s, rmin_s;
     const int tile = blockIdx.x, tid = threadIdx.x;
     int32_t row[kPlanItems];
     uint8_t col[kPlanItems];
-    uint32_t rmax = 1;
+    uint32_t rmax = 1, rmin = 0xFFFFFFFFu;
 #pragma unroll
     for (int k = 0; k < kPlanItems; ++k) {
         const int e = tid + k * kPlanThreads;  // a warp's 32 entries: consecutive rows of one offset
@@ -2204,11 +2204,15 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
             if (o < n_out) row[k] = __ldg(nbr + (int64_t)(e / kTileRows) * ld + o);
         }
         if (row[k] > (int32_t)rmax) rmax = (uint32_t)row[k];
+        if (row[k] >= 0 && (uint32_t)row[k] < rmin) rmin = (uint32_t)row[k];
     }
     // colours loaded up front (independent loads in flight together, not one dependent load per new key)
 #pragma unroll
     for (int k = 0; k < kPlanItems; ++k) col[k] = (color && row[k] >= 0) ? (__ldg(color + row[k]) & 1) : 0;
-    if (tid == 0) rmax_s = 1;
+    if (tid == 0) {
+        rmax_s = 1;
+        rmin_s = 0xFFFFFFFFu;
+    }
     // dedupe per (phase, row); raise the phase count until every phase's halo fits the capacity
     int level = 1;
     for (;; level *= 3) {
@@ -2259,7 +2263,10 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
         __syncthreads();
     }
     atomicMax(&rmax_s, rmax);
-    // unique keys -> (phase << rb) | row, sorted over rb + 5 bits: slots follow ascending rows per (phase, colour)
+    atomicMin(&rmin_s, rmin);
+    // unique keys -> (phase << rb) | (row - rmin), sorted over rb + pb bits (rb: the tile's row span, pb: the phase
+    // bits its level needs, 0 for one phase): slots follow ascending rows per (phase, colour).  Relative rows cut
+    // a single-phase tile's sort from ~25 key bits (absolute rows + 5 phase bits: 7 radix passes) to its span's
     for (int h = tid; h < kHashSize; h += kPlanThreads) {
         const uint32_t k = S.hkey[h];
         if (k != kEmpty32) {
@@ -2269,8 +2276,11 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
     }
     __syncthreads();
     const int n_u = nu;
+    // ~12-14 bits (4 passes)
     if (n_u <= kPlanThreads * kSortSmall) {
-        const int rb = 32 - __clz((int)rmax_s);
+        const uint32_t r0 = rmin_s <= rmax_s ? rmin_s : 0u;
+        const int rb = 32 - __clz((int)(rmax_s - r0) | 1);
+        const int pb = level > 1 ? 32 - __clz(level - 1) : 0;
         uint32_t key[kSortSmall];
         uint16_t hv[kSortSmall];
 #pragma unroll
@@ -2278,10 +2288,10 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
             const int i = tid * kSortSmall + k;
             hv[k] = i < n_u ? S.uh[i] : (uint16_t)0;
             const uint32_t u = i < n_u ? S.hkey[hv[k]] : kEmpty32;
-            key[k] = i < n_u ? ((u & 31) << rb) | (u >> 5) : kEmpty32;
+            key[k] = i < n_u ? ((u & 31) << rb) | ((u >> 5) - r0) : kEmpty32;
         }
         __syncthreads();
-        PlanSortSmall(S.tmp.sort).Sort(key, hv, 0, rb + 5);
+        PlanSortSmall(S.tmp.sort).Sort(key, hv, 0, rb + pb);
         __syncthreads();
         uint32_t packed = 0;
         uint8_t c1[kSortSmall];
