@@ -2164,6 +2164,7 @@ constexpr int kTileSlotsMax = 2 * 27 * kTileRows + 27 * 8;
 constexpr int kSortSmall = 4;  // 256 x 4 = 1024 unique keys sorted; more (dense 128-channel tiles) keep hash order
 constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 using PlanSortSmall = cub::BlockRadixSort<uint32_t, kPlanThreads, kSortSmall, uint16_t>;
+using PlanSortTiny = cub::BlockRadixSort<uint32_t, kPlanThreads, 2, uint16_t>;  // <= 512 unique keys (most tiles)
 // 32-bit keys (row << 5 | phase): input rows < 2^27 (fvdb_halo_plan_build rejects larger tables)
 struct PlanOneSmem {
     uint32_t hkey[kHashSize];
@@ -2172,6 +2173,7 @@ struct PlanOneSmem {
     uint16_t hpos[kPlanKeys];  // hash entry of element e = d * 128 + lane row (0xFFFF: no pair)
     union {
         typename PlanSortSmall::TempStorage sort;
+        typename PlanSortTiny::TempStorage sort2;
         typename PlanScan::TempStorage scan;
     } tmp;
     uint32_t ukey[kPlanThreads * kSortSmall];
@@ -2179,6 +2181,66 @@ struct PlanOneSmem {
 };
 
 __device__ __forceinline__ uint32_t plan_hash32(uint32_t k) { return (k * 0x9E3779B1u) >> (32 - kHashBits); }
+
+// Sort a tile's unique keys (rows relative to r0, phase above bit rb, rb + pb significant bits) with ITEMS keys per
+// thread and give each its slot: rank among its (phase, colour) in ascending-row order.  Block-wide.
+template <int ITEMS, class SortT>
+__device__ __forceinline__ void plan_sort_slots(PlanOneSmem& S, typename SortT::TempStorage& tmp, PlanCounts& pc,
+                                                int n_u, uint32_t r0, int rb, int pb) {
+    const int tid = threadIdx.x;
+    uint32_t key[ITEMS];
+    uint16_t hv[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const int i = tid * ITEMS + k;
+        hv[k] = i < n_u ? S.uh[i] : (uint16_t)0;
+        const uint32_t u = i < n_u ? S.hkey[hv[k]] : kEmpty32;
+        key[k] = i < n_u ? ((u & 31) << rb) | ((u >> 5) - r0) : kEmpty32;
+    }
+    __syncthreads();
+    SortT(tmp).Sort(key, hv, 0, rb + pb);
+    __syncthreads();
+    uint32_t packed = 0;
+    uint8_t c1[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        c1[k] = 0;
+        if (key[k] != kEmpty32) {
+            const int c = S.hcol[hv[k]];
+            c1[k] = (uint8_t)(1 + c);
+            packed += c ? (1u << 16) : 1u;
+        }
+    }
+    uint32_t excl;
+    PlanScan(S.tmp.scan).ExclusiveSum(packed, excl);
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) S.ukey[tid * ITEMS + k] = key[k];
+    __syncthreads();
+    uint32_t run = excl;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const int e = tid * ITEMS + k;
+        if (c1[k]) {
+            const int gr = (int)(key[k] >> rb);
+            if (e == 0 || (int)(S.ukey[e - 1] >> rb) != gr) {
+                pc.gfirst[0][gr] = (int)(run & 0xFFFF);
+                pc.gfirst[1][gr] = (int)(run >> 16);
+            }
+            run += (c1[k] == 2) ? (1u << 16) : 1u;
+        }
+    }
+    __syncthreads();
+    run = excl;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        if (c1[k]) {
+            const int gr = (int)(key[k] >> rb), c = c1[k] - 1;
+            const int rank = (c ? (int)(run >> 16) : (int)(run & 0xFFFF)) - pc.gfirst[c][gr];
+            S.hslot[hv[k]] = (uint16_t)(2 * rank + c);
+            run += c ? (1u << 16) : 1u;
+        }
+    }
+}
 
 __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* __restrict__ nbr, int64_t ld,
                                                                int64_t n_out, const uint8_t* __restrict__ color,
@@ -2281,58 +2343,10 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
         const uint32_t r0 = rmin_s <= rmax_s ? rmin_s : 0u;
         const int rb = 32 - __clz((int)(rmax_s - r0) | 1);
         const int pb = level > 1 ? 32 - __clz(level - 1) : 0;
-        uint32_t key[kSortSmall];
-        uint16_t hv[kSortSmall];
-#pragma unroll
-        for (int k = 0; k < kSortSmall; ++k) {
-            const int i = tid * kSortSmall + k;
-            hv[k] = i < n_u ? S.uh[i] : (uint16_t)0;
-            const uint32_t u = i < n_u ? S.hkey[hv[k]] : kEmpty32;
-            key[k] = i < n_u ? ((u & 31) << rb) | ((u >> 5) - r0) : kEmpty32;
-        }
-        __syncthreads();
-        PlanSortSmall(S.tmp.sort).Sort(key, hv, 0, rb + pb);
-        __syncthreads();
-        uint32_t packed = 0;
-        uint8_t c1[kSortSmall];
-#pragma unroll
-        for (int k = 0; k < kSortSmall; ++k) {
-            c1[k] = 0;
-            if (key[k] != kEmpty32) {
-                const int c = S.hcol[hv[k]];
-                c1[k] = (uint8_t)(1 + c);
-                packed += c ? (1u << 16) : 1u;
-            }
-        }
-        uint32_t excl;
-        PlanScan(S.tmp.scan).ExclusiveSum(packed, excl);
-#pragma unroll
-        for (int k = 0; k < kSortSmall; ++k) S.ukey[tid * kSortSmall + k] = key[k];
-        __syncthreads();
-        uint32_t run = excl;
-#pragma unroll
-        for (int k = 0; k < kSortSmall; ++k) {
-            const int e = tid * kSortSmall + k;
-            if (c1[k]) {
-                const int gr = (int)(key[k] >> rb);
-                if (e == 0 || (int)(S.ukey[e - 1] >> rb) != gr) {
-                    pc.gfirst[0][gr] = (int)(run & 0xFFFF);
-                    pc.gfirst[1][gr] = (int)(run >> 16);
-                }
-                run += (c1[k] == 2) ? (1u << 16) : 1u;
-            }
-        }
-        __syncthreads();
-        run = excl;
-#pragma unroll
-        for (int k = 0; k < kSortSmall; ++k) {
-            if (c1[k]) {
-                const int gr = (int)(key[k] >> rb), c = c1[k] - 1;
-                const int rank = (c ? (int)(run >> 16) : (int)(run & 0xFFFF)) - pc.gfirst[c][gr];
-                S.hslot[hv[k]] = (uint16_t)(2 * rank + c);
-                run += c ? (1u << 16) : 1u;
-            }
-        }
+        if (n_u <= kPlanThreads * 2)
+            plan_sort_slots<2, PlanSortTiny>(S, S.tmp.sort2, pc, n_u, r0, rb, pb);
+        else
+            plan_sort_slots<kSortSmall, PlanSortSmall>(S, S.tmp.sort, pc, n_u, r0, rb, pb);
     }
     if (tid == 0) base_s = atomicAdd(counter, pc.total);
     if (tid < 27) {
