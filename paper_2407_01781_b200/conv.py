@@ -150,15 +150,20 @@ class NbrTable:
     uses to pair lanes; halo plans are built lazily per kernel capacity and cached.
     """
 
-    __slots__ = ("t", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
+    __slots__ = ("_t", "_t_fn", "ld", "n", "_colors_fn", "_colors", "_plans", "uses", "counts", "_density", "_sorted",
                  "_masks", "sparse", "_steady", "_pairs", "_pair_tp", "exact_uses", "wgrad_uses", "rows_bound",
                  "rev_src", "plan_shared")
 
-    def __init__(self, t, n, colors_fn=None, counts=None):
+    def __init__(self, t, n, colors_fn=None, counts=None, ld=None):
+        """t: the [27, ld] table, or a function returning it (materialised on first access of ``.t``; ld given)."""
         self.rows_bound = None  # exclusive bound of the input rows in t (known: single-pass halo plans)
         self.rev_src = None  # NbrTable whose offset rows reversed are this table (halo plans are shared)
         self.plan_shared = False  # one halo plan serves this table and its reversed partner (fwd + dgrad)
-        self.t, self.ld, self.n = t, int(t.shape[1]), int(n)
+        if callable(t):
+            self._t, self._t_fn, self.ld = None, t, int(ld)
+        else:
+            self._t, self._t_fn, self.ld = t, None, int(t.shape[1])
+        self.n = int(n)
         self._colors_fn, self._colors, self._plans = colors_fn, None, {}
         self.uses = 0  # bf16 tensor-core convolutions run over this table (conv_impl "auto")
         self.counts = counts  # per-offset pair counts (device or host int64 [27]), when known
@@ -171,6 +176,12 @@ class NbrTable:
         self._pair_tp = None  # per-(offset, tile) positions in the pair lists
         self.exact_uses = 0  # fp32 / f64 gather convolutions run over this table
         self.wgrad_uses = 0  # bf16 weight gradients run over this table
+
+    @property
+    def t(self) -> torch.Tensor:
+        if self._t is None:
+            self._t, self._t_fn = self._t_fn(), None
+        return self._t
 
     def density(self) -> float:
         """Mean pairs per output row (27 = every offset active); 27 when unknown."""
@@ -435,15 +446,18 @@ class KernelMap:
             if flipped:
                 # stride 1 onto the same grid: nbr[d][o] = i  <=>  nbr[26 - d][i] = o (the mirrored offset),
                 # so the transposed table is the forward table with its offset rows reversed (a contiguous
-                # copy instead of the scatter; padding columns are -1 in every row)
-                t = torch.flip(self.fwd.t, dims=[0])
+                # copy instead of the scatter; padding columns are -1 in every row).  Made only when read:
+                # the halo kernel runs the forward table's plan reversed and never reads it (cfg2 training step:
+                # no 110 MB copy, 0.08 ms per new map)
+                fwd = self.fwd
+                t = lambda: torch.flip(fwd.t, dims=[0])  # noqa: E731
             else:
                 t = torch.empty((27, padded_len(self.num_in)), dtype=torch.int32, device=self.device)
                 L = _lib.lib()
                 _lib.check(L.fvdb_kmap_transpose(self.fwd.t.data_ptr(), self.fwd.ld, self.num_out, self.num_in,
                                                  t.data_ptr(), t.shape[1], _lib.stream_ptr()), "kmap_transpose")
             self._bwd = NbrTable(t, self.num_in, _colors_fn(self._grids, self.stride, True) if self._grids else None,
-                                 counts=self._counts)
+                                 counts=self._counts, ld=self.fwd.ld)
             self._bwd.sparse = self.stride == 2  # fine voxel i pairs only offsets d with i - d even: <= 8 of 27
             self._bwd.rows_bound = int(self.num_out)
             if flipped:
