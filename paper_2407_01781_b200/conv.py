@@ -486,7 +486,7 @@ def build_kernel_map(grid_in, grid_out, stride=1):
     dev = grid_out.device
     n_out = grid_out.num_voxels
     t = torch.empty((27, padded_len(n_out)), dtype=torch.int32, device=dev)
-    counts = torch.zeros(27, dtype=torch.int64, device=dev)
+    counts = torch.empty(27, dtype=torch.int64, device=dev)  # zeroed by fvdb_kernel_map_batch
     L = _lib.lib()
     wsb = L.fvdb_kmap_workspace_bytes(grid_out.num_leaf_nodes)
     ws = _lib.workspace(wsb, dev)
@@ -514,7 +514,7 @@ def build_batch_kernel_map(batch_in, batch_out, stride=1):
     dev = go[0].device
     n_in, n_out = batch_in.total_voxels, batch_out.total_voxels
     t = torch.empty((27, padded_len(n_out)), dtype=torch.int32, device=dev)
-    counts = torch.zeros(27, dtype=torch.int64, device=dev)
+    counts = torch.empty(27, dtype=torch.int64, device=dev)  # zeroed by fvdb_kernel_map_batch
     L = _lib.lib()
     views_in = (_lib.GridView * B)(*[g.view() for g in gi])
     views_out = (_lib.GridView * B)(*[g.leaf_view() for g in go])  # output grids are never probed
