@@ -2281,6 +2281,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
         const int gsz = 27 / level;
         for (int h = tid; h < kHashSize; h += kPlanThreads) S.hkey[h] = kEmpty32;
         if (tid < 27) pc.cnt[0][tid] = pc.cnt[1][tid] = 0;
+        if (tid == 0) nu = 0;
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kPlanItems; ++k) {
@@ -2293,6 +2294,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
                     if (prev == kEmpty32) {
                         const int c = col[k];
                         const int r = atomicAdd(&pc.cnt[c][key & 31], 1);
+                        // unique keys listed as they are inserted (no scan of the hash table afterwards)
+                        const int iu = atomicAdd(&nu, 1);
+                        if (iu < kPlanThreads * kSortSmall) S.uh[iu] = (uint16_t)h;
                         S.hslot[h] = (uint16_t)(2 * r + c);  // hash order (kept when too many keys to sort)
                         S.hcol[h] = (uint8_t)c;
                         break;
@@ -2318,7 +2322,6 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
             }
             pc.total = acc;
             pc.rb = fits ? 1 : 0;  // (flag)
-            nu = 0;
         }
         __syncthreads();
         if (level == 27 || pc.rb) break;
@@ -2326,18 +2329,11 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
     }
     atomicMax(&rmax_s, rmax);
     atomicMin(&rmin_s, rmin);
+    __syncthreads();
+    const int n_u = nu;
     // unique keys -> (phase << rb) | (row - rmin), sorted over rb + pb bits (rb: the tile's row span, pb: the phase
     // bits its level needs, 0 for one phase): slots follow ascending rows per (phase, colour).  Relative rows cut
     // a single-phase tile's sort from ~25 key bits (absolute rows + 5 phase bits: 7 radix passes) to its span's
-    for (int h = tid; h < kHashSize; h += kPlanThreads) {
-        const uint32_t k = S.hkey[h];
-        if (k != kEmpty32) {
-            const int i = atomicAdd(&nu, 1);
-            if (i < kPlanThreads * kSortSmall) S.uh[i] = (uint16_t)h;
-        }
-    }
-    __syncthreads();
-    const int n_u = nu;
     // ~12-14 bits (4 passes)
     if (n_u <= kPlanThreads * kSortSmall) {
         const uint32_t r0 = rmin_s <= rmax_s ? rmin_s : 0u;
@@ -2362,9 +2358,17 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
     }
     for (int s = tid; s < pc.total; s += kPlanThreads) P.halo_rows[base + s] = -1;
     __syncthreads();
-    for (int h = tid; h < kHashSize; h += kPlanThreads) {
-        const uint32_t k = S.hkey[h];
-        if (k != kEmpty32) P.halo_rows[base + pc.goff[k & 31] + S.hslot[h]] = (int32_t)(k >> 5);
+    if (n_u <= kPlanThreads * kSortSmall) {  // the listed unique keys
+        for (int i = tid; i < n_u; i += kPlanThreads) {
+            const int h = S.uh[i];
+            const uint32_t k = S.hkey[h];
+            P.halo_rows[base + pc.goff[k & 31] + S.hslot[h]] = (int32_t)(k >> 5);
+        }
+    } else {
+        for (int h = tid; h < kHashSize; h += kPlanThreads) {
+            const uint32_t k = S.hkey[h];
+            if (k != kEmpty32) P.halo_rows[base + pc.goff[k & 31] + S.hslot[h]] = (int32_t)(k >> 5);
+        }
     }
     int f = -1, o = -1;
     if (tid < kTileRows) {
