@@ -2279,7 +2279,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_halo_plan_one(const int32_t* _
     int level = 1;
     for (;; level *= 3) {
         const int gsz = 27 / level;
-        for (int h = tid; h < kHashSize; h += kPlanThreads) S.hkey[h] = kEmpty32;
+        for (int h = tid; h < kHashSize / 4; h += kPlanThreads)  // 16-byte stores (hkey leads the 16-aligned smem)
+            reinterpret_cast<uint4*>(S.hkey)[h] = make_uint4(kEmpty32, kEmpty32, kEmpty32, kEmpty32);
         if (tid < 27) pc.cnt[0][tid] = pc.cnt[1][tid] = 0;
         if (tid == 0) nu = 0;
         __syncthreads();
