@@ -210,6 +210,11 @@ __global__ void __launch_bounds__(kSchedThreads) k_pl_schedule(const int32_t* __
 // (FVDB_WG_PAIRS_SCHED=tiles in conv.py).
 // ---------------------------------------------------------------------------------------------------------
 constexpr int kPtStage = 32;  // pairs per stage of the tile-ordered kernel
+// offsets per group: one (dx, dy) line (3) or two (6); FVDB_PT_GS overrides (profiling: 1 = no interleaving)
+#ifndef FVDB_PT_GS
+#define FVDB_PT_GS 0
+#endif
+__host__ __device__ constexpr int pt_gs(int nacc) { return FVDB_PT_GS > 0 ? FVDB_PT_GS : nacc / 3 * 3; }
 
 // work[g][t] = 32-pair stages of group g in tile t (work[ng * tiles] = 0: the scan's total slot)
 __global__ void k_pt_work(const int32_t* __restrict__ tp, int tiles, int gs, int32_t* __restrict__ work) {
@@ -235,8 +240,8 @@ __global__ void k_pt_work(const int32_t* __restrict__ tp, int tiles, int gs, int
 // Slots past the groups are idle (c0 = c1 = 0, d0 = -1).  lo / hi[d] = the slots of d's group.
 __global__ void __launch_bounds__(kSchedThreads) k_pt_schedule(const int32_t* __restrict__ ex, int tiles, int gs,
                                                                int G, int slots, PlSched s) {
-    __shared__ int32_t gcnt[10], gstart[10];
-    __shared__ int64_t gw[10];
+    __shared__ int32_t gcnt[28], gstart[28];  // groups <= 27 (+ the end)
+    __shared__ int64_t gw[28];
     const int ng = (27 + gs - 1) / gs;
     if (threadIdx.x == 0) {
         int64_t W = 0;
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_pt_schedule(const int32_t* __
             W += gw[g];
         }
         // largest remainder: sum G_g = G when every group has work (each group >= 1 CTA)
-        int64_t rem[10];
+        int64_t rem[28];
         int used = 0;
         for (int g = 0; g < ng; ++g) {
             const int64_t q = W > 0 ? (int64_t)G * gw[g] : 0;
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(kWpThreads, 1)
                         const int32_t* __restrict__ ib, const int32_t* __restrict__ tp, int tiles, PlSched sch,
                         float* __restrict__ part) {
     using C = WpCfg<NC, kPtStage>;
-    constexpr int GS = C::NACC / 3 * 3;
+    constexpr int GS = pt_gs(C::NACC);
     const int cta = blockIdx.x;
     const int t0 = sch.c0[cta], t1 = sch.c1[cta], d0 = sch.d0[cta];
     if (d0 < 0) return;  // slot past the groups: never reduced
@@ -734,7 +739,7 @@ int pl_sm_count() {
 
 int pl_nacc(int nc) { return nc == 32 ? WpCfg<32, 32>::NACC : nc == 64 ? WpCfg<64, 32>::NACC : WpCfg<128, 32>::NACC; }
 
-int pl_groups(int nc) { return (27 + pl_nacc(nc) / 3 * 3 - 1) / (pl_nacc(nc) / 3 * 3); }
+int pl_groups(int nc) { return (27 + pt_gs(pl_nacc(nc)) - 1) / pt_gs(pl_nacc(nc)); }
 
 // tiles > 0: the tile-ordered schedule's stage counts and their scan follow the partials
 size_t pl_scan_bytes(int n) {
@@ -854,7 +859,7 @@ extern "C" int fvdb_conv_wgrad_pairs_tc(const void* in_bf16, int64_t n_in, int c
     const int32_t* ib = swapped ? pin : pout;
     int rc = FVDB_OK;
     if (by_tiles) {
-        const int gs = nacc / 3 * 3, n = pl_groups(nc) * tiles + 1;
+        const int gs = pt_gs(nacc), n = pl_groups(nc) * tiles + 1;
         k_pt_work<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(tile_pos, tiles, gs, work);
         FVDB_LAUNCH_CHECK();
         FVDB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmpp, tmp, work, ex, n, st));
