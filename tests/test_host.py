@@ -167,3 +167,22 @@ def test_exact_skip_policy(monkeypatch):
     assert exact_skip_mode(t, 32, 128) == "none"  # N > 64: untiled kernel, no row permutation
     monkeypatch.setenv("FVDB_EXACT_SKIP", "sort")
     assert exact_skip_mode(t, 32, 128) == "masks"
+
+
+def test_nbr_table_lazy_construction():
+    """NbrTable(t=callable, ld=...): the table is built once, on the first read of .t (a same-grid map's transposed
+    table: the halo dgrad runs the forward plan reversed and never reads it; conv.py KernelMap.bwd)."""
+    from paper_2407_01781_b200.conv import NbrTable
+    calls = []
+    base = torch.arange(27 * 256, dtype=torch.int32).reshape(27, 256)
+
+    def make():
+        calls.append(1)
+        return torch.flip(base, dims=[0])
+
+    t = NbrTable(make, 200, ld=256)
+    assert t.ld == 256 and t.n == 200 and not calls  # shape known, nothing built
+    assert torch.equal(t.t, torch.flip(base, dims=[0])) and len(calls) == 1
+    assert t.t is t.t and len(calls) == 1            # cached
+    eager = NbrTable(base, 200)
+    assert eager.ld == 256 and eager.t is base
